@@ -1,0 +1,150 @@
+/*
+ * fe2rom_gpu.h — C ABI of the B200 hyper-ROM macro-Gauss-point engine.
+ *
+ * Drop-in boundary for the online hot path of the monolithic hyper-ROM FE²
+ * scheme (arXiv 2306.02687): the batched evaluation of hyper-reduced RVE
+ * models at every macro Gauss point. Each entry point replaces a reference
+ * interface (paths relative to /root/reference/proj/include/fe2rom/):
+ *
+ *   fe2_material_update_batch  <- update_material        materials.hpp:317-325
+ *                                 (batched; update4 J2/elastic :199-214)
+ *   fe2_hrom_create            <- build_rve_problem      rve.hpp:167-185, in the
+ *                                 reduced form of SPEC.md:351-359 (G_q = B_q Φ,
+ *                                 cubature weights), materials by id (:158-162)
+ *   fe2_hrom_alloc_points      <- std::vector<MaterialState>(n_ips)  rve.hpp:450,
+ *                                 run_trajectory's virgin states, one set per point
+ *   fe2_hrom_solve_increment   <- one path step of run_trajectory rve.hpp:459-491:
+ *                                 set_macro_strain + micro_newton (:285-346, reduced:
+ *                                 SPEC.md:289-297) + homogenize (:350-392) + the
+ *                                 commit of states (:480), with load-step bisection
+ *                                 (:473-478), for every point of the batch
+ *   fe2_hrom_read_state        <- MicroResult::states / MaterialState   rve.hpp:207,
+ *                                 materials.hpp:102-106
+ *   fe2_last_error             <- fe2rom::Error::what()  common.hpp:39-46
+ *
+ * Conventions
+ *   - Strain is engineering Voigt (E11, E22, g12), stress (S11, S22, S12)
+ *     (rve.hpp:13-19, materials.hpp:21). C is row-major 3x3.
+ *   - History per cubature point is MaterialState = (eps_p[4] packed
+ *     11,22,33,12-tensor, eq, sigma33): 6 doubles (materials.hpp:102-106).
+ *   - Return codes: 0 = OK, else 1 + the reference ErrorCode ordinal
+ *     (common.hpp:26-37): 1 config, 2 geometry, 3 mesh, 4 material,
+ *     5 solver, 6 numeric, 7 rank, 8 bc, 9 io, 10 provenance. No exception
+ *     crosses the ABI. Per-point Newton failure is reported in status[]
+ *     with the same codes (run_trajectory throws ErrorCode::solver after
+ *     max_bisections, rve.hpp:474-476).
+ *   - The caller owns host arrays; the library owns device buffers. A handle
+ *     is bound to one device and is not thread-safe. Multi-GPU = one handle
+ *     per device (one process per GPU); points are sharded, never split.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with code 6 (numeric) and a message.
+ */
+#ifndef FE2ROM_GPU_H
+#define FE2ROM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Material parameters (materials.hpp:37-49, validate :80-87).
+ * kind 0: ElasticParams  p = {E, nu}
+ * kind 1: J2LinearParams p = {E, nu, sigma_y0, hardening} */
+typedef struct {
+  int kind;
+  double p[4];
+} fe2_material_t;
+
+/* MicroOptions (rve.hpp:195-200) + TrajectoryOptions::max_bisections (:439-443) */
+typedef struct {
+  double tol;         /* default 1e-8 */
+  int max_iter;       /* default 30   */
+  int max_bisections; /* default 4    */
+} fe2_newton_opts_t;
+
+typedef struct fe2_hrom_s* fe2_hrom_t;
+
+const char* fe2_last_error(void);
+/* library version string, e.g. "fe2rom-b200 0.1 sm_100a" */
+const char* fe2_version(void);
+/* number of usable CUDA devices (0 on a host without GPU) */
+int fe2_device_count(void);
+
+/* ---- batched material point: update_material over N points on the GPU.
+ * eps[N*3], state_in[N*6] (may be NULL = virgin), outputs sigma[N*3],
+ * C[N*9], state_out[N*6] (nullable), plastic[N] (nullable). Host buffers. */
+int fe2_material_update_batch(int device, const fe2_material_t* mat, int64_t N, const double* eps,
+                              const double* state_in, double* sigma, double* C, double* state_out,
+                              uint8_t* plastic);
+
+/* ---- hyper-ROM model on one device.
+ * G[K][3][n] host, w[K], mat_id[K] (index into mats), volume = RVE area. */
+int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, const int* mat_id,
+                    const fe2_material_t* mats, int n_mats, double volume, fe2_hrom_t* out);
+void fe2_hrom_destroy(fe2_hrom_t h);
+
+/* Allocate P macro points in the virgin state (α = 0, MaterialState{}).
+ * keep_flags != 0 also keeps per-(point, cubature point) plastic flags of
+ * the last commit (P*K bytes) for parity checks. */
+int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags);
+
+/* One load increment for all P points: E[P*3] is the path point of this
+ * increment (the previous one is remembered; the first starts from 0).
+ * Host buffers; every output is nullable. iters[P] counts all Newton
+ * iterations of the increment (bisected sub-steps included). */
+int fe2_hrom_solve_increment(fe2_hrom_t h, const double* E, const fe2_newton_opts_t* opts,
+                             double* sigma, double* C, int* iters, int* plastic_count,
+                             double* res_norm, int* status);
+
+/* Same, on DEVICE buffers already resident in HBM (E, outputs), ordered on
+ * `stream` (cudaStream_t, NULL = the handle's stream). The call returns
+ * after the increment is complete on `stream`. */
+int fe2_hrom_solve_increment_device(fe2_hrom_t h, const double* d_E, const fe2_newton_opts_t* opts,
+                                    double* d_sigma, double* d_C, int* d_iters, int* d_plastic_count,
+                                    double* d_res_norm, int* d_status, void* stream);
+
+/* Committed state readback (host): alpha[P*n], state[P*K*6] in the caller's
+ * cubature order (elastic-material points report eps_p = 0, eq = 0 and the
+ * sigma33 of their last commit), flags[P*K] (needs keep_flags). Nullable. */
+int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* flags);
+
+/* One hyper-assembly of point 0's committed history at a
+ * given (α, E): r[n], Kaa[n*n], KaE[n*3], C_EE[9], S_raw[3] (host). */
+int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, const double* E,
+                            double* r, double* Kaa, double* KaE, double* C_EE, double* S_raw);
+
+typedef struct {
+  int64_t points;
+  int n, K, K_j2;
+  int64_t kernel_launches;   /* own kernels launched since create */
+  int64_t newton_rounds;     /* fused assemble+step rounds since create */
+  int64_t point_assemblies;  /* (point, assembly) pairs processed since create */
+  int64_t j2_point_evals;    /* (point, J2 cubature point) material updates in assembly */
+  double last_increment_ms;  /* device time of the last increment */
+  double last_commit_ms;     /* device time of the last commit kernel */
+  double last_assembly_ms;   /* device time summed over the rounds of the last increment */
+  int64_t last_commit_bytes; /* algorithmic HBM bytes of the last commit kernel */
+} fe2_hrom_stats_t;
+int fe2_hrom_stats(fe2_hrom_t h, fe2_hrom_stats_t* out);
+/* enable per-kernel CUDA-event timing inside solve_increment (costs syncs) */
+int fe2_hrom_set_timing(fe2_hrom_t h, int on);
+
+/* ---- offline stage (host only, no GPU): seeded hyper-ROM model and paths
+ * matching BASELINE.json configs. */
+typedef struct fe2_model_s* fe2_model_t;
+/* default_cell(subdivisions) RVE (mesh.hpp:185-191, :218-352), linear BC,
+ * n random orthonormal modes, K random cubature points. */
+int fe2_model_build(int subdivisions, int n, int K, uint64_t seed, fe2_model_t* out);
+void fe2_model_free(fe2_model_t m);
+int fe2_model_sizes(fe2_model_t m, int* n, int* K, int* n_free, double* volume);
+int fe2_model_arrays(fe2_model_t m, double* G, double* w, int* ip_id, int* mat_id);
+/* path kind 0 = config-0 uniaxial rotated, 1 = config-1 reversal;
+ * E[P][n_incr][3] for global points p0..p0+P-1 */
+int fe2_paths(int kind, uint64_t seed, int64_t p0, int64_t P, int n_incr, double* E);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,36 @@
+"""fe2rom-b200: B200-native online hot path of the monolithic hyper-ROM FE²
+method (arXiv 2306.02687) — batched evaluation of hyper-reduced RVE models at
+every macro Gauss point.
+
+The compute path is the native library ``lib/libfe2rom_gpu.so`` (C ABI in
+``include/fe2rom/fe2rom_gpu.h``; sm_100a kernels). This package is the thin
+Python mirror of the reference's material-point and solver interface
+(``/root/reference/proj/include/fe2rom``: ``update_material``,
+``micro_newton``/``homogenize``/``run_trajectory``) over that ABI. There is
+no CPU fallback: without the library or a B200, calls raise.
+"""
+from .hrom import (  # noqa: F401
+    ElasticParams,
+    Fe2Error,
+    HyperRomEngine,
+    HyperRomModel,
+    J2LinearParams,
+    NewtonOptions,
+    device_count,
+    lib,
+    make_paths,
+    update_material_batch,
+)
+
+__all__ = [
+    "ElasticParams",
+    "Fe2Error",
+    "HyperRomEngine",
+    "HyperRomModel",
+    "J2LinearParams",
+    "NewtonOptions",
+    "device_count",
+    "lib",
+    "make_paths",
+    "update_material_batch",
+]

@@ -1,0 +1,556 @@
+// Host driver of the B200 hyper-ROM engine behind the C ABI
+// (include/fe2rom/fe2rom_gpu.h). Owns the device model (projected operator
+// rows, weights, elastic-inclusion constants), the per-point SoA state in
+// HBM, and the increment loop: begin → fused Newton rounds over a shrinking
+// active list → history commit. One handle per device; no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "fe2rom/fe2rom_gpu.h"
+#include "hrom_kernels.cuh"
+
+namespace fe2 {
+
+namespace {
+thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Failure(Code::numeric, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+void require_device(int device) {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw Failure(Code::numeric, "no CUDA device available: the B200 engine has no CPU fallback");
+  check(device >= 0 && device < count, Code::config, "device index out of range");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  check(prop.major == 10, Code::numeric,
+        std::string("the engine is built for sm_100a (B200); found ") + prop.name);
+  CK(cudaSetDevice(device));
+}
+
+MatDev to_dev(const fe2_material_t& m) {
+  check(m.kind == 0 || m.kind == 1, Code::config, "unsupported material kind");
+  const double E = m.p[0], nu = m.p[1];
+  check(E > 0.0 && nu >= 0.0 && nu < 0.5, Code::config, "invalid elastic parameters");  // materials.hpp:80-82
+  if (m.kind == 1) check(m.p[2] > 0.0 && m.p[3] >= 0.0, Code::config, "invalid J2 parameters");  // :83-87
+  return make_mat(m.kind, E, nu, m.kind == 1 ? m.p[2] : 0.0, m.kind == 1 ? m.p[3] : 0.0);
+}
+
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace fe2
+
+using namespace fe2;
+
+struct fe2_hrom_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int n = 0, NP = 0, S = 0, K = 0, K2 = 0, K2p = 0;
+  double volume = 0.0;
+  std::vector<int> j2_idx, el_idx;  // original cubature indices
+  std::vector<double> G, w;         // host copy (caller order)
+  std::vector<MatDev> qmat;         // per original cubature point
+  MatDev mat2{};
+  double CEEinc[9] = {0};
+  // device model
+  double *G2 = nullptr, *w2 = nullptr, *Kinc = nullptr, *KaEinc = nullptr;
+  // device points
+  int64_t P = 0;
+  bool keep_flags = false;
+  double *hist = nullptr, *alpha_c = nullptr, *alpha = nullptr, *alpha_ev = nullptr, *dalpha = nullptr;
+  double *E_prev = nullptr, *E_tgt = nullptr, *E_ev = nullptr;
+  PointState* st = nullptr;
+  uint8_t* flags = nullptr;
+  int *act[2] = {nullptr, nullptr}, *cnt = nullptr;
+  int* h_cnt = nullptr;  // pinned
+  // staging for the host-buffer API
+  double *dE = nullptr, *o_sigma = nullptr, *o_C = nullptr, *o_res = nullptr;
+  int *o_iters = nullptr, *o_status = nullptr, *o_pc = nullptr;
+  // stats
+  bool timing = false;
+  fe2_hrom_stats_t stats{};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+  ModelDev model() const {
+    ModelDev M{};
+    M.n = n;
+    M.NP = NP;
+    M.S = S;
+    M.K2 = K2;
+    M.K2p = K2p;
+    M.nchunks = K2p / kQC;
+    M.G2 = G2;
+    M.w2 = w2;
+    M.Kinc = Kinc;
+    M.KaEinc = KaEinc;
+    std::memcpy(M.CEEinc, CEEinc, sizeof CEEinc);
+    M.volume = volume;
+    M.mat2 = mat2;
+    return M;
+  }
+  PointsDev points() const {
+    PointsDev D{};
+    D.P = P;
+    D.hist = hist;
+    D.alpha_c = alpha_c;
+    D.alpha = alpha;
+    D.alpha_ev = alpha_ev;
+    D.dalpha = dalpha;
+    D.E_prev = E_prev;
+    D.E_tgt = E_tgt;
+    D.E_ev = E_ev;
+    D.st = st;
+    D.flags = flags;
+    return D;
+  }
+  void free_points() {
+    dfree(hist);
+    dfree(alpha_c);
+    dfree(alpha);
+    dfree(alpha_ev);
+    dfree(dalpha);
+    dfree(E_prev);
+    dfree(E_tgt);
+    dfree(E_ev);
+    dfree(st);
+    dfree(flags);
+    dfree(act[0]);
+    dfree(act[1]);
+    dfree(dE);
+    dfree(o_sigma);
+    dfree(o_C);
+    dfree(o_res);
+    dfree(o_iters);
+    dfree(o_status);
+    dfree(o_pc);
+    P = 0;
+  }
+  ~fe2_hrom_s() {
+    cudaSetDevice(device);
+    free_points();
+    dfree(G2);
+    dfree(w2);
+    dfree(Kinc);
+    dfree(KaEinc);
+    dfree(cnt);
+    if (h_cnt) cudaFreeHost(h_cnt);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+void count_launch(fe2_hrom_t h, int k = 1) { h->stats.kernel_launches += k; }
+
+// One increment on device buffers (the engine's core loop).
+void run_increment(fe2_hrom_t h, const double* d_E, const fe2_newton_opts_t* opts, const Outputs& O,
+                   cudaStream_t s) {
+  check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+  NewtonCfg cfg{1e-8, 30, 4};
+  if (opts) {
+    cfg.tol = opts->tol;
+    cfg.max_iter = opts->max_iter;
+    cfg.max_bis = opts->max_bisections;
+  }
+  check(cfg.tol > 0.0 && cfg.max_iter >= 0 && cfg.max_bis >= 0, Code::config, "invalid Newton options");
+  const ModelDev M = h->model();
+  const PointsDev D = h->points();
+  if (h->timing) CK(cudaEventRecord(h->ev[0], s));
+  CK(cudaMemsetAsync(h->cnt, 0, 2 * sizeof(int), s));
+  launch_begin_increment(M, D, O, d_E, h->act[0], h->cnt, s);
+  count_launch(h);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h->h_cnt, h->cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int n_active = *h->h_cnt;
+  int cur = 0;
+  // bound: every Newton iteration costs at most 1 + 8 rounds, per sub-step
+  const int64_t max_rounds = static_cast<int64_t>(cfg.max_iter + 1) * 9 * (cfg.max_bis + 2) * 8 + 64;
+  int64_t rounds = 0;
+  while (n_active > 0) {
+    check(++rounds <= max_rounds, Code::solver, "round limit exceeded (state machine did not terminate)");
+    int* next_cnt = h->cnt + 1;
+    CK(cudaMemsetAsync(next_cnt, 0, sizeof(int), s));
+    RoundArgs a{};
+    a.M = M;
+    a.D = D;
+    a.O = O;
+    a.cfg = cfg;
+    a.active = h->act[cur];
+    a.n_active = n_active;
+    a.next_active = h->act[cur ^ 1];
+    a.n_next = next_cnt;
+    a.dbg = nullptr;
+    launch_newton_round(a, s);
+    count_launch(h);
+    CK(cudaGetLastError());
+    h->stats.newton_rounds += 1;
+    h->stats.point_assemblies += n_active;
+    h->stats.j2_point_evals += static_cast<int64_t>(n_active) * h->K2;
+    CK(cudaMemcpyAsync(h->h_cnt, next_cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    n_active = *h->h_cnt;
+    cur ^= 1;
+  }
+  if (h->timing) CK(cudaEventRecord(h->ev[1], s));
+  launch_commit(M, D, O, s);
+  count_launch(h);
+  CK(cudaGetLastError());
+  if (h->timing) CK(cudaEventRecord(h->ev[2], s));
+  CK(cudaStreamSynchronize(s));
+  if (h->timing) {
+    float t01 = 0, t12 = 0;
+    CK(cudaEventElapsedTime(&t01, h->ev[0], h->ev[1]));
+    CK(cudaEventElapsedTime(&t12, h->ev[1], h->ev[2]));
+    h->stats.last_assembly_ms = t01;
+    h->stats.last_commit_ms = t12;
+    h->stats.last_increment_ms = t01 + t12;
+  }
+  h->stats.last_commit_bytes = h->P * static_cast<int64_t>(h->K2) * 88;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fe2_last_error(void) { return fe2::g_last_error.c_str(); }
+
+const char* fe2_version(void) { return "fe2rom-b200 0.1 sm_100a"; }
+
+int fe2_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int fe2_material_update_batch(int device, const fe2_material_t* mat, int64_t N, const double* eps,
+                              const double* state_in, double* sigma, double* C, double* state_out,
+                              uint8_t* plastic) {
+  return guard([&] {
+    check(mat && eps && sigma && C && N >= 0, Code::config, "bad arguments");
+    const MatDev m = to_dev(*mat);
+    require_device(device);
+    if (N == 0) return;
+    double *d_eps = dalloc<double>(N * 3), *d_in = state_in ? dalloc<double>(N * 6) : nullptr;
+    double *d_sig = dalloc<double>(N * 3), *d_C = dalloc<double>(N * 9);
+    double* d_out = state_out ? dalloc<double>(N * 6) : nullptr;
+    uint8_t* d_pl = plastic ? dalloc<uint8_t>(N) : nullptr;
+    CK(cudaMemcpy(d_eps, eps, N * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    if (state_in) CK(cudaMemcpy(d_in, state_in, N * 6 * sizeof(double), cudaMemcpyHostToDevice));
+    launch_material_batch(m, N, d_eps, d_in, d_sig, d_C, d_out, d_pl, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(sigma, d_sig, N * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(C, d_C, N * 9 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (state_out) CK(cudaMemcpy(state_out, d_out, N * 6 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (plastic) CK(cudaMemcpy(plastic, d_pl, N, cudaMemcpyDeviceToHost));
+    dfree(d_eps);
+    dfree(d_in);
+    dfree(d_sig);
+    dfree(d_C);
+    dfree(d_out);
+    dfree(d_pl);
+  });
+}
+
+int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, const int* mat_id,
+                    const fe2_material_t* mats, int n_mats, double volume, fe2_hrom_t* out) {
+  return guard([&] {
+    check(out != nullptr, Code::config, "null output handle");
+    *out = nullptr;
+    check(n >= 1 && K >= 1 && G && w && mat_id && mats && n_mats >= 1, Code::config, "bad model arguments");
+    check(n <= 32, Code::config, "this build supports n <= 32 modes");
+    check(volume > 0.0, Code::config, "RVE volume must be positive");
+    std::vector<MatDev> md;
+    for (int i = 0; i < n_mats; ++i) md.push_back(to_dev(mats[i]));
+    require_device(device);
+    auto h = new fe2_hrom_s;
+    try {
+      h->device = device;
+      h->n = n;
+      h->NP = (n + 7) / 8 * 8;
+      h->S = 3 * h->NP + 1;
+      h->K = K;
+      h->volume = volume;
+      h->G.assign(G, G + static_cast<size_t>(K) * 3 * n);
+      h->w.assign(w, w + K);
+      int j2_mat = -1;
+      for (int q = 0; q < K; ++q) {
+        check(mat_id[q] >= 0 && mat_id[q] < n_mats, Code::config, "cubature material id out of range");
+        check(w[q] > 0.0, Code::config, "cubature weights must be positive");
+        h->qmat.push_back(md[mat_id[q]]);
+        if (md[mat_id[q]].kind == 1) {
+          check(j2_mat < 0 || j2_mat == mat_id[q], Code::config, "this build supports one J2 material per model");
+          j2_mat = mat_id[q];
+          h->j2_idx.push_back(q);
+        } else {
+          h->el_idx.push_back(q);
+        }
+      }
+      h->mat2 = j2_mat >= 0 ? md[j2_mat] : make_mat(1, 1.0, 0.3, 1.0, 0.0);
+      h->K2 = static_cast<int>(h->j2_idx.size());
+      h->K2p = std::max(kQC, (h->K2 + kQC - 1) / kQC * kQC);
+      const int NP = h->NP, S = h->S;
+      std::vector<double> G2(static_cast<size_t>(h->K2p) * S, 0.0), w2(h->K2p, 0.0);
+      for (int q2 = 0; q2 < h->K2; ++q2) {
+        const int q = h->j2_idx[q2];
+        for (int i = 0; i < 3; ++i)
+          for (int a = 0; a < n; ++a) G2[static_cast<size_t>(q2) * S + i * NP + a] = G[(static_cast<size_t>(q) * 3 + i) * n + a];
+        w2[q2] = w[q];
+      }
+      // elastic cubature points: σ = C_e (E + G α) is linear -> constants
+      std::vector<double> Kinc(static_cast<size_t>(NP) * NP, 0.0), KaEinc(static_cast<size_t>(NP) * 3, 0.0);
+      for (int q : h->el_idx) {
+        const MatDev& m = h->qmat[q];
+        const double Ce[3][3] = {{m.lam + 2.0 * m.mu, m.lam, 0.0}, {m.lam, m.lam + 2.0 * m.mu, 0.0}, {0.0, 0.0, m.mu}};
+        const double* Gq = G + static_cast<size_t>(q) * 3 * n;
+        const double wq = w[q];
+        double wC[3][3];
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) {
+            wC[i][j] = wq * Ce[i][j];
+            h->CEEinc[3 * i + j] += wC[i][j];
+          }
+        for (int a = 0; a < n; ++a) {
+          for (int j = 0; j < 3; ++j)
+            KaEinc[a * 3 + j] += Gq[a] * wC[0][j] + Gq[n + a] * wC[1][j] + Gq[2 * n + a] * wC[2][j];
+          for (int b = 0; b < n; ++b) {
+            double s = 0.0;
+            for (int i = 0; i < 3; ++i)
+              s += Gq[i * n + a] * (wC[i][0] * Gq[b] + wC[i][1] * Gq[n + b] + wC[i][2] * Gq[2 * n + b]);
+            Kinc[static_cast<size_t>(a) * NP + b] += s;
+          }
+        }
+      }
+      CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      for (auto& e : h->ev) CK(cudaEventCreate(&e));
+      h->G2 = dalloc<double>(G2.size());
+      h->w2 = dalloc<double>(w2.size());
+      h->Kinc = dalloc<double>(Kinc.size());
+      h->KaEinc = dalloc<double>(KaEinc.size());
+      h->cnt = dalloc<int>(2);
+      CK(cudaMallocHost(&h->h_cnt, sizeof(int)));
+      CK(cudaMemcpy(h->G2, G2.data(), G2.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->w2, w2.data(), w2.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->Kinc, Kinc.data(), Kinc.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->KaEinc, KaEinc.data(), KaEinc.size() * sizeof(double), cudaMemcpyHostToDevice));
+      h->stats.n = n;
+      h->stats.K = K;
+      h->stats.K_j2 = h->K2;
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void fe2_hrom_destroy(fe2_hrom_t h) { delete h; }
+
+int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
+  return guard([&] {
+    check(h != nullptr && P >= 1, Code::config, "bad arguments");
+    check(P < (int64_t(1) << 31), Code::config, "at most 2^31-1 points per device");
+    CK(cudaSetDevice(h->device));
+    h->free_points();
+    const size_t hist_n = static_cast<size_t>(P) * h->K2p * 6;
+    h->hist = dalloc<double>(hist_n);
+    const size_t an = static_cast<size_t>(P) * h->NP;
+    h->alpha_c = dalloc<double>(an);
+    h->alpha = dalloc<double>(an);
+    h->alpha_ev = dalloc<double>(an);
+    h->dalpha = dalloc<double>(an);
+    h->E_prev = dalloc<double>(P * 3);
+    h->E_tgt = dalloc<double>(P * 3);
+    h->E_ev = dalloc<double>(P * 3);
+    h->st = dalloc<PointState>(P);
+    h->keep_flags = keep_flags != 0;
+    if (h->keep_flags) h->flags = dalloc<uint8_t>(static_cast<size_t>(P) * h->K2p);
+    h->act[0] = dalloc<int>(P);
+    h->act[1] = dalloc<int>(P);
+    h->dE = dalloc<double>(P * 3);
+    h->o_sigma = dalloc<double>(P * 3);
+    h->o_C = dalloc<double>(P * 9);
+    h->o_res = dalloc<double>(P);
+    h->o_iters = dalloc<int>(P);
+    h->o_status = dalloc<int>(P);
+    h->o_pc = dalloc<int>(P);
+    CK(cudaMemsetAsync(h->hist, 0, hist_n * sizeof(double), h->stream));
+    for (double* p : {h->alpha_c, h->alpha, h->alpha_ev, h->dalpha})
+      CK(cudaMemsetAsync(p, 0, an * sizeof(double), h->stream));
+    for (double* p : {h->E_prev, h->E_tgt, h->E_ev}) CK(cudaMemsetAsync(p, 0, P * 3 * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(h->st, 0, P * sizeof(PointState), h->stream));
+    if (h->flags) CK(cudaMemsetAsync(h->flags, 0, static_cast<size_t>(P) * h->K2p, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->P = P;
+    h->stats.points = P;
+  });
+}
+
+int fe2_hrom_solve_increment_device(fe2_hrom_t h, const double* d_E, const fe2_newton_opts_t* opts, double* d_sigma,
+                                    double* d_C, int* d_iters, int* d_pc, double* d_res, int* d_status,
+                                    void* stream) {
+  return guard([&] {
+    check(h != nullptr && d_E != nullptr, Code::config, "bad arguments");
+    CK(cudaSetDevice(h->device));
+    Outputs O{d_sigma ? d_sigma : h->o_sigma, d_C ? d_C : h->o_C, d_res ? d_res : h->o_res,
+              d_iters ? d_iters : h->o_iters, d_status ? d_status : h->o_status, d_pc ? d_pc : h->o_pc};
+    run_increment(h, d_E, opts, O, stream ? static_cast<cudaStream_t>(stream) : h->stream);
+  });
+}
+
+int fe2_hrom_solve_increment(fe2_hrom_t h, const double* E, const fe2_newton_opts_t* opts, double* sigma, double* C,
+                             int* iters, int* plastic_count, double* res_norm, int* status) {
+  return guard([&] {
+    check(h != nullptr && E != nullptr, Code::config, "bad arguments");
+    check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+    CK(cudaSetDevice(h->device));
+    const int64_t P = h->P;
+    cudaStream_t s = h->stream;
+    CK(cudaMemcpyAsync(h->dE, E, P * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    Outputs O{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc};
+    run_increment(h, h->dE, opts, O, s);
+    if (sigma) CK(cudaMemcpyAsync(sigma, h->o_sigma, P * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (C) CK(cudaMemcpyAsync(C, h->o_C, P * 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (iters) CK(cudaMemcpyAsync(iters, h->o_iters, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (plastic_count) CK(cudaMemcpyAsync(plastic_count, h->o_pc, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (res_norm) CK(cudaMemcpyAsync(res_norm, h->o_res, P * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (status) CK(cudaMemcpyAsync(status, h->o_status, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* flags) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated");
+    check(!flags || h->keep_flags, Code::config, "plastic flags were not kept (alloc_points keep_flags=0)");
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    const int64_t P = h->P;
+    const int n = h->n, NP = h->NP, K = h->K, K2p = h->K2p;
+    std::vector<double> ac(static_cast<size_t>(P) * NP);
+    CK(cudaMemcpy(ac.data(), h->alpha_c, ac.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (alpha)
+      for (int64_t p = 0; p < P; ++p)
+        for (int a = 0; a < n; ++a) alpha[p * n + a] = ac[p * NP + a];
+    if (state) {
+      std::vector<double> hs(static_cast<size_t>(P) * K2p * 6), Ec(static_cast<size_t>(P) * 3);
+      CK(cudaMemcpy(hs.data(), h->hist, hs.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(Ec.data(), h->E_ev, Ec.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      const size_t PK = static_cast<size_t>(P) * K2p;
+      for (int64_t p = 0; p < P; ++p) {
+        for (int q2 = 0; q2 < h->K2; ++q2) {
+          double* s = state + (static_cast<size_t>(p) * K + h->j2_idx[q2]) * 6;
+          for (int c = 0; c < 6; ++c) s[c] = hs[c * PK + static_cast<size_t>(p) * K2p + q2];
+        }
+        for (int q : h->el_idx) {  // elastic: no history; sigma33 = lam (e11 + e22)
+          const double* Gq = h->G.data() + static_cast<size_t>(q) * 3 * n;
+          double e[3];
+          for (int i = 0; i < 3; ++i) {
+            double s = 0.0;
+            for (int a = 0; a < n; ++a) s += Gq[i * n + a] * ac[p * NP + a];
+            e[i] = Ec[p * 3 + i] + s;
+          }
+          double* s = state + (static_cast<size_t>(p) * K + q) * 6;
+          for (int c = 0; c < 5; ++c) s[c] = 0.0;
+          s[5] = h->qmat[q].lam * (e[0] + e[1]);
+        }
+      }
+    }
+    if (flags) {
+      std::vector<uint8_t> fl(static_cast<size_t>(P) * K2p);
+      CK(cudaMemcpy(fl.data(), h->flags, fl.size(), cudaMemcpyDeviceToHost));
+      std::memset(flags, 0, static_cast<size_t>(P) * K);
+      for (int64_t p = 0; p < P; ++p)
+        for (int q2 = 0; q2 < h->K2; ++q2) flags[static_cast<size_t>(p) * K + h->j2_idx[q2]] = fl[p * K2p + q2];
+    }
+  });
+}
+
+int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, const double* E, double* r,
+                            double* Kaa, double* KaE, double* C_EE, double* S_raw) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0 && point >= 0 && point < h->P, Code::config, "bad point");
+    check(alpha && E && r && Kaa && KaE && C_EE && S_raw, Code::config, "null buffer");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    const int n = h->n, NP = h->NP;
+    // save the point's evaluation state, evaluate, restore
+    std::vector<double> save_a(NP), save_e(3), a_in(NP, 0.0);
+    CK(cudaMemcpy(save_a.data(), h->alpha_ev + point * NP, NP * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(save_e.data(), h->E_ev + point * 3, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int a = 0; a < n; ++a) a_in[a] = alpha[a];
+    CK(cudaMemcpy(h->alpha_ev + point * NP, a_in.data(), NP * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->E_ev + point * 3, E, 3 * sizeof(double), cudaMemcpyHostToDevice));
+    const int idx = static_cast<int>(point);
+    CK(cudaMemcpy(h->act[0], &idx, sizeof(int), cudaMemcpyHostToDevice));
+    const size_t dn = static_cast<size_t>(n) + n * n + 3 * n + 12;
+    double* dbg = dalloc<double>(dn);
+    RoundArgs a{};
+    a.M = h->model();
+    a.D = h->points();
+    a.O = Outputs{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc};
+    a.cfg = NewtonCfg{1e-8, 30, 4};
+    a.active = h->act[0];
+    a.n_active = 1;
+    a.next_active = h->act[1];
+    a.n_next = h->cnt + 1;
+    a.dbg = dbg;
+    launch_newton_round(a, s);
+    count_launch(h);
+    CK(cudaGetLastError());
+    std::vector<double> o(dn);
+    CK(cudaMemcpyAsync(o.data(), dbg, dn * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(dbg);
+    CK(cudaMemcpy(h->alpha_ev + point * NP, save_a.data(), NP * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->E_ev + point * 3, save_e.data(), 3 * sizeof(double), cudaMemcpyHostToDevice));
+    std::memcpy(r, o.data(), n * sizeof(double));
+    std::memcpy(Kaa, o.data() + n, static_cast<size_t>(n) * n * sizeof(double));
+    std::memcpy(KaE, o.data() + n + n * n, 3 * n * sizeof(double));
+    std::memcpy(C_EE, o.data() + n + n * n + 3 * n, 9 * sizeof(double));
+    std::memcpy(S_raw, o.data() + n + n * n + 3 * n + 9, 3 * sizeof(double));
+  });
+}
+
+int fe2_hrom_stats(fe2_hrom_t h, fe2_hrom_stats_t* out) {
+  return guard([&] {
+    check(h && out, Code::config, "bad arguments");
+    *out = h->stats;
+  });
+}
+
+int fe2_hrom_set_timing(fe2_hrom_t h, int on) {
+  return guard([&] {
+    check(h != nullptr, Code::config, "bad arguments");
+    h->timing = on != 0;
+  });
+}
+
+}  // extern "C"

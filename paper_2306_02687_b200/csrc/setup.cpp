@@ -1,0 +1,406 @@
+// Offline stage of the hyper-ROM model (host C++, no GPU): the unit-cell RVE
+// mesh, the per-integration-point strain operators, a seeded orthonormal
+// fluctuation basis Φ, a seeded cubature rule, and the projected operators
+// G_q = B_q Φ that the device kernels contract. This is the input generator
+// for BASELINE.json's configs; the online path never calls back into it.
+//
+// Reference behaviour followed (paths relative to
+// /root/reference/proj/include/fe2rom/):
+//   RveGeometry::default_cell           mesh.hpp:185-191
+//   build_rve_mesh (snap, mid-edge, pore) mesh.hpp:218-352
+//   tri6 gradients / shape_eval          mesh.hpp:67-115 ; tri3 rule :33-38
+//   linear BC (boundary DOFs fixed)      rve.hpp:84-92 ; free numbering :122-124
+//   IpData weight = w_g * detJ           rve.hpp:178-181
+//   Rng (mt19937_64, uniform, normal)    common.hpp:56-88
+// Seeded choices the reference leaves open (Φ, cubature, paths) are the
+// DESIGN.md "Inputs" decisions; tests/test_setup.py checks this builder
+// against the independent CPU oracle bit for bit.
+#include "fe2rom/fe2rom_gpu.h"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numbers>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace fe2 {
+
+namespace {
+
+class SeededStream {  // common.hpp:56-88
+ public:
+  explicit SeededStream(std::uint64_t seed) : mt_(seed) {}
+  double unit() { return static_cast<double>(mt_() >> 11) * 0x1.0p-53; }
+  double in(double lo, double hi) { return lo + (hi - lo) * unit(); }
+  int below(int n) { return std::min(n - 1, static_cast<int>(unit() * n)); }
+  double gauss() {
+    if (cached_) {
+      cached_ = false;
+      return spare_;
+    }
+    double u1 = unit();
+    while (u1 <= 1e-300) u1 = unit();
+    const double rad = std::sqrt(-2.0 * std::log(u1));
+    const double ang = 2.0 * std::numbers::pi * unit();
+    spare_ = rad * std::sin(ang);
+    cached_ = true;
+    return rad * std::cos(ang);
+  }
+
+ private:
+  std::mt19937_64 mt_;
+  double spare_ = 0.0;
+  bool cached_ = false;
+};
+
+constexpr std::uint64_t kPhiStream = 0x243F6A8885A308D3ull;
+constexpr std::uint64_t kRuleStream = 0x13198A2E03707344ull;
+constexpr std::uint64_t kPathStream = 0xA4093822299F31D0ull;
+
+std::uint64_t mix64(std::uint64_t x) {  // splitmix64 finaliser
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+struct Disc {
+  double cx, cy, rad;
+  double distance(double x, double y) const { return std::hypot(x - cx, y - cy); }
+};
+
+struct Cell {  // unit-cell mesh
+  std::vector<double> x, y;           // nodes
+  std::vector<std::array<int, 6>> tri;
+  std::vector<int> phase;             // 0 matrix, 1 inclusion
+  std::vector<char> on_boundary;      // node lies on the cell boundary
+  double area = 0.0;
+};
+
+// Element strain operator at reference point (xi, eta): returns detJ and
+// writes the 3x12 operator rows (dN/dx, dN/dy interleaved per node).
+double strain_operator(const Cell& c, const std::array<int, 6>& t, double xi, double eta, double Bop[3][12]) {
+  const double l1 = 1.0 - xi - eta, l2 = xi, l3 = eta;
+  const double g[6][2] = {{-(4.0 * l1 - 1.0), -(4.0 * l1 - 1.0)},
+                          {4.0 * l2 - 1.0, 0.0},
+                          {0.0, 4.0 * l3 - 1.0},
+                          {4.0 * (l1 - l2), -4.0 * l2},
+                          {4.0 * l3, 4.0 * l2},
+                          {-4.0 * l3, 4.0 * (l1 - l3)}};
+  double j00 = 0.0, j01 = 0.0, j10 = 0.0, j11 = 0.0;
+  for (int a = 0; a < 6; ++a) {
+    j00 += g[a][0] * c.x[t[a]];
+    j01 += g[a][0] * c.y[t[a]];
+    j10 += g[a][1] * c.x[t[a]];
+    j11 += g[a][1] * c.y[t[a]];
+  }
+  const double det = j00 * j11 - j01 * j10;
+  if (!(det > 0.0)) throw Failure(Code::mesh, "inverted element (detJ <= 0)");
+  const double k00 = j11 / det, k01 = -j01 / det, k10 = -j10 / det, k11 = j00 / det;
+  std::memset(Bop, 0, sizeof(double) * 36);
+  for (int a = 0; a < 6; ++a) {
+    const double dx = k00 * g[a][0] + k01 * g[a][1];
+    const double dy = k10 * g[a][0] + k11 * g[a][1];
+    Bop[0][2 * a] = dx;
+    Bop[1][2 * a + 1] = dy;
+    Bop[2][2 * a] = dy;
+    Bop[2][2 * a + 1] = dx;
+  }
+  return det;
+}
+
+constexpr double kGauss[3][2] = {{1.0 / 6.0, 1.0 / 6.0}, {2.0 / 3.0, 1.0 / 6.0}, {1.0 / 6.0, 2.0 / 3.0}};
+constexpr double kGaussW = 1.0 / 6.0;
+
+Cell mesh_default_cell(int sub) {
+  if (sub < 2) throw Failure(Code::config, "rve subdivisions must be >= 2");
+  const std::vector<Disc> incl = {{0.3, 0.3, 0.2}, {0.7, 0.65, 0.2}};
+  const Disc pore{0.65, 0.25, 0.15};
+  std::vector<Disc> discs = incl;
+  discs.push_back(pore);
+  const double margin = 0.5 / sub;
+  for (const auto& d : discs) {
+    const bool inside = d.cx - d.rad > margin && d.cx + d.rad < 1.0 - margin && d.cy - d.rad > margin &&
+                        d.cy + d.rad < 1.0 - margin;
+    if (!inside) throw Failure(Code::geometry, "inclusion/pore not inside unit cell");
+  }
+  const int g = 2 * sub + 1;
+  const int nn = g * g;
+  std::vector<double> px(nn), py(nn);
+  for (int j = 0; j < g; ++j)
+    for (int i = 0; i < g; ++i) {
+      px[j * g + i] = i / (g - 1.0);
+      py[j * g + i] = j / (g - 1.0);
+    }
+  const double band = 0.3 / sub;
+  std::vector<int> snapped(nn, -1);
+  auto project = [&](int id, const Disc& d) {
+    const double r = d.distance(px[id], py[id]);
+    if (r > 1e-12) {
+      px[id] = d.cx + (px[id] - d.cx) * d.rad / r;
+      py[id] = d.cy + (py[id] - d.cy) * d.rad / r;
+    }
+  };
+  for (int j = 2; j < g - 1; j += 2)
+    for (int i = 2; i < g - 1; i += 2) {
+      const int id = j * g + i;
+      int pick = -1, near = 0;
+      double gap_best = band;
+      for (int c = 0; c < (int)discs.size(); ++c) {
+        const double gap = std::abs(discs[c].distance(px[id], py[id]) - discs[c].rad);
+        near += gap < band;
+        if (gap < gap_best) {
+          gap_best = gap;
+          pick = c;
+        }
+      }
+      if (near > 1 || pick < 0) continue;
+      project(id, discs[pick]);
+      snapped[id] = pick;
+    }
+  auto midpoint = [&](int mid, int a, int b) {
+    px[mid] = 0.5 * (px[a] + px[b]);
+    py[mid] = 0.5 * (py[a] + py[b]);
+    if (snapped[a] >= 0 && snapped[a] == snapped[b]) project(mid, discs[snapped[a]]);
+  };
+  for (int j = 0; j < g; ++j)
+    for (int i = 0; i < g; ++i) {
+      const int oi = i & 1, oj = j & 1;
+      if (oi && !oj) midpoint(j * g + i, j * g + i - 1, j * g + i + 1);
+      if (!oi && oj) midpoint(j * g + i, (j - 1) * g + i, (j + 1) * g + i);
+      if (oi && oj) midpoint(j * g + i, (j - 1) * g + i - 1, (j + 1) * g + i + 1);
+    }
+  Cell cell;
+  std::vector<int> renum(nn, -1);
+  for (int j = 0; j < sub; ++j)
+    for (int i = 0; i < sub; ++i) {
+      const int b = (2 * j) * g + 2 * i;  // lower-left corner
+      const std::array<std::array<int, 6>, 2> pair = {{
+          {b, b + 2, b + 2 * g + 2, b + 1, b + g + 2, b + g + 1},
+          {b, b + 2 * g + 2, b + 2 * g, b + g + 1, b + 2 * g + 1, b + g},
+      }};
+      for (const auto& t : pair) {
+        const double cx = (px[t[0]] + px[t[1]] + px[t[2]]) / 3.0;
+        const double cy = (py[t[0]] + py[t[1]] + py[t[2]]) / 3.0;
+        if (pore.distance(cx, cy) < pore.rad) continue;
+        int ph = 0;
+        for (const auto& d : incl)
+          if (d.distance(cx, cy) < d.rad) {
+            ph = 1;
+            break;
+          }
+        std::array<int, 6> loc;
+        for (int a = 0; a < 6; ++a) {
+          if (renum[t[a]] < 0) {
+            renum[t[a]] = (int)cell.x.size();
+            cell.x.push_back(px[t[a]]);
+            cell.y.push_back(py[t[a]]);
+          }
+          loc[a] = renum[t[a]];
+        }
+        cell.tri.push_back(loc);
+        cell.phase.push_back(ph);
+      }
+    }
+  if (cell.tri.empty()) throw Failure(Code::mesh, "meshing produced no elements");
+  cell.on_boundary.assign(cell.x.size(), 0);
+  for (size_t k = 0; k < cell.x.size(); ++k) {
+    const double x = cell.x[k], y = cell.y[k];
+    cell.on_boundary[k] = std::abs(x) < 1e-12 || std::abs(x - 1.0) < 1e-12 || std::abs(y) < 1e-12 ||
+                          std::abs(y - 1.0) < 1e-12;
+  }
+  double area = 0.0;
+  double Bop[3][12];
+  for (const auto& t : cell.tri) {
+    double a = 0.0;
+    for (int q = 0; q < 3; ++q) a += kGaussW * strain_operator(cell, t, kGauss[q][0], kGauss[q][1], Bop);
+    area += a;
+  }
+  cell.area = area;
+  return cell;
+}
+
+// Orthonormal basis by Householder reflections: Q = H_0 ... H_{n-1} [I; 0].
+void orthonormalise(std::vector<double>& A, int m, int n) {
+  std::vector<double> refl;        // packed reflectors
+  std::vector<size_t> off(n + 1, 0);
+  std::vector<double> beta(n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double ss = 0.0;
+    for (int i = j; i < m; ++i) ss += A[(size_t)i * n + j] * A[(size_t)i * n + j];
+    const double len = std::sqrt(ss);
+    const double shift = A[(size_t)j * n + j] >= 0.0 ? -len : len;
+    off[j] = refl.size();
+    for (int i = j; i < m; ++i) refl.push_back(A[(size_t)i * n + j]);
+    double* v = refl.data() + off[j];
+    v[0] = v[0] - shift;
+    double vv = 0.0;
+    for (int i = 0; i < m - j; ++i) vv += v[i] * v[i];
+    if (vv > 0.0) {
+      beta[j] = 2.0 / vv;
+      for (int c = j; c < n; ++c) {
+        double dot = 0.0;
+        for (int i = j; i < m; ++i) dot += v[i - j] * A[(size_t)i * n + c];
+        const double s = beta[j] * dot;
+        for (int i = j; i < m; ++i) A[(size_t)i * n + c] = A[(size_t)i * n + c] - s * v[i - j];
+      }
+    }
+  }
+  off[n] = refl.size();
+  std::vector<double> Q((size_t)m * n, 0.0);
+  for (int j = 0; j < n; ++j) Q[(size_t)j * n + j] = 1.0;
+  for (int j = n - 1; j >= 0; --j) {
+    if (beta[j] == 0.0) continue;
+    const double* v = refl.data() + off[j];
+    for (int c = 0; c < n; ++c) {
+      double dot = 0.0;
+      for (int i = j; i < m; ++i) dot += v[i - j] * Q[(size_t)i * n + c];
+      const double s = beta[j] * dot;
+      for (int i = j; i < m; ++i) Q[(size_t)i * n + c] = Q[(size_t)i * n + c] - s * v[i - j];
+    }
+  }
+  A.swap(Q);
+}
+
+}  // namespace
+
+struct Model {
+  int n = 0, K = 0, n_free = 0;
+  double volume = 0.0;
+  std::vector<double> G, w;
+  std::vector<int> ip, mat;
+};
+
+Model build_model(int sub, int n, int K, std::uint64_t seed) {
+  const Cell cell = mesh_default_cell(sub);
+  const int n_nodes = (int)cell.x.size();
+  const int n_ip = 3 * (int)cell.tri.size();
+  std::vector<int> dof_free(2 * n_nodes, -1);
+  int nf = 0;
+  for (int d = 0; d < 2 * n_nodes; ++d)
+    if (!cell.on_boundary[d / 2]) dof_free[d] = nf++;
+  if (n < 1 || n > nf) throw Failure(Code::config, "mode count out of range");
+  if (K < 1 || K > n_ip) throw Failure(Code::config, "cubature size out of range");
+
+  std::vector<double> phi((size_t)nf * n);
+  {
+    SeededStream s(seed ^ kPhiStream);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < nf; ++i) phi[(size_t)i * n + j] = s.gauss();
+    orthonormalise(phi, nf, n);
+  }
+  Model md;
+  md.n = n;
+  md.K = K;
+  md.n_free = nf;
+  md.volume = cell.area;
+  {
+    SeededStream s(seed ^ kRuleStream);
+    std::vector<int> perm(n_ip);
+    for (int i = 0; i < n_ip; ++i) perm[i] = i;
+    for (int i = 0; i < K; ++i) std::swap(perm[i], perm[i + s.below(n_ip - i)]);
+    const double unit_w = cell.area / K;
+    md.ip.assign(perm.begin(), perm.begin() + K);
+    for (int i = 0; i < K; ++i) md.w.push_back(s.in(0.5, 1.5) * unit_w);
+  }
+  md.G.assign((size_t)K * 3 * n, 0.0);
+  md.mat.resize(K);
+  double Bop[3][12];
+  for (int q = 0; q < K; ++q) {
+    const int e = md.ip[q] / 3, gp = md.ip[q] % 3;
+    const auto& t = cell.tri[e];
+    md.mat[q] = cell.phase[e];
+    strain_operator(cell, t, kGauss[gp][0], kGauss[gp][1], Bop);
+    int rows[12];
+    for (int d = 0; d < 12; ++d) rows[d] = dof_free[2 * t[d / 2] + d % 2];
+    double* Gq = md.G.data() + (size_t)q * 3 * n;
+    for (int i = 0; i < 3; ++i)
+      for (int a = 0; a < n; ++a) {
+        double acc = 0.0;
+        for (int d = 0; d < 12; ++d)
+          if (rows[d] >= 0) acc += Bop[i][d] * phi[(size_t)rows[d] * n + a];
+        Gq[i * n + a] = acc;
+      }
+  }
+  return md;
+}
+
+void make_paths(int kind, std::uint64_t seed, std::int64_t p0, std::int64_t P, int n_incr, double* E) {
+  for (std::int64_t k = 0; k < P; ++k) {
+    const std::uint64_t p = static_cast<std::uint64_t>(p0 + k);
+    SeededStream s(mix64(seed ^ kPathStream) ^ mix64(p));
+    double end[3];
+    double* out = E + (size_t)k * n_incr * 3;
+    if (kind == 0) {  // config 0: uniaxial E11 = 0.05 scaled by s, rotated by theta
+      const double scale = s.in(0.5, 1.5);
+      const double th = s.in(0.0, std::numbers::pi);
+      const double c = std::cos(th), sn = std::sin(th);
+      const double e = 0.05 * scale;
+      end[0] = e * (c * c);
+      end[1] = e * (sn * sn);
+      end[2] = e * (2.0 * sn * c);
+      for (int i = 1; i <= n_incr; ++i) {
+        const double f = static_cast<double>(i) / n_incr;
+        for (int c3 = 0; c3 < 3; ++c3) out[(i - 1) * 3 + c3] = end[c3] * f;
+      }
+    } else if (kind == 1) {  // config 1: bending-like (E11, 2 E12), reversed halfway
+      const double a = s.in(-0.03, 0.03);
+      const double b = s.in(-0.02, 0.02);
+      end[0] = a;
+      end[1] = 0.0;
+      end[2] = 2.0 * b;
+      const int half = n_incr / 2;
+      for (int i = 1; i <= n_incr; ++i) {
+        const double f = i <= half ? static_cast<double>(i) / half : static_cast<double>(n_incr - i) / half;
+        for (int c3 = 0; c3 < 3; ++c3) out[(i - 1) * 3 + c3] = end[c3] * f;
+      }
+    } else {
+      throw Failure(Code::config, "unknown path kind");
+    }
+  }
+}
+
+}  // namespace fe2
+
+struct fe2_model_s {
+  fe2::Model m;
+};
+
+extern "C" {
+
+int fe2_model_build(int subdivisions, int n, int K, uint64_t seed, fe2_model_t* out) {
+  return fe2::guard([&] { *out = new fe2_model_s{fe2::build_model(subdivisions, n, K, seed)}; });
+}
+void fe2_model_free(fe2_model_t m) { delete m; }
+int fe2_model_sizes(fe2_model_t m, int* n, int* K, int* n_free, double* volume) {
+  return fe2::guard([&] {
+    fe2::check(m != nullptr, fe2::Code::config, "null model");
+    if (n) *n = m->m.n;
+    if (K) *K = m->m.K;
+    if (n_free) *n_free = m->m.n_free;
+    if (volume) *volume = m->m.volume;
+  });
+}
+int fe2_model_arrays(fe2_model_t m, double* G, double* w, int* ip_id, int* mat_id) {
+  return fe2::guard([&] {
+    fe2::check(m != nullptr, fe2::Code::config, "null model");
+    if (G) std::memcpy(G, m->m.G.data(), m->m.G.size() * sizeof(double));
+    if (w) std::memcpy(w, m->m.w.data(), m->m.w.size() * sizeof(double));
+    if (ip_id) std::memcpy(ip_id, m->m.ip.data(), m->m.ip.size() * sizeof(int));
+    if (mat_id) std::memcpy(mat_id, m->m.mat.data(), m->m.mat.size() * sizeof(int));
+  });
+}
+int fe2_paths(int kind, uint64_t seed, int64_t p0, int64_t P, int n_incr, double* E) {
+  return fe2::guard([&] {
+    fe2::check(P >= 0 && n_incr >= 1 && E != nullptr, fe2::Code::config, "bad path arguments");
+    fe2::make_paths(kind, seed, p0, P, n_incr, E);
+  });
+}
+
+}  // extern "C"

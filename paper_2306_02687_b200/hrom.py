@@ -1,0 +1,274 @@
+"""ctypes mirror of the reference interface over the native C ABI.
+
+Reference names kept (paths relative to /root/reference/proj/include/fe2rom/):
+  ElasticParams / J2LinearParams          materials.hpp:37-49
+  update_material (batched)               materials.hpp:317-325
+  MicroOptions {tol, max_iter} + max_bisections   rve.hpp:195-200, :439-443
+  run_trajectory step per macro point     rve.hpp:448-494 (reduced: SPEC.md:289-297)
+Errors: Fe2Error carries the reference ErrorCode name (common.hpp:26-37).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libfe2rom_gpu.so")
+
+ERROR_CODES = ["config", "geometry", "mesh", "material", "solver", "numeric", "rank", "bc", "io", "provenance"]
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_u8p = C.POINTER(C.c_uint8)
+
+
+class Fe2Error(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        self.kind = ERROR_CODES[code - 1] if 1 <= code <= len(ERROR_CODES) else f"code{code}"
+        super().__init__(f"[{self.kind}] {msg}")
+
+
+class _Material(C.Structure):
+    _fields_ = [("kind", C.c_int), ("p", C.c_double * 4)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("max_bisections", C.c_int)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [
+        ("points", C.c_int64),
+        ("n", C.c_int),
+        ("K", C.c_int),
+        ("K_j2", C.c_int),
+        ("kernel_launches", C.c_int64),
+        ("newton_rounds", C.c_int64),
+        ("point_assemblies", C.c_int64),
+        ("j2_point_evals", C.c_int64),
+        ("last_increment_ms", C.c_double),
+        ("last_commit_ms", C.c_double),
+        ("last_assembly_ms", C.c_double),
+        ("last_commit_bytes", C.c_int64),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"native library missing: {LIB_PATH} — run __graft_entry__.build() "
+            "(there is no CPU fallback for the hyper-ROM engine)"
+        )
+    L = C.CDLL(LIB_PATH)
+    L.fe2_last_error.restype = C.c_char_p
+    L.fe2_version.restype = C.c_char_p
+    L.fe2_device_count.restype = C.c_int
+    L.fe2_material_update_batch.argtypes = [C.c_int, C.POINTER(_Material), C.c_int64, _dp, _dp, _dp, _dp, _dp, _u8p]
+    L.fe2_hrom_create.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _ip, C.POINTER(_Material), C.c_int, C.c_double,
+                                  C.POINTER(C.c_void_p)]
+    L.fe2_hrom_destroy.argtypes = [C.c_void_p]
+    L.fe2_hrom_destroy.restype = None
+    L.fe2_hrom_alloc_points.argtypes = [C.c_void_p, C.c_int64, C.c_int]
+    L.fe2_hrom_solve_increment.argtypes = [C.c_void_p, _dp, C.POINTER(_Opts), _dp, _dp, _ip, _ip, _dp, _ip]
+    L.fe2_hrom_solve_increment_device.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Opts), C.c_void_p, C.c_void_p,
+                                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.fe2_hrom_read_state.argtypes = [C.c_void_p, _dp, _dp, _u8p]
+    L.fe2_hrom_assemble_point.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+    L.fe2_hrom_stats.argtypes = [C.c_void_p, C.POINTER(_Stats)]
+    L.fe2_hrom_set_timing.argtypes = [C.c_void_p, C.c_int]
+    L.fe2_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
+    L.fe2_model_free.argtypes = [C.c_void_p]
+    L.fe2_model_free.restype = None
+    L.fe2_model_sizes.argtypes = [C.c_void_p, _ip, _ip, _ip, _dp]
+    L.fe2_model_arrays.argtypes = [C.c_void_p, _dp, _dp, _ip, _ip]
+    L.fe2_paths.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_int, _dp]
+    return L
+
+
+lib = _load()
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise Fe2Error(rc, lib.fe2_last_error().decode())
+
+
+def _d(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _i(a):
+    return None if a is None else a.ctypes.data_as(_ip)
+
+
+def _u8(a):
+    return None if a is None else a.ctypes.data_as(_u8p)
+
+
+def device_count() -> int:
+    return lib.fe2_device_count()
+
+
+@dataclass
+class ElasticParams:  # materials.hpp:37-43
+    E: float = 1.0
+    nu: float = 0.3
+
+    def _c(self):
+        return _Material(0, (C.c_double * 4)(self.E, self.nu, 0.0, 0.0))
+
+
+@dataclass
+class J2LinearParams:  # materials.hpp:45-49
+    E: float = 1.0
+    nu: float = 0.3
+    sigma_y0: float = 0.01
+    hardening: float = 0.016
+
+    def _c(self):
+        return _Material(1, (C.c_double * 4)(self.E, self.nu, self.sigma_y0, self.hardening))
+
+
+@dataclass
+class NewtonOptions:  # MicroOptions rve.hpp:195-200 + TrajectoryOptions::max_bisections
+    tol: float = 1e-8
+    max_iter: int = 30
+    max_bisections: int = 4
+
+    def _c(self):
+        return _Opts(self.tol, self.max_iter, self.max_bisections)
+
+
+def update_material_batch(mat, eps, state=None, device=0):
+    """Batched update_material on the GPU. eps (N,3) engineering Voigt,
+    state (N,6) = (eps_p[4], eq, sigma33) or None (virgin).
+    Returns sigma (N,3), C (N,3,3), state_out (N,6), plastic (N,) bool."""
+    eps = np.ascontiguousarray(eps, dtype=np.float64).reshape(-1, 3)
+    N = eps.shape[0]
+    st = None if state is None else np.ascontiguousarray(state, dtype=np.float64).reshape(N, 6)
+    sig = np.empty((N, 3))
+    Cm = np.empty((N, 3, 3))
+    so = np.empty((N, 6))
+    pl = np.empty(N, dtype=np.uint8)
+    m = mat._c()
+    _check(lib.fe2_material_update_batch(device, C.byref(m), N, _d(eps), _d(st), _d(sig), _d(Cm), _d(so), _u8(pl)))
+    return sig, Cm, so, pl.astype(bool)
+
+
+class HyperRomModel:
+    """Offline stage: seeded hyper-ROM model on the default_cell RVE
+    (mesh.hpp:185-191) — G[K,3,n], w[K], ip ids, material ids (0 matrix J2,
+    1 inclusion), volume. Host only."""
+
+    def __init__(self, subdivisions=33, n=12, K=200, seed=0):
+        h = C.c_void_p()
+        _check(lib.fe2_model_build(subdivisions, n, K, seed, C.byref(h)))
+        try:
+            n_, K_, nf, vol = C.c_int(), C.c_int(), C.c_int(), C.c_double()
+            _check(lib.fe2_model_sizes(h, C.byref(n_), C.byref(K_), C.byref(nf), C.byref(vol)))
+            self.n, self.K, self.n_free, self.volume = n_.value, K_.value, nf.value, vol.value
+            self.G = np.empty((self.K, 3, self.n))
+            self.w = np.empty(self.K)
+            self.ip = np.empty(self.K, dtype=np.int32)
+            self.mat = np.empty(self.K, dtype=np.int32)
+            _check(lib.fe2_model_arrays(h, _d(self.G), _d(self.w), _i(self.ip), _i(self.mat)))
+        finally:
+            lib.fe2_model_free(h)
+        self.subdivisions, self.seed = subdivisions, seed
+        self.materials = [J2LinearParams(1.0, 0.3, 0.01, 0.016), ElasticParams(10.0, 0.3)]
+
+    @property
+    def K_j2(self):
+        return int(np.sum(self.mat == 0))
+
+
+def make_paths(kind, seed, P, n_incr, p0=0):
+    """Seeded macro strain paths E[P, n_incr, 3] (BASELINE configs 0/1)."""
+    E = np.empty((P, n_incr, 3))
+    _check(lib.fe2_paths(kind, seed, p0, P, n_incr, _d(E)))
+    return E
+
+
+class HyperRomEngine:
+    """One device's batch of macro Gauss points evaluated with a hyper-ROM
+    RVE model: the reduced form of run_trajectory (rve.hpp:448-494) per
+    point, one increment per call."""
+
+    def __init__(self, G, w, mat_id, materials, volume, device=0):
+        G = np.ascontiguousarray(G, dtype=np.float64)
+        K, three, n = G.shape
+        assert three == 3
+        self.n, self.K = n, K
+        self._w = np.ascontiguousarray(w, dtype=np.float64)
+        self._mid = np.ascontiguousarray(mat_id, dtype=np.int32)
+        mats = (_Material * len(materials))(*[m._c() for m in materials])
+        h = C.c_void_p()
+        _check(lib.fe2_hrom_create(device, n, K, _d(G), _d(self._w), _i(self._mid), mats, len(materials),
+                                   float(volume), C.byref(h)))
+        self._h = h
+        self.P = 0
+
+    @classmethod
+    def from_model(cls, model: HyperRomModel, device=0):
+        return cls(model.G, model.w, model.mat, model.materials, model.volume, device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.fe2_hrom_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def alloc_points(self, P, keep_flags=False):
+        _check(lib.fe2_hrom_alloc_points(self._h, P, 1 if keep_flags else 0))
+        self.P = P
+
+    def solve_increment(self, E, opts: NewtonOptions | None = None):
+        """E (P,3) host → dict of sigma (P,3), C (P,3,3), iters, plastic_count, res_norm, status."""
+        E = np.ascontiguousarray(E, dtype=np.float64).reshape(self.P, 3)
+        out = dict(
+            sigma=np.empty((self.P, 3)), C=np.empty((self.P, 3, 3)), iters=np.empty(self.P, dtype=np.int32),
+            plastic_count=np.empty(self.P, dtype=np.int32), res_norm=np.empty(self.P),
+            status=np.empty(self.P, dtype=np.int32))
+        o = (opts or NewtonOptions())._c()
+        _check(lib.fe2_hrom_solve_increment(self._h, _d(E), C.byref(o), _d(out["sigma"]), _d(out["C"]),
+                                            _i(out["iters"]), _i(out["plastic_count"]), _d(out["res_norm"]),
+                                            _i(out["status"])))
+        return out
+
+    def solve_increment_device(self, E_ptr, sigma_ptr, C_ptr, iters_ptr, pc_ptr, res_ptr, status_ptr, stream=0,
+                               opts: NewtonOptions | None = None):
+        """Device-pointer variant (inputs already resident in HBM)."""
+        o = (opts or NewtonOptions())._c()
+        _check(lib.fe2_hrom_solve_increment_device(self._h, E_ptr, C.byref(o), sigma_ptr, C_ptr, iters_ptr, pc_ptr,
+                                                   res_ptr, status_ptr, stream or None))
+
+    def read_state(self, flags=False):
+        alpha = np.empty((self.P, self.n))
+        state = np.empty((self.P, self.K, 6))
+        fl = np.empty((self.P, self.K), dtype=np.uint8) if flags else None
+        _check(lib.fe2_hrom_read_state(self._h, _d(alpha), _d(state), _u8(fl)))
+        return alpha, state, fl
+
+    def assemble_point(self, point, alpha, E):
+        n = self.n
+        r, Kaa, KaE = np.empty(n), np.empty((n, n)), np.empty((n, 3))
+        CEE, S = np.empty((3, 3)), np.empty(3)
+        alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+        E = np.ascontiguousarray(E, dtype=np.float64)
+        _check(lib.fe2_hrom_assemble_point(self._h, point, _d(alpha), _d(E), _d(r), _d(Kaa), _d(KaE), _d(CEE),
+                                           _d(S)))
+        return dict(r=r, Kaa=Kaa, KaE=KaE, C_EE=CEE, S_raw=S)
+
+    def stats(self):
+        s = _Stats()
+        _check(lib.fe2_hrom_stats(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def set_timing(self, on=True):
+        _check(lib.fe2_hrom_set_timing(self._h, 1 if on else 0))
