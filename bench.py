@@ -1,0 +1,365 @@
+#!/usr/bin/env python3
+"""Benchmark: macro Gauss-point hyper-ROM evaluations/sec (fp64) on B200.
+
+One evaluation = one macro Gauss point advanced by one load increment to
+reduced-Newton convergence, returning Σ and the condensed C_macro
+(BASELINE.md). A bench "step" is one full BASELINE config-1 trajectory of the
+per-rank batch: P = 65,536 points x 50 increments (n = 24 modes, K = 400
+cubature points, seeded reversal paths), from the virgin state. Weak scaling
+over ranks: every rank owns P points (global ids rank*P..), and after every
+increment the macro stress, condensed tangent, residual norms and status are
+all-gathered over NCCL (the monolithic scheme's exchange).
+
+  value  : device-resident inputs (all increments' E already in HBM),
+           CUDA events on the engine's stream, max over ranks.
+  e2e    : the host-buffer C-ABI call fe2_hrom_solve_increment per increment
+           (pinned E H2D + outputs D2H inside the timed region).
+  --impl reference : the reference CPU algorithm (the C++ oracle restatement,
+           oracle/) on all host cores, bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]: the metric's quoted workload (fits one GPU)
+    1: dict(name="config1_beam_small_strain_j2", P=65536, n=24, K=400, incr=50, path=1, subdivisions=33),
+    # configs[0]: the reference's CPU-runnable case (parity config)
+    0: dict(name="config0_small_strain_j2", P=1024, n=12, K=200, incr=20, path=0, subdivisions=33),
+}
+METRIC = "macro Gauss-point hyper-ROM evaluations/sec (fp64)"
+UNIT = "evals/s"
+DMMA_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--points", type=int, default=0, help="override points per rank (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-points", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def flops_per_assembly(n, K_j2):
+    # F_asm = 3 K n (n + 9) (upper-triangle K_aa + K_aE + r),
+    # K = the J2 cubature points actually contracted (elastic block precomputed)
+    return 3.0 * K_j2 * n * (n + 9)
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out, _ = self.p.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def wrap_dev(ptr, shape, typestr, dev):
+    """torch view of a device buffer owned by the native engine."""
+    import torch
+
+    class _Buf:
+        __cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3,
+                                    "strides": None, "stream": None}
+
+    return torch.as_tensor(_Buf(), device=dev)
+
+
+def cpu_reference_run(cfg, n_points, threads, seed=0):
+    """The reference CPU algorithm (oracle restatement) on a sample of the
+    workload: the first n_points points, all increments. Returns evals/s."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    m = O.Model(cfg["subdivisions"], cfg["n"], cfg["K"], seed)
+    E = O.paths(cfg["path"], seed, n_points, cfg["incr"])
+    mats = [("j2", 1.0, 0.3, 0.01, 0.016), ("elastic", 10.0, 0.3)]
+    h = O.Hrom(m.G, m.w, m.mat, mats, m.volume)
+    t0 = time.perf_counter()
+    r = h.run(E, threads=threads)
+    dt = time.perf_counter() - t0
+    assert (r["status"] == 0).all()
+    return n_points * cfg["incr"] / dt, dt
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_pts = args.cpu_sample_points or max(threads * 8, 128)
+    for _ in range(args.warmup):
+        cpu_reference_run(cfg, max(threads, 16), threads)
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, dt = cpu_reference_run(cfg, n_pts, threads)
+        vals.append(v)
+        times.append(dt)
+    value = float(np.mean(vals))
+    sample = f"first {n_pts} points x {cfg['incr']} increments of {cfg['name']} per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "points": n_pts, "modes": cfg["n"], "cubature": cfg["K"],
+                   "increments": cfg["incr"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = dict(CONFIGS[args.config])
+    if args.points:
+        cfg["P"] = args.points
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_02687_b200 as F
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    P, incr = cfg["P"], cfg["incr"]
+    model = F.HyperRomModel(cfg["subdivisions"], cfg["n"], cfg["K"], seed=0)
+    E_host = F.make_paths(cfg["path"], 0, P, incr, p0=rank * P)  # (P, incr, 3), global-id streams
+    E_inc = np.ascontiguousarray(E_host.transpose(1, 0, 2))   # (incr, P, 3)
+    eng = F.HyperRomEngine.from_model(model, device=local)
+    eng.alloc_points(P)
+    stream = torch.cuda.current_stream(dev)
+    eng.set_stream(stream.cuda_stream)
+
+    # device-resident buffers
+    dE = torch.from_numpy(E_inc).to(dev)
+    d_sig = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    d_C = torch.empty((P, 9), dtype=torch.float64, device=dev)
+    d_res = torch.empty(P, dtype=torch.float64, device=dev)
+    d_it = torch.empty(P, dtype=torch.int32, device=dev)
+    d_pc = torch.empty(P, dtype=torch.int32, device=dev)
+    d_st = torch.empty(P, dtype=torch.int32, device=dev)
+    pack = torch.empty((P, 14), dtype=torch.float64, device=dev)
+    gathered = torch.empty((ws, P, 14), dtype=torch.float64, device=dev) if ws > 1 else None
+
+    def gather():
+        if ws == 1:
+            return
+        pack[:, 0:3] = d_sig
+        pack[:, 3:12] = d_C
+        pack[:, 12] = d_res
+        pack[:, 13] = d_st.to(torch.float64)
+        dist.all_gather_into_tensor(gathered, pack)
+
+    def device_step():
+        eng.reset_points()
+        for k in range(incr):
+            eng.solve_increment_device(dE[k].data_ptr(), d_sig.data_ptr(), d_C.data_ptr(), d_it.data_ptr(),
+                                       d_pc.data_ptr(), d_res.data_ptr(), d_st.data_ptr(), stream.cuda_stream)
+            gather()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, steps):
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        device_step()
+    # correctness guard on the warm-up trajectory
+    st_host = d_st.cpu().numpy()
+    if (st_host != 0).any():
+        raise SystemExit(f"bench: {int((st_host != 0).sum())} points failed to converge")
+
+    eng.reset_stats()
+    eng.set_timing(True)
+    launches0 = eng.stats()["kernel_launches"]
+    with ClockSampler(local) as clk:
+        ms = timed(device_step, args.steps)
+    stats = eng.stats()
+    eng.set_timing(False)
+    launches = stats["kernel_launches"] - launches0
+    evals = ws * P * incr * args.steps
+    value = evals / (ms / 1e3)
+
+    # ---- e2e through the host-buffer C-ABI (pinned host memory)
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+    E_pin = pin(E_inc)
+    o_sig, o_C, o_res = pin(np.empty((P, 3))), pin(np.empty((P, 9))), pin(np.empty(P))
+    o_it, o_pc, o_st = (pin(np.empty(P, dtype=np.int32)) for _ in range(3))
+    if ws > 1:  # the engine's own device output buffers, gathered after each host-API call
+        p_sig, p_C, p_it, p_pc, p_res, p_st = eng.output_ptrs()
+        e_sig = wrap_dev(p_sig, (P, 3), "<f8", dev)
+        e_C = wrap_dev(p_C, (P, 9), "<f8", dev)
+        e_res = wrap_dev(p_res, (P,), "<f8", dev)
+        e_st = wrap_dev(p_st, (P,), "<i4", dev)
+
+    def e2e_step():
+        eng.reset_points()
+        for k in range(incr):
+            eng.solve_increment_into(E_pin[k], o_sig, o_C, o_it, o_pc, o_res, o_st)
+            if ws > 1:
+                pack[:, 0:3] = e_sig
+                pack[:, 3:12] = e_C
+                pack[:, 12] = e_res
+                pack[:, 13] = e_st.to(torch.float64)
+                dist.all_gather_into_tensor(gathered, pack)
+
+    e2e_step()
+    ms_e2e = timed(e2e_step, max(1, min(args.steps, 3)))
+    e2e_steps = max(1, min(args.steps, 3))
+    e2e_value = ws * P * incr * e2e_steps / (ms_e2e / 1e3)
+    h2d = incr * P * 3 * 8
+    d2h = incr * P * (3 * 8 + 9 * 8 + 8 + 3 * 4)
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (fused assembly + Newton round)
+    F_asm = flops_per_assembly(cfg["n"], model.K_j2)
+    achieved = stats["round_assemblies"] * F_asm / (stats["round_ms"] / 1e3) / 1e12 if stats["round_ms"] else None
+    try:
+        peak = json.load(open(DMMA_PEAK_FILE))["dmma_tflops_w16"]
+        peak_src = "measured DMMA m8n8k4 f64 peak (tools/fp64_peak.cu, profiles/r01_fp64_peak.json)"
+    except Exception:
+        peak, peak_src = 37.0, "fallback: DMMA peak estimate"
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_round_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    avg_launch_ms = stats["round_ms"] / max(1, stats["timed_rounds"])
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "k_newton_round (fused hyper-assembly on DMMA + warp Cholesky/Newton/condensation)",
+                "peak_source": peak_src, "flops_per_point_assembly": F_asm,
+                "avg_launch_ms": avg_launch_ms, "share_of_step": stats["round_ms"] / ms if ms else None}
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        hbm_src = "MEASURED_PEAKS.json"
+    except Exception:
+        hbm, hbm_src = 6650.0, "fallback 6.65 TB/s"
+    commit_gbs = stats["commit_j2_evals"] * 88 / (stats["commit_ms"] / 1e3) / 1e9 if stats["commit_ms"] else None
+    roofline_commit = {"bound": "hbm", "achieved": commit_gbs, "peak": hbm, "unit": "GB/s",
+                       "frac": commit_gbs / hbm if commit_gbs else None, "peak_source": hbm_src,
+                       "kernel": "k_commit (constitutive update + SoA history write)", "bytes_per_j2_point": 88,
+                       "share_of_step": stats["commit_ms"] / ms if ms else None}
+
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        threads = os.cpu_count() or 1
+        n_pts = args.cpu_sample_points or max(threads * 8, 128)
+        v, dt = cpu_reference_run(cfg, n_pts, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"first {n_pts} points x {incr} increments of {cfg['name']} ({dt:.1f} s)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded Φ, cubature and paths, BASELINE configs)",
+        "config": {"workload": cfg["name"], "points_per_rank": P, "modes": cfg["n"], "cubature": cfg["K"],
+                   "cubature_j2": model.K_j2, "increments": incr, "parallelism": f"dp{ws} (points sharded)",
+                   "l2": "inputs larger than L2 (history %.2f GB per rank > 126 MB L2)" % (P * model.K_j2 * 48 / 1e9),
+                   "step": "one full trajectory of all points (reset to virgin state)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "api": "fe2_hrom_solve_increment (host buffers, pinned)"},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "roofline_commit": roofline_commit,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "newton": {"rounds": stats["newton_rounds"], "point_assemblies_per_eval": stats["round_assemblies"] / evals * ws},
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -89,6 +89,12 @@ void fe2_hrom_destroy(fe2_hrom_t h);
  * keep_flags != 0 also keeps per-(point, cubature point) plastic flags of
  * the last commit (P*K bytes) for parity checks. */
 int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags);
+/* Return the allocated points to the virgin state (no reallocation). */
+int fe2_hrom_reset_points(fe2_hrom_t h);
+/* Device pointers of the handle's own output buffers (filled by every
+ * fe2_hrom_solve_increment call), e.g. to all-gather them over NCCL. */
+int fe2_hrom_output_ptrs(fe2_hrom_t h, double** d_sigma, double** d_C, int** d_iters, int** d_plastic_count,
+                         double** d_res_norm, int** d_status);
 
 /* One load increment for all P points: E[P*3] is the path point of this
  * increment (the previous one is remembered; the first starts from 0).
@@ -122,14 +128,20 @@ typedef struct {
   int64_t newton_rounds;     /* fused assemble+step rounds since create */
   int64_t point_assemblies;  /* (point, assembly) pairs processed since create */
   int64_t j2_point_evals;    /* (point, J2 cubature point) material updates in assembly */
-  double last_increment_ms;  /* device time of the last increment */
-  double last_commit_ms;     /* device time of the last commit kernel */
-  double last_assembly_ms;   /* device time summed over the rounds of the last increment */
-  int64_t last_commit_bytes; /* algorithmic HBM bytes of the last commit kernel */
+  /* CUDA-event kernel timing (only while fe2_hrom_set_timing is on) */
+  double round_ms;            /* summed duration of the fused assemble+Newton launches */
+  int64_t round_assemblies;   /* (point, assembly) pairs in those launches */
+  double commit_ms;           /* summed duration of the history-commit launches */
+  int64_t commit_j2_evals;    /* (point, J2 cubature point) pairs committed in them */
+  int64_t timed_rounds, timed_commits;
 } fe2_hrom_stats_t;
 int fe2_hrom_stats(fe2_hrom_t h, fe2_hrom_stats_t* out);
-/* enable per-kernel CUDA-event timing inside solve_increment (costs syncs) */
+/* zero every counter of fe2_hrom_stats */
+int fe2_hrom_reset_stats(fe2_hrom_t h);
+/* enable per-launch CUDA-event timing inside solve_increment */
 int fe2_hrom_set_timing(fe2_hrom_t h, int on);
+/* order all later work of the handle on `stream` (cudaStream_t; NULL = own) */
+int fe2_hrom_set_stream(fe2_hrom_t h, void* stream);
 
 /* ---- offline stage (host only, no GPU): seeded hyper-ROM model and paths
  * matching BASELINE.json configs. */

@@ -69,7 +69,8 @@ using namespace fe2;
 
 struct fe2_hrom_s {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;       // work stream (own, or the caller's)
+  cudaStream_t own_stream = nullptr;
   int n = 0, NP = 0, S = 0, K = 0, K2 = 0, K2p = 0;
   double volume = 0.0;
   std::vector<int> j2_idx, el_idx;  // original cubature indices
@@ -161,7 +162,7 @@ struct fe2_hrom_s {
     if (h_cnt) cudaFreeHost(h_cnt);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
-    if (stream) cudaStreamDestroy(stream);
+    if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
 
@@ -182,7 +183,6 @@ void run_increment(fe2_hrom_t h, const double* d_E, const fe2_newton_opts_t* opt
   check(cfg.tol > 0.0 && cfg.max_iter >= 0 && cfg.max_bis >= 0, Code::config, "invalid Newton options");
   const ModelDev M = h->model();
   const PointsDev D = h->points();
-  if (h->timing) CK(cudaEventRecord(h->ev[0], s));
   CK(cudaMemsetAsync(h->cnt, 0, 2 * sizeof(int), s));
   launch_begin_increment(M, D, O, d_E, h->act[0], h->cnt, s);
   count_launch(h);
@@ -208,32 +208,39 @@ void run_increment(fe2_hrom_t h, const double* d_E, const fe2_newton_opts_t* opt
     a.next_active = h->act[cur ^ 1];
     a.n_next = next_cnt;
     a.dbg = nullptr;
+    if (h->timing) CK(cudaEventRecord(h->ev[0], s));
     launch_newton_round(a, s);
     count_launch(h);
     CK(cudaGetLastError());
+    if (h->timing) CK(cudaEventRecord(h->ev[1], s));
     h->stats.newton_rounds += 1;
     h->stats.point_assemblies += n_active;
     h->stats.j2_point_evals += static_cast<int64_t>(n_active) * h->K2;
     CK(cudaMemcpyAsync(h->h_cnt, next_cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (h->timing) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+      h->stats.round_ms += ms;
+      h->stats.round_assemblies += n_active;
+      h->stats.timed_rounds += 1;
+    }
     n_active = *h->h_cnt;
     cur ^= 1;
   }
-  if (h->timing) CK(cudaEventRecord(h->ev[1], s));
+  if (h->timing) CK(cudaEventRecord(h->ev[2], s));
   launch_commit(M, D, O, s);
   count_launch(h);
   CK(cudaGetLastError());
-  if (h->timing) CK(cudaEventRecord(h->ev[2], s));
+  if (h->timing) CK(cudaEventRecord(h->ev[3], s));
   CK(cudaStreamSynchronize(s));
   if (h->timing) {
-    float t01 = 0, t12 = 0;
-    CK(cudaEventElapsedTime(&t01, h->ev[0], h->ev[1]));
-    CK(cudaEventElapsedTime(&t12, h->ev[1], h->ev[2]));
-    h->stats.last_assembly_ms = t01;
-    h->stats.last_commit_ms = t12;
-    h->stats.last_increment_ms = t01 + t12;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
+    h->stats.commit_ms += ms;
+    h->stats.commit_j2_evals += h->P * static_cast<int64_t>(h->K2);
+    h->stats.timed_commits += 1;
   }
-  h->stats.last_commit_bytes = h->P * static_cast<int64_t>(h->K2) * 88;
 }
 
 }  // namespace
@@ -348,7 +355,8 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
           }
         }
       }
-      CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+      h->stream = h->own_stream;
       for (auto& e : h->ev) CK(cudaEventCreate(&e));
       h->G2 = dalloc<double>(G2.size());
       h->w2 = dalloc<double>(w2.size());
@@ -410,6 +418,34 @@ int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
     CK(cudaStreamSynchronize(h->stream));
     h->P = P;
     h->stats.points = P;
+  });
+}
+
+int fe2_hrom_reset_points(fe2_hrom_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated");
+    CK(cudaSetDevice(h->device));
+    const int64_t P = h->P;
+    cudaStream_t s = h->stream;
+    CK(cudaMemsetAsync(h->hist, 0, static_cast<size_t>(P) * h->K2p * 6 * sizeof(double), s));
+    const size_t an = static_cast<size_t>(P) * h->NP * sizeof(double);
+    for (double* p : {h->alpha_c, h->alpha, h->alpha_ev, h->dalpha}) CK(cudaMemsetAsync(p, 0, an, s));
+    for (double* p : {h->E_prev, h->E_tgt, h->E_ev}) CK(cudaMemsetAsync(p, 0, P * 3 * sizeof(double), s));
+    CK(cudaMemsetAsync(h->st, 0, P * sizeof(PointState), s));
+    if (h->flags) CK(cudaMemsetAsync(h->flags, 0, static_cast<size_t>(P) * h->K2p, s));
+  });
+}
+
+int fe2_hrom_output_ptrs(fe2_hrom_t h, double** d_sigma, double** d_C, int** d_iters, int** d_pc, double** d_res,
+                         int** d_status) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated");
+    if (d_sigma) *d_sigma = h->o_sigma;
+    if (d_C) *d_C = h->o_C;
+    if (d_iters) *d_iters = h->o_iters;
+    if (d_pc) *d_pc = h->o_pc;
+    if (d_res) *d_res = h->o_res;
+    if (d_status) *d_status = h->o_status;
   });
 }
 
@@ -543,6 +579,27 @@ int fe2_hrom_stats(fe2_hrom_t h, fe2_hrom_stats_t* out) {
   return guard([&] {
     check(h && out, Code::config, "bad arguments");
     *out = h->stats;
+  });
+}
+
+int fe2_hrom_reset_stats(fe2_hrom_t h) {
+  return guard([&] {
+    check(h != nullptr, Code::config, "bad arguments");
+    const fe2_hrom_stats_t keep = h->stats;
+    h->stats = fe2_hrom_stats_t{};
+    h->stats.points = keep.points;
+    h->stats.n = keep.n;
+    h->stats.K = keep.K;
+    h->stats.K_j2 = keep.K_j2;
+  });
+}
+
+int fe2_hrom_set_stream(fe2_hrom_t h, void* stream) {
+  return guard([&] {
+    check(h != nullptr, Code::config, "bad arguments");
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
   });
 }
 

@@ -50,10 +50,12 @@ class _Stats(C.Structure):
         ("newton_rounds", C.c_int64),
         ("point_assemblies", C.c_int64),
         ("j2_point_evals", C.c_int64),
-        ("last_increment_ms", C.c_double),
-        ("last_commit_ms", C.c_double),
-        ("last_assembly_ms", C.c_double),
-        ("last_commit_bytes", C.c_int64),
+        ("round_ms", C.c_double),
+        ("round_assemblies", C.c_int64),
+        ("commit_ms", C.c_double),
+        ("commit_j2_evals", C.c_int64),
+        ("timed_rounds", C.c_int64),
+        ("timed_commits", C.c_int64),
     ]
 
 
@@ -80,6 +82,10 @@ def _load():
     L.fe2_hrom_assemble_point.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
     L.fe2_hrom_stats.argtypes = [C.c_void_p, C.POINTER(_Stats)]
     L.fe2_hrom_set_timing.argtypes = [C.c_void_p, C.c_int]
+    L.fe2_hrom_reset_stats.argtypes = [C.c_void_p]
+    L.fe2_hrom_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+    L.fe2_hrom_reset_points.argtypes = [C.c_void_p]
+    L.fe2_hrom_output_ptrs.argtypes = [C.c_void_p] + [C.POINTER(C.c_void_p)] * 6
     L.fe2_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.fe2_model_free.argtypes = [C.c_void_p]
     L.fe2_model_free.restype = None
@@ -228,6 +234,23 @@ class HyperRomEngine:
         _check(lib.fe2_hrom_alloc_points(self._h, P, 1 if keep_flags else 0))
         self.P = P
 
+    def reset_points(self):
+        _check(lib.fe2_hrom_reset_points(self._h))
+
+    def output_ptrs(self):
+        """Device pointers (ints) of the handle's own output buffers:
+        sigma, C, iters, plastic_count, res_norm, status."""
+        ps = [C.c_void_p() for _ in range(6)]
+        _check(lib.fe2_hrom_output_ptrs(self._h, *[C.byref(p) for p in ps]))
+        return [p.value for p in ps]
+
+    def solve_increment_into(self, E, sigma, Cm, iters, pc, res, status, opts: NewtonOptions | None = None):
+        """Host-buffer C-ABI call writing into caller-provided (e.g. pinned)
+        numpy arrays; E (P,3) host."""
+        o = (opts or NewtonOptions())._c()
+        _check(lib.fe2_hrom_solve_increment(self._h, _d(E), C.byref(o), _d(sigma), _d(Cm), _i(iters), _i(pc),
+                                            _d(res), _i(status)))
+
     def solve_increment(self, E, opts: NewtonOptions | None = None):
         """E (P,3) host → dict of sigma (P,3), C (P,3,3), iters, plastic_count, res_norm, status."""
         E = np.ascontiguousarray(E, dtype=np.float64).reshape(self.P, 3)
@@ -272,3 +295,10 @@ class HyperRomEngine:
 
     def set_timing(self, on=True):
         _check(lib.fe2_hrom_set_timing(self._h, 1 if on else 0))
+
+    def reset_stats(self):
+        _check(lib.fe2_hrom_reset_stats(self._h))
+
+    def set_stream(self, stream_ptr):
+        """Order the engine's work on a caller's cudaStream_t (int handle; 0 = own)."""
+        _check(lib.fe2_hrom_set_stream(self._h, stream_ptr or None))
