@@ -77,14 +77,15 @@ struct fe2_hrom_s {
   std::vector<double> G, w;         // host copy (caller order)
   std::vector<MatDev> qmat;         // per original cubature point
   MatDev mat2{};
-  double CEEinc[9] = {0};
+  double CEEe[9] = {0};
   // device model
-  double *G2 = nullptr, *w2 = nullptr, *Kinc = nullptr, *KaEinc = nullptr;
+  double *G2 = nullptr, *w2 = nullptr, *Ke = nullptr, *KaEe = nullptr;
   // device points
   int64_t P = 0;
   bool keep_flags = false;
   double *hist = nullptr, *alpha_c = nullptr, *alpha = nullptr, *alpha_ev = nullptr, *dalpha = nullptr;
   double *E_prev = nullptr, *E_tgt = nullptr, *E_ev = nullptr;
+  double *bp = nullptr, *sp = nullptr;
   PointState* st = nullptr;
   uint8_t* flags = nullptr;
   int *act[2] = {nullptr, nullptr}, *cnt = nullptr;
@@ -107,9 +108,9 @@ struct fe2_hrom_s {
     M.nchunks = K2p / kQC;
     M.G2 = G2;
     M.w2 = w2;
-    M.Kinc = Kinc;
-    M.KaEinc = KaEinc;
-    std::memcpy(M.CEEinc, CEEinc, sizeof CEEinc);
+    M.Ke = Ke;
+    M.KaEe = KaEe;
+    std::memcpy(M.CEEe, CEEe, sizeof CEEe);
     M.volume = volume;
     M.mat2 = mat2;
     return M;
@@ -125,6 +126,8 @@ struct fe2_hrom_s {
     D.E_prev = E_prev;
     D.E_tgt = E_tgt;
     D.E_ev = E_ev;
+    D.bp = bp;
+    D.sp = sp;
     D.st = st;
     D.flags = flags;
     return D;
@@ -138,6 +141,8 @@ struct fe2_hrom_s {
     dfree(E_prev);
     dfree(E_tgt);
     dfree(E_ev);
+    dfree(bp);
+    dfree(sp);
     dfree(st);
     dfree(flags);
     dfree(act[0]);
@@ -156,8 +161,8 @@ struct fe2_hrom_s {
     free_points();
     dfree(G2);
     dfree(w2);
-    dfree(Kinc);
-    dfree(KaEinc);
+    dfree(Ke);
+    dfree(KaEe);
     dfree(cnt);
     if (h_cnt) cudaFreeHost(h_cnt);
     for (auto& e : ev)
@@ -169,6 +174,22 @@ struct fe2_hrom_s {
 namespace {
 
 void count_launch(fe2_hrom_t h, int k = 1) { h->stats.kernel_launches += k; }
+
+struct Eps3 {
+  double v[3];
+};
+// committed strain eps_q = E + G_q alpha_c of point p (host, readback only)
+Eps3 strain_at(fe2_hrom_t h, int64_t p, int q, const double* ac, const double* Ec) {
+  const int n = h->n, NP = h->NP;
+  const double* Gq = h->G.data() + static_cast<size_t>(q) * 3 * n;
+  Eps3 e;
+  for (int i = 0; i < 3; ++i) {
+    double s = 0.0;
+    for (int a = 0; a < n; ++a) s += Gq[i * n + a] * ac[p * NP + a];
+    e.v[i] = Ec[p * 3 + i] + s;
+  }
+  return e;
+}
 
 // One increment on device buffers (the engine's core loop).
 void run_increment(fe2_hrom_t h, const double* d_E, const fe2_newton_opts_t* opts, const Outputs& O,
@@ -331,9 +352,11 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
           for (int a = 0; a < n; ++a) G2[static_cast<size_t>(q2) * S + i * NP + a] = G[(static_cast<size_t>(q) * 3 + i) * n + a];
         w2[q2] = w[q];
       }
-      // elastic cubature points: σ = C_e (E + G α) is linear -> constants
-      std::vector<double> Kinc(static_cast<size_t>(NP) * NP, 0.0), KaEinc(static_cast<size_t>(NP) * 3, 0.0);
-      for (int q : h->el_idx) {
+      // elastic predictor over ALL cubature points (J2 points with the J2
+      // material's C_e): K_e = Σ w G^T C_e G, K_aE,e = Σ w G^T C_e, C_EE,e = Σ w C_e.
+      // The device adds only the plastic corrections ΔC_q of plastic points.
+      std::vector<double> Ke(static_cast<size_t>(NP) * NP, 0.0), KaEe(static_cast<size_t>(NP) * 3, 0.0);
+      for (int q = 0; q < K; ++q) {
         const MatDev& m = h->qmat[q];
         const double Ce[3][3] = {{m.lam + 2.0 * m.mu, m.lam, 0.0}, {m.lam, m.lam + 2.0 * m.mu, 0.0}, {0.0, 0.0, m.mu}};
         const double* Gq = G + static_cast<size_t>(q) * 3 * n;
@@ -342,32 +365,37 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
         for (int i = 0; i < 3; ++i)
           for (int j = 0; j < 3; ++j) {
             wC[i][j] = wq * Ce[i][j];
-            h->CEEinc[3 * i + j] += wC[i][j];
+            h->CEEe[3 * i + j] += wC[i][j];
           }
         for (int a = 0; a < n; ++a) {
           for (int j = 0; j < 3; ++j)
-            KaEinc[a * 3 + j] += Gq[a] * wC[0][j] + Gq[n + a] * wC[1][j] + Gq[2 * n + a] * wC[2][j];
+            KaEe[a * 3 + j] += Gq[a] * wC[0][j] + Gq[n + a] * wC[1][j] + Gq[2 * n + a] * wC[2][j];
           for (int b = 0; b < n; ++b) {
             double s = 0.0;
             for (int i = 0; i < 3; ++i)
               s += Gq[i * n + a] * (wC[i][0] * Gq[b] + wC[i][1] * Gq[n + b] + wC[i][2] * Gq[2 * n + b]);
-            Kinc[static_cast<size_t>(a) * NP + b] += s;
+            Ke[static_cast<size_t>(a) * NP + b] += s;
           }
         }
       }
+      for (int a = 0; a < n; ++a)  // exact symmetry
+        for (int b = 0; b < a; ++b) {
+          const double v = 0.5 * (Ke[static_cast<size_t>(a) * NP + b] + Ke[static_cast<size_t>(b) * NP + a]);
+          Ke[static_cast<size_t>(a) * NP + b] = Ke[static_cast<size_t>(b) * NP + a] = v;
+        }
       CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
       h->stream = h->own_stream;
       for (auto& e : h->ev) CK(cudaEventCreate(&e));
       h->G2 = dalloc<double>(G2.size());
       h->w2 = dalloc<double>(w2.size());
-      h->Kinc = dalloc<double>(Kinc.size());
-      h->KaEinc = dalloc<double>(KaEinc.size());
+      h->Ke = dalloc<double>(Ke.size());
+      h->KaEe = dalloc<double>(KaEe.size());
       h->cnt = dalloc<int>(2);
       CK(cudaMallocHost(&h->h_cnt, sizeof(int)));
       CK(cudaMemcpy(h->G2, G2.data(), G2.size() * sizeof(double), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(h->w2, w2.data(), w2.size() * sizeof(double), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(h->Kinc, Kinc.data(), Kinc.size() * sizeof(double), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(h->KaEinc, KaEinc.data(), KaEinc.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->Ke, Ke.data(), Ke.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->KaEe, KaEe.data(), KaEe.size() * sizeof(double), cudaMemcpyHostToDevice));
       h->stats.n = n;
       h->stats.K = K;
       h->stats.K_j2 = h->K2;
@@ -387,7 +415,7 @@ int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
     check(P < (int64_t(1) << 31), Code::config, "at most 2^31-1 points per device");
     CK(cudaSetDevice(h->device));
     h->free_points();
-    const size_t hist_n = static_cast<size_t>(P) * h->K2p * 6;
+    const size_t hist_n = static_cast<size_t>(P) * h->K2p * 5;
     h->hist = dalloc<double>(hist_n);
     const size_t an = static_cast<size_t>(P) * h->NP;
     h->alpha_c = dalloc<double>(an);
@@ -397,6 +425,8 @@ int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
     h->E_prev = dalloc<double>(P * 3);
     h->E_tgt = dalloc<double>(P * 3);
     h->E_ev = dalloc<double>(P * 3);
+    h->bp = dalloc<double>(an);
+    h->sp = dalloc<double>(P * 4);
     h->st = dalloc<PointState>(P);
     h->keep_flags = keep_flags != 0;
     if (h->keep_flags) h->flags = dalloc<uint8_t>(static_cast<size_t>(P) * h->K2p);
@@ -410,8 +440,9 @@ int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
     h->o_status = dalloc<int>(P);
     h->o_pc = dalloc<int>(P);
     CK(cudaMemsetAsync(h->hist, 0, hist_n * sizeof(double), h->stream));
-    for (double* p : {h->alpha_c, h->alpha, h->alpha_ev, h->dalpha})
+    for (double* p : {h->alpha_c, h->alpha, h->alpha_ev, h->dalpha, h->bp})
       CK(cudaMemsetAsync(p, 0, an * sizeof(double), h->stream));
+    CK(cudaMemsetAsync(h->sp, 0, P * 4 * sizeof(double), h->stream));
     for (double* p : {h->E_prev, h->E_tgt, h->E_ev}) CK(cudaMemsetAsync(p, 0, P * 3 * sizeof(double), h->stream));
     CK(cudaMemsetAsync(h->st, 0, P * sizeof(PointState), h->stream));
     if (h->flags) CK(cudaMemsetAsync(h->flags, 0, static_cast<size_t>(P) * h->K2p, h->stream));
@@ -427,9 +458,10 @@ int fe2_hrom_reset_points(fe2_hrom_t h) {
     CK(cudaSetDevice(h->device));
     const int64_t P = h->P;
     cudaStream_t s = h->stream;
-    CK(cudaMemsetAsync(h->hist, 0, static_cast<size_t>(P) * h->K2p * 6 * sizeof(double), s));
+    CK(cudaMemsetAsync(h->hist, 0, static_cast<size_t>(P) * h->K2p * 5 * sizeof(double), s));
     const size_t an = static_cast<size_t>(P) * h->NP * sizeof(double);
-    for (double* p : {h->alpha_c, h->alpha, h->alpha_ev, h->dalpha}) CK(cudaMemsetAsync(p, 0, an, s));
+    for (double* p : {h->alpha_c, h->alpha, h->alpha_ev, h->dalpha, h->bp}) CK(cudaMemsetAsync(p, 0, an, s));
+    CK(cudaMemsetAsync(h->sp, 0, P * 4 * sizeof(double), s));
     for (double* p : {h->E_prev, h->E_tgt, h->E_ev}) CK(cudaMemsetAsync(p, 0, P * 3 * sizeof(double), s));
     CK(cudaMemsetAsync(h->st, 0, P * sizeof(PointState), s));
     if (h->flags) CK(cudaMemsetAsync(h->flags, 0, static_cast<size_t>(P) * h->K2p, s));
@@ -496,16 +528,15 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
       for (int64_t p = 0; p < P; ++p)
         for (int a = 0; a < n; ++a) alpha[p * n + a] = ac[p * NP + a];
     if (state) {
-      std::vector<double> hs(static_cast<size_t>(P) * K2p * 6), Ec(static_cast<size_t>(P) * 3);
+      std::vector<double> hs(static_cast<size_t>(P) * K2p * 5), Ec(static_cast<size_t>(P) * 3);
       CK(cudaMemcpy(hs.data(), h->hist, hs.size() * sizeof(double), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(Ec.data(), h->E_ev, Ec.size() * sizeof(double), cudaMemcpyDeviceToHost));
       const size_t PK = static_cast<size_t>(P) * K2p;
       for (int64_t p = 0; p < P; ++p) {
-        for (int q2 = 0; q2 < h->K2; ++q2) {
-          double* s = state + (static_cast<size_t>(p) * K + h->j2_idx[q2]) * 6;
-          for (int c = 0; c < 6; ++c) s[c] = hs[c * PK + static_cast<size_t>(p) * K2p + q2];
-        }
-        for (int q : h->el_idx) {  // elastic: no history; sigma33 = lam (e11 + e22)
+        // sigma33 is write-only in the reference (materials.hpp:181, :193): it is
+        // not kept in HBM but recomputed here from the committed strain and eps_p,
+        // sigma33 = lam tr(eps - eps_p) + 2 mu (0 - eps_p,33) (tr Δeps_p = 0).
+        for (int q = 0; q < K; ++q) {
           const double* Gq = h->G.data() + static_cast<size_t>(q) * 3 * n;
           double e[3];
           for (int i = 0; i < 3; ++i) {
@@ -515,7 +546,15 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
           }
           double* s = state + (static_cast<size_t>(p) * K + q) * 6;
           for (int c = 0; c < 5; ++c) s[c] = 0.0;
-          s[5] = h->qmat[q].lam * (e[0] + e[1]);
+          const MatDev& m = h->qmat[q];
+          s[5] = m.lam * (e[0] + e[1]);
+        }
+        for (int q2 = 0; q2 < h->K2; ++q2) {
+          double* s = state + (static_cast<size_t>(p) * K + h->j2_idx[q2]) * 6;
+          for (int c = 0; c < 5; ++c) s[c] = hs[c * PK + static_cast<size_t>(p) * K2p + q2];
+          const MatDev& m = h->mat2;
+          const Eps3 e = strain_at(h, p, h->j2_idx[q2], ac.data(), Ec.data());
+          s[5] = m.lam * ((e.v[0] - s[0]) + (e.v[1] - s[1]) + (0.0 - s[2])) + 2.0 * m.mu * (0.0 - s[2]);
         }
       }
     }

@@ -1,25 +1,32 @@
 // B200 (sm_100a) kernels of the hyper-ROM engine.
 //
-//  K2+K3  k_newton_round  — one warp per macro point. The J2 cubature rows
-//         G_q (3 x NP) stream through shared memory in 32-point chunks by
-//         TMA bulk copies (cp.async.bulk + mbarrier, double buffered) and are
-//         shared by the W points of the CTA. Per chunk each lane runs the
-//         constitutive update of one cubature point (HBM history stream,
-//         prefetched one chunk ahead), then the warp contracts
-//           K_aa += Σ_q G_q^T (w C_q) G_q        on FP64 tensor cores
-//                                                 (mma.sync m8n8k4 f64 = DMMA)
-//           K_aE += Σ_q G_q^T (w C_q),  r += Σ_q G_q^T (w σ_q)   (DFMA)
-//         over the flattened (q, strain-row) index in k-steps of 4. The
-//         elastic-inclusion cubature points are linear, so their part is a
-//         precomputed constant (K_inc, K_aE_inc, C_EE_inc) added once. The
-//         same warp then runs the reduced Newton / line-search state machine
-//         of micro_newton (rve.hpp:285-346): Cholesky of K_aa in shared memory
-//         with warp shuffles, the step, the Armijo test, and at convergence
-//         the static condensation C = (C_EE - K_Ea K_aa^-1 K_aE)/V
-//         (homogenize, rve.hpp:350-392) — K_aa never touches HBM.
-//  K1     k_commit        — recomputes the constitutive update at the
-//         converged (E, α) and writes the history (commit-after-acceptance,
-//         rve.hpp:283-284, :480): a coalesced SoA stream, HBM bound.
+// Decomposition used on the device (exact algebra):
+//   σ_q = C_e ε_q − S(εp_q) + Δσ_q ,  C_q = C_e + ΔC_q ,  ε_q = E + G_q α
+// where Δσ_q, ΔC_q are the radial-return corrections (zero at elastic
+// points). Summed with the cubature weights:
+//   r    = K_e α + K_aE,e E − b_p + Σ_plastic w G_q^T Δσ_q
+//   K_aa = K_e + Σ_plastic w G_q^T ΔC_q G_q
+//   K_aE = K_aE,e + Σ_plastic w G_q^T ΔC_q ,   C_EE = C_EE,e + Σ_plastic w ΔC_q
+//   Σraw = K_aE,e^T α + C_EE,e E − s_p + Σ_plastic w Δσ_q
+// with K_e, K_aE,e, C_EE,e constant over the model (host, once) and
+// b_p = Σ w G^T S(εp), s_p = Σ w S(εp) constant over an increment (kept
+// per point, updated by the commit kernel from the plastic increments only).
+//
+//  K2+K3  k_newton_round — one warp per macro point; the J2 cubature rows G_q
+//         stream through shared memory in 32-point chunks (TMA bulk copies,
+//         mbarrier double buffering) shared by the CTA's points. Per chunk:
+//         lane = cubature point: ε_q, elastic trial and yield test from the
+//         HBM history (prefetched a chunk ahead); plastic points are
+//         compacted (ballot/popc) and only they are contracted on the FP64
+//         tensor cores (mma.sync m8n8k4 f64 = DMMA) over the flattened
+//         (point, strain-row) index. The warp then runs the reduced Newton /
+//         line-search state machine of micro_newton (rve.hpp:285-346):
+//         Cholesky of K_aa in shared memory, step, Armijo test, and at
+//         convergence the static condensation C = (C_EE − K_Ea K_aa^-1 K_aE)/V
+//         (homogenize, rve.hpp:350-392). K_aa never touches HBM.
+//  K1     k_commit — recomputes the update at the converged (E, α), writes the
+//         history SoA stream (commit-after-acceptance, rve.hpp:283-284, :480)
+//         and folds the plastic-strain increments into b_p, s_p.
 #include <cstdio>
 
 #include "hrom_kernels.cuh"
@@ -93,6 +100,8 @@ __device__ __forceinline__ double lerp_rn(double e0, double e1, double t) {
   return __dadd_rn(e0, __dmul_rn(__dsub_rn(e1, e0), t));
 }
 
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
+
 // Cholesky of the lower triangle of sK (row stride ld) in place; lane i owns
 // row i (n <= 32). Returns false if K is not positive definite.
 __device__ bool warp_cholesky(double* sK, int ld, int n, int lane) {
@@ -101,9 +110,10 @@ __device__ bool warp_cholesky(double* sK, int ld, int n, int lane) {
     const double d = sK[j * ld + j];
     if (!(d > 0.0)) return false;
     const double ljj = sqrt(d);
+    const double inv = 1.0 / ljj;
     __syncwarp();
     if (lane == j) sK[j * ld + j] = ljj;
-    if (lane > j && lane < n) sK[lane * ld + j] = sK[lane * ld + j] / ljj;
+    if (lane > j && lane < n) sK[lane * ld + j] *= inv;
     __syncwarp();
     if (lane > j && lane < n) {
       const double lij = sK[lane * ld + j];
@@ -130,47 +140,142 @@ __device__ double warp_chol_solve(const double* sK, int ld, int n, int lane, dou
   return x;
 }
 
+// Elastic trial state of update4 (materials.hpp:162-169) and the yield test
+// (:208-210); the plastic branch returns the radial-return corrections
+// Δσ = σ − σ_tr (condensed) and ΔC = C − C_e (6 unique).
+struct Trial {
+  double t0, t1, t2, t3;  // trial stress (packed 4)
+  double d0, d1, d2, d3;  // trial deviator
+  double ss, q_tr, f;
+};
+
+__device__ __forceinline__ Trial trial_state(const MatDev& m, double ep0, double ep1, double ep2, double ep3,
+                                             double eq, double e11, double e22, double g12) {
+  Trial T;
+  const double two_mu = 2.0 * m.mu;
+  const double x0 = e11 - ep0, x1 = e22 - ep1, x2 = 0.0 - ep2, x3 = 0.5 * g12 - ep3;
+  const double lt = m.lam * (x0 + x1 + x2);
+  T.t0 = lt + two_mu * x0;
+  T.t1 = lt + two_mu * x1;
+  T.t2 = lt + two_mu * x2;
+  T.t3 = two_mu * x3;
+  const double p = (T.t0 + T.t1 + T.t2) / 3.0;
+  T.d0 = T.t0 - p;
+  T.d1 = T.t1 - p;
+  T.d2 = T.t2 - p;
+  T.d3 = T.t3;
+  T.ss = T.d0 * T.d0 + T.d1 * T.d1 + T.d2 * T.d2 + 2.0 * T.d3 * T.d3;
+  T.q_tr = sqrt(1.5) * sqrt(T.ss);
+  T.f = T.q_tr - (m.sy0 + m.h * eq);
+  return T;
+}
+
+struct Corr {
+  double dc00, dc01, dc02, dc11, dc12, dc22;  // ΔC
+  double ds0, ds1, ds2;                       // Δσ (11, 22, 12)
+};
+
+__device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
+  Corr c;
+  const double mu = m.mu;
+  const double denom = 3.0 * mu + m.h;
+  const double dlam = T.f / denom;
+  const double inv_q = 1.0 / T.q_tr;
+  const double cs = 3.0 * mu * dlam * inv_q;
+  c.ds0 = -cs * T.d0;
+  c.ds1 = -cs * T.d1;
+  c.ds2 = -cs * T.d3;
+  const double inv_n = 1.0 / sqrt(T.ss);
+  const double n0 = T.d0 * inv_n, n1 = T.d1 * inv_n, n3 = T.d3 * inv_n;
+  const double mu2 = 6.0 * mu * mu;
+  const double c1 = mu2 * dlam * inv_q;
+  const double c2 = mu2 * (1.0 / denom - dlam * inv_q);
+  c.dc00 = -c1 * (2.0 / 3.0) - c2 * (n0 * n0);
+  c.dc01 = c1 * (1.0 / 3.0) - c2 * (n0 * n1);
+  c.dc02 = -c2 * (n0 * n3);
+  c.dc11 = -c1 * (2.0 / 3.0) - c2 * (n1 * n1);
+  c.dc12 = -c2 * (n1 * n3);
+  c.dc22 = -0.5 * c1 - c2 * (n3 * n3);
+  return c;
+}
+
 constexpr int kW = 8;  // warps (= macro points) per CTA in the round kernel
 
 template <int NP>
 struct RoundLayout {
   static constexpr int S = 3 * NP + 1;
-  static constexpr int kUnion = (kQC * 12 > NP * (NP + 1)) ? kQC * 12 : NP * (NP + 1);
+  static constexpr int kSlots = kQC * 9 + kQC * 3 + kQC;  // ΔC rows, Δσ, point index (as doubles)
+  static constexpr int kUnion = (kSlots > NP * (NP + 1)) ? kSlots : NP * (NP + 1);
   static constexpr int WS = NP /*alpha_ev*/ + NP /*r*/ + 3 * NP /*KaE*/ + kUnion;
   static constexpr size_t gbuf = static_cast<size_t>(kQC) * S;
   static constexpr size_t bytes = (2 * gbuf + static_cast<size_t>(kW) * WS) * sizeof(double) + 16;
 };
 
-// Recompute the constitutive update at (E, α) for all J2 cubature points of
-// point p and write its history (one warp). Used for bisected sub-steps.
+// Commit one point's history at (E, α) from global G (one warp; used for the
+// converged sub-steps of bisected increments), folding the plastic-strain
+// increments into b_p, s_p.
 template <int NP>
 __device__ void warp_commit_point(const ModelDev& M, const PointsDev& D, int64_t p, const double* sAl, double E0,
                                   double E1, double E2, int lane) {
   constexpr int S = 3 * NP + 1;
   const int64_t PK = D.P * static_cast<int64_t>(M.K2p);
   double* H = D.hist + p * M.K2p;
-  for (int q = lane; q < M.K2; q += 32) {
-    const double* Gq = M.G2 + static_cast<size_t>(q) * S;
-    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-    for (int a = 0; a < NP; ++a) {
-      const double al = sAl[a];
-      e0 += Gq[a] * al;
-      e1 += Gq[NP + a] * al;
-      e2 += Gq[2 * NP + a] * al;
+  const MatDev& m = M.mat2;
+  double bacc = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int q0 = 0; q0 < M.K2; q0 += 32) {
+    const int q = q0 + lane;
+    double w0 = 0.0, w1 = 0.0, w2v = 0.0;
+    if (q < M.K2) {
+      const double* Gq = M.G2 + static_cast<size_t>(q) * S;
+      double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+      for (int a = 0; a < NP; ++a) {
+        const double al = sAl[a];
+        e0 += Gq[a] * al;
+        e1 += Gq[NP + a] * al;
+        e2 += Gq[2 * NP + a] * al;
+      }
+      const MatOut o = update_material(m, H[q], H[PK + q], H[2 * PK + q], H[3 * PK + q], H[4 * PK + q],
+                                       E0 + e0, E1 + e1, E2 + e2);
+      const double x0 = o.ep0 - H[q], x1 = o.ep1 - H[PK + q], x2 = o.ep2 - H[2 * PK + q],
+                   x3 = o.ep3 - H[3 * PK + q];
+      const double lt = m.lam * (x0 + x1 + x2), wq = M.w2[q];
+      w0 = wq * (lt + 2.0 * m.mu * x0);
+      w1 = wq * (lt + 2.0 * m.mu * x1);
+      w2v = wq * (2.0 * m.mu * x3);
+      if (o.plastic) {
+        H[q] = o.ep0;
+        H[PK + q] = o.ep1;
+        H[2 * PK + q] = o.ep2;
+        H[3 * PK + q] = o.ep3;
+        H[4 * PK + q] = o.eq;
+      }
     }
-    const MatOut o = update_material(M.mat2, H[q], H[PK + q], H[2 * PK + q], H[3 * PK + q],
-                                     H[4 * PK + q], E0 + e0, E1 + e1, E2 + e2);
-    H[q] = o.ep0;
-    H[PK + q] = o.ep1;
-    H[2 * PK + q] = o.ep2;
-    H[3 * PK + q] = o.ep3;
-    H[4 * PK + q] = o.eq;
-    H[5 * PK + q] = o.s33;
+    s0 += w0;
+    s1 += w1;
+    s2 += w2v;
+    for (int l = 0; l < 32; ++l) {
+      const double a0 = __shfl_sync(0xffffffffu, w0, l), a1 = __shfl_sync(0xffffffffu, w1, l),
+                   a2 = __shfl_sync(0xffffffffu, w2v, l);
+      const int ql = q0 + l;
+      if (ql < M.K2 && lane < NP) {
+        const double* Gq = M.G2 + static_cast<size_t>(ql) * S;
+        bacc += Gq[lane] * a0 + Gq[NP + lane] * a1 + Gq[2 * NP + lane] * a2;
+      }
+    }
+  }
+  if (lane < NP) D.bp[p * NP + lane] += bacc;
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    D.sp[p * 4 + 0] += s0;
+    D.sp[p * 4 + 1] += s1;
+    D.sp[p * 4 + 2] += s2;
   }
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
+__global__ void __launch_bounds__(kW * 32, 2) k_newton_round(RoundArgs A) {
   constexpr int NP = 8 * NT;
   constexpr int NTP = NT * (NT + 1) / 2;
   using L = RoundLayout<NP>;
@@ -185,13 +290,15 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
   double* sV = sA + NP;      // residual r
   double* sKaE = sV + NP;    // K_aE [NP][3]
   double* sU = sKaE + 3 * NP;
-  double* sWC = sU;             // w C_q rows  [32][9]   (material phase)
-  double* sWS = sU + kQC * 9;   // w σ_q       [32][3]
-  double* sK = sU;              // K_aa lower  [NP][NP+1] (after the chunk loop)
+  double* sDC = sU;                                   // [32][9] w ΔC rows of the plastic slots
+  double* sDS = sU + kQC * 9;                         // [32][3] w Δσ
+  int* sQ = reinterpret_cast<int*>(sU + kQC * 12);    // [32]    chunk-local cubature index
+  double* sK = sU;                                    // K_aa lower [NP][NP+1] (after the chunk loop)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(Gbuf1 + L::gbuf + static_cast<size_t>(kW) * L::WS);
 
   const ModelDev& M = A.M;
   const PointsDev& D = A.D;
+  const MatDev& mt = M.mat2;
   const int nch = M.nchunks;
   constexpr uint32_t kChunkBytes = kQC * S * sizeof(double);
 
@@ -230,9 +337,8 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
     rr[t] = 0.0;
     kae[t][0] = kae[t][1] = kae[t][2] = 0.0;
   }
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  double ce00 = 0.0, ce01 = 0.0, ce02 = 0.0, ce11 = 0.0, ce12 = 0.0, ce22 = 0.0;
-  int pc = 0;
+  // lane-partial plastic corrections of C_EE and Σraw
+  double c00 = 0.0, c01 = 0.0, c02 = 0.0, c11 = 0.0, c12 = 0.0, c22 = 0.0, ds0 = 0.0, ds1 = 0.0, ds2 = 0.0;
 
   const int64_t PK = D.P * static_cast<int64_t>(M.K2p);
   const double* H0 = D.hist + p * M.K2p;
@@ -258,45 +364,58 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
     mbar_wait(&mbar[buf], (c >> 1) & 1);
     if (valid) {
       const int q = c * kQC + lane;
-      // ---- material phase: lane = cubature point
-      {
-        const double* Gq = Gb + lane * S;
-        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+      // ---- lane = cubature point: strain, elastic trial, yield test
+      const double* Gq = Gb + lane * S;
+      double e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll 8
-        for (int a = 0; a < NP; ++a) {
-          const double al = sA[a];
-          e0 += Gq[a] * al;
-          e1 += Gq[NP + a] * al;
-          e2 += Gq[2 * NP + a] * al;
-        }
-        const MatOut o = update_material(M.mat2, h0, h1, h2, h3, h4, E0 + e0, E1 + e1, E2 + e2);
+      for (int a = 0; a < NP; ++a) {
+        const double al = sA[a];
+        e0 += Gq[a] * al;
+        e1 += Gq[NP + a] * al;
+        e2 += Gq[2 * NP + a] * al;
+      }
+      const Trial T = trial_state(mt, h0, h1, h2, h3, h4, E0 + e0, E1 + e1, E2 + e2);
+      const bool plastic = (T.f > 0.0) && (q < M.K2);
+      const unsigned bal = __ballot_sync(0xffffffffu, plastic);
+      const int np = __popc(bal);
+      if (plastic) {
+        const Corr cr = radial_return(mt, T);
         const double wq = M.w2[q];
-        double* wc = sWC + lane * 9;
-        const double w00 = wq * o.c00, w01 = wq * o.c01, w02 = wq * o.c02;
-        const double w11 = wq * o.c11, w12 = wq * o.c12, w22 = wq * o.c22;
-        wc[0] = w00;
-        wc[1] = w01;
-        wc[2] = w02;
-        wc[3] = w01;
-        wc[4] = w11;
-        wc[5] = w12;
-        wc[6] = w02;
-        wc[7] = w12;
-        wc[8] = w22;
-        const double f0 = wq * o.s0, f1 = wq * o.s1, f2 = wq * o.s2;
-        sWS[lane * 3 + 0] = f0;
-        sWS[lane * 3 + 1] = f1;
-        sWS[lane * 3 + 2] = f2;
-        s0 += f0;
-        s1 += f1;
-        s2 += f2;
-        ce00 += w00;
-        ce01 += w01;
-        ce02 += w02;
-        ce11 += w11;
-        ce12 += w12;
-        ce22 += w22;
-        pc += (o.plastic && q < M.K2) ? 1 : 0;
+        const int slot = __popc(bal & ((1u << lane) - 1u));
+        const double w00 = wq * cr.dc00, w01 = wq * cr.dc01, w02 = wq * cr.dc02;
+        const double w11 = wq * cr.dc11, w12 = wq * cr.dc12, w22 = wq * cr.dc22;
+        double* dc = sDC + slot * 9;
+        dc[0] = w00;
+        dc[1] = w01;
+        dc[2] = w02;
+        dc[3] = w01;
+        dc[4] = w11;
+        dc[5] = w12;
+        dc[6] = w02;
+        dc[7] = w12;
+        dc[8] = w22;
+        const double f0 = wq * cr.ds0, f1 = wq * cr.ds1, f2 = wq * cr.ds2;
+        sDS[slot * 3 + 0] = f0;
+        sDS[slot * 3 + 1] = f1;
+        sDS[slot * 3 + 2] = f2;
+        sQ[slot] = lane;
+        c00 += w00;
+        c01 += w01;
+        c02 += w02;
+        c11 += w11;
+        c12 += w12;
+        c22 += w22;
+        ds0 += f0;
+        ds1 += f1;
+        ds2 += f2;
+      }
+      // zero the slots that round the plastic count up to a multiple of 4
+      const int np4 = (np + 3) & ~3;
+      if (lane >= np && lane < np4) {
+#pragma unroll
+        for (int e = 0; e < 9; ++e) sDC[lane * 9 + e] = 0.0;
+        sDS[lane * 3 + 0] = sDS[lane * 3 + 1] = sDS[lane * 3 + 2] = 0.0;
+        sQ[lane] = 0;
       }
       if (c + 1 < nch) {  // prefetch the next chunk's history
         const int qn = q + kQC;
@@ -307,23 +426,24 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
         h4 = H0[4 * PK + qn];
       }
       __syncwarp();
-      // ---- contraction phase: k = 3 q_local + i, four k per DMMA k-step
+      // ---- plastic contraction on DMMA: k = 3 slot + i, four k per k-step
+      const int ng = np4 >> 2;
 #pragma unroll 1
-      for (int c3 = 0; c3 < (kQC * 3) / 12; ++c3) {
+      for (int g = 0; g < ng; ++g) {
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
-          const int ql = 4 * c3 + qo[s];
+          const int slot = 4 * g + qo[s];
           const int i = io[s];
-          const double* wc = sWC + ql * 9 + i * 3;
-          const double c0 = wc[0], c1 = wc[1], c2 = wc[2];
-          const double ws = sWS[ql * 3 + i];
-          const double* g = Gb + ql * S + col;
+          const double* wc = sDC + slot * 9 + i * 3;
+          const double k0 = wc[0], k1 = wc[1], k2 = wc[2];
+          const double ws = sDS[slot * 3 + i];
+          const double* gp = Gb + sQ[slot] * S + col;
           double Af[NT], Bf[NT];
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
-            const double g0 = g[t * 8], g1 = g[NP + t * 8], g2 = g[2 * NP + t * 8];
+            const double g0 = gp[t * 8], g1 = gp[NP + t * 8], g2 = gp[2 * NP + t * 8];
             Af[t] = (i == 0) ? g0 : ((i == 1) ? g1 : g2);
-            Bf[t] = c0 * g0 + c1 * g1 + c2 * g2;
+            Bf[t] = k0 * g0 + k1 * g1 + k2 * g2;
             kae[t][s] += Bf[t];
             rr[t] += ws * Af[t];
           }
@@ -348,7 +468,7 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
   }
   if (!valid) return;
 
-  // ---- reductions: r and K_aE over the four k-lanes of each column
+  // ---- reductions: r and K_aE corrections over the four k-lanes of each column
   const int n = M.n;
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
@@ -372,7 +492,8 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
       sKaE[a * 3 + 2] = ki[2];
     }
   }
-  // K tiles -> lower triangle of sK
+  __syncwarp();
+  // K_aa corrections -> lower triangle of sK (slots are dead now)
   {
     const int r_ = lane >> 2, c_ = 2 * (lane & 3);
     int ti = 0;
@@ -391,47 +512,46 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
         ++ti;
       }
   }
-  s0 = warp_sum(s0);
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
-  ce00 = warp_sum(ce00);
-  ce01 = warp_sum(ce01);
-  ce02 = warp_sum(ce02);
-  ce11 = warp_sum(ce11);
-  ce12 = warp_sum(ce12);
-  ce22 = warp_sum(ce22);
-  pc = warp_sum_i(pc);
+  c00 = warp_sum(c00);
+  c01 = warp_sum(c01);
+  c02 = warp_sum(c02);
+  c11 = warp_sum(c11);
+  c12 = warp_sum(c12);
+  c22 = warp_sum(c22);
+  ds0 = warp_sum(ds0);
+  ds1 = warp_sum(ds1);
+  ds2 = warp_sum(ds2);
   __syncwarp();
-  // ---- constant elastic-inclusion part: σ_q = C_e (E + G_q α) is linear
+  // ---- elastic predictor part (constant K_e, K_aE,e, C_EE,e) and b_p, s_p
   double sa0 = 0.0, sa1 = 0.0, sa2 = 0.0;
-  for (int a = lane; a < n; a += 32) {
-    const double* kr = M.Kinc + a * NP;
+  if (lane < n) {
+    const int a = lane;
+    const double* ke = M.KaEe + a * 3;
     double s = 0.0;
-    for (int b = 0; b < n; ++b) s += kr[b] * sA[b];
-    const double* ke = M.KaEinc + a * 3;
+    for (int b = 0; b < n; ++b) {
+      const double kab = M.Ke[b * NP + a];  // K_e symmetric: coalesced column read
+      s += kab * sA[b];
+      if (b <= a) sK[a * LD + b] += kab;
+    }
     s += ke[0] * E0 + ke[1] * E1 + ke[2] * E2;
-    sV[a] += s;
-    for (int b = 0; b <= a; ++b) sK[a * LD + b] += kr[b];
+    sV[a] += s - D.bp[p * NP + a];
     sKaE[a * 3 + 0] += ke[0];
     sKaE[a * 3 + 1] += ke[1];
     sKaE[a * 3 + 2] += ke[2];
-    sa0 += ke[0] * sA[a];
-    sa1 += ke[1] * sA[a];
-    sa2 += ke[2] * sA[a];
+    sa0 = ke[0] * sA[a];
+    sa1 = ke[1] * sA[a];
+    sa2 = ke[2] * sA[a];
   }
   sa0 = warp_sum(sa0);
   sa1 = warp_sum(sa1);
   sa2 = warp_sum(sa2);
-  const double* ci = M.CEEinc;
-  s0 += sa0 + (ci[0] * E0 + ci[1] * E1 + ci[2] * E2);
-  s1 += sa1 + (ci[3] * E0 + ci[4] * E1 + ci[5] * E2);
-  s2 += sa2 + (ci[6] * E0 + ci[7] * E1 + ci[8] * E2);
-  ce00 += ci[0];
-  ce01 += ci[1];
-  ce02 += ci[2];
-  ce11 += ci[4];
-  ce12 += ci[5];
-  ce22 += ci[8];
+  const double* ce = M.CEEe;
+  const double* spp = D.sp + p * 4;
+  const double s0 = ds0 + sa0 + (ce[0] * E0 + ce[1] * E1 + ce[2] * E2) - spp[0];
+  const double s1 = ds1 + sa1 + (ce[3] * E0 + ce[4] * E1 + ce[5] * E2) - spp[1];
+  const double s2 = ds2 + sa2 + (ce[6] * E0 + ce[7] * E1 + ce[8] * E2) - spp[2];
+  const double ce00 = ce[0] + c00, ce01 = ce[1] + c01, ce02 = ce[2] + c02;
+  const double ce11 = ce[4] + c11, ce12 = ce[5] + c12, ce22 = ce[8] + c22;
   __syncwarp();
 
   if (A.dbg) {  // assembly dump for parity tests (r, K full, KaE, C_EE, S_raw)
@@ -477,8 +597,8 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
       A.O.status[p] = code;
       A.O.iters[p] = st.iters;
       A.O.res[p] = rn;
-      for (int i = 0; i < 3; ++i) A.O.sigma[p * 3 + i] = __longlong_as_double(0x7ff8000000000000ll);
-      for (int i = 0; i < 9; ++i) A.O.C[p * 9 + i] = __longlong_as_double(0x7ff8000000000000ll);
+      for (int i = 0; i < 3; ++i) A.O.sigma[p * 3 + i] = qnan();
+      for (int i = 0; i < 9; ++i) A.O.C[p * 9 + i] = qnan();
     }
   };
   constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
@@ -623,80 +743,168 @@ __global__ void __launch_bounds__(kW * 32, 1) k_newton_round(RoundArgs A) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: history commit at the converged (E, α) of every finished point.
-constexpr int kCommitWarps = 8;
-constexpr int kCommitPPW = 4;  // points per warp
+// K1: history commit at the converged (E, α) of every finished point, plus
+// the b_p, s_p update from the plastic-strain increments. HBM stream: read
+// εp(4), eq; write εp(4), eq — 80 B per J2 cubature point (σ33 is write-only
+// in the reference, materials.hpp:181/:193, and is recomputed on readback).
+// G chunks arrive by TMA bulk copies (double buffered); each warp owns kCPPW
+// points and prefetches their next-chunk history while it computes.
+constexpr int kCW = 8;    // warps per commit CTA
+constexpr int kCPPW = 2;  // points per warp
 
 template <int NP>
-__global__ void __launch_bounds__(kCommitWarps * 32) k_commit(ModelDev M, PointsDev D, Outputs O) {
-  constexpr int S = 3 * NP + 1;
-  constexpr int TS = kQC + 1;  // transposed row stride
+struct CommitLayout {
+  static constexpr int S = 3 * NP + 1;
+  static constexpr size_t gbuf = static_cast<size_t>(kQC) * S;
+  static constexpr size_t bytes = (2 * gbuf + static_cast<size_t>(kCW) * (kCPPW * NP + kQC * 3)) * sizeof(double) + 16;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(kCW * 32, 2) k_commit(ModelDev M, PointsDev D, Outputs O) {
+  using L = CommitLayout<NP>;
+  constexpr int S = L::S;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sG = reinterpret_cast<double*>(smem_raw);              // [3*NP][TS]
-  double* sAl = sG + 3 * NP * TS;                                 // [warps][PPW][NP]
+  double* Gbuf0 = reinterpret_cast<double*>(smem_raw);
+  double* Gbuf1 = Gbuf0 + L::gbuf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p_base = (static_cast<int64_t>(blockIdx.x) * kCommitWarps + warp) * kCommitPPW;
+  double* sAl = Gbuf1 + L::gbuf + static_cast<size_t>(warp) * (kCPPW * NP + kQC * 3);  // [kCPPW][NP]
+  double* sWw = sAl + kCPPW * NP;                                                        // [32][3]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(Gbuf1 + L::gbuf + static_cast<size_t>(kCW) * (kCPPW * NP + kQC * 3));
+  const int nch = M.nchunks;
+  constexpr uint32_t kChunkBytes = kQC * S * sizeof(double);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < 2 && c < nch; ++c) {
+      mbar_expect_tx(&mbar[c], kChunkBytes);
+      tma_load_1d(c ? Gbuf1 : Gbuf0, M.G2 + static_cast<size_t>(c) * kQC * S, kChunkBytes, &mbar[c]);
+    }
+  }
+  const int64_t p_base = (static_cast<int64_t>(blockIdx.x) * kCW + warp) * kCPPW;
   const int64_t PK = D.P * static_cast<int64_t>(M.K2p);
-  bool live[kCommitPPW];
-  double Ep[kCommitPPW][3];
-  int pc[kCommitPPW];
+  const MatDev& mt = M.mat2;
+  bool live[kCPPW];
+  double Ep[kCPPW][3], hv[kCPPW][5], bacc[kCPPW], sacc[kCPPW][3];
+  int pc[kCPPW];
 #pragma unroll
-  for (int k = 0; k < kCommitPPW; ++k) {
+  for (int k = 0; k < kCPPW; ++k) {
     const int64_t p = p_base + k;
     live[k] = p < D.P && D.st[p].phase == kDone;
     pc[k] = 0;
+    bacc[k] = 0.0;
+    sacc[k][0] = sacc[k][1] = sacc[k][2] = 0.0;
     Ep[k][0] = Ep[k][1] = Ep[k][2] = 0.0;
+    hv[k][0] = hv[k][1] = hv[k][2] = hv[k][3] = hv[k][4] = 0.0;
     if (live[k]) {
       Ep[k][0] = D.E_ev[p * 3 + 0];
       Ep[k][1] = D.E_ev[p * 3 + 1];
       Ep[k][2] = D.E_ev[p * 3 + 2];
-      for (int a = lane; a < NP; a += 32) sAl[(warp * kCommitPPW + k) * NP + a] = D.alpha_ev[p * NP + a];
+      for (int a = lane; a < NP; a += 32) sAl[k * NP + a] = D.alpha_ev[p * NP + a];
+      const double* H = D.hist + p * M.K2p + lane;
+      hv[k][0] = H[0];
+      hv[k][1] = H[PK];
+      hv[k][2] = H[2 * PK];
+      hv[k][3] = H[3 * PK];
+      hv[k][4] = H[4 * PK];
     }
   }
-  for (int c = 0; c < M.nchunks; ++c) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kQC * 3 * NP; e += blockDim.x) {
-      const int ql = e / (3 * NP), j = e - ql * (3 * NP);
-      sG[j * TS + ql] = M.G2[static_cast<size_t>(c * kQC + ql) * S + j];
-    }
-    __syncthreads();
+  __syncwarp();
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    const double* Gb = buf ? Gbuf1 : Gbuf0;
+    mbar_wait(&mbar[buf], (c >> 1) & 1);
     const int q = c * kQC + lane;
     const bool real = q < M.K2;
-    const MatDev mt = M.mat2;
+    const double wq = M.w2[q];
+    const double* Gq = Gb + lane * S;
 #pragma unroll
-    for (int k = 0; k < kCommitPPW; ++k) {
+    for (int k = 0; k < kCPPW; ++k) {
       if (!live[k]) continue;
       const int64_t p = p_base + k;
-      const double* a = sAl + (warp * kCommitPPW + k) * NP;
+      const double* a = sAl + k * NP;
       double e0 = 0.0, e1 = 0.0, e2 = 0.0;
 #pragma unroll 8
       for (int j = 0; j < NP; ++j) {
         const double al = a[j];
-        e0 += sG[j * TS + lane] * al;
-        e1 += sG[(NP + j) * TS + lane] * al;
-        e2 += sG[(2 * NP + j) * TS + lane] * al;
+        e0 += Gq[j] * al;
+        e1 += Gq[NP + j] * al;
+        e2 += Gq[2 * NP + j] * al;
+      }
+      const MatOut o = update_material(mt, hv[k][0], hv[k][1], hv[k][2], hv[k][3], hv[k][4], Ep[k][0] + e0,
+                                       Ep[k][1] + e1, Ep[k][2] + e2);
+      const bool pl = real && o.plastic;
+      double w0 = 0.0, w1 = 0.0, w2 = 0.0;  // w S(Δεp): change of the plastic-strain load
+      if (pl) {
+        const double x0 = o.ep0 - hv[k][0], x1 = o.ep1 - hv[k][1], x2 = o.ep2 - hv[k][2], x3 = o.ep3 - hv[k][3];
+        const double lt = mt.lam * (x0 + x1 + x2);
+        w0 = wq * (lt + 2.0 * mt.mu * x0);
+        w1 = wq * (lt + 2.0 * mt.mu * x1);
+        w2 = wq * (2.0 * mt.mu * x3);
       }
       double* H = D.hist + p * M.K2p + q;
-      const MatOut o = update_material(mt, H[0], H[PK], H[2 * PK], H[3 * PK], H[4 * PK], Ep[k][0] + e0,
-                                       Ep[k][1] + e1, Ep[k][2] + e2);
-      if (real) {
+      if (c + 1 < nch) {  // prefetch this point's next chunk
+        hv[k][0] = H[kQC];
+        hv[k][1] = H[PK + kQC];
+        hv[k][2] = H[2 * PK + kQC];
+        hv[k][3] = H[3 * PK + kQC];
+        hv[k][4] = H[4 * PK + kQC];
+      }
+      if (pl) {  // elastic points keep their history bit for bit
         H[0] = o.ep0;
         H[PK] = o.ep1;
         H[2 * PK] = o.ep2;
         H[3 * PK] = o.ep3;
         H[4 * PK] = o.eq;
-        H[5 * PK] = o.s33;
-        if (D.flags) D.flags[p * M.K2p + q] = o.plastic ? 1 : 0;
       }
-      pc[k] += __popc(__ballot_sync(0xffffffffu, real && o.plastic));
+      if (D.flags && real) D.flags[p * M.K2p + q] = o.plastic ? 1 : 0;
+      sacc[k][0] += w0;
+      sacc[k][1] += w1;
+      sacc[k][2] += w2;
+      const unsigned bal = __ballot_sync(0xffffffffu, pl);
+      pc[k] += __popc(bal);
+      if (bal) {  // b_p[a] += Σ_plastic q  G_q[:, a] . w S(Δεp_q)   (lane = mode a)
+        sWw[lane * 3 + 0] = w0;
+        sWw[lane * 3 + 1] = w1;
+        sWw[lane * 3 + 2] = w2;
+        __syncwarp();
+        if (lane < NP) {
+          unsigned bits = bal;
+          double b = 0.0;
+          while (bits) {
+            const int l = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const double* gl = Gb + l * S + lane;
+            b += gl[0] * sWw[l * 3 + 0] + gl[NP] * sWw[l * 3 + 1] + gl[2 * NP] * sWw[l * 3 + 2];
+          }
+          bacc[k] += b;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && c + 2 < nch) {
+      fence_proxy_async();
+      mbar_expect_tx(&mbar[buf], kChunkBytes);
+      tma_load_1d(buf ? Gbuf1 : Gbuf0, M.G2 + static_cast<size_t>(c + 2) * kQC * S, kChunkBytes, &mbar[buf]);
     }
   }
 #pragma unroll
-  for (int k = 0; k < kCommitPPW; ++k) {
+  for (int k = 0; k < kCPPW; ++k) {
     const int64_t p = p_base + k;
     if (!live[k]) continue;
     if (lane == 0 && O.pcount) O.pcount[p] = pc[k];
     for (int a = lane; a < NP; a += 32) D.alpha_c[p * NP + a] = D.alpha_ev[p * NP + a];
+    if (lane < NP) D.bp[p * NP + lane] += bacc[k];
+    const double t0 = warp_sum(sacc[k][0]), t1 = warp_sum(sacc[k][1]), t2 = warp_sum(sacc[k][2]);
+    if (lane == 0) {
+      D.sp[p * 4 + 0] += t0;
+      D.sp[p * 4 + 1] += t1;
+      D.sp[p * 4 + 2] += t2;
+    }
   }
 }
 
@@ -715,9 +923,9 @@ __global__ void k_begin_increment(PointsDev D, Outputs O, const double* dE, int*
   if (st.phase == kFailed) {  // a point whose trajectory already failed stays failed
     O.status[p] = st.err;
     O.iters[p] = 0;
-    O.res[p] = __longlong_as_double(0x7ff8000000000000ll);
-    for (int i = 0; i < 3; ++i) O.sigma[p * 3 + i] = __longlong_as_double(0x7ff8000000000000ll);
-    for (int i = 0; i < 9; ++i) O.C[p * 9 + i] = __longlong_as_double(0x7ff8000000000000ll);
+    O.res[p] = qnan();
+    for (int i = 0; i < 3; ++i) O.sigma[p * 3 + i] = qnan();
+    for (int i = 0; i < 9; ++i) O.C[p * 9 + i] = qnan();
     return;
   }
   for (int i = 0; i < 3; ++i) D.E_ev[p * 3 + i] = lerp_rn(D.E_prev[p * 3 + i], D.E_tgt[p * 3 + i], 1.0);
@@ -787,15 +995,15 @@ void launch_round_nt(const RoundArgs& a, cudaStream_t s) {
 
 template <int NP>
 void launch_commit_np(const ModelDev& M, const PointsDev& D, const Outputs& O, cudaStream_t s) {
-  const size_t smem = (3 * NP * (kQC + 1) + kCommitWarps * kCommitPPW * NP) * sizeof(double);
+  const size_t smem = CommitLayout<NP>::bytes;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_commit<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     configured = true;
   }
-  const int64_t per_cta = kCommitWarps * kCommitPPW;
+  const int64_t per_cta = kCW * kCPPW;
   const int64_t grid = (D.P + per_cta - 1) / per_cta;
-  k_commit<NP><<<static_cast<unsigned>(grid), kCommitWarps * 32, smem, s>>>(M, D, O);
+  k_commit<NP><<<static_cast<unsigned>(grid), kCW * 32, smem, s>>>(M, D, O);
 }
 
 }  // namespace

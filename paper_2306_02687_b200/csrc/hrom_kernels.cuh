@@ -37,16 +37,16 @@ struct ModelDev {
   int nchunks;  // K2p / kQC
   const double* G2;       // [K2p][S]   projected operator rows (zero padded)
   const double* w2;       // [K2p]      cubature weights (0 on pads)
-  const double* Kinc;     // [NP][NP]   Σ_{elastic q} w G^T C_e G
-  const double* KaEinc;   // [NP][3]    Σ_{elastic q} w G^T C_e
-  double CEEinc[9];       //            Σ_{elastic q} w C_e
+  const double* Ke;       // [NP][NP]   Σ_{all q} w G^T C_e G   (elastic predictor stiffness)
+  const double* KaEe;     // [NP][3]    Σ_{all q} w G^T C_e
+  double CEEe[9];         //            Σ_{all q} w C_e
   double volume;
   MatDev mat2;            // the (single) J2 material of the history-carrying points
 };
 
 struct PointsDev {
   int64_t P;
-  double* hist;  // 6 SoA components [6][P][K2p]: eps_p(4), eq, sigma33
+  double* hist;  // 5 SoA components [5][P][K2p]: eps_p(4), eq (sigma33 is recomputed on readback)
   double* alpha_c;
   double* alpha;
   double* alpha_ev;
@@ -54,6 +54,8 @@ struct PointsDev {
   double* E_prev;
   double* E_tgt;
   double* E_ev;  // [P][3] each
+  double* bp;     // [P][NP]  Σ_{J2 q} w G_q^T S(eps_p,q)  (committed plastic-strain load)
+  double* sp;     // [P][4]   Σ_{J2 q} w S(eps_p,q)
   PointState* st;
   uint8_t* flags;  // [P][K2p] plastic flags of the last commit (optional)
 };
