@@ -142,12 +142,19 @@ def cpu_reference_run(cfg, n_points, threads, seed=0):
     return n_points * cfg["incr"] / dt, dt
 
 
+def calibrate_cpu_points(cfg, threads, seconds):
+    """Sample size (points, all increments) giving about `seconds` of CPU work."""
+    n0 = max(2 * threads, 16)
+    v0, _ = cpu_reference_run(cfg, n0, threads)
+    return int(max(n0, min(1 << 16, v0 * seconds / cfg["incr"])))
+
+
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n_pts = args.cpu_sample_points or max(threads * 8, 128)
+    n_pts = args.cpu_sample_points or calibrate_cpu_points(cfg, threads, seconds=8.0)
     for _ in range(args.warmup):
         cpu_reference_run(cfg, max(threads, 16), threads)
     vals, times = [], []
@@ -299,42 +306,53 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (fused assembly + Newton round)
-    F_asm = flops_per_assembly(cfg["n"], model.K_j2)
-    achieved = stats["round_assemblies"] * F_asm / (stats["round_ms"] / 1e3) / 1e12 if stats["round_ms"] else None
+    # ---- roofline of the dominant kernel: k_increment (one persistent launch
+    # per increment: hyper-assembly on DMMA + Newton + condensation + commit)
+    K_j2, n_modes = model.K_j2, cfg["n"]
+    kms = stats["kernel_ms"]
+    F_asm = flops_per_assembly(n_modes, K_j2)
+    achieved = stats["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12 if kms else None
+    ntp = ((n_modes + 7) // 8) * ((n_modes + 7) // 8 + 1) // 2
+    # executed tensor work: every plastic point = 3 k-entries = 0.75 k-steps of NTP DMMA.8x8x4 (512 flop)
+    dmma_tflops = stats["timed_plastic_evals"] * 0.75 * ntp * 512 / (kms / 1e3) / 1e12 if kms else None
     try:
         peak = json.load(open(DMMA_PEAK_FILE))["dmma_tflops_w16"]
-        peak_src = "measured DMMA m8n8k4 f64 peak (tools/fp64_peak.cu, profiles/r01_fp64_peak.json)"
+        peak_src = "measured DMMA m8n8k4 f64 peak on this pool's B200 (tools/fp64_peak.cu, profiles/r01_fp64_peak.json)"
     except Exception:
         peak, peak_src = 37.0, "fallback: DMMA peak estimate"
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_round_summary.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_increment_summary.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    avg_launch_ms = stats["round_ms"] / max(1, stats["timed_rounds"])
+    launches_t = max(1, stats["timed_launches"])
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "k_newton_round (fused hyper-assembly on DMMA + warp Cholesky/Newton/condensation)",
+                "kernel": "k_increment (persistent: DMMA hyper-assembly + warp Cholesky/Newton/condensation + commit)",
                 "peak_source": peak_src, "flops_per_point_assembly": F_asm,
-                "avg_launch_ms": avg_launch_ms, "share_of_step": stats["round_ms"] / ms if ms else None}
+                "flops_definition": "SURVEY §8(d) F_asm = 3 K_J2 n (n+9) per point-assembly (elastic block precomputed)",
+                "executed_dmma_tflops": dmma_tflops,
+                "avg_launch_ms": kms / launches_t, "share_of_step": kms / ms if ms else None}
     try:
         hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
         hbm_src = "MEASURED_PEAKS.json"
     except Exception:
         hbm, hbm_src = 6650.0, "fallback 6.65 TB/s"
-    commit_gbs = stats["commit_j2_evals"] * 88 / (stats["commit_ms"] / 1e3) / 1e9 if stats["commit_ms"] else None
-    roofline_commit = {"bound": "hbm", "achieved": commit_gbs, "peak": hbm, "unit": "GB/s",
-                       "frac": commit_gbs / hbm if commit_gbs else None, "peak_source": hbm_src,
-                       "kernel": "k_commit (constitutive update + SoA history write)", "bytes_per_j2_point": 88,
-                       "share_of_step": stats["commit_ms"] / ms if ms else None}
+    # history stream of the same kernel: 40 B read per J2 point per pass, 40 B written per plastic commit
+    hbm_bytes = (stats["timed_assemblies"] + stats["timed_commits"]) * K_j2 * 40 + stats["timed_commit_plastic"] * 40
+    gbs = hbm_bytes / (kms / 1e3) / 1e9 if kms else None
+    roofline_hbm = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                    "frac": gbs / hbm if gbs else None, "peak_source": hbm_src,
+                    "kernel": "k_increment history stream (eps_p[4], eq SoA)",
+                    "bytes_definition": "40 B read per J2 point per assembly/commit pass + 40 B written per plastic commit",
+                    "bytes_per_step": hbm_bytes / args.steps}
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         threads = os.cpu_count() or 1
-        n_pts = args.cpu_sample_points or max(threads * 8, 128)
+        n_pts = args.cpu_sample_points or calibrate_cpu_points(cfg, threads, seconds=12.0)
         v, dt = cpu_reference_run(cfg, n_pts, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"first {n_pts} points x {incr} increments of {cfg['name']} ({dt:.1f} s)"}
@@ -351,10 +369,12 @@ def main():
                 "steps": e2e_steps, "api": "fe2_hrom_solve_increment (host buffers, pinned)"},
         "gpu_launches": launches,
         "roofline": roofline,
-        "roofline_commit": roofline_commit,
+        "roofline_hbm": roofline_hbm,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
-        "newton": {"rounds": stats["newton_rounds"], "point_assemblies_per_eval": stats["round_assemblies"] / evals * ws},
+        "newton": {"assemblies_per_eval": stats["timed_assemblies"] / (evals / ws),
+                   "commits_per_eval": stats["timed_commits"] / (evals / ws),
+                   "plastic_fraction": stats["timed_plastic_evals"] / max(1, stats["timed_assemblies"] * K_j2)},
     }
     print(json.dumps(line), flush=True)
     if ws > 1:

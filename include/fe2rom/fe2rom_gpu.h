@@ -125,15 +125,14 @@ typedef struct {
   int64_t points;
   int n, K, K_j2;
   int64_t kernel_launches;   /* own kernels launched since create */
-  int64_t newton_rounds;     /* fused assemble+step rounds since create */
-  int64_t point_assemblies;  /* (point, assembly) pairs processed since create */
-  int64_t j2_point_evals;    /* (point, J2 cubature point) material updates in assembly */
+  int64_t increments;        /* increments solved (one persistent launch each) */
+  int64_t assemblies;        /* (point, hyper-assembly pass) pairs since create */
+  int64_t commits;           /* (point, history-commit pass) pairs since create */
+  int64_t plastic_evals;     /* (point, J2 cubature point) found plastic in assembly passes */
   /* CUDA-event kernel timing (only while fe2_hrom_set_timing is on) */
-  double round_ms;            /* summed duration of the fused assemble+Newton launches */
-  int64_t round_assemblies;   /* (point, assembly) pairs in those launches */
-  double commit_ms;           /* summed duration of the history-commit launches */
-  int64_t commit_j2_evals;    /* (point, J2 cubature point) pairs committed in them */
-  int64_t timed_rounds, timed_commits;
+  double kernel_ms;          /* summed duration of the increment kernels */
+  int64_t timed_launches, timed_assemblies, timed_commits, timed_plastic_evals;
+  int64_t timed_commit_plastic; /* J2 points written by commit passes in timed launches */
 } fe2_hrom_stats_t;
 int fe2_hrom_stats(fe2_hrom_t h, fe2_hrom_stats_t* out);
 /* zero every counter of fe2_hrom_stats */

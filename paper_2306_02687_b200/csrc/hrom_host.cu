@@ -1,14 +1,19 @@
 // Host driver of the B200 hyper-ROM engine behind the C ABI
 // (include/fe2rom/fe2rom_gpu.h). Owns the device model (projected operator
-// rows, weights, elastic-inclusion constants), the per-point SoA state in
-// HBM, and the increment loop: begin → fused Newton rounds over a shrinking
-// active list → history commit. One handle per device; no CPU fallback.
+// rows, weights, elastic-predictor constants), the per-point SoA state in
+// HBM, and the increment loop: one persistent kernel launch per increment
+// (assembly + Newton + condensation + commit fused, see hrom_kernels.cu).
+// One handle per device; no CPU fallback.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.hpp"
@@ -46,15 +51,14 @@ void require_device(int device) {
   check(device >= 0 && device < count, Code::config, "device index out of range");
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
-  check(prop.major == 10, Code::numeric,
-        std::string("the engine is built for sm_100a (B200); found ") + prop.name);
+  check(prop.major == 10, Code::numeric, std::string("the engine is built for sm_100a (B200); found ") + prop.name);
   CK(cudaSetDevice(device));
 }
 
 MatDev to_dev(const fe2_material_t& m) {
   check(m.kind == 0 || m.kind == 1, Code::config, "unsupported material kind");
   const double E = m.p[0], nu = m.p[1];
-  check(E > 0.0 && nu >= 0.0 && nu < 0.5, Code::config, "invalid elastic parameters");  // materials.hpp:80-82
+  check(E > 0.0 && nu >= 0.0 && nu < 0.5, Code::config, "invalid elastic parameters");            // materials.hpp:80-82
   if (m.kind == 1) check(m.p[2] > 0.0 && m.p[3] >= 0.0, Code::config, "invalid J2 parameters");  // :83-87
   return make_mat(m.kind, E, nu, m.kind == 1 ? m.p[2] : 0.0, m.kind == 1 ? m.p[3] : 0.0);
 }
@@ -68,8 +72,8 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 using namespace fe2;
 
 struct fe2_hrom_s {
-  int device = 0;
-  cudaStream_t stream = nullptr;       // work stream (own, or the caller's)
+  int device = 0, num_sms = 148;
+  cudaStream_t stream = nullptr;  // work stream (own, or the caller's)
   cudaStream_t own_stream = nullptr;
   int n = 0, NP = 0, S = 0, K = 0, K2 = 0, K2p = 0;
   double volume = 0.0;
@@ -83,20 +87,19 @@ struct fe2_hrom_s {
   // device points
   int64_t P = 0;
   bool keep_flags = false;
-  double *hist = nullptr, *alpha_c = nullptr, *alpha = nullptr, *alpha_ev = nullptr, *dalpha = nullptr;
-  double *E_prev = nullptr, *E_tgt = nullptr, *E_ev = nullptr;
-  double *bp = nullptr, *sp = nullptr;
+  double *hist = nullptr, *alpha_c = nullptr, *E_c = nullptr, *bp = nullptr, *sp = nullptr;
   PointState* st = nullptr;
   uint8_t* flags = nullptr;
-  int *act[2] = {nullptr, nullptr}, *cnt = nullptr;
-  int* h_cnt = nullptr;  // pinned
-  // staging for the host-buffer API
+  int* work = nullptr;              // work-queue counter
+  IncCounters* cnt = nullptr;       // device counters of a launch
+  IncCounters* h_cnt = nullptr;     // pinned copy
+  // staging for the host-buffer API and default outputs
   double *dE = nullptr, *o_sigma = nullptr, *o_C = nullptr, *o_res = nullptr;
   int *o_iters = nullptr, *o_status = nullptr, *o_pc = nullptr;
   // stats
   bool timing = false;
   fe2_hrom_stats_t stats{};
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
 
   ModelDev model() const {
     ModelDev M{};
@@ -120,12 +123,7 @@ struct fe2_hrom_s {
     D.P = P;
     D.hist = hist;
     D.alpha_c = alpha_c;
-    D.alpha = alpha;
-    D.alpha_ev = alpha_ev;
-    D.dalpha = dalpha;
-    D.E_prev = E_prev;
-    D.E_tgt = E_tgt;
-    D.E_ev = E_ev;
+    D.E_c = E_c;
     D.bp = bp;
     D.sp = sp;
     D.st = st;
@@ -135,18 +133,11 @@ struct fe2_hrom_s {
   void free_points() {
     dfree(hist);
     dfree(alpha_c);
-    dfree(alpha);
-    dfree(alpha_ev);
-    dfree(dalpha);
-    dfree(E_prev);
-    dfree(E_tgt);
-    dfree(E_ev);
+    dfree(E_c);
     dfree(bp);
     dfree(sp);
     dfree(st);
     dfree(flags);
-    dfree(act[0]);
-    dfree(act[1]);
     dfree(dE);
     dfree(o_sigma);
     dfree(o_C);
@@ -156,6 +147,16 @@ struct fe2_hrom_s {
     dfree(o_pc);
     P = 0;
   }
+  void zero_points(cudaStream_t s) {
+    CK(cudaMemsetAsync(hist, 0, static_cast<size_t>(P) * K2p * 5 * sizeof(double), s));
+    const size_t an = static_cast<size_t>(P) * NP * sizeof(double);
+    CK(cudaMemsetAsync(alpha_c, 0, an, s));
+    CK(cudaMemsetAsync(bp, 0, an, s));
+    CK(cudaMemsetAsync(E_c, 0, P * 3 * sizeof(double), s));
+    CK(cudaMemsetAsync(sp, 0, P * 4 * sizeof(double), s));
+    CK(cudaMemsetAsync(st, 0, P * sizeof(PointState), s));
+    if (flags) CK(cudaMemsetAsync(flags, 0, static_cast<size_t>(P) * K2p, s));
+  }
   ~fe2_hrom_s() {
     cudaSetDevice(device);
     free_points();
@@ -163,6 +164,7 @@ struct fe2_hrom_s {
     dfree(w2);
     dfree(Ke);
     dfree(KaEe);
+    dfree(work);
     dfree(cnt);
     if (h_cnt) cudaFreeHost(h_cnt);
     for (auto& e : ev)
@@ -173,12 +175,10 @@ struct fe2_hrom_s {
 
 namespace {
 
-void count_launch(fe2_hrom_t h, int k = 1) { h->stats.kernel_launches += k; }
-
 struct Eps3 {
   double v[3];
 };
-// committed strain eps_q = E + G_q alpha_c of point p (host, readback only)
+// committed strain eps_q = E_c + G_q alpha_c of point p (host, readback only)
 Eps3 strain_at(fe2_hrom_t h, int64_t p, int q, const double* ac, const double* Ec) {
   const int n = h->n, NP = h->NP;
   const double* Gq = h->G.data() + static_cast<size_t>(q) * 3 * n;
@@ -191,10 +191,7 @@ Eps3 strain_at(fe2_hrom_t h, int64_t p, int q, const double* ac, const double* E
   return e;
 }
 
-// One increment on device buffers (the engine's core loop).
-void run_increment(fe2_hrom_t h, const double* d_E, const fe2_newton_opts_t* opts, const Outputs& O,
-                   cudaStream_t s) {
-  check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+NewtonCfg make_cfg(const fe2_newton_opts_t* opts) {
   NewtonCfg cfg{1e-8, 30, 4};
   if (opts) {
     cfg.tol = opts->tol;
@@ -202,65 +199,88 @@ void run_increment(fe2_hrom_t h, const double* d_E, const fe2_newton_opts_t* opt
     cfg.max_bis = opts->max_bisections;
   }
   check(cfg.tol > 0.0 && cfg.max_iter >= 0 && cfg.max_bis >= 0, Code::config, "invalid Newton options");
-  const ModelDev M = h->model();
-  const PointsDev D = h->points();
-  CK(cudaMemsetAsync(h->cnt, 0, 2 * sizeof(int), s));
-  launch_begin_increment(M, D, O, d_E, h->act[0], h->cnt, s);
-  count_launch(h);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(h->h_cnt, h->cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  int n_active = *h->h_cnt;
-  int cur = 0;
-  // bound: every Newton iteration costs at most 1 + 8 rounds, per sub-step
-  const int64_t max_rounds = static_cast<int64_t>(cfg.max_iter + 1) * 9 * (cfg.max_bis + 2) * 8 + 64;
-  int64_t rounds = 0;
-  while (n_active > 0) {
-    check(++rounds <= max_rounds, Code::solver, "round limit exceeded (state machine did not terminate)");
-    int* next_cnt = h->cnt + 1;
-    CK(cudaMemsetAsync(next_cnt, 0, sizeof(int), s));
-    RoundArgs a{};
-    a.M = M;
-    a.D = D;
-    a.O = O;
-    a.cfg = cfg;
-    a.active = h->act[cur];
-    a.n_active = n_active;
-    a.next_active = h->act[cur ^ 1];
-    a.n_next = next_cnt;
-    a.dbg = nullptr;
-    if (h->timing) CK(cudaEventRecord(h->ev[0], s));
-    launch_newton_round(a, s);
-    count_launch(h);
-    CK(cudaGetLastError());
-    if (h->timing) CK(cudaEventRecord(h->ev[1], s));
-    h->stats.newton_rounds += 1;
-    h->stats.point_assemblies += n_active;
-    h->stats.j2_point_evals += static_cast<int64_t>(n_active) * h->K2;
-    CK(cudaMemcpyAsync(h->h_cnt, next_cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (h->timing) {
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
-      h->stats.round_ms += ms;
-      h->stats.round_assemblies += n_active;
-      h->stats.timed_rounds += 1;
-    }
-    n_active = *h->h_cnt;
-    cur ^= 1;
+  return cfg;
+}
+
+// Watchdog (debug aid, FE2_TRACE=<seconds>): the persistent kernel writes its
+// per-warp ring position and state into mapped pinned host memory; if the
+// launch does not finish in time the trace is printed and the process exits
+// instead of hanging the device.
+struct Watchdog {
+  int* host = nullptr;
+  int* dev = nullptr;
+  int slots = 0;
+  double seconds = 0.0;
+  explicit Watchdog(int num_sms) {
+    const char* env = std::getenv("FE2_TRACE");
+    if (!env || !*env) return;
+    seconds = std::atof(env);
+    if (seconds <= 0.0) seconds = 60.0;
+    slots = num_sms * 4 * 8;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&host), slots * 4 * sizeof(int), cudaHostAllocMapped));
+    std::memset(host, 0xff, slots * 4 * sizeof(int));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0));
   }
-  if (h->timing) CK(cudaEventRecord(h->ev[2], s));
-  launch_commit(M, D, O, s);
-  count_launch(h);
+  ~Watchdog() {
+    if (host) cudaFreeHost(host);
+  }
+  void wait(cudaStream_t s, const char* what) {
+    if (!host) return;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (cudaStreamQuery(s) == cudaErrorNotReady) {
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > seconds) {
+        std::fprintf(stderr, "[fe2 watchdog] %s did not finish in %.0f s; warp {pos, state, issued, working}:\n",
+                     what, seconds);
+        for (int i = 0; i < slots; ++i)
+          if (host[4 * i] != -1)
+            std::fprintf(stderr, "  cta %d warp %d: %d %d %d %d\n", i / 8, i % 8, host[4 * i], host[4 * i + 1],
+                         host[4 * i + 2], host[4 * i + 3]);
+        std::fflush(stderr);
+        std::_Exit(3);
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    }
+  }
+};
+
+// One increment on device buffers: a single persistent kernel launch.
+void run_increment(fe2_hrom_t h, const double* d_E, const NewtonCfg& cfg, const Outputs& O, cudaStream_t s) {
+  check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+  IncArgs a{};
+  a.M = h->model();
+  a.D = h->points();
+  a.O = O;
+  a.cfg = cfg;
+  a.dE = d_E;
+  a.work = h->work;
+  a.cnt = h->cnt;
+  CK(cudaMemsetAsync(h->work, 0, sizeof(int), s));
+  CK(cudaMemsetAsync(h->cnt, 0, sizeof(IncCounters), s));
+  Watchdog wd(h->num_sms);
+  a.trace = wd.dev;
+  if (h->timing) CK(cudaEventRecord(h->ev[0], s));
+  launch_increment(a, h->num_sms, s);
   CK(cudaGetLastError());
-  if (h->timing) CK(cudaEventRecord(h->ev[3], s));
+  if (h->timing) CK(cudaEventRecord(h->ev[1], s));
+  wd.wait(s, "k_increment");
+  CK(cudaMemcpyAsync(h->h_cnt, h->cnt, sizeof(IncCounters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  const IncCounters c = *h->h_cnt;
+  h->stats.kernel_launches += 1;
+  h->stats.increments += 1;
+  h->stats.assemblies += static_cast<int64_t>(c.assemblies);
+  h->stats.commits += static_cast<int64_t>(c.commits);
+  h->stats.plastic_evals += static_cast<int64_t>(c.plastic_evals);
   if (h->timing) {
     float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
-    h->stats.commit_ms += ms;
-    h->stats.commit_j2_evals += h->P * static_cast<int64_t>(h->K2);
-    h->stats.timed_commits += 1;
+    CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+    h->stats.kernel_ms += ms;
+    h->stats.timed_launches += 1;
+    h->stats.timed_assemblies += static_cast<int64_t>(c.assemblies);
+    h->stats.timed_commits += static_cast<int64_t>(c.commits);
+    h->stats.timed_plastic_evals += static_cast<int64_t>(c.plastic_evals);
+    h->stats.timed_commit_plastic += static_cast<int64_t>(c.commit_plastic);
   }
 }
 
@@ -270,7 +290,7 @@ extern "C" {
 
 const char* fe2_last_error(void) { return fe2::g_last_error.c_str(); }
 
-const char* fe2_version(void) { return "fe2rom-b200 0.1 sm_100a"; }
+const char* fe2_version(void) { return "fe2rom-b200 0.2 sm_100a"; }
 
 int fe2_device_count(void) {
   int c = 0;
@@ -321,6 +341,7 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
     auto h = new fe2_hrom_s;
     try {
       h->device = device;
+      CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
       h->n = n;
       h->NP = (n + 7) / 8 * 8;
       h->S = 3 * h->NP + 1;
@@ -349,7 +370,8 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
       for (int q2 = 0; q2 < h->K2; ++q2) {
         const int q = h->j2_idx[q2];
         for (int i = 0; i < 3; ++i)
-          for (int a = 0; a < n; ++a) G2[static_cast<size_t>(q2) * S + i * NP + a] = G[(static_cast<size_t>(q) * 3 + i) * n + a];
+          for (int a = 0; a < n; ++a)
+            G2[static_cast<size_t>(q2) * S + i * NP + a] = G[(static_cast<size_t>(q) * 3 + i) * n + a];
         w2[q2] = w[q];
       }
       // elastic predictor over ALL cubature points (J2 points with the J2
@@ -390,8 +412,9 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
       h->w2 = dalloc<double>(w2.size());
       h->Ke = dalloc<double>(Ke.size());
       h->KaEe = dalloc<double>(KaEe.size());
-      h->cnt = dalloc<int>(2);
-      CK(cudaMallocHost(&h->h_cnt, sizeof(int)));
+      h->work = dalloc<int>(1);
+      h->cnt = dalloc<IncCounters>(1);
+      CK(cudaMallocHost(&h->h_cnt, sizeof(IncCounters)));
       CK(cudaMemcpy(h->G2, G2.data(), G2.size() * sizeof(double), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(h->w2, w2.data(), w2.size() * sizeof(double), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(h->Ke, Ke.data(), Ke.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -414,24 +437,16 @@ int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
     check(h != nullptr && P >= 1, Code::config, "bad arguments");
     check(P < (int64_t(1) << 31), Code::config, "at most 2^31-1 points per device");
     CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
     h->free_points();
-    const size_t hist_n = static_cast<size_t>(P) * h->K2p * 5;
-    h->hist = dalloc<double>(hist_n);
-    const size_t an = static_cast<size_t>(P) * h->NP;
-    h->alpha_c = dalloc<double>(an);
-    h->alpha = dalloc<double>(an);
-    h->alpha_ev = dalloc<double>(an);
-    h->dalpha = dalloc<double>(an);
-    h->E_prev = dalloc<double>(P * 3);
-    h->E_tgt = dalloc<double>(P * 3);
-    h->E_ev = dalloc<double>(P * 3);
-    h->bp = dalloc<double>(an);
+    h->hist = dalloc<double>(static_cast<size_t>(P) * h->K2p * 5);
+    h->alpha_c = dalloc<double>(static_cast<size_t>(P) * h->NP);
+    h->bp = dalloc<double>(static_cast<size_t>(P) * h->NP);
+    h->E_c = dalloc<double>(P * 3);
     h->sp = dalloc<double>(P * 4);
     h->st = dalloc<PointState>(P);
     h->keep_flags = keep_flags != 0;
     if (h->keep_flags) h->flags = dalloc<uint8_t>(static_cast<size_t>(P) * h->K2p);
-    h->act[0] = dalloc<int>(P);
-    h->act[1] = dalloc<int>(P);
     h->dE = dalloc<double>(P * 3);
     h->o_sigma = dalloc<double>(P * 3);
     h->o_C = dalloc<double>(P * 9);
@@ -439,15 +454,9 @@ int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
     h->o_iters = dalloc<int>(P);
     h->o_status = dalloc<int>(P);
     h->o_pc = dalloc<int>(P);
-    CK(cudaMemsetAsync(h->hist, 0, hist_n * sizeof(double), h->stream));
-    for (double* p : {h->alpha_c, h->alpha, h->alpha_ev, h->dalpha, h->bp})
-      CK(cudaMemsetAsync(p, 0, an * sizeof(double), h->stream));
-    CK(cudaMemsetAsync(h->sp, 0, P * 4 * sizeof(double), h->stream));
-    for (double* p : {h->E_prev, h->E_tgt, h->E_ev}) CK(cudaMemsetAsync(p, 0, P * 3 * sizeof(double), h->stream));
-    CK(cudaMemsetAsync(h->st, 0, P * sizeof(PointState), h->stream));
-    if (h->flags) CK(cudaMemsetAsync(h->flags, 0, static_cast<size_t>(P) * h->K2p, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
     h->P = P;
+    h->zero_points(h->stream);
+    CK(cudaStreamSynchronize(h->stream));
     h->stats.points = P;
   });
 }
@@ -456,15 +465,7 @@ int fe2_hrom_reset_points(fe2_hrom_t h) {
   return guard([&] {
     check(h != nullptr && h->P > 0, Code::config, "no points allocated");
     CK(cudaSetDevice(h->device));
-    const int64_t P = h->P;
-    cudaStream_t s = h->stream;
-    CK(cudaMemsetAsync(h->hist, 0, static_cast<size_t>(P) * h->K2p * 5 * sizeof(double), s));
-    const size_t an = static_cast<size_t>(P) * h->NP * sizeof(double);
-    for (double* p : {h->alpha_c, h->alpha, h->alpha_ev, h->dalpha, h->bp}) CK(cudaMemsetAsync(p, 0, an, s));
-    CK(cudaMemsetAsync(h->sp, 0, P * 4 * sizeof(double), s));
-    for (double* p : {h->E_prev, h->E_tgt, h->E_ev}) CK(cudaMemsetAsync(p, 0, P * 3 * sizeof(double), s));
-    CK(cudaMemsetAsync(h->st, 0, P * sizeof(PointState), s));
-    if (h->flags) CK(cudaMemsetAsync(h->flags, 0, static_cast<size_t>(P) * h->K2p, s));
+    h->zero_points(h->stream);
   });
 }
 
@@ -489,7 +490,7 @@ int fe2_hrom_solve_increment_device(fe2_hrom_t h, const double* d_E, const fe2_n
     CK(cudaSetDevice(h->device));
     Outputs O{d_sigma ? d_sigma : h->o_sigma, d_C ? d_C : h->o_C, d_res ? d_res : h->o_res,
               d_iters ? d_iters : h->o_iters, d_status ? d_status : h->o_status, d_pc ? d_pc : h->o_pc};
-    run_increment(h, d_E, opts, O, stream ? static_cast<cudaStream_t>(stream) : h->stream);
+    run_increment(h, d_E, make_cfg(opts), O, stream ? static_cast<cudaStream_t>(stream) : h->stream);
   });
 }
 
@@ -499,11 +500,12 @@ int fe2_hrom_solve_increment(fe2_hrom_t h, const double* E, const fe2_newton_opt
     check(h != nullptr && E != nullptr, Code::config, "bad arguments");
     check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
     CK(cudaSetDevice(h->device));
+    const NewtonCfg cfg = make_cfg(opts);
     const int64_t P = h->P;
     cudaStream_t s = h->stream;
     CK(cudaMemcpyAsync(h->dE, E, P * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
     Outputs O{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc};
-    run_increment(h, h->dE, opts, O, s);
+    run_increment(h, h->dE, cfg, O, s);
     if (sigma) CK(cudaMemcpyAsync(sigma, h->o_sigma, P * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (C) CK(cudaMemcpyAsync(C, h->o_C, P * 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (iters) CK(cudaMemcpyAsync(iters, h->o_iters, P * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -530,30 +532,24 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
     if (state) {
       std::vector<double> hs(static_cast<size_t>(P) * K2p * 5), Ec(static_cast<size_t>(P) * 3);
       CK(cudaMemcpy(hs.data(), h->hist, hs.size() * sizeof(double), cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(Ec.data(), h->E_ev, Ec.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(Ec.data(), h->E_c, Ec.size() * sizeof(double), cudaMemcpyDeviceToHost));
       const size_t PK = static_cast<size_t>(P) * K2p;
       for (int64_t p = 0; p < P; ++p) {
         // sigma33 is write-only in the reference (materials.hpp:181, :193): it is
         // not kept in HBM but recomputed here from the committed strain and eps_p,
-        // sigma33 = lam tr(eps - eps_p) + 2 mu (0 - eps_p,33) (tr Δeps_p = 0).
+        // sigma33 = lam tr(eps - eps_p) + 2 mu (0 - eps_p,33).
         for (int q = 0; q < K; ++q) {
-          const double* Gq = h->G.data() + static_cast<size_t>(q) * 3 * n;
-          double e[3];
-          for (int i = 0; i < 3; ++i) {
-            double s = 0.0;
-            for (int a = 0; a < n; ++a) s += Gq[i * n + a] * ac[p * NP + a];
-            e[i] = Ec[p * 3 + i] + s;
-          }
+          const Eps3 e = strain_at(h, p, q, ac.data(), Ec.data());
           double* s = state + (static_cast<size_t>(p) * K + q) * 6;
           for (int c = 0; c < 5; ++c) s[c] = 0.0;
-          const MatDev& m = h->qmat[q];
-          s[5] = m.lam * (e[0] + e[1]);
+          s[5] = h->qmat[q].lam * (e.v[0] + e.v[1]);
         }
         for (int q2 = 0; q2 < h->K2; ++q2) {
-          double* s = state + (static_cast<size_t>(p) * K + h->j2_idx[q2]) * 6;
+          const int q = h->j2_idx[q2];
+          double* s = state + (static_cast<size_t>(p) * K + q) * 6;
           for (int c = 0; c < 5; ++c) s[c] = hs[c * PK + static_cast<size_t>(p) * K2p + q2];
           const MatDev& m = h->mat2;
-          const Eps3 e = strain_at(h, p, h->j2_idx[q2], ac.data(), Ec.data());
+          const Eps3 e = strain_at(h, p, q, ac.data(), Ec.data());
           s[5] = m.lam * ((e.v[0] - s[0]) + (e.v[1] - s[1]) + (0.0 - s[2])) + 2.0 * m.mu * (0.0 - s[2]);
         }
       }
@@ -575,37 +571,31 @@ int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, co
     check(alpha && E && r && Kaa && KaE && C_EE && S_raw, Code::config, "null buffer");
     CK(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
-    const int n = h->n, NP = h->NP;
-    // save the point's evaluation state, evaluate, restore
-    std::vector<double> save_a(NP), save_e(3), a_in(NP, 0.0);
-    CK(cudaMemcpy(save_a.data(), h->alpha_ev + point * NP, NP * sizeof(double), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(save_e.data(), h->E_ev + point * 3, 3 * sizeof(double), cudaMemcpyDeviceToHost));
-    for (int a = 0; a < n; ++a) a_in[a] = alpha[a];
-    CK(cudaMemcpy(h->alpha_ev + point * NP, a_in.data(), NP * sizeof(double), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->E_ev + point * 3, E, 3 * sizeof(double), cudaMemcpyHostToDevice));
-    const int idx = static_cast<int>(point);
-    CK(cudaMemcpy(h->act[0], &idx, sizeof(int), cudaMemcpyHostToDevice));
+    const int n = h->n;
     const size_t dn = static_cast<size_t>(n) + n * n + 3 * n + 12;
-    double* dbg = dalloc<double>(dn);
-    RoundArgs a{};
+    double* dbg = dalloc<double>(dn + n + 3);
+    CK(cudaMemcpyAsync(dbg + dn, alpha, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dbg + dn + n, E, 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    IncArgs a{};
     a.M = h->model();
     a.D = h->points();
     a.O = Outputs{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc};
     a.cfg = NewtonCfg{1e-8, 30, 4};
-    a.active = h->act[0];
-    a.n_active = 1;
-    a.next_active = h->act[1];
-    a.n_next = h->cnt + 1;
+    a.work = h->work;
     a.dbg = dbg;
-    launch_newton_round(a, s);
-    count_launch(h);
+    a.dbg_alpha = dbg + dn;
+    a.dbg_E = dbg + dn + n;
+    a.dbg_point = point;
+    Watchdog wd(h->num_sms);
+    a.trace = wd.dev;
+    launch_increment(a, h->num_sms, s);
+    h->stats.kernel_launches += 1;
     CK(cudaGetLastError());
+    wd.wait(s, "k_increment (assembly dump)");
     std::vector<double> o(dn);
     CK(cudaMemcpyAsync(o.data(), dbg, dn * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     dfree(dbg);
-    CK(cudaMemcpy(h->alpha_ev + point * NP, save_a.data(), NP * sizeof(double), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->E_ev + point * 3, save_e.data(), 3 * sizeof(double), cudaMemcpyHostToDevice));
     std::memcpy(r, o.data(), n * sizeof(double));
     std::memcpy(Kaa, o.data() + n, static_cast<size_t>(n) * n * sizeof(double));
     std::memcpy(KaE, o.data() + n + n * n, 3 * n * sizeof(double));

@@ -1,6 +1,7 @@
-// Device side of the B200 hyper-ROM engine: data layout, the fused
-// assemble + Newton-step round (K2+K3), the history commit (K1) and the
-// batched material update. See DESIGN.md for the layout and rooflines.
+// Device side of the B200 hyper-ROM engine: data layout and the launchers of
+// the persistent per-increment kernel (assembly + Newton + condensation +
+// commit, fused) and of the batched material update. See DESIGN.md for the
+// layout and rooflines.
 #pragma once
 
 #include <cstdint>
@@ -12,20 +13,11 @@ namespace fe2 {
 
 constexpr int kQC = 32;  // cubature points per chunk (one per lane in the material phase)
 
-enum Phase : int { kActive = 0, kDone = 1, kFailed = 2 };
-enum Mode : int { kNewton = 0, kLineSearch = 1 };
-
-// Per-point Newton / increment state (one 96-byte record per macro point).
+// Per-point persistent record: only the trajectory-failure code survives
+// between increments (run_trajectory throws and the point stops, rve.hpp:474).
 struct PointState {
-  double a;        // current line-search step
-  double rn_it;    // residual norm at the current iterate
-  double best_rn;  // best line-search residual so far
-  double best_a;   // its step
-  double ref;      // convergence reference (fixed at it = 0)
-  double done;     // fraction of the increment committed (run_trajectory)
-  double frac;     // current sub-step fraction
-  double rn_last;  // last residual norm
-  int mode, it, ls, iters, bis, phase, err, pad;
+  int err;  // 0 alive, else 1 + ErrorCode
+  int pad[3];
 };
 
 struct ModelDev {
@@ -46,18 +38,13 @@ struct ModelDev {
 
 struct PointsDev {
   int64_t P;
-  double* hist;  // 5 SoA components [5][P][K2p]: eps_p(4), eq (sigma33 is recomputed on readback)
-  double* alpha_c;
-  double* alpha;
-  double* alpha_ev;
-  double* dalpha;  // [P][NP] each
-  double* E_prev;
-  double* E_tgt;
-  double* E_ev;  // [P][3] each
-  double* bp;     // [P][NP]  Σ_{J2 q} w G_q^T S(eps_p,q)  (committed plastic-strain load)
-  double* sp;     // [P][4]   Σ_{J2 q} w S(eps_p,q)
+  double* hist;     // 5 SoA components [5][P][K2p]: eps_p(4), eq (sigma33 is recomputed on readback)
+  double* alpha_c;  // [P][NP] committed reduced coordinates
+  double* E_c;      // [P][3]  committed macro strain (= previous path point)
+  double* bp;       // [P][NP] Σ_{J2 q} w G_q^T S(eps_p,q)  (committed plastic-strain load)
+  double* sp;       // [P][4]  Σ_{J2 q} w S(eps_p,q)
   PointState* st;
-  uint8_t* flags;  // [P][K2p] plastic flags of the last commit (optional)
+  uint8_t* flags;   // [P][K2p] plastic flags of the last commit (optional)
 };
 
 struct Outputs {
@@ -75,25 +62,37 @@ struct NewtonCfg {
   int max_bis;
 };
 
-struct RoundArgs {
+// Device counters of one launch (for the roofline): assembly passes, commit
+// passes, J2 points that were plastic in assembly passes.
+struct IncCounters {
+  unsigned long long assemblies;
+  unsigned long long commits;
+  unsigned long long plastic_evals;
+  unsigned long long commit_plastic;  // J2 points whose history was written by commit passes
+};
+
+struct IncArgs {
   ModelDev M;
   PointsDev D;
   Outputs O;
   NewtonCfg cfg;
-  const int* active;
-  int n_active;
-  int* next_active;
-  int* n_next;
-  double* dbg;  // debug assembly dump (r, K, KaE, CEE, Sraw) or nullptr
+  const double* dE;    // [P][3] this increment's path point
+  int* work;           // work-queue counter (zeroed before launch)
+  IncCounters* cnt;    // optional
+  // debug: one assembly of point dbg_point at (dbg_alpha, dbg_E), dumped to dbg
+  double* dbg;
+  const double* dbg_alpha;
+  const double* dbg_E;
+  int64_t dbg_point;
+  // watchdog trace (mapped pinned host memory, FE2_TRACE=1): per warp
+  // {ring position, state code, point, stage-counter snapshot}
+  volatile int* trace;
 };
 
 // host launchers (hrom_kernels.cu)
-void launch_newton_round(const RoundArgs& a, cudaStream_t s);
-void launch_commit(const ModelDev& M, const PointsDev& D, const Outputs& O, cudaStream_t s);
-void launch_begin_increment(const ModelDev& M, const PointsDev& D, const Outputs& O, const double* dE,
-                            int* active, int* n_active, cudaStream_t s);
+void launch_increment(const IncArgs& a, int num_sms, cudaStream_t s);
 void launch_material_batch(const MatDev& m, int64_t N, const double* eps, const double* st_in, double* sigma,
                            double* C, double* st_out, uint8_t* plastic, cudaStream_t s);
-size_t newton_round_smem(int NP);
+size_t increment_smem(int NP);
 
 }  // namespace fe2

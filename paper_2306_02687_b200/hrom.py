@@ -47,15 +47,16 @@ class _Stats(C.Structure):
         ("K", C.c_int),
         ("K_j2", C.c_int),
         ("kernel_launches", C.c_int64),
-        ("newton_rounds", C.c_int64),
-        ("point_assemblies", C.c_int64),
-        ("j2_point_evals", C.c_int64),
-        ("round_ms", C.c_double),
-        ("round_assemblies", C.c_int64),
-        ("commit_ms", C.c_double),
-        ("commit_j2_evals", C.c_int64),
-        ("timed_rounds", C.c_int64),
+        ("increments", C.c_int64),
+        ("assemblies", C.c_int64),
+        ("commits", C.c_int64),
+        ("plastic_evals", C.c_int64),
+        ("kernel_ms", C.c_double),
+        ("timed_launches", C.c_int64),
+        ("timed_assemblies", C.c_int64),
         ("timed_commits", C.c_int64),
+        ("timed_plastic_evals", C.c_int64),
+        ("timed_commit_plastic", C.c_int64),
     ]
 
 
