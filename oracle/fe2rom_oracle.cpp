@@ -1164,6 +1164,10 @@ inline void hrom_point_trajectory(const Hrom& h, std::int64_t pi, int n_incr, co
     } else {
       status = 1 + (int)ErrorCode::solver;
     }
+    if (status != 0) {  // run_trajectory throws: no response for this increment
+      for (double& s : sig) s = NAN;
+      for (double& c : C) c = NAN;
+    }
     if (out->sigma) std::memcpy(out->sigma + o * 3, sig, sizeof sig);
     if (out->C) std::memcpy(out->C + o * 9, C, sizeof C);
     if (out->iters) out->iters[o] = iters;

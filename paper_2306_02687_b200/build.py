@@ -1,4 +1,4 @@
-"""Build recipe for the native engine (sm_100a) and the CPU oracle.
+"""Build recipe for the native engine (sm_100a).
 
 libfe2rom_gpu.so = C-ABI host driver + sm_100a kernels + offline setup,
 built in-tree with nvcc so the .so travels with the repo snapshot.
@@ -47,14 +47,5 @@ def build_native(force=False, verbose=False):
     return LIB
 
 
-def build_oracle():
-    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("oracle build failed")
-    return os.path.join(ROOT, "oracle", "build", "liboracle.so")
-
-
 if __name__ == "__main__":
     print(build_native(force="--force" in sys.argv, verbose=True))
-    print(build_oracle())

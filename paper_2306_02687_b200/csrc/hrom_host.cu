@@ -83,7 +83,7 @@ struct fe2_hrom_s {
   MatDev mat2{};
   double CEEe[9] = {0};
   // device model
-  double *G2 = nullptr, *w2 = nullptr, *Ke = nullptr, *KaEe = nullptr;
+  double *G2 = nullptr, *w2 = nullptr, *Ke = nullptr, *KaEe = nullptr, *Le = nullptr, *LeInv = nullptr;
   // device points
   int64_t P = 0;
   bool keep_flags = false;
@@ -113,6 +113,9 @@ struct fe2_hrom_s {
     M.w2 = w2;
     M.Ke = Ke;
     M.KaEe = KaEe;
+    M.Le = Le;
+    M.LeInv = LeInv;
+    M.inv_denom = mat2.inv_denom;
     std::memcpy(M.CEEe, CEEe, sizeof CEEe);
     M.volume = volume;
     M.mat2 = mat2;
@@ -164,6 +167,8 @@ struct fe2_hrom_s {
     dfree(w2);
     dfree(Ke);
     dfree(KaEe);
+    dfree(Le);
+    dfree(LeInv);
     dfree(work);
     dfree(cnt);
     if (h_cnt) cudaFreeHost(h_cnt);
@@ -344,7 +349,7 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
       CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
       h->n = n;
       h->NP = (n + 7) / 8 * 8;
-      h->S = 3 * h->NP + 1;
+      h->S = 3 * h->NP + 2;
       h->K = K;
       h->volume = volume;
       h->G.assign(G, G + static_cast<size_t>(K) * 3 * n);
@@ -405,6 +410,27 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
           const double v = 0.5 * (Ke[static_cast<size_t>(a) * NP + b] + Ke[static_cast<size_t>(b) * NP + a]);
           Ke[static_cast<size_t>(a) * NP + b] = Ke[static_cast<size_t>(b) * NP + a] = v;
         }
+      // Cholesky factor of K_e in the kernel's shared layout [NP][NP+1]: the
+      // device reuses it whenever an assembly has no plastic point.
+      const int LD = NP + 1;
+      std::vector<double> Le(static_cast<size_t>(NP) * LD, 0.0), LeInv(NP, 0.0);
+      for (int j = 0; j < n; ++j) {
+        double d = Ke[static_cast<size_t>(j) * NP + j];
+        for (int k = 0; k < j; ++k) d -= Le[j * LD + k] * Le[j * LD + k];
+        check(d > 0.0, Code::solver, "elastic reduced stiffness K_e is not positive definite");
+        const double ljj = std::sqrt(d);
+        Le[j * LD + j] = ljj;
+        LeInv[j] = 1.0 / ljj;
+        for (int i = j + 1; i < n; ++i) {
+          double s = Ke[static_cast<size_t>(i) * NP + j];
+          for (int k = 0; k < j; ++k) s -= Le[i * LD + k] * Le[j * LD + k];
+          Le[i * LD + j] = s / ljj;
+        }
+      }
+      h->Le = dalloc<double>(Le.size());
+      h->LeInv = dalloc<double>(LeInv.size());
+      CK(cudaMemcpy(h->Le, Le.data(), Le.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->LeInv, LeInv.data(), LeInv.size() * sizeof(double), cudaMemcpyHostToDevice));
       CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
       h->stream = h->own_stream;
       for (auto& e : h->ev) CK(cudaEventCreate(&e));

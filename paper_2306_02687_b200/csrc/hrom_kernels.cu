@@ -101,6 +101,25 @@ __device__ __forceinline__ double lerp_rn(double e0, double e1, double t) {
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
+// 1/x and 1/sqrt(x) from the MUFU seeds plus two Newton steps (full fp64
+// accuracy to within an ulp; no IEEE division/sqrt sequences on the critical path).
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+
 // Left-looking Cholesky of the lower triangle of sK (row stride ld) in place;
 // lane i owns row i (n <= 32). sInv[j] = 1 / L_jj. False if not SPD.
 __device__ bool warp_cholesky(double* sK, double* sInv, int ld, int n, int lane) {
@@ -120,8 +139,8 @@ __device__ bool warp_cholesky(double* sK, double* sInv, int ld, int n, int lane)
     }
     const double d = __shfl_sync(0xffffffffu, s, j);
     if (!(d > 0.0)) return false;
-    const double ljj = sqrt(d);
-    const double inv = 1.0 / ljj;
+    const double inv = rsqrt_fast(d);
+    const double ljj = d * inv;
     if (lane == j) {
       sK[j * ld + j] = ljj;
       sInv[j] = inv;
@@ -187,18 +206,17 @@ struct Corr {
 __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
   Corr c;
   const double mu = m.mu;
-  const double denom = 3.0 * mu + m.h;
-  const double dlam = T.f / denom;
-  const double inv_q = 1.0 / T.q_tr;
+  const double dlam = T.f * m.inv_denom;  // f / (3 mu + h)
+  const double inv_q = rcp_fast(T.q_tr);
   const double cs = 3.0 * mu * dlam * inv_q;
   c.ds0 = -cs * T.d0;
   c.ds1 = -cs * T.d1;
   c.ds2 = -cs * T.d3;
-  const double inv_n = 1.0 / sqrt(T.ss);
+  const double inv_n = 1.2247448713915890491 * inv_q;  // 1/|s_tr| = sqrt(3/2) / q_tr
   const double n0 = T.d0 * inv_n, n1 = T.d1 * inv_n, n3 = T.d3 * inv_n;
   const double mu2 = 6.0 * mu * mu;
   const double c1 = mu2 * dlam * inv_q;
-  const double c2 = mu2 * (1.0 / denom - dlam * inv_q);
+  const double c2 = mu2 * (m.inv_denom - dlam * inv_q);
   c.dc00 = -c1 * (2.0 / 3.0) - c2 * (n0 * n0);
   c.dc01 = c1 * (1.0 / 3.0) - c2 * (n0 * n1);
   c.dc02 = -c2 * (n0 * n3);
@@ -213,7 +231,7 @@ constexpr int kStages = 3;  // G-chunk ring depth
 
 template <int NP>
 struct IncLayout {
-  static constexpr int S = 3 * NP + 1;
+  static constexpr int S = 3 * NP + 2;
   static constexpr int chunk = kQC * S;                      // doubles per ring stage
   static constexpr int kSlots = kQC * 9 + kQC * 3 + kQC;     // ΔC rows, Δσ, point index
   static constexpr int kUnion = (kSlots > NP * (NP + 1)) ? kSlots : NP * (NP + 1);
@@ -378,6 +396,8 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
 
   // outputs of an assembly pass (warp-uniform after the reductions)
   double s0 = 0, s1 = 0, s2 = 0, ce00 = 0, ce01 = 0, ce02 = 0, ce11 = 0, ce12 = 0, ce22 = 0;
+  bool k_linear = false;  // the last assembly had no plastic point (K_aa == K_e)
+  const int n = M.n;
 
   // ---------------------------------------------------------------- passes
   auto assembly_pass = [&](int64_t p, double E0, double E1, double E2) {
@@ -392,6 +412,7 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       kae[t][0] = kae[t][1] = kae[t][2] = 0.0;
     }
     double c00 = 0.0, c01 = 0.0, c02 = 0.0, c11 = 0.0, c12 = 0.0, c22 = 0.0, ds0 = 0.0, ds1 = 0.0, ds2 = 0.0;
+    int np_tot = 0;
     const double* H0 = D.hist + p * M.K2p;
     double h0 = H0[lane], h1 = H0[PK + lane], h2 = H0[2 * PK + lane], h3 = H0[3 * PK + lane],
            h4 = H0[4 * PK + lane];
@@ -401,21 +422,28 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       // lane = cubature point: strain, elastic trial, yield test
       const double* Gq = Gb + lane * S;
       double e0 = 0.0, e1 = 0.0, e2 = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
+      {  // ε = G_q α with 128-bit shared loads (rows are 16-B aligned, S even)
+        const double2* g0v = reinterpret_cast<const double2*>(Gq);
+        const double2* g1v = reinterpret_cast<const double2*>(Gq + NP);
+        const double2* g2v = reinterpret_cast<const double2*>(Gq + 2 * NP);
+        const double2* av = reinterpret_cast<const double2*>(sAev);
 #pragma unroll 4
-      for (int a = 0; a < NP; a += 2) {
-        const double al = sAev[a], bl = sAev[a + 1];
-        e0 += Gq[a] * al;
-        e1 += Gq[NP + a] * al;
-        e2 += Gq[2 * NP + a] * al;
-        f0 += Gq[a + 1] * bl;
-        f1 += Gq[NP + a + 1] * bl;
-        f2 += Gq[2 * NP + a + 1] * bl;
+        for (int a = 0; a < NP / 2; ++a) {
+          const double2 al = av[a], x0 = g0v[a], x1 = g1v[a], x2 = g2v[a];
+          e0 += x0.x * al.x;
+          f0 += x0.y * al.y;
+          e1 += x1.x * al.x;
+          f1 += x1.y * al.y;
+          e2 += x2.x * al.x;
+          f2 += x2.y * al.y;
+        }
       }
       const Trial T = trial_state(mt, h0, h1, h2, h3, h4, E0 + (e0 + f0), E1 + (e1 + f1), E2 + (e2 + f2));
       const bool plastic = (T.f > 0.0) && (q < M.K2);
       const unsigned bal = __ballot_sync(0xffffffffu, plastic);
       const int np = __popc(bal);
       n_pl += static_cast<unsigned long long>(np);
+      np_tot += np;
       if (plastic) {
         const Corr cr = radial_return(mt, T);
         const double wq = M.w2[q];
@@ -550,7 +578,6 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
     ds2 = warp_sum(ds2);
     __syncwarp();
     // elastic predictor part (constant K_e, K_aE,e, C_EE,e) and b_p, s_p
-    const int n = M.n;
     double sa0 = 0.0, sa1 = 0.0, sa2 = 0.0;
     if (lane < n) {
       const int a = lane;
@@ -592,8 +619,23 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
     ce11 = ce[4] + c11;
     ce12 = ce[5] + c12;
     ce22 = ce[8] + c22;
+    k_linear = (np_tot == 0);
     ++n_asm;
     __syncwarp();
+  };
+
+  // Factor K_aa. With no plastic point in the assembly K_aa == K_e exactly,
+  // whose factor was computed once on the host.
+  auto factor = [&]() -> bool {
+    if (k_linear) {
+      if (lane < n) {
+        for (int b = 0; b <= lane; ++b) sK[lane * LD + b] = M.Le[lane * LD + b];
+        sInv[lane] = M.LeInv[lane];
+      }
+      __syncwarp();
+      return true;
+    }
+    return warp_cholesky(sK, sInv, LD, n, lane);
   };
 
   // commit at (E, sAev): history of the plastic points, flags, b_p, s_p, α_c
@@ -609,15 +651,21 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       const bool real = q < M.K2;
       const double* Gq = Gb + lane * S;
       double e0 = 0.0, e1 = 0.0, e2 = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
+      {  // ε = G_q α with 128-bit shared loads (rows are 16-B aligned, S even)
+        const double2* g0v = reinterpret_cast<const double2*>(Gq);
+        const double2* g1v = reinterpret_cast<const double2*>(Gq + NP);
+        const double2* g2v = reinterpret_cast<const double2*>(Gq + 2 * NP);
+        const double2* av = reinterpret_cast<const double2*>(sAev);
 #pragma unroll 4
-      for (int a = 0; a < NP; a += 2) {
-        const double al = sAev[a], bl = sAev[a + 1];
-        e0 += Gq[a] * al;
-        e1 += Gq[NP + a] * al;
-        e2 += Gq[2 * NP + a] * al;
-        f0 += Gq[a + 1] * bl;
-        f1 += Gq[NP + a + 1] * bl;
-        f2 += Gq[2 * NP + a + 1] * bl;
+        for (int a = 0; a < NP / 2; ++a) {
+          const double2 al = av[a], x0 = g0v[a], x1 = g1v[a], x2 = g2v[a];
+          e0 += x0.x * al.x;
+          f0 += x0.y * al.y;
+          e1 += x1.x * al.x;
+          f1 += x1.y * al.y;
+          e2 += x2.x * al.x;
+          f2 += x2.y * al.y;
+        }
       }
       const MatOut o = update_material(mt, h0, h1, h2, h3, h4, E0 + (e0 + f0), E1 + (e1 + f1), E2 + (e2 + f2));
       const bool pl = real && o.plastic;
@@ -686,7 +734,6 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
     return pc;
   };
 
-  const int n = M.n;
   const NewtonCfg& cfg = A.cfg;
   constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
 
@@ -777,7 +824,7 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
             iters += it;
             const double target = fmin(1.0, done + frac);
             if (target >= 1.0 - 1e-12) {
-              if (!warp_cholesky(sK, sInv, LD, n, lane)) {
+              if (!factor()) {
                 err = kSolver;
                 write_fail(err, iters, rn);
                 action = 3;
@@ -855,7 +902,7 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
             break;
           }
           // Newton step: K Δα = -r
-          if (!warp_cholesky(sK, sInv, LD, n, lane)) {
+          if (!factor()) {
             err = kSolver;
             write_fail(err, iters, rn);
             action = 3;

@@ -23,7 +23,7 @@ struct PointState {
 struct ModelDev {
   int n;        // modes
   int NP;       // modes padded to a multiple of 8 (DMMA tile)
-  int S;        // doubles per cubature point in G2 (3*NP + 1, odd: bank-conflict free rows)
+  int S;        // doubles per cubature point in G2 (3*NP + 2: 16-B rows, conflict-free 128-bit lane loads)
   int K2;       // J2 cubature points
   int K2p;      // padded to a multiple of kQC
   int nchunks;  // K2p / kQC
@@ -31,7 +31,10 @@ struct ModelDev {
   const double* w2;       // [K2p]      cubature weights (0 on pads)
   const double* Ke;       // [NP][NP]   Σ_{all q} w G^T C_e G   (elastic predictor stiffness)
   const double* KaEe;     // [NP][3]    Σ_{all q} w G^T C_e
+  const double* Le;       // [NP][NP+1] Cholesky factor of K_e (lower), used when no point is plastic
+  const double* LeInv;    // [NP]       1 / diag(Le)
   double CEEe[9];         //            Σ_{all q} w C_e
+  double inv_denom;       // 1 / (3 mu + h) of the J2 material
   double volume;
   MatDev mat2;            // the (single) J2 material of the history-carrying points
 };

@@ -14,6 +14,7 @@ namespace fe2 {
 struct MatDev {
   int kind;  // 0 elastic, 1 J2 linear
   double lam, mu, sy0, h;
+  double inv_denom;  // 1 / (3 mu + h)
 };
 
 // Outputs of one update: condensed stress (3), symmetric condensed tangent
@@ -32,6 +33,7 @@ __host__ __device__ inline MatDev make_mat(int kind, double E, double nu, double
   m.mu = 0.5 * E / (1.0 + nu);
   m.sy0 = sy0;
   m.h = h;
+  m.inv_denom = 1.0 / (3.0 * m.mu + h);
   return m;
 }
 

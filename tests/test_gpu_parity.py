@@ -125,3 +125,63 @@ def test_config1_subset_parity():
     # pointwise relative error wherever the stress is not at rounding-noise level
     big = np.linalg.norm(o["sigma"], axis=2) > 1e-12
     assert rel_err(g["sigma"][big], o["sigma"][big]).max() < REL
+
+
+def run_gpu(m, E, opts=None, keep_flags=False):
+    eng = F.HyperRomEngine.from_model(m)
+    eng.alloc_points(E.shape[0], keep_flags=keep_flags)
+    outs = [eng.solve_increment(E[:, k], opts) for k in range(E.shape[1])]
+    return eng, {k: np.stack([o[k] for o in outs], axis=1) for k in outs[0]}
+
+
+def test_bisection_parity(cfg0):
+    """Load-step bisection (rve.hpp:473-478) on the device: with max_iter = 2
+    large plastic increments are halved; sub-steps commit inside the same
+    persistent launch. Iteration counts (all sub-steps) and responses match."""
+    m, E = cfg0
+    Eb = np.ascontiguousarray(E[:48, 4::5] * 1.6)  # 4 big increments
+    opts = F.NewtonOptions(1e-8, 2, 8)
+    _, g = run_gpu(m, Eb, opts)
+    o = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume).run(Eb, max_iter=2, max_bisections=8, threads=8)
+    assert (o["bisections"] > 0).sum() > 10
+    np.testing.assert_array_equal(g["status"], o["status"])
+    np.testing.assert_array_equal(g["iters"], o["iters"])
+    ok = o["status"] == 0
+    assert path_rel_err(g["sigma"], o["sigma"])[ok].max() < REL
+    assert rel_err(g["C"][ok].reshape(-1, 9), o["C"][ok].reshape(-1, 9)).max() < REL
+
+
+def test_failure_status_parity(cfg0):
+    """Exhausted bisections -> ErrorCode::solver (status 5), NaN response, and the
+    point stays failed for the rest of its path (run_trajectory throws)."""
+    m, E = cfg0
+    Eb = np.ascontiguousarray(E[:32, 4::5] * 1.6)
+    opts = F.NewtonOptions(1e-8, 1, 2)
+    _, g = run_gpu(m, Eb, opts)
+    o = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume).run(Eb, max_iter=1, max_bisections=2, threads=8)
+    assert (o["status"] == 5).any()
+    np.testing.assert_array_equal(g["status"], o["status"])
+    np.testing.assert_array_equal(np.isnan(g["sigma"]), np.isnan(o["sigma"]))
+
+
+def test_config1_full_size_properties_and_sampled_parity():
+    """BASELINE config 1 at full size (65,536 points x 50 increments, reversal
+    paths) on the device: every point converges; C_macro symmetric and
+    positive definite; a stride sample of 256 points matches the oracle
+    (iteration counts identical, Σ and C within 1e-10)."""
+    m = F.HyperRomModel(33, 24, 400, 0)
+    P = 65536
+    E = F.make_paths(1, 0, P, 50)
+    _, g = run_gpu(m, E)
+    assert (g["status"] == 0).all()
+    C = g["C"]
+    asym = np.abs(C - C.transpose(0, 1, 3, 2)).max(axis=(2, 3)) / np.abs(C).max(axis=(2, 3))
+    assert asym.max() < 1e-12
+    sample = np.arange(0, P, 256)
+    ev = np.linalg.eigvalsh(C[sample, ::7])
+    assert ev.min() > 0
+    o = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume).run(np.ascontiguousarray(E[sample]), threads=16)
+    np.testing.assert_array_equal(g["iters"][sample], o["iters"])
+    np.testing.assert_array_equal(g["plastic_count"][sample], o["plastic_count"])
+    assert path_rel_err(g["sigma"][sample], o["sigma"]).max() < REL
+    assert rel_err(C[sample].reshape(-1, 9), o["C"].reshape(-1, 9)).max() < REL
