@@ -1,0 +1,200 @@
+// fe2rom/hrom_gpu.hpp — header-only C++ mirror of the reference fe2rom
+// interface over the B200 C ABI (fe2rom_gpu.h). Eigen-free, so a caller of
+// /root/reference/proj/include/fe2rom can switch the per-macro-point RVE
+// solve to the GPU batch without other dependencies.
+//
+// Reference names kept (paths relative to /root/reference/proj/include/fe2rom/):
+//   ElasticParams, J2LinearParams, Material       materials.hpp:37-49, :78
+//   MaterialState (eps_p[4], eq, sigma33)          materials.hpp:102-106
+//   MicroOptions {tol, max_iter}                   rve.hpp:195-200
+//   TrajectoryOptions {micro, max_bisections}      rve.hpp:439-443
+//   HomogenizedResponse {sigma, tangent}           rve.hpp:37-40
+//   Error / ErrorCode                              common.hpp:26-52
+//   update_material (batched)                      materials.hpp:317-325
+// HyperRomBatch::solve_increment is run_trajectory's per-step body
+// (rve.hpp:459-491) — micro_newton + homogenize + commit — for a batch of
+// macro Gauss points with a hyper-reduced RVE model.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <variant>
+#include <vector>
+
+#include "fe2rom/fe2rom_gpu.h"
+
+namespace fe2rom::gpu {
+
+enum class ErrorCode { config, geometry, mesh, material, solver, numeric, rank, bc, io, provenance };
+
+class Error : public std::runtime_error {
+ public:
+  Error(ErrorCode c, const std::string& what) : std::runtime_error(what), code_(c) {}
+  ErrorCode code() const { return code_; }
+
+ private:
+  ErrorCode code_;
+};
+
+inline void check(int rc) {
+  if (rc != 0) throw Error(static_cast<ErrorCode>(rc - 1), fe2_last_error());
+}
+
+using Voigt3 = std::array<double, 3>;  // (e11, e22, g12) / (s11, s22, s12)
+using Mat3 = std::array<double, 9>;    // row-major
+
+struct ElasticParams {
+  double E = 1.0;
+  double nu = 0.3;
+};
+struct J2LinearParams {
+  ElasticParams elastic;
+  double sigma_y0 = 0.01;
+  double hardening = 0.016;
+};
+using Material = std::variant<ElasticParams, J2LinearParams>;
+
+struct MaterialState {
+  std::array<double, 4> eps_p{0, 0, 0, 0};
+  double eq = 0.0;
+  double sigma33 = 0.0;
+};
+
+struct MicroOptions {
+  double tol = 1e-8;
+  int max_iter = 30;
+};
+struct TrajectoryOptions {
+  MicroOptions micro;
+  int max_bisections = 4;
+};
+
+struct HomogenizedResponse {
+  Voigt3 sigma{};
+  Mat3 tangent{};
+  int iterations = 0;      // all Newton iterations of the increment
+  int plastic_points = 0;  // cubature points with f > 0 at the commit
+  double residual = 0.0;
+  int status = 0;          // 0 or 1 + ErrorCode
+};
+
+inline fe2_material_t to_c(const Material& m) {
+  fe2_material_t c{};
+  if (auto* e = std::get_if<ElasticParams>(&m)) {
+    c.kind = 0;
+    c.p[0] = e->E;
+    c.p[1] = e->nu;
+  } else {
+    const auto& j = std::get<J2LinearParams>(m);
+    c.kind = 1;
+    c.p[0] = j.elastic.E;
+    c.p[1] = j.elastic.nu;
+    c.p[2] = j.sigma_y0;
+    c.p[3] = j.hardening;
+  }
+  return c;
+}
+
+struct MaterialResult {
+  Voigt3 sigma{};
+  Mat3 tangent{};
+  MaterialState state;
+  bool plastic = false;
+};
+
+// Batched update_material on the device (materials.hpp:317-325).
+inline std::vector<MaterialResult> update_material(const Material& mat, const std::vector<MaterialState>& s0,
+                                                   const std::vector<Voigt3>& eps, int device = 0) {
+  const int64_t N = static_cast<int64_t>(eps.size());
+  std::vector<double> e(3 * N), st(6 * N), sig(3 * N), C(9 * N), so(6 * N);
+  std::vector<uint8_t> pl(N);
+  for (int64_t i = 0; i < N; ++i) {
+    for (int c = 0; c < 3; ++c) e[3 * i + c] = eps[i][c];
+    const MaterialState& s = s0.empty() ? MaterialState{} : s0[i];
+    for (int c = 0; c < 4; ++c) st[6 * i + c] = s.eps_p[c];
+    st[6 * i + 4] = s.eq;
+    st[6 * i + 5] = s.sigma33;
+  }
+  const fe2_material_t m = to_c(mat);
+  check(fe2_material_update_batch(device, &m, N, e.data(), st.data(), sig.data(), C.data(), so.data(), pl.data()));
+  std::vector<MaterialResult> out(N);
+  for (int64_t i = 0; i < N; ++i) {
+    for (int c = 0; c < 3; ++c) out[i].sigma[c] = sig[3 * i + c];
+    for (int c = 0; c < 9; ++c) out[i].tangent[c] = C[9 * i + c];
+    for (int c = 0; c < 4; ++c) out[i].state.eps_p[c] = so[6 * i + c];
+    out[i].state.eq = so[6 * i + 4];
+    out[i].state.sigma33 = so[6 * i + 5];
+    out[i].plastic = pl[i] != 0;
+  }
+  return out;
+}
+
+// A batch of macro Gauss points sharing one hyper-reduced RVE model on one
+// device: G[K][3][n] (G_q = B_q Φ), cubature weights, material per point.
+class HyperRomBatch {
+ public:
+  HyperRomBatch(int device, int n, int K, const std::vector<double>& G, const std::vector<double>& w,
+                const std::vector<int>& mat_id, const std::vector<Material>& materials, double volume)
+      : n_(n), K_(K) {
+    std::vector<fe2_material_t> mc;
+    for (const auto& m : materials) mc.push_back(to_c(m));
+    check(fe2_hrom_create(device, n, K, G.data(), w.data(), mat_id.data(), mc.data(), static_cast<int>(mc.size()),
+                          volume, &h_));
+  }
+  ~HyperRomBatch() { fe2_hrom_destroy(h_); }
+  HyperRomBatch(const HyperRomBatch&) = delete;
+  HyperRomBatch& operator=(const HyperRomBatch&) = delete;
+
+  // virgin states (std::vector<MaterialState>(n_ips), rve.hpp:450) for P points
+  void alloc_points(int64_t P, bool keep_flags = false) {
+    check(fe2_hrom_alloc_points(h_, P, keep_flags ? 1 : 0));
+    P_ = P;
+  }
+
+  // one path step for every point: E[p] is this increment's macro strain
+  std::vector<HomogenizedResponse> solve_increment(const std::vector<Voigt3>& E, const TrajectoryOptions& o = {}) {
+    if (static_cast<int64_t>(E.size()) != P_) throw Error(ErrorCode::config, "one macro strain per point");
+    std::vector<double> e(3 * P_), sig(3 * P_), C(9 * P_), res(P_);
+    std::vector<int> it(P_), pc(P_), st(P_);
+    for (int64_t p = 0; p < P_; ++p)
+      for (int c = 0; c < 3; ++c) e[3 * p + c] = E[p][c];
+    const fe2_newton_opts_t opts{o.micro.tol, o.micro.max_iter, o.max_bisections};
+    check(fe2_hrom_solve_increment(h_, e.data(), &opts, sig.data(), C.data(), it.data(), pc.data(), res.data(),
+                                   st.data()));
+    std::vector<HomogenizedResponse> out(P_);
+    for (int64_t p = 0; p < P_; ++p) {
+      for (int c = 0; c < 3; ++c) out[p].sigma[c] = sig[3 * p + c];
+      for (int c = 0; c < 9; ++c) out[p].tangent[c] = C[9 * p + c];
+      out[p].iterations = it[p];
+      out[p].plastic_points = pc[p];
+      out[p].residual = res[p];
+      out[p].status = st[p];
+    }
+    return out;
+  }
+
+  // committed MaterialState of every cubature point of point p
+  std::vector<MaterialState> states(int64_t p) const {
+    std::vector<double> a(static_cast<size_t>(P_) * n_), s(static_cast<size_t>(P_) * K_ * 6);
+    check(fe2_hrom_read_state(h_, a.data(), s.data(), nullptr));
+    std::vector<MaterialState> out(K_);
+    for (int q = 0; q < K_; ++q) {
+      const double* x = s.data() + (static_cast<size_t>(p) * K_ + q) * 6;
+      for (int c = 0; c < 4; ++c) out[q].eps_p[c] = x[c];
+      out[q].eq = x[4];
+      out[q].sigma33 = x[5];
+    }
+    return out;
+  }
+
+  fe2_hrom_t handle() const { return h_; }
+
+ private:
+  fe2_hrom_t h_ = nullptr;
+  int n_ = 0, K_ = 0;
+  int64_t P_ = 0;
+};
+
+}  // namespace fe2rom::gpu
