@@ -26,26 +26,33 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_native(force=False, verbose=False):
+def build_native(force=False, verbose=False, out=None, defines=()):
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "fe2rom", "fe2rom_gpu.h"))
     deps.append(os.path.abspath(__file__))
-    if not force and not _stale(LIB, deps):
-        return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    target = out or LIB
+    if not force and not _stale(target, deps):
+        return target
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-I", os.path.join(ROOT, "include"),
+           "-I", CSRC, "-o", target + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc build of libfe2rom_gpu.so failed")
-    with open(os.path.join(HERE, "lib", "ptxas.log"), "w") as f:
+    with open(target + ".ptxas.log", "w") as f:
         f.write(r.stdout + r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build_native(force="--force" in sys.argv, verbose=True))
+    # python build.py [--force] [--variant NAME D1=V1 D2=V2 ...]  (variants go to lib/variants/)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], sys.argv[i + 2:]
+        print(build_native(force=True, out=os.path.join(HERE, "lib", "variants", f"lib_{name}.so"), defines=defs))
+    else:
+        print(build_native(force="--force" in sys.argv, verbose=True))

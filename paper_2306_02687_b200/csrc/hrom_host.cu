@@ -410,21 +410,21 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
           const double v = 0.5 * (Ke[static_cast<size_t>(a) * NP + b] + Ke[static_cast<size_t>(b) * NP + a]);
           Ke[static_cast<size_t>(a) * NP + b] = Ke[static_cast<size_t>(b) * NP + a] = v;
         }
-      // Cholesky factor of K_e in the kernel's shared layout [NP][NP+1]: the
-      // device reuses it whenever an assembly has no plastic point.
-      const int LD = NP + 1;
-      std::vector<double> Le(static_cast<size_t>(NP) * LD, 0.0), LeInv(NP, 0.0);
+      // Cholesky factor of K_e in the kernel's packed-lower layout (row i at
+      // i(i+1)/2): the device reuses it whenever an assembly has no plastic point.
+      auto tri = [](int i) { return i * (i + 1) / 2; };
+      std::vector<double> Le(static_cast<size_t>(tri(NP)), 0.0), LeInv(NP, 0.0);
       for (int j = 0; j < n; ++j) {
         double d = Ke[static_cast<size_t>(j) * NP + j];
-        for (int k = 0; k < j; ++k) d -= Le[j * LD + k] * Le[j * LD + k];
+        for (int k = 0; k < j; ++k) d -= Le[tri(j) + k] * Le[tri(j) + k];
         check(d > 0.0, Code::solver, "elastic reduced stiffness K_e is not positive definite");
         const double ljj = std::sqrt(d);
-        Le[j * LD + j] = ljj;
+        Le[tri(j) + j] = ljj;
         LeInv[j] = 1.0 / ljj;
         for (int i = j + 1; i < n; ++i) {
           double s = Ke[static_cast<size_t>(i) * NP + j];
-          for (int k = 0; k < j; ++k) s -= Le[i * LD + k] * Le[j * LD + k];
-          Le[i * LD + j] = s / ljj;
+          for (int k = 0; k < j; ++k) s -= Le[tri(i) + k] * Le[tri(j) + k];
+          Le[tri(i) + j] = s / ljj;
         }
       }
       h->Le = dalloc<double>(Le.size());
@@ -559,7 +559,9 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
       std::vector<double> hs(static_cast<size_t>(P) * K2p * 5), Ec(static_cast<size_t>(P) * 3);
       CK(cudaMemcpy(hs.data(), h->hist, hs.size() * sizeof(double), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(Ec.data(), h->E_c, Ec.size() * sizeof(double), cudaMemcpyDeviceToHost));
-      const size_t PK = static_cast<size_t>(P) * K2p;
+      auto hidx = [&](int64_t p, int q2, int comp) {  // [P][K2p/32][5][32]
+        return (static_cast<size_t>(p) * (K2p / kQC) + q2 / kQC) * (5 * kQC) + comp * kQC + q2 % kQC;
+      };
       for (int64_t p = 0; p < P; ++p) {
         // sigma33 is write-only in the reference (materials.hpp:181, :193): it is
         // not kept in HBM but recomputed here from the committed strain and eps_p,
@@ -573,7 +575,7 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
         for (int q2 = 0; q2 < h->K2; ++q2) {
           const int q = h->j2_idx[q2];
           double* s = state + (static_cast<size_t>(p) * K + q) * 6;
-          for (int c = 0; c < 5; ++c) s[c] = hs[c * PK + static_cast<size_t>(p) * K2p + q2];
+          for (int c = 0; c < 5; ++c) s[c] = hs[hidx(p, q2, c)];
           const MatDev& m = h->mat2;
           const Eps3 e = strain_at(h, p, q, ac.data(), Ec.data());
           s[5] = m.lam * ((e.v[0] - s[0]) + (e.v[1] - s[1]) + (0.0 - s[2])) + 2.0 * m.mu * (0.0 - s[2]);

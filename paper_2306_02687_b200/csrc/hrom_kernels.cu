@@ -120,14 +120,16 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   return y * fma(-hx * y, y, 1.5);
 }
 
-// Left-looking Cholesky of the lower triangle of sK (row stride ld) in place;
-// lane i owns row i (n <= 32). sInv[j] = 1 / L_jj. False if not SPD.
-__device__ bool warp_cholesky(double* sK, double* sInv, int ld, int n, int lane) {
+__device__ __forceinline__ int tri_(int i) { return i * (i + 1) / 2; }
+
+// Left-looking Cholesky of the packed lower triangle sK (row i at i(i+1)/2)
+// in place; lane i owns row i (n <= 32). sInv[j] = 1 / L_jj. False if not SPD.
+__device__ bool warp_cholesky(double* sK, double* sInv, int n, int lane) {
   for (int j = 0; j < n; ++j) {
     double s = 0.0;
     if (lane >= j && lane < n) {
-      const double* ri = sK + lane * ld;
-      const double* rj = sK + j * ld;
+      const double* ri = sK + tri_(lane);
+      const double* rj = sK + tri_(j);
       double a0 = 0.0, a1 = 0.0;
       int k = 0;
       for (; k + 1 < j; k += 2) {
@@ -142,28 +144,29 @@ __device__ bool warp_cholesky(double* sK, double* sInv, int ld, int n, int lane)
     const double inv = rsqrt_fast(d);
     const double ljj = d * inv;
     if (lane == j) {
-      sK[j * ld + j] = ljj;
+      sK[tri_(j) + j] = ljj;
       sInv[j] = inv;
     } else if (lane > j && lane < n) {
-      sK[lane * ld + j] = s * inv;
+      sK[tri_(lane) + j] = s * inv;
     }
     __syncwarp();
   }
   return true;
 }
 
-// Solve L L^T x = b; lane i holds b_i in, x_i out (n <= 32).
-__device__ double warp_chol_solve(const double* sK, const double* sInv, int ld, int n, int lane, double b) {
+// Solve L L^T x = b (packed L); lane i holds b_i in, x_i out (n <= 32).
+__device__ double warp_chol_solve(const double* sK, const double* sInv, int n, int lane, double b) {
   double x = b;
+  const double* ri = sK + tri_(lane < n ? lane : 0);
   for (int j = 0; j < n; ++j) {
     const double yj = __shfl_sync(0xffffffffu, x, j) * sInv[j];
     if (lane == j) x = yj;
-    if (lane > j && lane < n) x -= sK[lane * ld + j] * yj;
+    if (lane > j && lane < n) x -= ri[j] * yj;
   }
   for (int j = n - 1; j >= 0; --j) {
     const double xj = __shfl_sync(0xffffffffu, x, j) * sInv[j];
     if (lane == j) x = xj;
-    if (lane < j) x -= sK[j * ld + lane] * xj;
+    if (lane < j) x -= sK[tri_(j) + lane] * xj;
   }
   return x;
 }
@@ -226,19 +229,35 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
   return c;
 }
 
-constexpr int kW = 8;       // warps per CTA
-constexpr int kStages = 3;  // G-chunk ring depth
+#ifndef FE2_KW
+#define FE2_KW 16
+#endif
+#ifndef FE2_STAGES
+#define FE2_STAGES 6
+#endif
+#ifndef FE2_MINB
+#define FE2_MINB 1
+#endif
+constexpr int kW = FE2_KW;            // warps per CTA
+constexpr int kStages = FE2_STAGES;   // G-chunk ring depth (shared by the CTA)
+constexpr int kHS = 2;      // per-warp history ring depth (TMA, 5 x 256 B per stage)
+
+__device__ __forceinline__ int tri(int i) { return i * (i + 1) / 2; }  // packed lower row offset
 
 template <int NP>
 struct IncLayout {
   static constexpr int S = 3 * NP + 2;
   static constexpr int chunk = kQC * S;                      // doubles per ring stage
-  static constexpr int kSlots = kQC * 9 + kQC * 3 + kQC;     // ΔC rows, Δσ, point index
-  static constexpr int kUnion = (kSlots > NP * (NP + 1)) ? kSlots : NP * (NP + 1);
-  static constexpr int WS = 5 * NP + 3 * NP + kUnion;        // per-warp scratch (doubles)
+  static constexpr int kSlots = kQC * 6 + kQC * 3 + kQC;     // w ΔC (6 unique), w Δσ, point index
+  static constexpr int kTri = NP * (NP + 1) / 2;              // packed lower K_aa
+  static constexpr int kUnion = (kSlots > kTri) ? kSlots : kTri;
+  static constexpr int kHist = kHS * 5 * kQC;                 // per-warp history ring (TMA)
+  static constexpr int WS = 5 * NP + 3 * NP + kUnion + kHist;  // per-warp scratch (doubles)
   static constexpr size_t ring_bytes = static_cast<size_t>(kStages) * chunk * sizeof(double);
-  // control block: full[kStages] (u64) | cnt[kStages] (int) | ctrl (u64 at +kCtrlOff)
-  static constexpr int kCtrlOff = ((kStages * 8 + kStages * 4 + 7) / 8) * 8;
+  // control block: full[kStages] (u64) | hbar[kW][kHS] (u64) | cnt[kStages] (int) | ctrl (u64)
+  static constexpr int kHbarOff = kStages * 8;
+  static constexpr int kCntOff = kHbarOff + kW * kHS * 8;
+  static constexpr int kCtrlOff = ((kCntOff + kStages * 4 + 7) / 8) * 8;
   static constexpr size_t bytes = ring_bytes + static_cast<size_t>(kW) * WS * sizeof(double) + kCtrlOff + 8;
 };
 
@@ -331,7 +350,7 @@ __device__ void ring_drain(const Ring& R, int seq, int lane) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
+__global__ void __launch_bounds__(kW * 32, FE2_MINB) k_increment(IncArgs A) {
   constexpr int NP = 8 * NT;
   constexpr int NTP = NT * (NT + 1) / 2;
   using L = IncLayout<NP>;
@@ -343,7 +362,8 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
   double* wbase = reinterpret_cast<double*>(smem_raw + L::ring_bytes) + static_cast<size_t>(warp) * L::WS;
   unsigned char* ctrl_base = smem_raw + L::ring_bytes + static_cast<size_t>(kW) * L::WS * sizeof(double);
   uint64_t* full = reinterpret_cast<uint64_t*>(ctrl_base);
-  int* cnt = reinterpret_cast<int*>(ctrl_base + kStages * sizeof(uint64_t));
+  uint64_t* hbar = reinterpret_cast<uint64_t*>(ctrl_base + L::kHbarOff) + warp * kHS;
+  int* cnt = reinterpret_cast<int*>(ctrl_base + L::kCntOff);
   unsigned long long* ctrl = reinterpret_cast<unsigned long long*>(ctrl_base + L::kCtrlOff);
 
   double* sAev = wbase;          // α at the evaluation point
@@ -353,10 +373,11 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
   double* sInv = sV + NP;        // 1 / L_jj
   double* sKaE = sInv + NP;      // K_aE [NP][3]
   double* sU = sKaE + 3 * NP;
-  double* sDC = sU;                                 // [32][9] w ΔC rows of the plastic slots
-  double* sDS = sU + kQC * 9;                       // [32][3] w Δσ (commit pass: w S(Δεp))
-  int* sQ = reinterpret_cast<int*>(sU + kQC * 12);  // [32]    chunk-local cubature index
-  double* sK = sU;                                  // K_aa lower [NP][NP+1] (after an assembly pass)
+  double* sDC = sU;                                 // [32][6] w ΔC (00 01 02 11 12 22) of the plastic slots
+  double* sDS = sU + kQC * 6;                       // [32][3] w Δσ (commit pass: w S(Δεp))
+  int* sQ = reinterpret_cast<int*>(sU + kQC * 9);   // [32]    chunk-local cubature index
+  double* sK = sU;                                  // K_aa packed lower (after an assembly pass)
+  double* hb = sU + L::kUnion;                      // [kHS][5][32] history stages
 
   const ModelDev& M = A.M;
   const PointsDev& D = A.D;
@@ -371,8 +392,10 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       cnt[s] = 0;
     }
     *ctrl = (static_cast<unsigned long long>(kW) << 32) | static_cast<unsigned long long>(kStages);
-    fence_mbar_init();
   }
+  if (lane == 0)
+    for (int s = 0; s < kHS; ++s) mbar_init(&hbar[s], 1);
+  if (lane == 0) fence_mbar_init();
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t bytes = static_cast<uint32_t>(L::chunk * sizeof(double));
@@ -383,7 +406,6 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
     }
   }
 
-  const int64_t PK = D.P * static_cast<int64_t>(M.K2p);
   const int m = lane & 3, col = lane >> 2;
   int qo[3], io[3];
 #pragma unroll
@@ -399,8 +421,58 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
   bool k_linear = false;  // the last assembly had no plastic point (K_aa == K_e)
   const int n = M.n;
 
+  // ------------------------------------------------ per-warp history stream
+  // (point, chunk) items of εp(4), eq arrive by TMA bulk copies into kHS
+  // shared stages. Within a pass the next chunks are in flight while the
+  // current one computes; the first chunks of the predicted next pass (same
+  // point after an assembly, next point after the final commit) are issued
+  // at the end of a pass, so they load during the Newton / Cholesky phase.
+  int h_iss = 0, h_con = 0;  // positions issued / consumed
+  int64_t pf_p = -1;         // point of the prefetched next-pass items
+  int pf_n = 0;              // how many of its first chunks are in flight
+  const int h_first = nch < kHS ? nch : kHS;
+  auto h_issue = [&](int64_t p, int c) {
+    const int s = h_iss % kHS;
+    if (lane == 0) {
+      fence_proxy_async();  // the stage's previous generic reads precede the async writes
+      mbar_expect_tx(&hbar[s], 5 * kQC * sizeof(double));
+      tma_load_1d(hb + s * 5 * kQC, D.hist + (p * nch + c) * (5 * kQC), 5 * kQC * sizeof(double), &hbar[s]);
+    }
+    ++h_iss;
+  };
+  auto h_take = [&]() -> const double* {
+    const int s = h_con % kHS;
+    mbar_wait(&hbar[s], static_cast<uint32_t>((h_con / kHS) & 1));
+    ++h_con;
+    return hb + s * 5 * kQC;
+  };
+  auto h_begin = [&](int64_t p, bool after_write) {
+    if (pf_p != p) {  // discard prefetches made for another point
+      while (h_con < h_iss) h_take();
+      __syncwarp();
+      pf_n = 0;
+    }
+    if (after_write && pf_n == 0) {  // this warp's history stores -> async-proxy reads
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
+    }
+    for (int c = pf_n; c < h_first; ++c) h_issue(p, c);
+    pf_p = -1;
+    pf_n = 0;
+  };
+  auto h_next = [&](int64_t p, int c, int64_t pred) {  // after consuming chunk c of point p
+    const int nc = c + kHS;
+    if (nc < nch) {
+      h_issue(p, nc);
+    } else if (pred >= 0 && nc - nch < h_first && pf_n == nc - nch && (pf_p == pred || pf_n == 0)) {
+      h_issue(pred, nc - nch);
+      pf_p = pred;
+      ++pf_n;
+    }
+  };
+
   // ---------------------------------------------------------------- passes
-  auto assembly_pass = [&](int64_t p, double E0, double E1, double E2) {
+  auto assembly_pass = [&](int64_t p, double E0, double E1, double E2, int64_t pred, bool after_write) {
     double acc[NTP][2];
     double kae[NT][3];
     double rr[NT];
@@ -413,10 +485,19 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
     }
     double c00 = 0.0, c01 = 0.0, c02 = 0.0, c11 = 0.0, c12 = 0.0, c22 = 0.0, ds0 = 0.0, ds1 = 0.0, ds2 = 0.0;
     int np_tot = 0;
-    const double* H0 = D.hist + p * M.K2p;
-    double h0 = H0[lane], h1 = H0[PK + lane], h2 = H0[2 * PK + lane], h3 = H0[3 * PK + lane],
-           h4 = H0[4 * PK + lane];
+    h_begin(p, after_write);
     for (int c = 0; c < nch; ++c) {
+      double h0, h1, h2, h3, h4;
+      {
+        const double* Hs = h_take();
+        h0 = Hs[lane];
+        h1 = Hs[kQC + lane];
+        h2 = Hs[2 * kQC + lane];
+        h3 = Hs[3 * kQC + lane];
+        h4 = Hs[4 * kQC + lane];
+        __syncwarp();
+        h_next(p, c, pred);
+      }
       const double* Gb = ring_wait(R, seq);
       const int q = c * kQC + lane;
       // lane = cubature point: strain, elastic trial, yield test
@@ -450,16 +531,13 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
         const int slot = __popc(bal & ((1u << lane) - 1u));
         const double w00 = wq * cr.dc00, w01 = wq * cr.dc01, w02 = wq * cr.dc02;
         const double w11 = wq * cr.dc11, w12 = wq * cr.dc12, w22 = wq * cr.dc22;
-        double* dc = sDC + slot * 9;
+        double* dc = sDC + slot * 6;
         dc[0] = w00;
         dc[1] = w01;
         dc[2] = w02;
-        dc[3] = w01;
-        dc[4] = w11;
-        dc[5] = w12;
-        dc[6] = w02;
-        dc[7] = w12;
-        dc[8] = w22;
+        dc[3] = w11;
+        dc[4] = w12;
+        dc[5] = w22;
         const double g0 = wq * cr.ds0, g1 = wq * cr.ds1, g2 = wq * cr.ds2;
         sDS[slot * 3 + 0] = g0;
         sDS[slot * 3 + 1] = g1;
@@ -478,17 +556,9 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       const int np4 = (np + 3) & ~3;  // zero the slots that round np up to a multiple of 4
       if (lane >= np && lane < np4) {
 #pragma unroll
-        for (int e = 0; e < 9; ++e) sDC[lane * 9 + e] = 0.0;
+        for (int e = 0; e < 6; ++e) sDC[lane * 6 + e] = 0.0;
         sDS[lane * 3 + 0] = sDS[lane * 3 + 1] = sDS[lane * 3 + 2] = 0.0;
         sQ[lane] = 0;
-      }
-      if (c + 1 < nch) {  // prefetch the next chunk's history
-        const int qn = q + kQC;
-        h0 = H0[qn];
-        h1 = H0[PK + qn];
-        h2 = H0[2 * PK + qn];
-        h3 = H0[3 * PK + qn];
-        h4 = H0[4 * PK + qn];
       }
       __syncwarp();
       // plastic contraction on DMMA: k = 3 slot + i, four k per k-step
@@ -499,8 +569,10 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
         for (int s = 0; s < 3; ++s) {
           const int slot = 4 * g + qo[s];
           const int i = io[s];
-          const double* wc = sDC + slot * 9 + i * 3;
-          const double k0 = wc[0], k1 = wc[1], k2 = wc[2];
+          // row i of the symmetric w ΔC from its 6 unique entries (00 01 02 11 12 22)
+          const int b = i > 0 ? 1 : 0;
+          const double* wc = sDC + slot * 6;
+          const double k0 = wc[i], k1 = wc[i + 1 + b], k2 = wc[i + 2 + b];
           const double ws = sDS[slot * 3 + i];
           const double* gp = Gb + sQ[slot] * S + col;
           double Af[NT], Bf[NT];
@@ -560,9 +632,9 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
           for (int e = 0; e < 2; ++e) {
             const int row = t1 * 8 + r_, cl = t2 * 8 + c_ + e;
             if (t1 < t2)
-              sK[cl * LD + row] = acc[ti][e];
+              sK[tri_(cl) + row] = acc[ti][e];
             else if (row >= cl)
-              sK[row * LD + cl] = acc[ti][e];
+              sK[tri_(row) + cl] = acc[ti][e];
           }
           ++ti;
         }
@@ -583,18 +655,19 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       const int a = lane;
       const double* ke = M.KaEe + a * 3;
       double sx = 0.0, sy = 0.0;
+      double* ka = sK + tri_(a);
       int b = 0;
       for (; b + 1 < n; b += 2) {
         const double k0 = M.Ke[b * NP + a], k1 = M.Ke[(b + 1) * NP + a];  // symmetric: coalesced reads
         sx += k0 * sAev[b];
         sy += k1 * sAev[b + 1];
-        if (b <= a) sK[a * LD + b] += k0;
-        if (b + 1 <= a) sK[a * LD + b + 1] += k1;
+        if (b <= a) ka[b] += k0;
+        if (b + 1 <= a) ka[b + 1] += k1;
       }
       if (b < n) {
         const double k0 = M.Ke[b * NP + a];
         sx += k0 * sAev[b];
-        if (b <= a) sK[a * LD + b] += k0;
+        if (b <= a) ka[b] += k0;
       }
       const double sr = (sx + sy) + (ke[0] * E0 + ke[1] * E1 + ke[2] * E2);
       sV[a] += sr - D.bp[p * NP + a];
@@ -628,24 +701,31 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
   // whose factor was computed once on the host.
   auto factor = [&]() -> bool {
     if (k_linear) {
-      if (lane < n) {
-        for (int b = 0; b <= lane; ++b) sK[lane * LD + b] = M.Le[lane * LD + b];
-        sInv[lane] = M.LeInv[lane];
-      }
+      for (int e = lane; e < tri_(n); e += 32) sK[e] = M.Le[e];  // packed lower, coalesced
+      if (lane < n) sInv[lane] = M.LeInv[lane];
       __syncwarp();
       return true;
     }
-    return warp_cholesky(sK, sInv, LD, n, lane);
+    return warp_cholesky(sK, sInv, n, lane);
   };
 
   // commit at (E, sAev): history of the plastic points, flags, b_p, s_p, α_c
-  auto commit_pass = [&](int64_t p, double E0, double E1, double E2) -> int {
-    const double* H0 = D.hist + p * M.K2p;
-    double h0 = H0[lane], h1 = H0[PK + lane], h2 = H0[2 * PK + lane], h3 = H0[3 * PK + lane],
-           h4 = H0[4 * PK + lane];
+  auto commit_pass = [&](int64_t p, double E0, double E1, double E2, int64_t pred) -> int {
     double bacc = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
     int pc = 0;
+    h_begin(p, false);
     for (int c = 0; c < nch; ++c) {
+      double h0, h1, h2, h3, h4;
+      {
+        const double* Hs = h_take();
+        h0 = Hs[lane];
+        h1 = Hs[kQC + lane];
+        h2 = Hs[2 * kQC + lane];
+        h3 = Hs[3 * kQC + lane];
+        h4 = Hs[4 * kQC + lane];
+        __syncwarp();
+        h_next(p, c, pred);
+      }
       const double* Gb = ring_wait(R, seq);
       const int q = c * kQC + lane;
       const bool real = q < M.K2;
@@ -677,20 +757,13 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
         w1 = wq * (lt + 2.0 * mt.mu * x1);
         w2 = wq * (2.0 * mt.mu * x3);
       }
-      double* H = D.hist + p * M.K2p + q;
-      if (c + 1 < nch) {  // prefetch the next chunk
-        h0 = H[kQC];
-        h1 = H[PK + kQC];
-        h2 = H[2 * PK + kQC];
-        h3 = H[3 * PK + kQC];
-        h4 = H[4 * PK + kQC];
-      }
+      double* H = D.hist + (p * nch + c) * (5 * kQC) + lane;
       if (pl) {  // elastic points keep their history bit for bit (elastic_result, materials.hpp:187-195)
         H[0] = o.ep0;
-        H[PK] = o.ep1;
-        H[2 * PK] = o.ep2;
-        H[3 * PK] = o.ep3;
-        H[4 * PK] = o.eq;
+        H[kQC] = o.ep1;
+        H[2 * kQC] = o.ep2;
+        H[3 * kQC] = o.ep3;
+        H[4 * kQC] = o.eq;
       }
       if (D.flags && real) D.flags[p * M.K2p + q] = o.plastic ? 1 : 0;
       t0 += w0;
@@ -742,12 +815,12 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       const int64_t p = A.dbg_point;
       for (int a = lane; a < NP; a += 32) sAev[a] = (a < n) ? A.dbg_alpha[a] : 0.0;
       __syncwarp();
-      assembly_pass(p, A.dbg_E[0], A.dbg_E[1], A.dbg_E[2]);
+      assembly_pass(p, A.dbg_E[0], A.dbg_E[1], A.dbg_E[2], -1, false);
       double* o = A.dbg;
       for (int a = lane; a < n; a += 32) o[a] = sV[a];
       for (int e = lane; e < n * n; e += 32) {
         const int i = e / n, j = e % n;
-        o[n + e] = (j <= i) ? sK[i * LD + j] : sK[j * LD + i];
+        o[n + e] = (j <= i) ? sK[tri_(i) + j] : sK[tri_(j) + i];
       }
       for (int e = lane; e < 3 * n; e += 32) o[n + n * n + e] = sKaE[e];
       if (lane == 0) {
@@ -766,17 +839,21 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
         cc[11] = s2;
       }
     }
+    while (h_con < h_iss) h_take();
     ring_drain(R, seq, lane);
     return;
   }
 
   // ------------------------------------------------------------ point loop
-  while (true) {
-    int pi = 0;
-    if (lane == 0) pi = atomicAdd(A.work, 1);
-    pi = __shfl_sync(0xffffffffu, pi, 0);
-    if (pi >= D.P) break;
-    const int64_t p = pi;
+  auto grab = [&]() -> int64_t {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(A.work, 1);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  int64_t p_next = grab();
+  while (p_next < D.P) {
+    const int64_t p = p_next;
+    p_next = -1;
     const double Ep0 = D.E_c[p * 3 + 0], Ep1 = D.E_c[p * 3 + 1], Ep2 = D.E_c[p * 3 + 2];
     const double Et0 = A.dE[p * 3 + 0], Et1 = A.dE[p * 3 + 1], Et2 = A.dE[p * 3 + 2];
     const int dead = D.st[p].err;
@@ -797,8 +874,10 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
         D.E_c[p * 3 + 1] = Et1;
         D.E_c[p * 3 + 2] = Et2;
       }
+      p_next = grab();
       continue;
     }
+    bool after_write = false;  // the previous pass (a sub-step commit) wrote this point's history
     // warm start α = α_committed, E = E_prev + (E_k - E_prev) * 1 (rve.hpp:465-472)
     for (int a = lane; a < NP; a += 32) {
       const double ac = D.alpha_c[p * NP + a];
@@ -811,7 +890,8 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
     double a = 1.0, rn_it = 0.0, best_rn = 0.0, best_a = 1.0, ref = 0.0, done = 0.0, frac = 1.0;
     int err = 0;
     while (true) {
-      assembly_pass(p, E0, E1, E2);
+      assembly_pass(p, E0, E1, E2, p, after_write);
+      after_write = false;
       const double rl = (lane < n) ? sV[lane] : 0.0;
       const double rn = sqrt(warp_sum(rl * rl));
       const double srn = sqrt(s0 * s0 + s1 * s1 + s2 * s2);
@@ -844,7 +924,7 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
                   x1 = y1;
                   x2 = y2;
                 } else if (lane > j && lane < n) {
-                  const double l = sK[lane * LD + j];
+                  const double l = sK[tri_(lane) + j];
                   x0 -= l * y0;
                   x1 -= l * y1;
                   x2 -= l * y2;
@@ -908,7 +988,7 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
             action = 3;
             break;
           }
-          const double du = warp_chol_solve(sK, sInv, LD, n, lane, -rl);
+          const double du = warp_chol_solve(sK, sInv, n, lane, -rl);
           if (lane < NP) {
             sDA[lane] = (lane < n) ? du : 0.0;
             sAev[lane] = (lane < n) ? axpy_rn(sAl[lane], 1.0, du) : 0.0;
@@ -954,12 +1034,15 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       __syncwarp();
       if (action == 0) continue;
       if (action == 3) break;
-      const int pc = commit_pass(p, E0, E1, E2);
-      if (action == 1) {
+      if (action == 1) {  // final commit; the next point's first chunks load behind it
+        p_next = grab();
+        const int pc = commit_pass(p, E0, E1, E2, p_next < D.P ? p_next : -1);
         if (lane == 0 && A.O.pcount) A.O.pcount[p] = pc;
         break;
       }
-      // converged sub-step: the next one starts from the new committed state
+      // converged sub-step: commit, the next one starts from the new committed state
+      commit_pass(p, E0, E1, E2, -1);
+      after_write = true;
       const double nt = fmin(1.0, done + frac);
       E0 = lerp_rn(Ep0, Et0, nt);
       E1 = lerp_rn(Ep1, Et1, nt);
@@ -975,7 +1058,9 @@ __global__ void __launch_bounds__(kW * 32, 2) k_increment(IncArgs A) {
       D.E_c[p * 3 + 1] = Et1;
       D.E_c[p * 3 + 2] = Et2;
     }
+    if (p_next < 0) p_next = grab();
   }
+  while (h_con < h_iss) h_take();  // no TMA may be in flight at exit
   ring_drain(R, seq, lane);
   if (A.cnt && lane == 0) {
     atomicAdd(&A.cnt->assemblies, n_asm);

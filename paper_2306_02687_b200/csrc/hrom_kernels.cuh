@@ -41,7 +41,9 @@ struct ModelDev {
 
 struct PointsDev {
   int64_t P;
-  double* hist;     // 5 SoA components [5][P][K2p]: eps_p(4), eq (sigma33 is recomputed on readback)
+  double* hist;     // [P][K2p/32][5][32]: per (point, 32-point chunk) one 1,280-B block of SoA
+                    // eps_p(4), eq — one bulk copy per chunk, coalesced lane stores
+                    // (sigma33 is write-only in the reference and recomputed on readback)
   double* alpha_c;  // [P][NP] committed reduced coordinates
   double* E_c;      // [P][3]  committed macro strain (= previous path point)
   double* bp;       // [P][NP] Σ_{J2 q} w G_q^T S(eps_p,q)  (committed plastic-strain load)

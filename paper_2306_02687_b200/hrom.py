@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfe2rom_gpu.so")
+LIB_PATH = os.environ.get("FE2_LIB") or os.path.join(_HERE, "lib", "libfe2rom_gpu.so")
 
 ERROR_CODES = ["config", "geometry", "mesh", "material", "solver", "numeric", "rank", "bc", "io", "provenance"]
 
