@@ -180,6 +180,13 @@ struct fe2_hrom_s {
 
 namespace {
 
+void launch_any(const IncArgs& a, int num_sms, cudaStream_t s) {
+  if (a.M.NP <= 32)
+    launch_increment(a, num_sms, s);
+  else
+    check(launch_increment_big(a, num_sms, s), Code::config, "unsupported mode count");
+}
+
 struct Eps3 {
   double v[3];
 };
@@ -265,7 +272,7 @@ void run_increment(fe2_hrom_t h, const double* d_E, const NewtonCfg& cfg, const 
   Watchdog wd(h->num_sms);
   a.trace = wd.dev;
   if (h->timing) CK(cudaEventRecord(h->ev[0], s));
-  launch_increment(a, h->num_sms, s);
+  launch_any(a, h->num_sms, s);
   CK(cudaGetLastError());
   if (h->timing) CK(cudaEventRecord(h->ev[1], s));
   wd.wait(s, "k_increment");
@@ -338,7 +345,7 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
     check(out != nullptr, Code::config, "null output handle");
     *out = nullptr;
     check(n >= 1 && K >= 1 && G && w && mat_id && mats && n_mats >= 1, Code::config, "bad model arguments");
-    check(n <= 32, Code::config, "this build supports n <= 32 modes");
+    check(n <= 128, Code::config, "this build supports n <= 128 modes");
     check(volume > 0.0, Code::config, "RVE volume must be positive");
     std::vector<MatDev> md;
     for (int i = 0; i < n_mats; ++i) md.push_back(to_dev(mats[i]));
@@ -348,7 +355,10 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
       h->device = device;
       CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
       h->n = n;
+      // DMMA tiles of 8; the one-CTA-per-point path uses 16-point chunks above
+      // 64 modes, whose mode split needs NP a multiple of 16
       h->NP = (n + 7) / 8 * 8;
+      if (h->NP > 64) h->NP = (n + 15) / 16 * 16;
       h->S = 3 * h->NP + 2;
       h->K = K;
       h->volume = volume;
@@ -616,7 +626,7 @@ int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, co
     a.dbg_point = point;
     Watchdog wd(h->num_sms);
     a.trace = wd.dev;
-    launch_increment(a, h->num_sms, s);
+    launch_any(a, h->num_sms, s);
     h->stats.kernel_launches += 1;
     CK(cudaGetLastError());
     wd.wait(s, "k_increment (assembly dump)");

@@ -94,8 +94,11 @@ struct IncArgs {
   volatile int* trace;
 };
 
-// host launchers (hrom_kernels.cu)
+// host launchers (hrom_kernels.cu: NP <= 32, one warp per point;
+// hrom_kernels_big.cu: NP in {40,48,56,64,80,96,112,128}, one CTA per point)
 void launch_increment(const IncArgs& a, int num_sms, cudaStream_t s);
+bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s);
+size_t increment_big_smem(int NP);
 void launch_material_batch(const MatDev& m, int64_t N, const double* eps, const double* st_in, double* sigma,
                            double* C, double* st_out, uint8_t* plastic, cudaStream_t s);
 size_t increment_smem(int NP);

@@ -1,0 +1,850 @@
+// B200 (sm_100a) persistent increment kernel for LARGE reduced bases
+// (n = 33…128, BASELINE configs 3 and 4): one CTA of 8 warps per macro point.
+//
+// Same algebra and same increment/Newton semantics as k_increment
+// (hrom_kernels.cu), re-tiled for n > 32:
+//  - G chunks (QB = 32 or 16 cubature points) stream through a 2-stage
+//    shared ring by TMA bulk copies; the CTA walks them in lockstep.
+//  - Material phase: TPQ = 256/QB threads per cubature point split the modes
+//    of ε_q = E + G_q α and reduce with shuffles; one lane runs the elastic
+//    trial / yield test / radial return.
+//  - Plastic points of a chunk are compacted CTA-wide (ballot + warp prefix,
+//    deterministic order) and contracted on the FP64 tensor cores (DMMA):
+//    the NT(NT+1)/2 upper tile pairs of K_aa are split over the 8 warps in
+//    2x2 / 4x4 tile blocks so each warp loads few distinct fragments; the
+//    K_aE and r corrections are scalar (O(n) per point).
+//  - Newton / line search / bisection / condensation run CTA-wide:
+//    left-looking Cholesky of the packed K_aa with one row per thread.
+#include "device_common.cuh"
+#include "hrom_kernels.cuh"
+
+namespace fe2 {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kBW = 8;         // warps per CTA
+constexpr int kBT = kBW * 32;  // threads per CTA
+
+template <int NT>
+struct Big {
+  static constexpr int NP = 8 * NT;
+  static constexpr int QB = (NP <= 64) ? 32 : 16;  // cubature points per chunk
+  static constexpr int TPQ = kBT / QB;             // threads per cubature point (8 | 16)
+  static constexpr int S = 3 * NP + 2;
+  static constexpr int chunk = QB * S;
+  static constexpr int TRI = NP * (NP + 1) / 2;
+  static constexpr int RED = 64;
+  // doubles: ring[2][chunk] | sK[TRI] | vectors 8 NP | slots QB*(6+3) + QB ints | red
+  static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + TRI + 8 * NP + QB * 10 + RED;
+  static constexpr size_t bytes = dbl * sizeof(double) + 2 * sizeof(uint64_t) + 16 * sizeof(int);
+};
+
+// Tile pairs (t1 <= t2) of one warp: upper-triangle tile blocks of size b,
+// dealt round-robin to the 8 warps (compile time).
+struct PairTable {
+  int n;
+  int t1[160];
+  int t2[160];
+};
+template <int NT>
+constexpr PairTable pairs_for(int W) {
+  PairTable P{};
+  const int b = NT >= 12 ? 4 : 2;
+  const int nb = (NT + b - 1) / b;
+  int blk = 0;
+  for (int B1 = 0; B1 < nb; ++B1)
+    for (int B2 = B1; B2 < nb; ++B2, ++blk) {
+      if (blk % kBW != W) continue;
+      for (int t1 = B1 * b; t1 < B1 * b + b && t1 < NT; ++t1)
+        for (int t2 = B2 * b; t2 < B2 * b + b && t2 < NT; ++t2)
+          if (t1 <= t2) {
+            P.t1[P.n] = t1;
+            P.t2[P.n] = t2;
+            ++P.n;
+          }
+    }
+  return P;
+}
+template <int NT>
+constexpr int max_pairs() {
+  int m = 0;
+  for (int w = 0; w < kBW; ++w) {
+    const int c = pairs_for<NT>(w).n;
+    m = c > m ? c : m;
+  }
+  return m;
+}
+
+// CTA-wide sum (all threads get the result); red has >= kBW + 1 doubles.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < kBW; ++w) s += red[w];
+  return s;
+}
+
+// DMMA over the chunk's plastic slots for warp W's tile pairs.
+template <int NT, int W, int MP>
+__device__ __forceinline__ void contract(const double* Gb, const double* sDC, const double* sDS, const int* sQ,
+                                         int np4, double (&acc)[MP][2], int lane) {
+  constexpr int NP = 8 * NT;
+  constexpr int S = Big<NT>::S;
+  constexpr PairTable P = pairs_for<NT>(W);
+  const int m = lane & 3, col = lane >> 2;
+  const int ng = np4 >> 2;
+  (void)sDS;
+#pragma unroll 1
+  for (int g = 0; g < ng; ++g) {
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int slot = 4 * g + (4 * s + m) / 3;
+      const int i = (4 * s + m) % 3;
+      const int bb = i > 0 ? 1 : 0;
+      const double* wc = sDC + slot * 6;
+      const double k0 = wc[i], k1 = wc[i + 1 + bb], k2 = wc[i + 2 + bb];
+      const double* gp = Gb + sQ[slot] * S + col;
+      double A[NT], B[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        A[t] = gp[i * NP + t * 8];
+        B[t] = k0 * gp[t * 8] + k1 * gp[NP + t * 8] + k2 * gp[2 * NP + t * 8];
+      }
+#pragma unroll
+      for (int j = 0; j < P.n; ++j) dmma(acc[j][0], acc[j][1], A[P.t1[j]], B[P.t2[j]]);
+    }
+  }
+}
+
+template <int NT, int W, int MP>
+__device__ __forceinline__ void store_tiles(double* sK, const double (&acc)[MP][2], int lane) {
+  constexpr PairTable P = pairs_for<NT>(W);
+  const int r_ = lane >> 2, c_ = 2 * (lane & 3);
+#pragma unroll
+  for (int j = 0; j < P.n; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int row = P.t1[j] * 8 + r_, cl = P.t2[j] * 8 + c_ + e;
+      if (P.t1[j] < P.t2[j])
+        sK[tri(cl) + row] = acc[j][e];
+      else if (row >= cl)
+        sK[tri(row) + cl] = acc[j][e];
+    }
+}
+
+template <int NT, int MP>
+__device__ __forceinline__ void contract_dispatch(int warp, const double* Gb, const double* sDC, const double* sDS,
+                                                  const int* sQ, int np4, double (&acc)[MP][2], int lane) {
+  switch (warp) {
+    case 0: contract<NT, 0, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+    case 1: contract<NT, 1, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+    case 2: contract<NT, 2, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+    case 3: contract<NT, 3, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+    case 4: contract<NT, 4, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+    case 5: contract<NT, 5, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+    case 6: contract<NT, 6, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+    default: contract<NT, 7, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+  }
+}
+template <int NT, int MP>
+__device__ __forceinline__ void store_dispatch(int warp, double* sK, const double (&acc)[MP][2], int lane) {
+  switch (warp) {
+    case 0: store_tiles<NT, 0, MP>(sK, acc, lane); break;
+    case 1: store_tiles<NT, 1, MP>(sK, acc, lane); break;
+    case 2: store_tiles<NT, 2, MP>(sK, acc, lane); break;
+    case 3: store_tiles<NT, 3, MP>(sK, acc, lane); break;
+    case 4: store_tiles<NT, 4, MP>(sK, acc, lane); break;
+    case 5: store_tiles<NT, 5, MP>(sK, acc, lane); break;
+    case 6: store_tiles<NT, 6, MP>(sK, acc, lane); break;
+    default: store_tiles<NT, 7, MP>(sK, acc, lane); break;
+  }
+}
+
+// CTA Cholesky of the packed lower sK (thread i = row i, n <= 256).
+__device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
+  const int tid = threadIdx.x;
+  for (int j = 0; j < n; ++j) {
+    double s = 0.0;
+    if (tid >= j && tid < n) {
+      const double* ri = sK + tri(tid);
+      const double* rj = sK + tri(j);
+      double a0 = 0.0, a1 = 0.0;
+      int k = 0;
+      for (; k + 1 < j; k += 2) {
+        a0 += ri[k] * rj[k];
+        a1 += ri[k + 1] * rj[k + 1];
+      }
+      if (k < j) a0 += ri[k] * rj[k];
+      s = ri[j] - (a0 + a1);
+      if (tid == j) red[0] = s;
+    }
+    __syncthreads();
+    const double d = red[0];
+    if (!(d > 0.0)) return false;  // uniform
+    const double inv = rsqrt_fast(d);
+    if (tid == j) {
+      sK[tri(j) + j] = d * inv;
+      sInv[j] = inv;
+    } else if (tid > j && tid < n) {
+      sK[tri(tid) + j] = s * inv;
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// Forward substitution L y = b in place on sB[n] (cols RHS interleaved: sB[i*cols + c]).
+__device__ void cta_forward(const double* sK, const double* sInv, double* sB, int n, int cols) {
+  const int tid = threadIdx.x;
+  for (int j = 0; j < n; ++j) {
+    if (tid < cols) sB[j * cols + tid] *= sInv[j];
+    __syncthreads();
+    if (tid > j && tid < n) {
+      const double l = sK[tri(tid) + j];
+      for (int c = 0; c < cols; ++c) sB[tid * cols + c] -= l * sB[j * cols + c];
+    }
+    __syncthreads();
+  }
+}
+// Backward substitution L^T x = y in place (single RHS).
+__device__ void cta_backward(const double* sK, const double* sInv, double* sB, int n) {
+  const int tid = threadIdx.x;
+  for (int j = n - 1; j >= 0; --j) {
+    if (tid == 0) sB[j] *= sInv[j];
+    __syncthreads();
+    if (tid < j) sB[tid] -= sK[tri(j) + tid] * sB[j];
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kBT, 1) k_increment_big(IncArgs A) {
+  using L = Big<NT>;
+  constexpr int NP = L::NP, QB = L::QB, TPQ = L::TPQ, S = L::S;
+  constexpr int MP = max_pairs<NT>();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  double* sK = ring + 2 * static_cast<size_t>(L::chunk);
+  double* sAev = sK + L::TRI;
+  double* sAl = sAev + NP;
+  double* sDA = sAl + NP;
+  double* sV = sDA + NP;
+  double* sInv = sV + NP;
+  double* sKaE = sInv + NP;  // [NP][3]
+  double* sDC = sKaE + 3 * NP;
+  double* sDS = sDC + QB * 6;
+  int* sQ = reinterpret_cast<int*>(sDS + QB * 3);
+  double* red = sDS + QB * 4;
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + L::RED);
+  int* ictl = reinterpret_cast<int*>(full + 2);  // [0..7] warp counts, [8] point
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const ModelDev& M = A.M;
+  const PointsDev& D = A.D;
+  const MatDev& mt = M.mat2;
+  const int nch = M.K2p / QB;
+  const int n = M.n;
+  constexpr uint32_t kChunkBytes = L::chunk * sizeof(double);
+
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < 2; ++s) {
+      mbar_expect_tx(&full[s], kChunkBytes);
+      tma_load_1d(ring + s * L::chunk, M.G2 + static_cast<size_t>(s % nch) * L::chunk, kChunkBytes, &full[s]);
+    }
+  int pos = 0;  // ring position (chunk pos % nch, stage pos % 2)
+  unsigned long long n_asm = 0, n_com = 0, n_pl = 0, n_cpl = 0;
+
+  const int qi = tid / TPQ, sub = tid % TPQ;  // cubature point of this thread within a chunk, mode slice
+  auto hist_ptr = [&](int64_t p, int q) {      // [P][K2p/32][5][32]
+    return D.hist + (p * (M.K2p / kQC) + q / kQC) * (5 * kQC) + (q % kQC);
+  };
+  auto ring_take = [&]() -> const double* {
+    const int s = pos & 1;
+    mbar_wait(&full[s], static_cast<uint32_t>((pos >> 1) & 1));
+    return ring + s * L::chunk;
+  };
+  auto ring_release = [&]() {  // after the CTA barrier that ends the chunk
+    if (tid == 0) {
+      const int s = pos & 1;
+      fence_proxy_async();
+      mbar_expect_tx(&full[s], kChunkBytes);
+      tma_load_1d(ring + s * L::chunk, M.G2 + static_cast<size_t>((pos + 2) % nch) * L::chunk, kChunkBytes,
+                  &full[s]);
+    }
+    ++pos;
+  };
+  // strain of this thread's cubature point (threads of a point split the modes)
+  auto strain = [&](const double* Gb, double E0, double E1, double E2, double& e0, double& e1, double& e2) {
+    const double* Gq = Gb + qi * S;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll 4
+    for (int a = sub; a < NP; a += TPQ) {
+      const double al = sAev[a];
+      a0 += Gq[a] * al;
+      a1 += Gq[NP + a] * al;
+      a2 += Gq[2 * NP + a] * al;
+    }
+#pragma unroll
+    for (int o = TPQ / 2; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    e0 = E0 + a0;
+    e1 = E1 + a1;
+    e2 = E2 + a2;
+  };
+  // deterministic CTA-wide compaction: returns the slot of this thread's
+  // point (if flagged) and the total count
+  auto compact = [&](bool flag, int& slot, int& total) {
+    const unsigned bal = __ballot_sync(0xffffffffu, flag && sub == 0);
+    if (lane == 0) ictl[warp] = __popc(bal);
+    __syncthreads();
+    int pre = 0;
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < kBW; ++w) {
+      const int c = ictl[w];
+      pre += (w < warp) ? c : 0;
+      total += c;
+    }
+    slot = pre + __popc(bal & ((1u << lane) - 1u));
+  };
+
+  // outputs of an assembly pass
+  double s0 = 0, s1 = 0, s2 = 0, ce00 = 0, ce01 = 0, ce02 = 0, ce11 = 0, ce12 = 0, ce22 = 0;
+  bool k_linear = false;
+
+  auto assembly_pass = [&](int64_t p, double E0, double E1, double E2) {
+    double acc[MP][2];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) acc[j][0] = acc[j][1] = 0.0;
+    double c00 = 0, c01 = 0, c02 = 0, c11 = 0, c12 = 0, c22 = 0, ds0 = 0, ds1 = 0, ds2 = 0;
+    double rr = 0.0, ka0 = 0.0, ka1 = 0.0, ka2 = 0.0;  // thread a < NP: r, K_aE corrections of mode a
+    int np_tot = 0;
+    double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
+    if (sub == 0) {
+      const double* H = hist_ptr(p, qi);
+      h0 = H[0];
+      h1 = H[kQC];
+      h2 = H[2 * kQC];
+      h3 = H[3 * kQC];
+      h4 = H[4 * kQC];
+    }
+    for (int c = 0; c < nch; ++c) {
+      const double* Gb = ring_take();
+      const int q = c * QB + qi;
+      double e0, e1, e2;
+      strain(Gb, E0, E1, E2, e0, e1, e2);
+      bool plastic = false;
+      Corr cr{};
+      if (sub == 0) {
+        const Trial T = trial_state(mt, h0, h1, h2, h3, h4, e0, e1, e2);
+        plastic = (T.f > 0.0) && (q < M.K2);
+        if (plastic) cr = radial_return(mt, T);
+        if (c + 1 < nch) {
+          const double* H = hist_ptr(p, q + QB);
+          h0 = H[0];
+          h1 = H[kQC];
+          h2 = H[2 * kQC];
+          h3 = H[3 * kQC];
+          h4 = H[4 * kQC];
+        }
+      }
+      int slot, np;
+      compact(plastic, slot, np);
+      if (plastic) {
+        const double wq = M.w2[q];
+        double* dc = sDC + slot * 6;
+        dc[0] = wq * cr.dc00;
+        dc[1] = wq * cr.dc01;
+        dc[2] = wq * cr.dc02;
+        dc[3] = wq * cr.dc11;
+        dc[4] = wq * cr.dc12;
+        dc[5] = wq * cr.dc22;
+        sDS[slot * 3 + 0] = wq * cr.ds0;
+        sDS[slot * 3 + 1] = wq * cr.ds1;
+        sDS[slot * 3 + 2] = wq * cr.ds2;
+        sQ[slot] = qi;
+        c00 += dc[0];
+        c01 += dc[1];
+        c02 += dc[2];
+        c11 += dc[3];
+        c12 += dc[4];
+        c22 += dc[5];
+        ds0 += sDS[slot * 3 + 0];
+        ds1 += sDS[slot * 3 + 1];
+        ds2 += sDS[slot * 3 + 2];
+      }
+      const int np4 = (np + 3) & ~3;
+      if (tid < np4 - np) {
+        const int z = np + tid;
+#pragma unroll
+        for (int e = 0; e < 6; ++e) sDC[z * 6 + e] = 0.0;
+        sDS[z * 3 + 0] = sDS[z * 3 + 1] = sDS[z * 3 + 2] = 0.0;
+        sQ[z] = 0;
+      }
+      n_pl += static_cast<unsigned long long>(tid == 0 ? np : 0);
+      np_tot += np;
+      __syncthreads();
+      contract_dispatch<NT, MP>(warp, Gb, sDC, sDS, sQ, np4, acc, lane);
+      if (tid < NP) {  // r and K_aE corrections of mode a = tid
+        for (int sl = 0; sl < np; ++sl) {
+          const double* Gq = Gb + sQ[sl] * S + tid;
+          const double g0 = Gq[0], g1 = Gq[NP], g2 = Gq[2 * NP];
+          const double* dc = sDC + sl * 6;
+          const double* ds = sDS + sl * 3;
+          rr += g0 * ds[0] + g1 * ds[1] + g2 * ds[2];
+          ka0 += g0 * dc[0] + g1 * dc[1] + g2 * dc[2];
+          ka1 += g0 * dc[1] + g1 * dc[3] + g2 * dc[4];
+          ka2 += g0 * dc[2] + g1 * dc[4] + g2 * dc[5];
+        }
+      }
+      __syncthreads();
+      ring_release();
+    }
+    store_dispatch<NT, MP>(warp, sK, acc, lane);
+    c00 = block_sum(c00, red);
+    c01 = block_sum(c01, red);
+    c02 = block_sum(c02, red);
+    c11 = block_sum(c11, red);
+    c12 = block_sum(c12, red);
+    c22 = block_sum(c22, red);
+    ds0 = block_sum(ds0, red);
+    ds1 = block_sum(ds1, red);
+    ds2 = block_sum(ds2, red);
+    __syncthreads();
+    // elastic predictor part and b_p, s_p (thread a = mode)
+    double sa0 = 0.0, sa1 = 0.0, sa2 = 0.0;
+    if (tid < n) {
+      const int a = tid;
+      const double* ke = M.KaEe + a * 3;
+      double sx = 0.0;
+      double* ka = sK + tri(a);
+      for (int b = 0; b < n; ++b) {
+        const double k0 = M.Ke[b * NP + a];
+        sx += k0 * sAev[b];
+        if (b <= a) ka[b] += k0;
+      }
+      sV[a] = rr + sx + (ke[0] * E0 + ke[1] * E1 + ke[2] * E2) - D.bp[p * NP + a];
+      sKaE[a * 3 + 0] = ka0 + ke[0];
+      sKaE[a * 3 + 1] = ka1 + ke[1];
+      sKaE[a * 3 + 2] = ka2 + ke[2];
+      sa0 = ke[0] * sAev[a];
+      sa1 = ke[1] * sAev[a];
+      sa2 = ke[2] * sAev[a];
+    }
+    sa0 = block_sum(sa0, red);
+    sa1 = block_sum(sa1, red);
+    sa2 = block_sum(sa2, red);
+    const double* ce = M.CEEe;
+    const double* spp = D.sp + p * 4;
+    s0 = ds0 + sa0 + (ce[0] * E0 + ce[1] * E1 + ce[2] * E2) - spp[0];
+    s1 = ds1 + sa1 + (ce[3] * E0 + ce[4] * E1 + ce[5] * E2) - spp[1];
+    s2 = ds2 + sa2 + (ce[6] * E0 + ce[7] * E1 + ce[8] * E2) - spp[2];
+    ce00 = ce[0] + c00;
+    ce01 = ce[1] + c01;
+    ce02 = ce[2] + c02;
+    ce11 = ce[4] + c11;
+    ce12 = ce[5] + c12;
+    ce22 = ce[8] + c22;
+    k_linear = (np_tot == 0);
+    ++n_asm;
+    __syncthreads();
+  };
+
+  auto factor = [&]() -> bool {
+    if (k_linear) {
+      for (int e = tid; e < tri(n); e += kBT) sK[e] = M.Le[e];
+      if (tid < n) sInv[tid] = M.LeInv[tid];
+      __syncthreads();
+      return true;
+    }
+    return cta_cholesky(sK, sInv, red, n);
+  };
+
+  auto commit_pass = [&](int64_t p, double E0, double E1, double E2) -> int {
+    double bacc = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    int pc = 0;
+    double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
+    if (sub == 0) {
+      const double* H = hist_ptr(p, qi);
+      h0 = H[0];
+      h1 = H[kQC];
+      h2 = H[2 * kQC];
+      h3 = H[3 * kQC];
+      h4 = H[4 * kQC];
+    }
+    for (int c = 0; c < nch; ++c) {
+      const double* Gb = ring_take();
+      const int q = c * QB + qi;
+      double e0, e1, e2;
+      strain(Gb, E0, E1, E2, e0, e1, e2);
+      bool pl = false;
+      double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+      if (sub == 0) {
+        const MatOut o = update_material(mt, h0, h1, h2, h3, h4, e0, e1, e2);
+        pl = (q < M.K2) && o.plastic;
+        double* H = hist_ptr(p, q);
+        if (pl) {
+          const double x0 = o.ep0 - h0, x1 = o.ep1 - h1, x2 = o.ep2 - h2, x3 = o.ep3 - h3;
+          const double lt = mt.lam * (x0 + x1 + x2), wq = M.w2[q];
+          w0 = wq * (lt + 2.0 * mt.mu * x0);
+          w1 = wq * (lt + 2.0 * mt.mu * x1);
+          w2 = wq * (2.0 * mt.mu * x3);
+        }
+        if (c + 1 < nch) {
+          const double* Hn = hist_ptr(p, q + QB);
+          h0 = Hn[0];
+          h1 = Hn[kQC];
+          h2 = Hn[2 * kQC];
+          h3 = Hn[3 * kQC];
+          h4 = Hn[4 * kQC];
+        }
+        if (pl) {
+          H[0] = o.ep0;
+          H[kQC] = o.ep1;
+          H[2 * kQC] = o.ep2;
+          H[3 * kQC] = o.ep3;
+          H[4 * kQC] = o.eq;
+        }
+        if (D.flags && q < M.K2) D.flags[p * M.K2p + q] = o.plastic ? 1 : 0;
+        t0 += w0;
+        t1 += w1;
+        t2 += w2;
+      }
+      int slot, np;
+      compact(pl, slot, np);
+      if (pl) {
+        sDS[slot * 3 + 0] = w0;
+        sDS[slot * 3 + 1] = w1;
+        sDS[slot * 3 + 2] = w2;
+        sQ[slot] = qi;
+      }
+      pc += np;
+      __syncthreads();
+      if (tid < NP)
+        for (int sl = 0; sl < np; ++sl) {
+          const double* Gq = Gb + sQ[sl] * S + tid;
+          bacc += Gq[0] * sDS[sl * 3 + 0] + Gq[NP] * sDS[sl * 3 + 1] + Gq[2 * NP] * sDS[sl * 3 + 2];
+        }
+      __syncthreads();
+      ring_release();
+    }
+    for (int a = tid; a < NP; a += kBT) D.alpha_c[p * NP + a] = sAev[a];
+    if (tid < NP) D.bp[p * NP + tid] += bacc;
+    t0 = block_sum(t0, red);
+    t1 = block_sum(t1, red);
+    t2 = block_sum(t2, red);
+    if (tid == 0) {
+      D.sp[p * 4 + 0] += t0;
+      D.sp[p * 4 + 1] += t1;
+      D.sp[p * 4 + 2] += t2;
+    }
+    ++n_com;
+    n_cpl += static_cast<unsigned long long>(tid == 0 ? pc : 0);
+    __syncthreads();
+    return pc;
+  };
+
+  const NewtonCfg& cfg = A.cfg;
+  constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
+
+  if (A.dbg) {
+    if (blockIdx.x == 0) {
+      const int64_t p = A.dbg_point;
+      for (int a = tid; a < NP; a += kBT) sAev[a] = (a < n) ? A.dbg_alpha[a] : 0.0;
+      __syncthreads();
+      assembly_pass(p, A.dbg_E[0], A.dbg_E[1], A.dbg_E[2]);
+      double* o = A.dbg;
+      for (int a = tid; a < n; a += kBT) o[a] = sV[a];
+      for (int e = tid; e < n * n; e += kBT) {
+        const int i = e / n, j = e % n;
+        o[n + e] = (j <= i) ? sK[tri(i) + j] : sK[tri(j) + i];
+      }
+      for (int e = tid; e < 3 * n; e += kBT) o[n + n * n + e] = sKaE[e];
+      if (tid == 0) {
+        double* cc = o + n + n * n + 3 * n;
+        cc[0] = ce00;
+        cc[1] = ce01;
+        cc[2] = ce02;
+        cc[3] = ce01;
+        cc[4] = ce11;
+        cc[5] = ce12;
+        cc[6] = ce02;
+        cc[7] = ce12;
+        cc[8] = ce22;
+        cc[9] = s0;
+        cc[10] = s1;
+        cc[11] = s2;
+      }
+    }
+  } else {
+    while (true) {
+      __syncthreads();
+      if (tid == 0) ictl[8] = atomicAdd(A.work, 1);
+      __syncthreads();
+      const int64_t p = ictl[8];
+      if (p >= D.P) break;
+      const double Ep0 = D.E_c[p * 3 + 0], Ep1 = D.E_c[p * 3 + 1], Ep2 = D.E_c[p * 3 + 2];
+      const double Et0 = A.dE[p * 3 + 0], Et1 = A.dE[p * 3 + 1], Et2 = A.dE[p * 3 + 2];
+      const int dead = D.st[p].err;
+      auto write_fail = [&](int code, int iters, double rn) {
+        if (tid == 0) {
+          A.O.status[p] = code;
+          A.O.iters[p] = iters;
+          A.O.res[p] = rn;
+          for (int i = 0; i < 3; ++i) A.O.sigma[p * 3 + i] = qnan();
+          for (int i = 0; i < 9; ++i) A.O.C[p * 9 + i] = qnan();
+          if (A.O.pcount) A.O.pcount[p] = 0;
+        }
+      };
+      auto finish = [&](int err) {
+        __syncthreads();
+        if (tid == 0) {
+          if (err) D.st[p].err = err;
+          D.E_c[p * 3 + 0] = Et0;
+          D.E_c[p * 3 + 1] = Et1;
+          D.E_c[p * 3 + 2] = Et2;
+        }
+      };
+      if (dead) {
+        write_fail(dead, 0, qnan());
+        finish(0);
+        continue;
+      }
+      for (int a = tid; a < NP; a += kBT) {
+        const double ac = D.alpha_c[p * NP + a];
+        sAev[a] = ac;
+        sAl[a] = ac;
+      }
+      double E0 = lerp_rn(Ep0, Et0, 1.0), E1 = lerp_rn(Ep1, Et1, 1.0), E2 = lerp_rn(Ep2, Et2, 1.0);
+      __syncthreads();
+      int mode = 0, it = 0, ls = 0, iters = 0, bis = 0, err = 0;
+      double a = 1.0, rn_it = 0.0, best_rn = 0.0, best_a = 1.0, ref = 0.0, done = 0.0, frac = 1.0;
+      while (true) {
+        assembly_pass(p, E0, E1, E2);
+        const double rl = (tid < n) ? sV[tid] : 0.0;
+        const double rn = sqrt(block_sum(rl * rl, red));
+        const double srn = sqrt(s0 * s0 + s1 * s1 + s2 * s2);
+        int action = 0;  // 0 assemble again, 1 final commit, 2 sub-step commit, 3 failed
+        for (int pass = 0; pass < 2; ++pass) {
+          if (mode == 0) {
+            if (it == 0) ref = fmax(fmax(rn, srn), 1e-30);
+            if (rn <= cfg.tol * ref) {
+              iters += it;
+              const double target = fmin(1.0, done + frac);
+              if (target >= 1.0 - 1e-12) {
+                if (!factor()) {
+                  err = kSolver;
+                  write_fail(err, iters, rn);
+                  action = 3;
+                  break;
+                }
+                // condensation X = L^-1 K_aE, C = (C_EE - X^T X)/V (homogenize, rve.hpp:372-390)
+                cta_forward(sK, sInv, sKaE, n, 3);
+                double x0 = 0, x1 = 0, x2 = 0;
+                if (tid < n) {
+                  x0 = sKaE[tid * 3 + 0];
+                  x1 = sKaE[tid * 3 + 1];
+                  x2 = sKaE[tid * 3 + 2];
+                }
+                const double q00 = block_sum(x0 * x0, red), q01 = block_sum(x0 * x1, red);
+                const double q02 = block_sum(x0 * x2, red), q11 = block_sum(x1 * x1, red);
+                const double q12 = block_sum(x1 * x2, red), q22 = block_sum(x2 * x2, red);
+                if (tid == 0) {
+                  const double V = M.volume;
+                  double* Cp = A.O.C + p * 9;
+                  Cp[0] = (ce00 - q00) / V;
+                  Cp[1] = (ce01 - q01) / V;
+                  Cp[2] = (ce02 - q02) / V;
+                  Cp[3] = (ce01 - q01) / V;
+                  Cp[4] = (ce11 - q11) / V;
+                  Cp[5] = (ce12 - q12) / V;
+                  Cp[6] = (ce02 - q02) / V;
+                  Cp[7] = (ce12 - q12) / V;
+                  Cp[8] = (ce22 - q22) / V;
+                  A.O.sigma[p * 3 + 0] = s0 / V;
+                  A.O.sigma[p * 3 + 1] = s1 / V;
+                  A.O.sigma[p * 3 + 2] = s2 / V;
+                  A.O.res[p] = rn;
+                  A.O.iters[p] = iters;
+                  A.O.status[p] = 0;
+                }
+                action = 1;
+              } else {
+                action = 2;
+                done = target;
+              }
+              break;
+            }
+            if (it == cfg.max_iter) {  // bisect the load step (rve.hpp:473-478)
+              iters += cfg.max_iter;
+              if (++bis > cfg.max_bis) {
+                err = kSolver;
+                write_fail(err, iters, rn);
+                action = 3;
+                break;
+              }
+              frac *= 0.5;
+              const double nt = fmin(1.0, done + frac);
+              E0 = lerp_rn(Ep0, Et0, nt);
+              E1 = lerp_rn(Ep1, Et1, nt);
+              E2 = lerp_rn(Ep2, Et2, nt);
+              __syncthreads();
+              for (int b = tid; b < NP; b += kBT) {
+                const double ac = D.alpha_c[p * NP + b];
+                sAl[b] = ac;
+                sAev[b] = ac;
+              }
+              it = 0;
+              action = 0;
+              break;
+            }
+            if (!factor()) {
+              err = kSolver;
+              write_fail(err, iters, rn);
+              action = 3;
+              break;
+            }
+            if (tid < n) sDA[tid] = -sV[tid];
+            __syncthreads();
+            cta_forward(sK, sInv, sDA, n, 1);
+            cta_backward(sK, sInv, sDA, n);
+            for (int b = tid; b < NP; b += kBT) sAev[b] = (b < n) ? axpy_rn(sAl[b], 1.0, sDA[b]) : 0.0;
+            rn_it = rn;
+            a = 1.0;
+            ls = 0;
+            best_rn = __longlong_as_double(0x7ff0000000000000ll);
+            best_a = 1.0;
+            mode = 1;
+            action = 0;
+            break;
+          } else {  // backtracking line search (rve.hpp:327-341)
+            const double trial = rn;
+            if (trial < best_rn) {
+              best_rn = trial;
+              best_a = a;
+            }
+            const bool armijo = trial <= (1.0 - 1e-4 * a) * rn_it;
+            if (armijo || ls == 7) {
+              it += 1;
+              mode = 0;
+              __syncthreads();
+              if (best_a == a) {
+                for (int b = tid; b < NP; b += kBT) sAl[b] = sAev[b];
+                __syncthreads();
+                continue;
+              }
+              for (int b = tid; b < NP; b += kBT) {
+                const double nv = (b < n) ? axpy_rn(sAl[b], best_a, sDA[b]) : 0.0;
+                sAl[b] = nv;
+                sAev[b] = nv;
+              }
+              action = 0;
+              break;
+            }
+            ls += 1;
+            a *= 0.5;
+            __syncthreads();
+            for (int b = tid; b < NP; b += kBT) sAev[b] = (b < n) ? axpy_rn(sAl[b], a, sDA[b]) : 0.0;
+            action = 0;
+            break;
+          }
+        }
+        __syncthreads();
+        if (action == 0) continue;
+        if (action == 3) break;
+        const int pc = commit_pass(p, E0, E1, E2);
+        if (action == 1) {
+          if (tid == 0 && A.O.pcount) A.O.pcount[p] = pc;
+          break;
+        }
+        const double nt = fmin(1.0, done + frac);
+        E0 = lerp_rn(Ep0, Et0, nt);
+        E1 = lerp_rn(Ep1, Et1, nt);
+        E2 = lerp_rn(Ep2, Et2, nt);
+        for (int b = tid; b < NP; b += kBT) sAl[b] = sAev[b];
+        __syncthreads();
+        it = 0;
+        mode = 0;
+      }
+      finish(err);
+    }
+  }
+  // no TMA may be in flight at exit: the two positions issued ahead
+  __syncthreads();
+  for (int k = 0; k < 2; ++k) {
+    mbar_wait(&full[pos & 1], static_cast<uint32_t>((pos >> 1) & 1));
+    ++pos;
+  }
+  if (A.cnt && tid == 0) {
+    atomicAdd(&A.cnt->assemblies, n_asm);
+    atomicAdd(&A.cnt->commits, n_com);
+    atomicAdd(&A.cnt->plastic_evals, n_pl);
+    atomicAdd(&A.cnt->commit_plastic, n_cpl);
+  }
+}
+
+template <int NT>
+void launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
+  const size_t smem = Big<NT>::bytes;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_increment_big<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment_big<NT>, kBT, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = static_cast<int64_t>(num_sms) * per_sm;
+  if (a.dbg) grid = 1;
+  else if (grid > a.D.P) grid = a.D.P;
+  if (grid < 1) grid = 1;
+  k_increment_big<NT><<<static_cast<unsigned>(grid), kBT, smem, s>>>(a);
+}
+
+}  // namespace
+
+// NP = 40, 48, 56, 64 (32-point chunks) and 80, 96, 112, 128 (16-point chunks)
+bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s) {
+  switch (a.M.NP) {
+    case 40: launch_big_nt<5>(a, num_sms, s); return true;
+    case 48: launch_big_nt<6>(a, num_sms, s); return true;
+    case 56: launch_big_nt<7>(a, num_sms, s); return true;
+    case 64: launch_big_nt<8>(a, num_sms, s); return true;
+    case 80: launch_big_nt<10>(a, num_sms, s); return true;
+    case 96: launch_big_nt<12>(a, num_sms, s); return true;
+    case 112: launch_big_nt<14>(a, num_sms, s); return true;
+    case 128: launch_big_nt<16>(a, num_sms, s); return true;
+    default: return false;
+  }
+}
+
+size_t increment_big_smem(int NP) {
+  switch (NP) {
+    case 40: return Big<5>::bytes;
+    case 48: return Big<6>::bytes;
+    case 56: return Big<7>::bytes;
+    case 64: return Big<8>::bytes;
+    case 80: return Big<10>::bytes;
+    case 96: return Big<12>::bytes;
+    case 112: return Big<14>::bytes;
+    case 128: return Big<16>::bytes;
+    default: return 0;
+  }
+}
+
+}  // namespace fe2

@@ -185,3 +185,35 @@ def test_config1_full_size_properties_and_sampled_parity():
     np.testing.assert_array_equal(g["plastic_count"][sample], o["plastic_count"])
     assert path_rel_err(g["sigma"][sample], o["sigma"]).max() < REL
     assert rel_err(C[sample].reshape(-1, 9), o["C"].reshape(-1, 9)).max() < REL
+
+
+@pytest.mark.parametrize("n,K", [(40, 300), (64, 600), (72, 500), (128, 1000)])
+def test_large_basis_assembly_matches_oracle(n, K):
+    """n > 32 runs on the one-CTA-per-point kernel (BASELINE configs 3/4)."""
+    m = F.HyperRomModel(33, n, K, 1)
+    eng = F.HyperRomEngine.from_model(m)
+    eng.alloc_points(2)
+    orc = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume)
+    rng = np.random.default_rng(n)
+    for trial in range(2):
+        alpha = rng.normal(scale=0.01, size=n)
+        Ev = np.array([0.03, -0.01, 0.02]) * (trial + 1)
+        g = eng.assemble_point(0, alpha, Ev)
+        o = orc.assemble(alpha, Ev)
+        assert o["plastic_count"] > 0
+        for k in ("r", "Kaa", "KaE", "C_EE", "S_raw"):
+            err = np.linalg.norm(g[k] - o[k]) / np.linalg.norm(o[k])
+            assert err < 1e-12, (n, k, err)
+
+
+@pytest.mark.parametrize("n,K,P,incr", [(64, 600, 48, 6), (128, 1000, 16, 4)])
+def test_large_basis_trajectory_parity(n, K, P, incr):
+    m = F.HyperRomModel(33, n, K, 2)
+    E = F.make_paths(0, 2, P, incr)
+    eng, g = run_gpu(m, E, keep_flags=True)
+    o = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume).run(E, threads=16, flags=True)
+    assert (o["status"] == 0).all() and (g["status"] == 0).all()
+    np.testing.assert_array_equal(g["iters"], o["iters"])
+    np.testing.assert_array_equal(g["plastic_count"], o["plastic_count"])
+    assert path_rel_err(g["sigma"], o["sigma"]).max() < REL
+    assert rel_err(g["C"].reshape(-1, 9), o["C"].reshape(-1, 9)).max() < REL
