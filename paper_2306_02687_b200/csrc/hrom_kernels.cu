@@ -239,10 +239,8 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
 #define FE2_MINB 1
 #endif
 constexpr int kW = FE2_KW;            // warps per CTA
-constexpr int kStages = FE2_STAGES;   // G-chunk ring depth (shared by the CTA)
+constexpr int kMaxStages = FE2_STAGES;  // G-chunk ring depth (shared by the CTA), at most
 constexpr int kHS = 2;      // per-warp history ring depth (TMA, 5 x 256 B per stage)
-
-__device__ __forceinline__ int tri(int i) { return i * (i + 1) / 2; }  // packed lower row offset
 
 template <int NP>
 struct IncLayout {
@@ -253,11 +251,15 @@ struct IncLayout {
   static constexpr int kUnion = (kSlots > kTri) ? kSlots : kTri;
   static constexpr int kHist = kHS * 5 * kQC;                 // per-warp history ring (TMA)
   static constexpr int WS = 5 * NP + 3 * NP + kUnion + kHist;  // per-warp scratch (doubles)
-  static constexpr size_t ring_bytes = static_cast<size_t>(kStages) * chunk * sizeof(double);
-  // control block: full[kStages] (u64) | hbar[kW][kHS] (u64) | cnt[kStages] (int) | ctrl (u64)
-  static constexpr int kHbarOff = kStages * 8;
+  // ring depth: as deep as the 227 KB shared-memory budget allows (<= kMaxStages)
+  static constexpr long kBudget = 227L * 1024 - 512 - static_cast<long>(kW) * WS * 8;
+  static constexpr int kFit = static_cast<int>(kBudget / (static_cast<long>(chunk) * 8));
+  static constexpr int ST = kFit < 2 ? 2 : (kFit > kMaxStages ? kMaxStages : kFit);
+  static constexpr size_t ring_bytes = static_cast<size_t>(ST) * chunk * sizeof(double);
+  // control block: full[ST] (u64) | hbar[kW][kHS] (u64) | cnt[ST] (int) | ctrl (u64)
+  static constexpr int kHbarOff = ST * 8;
   static constexpr int kCntOff = kHbarOff + kW * kHS * 8;
-  static constexpr int kCtrlOff = ((kCntOff + kStages * 4 + 7) / 8) * 8;
+  static constexpr int kCtrlOff = ((kCntOff + ST * 4 + 7) / 8) * 8;
   static constexpr size_t bytes = ring_bytes + static_cast<size_t>(kW) * WS * sizeof(double) + kCtrlOff + 8;
 };
 
@@ -273,6 +275,7 @@ struct Ring {
   int nch;
   int chunk;           // doubles per stage
   volatile int* tr;    // watchdog trace slot of this warp (or null)
+  int stages;          // ring depth
 };
 
 __device__ __forceinline__ void trace(const Ring& R, int seq, int code) {
@@ -286,9 +289,9 @@ __device__ __forceinline__ void trace(const Ring& R, int seq, int code) {
 }
 
 __device__ __forceinline__ const double* ring_wait(const Ring& R, int seq) {
-  const int s = seq % kStages;
+  const int s = seq % R.stages;
   trace(R, seq, 1);
-  mbar_wait(&R.full[s], static_cast<uint32_t>((seq / kStages) & 1));
+  mbar_wait(&R.full[s], static_cast<uint32_t>((seq / R.stages) & 1));
   trace(R, seq, 2);
   return R.buf + static_cast<size_t>(s) * R.chunk;
 }
@@ -296,11 +299,11 @@ __device__ __forceinline__ const double* ring_wait(const Ring& R, int seq) {
 __device__ __forceinline__ void ring_release(const Ring& R, int seq, int lane) {
   __syncwarp();
   if (lane == 0) {
-    const int s = seq % kStages;
+    const int s = seq % R.stages;
     __threadfence_block();
     if (atomicAdd(&R.cnt[s], 1) == kW - 1) {
       R.cnt[s] = 0;
-      const int nxt = seq + kStages;
+      const int nxt = seq + R.stages;
       unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(R.ctrl);
       bool issue = false;
       while ((old >> 32) > 0) {
@@ -384,14 +387,14 @@ __global__ void __launch_bounds__(kW * 32, FE2_MINB) k_increment(IncArgs A) {
   const MatDev& mt = M.mat2;
   const int nch = M.nchunks;
   const Ring R{ring_buf, full, cnt, ctrl, M.G2, nch, L::chunk,
-               A.trace ? A.trace + (static_cast<size_t>(blockIdx.x) * kW + warp) * 4 : nullptr};
+               A.trace ? A.trace + (static_cast<size_t>(blockIdx.x) * kW + warp) * 4 : nullptr, L::ST};
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < L::ST; ++s) {
       mbar_init(&full[s], 1);
       cnt[s] = 0;
     }
-    *ctrl = (static_cast<unsigned long long>(kW) << 32) | static_cast<unsigned long long>(kStages);
+    *ctrl = (static_cast<unsigned long long>(kW) << 32) | static_cast<unsigned long long>(L::ST);
   }
   if (lane == 0)
     for (int s = 0; s < kHS; ++s) mbar_init(&hbar[s], 1);
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(kW * 32, FE2_MINB) k_increment(IncArgs A) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t bytes = static_cast<uint32_t>(L::chunk * sizeof(double));
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < L::ST; ++s) {
       mbar_expect_tx(&full[s], bytes);
       tma_load_1d(ring_buf + static_cast<size_t>(s) * L::chunk, M.G2 + static_cast<size_t>(s % nch) * L::chunk,
                   bytes, &full[s]);

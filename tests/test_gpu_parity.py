@@ -217,3 +217,16 @@ def test_large_basis_trajectory_parity(n, K, P, incr):
     np.testing.assert_array_equal(g["plastic_count"], o["plastic_count"])
     assert path_rel_err(g["sigma"], o["sigma"]).max() < REL
     assert rel_err(g["C"].reshape(-1, 9), o["C"].reshape(-1, 9)).max() < REL
+
+
+@pytest.mark.parametrize("n,K", [(8, 100), (16, 400), (32, 400)])
+def test_small_basis_widths_trajectory_parity(n, K):
+    """Every one-warp-per-point instantiation (NP = 8, 16, 32) end to end."""
+    m = F.HyperRomModel(33, n, K, 3)
+    E = F.make_paths(1, 3, 96, 12)
+    _, g = run_gpu(m, E)
+    o = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume).run(E, threads=16)
+    np.testing.assert_array_equal(g["status"], o["status"])
+    np.testing.assert_array_equal(g["iters"], o["iters"])
+    assert path_rel_err(g["sigma"], o["sigma"]).max() < REL
+    assert rel_err(g["C"].reshape(-1, 9), o["C"].reshape(-1, 9)).max() < REL
