@@ -24,13 +24,19 @@ namespace {
 
 using namespace dev;
 
+#ifndef FE2_BIG_MINB
+#define FE2_BIG_MINB 1
+#endif
+#ifndef FE2_BIG_QB32_MAXNP
+#define FE2_BIG_QB32_MAXNP 64
+#endif
 constexpr int kBW = 8;         // warps per CTA
 constexpr int kBT = kBW * 32;  // threads per CTA
 
 template <int NT>
 struct Big {
   static constexpr int NP = 8 * NT;
-  static constexpr int QB = (NP <= 64) ? 32 : 16;  // cubature points per chunk
+  static constexpr int QB = (NP <= FE2_BIG_QB32_MAXNP) ? 32 : 16;  // cubature points per chunk
   static constexpr int TPQ = kBT / QB;             // threads per cubature point (8 | 16)
   static constexpr int S = 3 * NP + 2;
   static constexpr int chunk = QB * S;
@@ -90,13 +96,64 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
+// Compile-time walk over warp W's tile pairs (keeps every index a constant,
+// so the accumulators and fragments stay in registers).
+template <int NT, int W, int J, int MP>
+__device__ __forceinline__ void dmma_pairs(double (&acc)[MP][2], const double (&A)[NT], const double (&B)[NT]) {
+  if constexpr (J < pairs_for<NT>(W).n) {
+    constexpr int t1 = pairs_for<NT>(W).t1[J];
+    constexpr int t2 = pairs_for<NT>(W).t2[J];
+    dmma(acc[J][0], acc[J][1], A[t1], B[t2]);
+    dmma_pairs<NT, W, J + 1, MP>(acc, A, B);
+  }
+}
+template <int NT, int W, int J, int MP>
+__device__ __forceinline__ void store_pairs(double* sK, const double (&acc)[MP][2], int r_, int c_) {
+  if constexpr (J < pairs_for<NT>(W).n) {
+    constexpr int t1 = pairs_for<NT>(W).t1[J];
+    constexpr int t2 = pairs_for<NT>(W).t2[J];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int row = t1 * 8 + r_, cl = t2 * 8 + c_ + e;
+      if constexpr (t1 < t2)
+        sK[tri(cl) + row] = acc[J][e];
+      else if (row >= cl)
+        sK[tri(row) + cl] = acc[J][e];
+    }
+    store_pairs<NT, W, J + 1, MP>(sK, acc, r_, c_);
+  }
+}
+// which fragment tiles warp W reads (so unused loads are never issued)
+template <int NT>
+constexpr bool uses_row(int W, int t) {
+  const PairTable P = pairs_for<NT>(W);
+  for (int j = 0; j < P.n; ++j)
+    if (P.t1[j] == t) return true;
+  return false;
+}
+template <int NT>
+constexpr bool uses_col(int W, int t) {
+  const PairTable P = pairs_for<NT>(W);
+  for (int j = 0; j < P.n; ++j)
+    if (P.t2[j] == t) return true;
+  return false;
+}
+template <int NT, int W, int T>
+__device__ __forceinline__ void load_frags(const double* gp, int i, double k0, double k1, double k2, double (&A)[NT],
+                                           double (&B)[NT]) {
+  if constexpr (T < NT) {
+    constexpr int NP = 8 * NT;
+    if constexpr (uses_row<NT>(W, T)) A[T] = gp[i * NP + T * 8];
+    if constexpr (uses_col<NT>(W, T)) B[T] = k0 * gp[T * 8] + k1 * gp[NP + T * 8] + k2 * gp[2 * NP + T * 8];
+    load_frags<NT, W, T + 1>(gp, i, k0, k1, k2, A, B);
+  }
+}
+
 // DMMA over the chunk's plastic slots for warp W's tile pairs.
 template <int NT, int W, int MP>
 __device__ __forceinline__ void contract(const double* Gb, const double* sDC, const double* sDS, const int* sQ,
                                          int np4, double (&acc)[MP][2], int lane) {
-  constexpr int NP = 8 * NT;
   constexpr int S = Big<NT>::S;
-  constexpr PairTable P = pairs_for<NT>(W);
   const int m = lane & 3, col = lane >> 2;
   const int ng = np4 >> 2;
   (void)sDS;
@@ -111,31 +168,15 @@ __device__ __forceinline__ void contract(const double* Gb, const double* sDC, co
       const double k0 = wc[i], k1 = wc[i + 1 + bb], k2 = wc[i + 2 + bb];
       const double* gp = Gb + sQ[slot] * S + col;
       double A[NT], B[NT];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        A[t] = gp[i * NP + t * 8];
-        B[t] = k0 * gp[t * 8] + k1 * gp[NP + t * 8] + k2 * gp[2 * NP + t * 8];
-      }
-#pragma unroll
-      for (int j = 0; j < P.n; ++j) dmma(acc[j][0], acc[j][1], A[P.t1[j]], B[P.t2[j]]);
+      load_frags<NT, W, 0>(gp, i, k0, k1, k2, A, B);
+      dmma_pairs<NT, W, 0, MP>(acc, A, B);
     }
   }
 }
 
 template <int NT, int W, int MP>
 __device__ __forceinline__ void store_tiles(double* sK, const double (&acc)[MP][2], int lane) {
-  constexpr PairTable P = pairs_for<NT>(W);
-  const int r_ = lane >> 2, c_ = 2 * (lane & 3);
-#pragma unroll
-  for (int j = 0; j < P.n; ++j)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int row = P.t1[j] * 8 + r_, cl = P.t2[j] * 8 + c_ + e;
-      if (P.t1[j] < P.t2[j])
-        sK[tri(cl) + row] = acc[j][e];
-      else if (row >= cl)
-        sK[tri(row) + cl] = acc[j][e];
-    }
+  store_pairs<NT, W, 0, MP>(sK, acc, lane >> 2, 2 * (lane & 3));
 }
 
 template <int NT, int MP>
@@ -224,7 +265,7 @@ __device__ void cta_backward(const double* sK, const double* sInv, double* sB, i
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kBT, 1) k_increment_big(IncArgs A) {
+__global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) {
   using L = Big<NT>;
   constexpr int NP = L::NP, QB = L::QB, TPQ = L::TPQ, S = L::S;
   constexpr int MP = max_pairs<NT>();

@@ -84,6 +84,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=2.0)
     ap.add_argument("--which", default="0,3,4")
+    ap.add_argument("--only", default="", help="comma-separated substrings of cell names to run")
     args = ap.parse_args()
     which = set(args.which.split(","))
     cells = []
@@ -95,6 +96,9 @@ def main():
         for n in (8, 16, 32, 64, 128):
             for K in (100, 400, 1000, 4000):
                 cells.append((f"config4_n{n}_K{K}", n, K, 131072, 5, 0))
+    if args.only:
+        keys = args.only.split(",")
+        cells = [c for c in cells if any(k in c[0] for k in keys)]
     for c in cells:
         t0 = time.time()
         r = run_cell(*c, seconds=args.seconds)
