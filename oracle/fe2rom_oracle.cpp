@@ -1187,6 +1187,396 @@ inline void hrom_point_trajectory(const Hrom& h, std::int64_t pi, int n_incr, co
     }
 }
 
+// ---------------------------------------------------------------------------
+// Finite strain, Biot stress (BASELINE config 2). PARITY UNPINNED: the
+// reference contains no finite-strain code (SPEC.md:8 declares it out of
+// scope; the paper's biot_stress section is absent from PAPER.md:19-20), so
+// this is our formulation, checked only for self-consistency (FD tangents,
+// objectivity, small-strain limit) in tests/test_oracle_fs.py:
+//   F = R U (2-D polar decomposition, R by the angle atan2(F10-F01, F00+F11)),
+//   Biot strain U - I -> the pinned small-strain update4 (J2 / elastic) gives
+//   the Biot stress T, P = R T (first Piola-Kirchhoff), A = dP/dF closed form.
+// Components are ordered (F00, F01, F10, F11) = (dx/dX, dx/dY, dy/dX, dy/dY).
+struct FsResult {
+  double P[4];
+  double A[16];  // A[r][s] = dP_r / dF_s
+  State state;
+  bool plastic;
+};
+
+inline FsResult update_biot(const Mat& m, const State& s0, const double* F) {
+  const double num = F[2] - F[1], den = F[0] + F[3];
+  const double th = std::atan2(num, den);
+  const double c = std::cos(th), s = std::sin(th);
+  // U = R^T F
+  const double U00 = c * F[0] + s * F[2], U01 = c * F[1] + s * F[3];
+  const double U10 = -s * F[0] + c * F[2], U11 = -s * F[1] + c * F[3];
+  const double e4[4] = {U00 - 1.0, U11 - 1.0, 0.0, 0.5 * (U01 + U10)};
+  const Result4 r4 = update4(m, s0, e4);
+  const double T00 = r4.sigma[0], T11 = r4.sigma[1], T01 = r4.sigma[3];
+  FsResult out;
+  out.P[0] = c * T00 - s * T01;
+  out.P[1] = c * T01 - s * T11;
+  out.P[2] = s * T00 + c * T01;
+  out.P[3] = s * T01 + c * T11;
+  out.state = r4.state;
+  out.plastic = r4.plastic;
+  const double rho2 = num * num + den * den;
+  const double g[4] = {-num / rho2, -den / rho2, den / rho2, -num / rho2};  // dθ/dF
+  // R J T with J = [[0,-1],[1,0]]: (RJ) = [[-s,-c],[c,-s]]
+  const double RJT00 = -s * T00 - c * T01, RJT01 = -s * T01 - c * T11;
+  const double RJT10 = c * T00 - s * T01, RJT11 = c * T01 - s * T11;
+  for (int k = 0; k < 4; ++k) {
+    const double dth = g[k];
+    double dF[4] = {0, 0, 0, 0};
+    dF[k] = 1.0;
+    // dU = -J U dθ + R^T dF,   -J U = [[U10, U11], [-U00, -U01]]
+    const double dU00 = U10 * dth + (c * dF[0] + s * dF[2]);
+    const double dU01 = U11 * dth + (c * dF[1] + s * dF[3]);
+    const double dU10 = -U00 * dth + (-s * dF[0] + c * dF[2]);
+    const double dU11 = -U01 * dth + (-s * dF[1] + c * dF[3]);
+    const double de[4] = {dU00, dU11, 0.0, 0.5 * (dU01 + dU10)};
+    double dT[4];
+    for (int i = 0; i < 4; ++i) {
+      double t = 0.0;
+      for (int j = 0; j < 4; ++j) t += r4.D[i][j] * de[j];
+      dT[i] = t;
+    }
+    const double d00 = dT[0], d11 = dT[1], d01 = dT[3];
+    out.A[0 * 4 + k] = RJT00 * dth + (c * d00 - s * d01);
+    out.A[1 * 4 + k] = RJT01 * dth + (c * d01 - s * d11);
+    out.A[2 * 4 + k] = RJT10 * dth + (s * d00 + c * d01);
+    out.A[3 * 4 + k] = RJT11 * dth + (s * d01 + c * d11);
+  }
+  return out;
+}
+
+// Dense LU with partial pivoting (the finite-strain K_aa is not symmetric).
+struct Lu {
+  int n = 0;
+  std::vector<double> a;
+  std::vector<int> piv;
+  bool factor(const std::vector<double>& A, int n_) {
+    n = n_;
+    a = A;
+    piv.resize(n);
+    for (int j = 0; j < n; ++j) {
+      int p = j;
+      double best = std::abs(a[(size_t)j * n + j]);
+      for (int i = j + 1; i < n; ++i)
+        if (std::abs(a[(size_t)i * n + j]) > best) {
+          best = std::abs(a[(size_t)i * n + j]);
+          p = i;
+        }
+      if (!(best > 0.0)) return false;
+      piv[j] = p;
+      if (p != j)
+        for (int k = 0; k < n; ++k) std::swap(a[(size_t)j * n + k], a[(size_t)p * n + k]);
+      const double inv = 1.0 / a[(size_t)j * n + j];
+      for (int i = j + 1; i < n; ++i) {
+        const double l = a[(size_t)i * n + j] * inv;
+        a[(size_t)i * n + j] = l;
+        for (int k = j + 1; k < n; ++k) a[(size_t)i * n + k] -= l * a[(size_t)j * n + k];
+      }
+    }
+    return true;
+  }
+  void solve(const double* b, double* x) const {
+    std::vector<double> y(b, b + n);
+    for (int j = 0; j < n; ++j) std::swap(y[j], y[piv[j]]);
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < i; ++k) y[i] -= a[(size_t)i * n + k] * y[k];
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < n; ++k) s -= a[(size_t)i * n + k] * x[k];
+      x[i] = s / a[(size_t)i * n + i];
+    }
+  }
+};
+
+// 4-row displacement-gradient operator at an IP from the strain operator B
+// (mesh.hpp:106-113): rows (dwx/dX, dwx/dY, dwy/dX, dwy/dY).
+inline void grad_operator(const double* B, double Bg[4][12]) {
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 12; ++c) Bg[r][c] = 0.0;
+  for (int a = 0; a < 6; ++a) {
+    Bg[0][2 * a] = B[0 * 12 + 2 * a];          // dN/dX
+    Bg[1][2 * a] = B[2 * 12 + 2 * a];          // dN/dY
+    Bg[2][2 * a + 1] = B[2 * 12 + 2 * a + 1];  // dN/dX
+    Bg[3][2 * a + 1] = B[1 * 12 + 2 * a + 1];  // dN/dY
+  }
+}
+
+// G4_q = Bg_q Φ[dofs(el(q))] for the cubature of a built model (same Φ, ids, weights).
+inline std::vector<double> build_g4(const Mesh& mesh, const Model& md) {
+  HfProblem hf = build_hf(mesh, {Mat{}, Mat{}});
+  const int n = md.n;
+  std::vector<double> G4((size_t)md.K * 4 * n, 0.0);
+  for (int q = 0; q < md.K; ++q) {
+    const int ip = md.ip[q];
+    const auto& el = mesh.elements[ip / 3];
+    double Bg[4][12];
+    grad_operator(hf.B[ip].data(), Bg);
+    int fidx[12];
+    for (int d = 0; d < 12; ++d) fidx[d] = hf.dm.free_index[2 * el.nodes[d / 2] + d % 2];
+    for (int r = 0; r < 4; ++r)
+      for (int a = 0; a < n; ++a) {
+        double s = 0.0;
+        for (int d = 0; d < 12; ++d)
+          if (fidx[d] >= 0) s += Bg[r][d] * md.phi[(size_t)fidx[d] * n + a];
+        G4[((size_t)q * 4 + r) * n + a] = s;
+      }
+  }
+  return G4;
+}
+
+// config-2 paths: H ~ U[-0.08, 0.08]^4 (H00, H01, H10, H11), redrawn until
+// det(I + H) > 0.8; increments H_k = (k / n_incr) H.
+inline void make_path_fs(std::uint64_t seed, std::int64_t p, int n_incr, double* Hout) {
+  Rng rng(path_seed(seed, p));
+  double H[4];
+  while (true) {
+    for (double& h : H) h = rng.uniform(-0.08, 0.08);
+    const double det = (1.0 + H[0]) * (1.0 + H[3]) - H[1] * H[2];
+    if (det > 0.8) break;
+  }
+  for (int k = 1; k <= n_incr; ++k) {
+    const double f = static_cast<double>(k) / n_incr;
+    for (int i = 0; i < 4; ++i) Hout[(k - 1) * 4 + i] = H[i] * f;
+  }
+}
+
+struct HromFs {
+  int n = 0, K = 0;
+  std::vector<double> G;  // [K][4][n]
+  std::vector<double> w;
+  std::vector<int> mat;
+  std::vector<Mat> mats;
+  double volume = 0.0;
+};
+
+struct AssemblyFs {
+  std::vector<double> r, Kaa, KaF, KFa;  // n, n*n, n*4, 4*n
+  double CFF[16], P_raw[4];
+  std::vector<State> states;
+  std::vector<uint8_t> plastic;
+  int plastic_count = 0;
+  double rn = 0.0;
+};
+
+// F_q = I + H + G4_q α ; P, A per point ; weighted sums.
+inline void fs_assemble(const HromFs& h, const double* alpha, const double* H, const std::vector<State>& s0,
+                        bool with_K, AssemblyFs& A) {
+  const int n = h.n;
+  A.r.assign(n, 0.0);
+  if (with_K) {
+    A.Kaa.assign((size_t)n * n, 0.0);
+    A.KaF.assign((size_t)n * 4, 0.0);
+    A.KFa.assign((size_t)4 * n, 0.0);
+  }
+  for (double& v : A.CFF) v = 0.0;
+  for (double& v : A.P_raw) v = 0.0;
+  A.states.resize(h.K);
+  A.plastic.assign(h.K, 0);
+  A.plastic_count = 0;
+  const double I4[4] = {1.0, 0.0, 0.0, 1.0};
+  std::vector<double> Hq((size_t)4 * n);
+  for (int q = 0; q < h.K; ++q) {
+    const double* Gq = h.G.data() + (size_t)q * 4 * n;
+    double F[4];
+    for (int r = 0; r < 4; ++r) {
+      double s = 0.0;
+      for (int a = 0; a < n; ++a) s += Gq[r * n + a] * alpha[a];
+      F[r] = (I4[r] + H[r]) + s;
+    }
+    const FsResult res = update_biot(h.mats[h.mat[q]], s0[q], F);
+    A.states[q] = res.state;
+    A.plastic[q] = res.plastic ? 1 : 0;
+    A.plastic_count += res.plastic ? 1 : 0;
+    const double wq = h.w[q];
+    double wP[4];
+    for (int r = 0; r < 4; ++r) {
+      wP[r] = wq * res.P[r];
+      A.P_raw[r] += wP[r];
+    }
+    for (int a = 0; a < n; ++a)
+      A.r[a] += Gq[a] * wP[0] + Gq[n + a] * wP[1] + Gq[2 * n + a] * wP[2] + Gq[3 * n + a] * wP[3];
+    if (!with_K) continue;
+    double wA[4][4];
+    for (int r = 0; r < 4; ++r)
+      for (int s = 0; s < 4; ++s) {
+        wA[r][s] = wq * res.A[r * 4 + s];
+        A.CFF[r * 4 + s] += wA[r][s];
+      }
+    for (int r = 0; r < 4; ++r)  // Hq = wA G_q (4 x n)
+      for (int b = 0; b < n; ++b)
+        Hq[r * n + b] = wA[r][0] * Gq[b] + wA[r][1] * Gq[n + b] + wA[r][2] * Gq[2 * n + b] + wA[r][3] * Gq[3 * n + b];
+    for (int r = 0; r < 4; ++r)
+      for (int b = 0; b < n; ++b) A.KFa[r * n + b] += Hq[r * n + b];
+    for (int a = 0; a < n; ++a) {
+      const double g0 = Gq[a], g1 = Gq[n + a], g2 = Gq[2 * n + a], g3 = Gq[3 * n + a];
+      for (int s = 0; s < 4; ++s) A.KaF[a * 4 + s] += g0 * wA[0][s] + g1 * wA[1][s] + g2 * wA[2][s] + g3 * wA[3][s];
+      double* Krow = A.Kaa.data() + (size_t)a * n;
+      for (int b = 0; b < n; ++b) Krow[b] += g0 * Hq[b] + g1 * Hq[n + b] + g2 * Hq[2 * n + b] + g3 * Hq[3 * n + b];
+    }
+  }
+  A.rn = norm2(A.r.data(), n);
+}
+
+struct PointResultFs {
+  bool converged = false;
+  int iterations = 0;
+  double rn = 0.0;
+  std::vector<double> alpha;
+  AssemblyFs A;
+};
+
+inline PointResultFs fs_newton(const HromFs& h, const std::vector<double>& alpha0, const double* H,
+                               const std::vector<State>& s0, double tol, int max_iter) {
+  const int n = h.n;
+  PointResultFs pr;
+  std::vector<double> alpha = alpha0, du(n), mres(n), ta(n);
+  AssemblyFs& A = pr.A;
+  AssemblyFs T;
+  double ref = 0.0;
+  for (int it = 0; it <= max_iter; ++it) {
+    fs_assemble(h, alpha.data(), H, s0, true, A);
+    const double rn = A.rn;
+    if (it == 0) ref = std::max({rn, norm2(A.P_raw, 4), 1e-30});
+    if (rn <= tol * ref) {
+      pr.converged = true;
+      pr.iterations = it;
+      pr.rn = rn;
+      pr.alpha = alpha;
+      return pr;
+    }
+    if (it == max_iter) {
+      pr.rn = rn;
+      break;
+    }
+    Lu lu;
+    require(lu.factor(A.Kaa, n), ErrorCode::solver, "reduced stiffness factorization failed");
+    for (int i = 0; i < n; ++i) mres[i] = -A.r[i];
+    lu.solve(mres.data(), du.data());
+    double a = 1.0, best_a = 1.0, best_rn = std::numeric_limits<double>::infinity();
+    for (int ls = 0; ls < 8; ++ls) {
+      for (int i = 0; i < n; ++i) ta[i] = alpha[i] + a * du[i];
+      fs_assemble(h, ta.data(), H, s0, false, T);
+      if (T.rn < best_rn) {
+        best_rn = T.rn;
+        best_a = a;
+      }
+      if (T.rn <= (1.0 - 1e-4 * a) * rn) break;
+      a *= 0.5;
+    }
+    for (int i = 0; i < n; ++i) alpha[i] = alpha[i] + best_a * du[i];
+  }
+  pr.converged = false;
+  pr.iterations = max_iter;
+  pr.alpha = alpha;
+  return pr;
+}
+
+// A_M = (C_FF - K_Fa K_aa^-1 K_aF) / V ; P_M = P_raw / V
+inline void fs_condense(const HromFs& h, const AssemblyFs& A, double* P, double* AM) {
+  const int n = h.n;
+  for (int r = 0; r < 4; ++r) P[r] = A.P_raw[r] / h.volume;
+  Lu lu;
+  require(lu.factor(A.Kaa, n), ErrorCode::solver, "condensation: singular reduced stiffness");
+  double c[16];
+  for (int k = 0; k < 16; ++k) c[k] = A.CFF[k];
+  std::vector<double> rhs(n), y(n);
+  for (int s = 0; s < 4; ++s) {
+    for (int a = 0; a < n; ++a) rhs[a] = -A.KaF[a * 4 + s];
+    lu.solve(rhs.data(), y.data());
+    for (int r = 0; r < 4; ++r) {
+      double t = 0.0;
+      for (int a = 0; a < n; ++a) t += A.KFa[r * n + a] * y[a];
+      c[r * 4 + s] += t;
+    }
+  }
+  for (int k = 0; k < 16; ++k) AM[k] = c[k] / h.volume;
+}
+
+inline void fs_point_trajectory(const HromFs& h, std::int64_t pi, int n_incr, const double* Hp, double tol,
+                                int max_iter, int max_bis, orc_hrom_out_t* out) {
+  const int n = h.n, K = h.K;
+  std::vector<double> alpha_c(n, 0.0);
+  std::vector<State> states(K);
+  double H_prev[4] = {0, 0, 0, 0};
+  bool dead = false;
+  for (int k = 0; k < n_incr; ++k) {
+    const std::int64_t o = pi * n_incr + k;
+    const double* Hk = Hp + 4 * k;
+    int iters = 0, bis = 0, status = 0, pc = 0;
+    double P[4], AM[16], rn = NAN;
+    for (double& v : P) v = NAN;
+    for (double& v : AM) v = NAN;
+    if (!dead) {
+      double done = 0.0, frac = 1.0;
+      while (done < 1.0 - 1e-12) {
+        const double target = std::min(1.0, done + frac);
+        double H[4];
+        for (int i = 0; i < 4; ++i) H[i] = H_prev[i] + (Hk[i] - H_prev[i]) * target;
+        PointResultFs pr;
+        try {
+          pr = fs_newton(h, alpha_c, H, states, tol, max_iter);
+        } catch (const Error& e) {
+          status = 1 + (int)e.code;
+          dead = true;
+          break;
+        }
+        iters += pr.iterations;
+        rn = pr.rn;
+        if (!pr.converged) {
+          if (++bis > max_bis) {
+            status = 1 + (int)ErrorCode::solver;
+            dead = true;
+            break;
+          }
+          frac *= 0.5;
+          continue;
+        }
+        try {
+          fs_condense(h, pr.A, P, AM);
+        } catch (const Error& e) {
+          status = 1 + (int)e.code;
+          dead = true;
+          break;
+        }
+        states = pr.A.states;
+        alpha_c = pr.alpha;
+        pc = pr.A.plastic_count;
+        if (out->plastic_flags)
+          std::memcpy(out->plastic_flags + (size_t)o * K, pr.A.plastic.data(), (size_t)K);
+        done = target;
+      }
+    } else {
+      status = 1 + (int)ErrorCode::solver;
+    }
+    if (status != 0) {
+      for (double& v : P) v = NAN;
+      for (double& v : AM) v = NAN;
+    }
+    if (out->sigma) std::memcpy(out->sigma + o * 4, P, sizeof P);
+    if (out->C) std::memcpy(out->C + o * 16, AM, sizeof AM);
+    if (out->iters) out->iters[o] = iters;
+    if (out->plastic_count) out->plastic_count[o] = pc;
+    if (out->res_norm) out->res_norm[o] = rn;
+    if (out->status) out->status[o] = status;
+    if (out->bisections) out->bisections[o] = bis;
+    for (int i = 0; i < 4; ++i) H_prev[i] = Hk[i];
+  }
+  if (out->alpha) std::memcpy(out->alpha + pi * n, alpha_c.data(), sizeof(double) * n);
+  if (out->state)
+    for (int q = 0; q < K; ++q) {
+      double* s = out->state + ((size_t)pi * K + q) * 6;
+      for (int c = 0; c < 4; ++c) s[c] = states[q].ep[c];
+      s[4] = states[q].eq;
+      s[5] = states[q].s33;
+    }
+}
+
 }  // namespace orc
 
 // ===========================================================================
@@ -1431,6 +1821,84 @@ int orc_hrom_assemble(orc_hrom_t h, const double* alpha, const double* E, const 
     std::memcpy(KaE, A.KaE.data(), sizeof(double) * h->h.n * 3);
     std::memcpy(C_EE, A.C_EE, sizeof A.C_EE);
     std::memcpy(S_raw, A.S_raw, sizeof A.S_raw);
+    if (plastic_count) *plastic_count = A.plastic_count;
+  });
+}
+
+// ---- finite strain (config 2; parity unpinned, see update_biot)
+struct orc_hrom_fs_s {
+  HromFs h;
+};
+
+int orc_update_biot(const orc_material_t* mat, const double* state_in6, const double* F4, double* P4, double* A16,
+                    double* state_out6, int* plastic) {
+  return guarded([&] {
+    const Mat m = to_mat(*mat);
+    const FsResult r = update_biot(m, unpack_state(state_in6), F4);
+    std::memcpy(P4, r.P, sizeof r.P);
+    std::memcpy(A16, r.A, sizeof r.A);
+    if (state_out6) pack_state(r.state, state_out6);
+    if (plastic) *plastic = r.plastic ? 1 : 0;
+  });
+}
+
+int orc_model_g4(int subdivisions, int n, int K, uint64_t seed, double* G4) {
+  return guarded([&] {
+    const Mesh mesh = build_rve_mesh(default_cell(subdivisions));
+    const Model md = build_model(mesh, n, K, seed);
+    const std::vector<double> g = build_g4(mesh, md);
+    std::memcpy(G4, g.data(), g.size() * sizeof(double));
+  });
+}
+
+int orc_paths_fs(uint64_t seed, int64_t p0, int64_t P, int n_incr, double* H) {
+  return guarded([&] {
+    for (int64_t p = 0; p < P; ++p) make_path_fs(seed, p0 + p, n_incr, H + (size_t)p * n_incr * 4);
+  });
+}
+
+int orc_hrom_fs_create(int n, int K, const double* G4, const double* w, const int* mat_id, const orc_material_t* mats,
+                       int n_mats, double volume, orc_hrom_fs_t* out) {
+  return guarded([&] {
+    require(n >= 1 && K >= 1, ErrorCode::config, "n and K must be positive");
+    auto* h = new orc_hrom_fs_s;
+    h->h.n = n;
+    h->h.K = K;
+    h->h.G.assign(G4, G4 + (size_t)K * 4 * n);
+    h->h.w.assign(w, w + K);
+    h->h.mat.assign(mat_id, mat_id + K);
+    for (int i = 0; i < n_mats; ++i) h->h.mats.push_back(to_mat(mats[i]));
+    h->h.volume = volume;
+    *out = h;
+  });
+}
+void orc_hrom_fs_free(orc_hrom_fs_t h) { delete h; }
+
+int orc_hrom_fs_run(orc_hrom_fs_t h, int64_t P, int n_incr, const double* H, const orc_newton_opts_t* opts,
+                    int n_threads, orc_hrom_out_t* out) {
+  return guarded([&] {
+    parallel_for(P, n_threads, [&](int64_t p) {
+      fs_point_trajectory(h->h, p, n_incr, H + (size_t)p * n_incr * 4, opts->tol, opts->max_iter,
+                          opts->max_bisections, out);
+    });
+  });
+}
+
+int orc_hrom_fs_assemble(orc_hrom_fs_t h, const double* alpha, const double* H, const double* state, double* r,
+                         double* Kaa, double* KaF, double* KFa, double* CFF, double* P_raw, int* plastic_count) {
+  return guarded([&] {
+    std::vector<State> s0(h->h.K);
+    if (state)
+      for (int q = 0; q < h->h.K; ++q) s0[q] = unpack_state(state + (size_t)q * 6);
+    AssemblyFs A;
+    fs_assemble(h->h, alpha, H, s0, true, A);
+    const int n = h->h.n;
+    std::memcpy(r, A.r.data(), sizeof(double) * n);
+    std::memcpy(Kaa, A.Kaa.data(), sizeof(double) * n * n);
+    std::memcpy(KaF, A.KaF.data(), sizeof(double) * n * 4);
+    std::memcpy(KFa, A.KFa.data(), sizeof(double) * 4 * n);
+    std::memcpy(CFF, A.CFF, sizeof A.CFF);
+    std::memcpy(P_raw, A.P_raw, sizeof A.P_raw);
     if (plastic_count) *plastic_count = A.plastic_count;
   });
 }

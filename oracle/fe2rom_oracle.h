@@ -136,6 +136,25 @@ int orc_hrom_assemble(orc_hrom_t h, const double* alpha, const double* E, const 
                       double* r, double* Kaa, double* KaE, double* C_EE, double* S_raw,
                       int* plastic_count);
 
+/* ---- finite strain, Biot stress (BASELINE config 2) — PARITY UNPINNED:
+ * the reference has no finite-strain code. Components ordered (F00, F01,
+ * F10, F11); P = R T(U - I); A = dP/dF row-major 4x4. */
+int orc_update_biot(const orc_material_t* mat, const double* state_in6, const double* F4, double* P4, double* A16,
+                    double* state_out6, int* plastic);
+/* 4-row displacement-gradient operator G4[K][4][n] of orc_model_build(subdivisions, n, K, seed) */
+int orc_model_g4(int subdivisions, int n, int K, uint64_t seed, double* G4);
+/* config-2 paths: H[P][n_incr][4] (F = I + H), det(I + H_end) > 0.8 */
+int orc_paths_fs(uint64_t seed, int64_t p0, int64_t P, int n_incr, double* H);
+typedef struct orc_hrom_fs_s* orc_hrom_fs_t;
+int orc_hrom_fs_create(int n, int K, const double* G4, const double* w, const int* mat_id, const orc_material_t* mats,
+                       int n_mats, double volume, orc_hrom_fs_t* out);
+void orc_hrom_fs_free(orc_hrom_fs_t h);
+/* outputs as orc_hrom_out_t with sigma -> P_M [P][n_incr][4], C -> A_M [P][n_incr][16] */
+int orc_hrom_fs_run(orc_hrom_fs_t h, int64_t P, int n_incr, const double* H, const orc_newton_opts_t* opts,
+                    int n_threads, orc_hrom_out_t* out);
+int orc_hrom_fs_assemble(orc_hrom_fs_t h, const double* alpha, const double* H, const double* state, double* r,
+                         double* Kaa, double* KaF, double* KFa, double* CFF, double* P_raw, int* plastic_count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -258,3 +258,85 @@ class Hrom:
         _check(lib.orc_hrom_assemble(self._h, _d(alpha), _d(E), _d(st), _d(r), _d(Kaa), _d(KaE), _d(CEE), _d(S),
                                      C.byref(pc)))
         return dict(r=r, Kaa=Kaa, KaE=KaE, C_EE=CEE, S_raw=S, plastic_count=pc.value)
+
+
+# ---- finite strain, Biot stress (config 2; parity unpinned) ----------------
+lib.orc_update_biot.argtypes = [C.POINTER(_Mat), _dp, _dp, _dp, _dp, _dp, _ip]
+lib.orc_model_g4.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, _dp]
+lib.orc_paths_fs.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int, _dp]
+lib.orc_hrom_fs_create.argtypes = [C.c_int, C.c_int, _dp, _dp, _ip, C.POINTER(_Mat), C.c_int, C.c_double,
+                                   C.POINTER(C.c_void_p)]
+lib.orc_hrom_fs_free.argtypes = [C.c_void_p]
+lib.orc_hrom_fs_run.argtypes = [C.c_void_p, C.c_int64, C.c_int, _dp, C.POINTER(_Opts), C.c_int, C.POINTER(_Out)]
+lib.orc_hrom_fs_assemble.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _ip]
+
+
+def update_biot(mat, state, F4):
+    """Returns P(4), A(4,4), state_out(6), plastic."""
+    m = mat_struct(mat)
+    st = np.zeros(6) if state is None else np.ascontiguousarray(state, dtype=np.float64)
+    F = np.ascontiguousarray(F4, dtype=np.float64)
+    P, A, so, pl = np.empty(4), np.empty((4, 4)), np.empty(6), C.c_int()
+    _check(lib.orc_update_biot(C.byref(m), _d(st), _d(F), _d(P), _d(A), _d(so), C.byref(pl)))
+    return P, A, so, bool(pl.value)
+
+
+def model_g4(subdivisions, n, K, seed):
+    G4 = np.empty((K, 4, n))
+    _check(lib.orc_model_g4(subdivisions, n, K, seed, _d(G4)))
+    return G4
+
+
+def paths_fs(seed, P, n_incr, p0=0):
+    H = np.empty((P, n_incr, 4))
+    _check(lib.orc_paths_fs(seed, p0, P, n_incr, _d(H)))
+    return H
+
+
+class HromFs:
+    """Oracle of the finite-strain (Biot) hyper-ROM path."""
+
+    def __init__(self, G4, w, mat_id, materials, volume):
+        G4 = np.ascontiguousarray(G4, dtype=np.float64)
+        self.K, _, self.n = G4.shape
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        mid = np.ascontiguousarray(mat_id, dtype=np.int32)
+        mats = (_Mat * len(materials))(*[mat_struct(m) for m in materials])
+        h = C.c_void_p()
+        _check(lib.orc_hrom_fs_create(self.n, self.K, _d(G4), _d(w), _i(mid), mats, len(materials), float(volume),
+                                      C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.orc_hrom_fs_free(self._h)
+
+    def run(self, H, tol=1e-8, max_iter=30, max_bisections=4, threads=1, flags=False, final_state=False):
+        H = np.ascontiguousarray(H, dtype=np.float64)
+        P, k, _ = H.shape
+        res = dict(P=np.empty((P, k, 4)), A=np.empty((P, k, 4, 4)), iters=np.empty((P, k), dtype=np.int32),
+                   plastic_count=np.empty((P, k), dtype=np.int32), res_norm=np.empty((P, k)),
+                   status=np.empty((P, k), dtype=np.int32), bisections=np.empty((P, k), dtype=np.int32))
+        if flags:
+            res["plastic_flags"] = np.zeros((P, k, self.K), dtype=np.uint8)
+        if final_state:
+            res["alpha"] = np.empty((P, self.n))
+            res["state"] = np.empty((P, self.K, 6))
+        o = _Out(_d(res["P"]), _d(res["A"]), _i(res["iters"]), _i(res["plastic_count"]), _d(res["res_norm"]),
+                 _i(res["status"]), _i(res["bisections"]),
+                 res["plastic_flags"].ctypes.data_as(_u8p) if flags else None,
+                 _d(res.get("alpha")), _d(res.get("state")))
+        opts = _Opts(tol, max_iter, max_bisections)
+        _check(lib.orc_hrom_fs_run(self._h, P, k, _d(H), C.byref(opts), threads, C.byref(o)))
+        return res
+
+    def assemble(self, alpha, H, state=None):
+        n = self.n
+        alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+        H = np.ascontiguousarray(H, dtype=np.float64)
+        st = None if state is None else np.ascontiguousarray(state, dtype=np.float64)
+        r, Kaa, KaF, KFa = np.empty(n), np.empty((n, n)), np.empty((n, 4)), np.empty((4, n))
+        CFF, Praw, pc = np.empty((4, 4)), np.empty(4), C.c_int()
+        _check(lib.orc_hrom_fs_assemble(self._h, _d(alpha), _d(H), _d(st), _d(r), _d(Kaa), _d(KaF), _d(KFa), _d(CFF),
+                                        _d(Praw), C.byref(pc)))
+        return dict(r=r, Kaa=Kaa, KaF=KaF, KFa=KFa, C_FF=CFF, P_raw=Praw, plastic_count=pc.value)
