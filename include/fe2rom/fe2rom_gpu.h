@@ -21,6 +21,9 @@
  *   fe2_hrom_read_state        <- MicroResult::states / MaterialState   rve.hpp:207,
  *                                 materials.hpp:102-106
  *   fe2_last_error             <- fe2rom::Error::what()  common.hpp:39-46
+ *   fe2_hrom_create_fs         <- (no reference counterpart: finite-strain Biot
+ *                                 variant of BASELINE config 2, SURVEY.md §8 a15;
+ *                                 parity unpinned, checked against oracle fs_*)
  *
  * Conventions
  *   - Strain is engineering Voigt (E11, E22, g12), stress (S11, S22, S12)
@@ -36,6 +39,10 @@
  *   - The caller owns host arrays; the library owns device buffers. A handle
  *     is bound to one device and is not thread-safe. Multi-GPU = one handle
  *     per device (one process per GPU); points are sharded, never split.
+ *   - Finite-strain handles (fe2_hrom_create_fs) take the macro displacement
+ *     gradient H = F - I as (H00, H01, H10, H11) in place of E, return the
+ *     first Piola-Kirchhoff stress P_M[4] in place of sigma and the tangent
+ *     A_M = dP_M/dF row-major 4x4 in place of C; everything else is shared.
  *   - There is no CPU fallback: without a usable sm_100 device every compute
  *     entry point fails with code 6 (numeric) and a message.
  */
@@ -84,6 +91,19 @@ int fe2_material_update_batch(int device, const fe2_material_t* mat, int64_t N, 
 int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, const int* mat_id,
                     const fe2_material_t* mats, int n_mats, double volume, fe2_hrom_t* out);
 void fe2_hrom_destroy(fe2_hrom_t h);
+
+/* ---- finite-strain (Biot stress) hyper-ROM model (BASELINE config 2).
+ * G4[K][4][n] is the displacement-gradient operator (rows dux/dX, dux/dY,
+ * duy/dX, duy/dY; fe2_model_g4), n <= 32, at most one J2 and one elastic
+ * material. Solve calls then take H[P*4] and return P_M[P*4], A_M[P*16]. */
+int fe2_hrom_create_fs(int device, int n, int K, const double* G4, const double* w, const int* mat_id,
+                       const fe2_material_t* mats, int n_mats, double volume, fe2_hrom_t* out);
+/* 0 = small strain (fe2_hrom_create), 1 = finite strain (fe2_hrom_create_fs) */
+int fe2_hrom_kinematics(fe2_hrom_t h, int* kinematics);
+/* finite-strain assembly of a point's committed history at (α, H): r[n],
+ * Kaa[n*n], KaF[n*4], KFa[4*n], C_FF[16], P_raw[4] (host) */
+int fe2_hrom_fs_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, const double* H, double* r,
+                               double* Kaa, double* KaF, double* KFa, double* C_FF, double* P_raw);
 
 /* Allocate P macro points in the virgin state (α = 0, MaterialState{}).
  * keep_flags != 0 also keeps per-(point, cubature point) plastic flags of
@@ -151,8 +171,12 @@ int fe2_model_build(int subdivisions, int n, int K, uint64_t seed, fe2_model_t* 
 void fe2_model_free(fe2_model_t m);
 int fe2_model_sizes(fe2_model_t m, int* n, int* K, int* n_free, double* volume);
 int fe2_model_arrays(fe2_model_t m, double* G, double* w, int* ip_id, int* mat_id);
-/* path kind 0 = config-0 uniaxial rotated, 1 = config-1 reversal;
- * E[P][n_incr][3] for global points p0..p0+P-1 */
+/* G4[K][4][n]: the displacement-gradient operator of the same Φ and cubature */
+int fe2_model_g4(fe2_model_t m, double* G4);
+/* path kind 0 = config-0 uniaxial rotated, 1 = config-1 reversal:
+ * E[P][n_incr][3]; kind 2 = config-2 finite strain: H[P][n_incr][4]
+ * (F = I + (k/n_incr) H_end, H_end ~ U[-0.08, 0.08]^4 with det F > 0.8),
+ * for global points p0..p0+P-1 */
 int fe2_paths(int kind, uint64_t seed, int64_t p0, int64_t P, int n_incr, double* E);
 
 #ifdef __cplusplus

@@ -1193,7 +1193,8 @@ inline void hrom_point_trajectory(const Hrom& h, std::int64_t pi, int n_incr, co
 // scope; the paper's biot_stress section is absent from PAPER.md:19-20), so
 // this is our formulation, checked only for self-consistency (FD tangents,
 // objectivity, small-strain limit) in tests/test_oracle_fs.py:
-//   F = R U (2-D polar decomposition, R by the angle atan2(F10-F01, F00+F11)),
+//   F = R U (2-D polar decomposition: R = rotation by θ = atan2(F10-F01, F00+F11),
+//   cos θ and sin θ formed directly as (F00+F11)/ρ, (F10-F01)/ρ),
 //   Biot strain U - I -> the pinned small-strain update4 (J2 / elastic) gives
 //   the Biot stress T, P = R T (first Piola-Kirchhoff), A = dP/dF closed form.
 // Components are ordered (F00, F01, F10, F11) = (dx/dX, dx/dY, dy/dX, dy/dY).
@@ -1206,8 +1207,9 @@ struct FsResult {
 
 inline FsResult update_biot(const Mat& m, const State& s0, const double* F) {
   const double num = F[2] - F[1], den = F[0] + F[3];
-  const double th = std::atan2(num, den);
-  const double c = std::cos(th), s = std::sin(th);
+  const double rho2 = num * num + den * den;
+  const double rho = std::sqrt(rho2);
+  const double c = den / rho, s = num / rho;  // R(θ), θ = atan2(num, den)
   // U = R^T F
   const double U00 = c * F[0] + s * F[2], U01 = c * F[1] + s * F[3];
   const double U10 = -s * F[0] + c * F[2], U11 = -s * F[1] + c * F[3];
@@ -1221,7 +1223,6 @@ inline FsResult update_biot(const Mat& m, const State& s0, const double* F) {
   out.P[3] = s * T01 + c * T11;
   out.state = r4.state;
   out.plastic = r4.plastic;
-  const double rho2 = num * num + den * den;
   const double g[4] = {-num / rho2, -den / rho2, den / rho2, -num / rho2};  // dθ/dF
   // R J T with J = [[0,-1],[1,0]]: (RJ) = [[-s,-c],[c,-s]]
   const double RJT00 = -s * T00 - c * T01, RJT01 = -s * T01 - c * T11;

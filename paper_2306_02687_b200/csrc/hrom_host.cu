@@ -75,8 +75,10 @@ struct fe2_hrom_s {
   int device = 0, num_sms = 148;
   cudaStream_t stream = nullptr;  // work stream (own, or the caller's)
   cudaStream_t own_stream = nullptr;
-  int n = 0, NP = 0, S = 0, K = 0, K2 = 0, K2p = 0;
+  int kin = 0;  // 0 small strain (E, sigma, C), 1 finite strain (H, P, A)
+  int n = 0, NP = 0, S = 0, K = 0, K2 = 0, K2p = 0, Kel = 0, Kelp = 0;
   double volume = 0.0;
+  MatDev matE{};  // finite strain: the elastic material
   std::vector<int> j2_idx, el_idx;  // original cubature indices
   std::vector<double> G, w;         // host copy (caller order)
   std::vector<MatDev> qmat;         // per original cubature point
@@ -101,6 +103,8 @@ struct fe2_hrom_s {
   fe2_hrom_stats_t stats{};
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
+  int ncomp() const { return kin ? 4 : 3; }   // macro input / stress components
+  int ntan() const { return kin ? 16 : 9; }    // macro tangent entries
   ModelDev model() const {
     ModelDev M{};
     M.n = n;
@@ -108,7 +112,10 @@ struct fe2_hrom_s {
     M.S = S;
     M.K2 = K2;
     M.K2p = K2p;
-    M.nchunks = K2p / kQC;
+    M.nchunks = (K2p + Kelp) / kQC;
+    M.nch_hist = K2p / kQC;
+    M.K_el = Kel;
+    M.matE = matE;
     M.G2 = G2;
     M.w2 = w2;
     M.Ke = Ke;
@@ -155,7 +162,7 @@ struct fe2_hrom_s {
     const size_t an = static_cast<size_t>(P) * NP * sizeof(double);
     CK(cudaMemsetAsync(alpha_c, 0, an, s));
     CK(cudaMemsetAsync(bp, 0, an, s));
-    CK(cudaMemsetAsync(E_c, 0, P * 3 * sizeof(double), s));
+    CK(cudaMemsetAsync(E_c, 0, P * ncomp() * sizeof(double), s));
     CK(cudaMemsetAsync(sp, 0, P * 4 * sizeof(double), s));
     CK(cudaMemsetAsync(st, 0, P * sizeof(PointState), s));
     if (flags) CK(cudaMemsetAsync(flags, 0, static_cast<size_t>(P) * K2p, s));
@@ -180,8 +187,10 @@ struct fe2_hrom_s {
 
 namespace {
 
-void launch_any(const IncArgs& a, int num_sms, cudaStream_t s) {
-  if (a.M.NP <= 32)
+void launch_any(fe2_hrom_t h, const IncArgs& a, int num_sms, cudaStream_t s) {
+  if (h->kin == 1)
+    launch_increment_fs(a, num_sms, s);
+  else if (a.M.NP <= 32)
     launch_increment(a, num_sms, s);
   else
     check(launch_increment_big(a, num_sms, s), Code::config, "unsupported mode count");
@@ -200,6 +209,27 @@ Eps3 strain_at(fe2_hrom_t h, int64_t p, int q, const double* ac, const double* E
     for (int a = 0; a < n; ++a) s += Gq[i * n + a] * ac[p * NP + a];
     e.v[i] = Ec[p * 3 + i] + s;
   }
+  return e;
+}
+
+// finite strain: Biot strain (U00 - 1, U11 - 1) of the committed F_q = I + H_c + G4_q alpha_c
+Eps3 biot_strain_at(fe2_hrom_t h, int64_t p, int q, const double* ac, const double* Hc) {
+  const int n = h->n, NP = h->NP;
+  const double* Gq = h->G.data() + static_cast<size_t>(q) * 4 * n;
+  const double I4[4] = {1.0, 0.0, 0.0, 1.0};
+  double F[4];
+  for (int i = 0; i < 4; ++i) {
+    double s = 0.0;
+    for (int a = 0; a < n; ++a) s += Gq[i * n + a] * ac[p * NP + a];
+    F[i] = (I4[i] + Hc[p * 4 + i]) + s;
+  }
+  const double num = F[2] - F[1], den = F[0] + F[3];
+  const double rho = std::sqrt(num * num + den * den);
+  const double c = den / rho, sn = num / rho;
+  Eps3 e;
+  e.v[0] = (c * F[0] + sn * F[2]) - 1.0;
+  e.v[1] = (-sn * F[1] + c * F[3]) - 1.0;
+  e.v[2] = 0.0;
   return e;
 }
 
@@ -272,7 +302,7 @@ void run_increment(fe2_hrom_t h, const double* d_E, const NewtonCfg& cfg, const 
   Watchdog wd(h->num_sms);
   a.trace = wd.dev;
   if (h->timing) CK(cudaEventRecord(h->ev[0], s));
-  launch_any(a, h->num_sms, s);
+  launch_any(h, a, h->num_sms, s);
   CK(cudaGetLastError());
   if (h->timing) CK(cudaEventRecord(h->ev[1], s));
   wd.wait(s, "k_increment");
@@ -478,14 +508,14 @@ int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
     h->hist = dalloc<double>(static_cast<size_t>(P) * h->K2p * 5);
     h->alpha_c = dalloc<double>(static_cast<size_t>(P) * h->NP);
     h->bp = dalloc<double>(static_cast<size_t>(P) * h->NP);
-    h->E_c = dalloc<double>(P * 3);
+    h->E_c = dalloc<double>(P * h->ncomp());
     h->sp = dalloc<double>(P * 4);
     h->st = dalloc<PointState>(P);
     h->keep_flags = keep_flags != 0;
     if (h->keep_flags) h->flags = dalloc<uint8_t>(static_cast<size_t>(P) * h->K2p);
-    h->dE = dalloc<double>(P * 3);
-    h->o_sigma = dalloc<double>(P * 3);
-    h->o_C = dalloc<double>(P * 9);
+    h->dE = dalloc<double>(P * h->ncomp());
+    h->o_sigma = dalloc<double>(P * h->ncomp());
+    h->o_C = dalloc<double>(P * h->ntan());
     h->o_res = dalloc<double>(P);
     h->o_iters = dalloc<int>(P);
     h->o_status = dalloc<int>(P);
@@ -539,11 +569,11 @@ int fe2_hrom_solve_increment(fe2_hrom_t h, const double* E, const fe2_newton_opt
     const NewtonCfg cfg = make_cfg(opts);
     const int64_t P = h->P;
     cudaStream_t s = h->stream;
-    CK(cudaMemcpyAsync(h->dE, E, P * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(h->dE, E, P * h->ncomp() * sizeof(double), cudaMemcpyHostToDevice, s));
     Outputs O{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc};
     run_increment(h, h->dE, cfg, O, s);
-    if (sigma) CK(cudaMemcpyAsync(sigma, h->o_sigma, P * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (C) CK(cudaMemcpyAsync(C, h->o_C, P * 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (sigma) CK(cudaMemcpyAsync(sigma, h->o_sigma, P * h->ncomp() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (C) CK(cudaMemcpyAsync(C, h->o_C, P * h->ntan() * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (iters) CK(cudaMemcpyAsync(iters, h->o_iters, P * sizeof(int), cudaMemcpyDeviceToHost, s));
     if (plastic_count) CK(cudaMemcpyAsync(plastic_count, h->o_pc, P * sizeof(int), cudaMemcpyDeviceToHost, s));
     if (res_norm) CK(cudaMemcpyAsync(res_norm, h->o_res, P * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -566,13 +596,31 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
       for (int64_t p = 0; p < P; ++p)
         for (int a = 0; a < n; ++a) alpha[p * n + a] = ac[p * NP + a];
     if (state) {
-      std::vector<double> hs(static_cast<size_t>(P) * K2p * 5), Ec(static_cast<size_t>(P) * 3);
+      std::vector<double> hs(static_cast<size_t>(P) * K2p * 5), Ec(static_cast<size_t>(P) * h->ncomp());
       CK(cudaMemcpy(hs.data(), h->hist, hs.size() * sizeof(double), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(Ec.data(), h->E_c, Ec.size() * sizeof(double), cudaMemcpyDeviceToHost));
       auto hidx = [&](int64_t p, int q2, int comp) {  // [P][K2p/32][5][32]
         return (static_cast<size_t>(p) * (K2p / kQC) + q2 / kQC) * (5 * kQC) + comp * kQC + q2 % kQC;
       };
-      for (int64_t p = 0; p < P; ++p) {
+      for (int64_t p = 0; p < P && h->kin == 1; ++p) {
+        // finite strain: sigma33 of the Biot stress from the committed U - I and eps_p
+        for (int q = 0; q < K; ++q) {
+          double* s = state + (static_cast<size_t>(p) * K + q) * 6;
+          for (int c = 0; c < 5; ++c) s[c] = 0.0;
+        }
+        for (int q2 = 0; q2 < h->K2; ++q2) {
+          const int q = h->j2_idx[q2];
+          double* s = state + (static_cast<size_t>(p) * K + q) * 6;
+          for (int c = 0; c < 5; ++c) s[c] = hs[hidx(p, q2, c)];
+        }
+        for (int q = 0; q < K; ++q) {
+          const Eps3 e = biot_strain_at(h, p, q, ac.data(), Ec.data());
+          double* s = state + (static_cast<size_t>(p) * K + q) * 6;
+          const MatDev& m = h->qmat[q];
+          s[5] = m.lam * ((e.v[0] - s[0]) + (e.v[1] - s[1]) + (0.0 - s[2])) + 2.0 * m.mu * (0.0 - s[2]);
+        }
+      }
+      for (int64_t p = 0; p < P && h->kin == 0; ++p) {
         // sigma33 is write-only in the reference (materials.hpp:181, :193): it is
         // not kept in HBM but recomputed here from the committed strain and eps_p,
         // sigma33 = lam tr(eps - eps_p) + 2 mu (0 - eps_p,33).
@@ -606,6 +654,7 @@ int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, co
                             double* Kaa, double* KaE, double* C_EE, double* S_raw) {
   return guard([&] {
     check(h != nullptr && h->P > 0 && point >= 0 && point < h->P, Code::config, "bad point");
+    check(h->kin == 0, Code::config, "finite-strain handle: use fe2_hrom_fs_assemble_point");
     check(alpha && E && r && Kaa && KaE && C_EE && S_raw, Code::config, "null buffer");
     CK(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
@@ -626,7 +675,7 @@ int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, co
     a.dbg_point = point;
     Watchdog wd(h->num_sms);
     a.trace = wd.dev;
-    launch_any(a, h->num_sms, s);
+    launch_any(h, a, h->num_sms, s);
     h->stats.kernel_launches += 1;
     CK(cudaGetLastError());
     wd.wait(s, "k_increment (assembly dump)");
@@ -674,6 +723,131 @@ int fe2_hrom_set_timing(fe2_hrom_t h, int on) {
   return guard([&] {
     check(h != nullptr, Code::config, "bad arguments");
     h->timing = on != 0;
+  });
+}
+
+int fe2_hrom_create_fs(int device, int n, int K, const double* G4, const double* w, const int* mat_id,
+                       const fe2_material_t* mats, int n_mats, double volume, fe2_hrom_t* out) {
+  return guard([&] {
+    check(out != nullptr, Code::config, "null output handle");
+    *out = nullptr;
+    check(n >= 1 && K >= 1 && G4 && w && mat_id && mats && n_mats >= 1, Code::config, "bad model arguments");
+    check(n <= 32, Code::config, "the finite-strain path supports n <= 32 modes");
+    check(volume > 0.0, Code::config, "RVE volume must be positive");
+    std::vector<MatDev> md;
+    for (int i = 0; i < n_mats; ++i) md.push_back(to_dev(mats[i]));
+    require_device(device);
+    auto h = new fe2_hrom_s;
+    try {
+      h->kin = 1;
+      h->device = device;
+      CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+      h->n = n;
+      h->NP = (n + 7) / 8 * 8;
+      h->S = 4 * h->NP + 2;
+      h->K = K;
+      h->volume = volume;
+      h->G.assign(G4, G4 + static_cast<size_t>(K) * 4 * n);
+      h->w.assign(w, w + K);
+      int j2_mat = -1, el_mat = -1;
+      for (int q = 0; q < K; ++q) {
+        check(mat_id[q] >= 0 && mat_id[q] < n_mats, Code::config, "cubature material id out of range");
+        check(w[q] > 0.0, Code::config, "cubature weights must be positive");
+        h->qmat.push_back(md[mat_id[q]]);
+        if (md[mat_id[q]].kind == 1) {
+          check(j2_mat < 0 || j2_mat == mat_id[q], Code::config, "this build supports one J2 material per model");
+          j2_mat = mat_id[q];
+          h->j2_idx.push_back(q);
+        } else {
+          check(el_mat < 0 || el_mat == mat_id[q], Code::config,
+                "the finite-strain path supports one elastic material per model");
+          el_mat = mat_id[q];
+          h->el_idx.push_back(q);
+        }
+      }
+      h->mat2 = j2_mat >= 0 ? md[j2_mat] : make_mat(1, 1.0, 0.3, 1.0, 0.0);
+      h->matE = el_mat >= 0 ? md[el_mat] : make_mat(0, 1.0, 0.3, 0.0, 0.0);
+      h->K2 = static_cast<int>(h->j2_idx.size());
+      h->K2p = (h->K2 + kQC - 1) / kQC * kQC;
+      h->Kel = static_cast<int>(h->el_idx.size());
+      h->Kelp = (h->Kel + kQC - 1) / kQC * kQC;
+      const int NP = h->NP, S = h->S;
+      // rows [G4 row 0..3 (NP each) | w | 0]: J2 points (padded to K2p), then elastic points
+      std::vector<double> G2(static_cast<size_t>(h->K2p + h->Kelp) * S, 0.0);
+      auto put = [&](int slot, int q) {
+        for (int i = 0; i < 4; ++i)
+          for (int a = 0; a < n; ++a)
+            G2[static_cast<size_t>(slot) * S + i * NP + a] = G4[(static_cast<size_t>(q) * 4 + i) * n + a];
+        G2[static_cast<size_t>(slot) * S + 4 * NP] = w[q];
+      };
+      for (int q2 = 0; q2 < h->K2; ++q2) put(q2, h->j2_idx[q2]);
+      for (int e = 0; e < h->Kel; ++e) put(h->K2p + e, h->el_idx[e]);
+      CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+      h->stream = h->own_stream;
+      for (auto& e : h->ev) CK(cudaEventCreate(&e));
+      h->G2 = dalloc<double>(G2.size());
+      h->work = dalloc<int>(1);
+      h->cnt = dalloc<IncCounters>(1);
+      CK(cudaMallocHost(&h->h_cnt, sizeof(IncCounters)));
+      CK(cudaMemcpy(h->G2, G2.data(), G2.size() * sizeof(double), cudaMemcpyHostToDevice));
+      h->stats.n = n;
+      h->stats.K = K;
+      h->stats.K_j2 = h->K2;
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int fe2_hrom_kinematics(fe2_hrom_t h, int* kinematics) {
+  return guard([&] {
+    check(h != nullptr && kinematics != nullptr, Code::config, "bad arguments");
+    *kinematics = h->kin;
+  });
+}
+
+int fe2_hrom_fs_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, const double* H, double* r,
+                               double* Kaa, double* KaF, double* KFa, double* C_FF, double* P_raw) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0 && point >= 0 && point < h->P, Code::config, "bad point");
+    check(h->kin == 1, Code::config, "small-strain handle: use fe2_hrom_assemble_point");
+    check(alpha && H && r && Kaa && KaF && KFa && C_FF && P_raw, Code::config, "null buffer");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    const int n = h->n;
+    const size_t dn = static_cast<size_t>(n) + n * n + 8 * n + 20;
+    double* dbg = dalloc<double>(dn + n + 4);
+    CK(cudaMemcpyAsync(dbg + dn, alpha, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dbg + dn + n, H, 4 * sizeof(double), cudaMemcpyHostToDevice, s));
+    IncArgs a{};
+    a.M = h->model();
+    a.D = h->points();
+    a.O = Outputs{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc};
+    a.cfg = NewtonCfg{1e-8, 30, 4};
+    a.work = h->work;
+    a.dbg = dbg;
+    a.dbg_alpha = dbg + dn;
+    a.dbg_E = dbg + dn + n;
+    a.dbg_point = point;
+    Watchdog wd(h->num_sms);
+    a.trace = wd.dev;
+    launch_any(h, a, h->num_sms, s);
+    h->stats.kernel_launches += 1;
+    CK(cudaGetLastError());
+    wd.wait(s, "k_increment_fs (assembly dump)");
+    std::vector<double> o(dn);
+    CK(cudaMemcpyAsync(o.data(), dbg, dn * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(dbg);
+    const double* src = o.data();
+    std::memcpy(r, src, n * sizeof(double));
+    std::memcpy(Kaa, src + n, static_cast<size_t>(n) * n * sizeof(double));
+    std::memcpy(KaF, src + n + n * n, 4 * n * sizeof(double));
+    std::memcpy(KFa, src + n + n * n + 4 * n, 4 * n * sizeof(double));
+    std::memcpy(C_FF, src + n + n * n + 8 * n, 16 * sizeof(double));
+    std::memcpy(P_raw, src + n + n * n + 8 * n + 16, 4 * sizeof(double));
   });
 }
 

@@ -37,6 +37,11 @@ struct ModelDev {
   double inv_denom;       // 1 / (3 mu + h) of the J2 material
   double volume;
   MatDev mat2;            // the (single) J2 material of the history-carrying points
+  // finite strain (kinematics 1): G2 is the 4-row gradient operator with rows
+  // [4 NP | w | 0] (S = 4 NP + 2), J2 chunks [0, nch_hist) then elastic chunks
+  int nch_hist;           // chunks carrying history (J2 points, = K2p / kQC)
+  int K_el;               // elastic cubature points (chunks nch_hist .. nchunks-1)
+  MatDev matE;            // the (single) elastic material of the finite-strain model
 };
 
 struct PointsDev {
@@ -45,7 +50,7 @@ struct PointsDev {
                     // eps_p(4), eq — one bulk copy per chunk, coalesced lane stores
                     // (sigma33 is write-only in the reference and recomputed on readback)
   double* alpha_c;  // [P][NP] committed reduced coordinates
-  double* E_c;      // [P][3]  committed macro strain (= previous path point)
+  double* E_c;      // [P][4]  committed macro strain (3) / displacement gradient H (4)
   double* bp;       // [P][NP] Σ_{J2 q} w G_q^T S(eps_p,q)  (committed plastic-strain load)
   double* sp;       // [P][4]  Σ_{J2 q} w S(eps_p,q)
   PointState* st;
@@ -53,8 +58,8 @@ struct PointsDev {
 };
 
 struct Outputs {
-  double* sigma;  // [P][3]
-  double* C;      // [P][9]
+  double* sigma;  // [P][3]  (finite strain: P_M [P][4])
+  double* C;      // [P][9]  (finite strain: A_M [P][16])
   double* res;    // [P]
   int* iters;     // [P]
   int* status;    // [P]
@@ -81,7 +86,7 @@ struct IncArgs {
   PointsDev D;
   Outputs O;
   NewtonCfg cfg;
-  const double* dE;    // [P][3] this increment's path point
+  const double* dE;    // [P][3] this increment's path point (finite strain: H [P][4])
   int* work;           // work-queue counter (zeroed before launch)
   IncCounters* cnt;    // optional
   // debug: one assembly of point dbg_point at (dbg_alpha, dbg_E), dumped to dbg
@@ -102,5 +107,8 @@ size_t increment_big_smem(int NP);
 void launch_material_batch(const MatDev& m, int64_t N, const double* eps, const double* st_in, double* sigma,
                            double* C, double* st_out, uint8_t* plastic, cudaStream_t s);
 size_t increment_smem(int NP);
+// finite-strain (Biot) path, hrom_kernels_fs.cu: NP <= 32, one warp per point
+void launch_increment_fs(const IncArgs& a, int num_sms, cudaStream_t s);
+size_t increment_fs_smem(int NP);
 
 }  // namespace fe2

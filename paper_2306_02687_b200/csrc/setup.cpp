@@ -274,6 +274,7 @@ struct Model {
   int n = 0, K = 0, n_free = 0;
   double volume = 0.0;
   std::vector<double> G, w;
+  std::vector<double> G4;  // [K][4][n] displacement-gradient operator (finite strain)
   std::vector<int> ip, mat;
 };
 
@@ -310,6 +311,7 @@ Model build_model(int sub, int n, int K, std::uint64_t seed) {
     for (int i = 0; i < K; ++i) md.w.push_back(s.in(0.5, 1.5) * unit_w);
   }
   md.G.assign((size_t)K * 3 * n, 0.0);
+  md.G4.assign((size_t)K * 4 * n, 0.0);
   md.mat.resize(K);
   double Bop[3][12];
   for (int q = 0; q < K; ++q) {
@@ -326,6 +328,22 @@ Model build_model(int sub, int n, int K, std::uint64_t seed) {
         for (int d = 0; d < 12; ++d)
           if (rows[d] >= 0) acc += Bop[i][d] * phi[(size_t)rows[d] * n + a];
         Gq[i * n + a] = acc;
+      }
+    // gradient rows (dux/dX, dux/dY, duy/dX, duy/dY) from the same dN/dx, dN/dy
+    double Bg[4][12] = {};
+    for (int a = 0; a < 6; ++a) {
+      Bg[0][2 * a] = Bop[0][2 * a];
+      Bg[1][2 * a] = Bop[2][2 * a];
+      Bg[2][2 * a + 1] = Bop[2][2 * a + 1];
+      Bg[3][2 * a + 1] = Bop[1][2 * a + 1];
+    }
+    double* G4q = md.G4.data() + (size_t)q * 4 * n;
+    for (int i = 0; i < 4; ++i)
+      for (int a = 0; a < n; ++a) {
+        double acc = 0.0;
+        for (int d = 0; d < 12; ++d)
+          if (rows[d] >= 0) acc += Bg[i][d] * phi[(size_t)rows[d] * n + a];
+        G4q[i * n + a] = acc;
       }
   }
   return md;
@@ -359,6 +377,16 @@ void make_paths(int kind, std::uint64_t seed, std::int64_t p0, std::int64_t P, i
       for (int i = 1; i <= n_incr; ++i) {
         const double f = i <= half ? static_cast<double>(i) / half : static_cast<double>(n_incr - i) / half;
         for (int c3 = 0; c3 < 3; ++c3) out[(i - 1) * 3 + c3] = end[c3] * f;
+      }
+    } else if (kind == 2) {  // config 2: F = I + (i / n_incr) H, H ~ U[-0.08, 0.08]^4, det(I + H) > 0.8
+      double H[4];
+      do {
+        for (double& h : H) h = s.in(-0.08, 0.08);
+      } while (!((1.0 + H[0]) * (1.0 + H[3]) - H[1] * H[2] > 0.8));
+      double* out4 = E + (size_t)k * n_incr * 4;
+      for (int i = 1; i <= n_incr; ++i) {
+        const double f = static_cast<double>(i) / n_incr;
+        for (int c4 = 0; c4 < 4; ++c4) out4[(i - 1) * 4 + c4] = H[c4] * f;
       }
     } else {
       throw Failure(Code::config, "unknown path kind");
@@ -394,6 +422,12 @@ int fe2_model_arrays(fe2_model_t m, double* G, double* w, int* ip_id, int* mat_i
     if (w) std::memcpy(w, m->m.w.data(), m->m.w.size() * sizeof(double));
     if (ip_id) std::memcpy(ip_id, m->m.ip.data(), m->m.ip.size() * sizeof(int));
     if (mat_id) std::memcpy(mat_id, m->m.mat.data(), m->m.mat.size() * sizeof(int));
+  });
+}
+int fe2_model_g4(fe2_model_t m, double* G4) {
+  return fe2::guard([&] {
+    fe2::check(m != nullptr && G4 != nullptr, fe2::Code::config, "null model or output");
+    std::memcpy(G4, m->m.G4.data(), m->m.G4.size() * sizeof(double));
   });
 }
 int fe2_paths(int kind, uint64_t seed, int64_t p0, int64_t P, int n_incr, double* E) {

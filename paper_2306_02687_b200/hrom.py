@@ -73,6 +73,10 @@ def _load():
     L.fe2_material_update_batch.argtypes = [C.c_int, C.POINTER(_Material), C.c_int64, _dp, _dp, _dp, _dp, _dp, _u8p]
     L.fe2_hrom_create.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _ip, C.POINTER(_Material), C.c_int, C.c_double,
                                   C.POINTER(C.c_void_p)]
+    L.fe2_hrom_create_fs.argtypes = L.fe2_hrom_create.argtypes
+    L.fe2_hrom_kinematics.argtypes = [C.c_void_p, _ip]
+    L.fe2_hrom_fs_assemble_point.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+    L.fe2_model_g4.argtypes = [C.c_void_p, _dp]
     L.fe2_hrom_destroy.argtypes = [C.c_void_p]
     L.fe2_hrom_destroy.restype = None
     L.fe2_hrom_alloc_points.argtypes = [C.c_void_p, C.c_int64, C.c_int]
@@ -183,6 +187,8 @@ class HyperRomModel:
             self.ip = np.empty(self.K, dtype=np.int32)
             self.mat = np.empty(self.K, dtype=np.int32)
             _check(lib.fe2_model_arrays(h, _d(self.G), _d(self.w), _i(self.ip), _i(self.mat)))
+            self.G4 = np.empty((self.K, 4, self.n))  # displacement-gradient rows (finite strain)
+            _check(lib.fe2_model_g4(h, _d(self.G4)))
         finally:
             lib.fe2_model_free(h)
         self.subdivisions, self.seed = subdivisions, seed
@@ -194,8 +200,10 @@ class HyperRomModel:
 
 
 def make_paths(kind, seed, P, n_incr, p0=0):
-    """Seeded macro strain paths E[P, n_incr, 3] (BASELINE configs 0/1)."""
-    E = np.empty((P, n_incr, 3))
+    """Seeded macro paths: kinds 0/1 (BASELINE configs 0/1) give strains
+    E[P, n_incr, 3]; kind 2 (config 2) gives displacement gradients
+    H[P, n_incr, 4] = (H00, H01, H10, H11), F = I + H."""
+    E = np.empty((P, n_incr, 4 if kind == 2 else 3))
     _check(lib.fe2_paths(kind, seed, p0, P, n_incr, _d(E)))
     return E
 
@@ -203,25 +211,34 @@ def make_paths(kind, seed, P, n_incr, p0=0):
 class HyperRomEngine:
     """One device's batch of macro Gauss points evaluated with a hyper-ROM
     RVE model: the reduced form of run_trajectory (rve.hpp:448-494) per
-    point, one increment per call."""
+    point, one increment per call.
+
+    Small strain (G[K,3,n]): inputs E (P,3), outputs sigma (P,3), C (P,3,3).
+    Finite strain (G[K,4,n], Biot J2, BASELINE config 2): inputs H = F - I
+    (P,4), outputs under the same keys: sigma = P_M (P,4) first
+    Piola-Kirchhoff stress, C = A_M (P,4,4) = dP_M/dF."""
 
     def __init__(self, G, w, mat_id, materials, volume, device=0):
         G = np.ascontiguousarray(G, dtype=np.float64)
-        K, three, n = G.shape
-        assert three == 3
+        K, rows, n = G.shape
+        assert rows in (3, 4)
         self.n, self.K = n, K
+        self.finite = rows == 4
+        self.nc = rows
         self._w = np.ascontiguousarray(w, dtype=np.float64)
         self._mid = np.ascontiguousarray(mat_id, dtype=np.int32)
         mats = (_Material * len(materials))(*[m._c() for m in materials])
         h = C.c_void_p()
-        _check(lib.fe2_hrom_create(device, n, K, _d(G), _d(self._w), _i(self._mid), mats, len(materials),
-                                   float(volume), C.byref(h)))
+        create = lib.fe2_hrom_create_fs if self.finite else lib.fe2_hrom_create
+        _check(create(device, n, K, _d(G), _d(self._w), _i(self._mid), mats, len(materials), float(volume),
+                      C.byref(h)))
         self._h = h
         self.P = 0
 
     @classmethod
-    def from_model(cls, model: HyperRomModel, device=0):
-        return cls(model.G, model.w, model.mat, model.materials, model.volume, device)
+    def from_model(cls, model: HyperRomModel, device=0, finite_strain=False):
+        G = model.G4 if finite_strain else model.G
+        return cls(G, model.w, model.mat, model.materials, model.volume, device)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -253,10 +270,12 @@ class HyperRomEngine:
                                             _d(res), _i(status)))
 
     def solve_increment(self, E, opts: NewtonOptions | None = None):
-        """E (P,3) host → dict of sigma (P,3), C (P,3,3), iters, plastic_count, res_norm, status."""
-        E = np.ascontiguousarray(E, dtype=np.float64).reshape(self.P, 3)
+        """E (P,3) host → dict of sigma (P,3), C (P,3,3), iters, plastic_count, res_norm, status.
+        (finite strain: H (P,4) → sigma = P_M (P,4), C = A_M (P,4,4))"""
+        nc = self.nc
+        E = np.ascontiguousarray(E, dtype=np.float64).reshape(self.P, nc)
         out = dict(
-            sigma=np.empty((self.P, 3)), C=np.empty((self.P, 3, 3)), iters=np.empty(self.P, dtype=np.int32),
+            sigma=np.empty((self.P, nc)), C=np.empty((self.P, nc, nc)), iters=np.empty(self.P, dtype=np.int32),
             plastic_count=np.empty(self.P, dtype=np.int32), res_norm=np.empty(self.P),
             status=np.empty(self.P, dtype=np.int32))
         o = (opts or NewtonOptions())._c()
@@ -288,6 +307,17 @@ class HyperRomEngine:
         _check(lib.fe2_hrom_assemble_point(self._h, point, _d(alpha), _d(E), _d(r), _d(Kaa), _d(KaE), _d(CEE),
                                            _d(S)))
         return dict(r=r, Kaa=Kaa, KaE=KaE, C_EE=CEE, S_raw=S)
+
+    def fs_assemble_point(self, point, alpha, H):
+        """Finite-strain assembly of a point's committed history at (alpha, H)."""
+        n = self.n
+        r, Kaa, KaF, KFa = np.empty(n), np.empty((n, n)), np.empty((n, 4)), np.empty((4, n))
+        CFF, Praw = np.empty((4, 4)), np.empty(4)
+        alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+        H = np.ascontiguousarray(H, dtype=np.float64)
+        _check(lib.fe2_hrom_fs_assemble_point(self._h, point, _d(alpha), _d(H), _d(r), _d(Kaa), _d(KaF), _d(KFa),
+                                              _d(CFF), _d(Praw)))
+        return dict(r=r, Kaa=Kaa, KaF=KaF, KFa=KFa, C_FF=CFF, P_raw=Praw)
 
     def stats(self):
         s = _Stats()

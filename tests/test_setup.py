@@ -55,3 +55,17 @@ def test_paths_bitwise_and_shape(kind, n_incr):
         assert np.abs(E[:, -1]).max() == 0.0 and np.abs(E[:, :, 1]).max() == 0.0
         assert np.abs(E[:, 24, 0]).max() <= 0.03 and np.abs(E[:, 24, 2]).max() <= 0.04
         np.testing.assert_allclose(E[:, 10], E[:, 38], rtol=1e-14)
+
+
+@pytest.mark.parametrize("sub,n,K,seed", [(33, 32, 600, 0), (12, 8, 60, 1), (8, 6, 50, 7)])
+def test_gradient_operator_bitwise_equal_to_oracle(sub, n, K, seed):
+    """Finite strain (config 2): the 4-row displacement-gradient operator."""
+    m = F.HyperRomModel(sub, n, K, seed)
+    assert np.array_equal(m.G4, O.model_g4(sub, n, K, seed))
+
+
+def test_finite_strain_paths_bitwise():
+    H = F.make_paths(2, 0, 300, 30)
+    assert H.shape == (300, 30, 4)
+    assert np.array_equal(H, O.paths_fs(0, 300, 30))
+    assert np.array_equal(F.make_paths(2, 0, 50, 30, p0=200), H[200:250])

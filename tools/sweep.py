@@ -31,8 +31,10 @@ except Exception:
 def run_cell(name, n, K, P_max, incr, path, seconds, seed=0):
     import torch
 
+    fs = path == 2  # finite strain (config 2)
+    nc, nt = (4, 16) if fs else (3, 9)
     m = F.HyperRomModel(33, n, K, seed)
-    eng = F.HyperRomEngine.from_model(m)
+    eng = F.HyperRomEngine.from_model(m, finite_strain=fs)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     eng.set_stream(stream.cuda_stream)
@@ -41,7 +43,7 @@ def run_cell(name, n, K, P_max, incr, path, seconds, seed=0):
         E = F.make_paths(path, seed, P, incr)
         dE = torch.from_numpy(np.ascontiguousarray(E.transpose(1, 0, 2))).to(dev)
         outs = [torch.empty(s, dtype=t, device=dev) for s, t in
-                (((P, 3), torch.float64), ((P, 9), torch.float64), ((P,), torch.int32), ((P,), torch.int32),
+                (((P, nc), torch.float64), ((P, nt), torch.float64), ((P,), torch.int32), ((P,), torch.int32),
                  ((P,), torch.float64), ((P,), torch.int32))]
         eng.alloc_points(P)
         eng.reset_stats()
@@ -56,16 +58,18 @@ def run_cell(name, n, K, P_max, incr, path, seconds, seed=0):
         torch.cuda.synchronize()
         eng.set_timing(False)
         st = outs[5].cpu().numpy()
-        return e0.elapsed_time(e1) / 1e3, eng.stats(), int((st != 0).sum())
+        return e0.elapsed_time(e1) / 1e3, eng.stats(), int((st != 0).sum()), outs[2].cpu().numpy()
 
     P = min(P_max, 1024)
     trajectory(P)  # warm-up (module load, first launch)
-    t, _, _ = trajectory(P)
+    t, _, _, _ = trajectory(P)
     P = int(min(P_max, max(256, P * seconds / max(t, 1e-3))))
-    t, s, failed = trajectory(P)
+    t, s, failed, iters_sum = trajectory(P)
     K_j2 = m.K_j2
     evals = P * incr
-    F_asm = 3.0 * K_j2 * n * (n + 9)
+    # algorithmic flops of one assembly: small strain, plastic J2 points only
+    # (elastic predictor); finite strain, every cubature point (Kaa, Hq, KaF | r)
+    F_asm = 3.0 * K_j2 * n * (n + 9) if not fs else K * (8.0 * n * n + 72.0 * n)
     kms = s["kernel_ms"]
     hbm_bytes = (s["timed_assemblies"] + s["timed_commits"]) * K_j2 * 40 + s["timed_commit_plastic"] * 40
     return {
@@ -73,6 +77,7 @@ def run_cell(name, n, K, P_max, incr, path, seconds, seed=0):
         "evals_per_s": evals / t, "ms": t * 1e3,
         "assemblies_per_eval": s["timed_assemblies"] / evals,
         "plastic_fraction": s["timed_plastic_evals"] / max(1, s["timed_assemblies"] * K_j2),
+        "iters_per_eval": float(np.mean(iters_sum)) / incr if iters_sum is not None else None,
         "algorithmic_tflops": s["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12,
         "frac_of_dmma_peak": s["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12 / DMMA_PEAK,
         "history_gbs": hbm_bytes / (kms / 1e3) / 1e9, "frac_of_hbm": hbm_bytes / (kms / 1e3) / 1e9 / HBM,
@@ -90,6 +95,8 @@ def main():
     cells = []
     if "0" in which:
         cells.append(("config0", 12, 200, 1024, 20, 0))
+    if "2" in which:
+        cells.append(("config2", 32, 600, 262144, 30, 2))
     if "3" in which:
         cells.append(("config3_subset", 64, 2000, 1048576, 20, 0))
     if "4" in which:
