@@ -153,6 +153,14 @@ __device__ void fs_ring_drain(const FsRing& R, int seq, int lane) {
   fs_trace(R, seq, 5);
 }
 
+// D += A B on the FP64 tensor pipe (m8n8k4). Not volatile: only the data
+// dependences order it, so independent shared loads can be scheduled around it.
+__device__ __forceinline__ void mma_f64(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
 // LU with partial pivoting of the n x n matrix in sA (row stride lda), lane i
 // owning row i (n <= 32); multipliers stored below the diagonal, pivot rows
 // in piv (first maximal |a_ij|, as the oracle's Lu::factor). False if singular.
@@ -389,32 +397,53 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) sl[16 + e] = wq * o.P[e];
       __syncwarp();
-      if (lane < 20) {  // C_FF | P_raw partial sums of the chunk (fixed order)
-        double t = 0.0;
-#pragma unroll 8
-        for (int q = 0; q < kQC; ++q) t += sSlot[q * kSl + lane];
-        c20 += t;
+      if (lane < 20) {  // C_FF | P_raw partial sums of the chunk (fixed order, 4 chains)
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+        for (int q = 0; q < kQC; q += 4) {
+          t0 += sSlot[q * kSl + lane];
+          t1 += sSlot[(q + 1) * kSl + lane];
+          t2 += sSlot[(q + 2) * kSl + lane];
+          t3 += sSlot[(q + 3) * kSl + lane];
+        }
+        c20 += (t0 + t1) + (t2 + t3);
       }
-      // one MMA k-step per cubature point: A = G_q^T tile, B = (w A_q G_q) tile
-#pragma unroll 1
-      for (int q = 0; q < nv; ++q) {
+      // one MMA k-step per cubature point: A = G_q^T tile, B = (w A_q G_q) tile.
+      // Software-pipelined: the shared-memory operands of point q+1 are loaded
+      // before the MMAs of point q issue, so their latency hides behind them.
+      const int bidx = col < 4 ? m * 4 + col : 16 + m;
+      const bool bon = col <= 4;
+      double pg[NT][4], pa[NT], pw[4], pb;
+      auto load_q = [&](int q) {
         const double* g = Gb + q * S + col;
-        const double* s = sSlot + q * kSl;
-        const double w0 = s[m * 4 + 0], w1 = s[m * 4 + 1], w2 = s[m * 4 + 2], w3 = s[m * 4 + 3];
-        const double bx = col < 4 ? s[m * 4 + col] : (col == 4 ? s[16 + m] : 0.0);
-        double Af[NT], Bf[NT];
+        const double* sq = sSlot + q * kSl;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          const double g0 = g[t * 8], g1 = g[NP + t * 8], g2 = g[2 * NP + t * 8], g3 = g[3 * NP + t * 8];
-          Af[t] = m == 0 ? g0 : (m == 1 ? g1 : (m == 2 ? g2 : g3));
-          Bf[t] = w0 * g0 + w1 * g1 + w2 * g2 + w3 * g3;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) pg[t][r] = g[r * NP + t * 8];
+          pa[t] = g[m * NP + t * 8];
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) pw[r] = sq[m * 4 + r];
+        pb = bon ? sq[bidx] : 0.0;
+      };
+      load_q(0);
+#pragma unroll 1
+      for (int q = 0; q < nv; ++q) {
+        double Af[NT], Bf[NT];
+        const double bx = pb;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          Af[t] = pa[t];
+          Bf[t] = pw[0] * pg[t][0] + pw[1] * pg[t][1] + pw[2] * pg[t][2] + pw[3] * pg[t][3];
           kfa[t] += Bf[t];
         }
+        load_q(q + 1 < nv ? q + 1 : q);
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
 #pragma unroll
-          for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], Af[i], Bf[j]);
-          dmma(kx[i][0], kx[i][1], Af[i], bx);
+          for (int j = 0; j < NT; ++j) mma_f64(acc[i][j][0], acc[i][j][1], Af[i], Bf[j]);
+          mma_f64(kx[i][0], kx[i][1], Af[i], bx);
         }
       }
       fs_ring_release(R, seq, lane);

@@ -28,7 +28,7 @@ except Exception:
     HBM = 6650.0
 
 
-def run_cell(name, n, K, P_max, incr, path, seconds, seed=0):
+def run_cell(name, n, K, P_max, incr, path, seconds, seed=0, points=0):
     import torch
 
     fs = path == 2  # finite strain (config 2)
@@ -63,7 +63,7 @@ def run_cell(name, n, K, P_max, incr, path, seconds, seed=0):
     P = min(P_max, 1024)
     trajectory(P)  # warm-up (module load, first launch)
     t, _, _, _ = trajectory(P)
-    P = int(min(P_max, max(256, P * seconds / max(t, 1e-3))))
+    P = int(min(P_max, max(256, P * seconds / max(t, 1e-3)))) if not points else points
     t, s, failed, iters_sum = trajectory(P)
     K_j2 = m.K_j2
     evals = P * incr
@@ -77,11 +77,12 @@ def run_cell(name, n, K, P_max, incr, path, seconds, seed=0):
         "evals_per_s": evals / t, "ms": t * 1e3,
         "assemblies_per_eval": s["timed_assemblies"] / evals,
         "plastic_fraction": s["timed_plastic_evals"] / max(1, s["timed_assemblies"] * K_j2),
-        "iters_per_eval": float(np.mean(iters_sum)) / incr if iters_sum is not None else None,
+        "newton_iters_last_incr": float(np.mean(iters_sum)),
         "algorithmic_tflops": s["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12,
         "frac_of_dmma_peak": s["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12 / DMMA_PEAK,
         "history_gbs": hbm_bytes / (kms / 1e3) / 1e9, "frac_of_hbm": hbm_bytes / (kms / 1e3) / 1e9 / HBM,
         "kernel_share": kms / (t * 1e3),
+        "kernel_evals_per_s": evals / (kms / 1e3),
     }
 
 
@@ -90,6 +91,7 @@ def main():
     ap.add_argument("--seconds", type=float, default=2.0)
     ap.add_argument("--which", default="0,3,4")
     ap.add_argument("--only", default="", help="comma-separated substrings of cell names to run")
+    ap.add_argument("--points", type=int, default=0, help="fixed point count per cell (0 = scale to --seconds)")
     args = ap.parse_args()
     which = set(args.which.split(","))
     cells = []
@@ -108,7 +110,7 @@ def main():
         cells = [c for c in cells if any(k in c[0] for k in keys)]
     for c in cells:
         t0 = time.time()
-        r = run_cell(*c, seconds=args.seconds)
+        r = run_cell(*c, seconds=args.seconds, points=args.points)
         r["wall_s"] = time.time() - t0
         print(json.dumps(r), flush=True)
 
