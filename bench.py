@@ -34,6 +34,8 @@ CONFIGS = {
     1: dict(name="config1_beam_small_strain_j2", P=65536, n=24, K=400, incr=50, path=1, subdivisions=33),
     # configs[0]: the reference's CPU-runnable case (parity config)
     0: dict(name="config0_small_strain_j2", P=1024, n=12, K=200, incr=20, path=0, subdivisions=33),
+    # configs[2]: finite-strain Biot J2 (parity unpinned: no reference code)
+    2: dict(name="config2_finite_strain_biot_j2", P=262144, n=32, K=600, incr=30, path=2, subdivisions=33),
 }
 METRIC = "macro Gauss-point hyper-ROM evaluations/sec (fp64)"
 UNIT = "evals/s"
@@ -50,6 +52,9 @@ def parse():
     ap.add_argument("--points", type=int, default=0, help="override points per rank (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-points", type=int, default=0)
+    ap.add_argument("--extra-configs", default="2",
+                    help="comma-separated configs also timed device-resident (1 warm-up + 1 step) into "
+                         "extra_configs of the line; '' to skip")
     return ap.parse_args()
 
 
@@ -60,7 +65,11 @@ def dist_env():
     return ws, rank, local
 
 
-def flops_per_assembly(n, K_j2):
+def flops_per_assembly(n, K_j2, K=0, finite=False):
+    if finite:
+        # F_asm = 8 K n (n + 5) — every cubature point,
+        # the full non-symmetric K_aa, K_aF (n x 4) and r
+        return 8.0 * K * n * (n + 5)
     # F_asm = 3 K n (n + 9) (upper-triangle K_aa + K_aE + r),
     # K = the J2 cubature points actually contracted (elastic block precomputed)
     return 3.0 * K_j2 * n * (n + 9)
@@ -132,9 +141,14 @@ def cpu_reference_run(cfg, n_points, threads, seed=0):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
     m = O.Model(cfg["subdivisions"], cfg["n"], cfg["K"], seed)
-    E = O.paths(cfg["path"], seed, n_points, cfg["incr"])
     mats = [("j2", 1.0, 0.3, 0.01, 0.016), ("elastic", 10.0, 0.3)]
-    h = O.Hrom(m.G, m.w, m.mat, mats, m.volume)
+    if cfg["path"] == 2:
+        E = O.paths_fs(seed, n_points, cfg["incr"])
+        G4 = O.model_g4(cfg["subdivisions"], cfg["n"], cfg["K"], seed)
+        h = O.HromFs(G4, m.w, m.mat, mats, m.volume)
+    else:
+        E = O.paths(cfg["path"], seed, n_points, cfg["incr"])
+        h = O.Hrom(m.G, m.w, m.mat, mats, m.volume)
     t0 = time.perf_counter()
     r = h.run(E, threads=threads)
     dt = time.perf_counter() - t0
@@ -176,6 +190,82 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+class DeviceRun:
+    """One config on this rank: model, engine, device-resident path and outputs."""
+
+    def __init__(self, F, torch, cfg, rank, local, dev, stream):
+        self.cfg, self.dev, self.stream, self.torch = cfg, dev, stream, torch
+        self.finite = cfg["path"] == 2
+        self.nc, self.nt = (4, 16) if self.finite else (3, 9)
+        P, incr = cfg["P"], cfg["incr"]
+        self.model = F.HyperRomModel(cfg["subdivisions"], cfg["n"], cfg["K"], seed=0)
+        E_host = F.make_paths(cfg["path"], 0, P, incr, p0=rank * P)  # (P, incr, nc), global-id streams
+        self.E_inc = np.ascontiguousarray(E_host.transpose(1, 0, 2))  # (incr, P, nc)
+        self.eng = F.HyperRomEngine.from_model(self.model, device=local, finite_strain=self.finite)
+        self.eng.alloc_points(P)
+        self.eng.set_stream(stream.cuda_stream)
+        f64, i32 = torch.float64, torch.int32
+        self.dE = torch.from_numpy(self.E_inc).to(dev)
+        self.d_sig = torch.empty((P, self.nc), dtype=f64, device=dev)
+        self.d_C = torch.empty((P, self.nt), dtype=f64, device=dev)
+        self.d_res = torch.empty(P, dtype=f64, device=dev)
+        self.d_it = torch.empty(P, dtype=i32, device=dev)
+        self.d_pc = torch.empty(P, dtype=i32, device=dev)
+        self.d_st = torch.empty(P, dtype=i32, device=dev)
+        self.width = self.nc + self.nt + 2
+        self.pack = torch.empty((P, self.width), dtype=f64, device=dev)
+        self.gathered = None
+
+    def gather(self, dist, ws, sig, C, res, st):
+        """All-gather (Σ | P, C | A, residual norm, status) of every point."""
+        if ws == 1:
+            return
+        if self.gathered is None:
+            self.gathered = self.torch.empty((ws,) + tuple(self.pack.shape), dtype=self.pack.dtype,
+                                             device=self.dev)
+        nc, nt = self.nc, self.nt
+        self.pack[:, 0:nc] = sig
+        self.pack[:, nc:nc + nt] = C
+        self.pack[:, nc + nt] = res
+        self.pack[:, nc + nt + 1] = st.to(self.torch.float64)
+        dist.all_gather_into_tensor(self.gathered, self.pack)
+
+    def device_step(self, dist, ws):
+        self.eng.reset_points()
+        for k in range(self.cfg["incr"]):
+            self.eng.solve_increment_device(self.dE[k].data_ptr(), self.d_sig.data_ptr(), self.d_C.data_ptr(),
+                                            self.d_it.data_ptr(), self.d_pc.data_ptr(), self.d_res.data_ptr(),
+                                            self.d_st.data_ptr(), self.stream.cuda_stream)
+            self.gather(dist, ws, self.d_sig, self.d_C, self.d_res, self.d_st)
+
+    def check_converged(self):
+        st = self.d_st.cpu().numpy()
+        if (st != 0).any():
+            raise SystemExit(f"bench: {int((st != 0).sum())} points of {self.cfg['name']} failed to converge")
+
+    def roofline(self, stats, ms, peak, peak_src):
+        cfg, model = self.cfg, self.model
+        n, K_j2 = cfg["n"], model.K_j2
+        kms = stats["kernel_ms"]
+        F_asm = flops_per_assembly(n, K_j2, cfg["K"], self.finite)
+        achieved = stats["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12 if kms else None
+        nt = (n + 7) // 8
+        if self.finite:  # every cubature point: NT^2 + NT DMMA.8x8x4 (512 flop) per point-assembly
+            executed = stats["timed_assemblies"] * cfg["K"] * (nt * nt + nt) * 512
+            kernel = "k_increment_fs (persistent: Biot update + DMMA k-step per cubature point + warp LU/Newton/condensation + commit)"
+            definition = "SURVEY §8(d) config 2: F_asm = 8 K n (n+5) per point-assembly (all cubature points; full K_aa, K_aF, r)"
+        else:  # every plastic point = 3 k-entries = 0.75 k-steps of NTP DMMA.8x8x4
+            executed = stats["timed_plastic_evals"] * 0.75 * (nt * (nt + 1) // 2) * 512
+            kernel = "k_increment (persistent: DMMA hyper-assembly + warp Cholesky/Newton/condensation + commit)"
+            definition = "SURVEY §8(d) F_asm = 3 K_J2 n (n+9) per point-assembly (elastic block precomputed)"
+        launches_t = max(1, stats["timed_launches"])
+        return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "kernel": kernel, "peak_source": peak_src,
+                "flops_per_point_assembly": F_asm, "flops_definition": definition,
+                "executed_dmma_tflops": executed / (kms / 1e3) / 1e12 if kms else None,
+                "avg_launch_ms": kms / launches_t, "share_of_step": kms / ms if ms else None}
+
+
 def main():
     args = parse()
     cfg = dict(CONFIGS[args.config])
@@ -195,42 +285,7 @@ def main():
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
-
-    P, incr = cfg["P"], cfg["incr"]
-    model = F.HyperRomModel(cfg["subdivisions"], cfg["n"], cfg["K"], seed=0)
-    E_host = F.make_paths(cfg["path"], 0, P, incr, p0=rank * P)  # (P, incr, 3), global-id streams
-    E_inc = np.ascontiguousarray(E_host.transpose(1, 0, 2))   # (incr, P, 3)
-    eng = F.HyperRomEngine.from_model(model, device=local)
-    eng.alloc_points(P)
     stream = torch.cuda.current_stream(dev)
-    eng.set_stream(stream.cuda_stream)
-
-    # device-resident buffers
-    dE = torch.from_numpy(E_inc).to(dev)
-    d_sig = torch.empty((P, 3), dtype=torch.float64, device=dev)
-    d_C = torch.empty((P, 9), dtype=torch.float64, device=dev)
-    d_res = torch.empty(P, dtype=torch.float64, device=dev)
-    d_it = torch.empty(P, dtype=torch.int32, device=dev)
-    d_pc = torch.empty(P, dtype=torch.int32, device=dev)
-    d_st = torch.empty(P, dtype=torch.int32, device=dev)
-    pack = torch.empty((P, 14), dtype=torch.float64, device=dev)
-    gathered = torch.empty((ws, P, 14), dtype=torch.float64, device=dev) if ws > 1 else None
-
-    def gather():
-        if ws == 1:
-            return
-        pack[:, 0:3] = d_sig
-        pack[:, 3:12] = d_C
-        pack[:, 12] = d_res
-        pack[:, 13] = d_st.to(torch.float64)
-        dist.all_gather_into_tensor(gathered, pack)
-
-    def device_step():
-        eng.reset_points()
-        for k in range(incr):
-            eng.solve_increment_device(dE[k].data_ptr(), d_sig.data_ptr(), d_C.data_ptr(), d_it.data_ptr(),
-                                       d_pc.data_ptr(), d_res.data_ptr(), d_st.data_ptr(), stream.cuda_stream)
-            gather()
 
     def barrier():
         if ws > 1:
@@ -253,18 +308,24 @@ def main():
             ms = float(t.item())
         return ms
 
+    try:
+        peak = json.load(open(DMMA_PEAK_FILE))["dmma_tflops_w16"]
+        peak_src = "measured DMMA m8n8k4 f64 peak on this pool's B200 (tools/fp64_peak.cu, profiles/r01_fp64_peak.json)"
+    except Exception:
+        peak, peak_src = 37.0, "fallback: DMMA peak estimate"
+
+    run = DeviceRun(F, torch, cfg, rank, local, dev, stream)
+    eng, model, P, incr = run.eng, run.model, cfg["P"], cfg["incr"]
+    nc, nt = run.nc, run.nt
     for _ in range(args.warmup):
-        device_step()
-    # correctness guard on the warm-up trajectory
-    st_host = d_st.cpu().numpy()
-    if (st_host != 0).any():
-        raise SystemExit(f"bench: {int((st_host != 0).sum())} points failed to converge")
+        run.device_step(dist, ws)
+    run.check_converged()  # correctness guard on the warm-up trajectory
 
     eng.reset_stats()
     eng.set_timing(True)
     launches0 = eng.stats()["kernel_launches"]
     with ClockSampler(local) as clk:
-        ms = timed(device_step, args.steps)
+        ms = timed(lambda: run.device_step(dist, ws), args.steps)
     stats = eng.stats()
     eng.set_timing(False)
     launches = stats["kernel_launches"] - launches0
@@ -273,13 +334,13 @@ def main():
 
     # ---- e2e through the host-buffer C-ABI (pinned host memory)
     pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
-    E_pin = pin(E_inc)
-    o_sig, o_C, o_res = pin(np.empty((P, 3))), pin(np.empty((P, 9))), pin(np.empty(P))
+    E_pin = pin(run.E_inc)
+    o_sig, o_C, o_res = pin(np.empty((P, nc))), pin(np.empty((P, nt))), pin(np.empty(P))
     o_it, o_pc, o_st = (pin(np.empty(P, dtype=np.int32)) for _ in range(3))
     if ws > 1:  # the engine's own device output buffers, gathered after each host-API call
         p_sig, p_C, p_it, p_pc, p_res, p_st = eng.output_ptrs()
-        e_sig = wrap_dev(p_sig, (P, 3), "<f8", dev)
-        e_C = wrap_dev(p_C, (P, 9), "<f8", dev)
+        e_sig = wrap_dev(p_sig, (P, nc), "<f8", dev)
+        e_C = wrap_dev(p_C, (P, nt), "<f8", dev)
         e_res = wrap_dev(p_res, (P,), "<f8", dev)
         e_st = wrap_dev(p_st, (P,), "<i4", dev)
 
@@ -288,53 +349,55 @@ def main():
         for k in range(incr):
             eng.solve_increment_into(E_pin[k], o_sig, o_C, o_it, o_pc, o_res, o_st)
             if ws > 1:
-                pack[:, 0:3] = e_sig
-                pack[:, 3:12] = e_C
-                pack[:, 12] = e_res
-                pack[:, 13] = e_st.to(torch.float64)
-                dist.all_gather_into_tensor(gathered, pack)
+                run.gather(dist, ws, e_sig, e_C, e_res, e_st)
 
     e2e_step()
-    ms_e2e = timed(e2e_step, max(1, min(args.steps, 3)))
     e2e_steps = max(1, min(args.steps, 3))
+    ms_e2e = timed(e2e_step, e2e_steps)
     e2e_value = ws * P * incr * e2e_steps / (ms_e2e / 1e3)
-    h2d = incr * P * 3 * 8
-    d2h = incr * P * (3 * 8 + 9 * 8 + 8 + 3 * 4)
+    h2d = incr * P * nc * 8
+    d2h = incr * P * (nc * 8 + nt * 8 + 8 + 3 * 4)
+
+    # ---- other BASELINE configs, device-resident (weak scaling, same rank layout)
+    extras = {}
+    for c in [int(x) for x in args.extra_configs.split(",") if x.strip()]:
+        if c == args.config or c not in CONFIGS:
+            continue
+        xcfg = dict(CONFIGS[c])
+        xrun = DeviceRun(F, torch, xcfg, rank, local, dev, stream)
+        xrun.device_step(dist, ws)
+        xrun.check_converged()
+        xrun.eng.reset_stats()
+        xrun.eng.set_timing(True)
+        xms = timed(lambda: xrun.device_step(dist, ws), 1)
+        xst = xrun.eng.stats()
+        xev = ws * xcfg["P"] * xcfg["incr"]
+        extras[xcfg["name"]] = {
+            "value": xev / (xms / 1e3), "unit": UNIT, "steps": 1, "warmup": 1, "ms_per_step": xms,
+            "points_per_rank": xcfg["P"], "modes": xcfg["n"], "cubature": xcfg["K"], "increments": xcfg["incr"],
+            "roofline": xrun.roofline(xst, xms, peak, peak_src),
+            "newton": {"assemblies_per_eval": xst["timed_assemblies"] / (xev / ws)},
+            "parity": "unpinned (no reference finite-strain code; oracle fs_* checked by tests/test_gpu_fs.py)"
+            if xrun.finite else "pinned"}
+        del xrun
 
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel: k_increment (one persistent launch
-    # per increment: hyper-assembly on DMMA + Newton + condensation + commit)
-    K_j2, n_modes = model.K_j2, cfg["n"]
-    kms = stats["kernel_ms"]
-    F_asm = flops_per_assembly(n_modes, K_j2)
-    achieved = stats["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12 if kms else None
-    ntp = ((n_modes + 7) // 8) * ((n_modes + 7) // 8 + 1) // 2
-    # executed tensor work: every plastic point = 3 k-entries = 0.75 k-steps of NTP DMMA.8x8x4 (512 flop)
-    dmma_tflops = stats["timed_plastic_evals"] * 0.75 * ntp * 512 / (kms / 1e3) / 1e12 if kms else None
-    try:
-        peak = json.load(open(DMMA_PEAK_FILE))["dmma_tflops_w16"]
-        peak_src = "measured DMMA m8n8k4 f64 peak on this pool's B200 (tools/fp64_peak.cu, profiles/r01_fp64_peak.json)"
-    except Exception:
-        peak, peak_src = 37.0, "fallback: DMMA peak estimate"
+    # ---- roofline of the dominant kernel (one persistent launch per increment)
+    roofline = run.roofline(stats, ms, peak, peak_src)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_increment_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get(cfg["name"], {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    launches_t = max(1, stats["timed_launches"])
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "k_increment (persistent: DMMA hyper-assembly + warp Cholesky/Newton/condensation + commit)",
-                "peak_source": peak_src, "flops_per_point_assembly": F_asm,
-                "flops_definition": "SURVEY §8(d) F_asm = 3 K_J2 n (n+9) per point-assembly (elastic block precomputed)",
-                "executed_dmma_tflops": dmma_tflops,
-                "avg_launch_ms": kms / launches_t, "share_of_step": kms / ms if ms else None}
+    roofline["traffic"] = traffic
+    kms = stats["kernel_ms"]
+    K_j2 = model.K_j2
     try:
         hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
         hbm_src = "MEASURED_PEAKS.json"
@@ -345,7 +408,7 @@ def main():
     gbs = hbm_bytes / (kms / 1e3) / 1e9 if kms else None
     roofline_hbm = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
                     "frac": gbs / hbm if gbs else None, "peak_source": hbm_src,
-                    "kernel": "k_increment history stream (eps_p[4], eq SoA)",
+                    "kernel": "history stream of the increment kernel (eps_p[4], eq SoA)",
                     "bytes_definition": "40 B read per J2 point per assembly/commit pass + 40 B written per plastic commit",
                     "bytes_per_step": hbm_bytes / args.steps}
 
@@ -375,6 +438,7 @@ def main():
         "newton": {"assemblies_per_eval": stats["timed_assemblies"] / (evals / ws),
                    "commits_per_eval": stats["timed_commits"] / (evals / ws),
                    "plastic_fraction": stats["timed_plastic_evals"] / max(1, stats["timed_assemblies"] * K_j2)},
+        "extra_configs": extras,
     }
     print(json.dumps(line), flush=True)
     if ws > 1:

@@ -32,6 +32,7 @@
 //  - Commit pass: recompute at the converged (E, α), write εp, eq of the
 //    plastic points (80 B/point stream), fold Δεp into b_p, s_p.
 #include <cstdio>
+#include <cstdlib>
 
 #include "hrom_kernels.cuh"
 
@@ -238,11 +239,15 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
 #ifndef FE2_MINB
 #define FE2_MINB 1
 #endif
-constexpr int kW = FE2_KW;            // warps per CTA
+#ifndef FE2_KWRES
+#define FE2_KWRES 8
+#endif
+constexpr int kW = FE2_KW;            // warps per CTA (streamed-G ring)
+constexpr int kWRes = FE2_KWRES;      // warps per CTA when the whole G2 is resident in shared memory
 constexpr int kMaxStages = FE2_STAGES;  // G-chunk ring depth (shared by the CTA), at most
 constexpr int kHS = 2;      // per-warp history ring depth (TMA, 5 x 256 B per stage)
 
-template <int NP>
+template <int NP, int W>
 struct IncLayout {
   static constexpr int S = 3 * NP + 2;
   static constexpr int chunk = kQC * S;                      // doubles per ring stage
@@ -252,15 +257,19 @@ struct IncLayout {
   static constexpr int kHist = kHS * 5 * kQC;                 // per-warp history ring (TMA)
   static constexpr int WS = 5 * NP + 3 * NP + kUnion + kHist;  // per-warp scratch (doubles)
   // ring depth: as deep as the 227 KB shared-memory budget allows (<= kMaxStages)
-  static constexpr long kBudget = 227L * 1024 - 512 - static_cast<long>(kW) * WS * 8;
+  static constexpr long kBudget = 227L * 1024 - 512 - static_cast<long>(W) * WS * 8;
   static constexpr int kFit = static_cast<int>(kBudget / (static_cast<long>(chunk) * 8));
   static constexpr int ST = kFit < 2 ? 2 : (kFit > kMaxStages ? kMaxStages : kFit);
   static constexpr size_t ring_bytes = static_cast<size_t>(ST) * chunk * sizeof(double);
-  // control block: full[ST] (u64) | hbar[kW][kHS] (u64) | cnt[ST] (int) | ctrl (u64)
+  // control block: full[ST] (u64) | hbar[W][kHS] (u64) | cnt[ST] (int) | ctrl (u64)
   static constexpr int kHbarOff = ST * 8;
-  static constexpr int kCntOff = kHbarOff + kW * kHS * 8;
+  static constexpr int kCntOff = kHbarOff + W * kHS * 8;
   static constexpr int kCtrlOff = ((kCntOff + ST * 4 + 7) / 8) * 8;
-  static constexpr size_t bytes = ring_bytes + static_cast<size_t>(kW) * WS * sizeof(double) + kCtrlOff + 8;
+  static constexpr size_t bytes = ring_bytes + static_cast<size_t>(W) * WS * sizeof(double) + kCtrlOff + 8;
+  // resident variant: the whole G2 (nch chunks) in shared memory, no ring
+  static constexpr size_t res_bytes(int nch) {
+    return static_cast<size_t>(nch) * chunk * sizeof(double) + static_cast<size_t>(W) * WS * sizeof(double) + kCtrlOff + 8;
+  }
 };
 
 // Shared-memory ring of G chunks. ctrl packs {working warps (hi 32), issued
@@ -276,6 +285,8 @@ struct Ring {
   int chunk;           // doubles per stage
   volatile int* tr;    // watchdog trace slot of this warp (or null)
   int stages;          // ring depth
+  int nwarps;          // warps consuming the ring
+  bool res;            // G2 fully resident: no waits, no refills
 };
 
 __device__ __forceinline__ void trace(const Ring& R, int seq, int code) {
@@ -289,6 +300,7 @@ __device__ __forceinline__ void trace(const Ring& R, int seq, int code) {
 }
 
 __device__ __forceinline__ const double* ring_wait(const Ring& R, int seq) {
+  if (R.res) return R.buf + static_cast<size_t>(seq % R.nch) * R.chunk;
   const int s = seq % R.stages;
   trace(R, seq, 1);
   mbar_wait(&R.full[s], static_cast<uint32_t>((seq / R.stages) & 1));
@@ -298,10 +310,11 @@ __device__ __forceinline__ const double* ring_wait(const Ring& R, int seq) {
 
 __device__ __forceinline__ void ring_release(const Ring& R, int seq, int lane) {
   __syncwarp();
+  if (R.res) return;
   if (lane == 0) {
     const int s = seq % R.stages;
     __threadfence_block();
-    if (atomicAdd(&R.cnt[s], 1) == kW - 1) {
+    if (atomicAdd(&R.cnt[s], 1) == R.nwarps - 1) {
       R.cnt[s] = 0;
       const int nxt = seq + R.stages;
       unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(R.ctrl);
@@ -331,6 +344,7 @@ __device__ __forceinline__ void ring_release(const Ring& R, int seq, int lane) {
 // A warp without more points keeps consuming (so the ring keeps turning for
 // the others) until no warp works and every issued position was consumed.
 __device__ void ring_drain(const Ring& R, int seq, int lane) {
+  if (R.res) return;
   if (lane == 0) atomicAdd(R.ctrl, 0xffffffff00000000ull);  // working -= 1 (mod 2^64)
   __syncwarp();
   trace(R, seq, 4);
@@ -352,18 +366,21 @@ __device__ void ring_drain(const Ring& R, int seq, int lane) {
   trace(R, seq, 5);
 }
 
-template <int NT>
-__global__ void __launch_bounds__(kW * 32, FE2_MINB) k_increment(IncArgs A) {
+// RES: the whole projected operator G2 sits in shared memory for the kernel's
+// lifetime (loaded once by TMA): warps never wait on each other for G chunks.
+// Otherwise G2 streams through the CTA-shared ring (W warps, ST stages).
+template <int NT, int W, bool RES>
+__global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArgs A) {
   constexpr int NP = 8 * NT;
   constexpr int NTP = NT * (NT + 1) / 2;
-  using L = IncLayout<NP>;
+  using L = IncLayout<NP, W>;
   constexpr int S = L::S;
-  constexpr int LD = NP + 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t ring_bytes = RES ? static_cast<size_t>(A.M.nchunks) * L::chunk * sizeof(double) : L::ring_bytes;
   double* ring_buf = reinterpret_cast<double*>(smem_raw);
-  double* wbase = reinterpret_cast<double*>(smem_raw + L::ring_bytes) + static_cast<size_t>(warp) * L::WS;
-  unsigned char* ctrl_base = smem_raw + L::ring_bytes + static_cast<size_t>(kW) * L::WS * sizeof(double);
+  double* wbase = reinterpret_cast<double*>(smem_raw + ring_bytes) + static_cast<size_t>(warp) * L::WS;
+  unsigned char* ctrl_base = smem_raw + ring_bytes + static_cast<size_t>(W) * L::WS * sizeof(double);
   uint64_t* full = reinterpret_cast<uint64_t*>(ctrl_base);
   uint64_t* hbar = reinterpret_cast<uint64_t*>(ctrl_base + L::kHbarOff) + warp * kHS;
   int* cnt = reinterpret_cast<int*>(ctrl_base + L::kCntOff);
@@ -387,20 +404,29 @@ __global__ void __launch_bounds__(kW * 32, FE2_MINB) k_increment(IncArgs A) {
   const MatDev& mt = M.mat2;
   const int nch = M.nchunks;
   const Ring R{ring_buf, full, cnt, ctrl, M.G2, nch, L::chunk,
-               A.trace ? A.trace + (static_cast<size_t>(blockIdx.x) * kW + warp) * 4 : nullptr, L::ST};
+               A.trace ? A.trace + (static_cast<size_t>(blockIdx.x) * W + warp) * 4 : nullptr, L::ST, W, RES};
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < L::ST; ++s) {
       mbar_init(&full[s], 1);
       cnt[s] = 0;
     }
-    *ctrl = (static_cast<unsigned long long>(kW) << 32) | static_cast<unsigned long long>(L::ST);
+    *ctrl = (static_cast<unsigned long long>(W) << 32) | static_cast<unsigned long long>(L::ST);
   }
   if (lane == 0)
     for (int s = 0; s < kHS; ++s) mbar_init(&hbar[s], 1);
   if (lane == 0) fence_mbar_init();
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (RES) {  // the whole operator, once: nch bulk copies on one barrier
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(L::chunk * sizeof(double));
+      mbar_expect_tx(&full[0], bytes * static_cast<uint32_t>(nch));
+      for (int c = 0; c < nch; ++c)
+        tma_load_1d(ring_buf + static_cast<size_t>(c) * L::chunk, M.G2 + static_cast<size_t>(c) * L::chunk, bytes,
+                    &full[0]);
+    }
+    mbar_wait(&full[0], 0);
+  } else if (threadIdx.x == 0) {
     const uint32_t bytes = static_cast<uint32_t>(L::chunk * sizeof(double));
     for (int s = 0; s < L::ST; ++s) {
       mbar_expect_tx(&full[s], bytes);
@@ -1106,34 +1132,49 @@ __global__ void k_material_batch(MatDev m, int64_t N, const double* eps, const d
   if (plastic) plastic[i] = o.plastic ? 1 : 0;
 }
 
-template <int NT>
-void launch_inc_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
-  constexpr int NP = 8 * NT;
-  const size_t smem = IncLayout<NP>::bytes;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_increment<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    configured = true;
-  }
+constexpr size_t kMaxDynSmem = 227 * 1024;
+
+template <int NT, int W, bool RES>
+void launch_inc_variant(const IncArgs& a, int num_sms, cudaStream_t s, size_t smem) {
+  auto kern = k_increment<NT, W, RES>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaxDynSmem));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment<NT>, kW * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = static_cast<int64_t>(num_sms) * per_sm;
-  const int64_t need = (a.D.P + kW - 1) / kW;
+  const int64_t need = (a.D.P + W - 1) / W;
   if (a.dbg) grid = 1;
   else if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  k_increment<NT><<<static_cast<unsigned>(grid), kW * 32, smem, s>>>(a);
+  kern<<<static_cast<unsigned>(grid), W * 32, smem, s>>>(a);
+}
+
+bool resident_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("FE2_NO_RESIDENT");
+    return e && *e && *e != '0';
+  }();
+  return off;
+}
+
+template <int NT>
+void launch_inc_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
+  constexpr int NP = 8 * NT;
+  const size_t res = IncLayout<NP, kWRes>::res_bytes(a.M.nchunks);
+  if (res <= kMaxDynSmem && !resident_disabled())
+    launch_inc_variant<NT, kWRes, true>(a, num_sms, s, res);
+  else
+    launch_inc_variant<NT, kW, false>(a, num_sms, s, IncLayout<NP, kW>::bytes);
 }
 
 }  // namespace
 
 size_t increment_smem(int NP) {
   switch (NP) {
-    case 8: return IncLayout<8>::bytes;
-    case 16: return IncLayout<16>::bytes;
-    case 24: return IncLayout<24>::bytes;
-    case 32: return IncLayout<32>::bytes;
+    case 8: return IncLayout<8, kW>::bytes;
+    case 16: return IncLayout<16, kW>::bytes;
+    case 24: return IncLayout<24, kW>::bytes;
+    case 32: return IncLayout<32, kW>::bytes;
     default: return 0;
   }
 }

@@ -69,7 +69,7 @@ def run_cell(name, n, K, P_max, incr, path, seconds, seed=0, points=0):
     evals = P * incr
     # algorithmic flops of one assembly: small strain, plastic J2 points only
     # (elastic predictor); finite strain, every cubature point (Kaa, Hq, KaF | r)
-    F_asm = 3.0 * K_j2 * n * (n + 9) if not fs else K * (8.0 * n * n + 72.0 * n)
+    F_asm = 3.0 * K_j2 * n * (n + 9) if not fs else 8.0 * K * n * (n + 5)
     kms = s["kernel_ms"]
     hbm_bytes = (s["timed_assemblies"] + s["timed_commits"]) * K_j2 * 40 + s["timed_commit_plastic"] * 40
     return {
