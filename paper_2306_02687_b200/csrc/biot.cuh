@@ -2,11 +2,14 @@
 // 2-D polar decomposition F = R U, Biot strain U - I through the small-strain
 // packed update (J2 radial return / elastic, materials.hpp:138-214), first
 // Piola-Kirchhoff stress P = R T and its consistent tangent A = dP/dF.
-// Same formulation and operation order as the CPU checker's update_biot (the
-// device may contract a*b+c into FMA, the parity tolerance covers that).
+// Same formulation as the CPU checker's update_biot; the device forms the
+// three reciprocals it needs (1/ρ, 1/|s_tr|, 1/(3μ+h)) once and multiplies,
+// and may contract a*b+c into FMA — ulp-level differences that the 1e-10
+// parity tolerance covers.
 // Components are ordered (F00, F01, F10, F11).
 #pragma once
 
+#include "device_common.cuh"
 #include "material.cuh"
 
 namespace fe2 {
@@ -23,8 +26,8 @@ __device__ __forceinline__ void update_biot(const MatDev& m, double ep0, double 
                                             double eq, double F0, double F1, double F2, double F3, BiotOut& o) {
   const double num = F2 - F1, den = F0 + F3;
   const double rho2 = num * num + den * den;
-  const double rho = sqrt(rho2);
-  const double c = den / rho, s = num / rho;
+  const double inv_rho = dev::rsqrt_fast(rho2);
+  const double c = den * inv_rho, s = num * inv_rho;
   const double U00 = c * F0 + s * F2, U01 = c * F1 + s * F3;
   const double U10 = -s * F0 + c * F2, U11 = -s * F1 + c * F3;
   // update4 on the Biot strain e = (U00 - 1, U11 - 1, 0, (U01 + U10) / 2)
@@ -34,8 +37,9 @@ __device__ __forceinline__ void update_biot(const MatDev& m, double ep0, double 
   const double t0 = lt + two_mu * x0, t1 = lt + two_mu * x1, t2 = lt + two_mu * x2, t3 = two_mu * x3;
   const double p = (t0 + t1 + t2) / 3.0;
   const double d0 = t0 - p, d1 = t1 - p, d2 = t2 - p, d3 = t3;
-  const double ns = sqrt(d0 * d0 + d1 * d1 + d2 * d2 + 2.0 * d3 * d3);
-  const double q_tr = sqrt(1.5) * ns;
+  const double ss = d0 * d0 + d1 * d1 + d2 * d2 + 2.0 * d3 * d3;
+  const double inv_ns = ss > 0.0 ? dev::rsqrt_fast(ss) : 0.0;
+  const double q_tr = sqrt(1.5) * (ss * inv_ns);
   const double f = (m.kind == 1) ? q_tr - (m.sy0 + m.h * eq) : 0.0;
   const bool plastic = (m.kind == 1) && !(f <= 0.0);
   double T00 = t0, T11 = t1, T01 = t3;
@@ -48,9 +52,9 @@ __device__ __forceinline__ void update_biot(const MatDev& m, double ep0, double 
   o.ep3 = ep3;
   o.eq = eq;
   if (plastic) {
-    const double denom = 3.0 * mu + m.h;
-    const double dlam = f / denom;
-    const double r0 = d0 / q_tr, r1 = d1 / q_tr, r2 = d2 / q_tr, r3 = d3 / q_tr;
+    const double dlam = f * m.inv_denom;                  // f / (3 mu + h)
+    const double inv_q = 0.81649658092772603273 * inv_ns;  // 1 / q_tr = sqrt(2/3) / |s_tr|
+    const double r0 = d0 * inv_q, r1 = d1 * inv_q, r2 = d2 * inv_q, r3 = d3 * inv_q;
     const double cs = 3.0 * mu * dlam;
     T00 = t0 - cs * r0;
     T11 = t1 - cs * r1;
@@ -62,9 +66,9 @@ __device__ __forceinline__ void update_biot(const MatDev& m, double ep0, double 
     o.ep3 = ep3 + ce * r3;
     o.eq = eq + dlam;
     if (kTangent) {
-      const double n0 = d0 / ns, n1 = d1 / ns, n3 = d3 / ns;
-      const double c1 = 6.0 * mu * mu * dlam / q_tr;
-      const double c2 = 6.0 * mu * mu * (1.0 / denom - dlam / q_tr);
+      const double n0 = d0 * inv_ns, n1 = d1 * inv_ns, n3 = d3 * inv_ns;
+      const double c1 = 6.0 * mu * mu * dlam * inv_q;
+      const double c2 = 6.0 * mu * mu * (m.inv_denom - dlam * inv_q);
       const double m3 = 2.0 * n3;
       D00 = (D00 - c1 * (2.0 / 3.0)) - c2 * (n0 * n0);
       D01 = (D01 - c1 * (-1.0 / 3.0)) - c2 * (n0 * n1);
@@ -84,7 +88,8 @@ __device__ __forceinline__ void update_biot(const MatDev& m, double ep0, double 
   o.P[3] = s * T01 + c * T11;
   if (!kTangent) return;
   // dθ/dF and R J T, J = [[0,-1],[1,0]]
-  const double g[4] = {-num / rho2, -den / rho2, den / rho2, -num / rho2};
+  const double inv_rho2 = inv_rho * inv_rho;
+  const double g[4] = {-num * inv_rho2, -den * inv_rho2, den * inv_rho2, -num * inv_rho2};
   const double RJT00 = -s * T00 - c * T01, RJT01 = -s * T01 - c * T11;
   const double RJT10 = c * T00 - s * T01, RJT11 = c * T01 - s * T11;
 #pragma unroll

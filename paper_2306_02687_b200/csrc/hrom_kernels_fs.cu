@@ -54,8 +54,8 @@ struct FsLayout {
   static constexpr int kKm = NP * LDK;
   static constexpr int kUnion = kSlots > kKm ? kSlots : kKm;
   static constexpr int kHist = kFHS * 5 * kQC;
-  // α_eval, α, Δα, r, K_aF [NP][4], K_Fa [4][NP], C_FF|P_raw [20] (+4 pad), pivots [NP] (as doubles)
-  static constexpr int WS = 4 * NP + 4 * NP + 4 * NP + 24 + NP + kUnion + kHist;
+  // α_eval, α, Δα, r, K_aF [NP][4], K_Fa [4][NP], C_FF|P_raw [20] (+4 pad), pivots [NP] (int), 1/U_jj [NP]
+  static constexpr int WS = 4 * NP + 4 * NP + 4 * NP + 24 + NP / 2 + NP + kUnion + kHist;
   static constexpr long kBudget = 227L * 1024 - 512 - static_cast<long>(kFW) * WS * 8;
   static constexpr int kFit = static_cast<int>(kBudget / (static_cast<long>(chunk) * 8));
   static constexpr int ST = kFit < 2 ? 2 : (kFit > FE2_FS_STAGES ? FE2_FS_STAGES : kFit);
@@ -164,7 +164,7 @@ __device__ __forceinline__ void mma_f64(double& d0, double& d1, double a, double
 // LU with partial pivoting of the n x n matrix in sA (row stride lda), lane i
 // owning row i (n <= 32); multipliers stored below the diagonal, pivot rows
 // in piv (first maximal |a_ij|, as the oracle's Lu::factor). False if singular.
-__device__ bool warp_lu(double* sA, int lda, int* piv, int n, int lane) {
+__device__ bool warp_lu(double* sA, int lda, int* piv, double* inv_diag, int n, int lane) {
   for (int j = 0; j < n; ++j) {
     double v = (lane >= j && lane < n) ? fabs(sA[lane * lda + j]) : -1.0;
     int idx = lane;
@@ -187,11 +187,13 @@ __device__ bool warp_lu(double* sA, int lda, int* piv, int n, int lane) {
       }
     __syncwarp();
     const double inv = 1.0 / sA[j * lda + j];
+    if (lane == 0) inv_diag[j] = inv;
     if (lane > j && lane < n) {
       double* ri = sA + lane * lda;
       const double* rj = sA + j * lda;
       const double l = ri[j] * inv;
       ri[j] = l;
+#pragma unroll 4
       for (int k = j + 1; k < n; ++k) ri[k] -= l * rj[k];
     }
     __syncwarp();
@@ -200,7 +202,8 @@ __device__ bool warp_lu(double* sA, int lda, int* piv, int n, int lane) {
 }
 
 // Solve A x = b with the factors of warp_lu; lane i holds b_i in, x_i out.
-__device__ double warp_lu_solve(const double* sA, int lda, const int* piv, int n, int lane, double b) {
+__device__ double warp_lu_solve(const double* sA, int lda, const int* piv, const double* inv_diag, int n, int lane,
+                                double b) {
   double y = b;
   for (int j = 0; j < n; ++j) {
     const int p = piv[j];
@@ -216,7 +219,7 @@ __device__ double warp_lu_solve(const double* sA, int lda, const int* piv, int n
   }
   for (int j = n - 1; j >= 0; --j) {
     double xj = 0.0;
-    if (lane == j) y = y / sA[j * lda + j];
+    if (lane == j) y = y * inv_diag[j];
     xj = __shfl_sync(0xffffffffu, y, j);
     if (lane < j) y -= sA[lane * lda + j] * xj;
   }
@@ -247,7 +250,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
   double* sKFa = sKaF + 4 * NP;     // [4][NP]
   double* sCP = sKFa + 4 * NP;      // C_FF (16) | P_raw (4)
   int* sPiv = reinterpret_cast<int*>(sCP + 24);
-  double* sU = sCP + 24 + NP;
+  double* sInvD = sCP + 24 + NP / 2;  // 1 / U_jj of the LU (pivots use the first NP/2 doubles)
+  double* sU = sInvD + NP;
   double* sSlot = sU;               // [32][kSl] per-point w A | w P (assembly pass)
   double* sK = sU;                  // [NP][LDK] K_aa / LU factors (after the pass)
   double* hb = sU + L::kUnion;      // [kFHS][5][32] history stages
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
             const double target = fmin(1.0, done + frac);
             if (target >= 1.0 - 1e-12) {
               // condensation (fs_condense): Y = K^-1 (-K_aF), A_M = (C_FF + K_Fa Y) / V
-              if (!warp_lu(sK, LDK, sPiv, n, lane)) {
+              if (!warp_lu(sK, LDK, sPiv, sInvD, n, lane)) {
                 err = kSolver;
                 write_fail(err, iters, rn);
                 action = 3;
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
               double y[4];
 #pragma unroll
               for (int s = 0; s < 4; ++s)
-                y[s] = warp_lu_solve(sK, LDK, sPiv, n, lane, (lane < n) ? -sKaF[lane * 4 + s] : 0.0);
+                y[s] = warp_lu_solve(sK, LDK, sPiv, sInvD, n, lane, (lane < n) ? -sKaF[lane * 4 + s] : 0.0);
               double out16[16];
 #pragma unroll
               for (int r = 0; r < 4; ++r) {
@@ -656,13 +660,13 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
             break;
           }
           // Newton step: K Δα = -r (LU)
-          if (!warp_lu(sK, LDK, sPiv, n, lane)) {
+          if (!warp_lu(sK, LDK, sPiv, sInvD, n, lane)) {
             err = kSolver;
             write_fail(err, iters, rn);
             action = 3;
             break;
           }
-          const double du = warp_lu_solve(sK, LDK, sPiv, n, lane, -rl);
+          const double du = warp_lu_solve(sK, LDK, sPiv, sInvD, n, lane, -rl);
           if (lane < NP) {
             sDA[lane] = (lane < n) ? du : 0.0;
             sAev[lane] = (lane < n) ? axpy_rn(sAl[lane], 1.0, du) : 0.0;
