@@ -839,42 +839,39 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   const NewtonCfg& cfg = A.cfg;
   constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
 
-  if (A.dbg) {  // assembly dump for parity tests (r, K full, KaE, C_EE, S_raw)
-    if (blockIdx.x == 0 && warp == 0) {
-      const int64_t p = A.dbg_point;
-      for (int a = lane; a < NP; a += 32) sAev[a] = (a < n) ? A.dbg_alpha[a] : 0.0;
-      __syncwarp();
-      assembly_pass(p, A.dbg_E[0], A.dbg_E[1], A.dbg_E[2], -1, false);
-      double* o = A.dbg;
-      for (int a = lane; a < n; a += 32) o[a] = sV[a];
-      for (int e = lane; e < n * n; e += 32) {
-        const int i = e / n, j = e % n;
-        o[n + e] = (j <= i) ? sK[tri_(i) + j] : sK[tri_(j) + i];
-      }
-      for (int e = lane; e < 3 * n; e += 32) o[n + n * n + e] = sKaE[e];
-      if (lane == 0) {
-        double* cc = o + n + n * n + 3 * n;
-        cc[0] = ce00;
-        cc[1] = ce01;
-        cc[2] = ce02;
-        cc[3] = ce01;
-        cc[4] = ce11;
-        cc[5] = ce12;
-        cc[6] = ce02;
-        cc[7] = ce12;
-        cc[8] = ce22;
-        cc[9] = s0;
-        cc[10] = s1;
-        cc[11] = s2;
-      }
+  // Every large piece (assembly pass, factorization, commit pass) has exactly
+  // one call site below, so each is inlined once: the kernel's instruction
+  // footprint stays small enough that warps in different phases do not
+  // thrash the instruction cache.
+  const bool dbg = A.dbg != nullptr;  // assembly dump for parity tests (r, K full, KaE, C_EE, S_raw)
+  auto dump = [&]() {
+    double* o = A.dbg;
+    for (int a = lane; a < n; a += 32) o[a] = sV[a];
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, j = e % n;
+      o[n + e] = (j <= i) ? sK[tri_(i) + j] : sK[tri_(j) + i];
     }
-    while (h_con < h_iss) h_take();
-    ring_drain(R, seq, lane);
-    return;
-  }
+    for (int e = lane; e < 3 * n; e += 32) o[n + n * n + e] = sKaE[e];
+    if (lane == 0) {
+      double* cc = o + n + n * n + 3 * n;
+      cc[0] = ce00;
+      cc[1] = ce01;
+      cc[2] = ce02;
+      cc[3] = ce01;
+      cc[4] = ce11;
+      cc[5] = ce12;
+      cc[6] = ce02;
+      cc[7] = ce12;
+      cc[8] = ce22;
+      cc[9] = s0;
+      cc[10] = s1;
+      cc[11] = s2;
+    }
+  };
 
   // ------------------------------------------------------------ point loop
   auto grab = [&]() -> int64_t {
+    if (dbg) return (blockIdx.x == 0 && warp == 0 && seq == 0) ? A.dbg_point : D.P;
     int v = 0;
     if (lane == 0) v = atomicAdd(A.work, 1);
     return __shfl_sync(0xffffffffu, v, 0);
@@ -883,9 +880,11 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   while (p_next < D.P) {
     const int64_t p = p_next;
     p_next = -1;
-    const double Ep0 = D.E_c[p * 3 + 0], Ep1 = D.E_c[p * 3 + 1], Ep2 = D.E_c[p * 3 + 2];
-    const double Et0 = A.dE[p * 3 + 0], Et1 = A.dE[p * 3 + 1], Et2 = A.dE[p * 3 + 2];
-    const int dead = D.st[p].err;
+    const double Ep0 = dbg ? 0.0 : D.E_c[p * 3 + 0], Ep1 = dbg ? 0.0 : D.E_c[p * 3 + 1],
+                 Ep2 = dbg ? 0.0 : D.E_c[p * 3 + 2];
+    const double Et0 = dbg ? A.dbg_E[0] : A.dE[p * 3 + 0], Et1 = dbg ? A.dbg_E[1] : A.dE[p * 3 + 1],
+                 Et2 = dbg ? A.dbg_E[2] : A.dE[p * 3 + 2];
+    const int dead = dbg ? 0 : D.st[p].err;
     auto write_fail = [&](int code, int iters, double rn) {
       if (lane == 0) {
         A.O.status[p] = code;
@@ -909,7 +908,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     bool after_write = false;  // the previous pass (a sub-step commit) wrote this point's history
     // warm start α = α_committed, E = E_prev + (E_k - E_prev) * 1 (rve.hpp:465-472)
     for (int a = lane; a < NP; a += 32) {
-      const double ac = D.alpha_c[p * NP + a];
+      const double ac = dbg ? ((a < n) ? A.dbg_alpha[a] : 0.0) : D.alpha_c[p * NP + a];
       sAev[a] = ac;
       sAl[a] = ac;
     }
@@ -919,8 +918,12 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     double a = 1.0, rn_it = 0.0, best_rn = 0.0, best_a = 1.0, ref = 0.0, done = 0.0, frac = 1.0;
     int err = 0;
     while (true) {
-      assembly_pass(p, E0, E1, E2, p, after_write);
+      assembly_pass(p, E0, E1, E2, dbg ? -1 : p, after_write);
       after_write = false;
+      if (dbg) {
+        dump();
+        break;
+      }
       const double rl = (lane < n) ? sV[lane] : 0.0;
       const double rn = sqrt(warp_sum(rl * rl));
       const double srn = sqrt(s0 * s0 + s1 * s1 + s2 * s2);
@@ -929,16 +932,21 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       for (int pass = 0; pass < 2; ++pass) {
         if (mode == 0) {  // Newton iterate (micro_newton, rve.hpp:300-342)
           if (it == 0) ref = fmax(fmax(rn, srn), 1e-30);
-          if (rn <= cfg.tol * ref) {
+          const bool conv = rn <= cfg.tol * ref;
+          const double target = fmin(1.0, done + frac);
+          const bool final_commit = conv && target >= 1.0 - 1e-12;
+          const bool newton_step = !conv && it != cfg.max_iter;
+          // the one factorization site: Newton step or final condensation
+          if ((final_commit || newton_step) && !factor()) {
+            if (conv) iters += it;
+            err = kSolver;
+            write_fail(err, iters, rn);
+            action = 3;
+            break;
+          }
+          if (conv) {
             iters += it;
-            const double target = fmin(1.0, done + frac);
-            if (target >= 1.0 - 1e-12) {
-              if (!factor()) {
-                err = kSolver;
-                write_fail(err, iters, rn);
-                action = 3;
-                break;
-              }
+            if (final_commit) {
               // condensation: X = L^-1 K_aE, C = (C_EE - X^T X) / V
               double x0 = (lane < n) ? sKaE[lane * 3 + 0] : 0.0;
               double x1 = (lane < n) ? sKaE[lane * 3 + 1] : 0.0;
@@ -1010,13 +1018,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
             action = 0;
             break;
           }
-          // Newton step: K Δα = -r
-          if (!factor()) {
-            err = kSolver;
-            write_fail(err, iters, rn);
-            action = 3;
-            break;
-          }
+          // Newton step: K Δα = -r (factor computed above)
           const double du = warp_chol_solve(sK, sInv, n, lane, -rl);
           if (lane < NP) {
             sDA[lane] = (lane < n) ? du : 0.0;
@@ -1063,14 +1065,18 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       __syncwarp();
       if (action == 0) continue;
       if (action == 3) break;
-      if (action == 1) {  // final commit; the next point's first chunks load behind it
+      // the one commit site: final (the next point's first chunks load behind it) or sub-step
+      int64_t pred = -1;
+      if (action == 1) {
         p_next = grab();
-        const int pc = commit_pass(p, E0, E1, E2, p_next < D.P ? p_next : -1);
+        pred = p_next < D.P ? p_next : -1;
+      }
+      const int pc = commit_pass(p, E0, E1, E2, pred);
+      if (action == 1) {
         if (lane == 0 && A.O.pcount) A.O.pcount[p] = pc;
         break;
       }
-      // converged sub-step: commit, the next one starts from the new committed state
-      commit_pass(p, E0, E1, E2, -1);
+      // converged sub-step: the next one starts from the new committed state
       after_write = true;
       const double nt = fmin(1.0, done + frac);
       E0 = lerp_rn(Ep0, Et0, nt);
@@ -1081,6 +1087,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       it = 0;
       mode = 0;
     }
+    if (dbg) break;
     if (lane == 0) {
       if (err) D.st[p].err = err;
       D.E_c[p * 3 + 0] = Et0;
