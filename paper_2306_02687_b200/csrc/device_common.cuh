@@ -77,7 +77,6 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double hx = 0.5 * x;
   y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
   return y * fma(-hx * y, y, 1.5);
 }
 

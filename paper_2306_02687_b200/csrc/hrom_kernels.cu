@@ -102,8 +102,9 @@ __device__ __forceinline__ double lerp_rn(double e0, double e1, double t) {
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
-// 1/x and 1/sqrt(x) from the MUFU seeds plus two Newton steps (full fp64
-// accuracy to within an ulp; no IEEE division/sqrt sequences on the critical path).
+// 1/x and 1/sqrt(x) from the MUFU seeds (~2^-22 relative) plus two Newton
+// steps (quadratic: ~2^-88 before rounding, i.e. within an ulp of the fp64
+// result); no IEEE division/sqrt sequences on the critical path.
 __device__ __forceinline__ double rcp_fast(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -116,7 +117,6 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
   y = y * fma(-hx * y, y, 1.5);
   return y * fma(-hx * y, y, 1.5);
 }
@@ -131,14 +131,16 @@ __device__ bool warp_cholesky(double* sK, double* sInv, int n, int lane) {
     if (lane >= j && lane < n) {
       const double* ri = sK + tri_(lane);
       const double* rj = sK + tri_(j);
-      double a0 = 0.0, a1 = 0.0;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int k = 0;
-      for (; k + 1 < j; k += 2) {
+      for (; k + 3 < j; k += 4) {
         a0 += ri[k] * rj[k];
         a1 += ri[k + 1] * rj[k + 1];
+        a2 += ri[k + 2] * rj[k + 2];
+        a3 += ri[k + 3] * rj[k + 3];
       }
-      if (k < j) a0 += ri[k] * rj[k];
-      s = ri[j] - (a0 + a1);
+      for (; k < j; ++k) a0 += ri[k] * rj[k];
+      s = ri[j] - ((a0 + a1) + (a2 + a3));
     }
     const double d = __shfl_sync(0xffffffffu, s, j);
     if (!(d > 0.0)) return false;
