@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--points", type=int, default=0, help="override points per rank (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-points", type=int, default=0)
+    ap.add_argument("--constitutive-points", type=int, default=1 << 25,
+                    help="material points of the SoA constitutive-update roofline run (0 = skip)")
     ap.add_argument("--extra-configs", default="2",
                     help="comma-separated configs also timed device-resident (1 warm-up + 1 step) into "
                          "extra_configs of the line; '' to skip")
@@ -358,6 +360,52 @@ def main():
     h2d = incr * P * nc * 8
     d2h = incr * P * (nc * 8 + nt * 8 + 8 + 3 * 4)
 
+    # ---- the batched constitutive update on SoA HBM buffers (north_star item 1):
+    # the HBM-bound kernel, timed alone on device-resident inputs: strains U[±0.03]
+    # from a history with eq U[0, 0.01] (most points return plastically)
+    constitutive = None
+    if args.constitutive_points > 0:
+        Nm = args.constitutive_points
+        g = torch.Generator(device=dev).manual_seed(1234 + rank)
+        c_eps = (torch.rand((3, Nm), dtype=torch.float64, device=dev, generator=g) - 0.5) * 0.06
+        c_h = [torch.zeros((6, Nm), dtype=torch.float64, device=dev) for _ in range(2)]
+        c_h[0][:4] = (torch.rand((4, Nm), dtype=torch.float64, device=dev, generator=g) - 0.5) * 0.004
+        c_h[0][2] = -(c_h[0][0] + c_h[0][1])
+        c_h[0][4] = torch.rand(Nm, dtype=torch.float64, device=dev, generator=g) * 0.01
+        c_sig = torch.empty((3, Nm), dtype=torch.float64, device=dev)
+        c_C6 = torch.empty((6, Nm), dtype=torch.float64, device=dev)
+        c_pl = torch.empty(Nm, dtype=torch.uint8, device=dev)
+        j2 = F.J2LinearParams()
+
+        def mat_step(k):
+            F.update_material_soa_device(j2, Nm, c_eps.data_ptr(), c_h[0].data_ptr(), c_sig.data_ptr(),
+                                         c_C6.data_ptr(), c_h[1].data_ptr(), c_pl.data_ptr(),
+                                         stream.cuda_stream, device=local)
+
+        for k in range(3):
+            mat_step(k)
+        reps = 10
+        cnt = [0]
+
+        def mat_rep():
+            mat_step(cnt[0])
+            cnt[0] += 1
+
+        mms = timed(lambda: [mat_rep() for _ in range(reps)], 1)
+        # read eps (3) + history (5) = 64 B, write sigma (3) + C6 (6) + history (6) = 120 B + 1 B flag
+        bpp = 64 + 120 + 1
+        gbs = bpp * Nm * reps / (mms / 1e3) / 1e9
+        try:
+            hbm_pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        except Exception:
+            hbm_pk = 6650.0
+        constitutive = {"bound": "hbm", "kernel": "k_material_soa (fe2_material_update_soa_device)",
+                        "points": Nm, "launches": reps, "ms_per_launch": mms / reps,
+                        "bytes_per_point": bpp, "achieved": gbs, "peak": hbm_pk, "unit": "GB/s",
+                        "frac": gbs / hbm_pk, "evals_per_s": Nm * reps / (mms / 1e3),
+                        "plastic_fraction": float(c_pl.float().mean().item())}
+        del c_eps, c_h, c_sig, c_C6, c_pl
+
     # ---- other BASELINE configs, device-resident (weak scaling, same rank layout)
     extras = {}
     for c in [int(x) for x in args.extra_configs.split(",") if x.strip()]:
@@ -433,6 +481,7 @@ def main():
         "gpu_launches": launches,
         "roofline": roofline,
         "roofline_hbm": roofline_hbm,
+        "roofline_constitutive": constitutive,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "newton": {"assemblies_per_eval": stats["timed_assemblies"] / (evals / ws),

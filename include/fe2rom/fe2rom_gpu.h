@@ -86,6 +86,16 @@ int fe2_material_update_batch(int device, const fe2_material_t* mat, int64_t N, 
                               const double* state_in, double* sigma, double* C, double* state_out,
                               uint8_t* plastic);
 
+/* ---- batched material point on DEVICE structure-of-arrays buffers (the
+ * HBM-bound constitutive update; SURVEY §8(b) fe2_material_update_batch with
+ * SoA history). eps[3][N] (E11, E22, g12), hist_in[5][N] (eps_p 11,22,33,12,
+ * eq; NULL = virgin) -> sigma[3][N], C6[6][N] (C00 C01 C02 C11 C12 C22 of the
+ * symmetric condensed tangent), hist_out[6][N] (eps_p[4], eq, sigma33;
+ * nullable), plastic[N] (nullable). Asynchronous on `stream` (cudaStream_t). */
+int fe2_material_update_soa_device(int device, const fe2_material_t* mat, int64_t N, const double* d_eps,
+                                   const double* d_hist_in, double* d_sigma, double* d_C6, double* d_hist_out,
+                                   uint8_t* d_plastic, void* stream);
+
 /* ---- hyper-ROM model on one device.
  * G[K][3][n] host, w[K], mat_id[K] (index into mats), volume = RVE area. */
 int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, const int* mat_id,

@@ -20,6 +20,7 @@ from .hrom import (  # noqa: F401
     lib,
     make_paths,
     update_material_batch,
+    update_material_soa_device,
 )
 
 __all__ = [
@@ -33,4 +34,5 @@ __all__ = [
     "lib",
     "make_paths",
     "update_material_batch",
+    "update_material_soa_device",
 ]

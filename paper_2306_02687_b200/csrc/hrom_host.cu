@@ -369,6 +369,25 @@ int fe2_material_update_batch(int device, const fe2_material_t* mat, int64_t N, 
   });
 }
 
+int fe2_material_update_soa_device(int device, const fe2_material_t* mat, int64_t N, const double* d_eps,
+                                   const double* d_hist_in, double* d_sigma, double* d_C6, double* d_hist_out,
+                                   uint8_t* d_plastic, void* stream) {
+  return guard([&] {
+    check(mat && d_eps && d_sigma && d_C6 && N >= 0, Code::config, "bad arguments");
+    const MatDev m = to_dev(*mat);
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw Failure(Code::numeric, "no CUDA device available: the B200 engine has no CPU fallback");
+    check(device >= 0 && device < count, Code::config, "device index out of range");
+    CK(cudaSetDevice(device));
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    launch_material_soa(m, N, d_eps, d_hist_in, d_sigma, d_C6, d_hist_out, d_plastic, sms,
+                        static_cast<cudaStream_t>(stream));
+    CK(cudaGetLastError());
+  });
+}
+
 int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, const int* mat_id,
                     const fe2_material_t* mats, int n_mats, double volume, fe2_hrom_t* out) {
   return guard([&] {

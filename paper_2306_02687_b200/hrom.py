@@ -71,6 +71,7 @@ def _load():
     L.fe2_version.restype = C.c_char_p
     L.fe2_device_count.restype = C.c_int
     L.fe2_material_update_batch.argtypes = [C.c_int, C.POINTER(_Material), C.c_int64, _dp, _dp, _dp, _dp, _dp, _u8p]
+    L.fe2_material_update_soa_device.argtypes = [C.c_int, C.POINTER(_Material), C.c_int64] + [C.c_void_p] * 7
     L.fe2_hrom_create.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _ip, C.POINTER(_Material), C.c_int, C.c_double,
                                   C.POINTER(C.c_void_p)]
     L.fe2_hrom_create_fs.argtypes = L.fe2_hrom_create.argtypes
@@ -168,6 +169,17 @@ def update_material_batch(mat, eps, state=None, device=0):
     m = mat._c()
     _check(lib.fe2_material_update_batch(device, C.byref(m), N, _d(eps), _d(st), _d(sig), _d(Cm), _d(so), _u8(pl)))
     return sig, Cm, so, pl.astype(bool)
+
+
+def update_material_soa_device(mat, N, eps_ptr, hist_in_ptr, sigma_ptr, C6_ptr, hist_out_ptr=0, plastic_ptr=0,
+                               stream=0, device=0):
+    """Batched update_material on device SoA buffers (pointers as ints):
+    eps[3][N], hist_in[5][N] (0 = virgin) -> sigma[3][N], C6[6][N]
+    (C00 C01 C02 C11 C12 C22), hist_out[6][N], plastic[N] (u8). Async on stream."""
+    m = mat._c()
+    _check(lib.fe2_material_update_soa_device(device, C.byref(m), N, eps_ptr or None, hist_in_ptr or None,
+                                              sigma_ptr or None, C6_ptr or None, hist_out_ptr or None,
+                                              plastic_ptr or None, stream or None))
 
 
 class HyperRomModel:

@@ -230,3 +230,43 @@ def test_small_basis_widths_trajectory_parity(n, K):
     np.testing.assert_array_equal(g["iters"], o["iters"])
     assert path_rel_err(g["sigma"], o["sigma"]).max() < REL
     assert rel_err(g["C"].reshape(-1, 9), o["C"].reshape(-1, 9)).max() < REL
+
+
+@pytest.mark.parametrize("N", [4096, 4097])
+def test_material_soa_device_matches_oracle(N):
+    """The SoA device constitutive update (vector path for even N, scalar
+    path for odd N) equals the oracle's update_material point by point."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    eps = rng.uniform(-0.03, 0.03, size=(N, 3))
+    state = np.zeros((N, 6))
+    state[:, :4] = rng.uniform(-0.01, 0.01, size=(N, 4))
+    state[:, 2] = -(state[:, 0] + state[:, 1])
+    state[:, 4] = rng.uniform(0.0, 0.02, size=N)
+    dev = torch.device("cuda", 0)
+    d_eps = torch.from_numpy(np.ascontiguousarray(eps.T)).to(dev)
+    d_hin = torch.from_numpy(np.ascontiguousarray(state[:, :5].T)).to(dev)
+    d_sig = torch.empty((3, N), dtype=torch.float64, device=dev)
+    d_C6 = torch.empty((6, N), dtype=torch.float64, device=dev)
+    d_hout = torch.empty((6, N), dtype=torch.float64, device=dev)
+    d_pl = torch.empty(N, dtype=torch.uint8, device=dev)
+    mat = F.J2LinearParams()
+    F.update_material_soa_device(mat, N, d_eps.data_ptr(), d_hin.data_ptr(), d_sig.data_ptr(), d_C6.data_ptr(),
+                                 d_hout.data_ptr(), d_pl.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+    torch.cuda.synchronize()
+    sig, C6, hout, pl = (t.cpu().numpy() for t in (d_sig, d_C6, d_hout, d_pl))
+    n_pl = 0
+    for i in list(range(0, N, 11)) + [N - 1]:
+        s_o, C_o, so_o, pl_o = O.update_material(mat, state[i], eps[i])
+        assert bool(pl[i]) == pl_o
+        n_pl += pl_o
+        np.testing.assert_allclose(sig[:, i], s_o, rtol=1e-13, atol=1e-16)
+        np.testing.assert_allclose(C6[:, i], C_o[[0, 0, 0, 1, 1, 2], [0, 1, 2, 1, 2, 2]], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(hout[:, i], so_o, rtol=1e-12, atol=1e-16)
+    assert n_pl > 50
+    # identical to the AoS host-buffer batch API (same device material code)
+    s2, C2, so2, pl2 = F.update_material_batch(mat, eps, state)
+    np.testing.assert_array_equal(sig.T, s2)
+    np.testing.assert_array_equal(hout.T, so2)
+    np.testing.assert_array_equal(pl.astype(bool), pl2)
