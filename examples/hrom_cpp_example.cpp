@@ -32,6 +32,24 @@ int main(int argc, char** argv) {
                   r[0].sigma[0], r[0].sigma[1], r[0].sigma[2], r[0].tangent[0], r[0].iterations,
                   r[0].plastic_points);
     }
+    // finite strain (config 2 kinematics) on the same model: G4 and H = F - I paths
+    fe2_model_t m4 = nullptr;
+    fe2rom::gpu::check(fe2_model_build(33, 12, 200, 0, &m4));
+    std::vector<double> G4(static_cast<size_t>(K) * 4 * n), H(static_cast<size_t>(P) * n_incr * 4);
+    fe2rom::gpu::check(fe2_model_g4(m4, G4.data()));
+    fe2_model_free(m4);
+    fe2rom::gpu::check(fe2_paths(2, 0, 0, P, n_incr, H.data()));
+    fe2rom::gpu::FiniteStrainBatch fs(0, n, K, G4, w, mat,
+                                      {fe2rom::gpu::J2LinearParams{}, fe2rom::gpu::ElasticParams{10.0, 0.3}}, vol);
+    fs.alloc_points(P);
+    for (int k = 0; k < n_incr; ++k) {
+      std::vector<std::array<double, 4>> Hk(P);
+      for (int p = 0; p < P; ++p)
+        for (int c = 0; c < 4; ++c) Hk[p][c] = H[(static_cast<size_t>(p) * n_incr + k) * 4 + c];
+      const auto r = fs.solve_increment(Hk);
+      std::printf("finite-strain increment %d point 0: P = (%.6e, %.6e, %.6e, %.6e) A00 = %.6e iters = %d\n", k + 1,
+                  r[0].P[0], r[0].P[1], r[0].P[2], r[0].P[3], r[0].A[0], r[0].iterations);
+    }
   } catch (const fe2rom::gpu::Error& e) {
     std::printf("fe2rom::gpu::Error code=%d: %s\n", static_cast<int>(e.code()), e.what());
     return e.code() == fe2rom::gpu::ErrorCode::numeric ? 2 : 1;

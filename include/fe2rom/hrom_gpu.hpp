@@ -197,4 +197,64 @@ class HyperRomBatch {
   int64_t P_ = 0;
 };
 
+// Finite-strain (Biot stress) response of one macro point: first
+// Piola-Kirchhoff stress P (F00, F01, F10, F11) and A = dP/dF row-major.
+struct FiniteStrainResponse {
+  std::array<double, 4> P{};
+  std::array<double, 16> A{};
+  int iterations = 0;
+  int plastic_points = 0;
+  double residual = 0.0;
+  int status = 0;
+};
+
+// BASELINE config 2: G4[K][4][n] displacement-gradient operator (n <= 32);
+// each increment takes H = F - I per point. No reference counterpart.
+class FiniteStrainBatch {
+ public:
+  FiniteStrainBatch(int device, int n, int K, const std::vector<double>& G4, const std::vector<double>& w,
+                    const std::vector<int>& mat_id, const std::vector<Material>& materials, double volume) {
+    std::vector<fe2_material_t> mc;
+    for (const auto& m : materials) mc.push_back(to_c(m));
+    check(fe2_hrom_create_fs(device, n, K, G4.data(), w.data(), mat_id.data(), mc.data(),
+                             static_cast<int>(mc.size()), volume, &h_));
+  }
+  ~FiniteStrainBatch() { fe2_hrom_destroy(h_); }
+  FiniteStrainBatch(const FiniteStrainBatch&) = delete;
+  FiniteStrainBatch& operator=(const FiniteStrainBatch&) = delete;
+
+  void alloc_points(int64_t P) {
+    check(fe2_hrom_alloc_points(h_, P, 0));
+    P_ = P;
+  }
+
+  std::vector<FiniteStrainResponse> solve_increment(const std::vector<std::array<double, 4>>& H,
+                                                    const TrajectoryOptions& o = {}) {
+    if (static_cast<int64_t>(H.size()) != P_) throw Error(ErrorCode::config, "one displacement gradient per point");
+    std::vector<double> h(4 * P_), Pm(4 * P_), A(16 * P_), res(P_);
+    std::vector<int> it(P_), pc(P_), st(P_);
+    for (int64_t p = 0; p < P_; ++p)
+      for (int c = 0; c < 4; ++c) h[4 * p + c] = H[p][c];
+    const fe2_newton_opts_t opts{o.micro.tol, o.micro.max_iter, o.max_bisections};
+    check(fe2_hrom_solve_increment(h_, h.data(), &opts, Pm.data(), A.data(), it.data(), pc.data(), res.data(),
+                                   st.data()));
+    std::vector<FiniteStrainResponse> out(P_);
+    for (int64_t p = 0; p < P_; ++p) {
+      for (int c = 0; c < 4; ++c) out[p].P[c] = Pm[4 * p + c];
+      for (int c = 0; c < 16; ++c) out[p].A[c] = A[16 * p + c];
+      out[p].iterations = it[p];
+      out[p].plastic_points = pc[p];
+      out[p].residual = res[p];
+      out[p].status = st[p];
+    }
+    return out;
+  }
+
+  fe2_hrom_t handle() const { return h_; }
+
+ private:
+  fe2_hrom_t h_ = nullptr;
+  int64_t P_ = 0;
+};
+
 }  // namespace fe2rom::gpu

@@ -34,4 +34,5 @@ def test_cpp_wrapper_runs_on_gpu(tmp_path):
     exe = build_example(tmp_path)
     r = subprocess.run([exe, "8"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("increment") == 5
+    assert r.stdout.count("finite-strain increment") == 5
+    assert r.stdout.count("increment") == 10
