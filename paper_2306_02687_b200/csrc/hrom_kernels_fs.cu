@@ -520,26 +520,21 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
   const NewtonCfg& cfg = A.cfg;
   constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
 
-  if (A.dbg) {  // assembly dump: r, K_aa, K_aF, K_Fa, C_FF, P_raw
-    if (blockIdx.x == 0 && warp == 0) {
-      const int64_t p = A.dbg_point;
-      for (int a = lane; a < NP; a += 32) sAev[a] = (a < n) ? A.dbg_alpha[a] : 0.0;
-      __syncwarp();
-      assembly_pass(p, A.dbg_E[0], A.dbg_E[1], A.dbg_E[2], A.dbg_E[3], -1, false);
-      double* o = A.dbg;
-      for (int a = lane; a < n; a += 32) o[a] = sV[a];
-      for (int e = lane; e < n * n; e += 32) o[n + e] = sK[(e / n) * LDK + e % n];
-      for (int e = lane; e < 4 * n; e += 32) o[n + n * n + e] = sKaF[(e / 4) * 4 + e % 4];
-      for (int e = lane; e < 4 * n; e += 32) o[n + n * n + 4 * n + e] = sKFa[(e / n) * NP + e % n];
-      if (lane < 20) o[n + n * n + 8 * n + lane] = sCP[lane];
-    }
-    while (h_con < h_iss) h_take();
-    fs_ring_drain(R, seq, lane);
-    return;
-  }
+  // One call site each for the assembly pass, the LU and the commit pass
+  // (small instruction footprint); the debug dump runs through the same loop.
+  const bool dbg = A.dbg != nullptr;  // assembly dump: r, K_aa, K_aF, K_Fa, C_FF, P_raw
+  auto dump = [&]() {
+    double* o = A.dbg;
+    for (int a = lane; a < n; a += 32) o[a] = sV[a];
+    for (int e = lane; e < n * n; e += 32) o[n + e] = sK[(e / n) * LDK + e % n];
+    for (int e = lane; e < 4 * n; e += 32) o[n + n * n + e] = sKaF[(e / 4) * 4 + e % 4];
+    for (int e = lane; e < 4 * n; e += 32) o[n + n * n + 4 * n + e] = sKFa[(e / n) * NP + e % n];
+    if (lane < 20) o[n + n * n + 8 * n + lane] = sCP[lane];
+  };
 
   // ------------------------------------------------------------ point loop
   auto grab = [&]() -> int64_t {
+    if (dbg) return (blockIdx.x == 0 && warp == 0 && seq == 0) ? A.dbg_point : D.P;
     int v = 0;
     if (lane == 0) v = atomicAdd(A.work, 1);
     return __shfl_sync(0xffffffffu, v, 0);
@@ -551,10 +546,10 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
     double Hp[4], Ht[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      Hp[i] = D.E_c[p * 4 + i];
-      Ht[i] = A.dE[p * 4 + i];
+      Hp[i] = dbg ? 0.0 : D.E_c[p * 4 + i];
+      Ht[i] = dbg ? A.dbg_E[i] : A.dE[p * 4 + i];
     }
-    const int dead = D.st[p].err;
+    const int dead = dbg ? 0 : D.st[p].err;
     auto write_fail = [&](int code, int iters, double rn) {
       if (lane == 0) {
         A.O.status[p] = code;
@@ -574,7 +569,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
     }
     bool after_write = false;
     for (int a = lane; a < NP; a += 32) {
-      const double ac = D.alpha_c[p * NP + a];
+      const double ac = dbg ? ((a < n) ? A.dbg_alpha[a] : 0.0) : D.alpha_c[p * NP + a];
       sAev[a] = ac;
       sAl[a] = ac;
     }
@@ -586,8 +581,12 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
     double a = 1.0, rn_it = 0.0, best_rn = 0.0, best_a = 1.0, ref = 0.0, done = 0.0, frac = 1.0;
     int err = 0;
     while (true) {
-      assembly_pass(p, H[0], H[1], H[2], H[3], p, after_write);
+      assembly_pass(p, H[0], H[1], H[2], H[3], dbg ? -1 : p, after_write);
       after_write = false;
+      if (dbg) {
+        dump();
+        break;
+      }
       const double rl = (lane < n) ? sV[lane] : 0.0;
       const double rn = sqrt(warp_sum(rl * rl));
       const double pr0 = sCP[16], pr1 = sCP[17], pr2 = sCP[18], pr3 = sCP[19];
@@ -596,17 +595,22 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       for (int pass = 0; pass < 2; ++pass) {
         if (mode == 0) {  // Newton iterate (fs_newton)
           if (it == 0) ref = fmax(fmax(rn, prn), 1e-30);
-          if (rn <= cfg.tol * ref) {
+          const bool conv = rn <= cfg.tol * ref;
+          const double target = fmin(1.0, done + frac);
+          const bool final_commit = conv && target >= 1.0 - 1e-12;
+          const bool newton_step = !conv && it != cfg.max_iter;
+          // the one LU site: Newton step or final condensation
+          if ((final_commit || newton_step) && !warp_lu(sK, LDK, sPiv, sInvD, n, lane)) {
+            if (conv) iters += it;
+            err = kSolver;
+            write_fail(err, iters, rn);
+            action = 3;
+            break;
+          }
+          if (conv) {
             iters += it;
-            const double target = fmin(1.0, done + frac);
-            if (target >= 1.0 - 1e-12) {
+            if (final_commit) {
               // condensation (fs_condense): Y = K^-1 (-K_aF), A_M = (C_FF + K_Fa Y) / V
-              if (!warp_lu(sK, LDK, sPiv, sInvD, n, lane)) {
-                err = kSolver;
-                write_fail(err, iters, rn);
-                action = 3;
-                break;
-              }
               double y[4];
 #pragma unroll
               for (int s = 0; s < 4; ++s)
@@ -659,13 +663,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
             action = 0;
             break;
           }
-          // Newton step: K Δα = -r (LU)
-          if (!warp_lu(sK, LDK, sPiv, sInvD, n, lane)) {
-            err = kSolver;
-            write_fail(err, iters, rn);
-            action = 3;
-            break;
-          }
+          // Newton step: K Δα = -r (LU factors computed above)
           const double du = warp_lu_solve(sK, LDK, sPiv, sInvD, n, lane, -rl);
           if (lane < NP) {
             sDA[lane] = (lane < n) ? du : 0.0;
@@ -712,13 +710,17 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       __syncwarp();
       if (action == 0) continue;
       if (action == 3) break;
+      // the one commit site: final (next point's history prefetched) or sub-step
+      int64_t pred = -1;
       if (action == 1) {
         p_next = grab();
-        const int pc = commit_pass(p, H[0], H[1], H[2], H[3], p_next < D.P ? p_next : -1);
+        pred = p_next < D.P ? p_next : -1;
+      }
+      const int pc = commit_pass(p, H[0], H[1], H[2], H[3], pred);
+      if (action == 1) {
         if (lane == 0 && A.O.pcount) A.O.pcount[p] = pc;
         break;
       }
-      commit_pass(p, H[0], H[1], H[2], H[3], -1);
       after_write = true;
       const double nt = fmin(1.0, done + frac);
 #pragma unroll
@@ -728,6 +730,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       it = 0;
       mode = 0;
     }
+    if (dbg) break;
     if (lane == 0) {
       if (err) D.st[p].err = err;
       for (int i = 0; i < 4; ++i) D.E_c[p * 4 + i] = Ht[i];
