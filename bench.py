@@ -451,14 +451,21 @@ def main():
         hbm_src = "MEASURED_PEAKS.json"
     except Exception:
         hbm, hbm_src = 6650.0, "fallback 6.65 TB/s"
-    # history stream of the same kernel: 40 B read per J2 point per pass, 40 B written per plastic commit
-    hbm_bytes = (stats["timed_assemblies"] + stats["timed_commits"]) * K_j2 * 40 + stats["timed_commit_plastic"] * 40
+    # history stream of the same kernel. Small-strain n <= 32 (double-buffered, no
+    # commit pass): every assembly pass reads 40 B and writes its 40-B candidate per
+    # J2 point. Otherwise: 40 B read per J2 point per assembly/commit pass + 40 B
+    # written per plastic commit.
+    if not run.finite and cfg["n"] <= 32:
+        hbm_bytes = stats["timed_assemblies"] * K_j2 * 80
+        bytes_def = "40 B read + 40 B candidate written per J2 point per assembly pass (no commit pass)"
+    else:
+        hbm_bytes = (stats["timed_assemblies"] + stats["timed_commits"]) * K_j2 * 40 + stats["timed_commit_plastic"] * 40
+        bytes_def = "40 B read per J2 point per assembly/commit pass + 40 B written per plastic commit"
     gbs = hbm_bytes / (kms / 1e3) / 1e9 if kms else None
     roofline_hbm = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
                     "frac": gbs / hbm if gbs else None, "peak_source": hbm_src,
                     "kernel": "history stream of the increment kernel (eps_p[4], eq SoA)",
-                    "bytes_definition": "40 B read per J2 point per assembly/commit pass + 40 B written per plastic commit",
-                    "bytes_per_step": hbm_bytes / args.steps}
+                    "bytes_definition": bytes_def, "bytes_per_step": hbm_bytes / args.steps}
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:

@@ -104,6 +104,8 @@ struct fe2_hrom_s {
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
   int ncomp() const { return kin ? 4 : 3; }   // macro input / stress components
+  // the small-n small-strain kernel double-buffers the history (no commit pass)
+  int nbuf() const { return (kin == 0 && NP <= 32) ? 2 : 1; }
   int ntan() const { return kin ? 16 : 9; }    // macro tangent entries
   ModelDev model() const {
     ModelDev M{};
@@ -138,6 +140,8 @@ struct fe2_hrom_s {
     D.sp = sp;
     D.st = st;
     D.flags = flags;
+    D.hist_alt = nbuf() == 2 ? static_cast<int64_t>(P) * K2p * 5 : 0;
+    D.flags_alt = (nbuf() == 2 && flags) ? static_cast<int64_t>(P) * K2p : 0;
     return D;
   }
   void free_points() {
@@ -158,14 +162,14 @@ struct fe2_hrom_s {
     P = 0;
   }
   void zero_points(cudaStream_t s) {
-    CK(cudaMemsetAsync(hist, 0, static_cast<size_t>(P) * K2p * 5 * sizeof(double), s));
+    CK(cudaMemsetAsync(hist, 0, static_cast<size_t>(nbuf()) * P * K2p * 5 * sizeof(double), s));
     const size_t an = static_cast<size_t>(P) * NP * sizeof(double);
     CK(cudaMemsetAsync(alpha_c, 0, an, s));
     CK(cudaMemsetAsync(bp, 0, an, s));
     CK(cudaMemsetAsync(E_c, 0, P * ncomp() * sizeof(double), s));
     CK(cudaMemsetAsync(sp, 0, P * 4 * sizeof(double), s));
     CK(cudaMemsetAsync(st, 0, P * sizeof(PointState), s));
-    if (flags) CK(cudaMemsetAsync(flags, 0, static_cast<size_t>(P) * K2p, s));
+    if (flags) CK(cudaMemsetAsync(flags, 0, static_cast<size_t>(nbuf()) * P * K2p, s));
   }
   ~fe2_hrom_s() {
     cudaSetDevice(device);
@@ -524,14 +528,14 @@ int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags) {
     CK(cudaSetDevice(h->device));
     CK(cudaStreamSynchronize(h->stream));
     h->free_points();
-    h->hist = dalloc<double>(static_cast<size_t>(P) * h->K2p * 5);
+    h->hist = dalloc<double>(static_cast<size_t>(h->nbuf()) * P * h->K2p * 5);
     h->alpha_c = dalloc<double>(static_cast<size_t>(P) * h->NP);
     h->bp = dalloc<double>(static_cast<size_t>(P) * h->NP);
     h->E_c = dalloc<double>(P * h->ncomp());
     h->sp = dalloc<double>(P * 4);
     h->st = dalloc<PointState>(P);
     h->keep_flags = keep_flags != 0;
-    if (h->keep_flags) h->flags = dalloc<uint8_t>(static_cast<size_t>(P) * h->K2p);
+    if (h->keep_flags) h->flags = dalloc<uint8_t>(static_cast<size_t>(h->nbuf()) * P * h->K2p);
     h->dE = dalloc<double>(P * h->ncomp());
     h->o_sigma = dalloc<double>(P * h->ncomp());
     h->o_C = dalloc<double>(P * h->ntan());
@@ -614,12 +618,17 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
     if (alpha)
       for (int64_t p = 0; p < P; ++p)
         for (int a = 0; a < n; ++a) alpha[p * n + a] = ac[p * NP + a];
+    // committed history buffer per point (double-buffered small-n kernel)
+    std::vector<PointState> pst(static_cast<size_t>(P));
+    CK(cudaMemcpy(pst.data(), h->st, pst.size() * sizeof(PointState), cudaMemcpyDeviceToHost));
+    auto curbuf = [&](int64_t p) { return (h->nbuf() == 2 && pst[p].pad[0]) ? 1 : 0; };
     if (state) {
-      std::vector<double> hs(static_cast<size_t>(P) * K2p * 5), Ec(static_cast<size_t>(P) * h->ncomp());
+      std::vector<double> hs(static_cast<size_t>(h->nbuf()) * P * K2p * 5), Ec(static_cast<size_t>(P) * h->ncomp());
       CK(cudaMemcpy(hs.data(), h->hist, hs.size() * sizeof(double), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(Ec.data(), h->E_c, Ec.size() * sizeof(double), cudaMemcpyDeviceToHost));
-      auto hidx = [&](int64_t p, int q2, int comp) {  // [P][K2p/32][5][32]
-        return (static_cast<size_t>(p) * (K2p / kQC) + q2 / kQC) * (5 * kQC) + comp * kQC + q2 % kQC;
+      auto hidx = [&](int64_t p, int q2, int comp) {  // [buf][P][K2p/32][5][32]
+        return static_cast<size_t>(curbuf(p)) * P * K2p * 5 +
+               (static_cast<size_t>(p) * (K2p / kQC) + q2 / kQC) * (5 * kQC) + comp * kQC + q2 % kQC;
       };
       for (int64_t p = 0; p < P && h->kin == 1; ++p) {
         // finite strain: sigma33 of the Biot stress from the committed U - I and eps_p
@@ -660,11 +669,13 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
       }
     }
     if (flags) {
-      std::vector<uint8_t> fl(static_cast<size_t>(P) * K2p);
+      std::vector<uint8_t> fl(static_cast<size_t>(h->nbuf()) * P * K2p);
       CK(cudaMemcpy(fl.data(), h->flags, fl.size(), cudaMemcpyDeviceToHost));
       std::memset(flags, 0, static_cast<size_t>(P) * K);
-      for (int64_t p = 0; p < P; ++p)
-        for (int q2 = 0; q2 < h->K2; ++q2) flags[static_cast<size_t>(p) * K + h->j2_idx[q2]] = fl[p * K2p + q2];
+      for (int64_t p = 0; p < P; ++p) {
+        const size_t off = static_cast<size_t>(curbuf(p)) * P * K2p;
+        for (int q2 = 0; q2 < h->K2; ++q2) flags[static_cast<size_t>(p) * K + h->j2_idx[q2]] = fl[off + p * K2p + q2];
+      }
     }
   });
 }

@@ -257,7 +257,7 @@ struct IncLayout {
   static constexpr int kTri = NP * (NP + 1) / 2;              // packed lower K_aa
   static constexpr int kUnion = (kSlots > kTri) ? kSlots : kTri;
   static constexpr int kHist = kHS * 5 * kQC;                 // per-warp history ring (TMA)
-  static constexpr int WS = 5 * NP + 3 * NP + kUnion + kHist;  // per-warp scratch (doubles)
+  static constexpr int WS = 6 * NP + 3 * NP + kUnion + kHist;  // per-warp scratch (doubles)
   // ring depth: as deep as the 227 KB shared-memory budget allows (<= kMaxStages)
   static constexpr long kBudget = 227L * 1024 - 512 - static_cast<long>(W) * WS * 8;
   static constexpr int kFit = static_cast<int>(kBudget / (static_cast<long>(chunk) * 8));
@@ -393,7 +393,8 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   double* sDA = sAl + NP;        // Δα
   double* sV = sDA + NP;         // residual r
   double* sInv = sV + NP;        // 1 / L_jj
-  double* sKaE = sInv + NP;      // K_aE [NP][3]
+  double* sRp = sInv + NP;       // plastic part of r (Σ_plastic w G^T Δσ) of the last pass
+  double* sKaE = sRp + NP;       // K_aE [NP][3]
   double* sU = sKaE + 3 * NP;
   double* sDC = sU;                                 // [32][6] w ΔC (00 01 02 11 12 22) of the plastic slots
   double* sDS = sU + kQC * 6;                       // [32][3] w Δσ (commit pass: w S(Δεp))
@@ -449,6 +450,9 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
 
   // outputs of an assembly pass (warp-uniform after the reductions)
   double s0 = 0, s1 = 0, s2 = 0, ce00 = 0, ce01 = 0, ce02 = 0, ce11 = 0, ce12 = 0, ce22 = 0;
+  double dsp0 = 0, dsp1 = 0, dsp2 = 0;  // plastic parts of Σraw (for the commit)
+  int np_last = 0;                      // plastic points of the last pass
+  const bool dbg = A.dbg != nullptr;
   bool k_linear = false;  // the last assembly had no plastic point (K_aa == K_e)
   const int n = M.n;
 
@@ -465,9 +469,10 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   auto h_issue = [&](int64_t p, int c) {
     const int s = h_iss % kHS;
     if (lane == 0) {
+      const double* base = D.hist + (D.st[p].pad[0] ? D.hist_alt : 0);  // the committed buffer of p
       fence_proxy_async();  // the stage's previous generic reads precede the async writes
       mbar_expect_tx(&hbar[s], 5 * kQC * sizeof(double));
-      tma_load_1d(hb + s * 5 * kQC, D.hist + (p * nch + c) * (5 * kQC), 5 * kQC * sizeof(double), &hbar[s]);
+      tma_load_1d(hb + s * 5 * kQC, base + (p * nch + c) * (5 * kQC), 5 * kQC * sizeof(double), &hbar[s]);
     }
     ++h_iss;
   };
@@ -490,6 +495,13 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     for (int c = pf_n; c < h_first; ++c) h_issue(p, c);
     pf_p = -1;
     pf_n = 0;
+  };
+  auto h_prefetch = [&](int64_t p) {  // first chunks of point p's next pass, discarding stale ones
+    while (h_con < h_iss) h_take();
+    __syncwarp();
+    for (int c = 0; c < h_first; ++c) h_issue(p, c);
+    pf_p = p;
+    pf_n = h_first;
   };
   auto h_next = [&](int64_t p, int c, int64_t pred) {  // after consuming chunk c of point p
     const int nc = c + kHS;
@@ -516,6 +528,9 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     }
     double c00 = 0.0, c01 = 0.0, c02 = 0.0, c11 = 0.0, c12 = 0.0, c22 = 0.0, ds0 = 0.0, ds1 = 0.0, ds2 = 0.0;
     int np_tot = 0;
+    const bool cur = D.st[p].pad[0] != 0;  // committed buffer; the candidate goes to the other one
+    double* hcand = D.hist + (cur ? 0 : D.hist_alt) + p * nch * (5 * kQC) + lane;
+    uint8_t* fcand = D.flags ? D.flags + (cur ? 0 : D.flags_alt) + p * M.K2p : nullptr;
     h_begin(p, after_write);
     for (int c = 0; c < nch; ++c) {
       double h0, h1, h2, h3, h4;
@@ -556,6 +571,26 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       const int np = __popc(bal);
       n_pl += static_cast<unsigned long long>(np);
       np_tot += np;
+      {  // candidate history of this state (finish_return, materials.hpp:173-185): written every
+         // pass into the non-committed buffer, adopted by a flip if the state is accepted
+        double n0 = h0, n1 = h1, n2 = h2, n3 = h3, n4 = h4;
+        if (plastic) {
+          const double dlam = T.f * mt.inv_denom;
+          const double ce = 1.5 * dlam * rcp_fast(T.q_tr);
+          n0 = h0 + ce * T.d0;
+          n1 = h1 + ce * T.d1;
+          n2 = h2 + ce * T.d2;
+          n3 = h3 + ce * T.d3;
+          n4 = h4 + dlam;
+        }
+        double* Hd = hcand + c * (5 * kQC);
+        Hd[0] = n0;
+        Hd[kQC] = n1;
+        Hd[2 * kQC] = n2;
+        Hd[3 * kQC] = n3;
+        Hd[4 * kQC] = n4;
+        if (fcand && q < M.K2) fcand[q] = plastic ? 1 : 0;
+      }
       if (plastic) {
         const Corr cr = radial_return(mt, T);
         const double wq = M.w2[q];
@@ -646,6 +681,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       if (m == 0) {
         const int a = t * 8 + col;
         sV[a] = v;
+        sRp[a] = v;
         sKaE[a * 3 + 0] = ki[0];
         sKaE[a * 3 + 1] = ki[1];
         sKaE[a * 3 + 2] = ki[2];
@@ -723,6 +759,10 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     ce11 = ce[4] + c11;
     ce12 = ce[5] + c12;
     ce22 = ce[8] + c22;
+    dsp0 = ds0;
+    dsp1 = ds1;
+    dsp2 = ds2;
+    np_last = np_tot;
     k_linear = (np_tot == 0);
     ++n_asm;
     __syncwarp();
@@ -740,102 +780,25 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     return warp_cholesky(sK, sInv, n, lane);
   };
 
-  // commit at (E, sAev): history of the plastic points, flags, b_p, s_p, α_c
-  auto commit_pass = [&](int64_t p, double E0, double E1, double E2, int64_t pred) -> int {
-    double bacc = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    int pc = 0;
-    h_begin(p, false);
-    for (int c = 0; c < nch; ++c) {
-      double h0, h1, h2, h3, h4;
-      {
-        const double* Hs = h_take();
-        h0 = Hs[lane];
-        h1 = Hs[kQC + lane];
-        h2 = Hs[2 * kQC + lane];
-        h3 = Hs[3 * kQC + lane];
-        h4 = Hs[4 * kQC + lane];
-        __syncwarp();
-        h_next(p, c, pred);
-      }
-      const double* Gb = ring_wait(R, seq);
-      const int q = c * kQC + lane;
-      const bool real = q < M.K2;
-      const double* Gq = Gb + lane * S;
-      double e0 = 0.0, e1 = 0.0, e2 = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
-      {  // ε = G_q α with 128-bit shared loads (rows are 16-B aligned, S even)
-        const double2* g0v = reinterpret_cast<const double2*>(Gq);
-        const double2* g1v = reinterpret_cast<const double2*>(Gq + NP);
-        const double2* g2v = reinterpret_cast<const double2*>(Gq + 2 * NP);
-        const double2* av = reinterpret_cast<const double2*>(sAev);
-#pragma unroll 4
-        for (int a = 0; a < NP / 2; ++a) {
-          const double2 al = av[a], x0 = g0v[a], x1 = g1v[a], x2 = g2v[a];
-          e0 += x0.x * al.x;
-          f0 += x0.y * al.y;
-          e1 += x1.x * al.x;
-          f1 += x1.y * al.y;
-          e2 += x2.x * al.x;
-          f2 += x2.y * al.y;
-        }
-      }
-      const MatOut o = update_material(mt, h0, h1, h2, h3, h4, E0 + (e0 + f0), E1 + (e1 + f1), E2 + (e2 + f2));
-      const bool pl = real && o.plastic;
-      double w0 = 0.0, w1 = 0.0, w2 = 0.0;  // w S(Δεp): change of the plastic-strain load
-      if (pl) {
-        const double x0 = o.ep0 - h0, x1 = o.ep1 - h1, x2 = o.ep2 - h2, x3 = o.ep3 - h3;
-        const double lt = mt.lam * (x0 + x1 + x2), wq = M.w2[q];
-        w0 = wq * (lt + 2.0 * mt.mu * x0);
-        w1 = wq * (lt + 2.0 * mt.mu * x1);
-        w2 = wq * (2.0 * mt.mu * x3);
-      }
-      double* H = D.hist + (p * nch + c) * (5 * kQC) + lane;
-      if (pl) {  // elastic points keep their history bit for bit (elastic_result, materials.hpp:187-195)
-        H[0] = o.ep0;
-        H[kQC] = o.ep1;
-        H[2 * kQC] = o.ep2;
-        H[3 * kQC] = o.ep3;
-        H[4 * kQC] = o.eq;
-      }
-      if (D.flags && real) D.flags[p * M.K2p + q] = o.plastic ? 1 : 0;
-      t0 += w0;
-      t1 += w1;
-      t2 += w2;
-      const unsigned bal = __ballot_sync(0xffffffffu, pl);
-      pc += __popc(bal);
-      if (bal) {  // b_p[a] += Σ_plastic q  G_q[:, a] . w S(Δεp_q)   (lane = mode a)
-        sDS[lane * 3 + 0] = w0;
-        sDS[lane * 3 + 1] = w1;
-        sDS[lane * 3 + 2] = w2;
-        __syncwarp();
-        if (lane < NP) {
-          unsigned bits = bal;
-          double b = 0.0;
-          while (bits) {
-            const int l = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const double* gl = Gb + l * S + lane;
-            b += gl[0] * sDS[l * 3 + 0] + gl[NP] * sDS[l * 3 + 1] + gl[2 * NP] * sDS[l * 3 + 2];
-          }
-          bacc += b;
-        }
-      }
-      ring_release(R, seq, lane);
-      ++seq;
+  // Accept the state of the last assembly pass: its candidate history (already
+  // in the other buffer) becomes the committed one, and the committed
+  // plastic-strain loads move by the pass's plastic corrections
+  // (w S(Δεp) = -w Δσ for the deviatoric return): b_p -= r_plastic, s_p -= Σ w Δσ.
+  auto commit_point = [&](int64_t p) -> int {
+    for (int a = lane; a < NP; a += 32) {
+      D.alpha_c[p * NP + a] = sAev[a];
+      D.bp[p * NP + a] -= sRp[a];
     }
-    for (int a = lane; a < NP; a += 32) D.alpha_c[p * NP + a] = sAev[a];
-    if (lane < NP) D.bp[p * NP + lane] += bacc;
-    t0 = warp_sum(t0);
-    t1 = warp_sum(t1);
-    t2 = warp_sum(t2);
     if (lane == 0) {
-      D.sp[p * 4 + 0] += t0;
-      D.sp[p * 4 + 1] += t1;
-      D.sp[p * 4 + 2] += t2;
+      D.sp[p * 4 + 0] -= dsp0;
+      D.sp[p * 4 + 1] -= dsp1;
+      D.sp[p * 4 + 2] -= dsp2;
+      D.st[p].pad[0] ^= 1;
     }
     ++n_com;
-    n_cpl += static_cast<unsigned long long>(pc);
+    n_cpl += static_cast<unsigned long long>(np_last);
     __syncwarp();
-    return pc;
+    return np_last;
   };
 
   const NewtonCfg& cfg = A.cfg;
@@ -845,7 +808,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   // one call site below, so each is inlined once: the kernel's instruction
   // footprint stays small enough that warps in different phases do not
   // thrash the instruction cache.
-  const bool dbg = A.dbg != nullptr;  // assembly dump for parity tests (r, K full, KaE, C_EE, S_raw)
+  // (dbg: assembly dump for parity tests — r, K full, KaE, C_EE, S_raw)
   auto dump = [&]() {
     double* o = A.dbg;
     for (int a = lane; a < n; a += 32) o[a] = sV[a];
@@ -1067,18 +1030,19 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       __syncwarp();
       if (action == 0) continue;
       if (action == 3) break;
-      // the one commit site: final (the next point's first chunks load behind it) or sub-step
-      int64_t pred = -1;
-      if (action == 1) {
-        p_next = grab();
-        pred = p_next < D.P ? p_next : -1;
-      }
-      const int pc = commit_pass(p, E0, E1, E2, pred);
+      // the one commit site: final (the next point's first history chunks are
+      // requested right away) or a converged sub-step
+      const int pc = commit_point(p);
       if (action == 1) {
         if (lane == 0 && A.O.pcount) A.O.pcount[p] = pc;
+        p_next = grab();
+        if (p_next < D.P) h_prefetch(p_next);
         break;
       }
       // converged sub-step: the next one starts from the new committed state
+      // (prefetched chunks came from the old buffer; the new one was written
+      // by generic stores -> fence before the async-proxy reads)
+      pf_p = -1;
       after_write = true;
       const double nt = fmin(1.0, done + frac);
       E0 = lerp_rn(Ep0, Et0, nt);

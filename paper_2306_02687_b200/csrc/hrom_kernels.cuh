@@ -53,8 +53,14 @@ struct PointsDev {
   double* E_c;      // [P][4]  committed macro strain (3) / displacement gradient H (4)
   double* bp;       // [P][NP] Σ_{J2 q} w G_q^T S(eps_p,q)  (committed plastic-strain load)
   double* sp;       // [P][4]  Σ_{J2 q} w S(eps_p,q)
-  PointState* st;
+  PointState* st;   // .pad[0] = which history buffer is committed (small-n kernel)
   uint8_t* flags;   // [P][K2p] plastic flags of the last commit (optional)
+  // small-n kernel (k_increment): double-buffered history. Every assembly pass
+  // writes its candidate history into the non-committed buffer; accepting a
+  // converged state flips st[p].pad[0] (no separate commit pass). Offsets in
+  // elements from hist / flags to the second buffer (0 = single buffer).
+  int64_t hist_alt;
+  int64_t flags_alt;
 };
 
 struct Outputs {
