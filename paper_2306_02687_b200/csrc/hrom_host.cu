@@ -104,8 +104,9 @@ struct fe2_hrom_s {
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
   int ncomp() const { return kin ? 4 : 3; }   // macro input / stress components
-  // the small-n small-strain kernel double-buffers the history (no commit pass)
-  int nbuf() const { return (kin == 0 && NP <= 32) ? 2 : 1; }
+  // the warp-per-point kernels (small strain and finite strain, n <= 32)
+  // double-buffer the history (no commit pass)
+  int nbuf() const { return NP <= 32 ? 2 : 1; }
   int ntan() const { return kin ? 16 : 9; }    // macro tangent entries
   ModelDev model() const {
     ModelDev M{};

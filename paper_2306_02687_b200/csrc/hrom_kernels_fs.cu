@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
   const int m = lane & 3, col = lane >> 2;
   int seq = 0;
   unsigned long long n_asm = 0, n_com = 0, n_pl = 0, n_cpl = 0;
+  int np_last = 0;  // plastic points of the last assembly pass
   const int n = M.n;
   const double volume = M.volume;
   auto valid = [&](int c) -> int {  // real cubature points of chunk c
@@ -300,9 +301,10 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
   auto h_issue = [&](int64_t p, int c) {
     const int s = h_iss % kFHS;
     if (lane == 0) {
+      const double* base = D.hist + (D.st[p].pad[0] ? D.hist_alt : 0);  // the committed buffer of p
       fence_proxy_async();
       mbar_expect_tx(&hbar[s], 5 * kQC * sizeof(double));
-      tma_load_1d(hb + s * 5 * kQC, D.hist + (p * nchh + c) * (5 * kQC), 5 * kQC * sizeof(double), &hbar[s]);
+      tma_load_1d(hb + s * 5 * kQC, base + (p * nchh + c) * (5 * kQC), 5 * kQC * sizeof(double), &hbar[s]);
     }
     ++h_iss;
   };
@@ -325,6 +327,13 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
     for (int c = pf_n; c < h_first; ++c) h_issue(p, c);
     pf_p = -1;
     pf_n = 0;
+  };
+  auto h_prefetch = [&](int64_t p) {  // first chunks of point p's next pass, discarding stale ones
+    while (h_con < h_iss) h_take();
+    __syncwarp();
+    for (int c = 0; c < h_first; ++c) h_issue(p, c);
+    pf_p = p;
+    pf_n = h_first;
   };
   auto h_next = [&](int64_t p, int c, int64_t pred) {
     const int nc = c + kFHS;
@@ -383,6 +392,12 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       kx[i][0] = kx[i][1] = 0.0;
       kfa[i] = 0.0;
     }
+    // candidate history of this state, written into the non-committed buffer;
+    // accepting the state flips st[p].pad[0] (no separate commit pass)
+    const bool cur = D.st[p].pad[0] != 0;
+    double* hcand = D.hist + (cur ? 0 : D.hist_alt) + p * nchh * (5 * kQC) + lane;
+    uint8_t* fcand = D.flags ? D.flags + (cur ? 0 : D.flags_alt) + p * M.K2p : nullptr;
+    int np_tot = 0;
     h_begin(p, after_write);
     for (int c = 0; c < nch; ++c) {
       double h[5];
@@ -394,7 +409,19 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       const double wq = Gb[lane * S + 4 * NP];
       BiotOut o;
       update_biot<true>(c < nchh ? M.mat2 : M.matE, h[0], h[1], h[2], h[3], h[4], F[0], F[1], F[2], F[3], o);
-      n_pl += static_cast<unsigned long long>(__popc(__ballot_sync(0xffffffffu, o.plastic && lane < nv)));
+      const int npc = __popc(__ballot_sync(0xffffffffu, o.plastic && lane < nv));
+      n_pl += static_cast<unsigned long long>(npc);
+      np_tot += npc;
+      if (c < nchh) {  // J2 chunk: candidate εp, eq (pads keep theirs)
+        const bool real = lane < nv;
+        double* Hd = hcand + c * (5 * kQC);
+        Hd[0] = real ? o.ep0 : h[0];
+        Hd[kQC] = real ? o.ep1 : h[1];
+        Hd[2 * kQC] = real ? o.ep2 : h[2];
+        Hd[3 * kQC] = real ? o.ep3 : h[3];
+        Hd[4 * kQC] = real ? o.eq : h[4];
+        if (fcand && real) fcand[c * kQC + lane] = o.plastic ? 1 : 0;
+      }
       double* sl = sSlot + lane * kSl;
 #pragma unroll
       for (int e = 0; e < 16; ++e) sl[e] = wq * o.A[e];
@@ -472,49 +499,20 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       }
       if (lane < 20) sCP[lane] = c20;
     }
+    np_last = np_tot;
     ++n_asm;
     __syncwarp();
   };
 
-  // commit at (H, sAev): history of the plastic J2 points, flags, α_c
-  auto commit_pass = [&](int64_t p, double H0, double H1, double H2, double H3, int64_t pred) -> int {
-    int pc = 0;
-    h_begin(p, false);
-    for (int c = 0; c < nch; ++c) {
-      if (c >= nchh) {  // elastic chunks: nothing to commit, keep the ring turning
-        fs_ring_wait(R, seq);
-        fs_ring_release(R, seq, lane);
-        ++seq;
-        continue;
-      }
-      double h[5];
-      h_read(p, c, pred, h);
-      const double* Gb = fs_ring_wait(R, seq);
-      const int q = c * kQC + lane;
-      const bool real = q < M.K2;
-      double F[4];
-      deformation(Gb, H0, H1, H2, H3, F);
-      BiotOut o;
-      update_biot<false>(M.mat2, h[0], h[1], h[2], h[3], h[4], F[0], F[1], F[2], F[3], o);
-      const bool pl = real && o.plastic;
-      if (pl) {  // elastic points keep their history bit for bit
-        double* Hd = D.hist + (p * nchh + c) * (5 * kQC) + lane;
-        Hd[0] = o.ep0;
-        Hd[kQC] = o.ep1;
-        Hd[2 * kQC] = o.ep2;
-        Hd[3 * kQC] = o.ep3;
-        Hd[4 * kQC] = o.eq;
-      }
-      if (D.flags && real) D.flags[p * M.K2p + q] = o.plastic ? 1 : 0;
-      pc += __popc(__ballot_sync(0xffffffffu, pl));
-      fs_ring_release(R, seq, lane);
-      ++seq;
-    }
+  // accept the state of the last assembly pass: its candidate history becomes
+  // the committed one (flip), α_c, plastic count
+  auto commit_point = [&](int64_t p) -> int {
     for (int a = lane; a < NP; a += 32) D.alpha_c[p * NP + a] = sAev[a];
+    if (lane == 0) D.st[p].pad[0] ^= 1;
     ++n_com;
-    n_cpl += static_cast<unsigned long long>(pc);
+    n_cpl += static_cast<unsigned long long>(np_last);
     __syncwarp();
-    return pc;
+    return np_last;
   };
 
   const NewtonCfg& cfg = A.cfg;
@@ -710,17 +708,17 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       __syncwarp();
       if (action == 0) continue;
       if (action == 3) break;
-      // the one commit site: final (next point's history prefetched) or sub-step
-      int64_t pred = -1;
-      if (action == 1) {
-        p_next = grab();
-        pred = p_next < D.P ? p_next : -1;
-      }
-      const int pc = commit_pass(p, H[0], H[1], H[2], H[3], pred);
+      // the one commit site: final (the next point's history is requested right
+      // away) or a converged sub-step (stale prefetches dropped; fence before
+      // the async-proxy reads of the buffer just written by generic stores)
+      const int pc = commit_point(p);
       if (action == 1) {
         if (lane == 0 && A.O.pcount) A.O.pcount[p] = pc;
+        p_next = grab();
+        if (p_next < D.P && nchh > 0) h_prefetch(p_next);
         break;
       }
+      pf_p = -1;
       after_write = true;
       const double nt = fmin(1.0, done + frac);
 #pragma unroll
