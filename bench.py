@@ -444,6 +444,11 @@ def main():
         except Exception:
             traffic = None
     roofline["traffic"] = traffic
+    if constitutive is not None and os.path.exists(prof):
+        try:
+            constitutive["traffic"] = json.load(open(prof)).get("constitutive_soa", {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
     kms = stats["kernel_ms"]
     K_j2 = model.K_j2
     try:
@@ -451,11 +456,11 @@ def main():
         hbm_src = "MEASURED_PEAKS.json"
     except Exception:
         hbm, hbm_src = 6650.0, "fallback 6.65 TB/s"
-    # history stream of the same kernel. Small-strain n <= 32 (double-buffered, no
-    # commit pass): every assembly pass reads 40 B and writes its 40-B candidate per
-    # J2 point. Otherwise: 40 B read per J2 point per assembly/commit pass + 40 B
-    # written per plastic commit.
-    if not run.finite and cfg["n"] <= 32:
+    # history stream of the same kernel. n <= 32 (warp-per-point kernels, double-
+    # buffered history, no commit pass): every assembly pass reads 40 B and writes
+    # its 40-B candidate per J2 point. Otherwise: 40 B read per J2 point per
+    # assembly/commit pass + 40 B written per plastic commit.
+    if cfg["n"] <= 32:
         hbm_bytes = stats["timed_assemblies"] * K_j2 * 80
         bytes_def = "40 B read + 40 B candidate written per J2 point per assembly pass (no commit pass)"
     else:
