@@ -456,16 +456,10 @@ def main():
         hbm_src = "MEASURED_PEAKS.json"
     except Exception:
         hbm, hbm_src = 6650.0, "fallback 6.65 TB/s"
-    # history stream of the same kernel. n <= 32 (warp-per-point kernels, double-
-    # buffered history, no commit pass): every assembly pass reads 40 B and writes
-    # its 40-B candidate per J2 point. Otherwise: 40 B read per J2 point per
-    # assembly/commit pass + 40 B written per plastic commit.
-    if cfg["n"] <= 32:
-        hbm_bytes = stats["timed_assemblies"] * K_j2 * 80
-        bytes_def = "40 B read + 40 B candidate written per J2 point per assembly pass (no commit pass)"
-    else:
-        hbm_bytes = (stats["timed_assemblies"] + stats["timed_commits"]) * K_j2 * 40 + stats["timed_commit_plastic"] * 40
-        bytes_def = "40 B read per J2 point per assembly/commit pass + 40 B written per plastic commit"
+    # history stream of the same kernel (double-buffered history, no commit pass):
+    # every assembly pass reads 40 B and writes its 40-B candidate per J2 point
+    hbm_bytes = stats["timed_assemblies"] * K_j2 * 80
+    bytes_def = "40 B read + 40 B candidate written per J2 point per assembly pass (no commit pass)"
     gbs = hbm_bytes / (kms / 1e3) / 1e9 if kms else None
     roofline_hbm = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
                     "frac": gbs / hbm if gbs else None, "peak_source": hbm_src,

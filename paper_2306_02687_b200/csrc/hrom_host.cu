@@ -104,9 +104,8 @@ struct fe2_hrom_s {
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
   int ncomp() const { return kin ? 4 : 3; }   // macro input / stress components
-  // the warp-per-point kernels (small strain and finite strain, n <= 32)
-  // double-buffer the history (no commit pass)
-  int nbuf() const { return NP <= 32 ? 2 : 1; }
+  // every increment kernel double-buffers the history (no commit pass)
+  int nbuf() const { return 2; }
   int ntan() const { return kin ? 16 : 9; }    // macro tangent entries
   ModelDev model() const {
     ModelDev M{};

@@ -42,8 +42,8 @@ struct Big {
   static constexpr int chunk = QB * S;
   static constexpr int TRI = NP * (NP + 1) / 2;
   static constexpr int RED = 64;
-  // doubles: ring[2][chunk] | sK[TRI] | vectors 8 NP | slots QB*(6+3) + QB ints | red
-  static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + TRI + 8 * NP + QB * 10 + RED;
+  // doubles: ring[2][chunk] | sK[TRI] | vectors 9 NP | slots QB*(6+3) + QB ints | red
+  static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + TRI + 9 * NP + QB * 10 + RED;
   static constexpr size_t bytes = dbl * sizeof(double) + 2 * sizeof(uint64_t) + 16 * sizeof(int);
 };
 
@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
   double* sDA = sAl + NP;
   double* sV = sDA + NP;
   double* sInv = sV + NP;
-  double* sKaE = sInv + NP;  // [NP][3]
+  double* sRp = sInv + NP;   // plastic part of r of the last pass (for the commit)
+  double* sKaE = sRp + NP;   // [NP][3]
   double* sDC = sKaE + 3 * NP;
   double* sDS = sDC + QB * 6;
   int* sQ = reinterpret_cast<int*>(sDS + QB * 3);
@@ -308,8 +309,11 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
   unsigned long long n_asm = 0, n_com = 0, n_pl = 0, n_cpl = 0;
 
   const int qi = tid / TPQ, sub = tid % TPQ;  // cubature point of this thread within a chunk, mode slice
-  auto hist_ptr = [&](int64_t p, int q) {      // [P][K2p/32][5][32]
-    return D.hist + (p * (M.K2p / kQC) + q / kQC) * (5 * kQC) + (q % kQC);
+  // [buf][P][K2p/32][5][32]: the committed buffer of a point is st[p].pad[0];
+  // every assembly pass writes its candidate history into the other one and
+  // accepting a state flips the bit (no commit pass)
+  auto hist_ptr = [&](int64_t p, int q, bool buf) {
+    return D.hist + (buf ? D.hist_alt : 0) + (p * (M.K2p / kQC) + q / kQC) * (5 * kQC) + (q % kQC);
   };
   auto ring_take = [&]() -> const double* {
     const int s = pos & 1;
@@ -366,6 +370,8 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
 
   // outputs of an assembly pass
   double s0 = 0, s1 = 0, s2 = 0, ce00 = 0, ce01 = 0, ce02 = 0, ce11 = 0, ce12 = 0, ce22 = 0;
+  double dsp0 = 0, dsp1 = 0, dsp2 = 0;  // plastic parts of Σraw
+  int np_last = 0;
   bool k_linear = false;
 
   auto assembly_pass = [&](int64_t p, double E0, double E1, double E2) {
@@ -375,9 +381,10 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
     double c00 = 0, c01 = 0, c02 = 0, c11 = 0, c12 = 0, c22 = 0, ds0 = 0, ds1 = 0, ds2 = 0;
     double rr = 0.0, ka0 = 0.0, ka1 = 0.0, ka2 = 0.0;  // thread a < NP: r, K_aE corrections of mode a
     int np_tot = 0;
+    const bool cur = D.st[p].pad[0] != 0;
     double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
     if (sub == 0) {
-      const double* H = hist_ptr(p, qi);
+      const double* H = hist_ptr(p, qi, cur);
       h0 = H[0];
       h1 = H[kQC];
       h2 = H[2 * kQC];
@@ -395,8 +402,27 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
         const Trial T = trial_state(mt, h0, h1, h2, h3, h4, e0, e1, e2);
         plastic = (T.f > 0.0) && (q < M.K2);
         if (plastic) cr = radial_return(mt, T);
+        {  // candidate history (finish_return) into the non-committed buffer
+          double n0 = h0, n1 = h1, n2 = h2, n3 = h3, n4 = h4;
+          if (plastic) {
+            const double dlam = T.f * mt.inv_denom;
+            const double ce = 1.5 * dlam * rcp_fast(T.q_tr);
+            n0 = h0 + ce * T.d0;
+            n1 = h1 + ce * T.d1;
+            n2 = h2 + ce * T.d2;
+            n3 = h3 + ce * T.d3;
+            n4 = h4 + dlam;
+          }
+          double* Hc = hist_ptr(p, q, !cur);
+          Hc[0] = n0;
+          Hc[kQC] = n1;
+          Hc[2 * kQC] = n2;
+          Hc[3 * kQC] = n3;
+          Hc[4 * kQC] = n4;
+          if (D.flags && q < M.K2) D.flags[(cur ? 0 : D.flags_alt) + p * M.K2p + q] = plastic ? 1 : 0;
+        }
         if (c + 1 < nch) {
-          const double* H = hist_ptr(p, q + QB);
+          const double* H = hist_ptr(p, q + QB, cur);
           h0 = H[0];
           h1 = H[kQC];
           h2 = H[2 * kQC];
@@ -457,6 +483,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
       ring_release();
     }
     store_dispatch<NT, MP>(warp, sK, acc, lane);
+    if (tid < NP) sRp[tid] = rr;
     c00 = block_sum(c00, red);
     c01 = block_sum(c01, red);
     c02 = block_sum(c02, red);
@@ -501,6 +528,10 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
     ce11 = ce[4] + c11;
     ce12 = ce[5] + c12;
     ce22 = ce[8] + c22;
+    dsp0 = ds0;
+    dsp1 = ds1;
+    dsp2 = ds2;
+    np_last = np_tot;
     k_linear = (np_tot == 0);
     ++n_asm;
     __syncthreads();
@@ -516,88 +547,25 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
     return cta_cholesky(sK, sInv, red, n);
   };
 
-  auto commit_pass = [&](int64_t p, double E0, double E1, double E2) -> int {
-    double bacc = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    int pc = 0;
-    double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
-    if (sub == 0) {
-      const double* H = hist_ptr(p, qi);
-      h0 = H[0];
-      h1 = H[kQC];
-      h2 = H[2 * kQC];
-      h3 = H[3 * kQC];
-      h4 = H[4 * kQC];
+  // accept the last pass's state: flip to its candidate history, α_c, and move
+  // the committed plastic-strain loads by its plastic corrections
+  // (w S(Δεp) = -w Δσ): b_p -= r_plastic, s_p -= Σ w Δσ
+  auto commit_point = [&](int64_t p) -> int {
+    for (int a = tid; a < NP; a += kBT) {
+      D.alpha_c[p * NP + a] = sAev[a];
+      D.bp[p * NP + a] -= sRp[a];
     }
-    for (int c = 0; c < nch; ++c) {
-      const double* Gb = ring_take();
-      const int q = c * QB + qi;
-      double e0, e1, e2;
-      strain(Gb, E0, E1, E2, e0, e1, e2);
-      bool pl = false;
-      double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-      if (sub == 0) {
-        const MatOut o = update_material(mt, h0, h1, h2, h3, h4, e0, e1, e2);
-        pl = (q < M.K2) && o.plastic;
-        double* H = hist_ptr(p, q);
-        if (pl) {
-          const double x0 = o.ep0 - h0, x1 = o.ep1 - h1, x2 = o.ep2 - h2, x3 = o.ep3 - h3;
-          const double lt = mt.lam * (x0 + x1 + x2), wq = M.w2[q];
-          w0 = wq * (lt + 2.0 * mt.mu * x0);
-          w1 = wq * (lt + 2.0 * mt.mu * x1);
-          w2 = wq * (2.0 * mt.mu * x3);
-        }
-        if (c + 1 < nch) {
-          const double* Hn = hist_ptr(p, q + QB);
-          h0 = Hn[0];
-          h1 = Hn[kQC];
-          h2 = Hn[2 * kQC];
-          h3 = Hn[3 * kQC];
-          h4 = Hn[4 * kQC];
-        }
-        if (pl) {
-          H[0] = o.ep0;
-          H[kQC] = o.ep1;
-          H[2 * kQC] = o.ep2;
-          H[3 * kQC] = o.ep3;
-          H[4 * kQC] = o.eq;
-        }
-        if (D.flags && q < M.K2) D.flags[p * M.K2p + q] = o.plastic ? 1 : 0;
-        t0 += w0;
-        t1 += w1;
-        t2 += w2;
-      }
-      int slot, np;
-      compact(pl, slot, np);
-      if (pl) {
-        sDS[slot * 3 + 0] = w0;
-        sDS[slot * 3 + 1] = w1;
-        sDS[slot * 3 + 2] = w2;
-        sQ[slot] = qi;
-      }
-      pc += np;
-      __syncthreads();
-      if (tid < NP)
-        for (int sl = 0; sl < np; ++sl) {
-          const double* Gq = Gb + sQ[sl] * S + tid;
-          bacc += Gq[0] * sDS[sl * 3 + 0] + Gq[NP] * sDS[sl * 3 + 1] + Gq[2 * NP] * sDS[sl * 3 + 2];
-        }
-      __syncthreads();
-      ring_release();
-    }
-    for (int a = tid; a < NP; a += kBT) D.alpha_c[p * NP + a] = sAev[a];
-    if (tid < NP) D.bp[p * NP + tid] += bacc;
-    t0 = block_sum(t0, red);
-    t1 = block_sum(t1, red);
-    t2 = block_sum(t2, red);
+    __syncthreads();  // every thread has read st[p].pad[0] of this pass before the flip
     if (tid == 0) {
-      D.sp[p * 4 + 0] += t0;
-      D.sp[p * 4 + 1] += t1;
-      D.sp[p * 4 + 2] += t2;
+      D.sp[p * 4 + 0] -= dsp0;
+      D.sp[p * 4 + 1] -= dsp1;
+      D.sp[p * 4 + 2] -= dsp2;
+      D.st[p].pad[0] ^= 1;
     }
     ++n_com;
-    n_cpl += static_cast<unsigned long long>(tid == 0 ? pc : 0);
+    n_cpl += static_cast<unsigned long long>(tid == 0 ? np_last : 0);
     __syncthreads();
-    return pc;
+    return np_last;
   };
 
   const NewtonCfg& cfg = A.cfg;
@@ -808,7 +776,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
         __syncthreads();
         if (action == 0) continue;
         if (action == 3) break;
-        const int pc = commit_pass(p, E0, E1, E2);
+        const int pc = commit_point(p);
         if (action == 1) {
           if (tid == 0 && A.O.pcount) A.O.pcount[p] = pc;
           break;
