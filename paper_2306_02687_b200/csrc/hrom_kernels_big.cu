@@ -149,14 +149,43 @@ __device__ __forceinline__ void load_frags(const double* gp, int i, double k0, d
   }
 }
 
+// does warp W own the diagonal tile pair (t, t)? Its owner also accumulates
+// the r and K_aE corrections of the modes of tile t from the same fragments
+// (NT <= 8; above that the extra accumulators would spill, and a per-mode
+// loop over the plastic slots is used instead).
+template <int NT>
+constexpr bool kFragCorr = NT <= 8;
+template <int NT>
+constexpr bool owns_diag(int W, int t) {
+  if (!kFragCorr<NT>) return false;
+  const PairTable P = pairs_for<NT>(W);
+  for (int j = 0; j < P.n; ++j)
+    if (P.t1[j] == t && P.t2[j] == t) return true;
+  return false;
+}
+template <int NT, int W, int T>
+__device__ __forceinline__ void diag_acc(const double (&A)[NT], const double (&B)[NT], double ws, int s,
+                                         double (&kae)[NT][3], double (&rr)[NT]) {
+  if constexpr (T < NT) {
+    if constexpr (owns_diag<NT>(W, T)) {
+      // K_aE correction row (s + m) mod 3 of mode 8T + col, and r correction
+      if (s == 0) kae[T][0] += B[T];
+      else if (s == 1) kae[T][1] += B[T];
+      else kae[T][2] += B[T];
+      rr[T] += ws * A[T];
+    }
+    diag_acc<NT, W, T + 1>(A, B, ws, s, kae, rr);
+  }
+}
+
 // DMMA over the chunk's plastic slots for warp W's tile pairs.
 template <int NT, int W, int MP>
 __device__ __forceinline__ void contract(const double* Gb, const double* sDC, const double* sDS, const int* sQ,
-                                         int np4, double (&acc)[MP][2], int lane) {
+                                         int np4, double (&acc)[MP][2], double (&kae)[NT][3], double (&rr)[NT],
+                                         int lane) {
   constexpr int S = Big<NT>::S;
   const int m = lane & 3, col = lane >> 2;
   const int ng = np4 >> 2;
-  (void)sDS;
 #pragma unroll 1
   for (int g = 0; g < ng; ++g) {
 #pragma unroll
@@ -166,11 +195,45 @@ __device__ __forceinline__ void contract(const double* Gb, const double* sDC, co
       const int bb = i > 0 ? 1 : 0;
       const double* wc = sDC + slot * 6;
       const double k0 = wc[i], k1 = wc[i + 1 + bb], k2 = wc[i + 2 + bb];
+      const double ws = sDS[slot * 3 + i];
       const double* gp = Gb + sQ[slot] * S + col;
       double A[NT], B[NT];
       load_frags<NT, W, 0>(gp, i, k0, k1, k2, A, B);
       dmma_pairs<NT, W, 0, MP>(acc, A, B);
+      diag_acc<NT, W, 0>(A, B, ws, s, kae, rr);
     }
+  }
+}
+
+// reduce the owned tiles' r / K_aE corrections over the four k-lanes of each
+// column and store them (sV = r_plastic, sKaE = K_aE correction)
+template <int NT, int W, int T>
+__device__ __forceinline__ void diag_store(const double (&kae)[NT][3], const double (&rr)[NT], double* sV,
+                                           double* sKaE, int lane) {
+  if constexpr (T < NT) {
+    if constexpr (owns_diag<NT>(W, T)) {
+      const int m = lane & 3, col = lane >> 2;
+      double v = rr[T];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      double ki[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int s = (i - (m % 3) + 3) % 3;  // slot s holds strain row (s + m) mod 3
+        double x = (s == 0) ? kae[T][0] : ((s == 1) ? kae[T][1] : kae[T][2]);
+        x += __shfl_xor_sync(0xffffffffu, x, 1);
+        x += __shfl_xor_sync(0xffffffffu, x, 2);
+        ki[i] = x;
+      }
+      if (m == 0) {
+        const int a = T * 8 + col;
+        sV[a] = v;
+        sKaE[a * 3 + 0] = ki[0];
+        sKaE[a * 3 + 1] = ki[1];
+        sKaE[a * 3 + 2] = ki[2];
+      }
+    }
+    diag_store<NT, W, T + 1>(kae, rr, sV, sKaE, lane);
   }
 }
 
@@ -181,16 +244,31 @@ __device__ __forceinline__ void store_tiles(double* sK, const double (&acc)[MP][
 
 template <int NT, int MP>
 __device__ __forceinline__ void contract_dispatch(int warp, const double* Gb, const double* sDC, const double* sDS,
-                                                  const int* sQ, int np4, double (&acc)[MP][2], int lane) {
+                                                  const int* sQ, int np4, double (&acc)[MP][2],
+                                                  double (&kae)[NT][3], double (&rr)[NT], int lane) {
   switch (warp) {
-    case 0: contract<NT, 0, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
-    case 1: contract<NT, 1, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
-    case 2: contract<NT, 2, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
-    case 3: contract<NT, 3, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
-    case 4: contract<NT, 4, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
-    case 5: contract<NT, 5, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
-    case 6: contract<NT, 6, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
-    default: contract<NT, 7, MP>(Gb, sDC, sDS, sQ, np4, acc, lane); break;
+    case 0: contract<NT, 0, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+    case 1: contract<NT, 1, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+    case 2: contract<NT, 2, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+    case 3: contract<NT, 3, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+    case 4: contract<NT, 4, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+    case 5: contract<NT, 5, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+    case 6: contract<NT, 6, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+    default: contract<NT, 7, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+  }
+}
+template <int NT>
+__device__ __forceinline__ void diag_store_dispatch(int warp, const double (&kae)[NT][3], const double (&rr)[NT],
+                                                    double* sV, double* sKaE, int lane) {
+  switch (warp) {
+    case 0: diag_store<NT, 0, 0>(kae, rr, sV, sKaE, lane); break;
+    case 1: diag_store<NT, 1, 0>(kae, rr, sV, sKaE, lane); break;
+    case 2: diag_store<NT, 2, 0>(kae, rr, sV, sKaE, lane); break;
+    case 3: diag_store<NT, 3, 0>(kae, rr, sV, sKaE, lane); break;
+    case 4: diag_store<NT, 4, 0>(kae, rr, sV, sKaE, lane); break;
+    case 5: diag_store<NT, 5, 0>(kae, rr, sV, sKaE, lane); break;
+    case 6: diag_store<NT, 6, 0>(kae, rr, sV, sKaE, lane); break;
+    default: diag_store<NT, 7, 0>(kae, rr, sV, sKaE, lane); break;
   }
 }
 template <int NT, int MP>
@@ -379,7 +457,10 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
 #pragma unroll
     for (int j = 0; j < MP; ++j) acc[j][0] = acc[j][1] = 0.0;
     double c00 = 0, c01 = 0, c02 = 0, c11 = 0, c12 = 0, c22 = 0, ds0 = 0, ds1 = 0, ds2 = 0;
-    double rr = 0.0, ka0 = 0.0, ka1 = 0.0, ka2 = 0.0;  // thread a < NP: r, K_aE corrections of mode a
+    double kae[NT][3], rr[NT];  // r / K_aE corrections of the diagonal tiles this warp owns
+#pragma unroll
+    for (int t = 0; t < NT; ++t) rr[t] = kae[t][0] = kae[t][1] = kae[t][2] = 0.0;
+    double rm = 0.0, ka0 = 0.0, ka1 = 0.0, ka2 = 0.0;  // NT > 8: thread a < NP, mode a
     int np_tot = 0;
     const bool cur = D.st[p].pad[0] != 0;
     double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
@@ -466,24 +547,33 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
       n_pl += static_cast<unsigned long long>(tid == 0 ? np : 0);
       np_tot += np;
       __syncthreads();
-      contract_dispatch<NT, MP>(warp, Gb, sDC, sDS, sQ, np4, acc, lane);
-      if (tid < NP) {  // r and K_aE corrections of mode a = tid
-        for (int sl = 0; sl < np; ++sl) {
-          const double* Gq = Gb + sQ[sl] * S + tid;
-          const double g0 = Gq[0], g1 = Gq[NP], g2 = Gq[2 * NP];
-          const double* dc = sDC + sl * 6;
-          const double* ds = sDS + sl * 3;
-          rr += g0 * ds[0] + g1 * ds[1] + g2 * ds[2];
-          ka0 += g0 * dc[0] + g1 * dc[1] + g2 * dc[2];
-          ka1 += g0 * dc[1] + g1 * dc[3] + g2 * dc[4];
-          ka2 += g0 * dc[2] + g1 * dc[4] + g2 * dc[5];
+      contract_dispatch<NT, MP>(warp, Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane);
+      if constexpr (!kFragCorr<NT>) {
+        if (tid < NP) {  // r and K_aE corrections of mode a = tid
+          for (int sl = 0; sl < np; ++sl) {
+            const double* Gq = Gb + sQ[sl] * S + tid;
+            const double g0 = Gq[0], g1 = Gq[NP], g2 = Gq[2 * NP];
+            const double* dc = sDC + sl * 6;
+            const double* ds = sDS + sl * 3;
+            rm += g0 * ds[0] + g1 * ds[1] + g2 * ds[2];
+            ka0 += g0 * dc[0] + g1 * dc[1] + g2 * dc[2];
+            ka1 += g0 * dc[1] + g1 * dc[3] + g2 * dc[4];
+            ka2 += g0 * dc[2] + g1 * dc[4] + g2 * dc[5];
+          }
         }
       }
       __syncthreads();
       ring_release();
     }
     store_dispatch<NT, MP>(warp, sK, acc, lane);
-    if (tid < NP) sRp[tid] = rr;
+    if constexpr (kFragCorr<NT>) {
+      diag_store_dispatch<NT>(warp, kae, rr, sRp, sKaE, lane);
+    } else if (tid < NP) {
+      sRp[tid] = rm;
+      sKaE[tid * 3 + 0] = ka0;
+      sKaE[tid * 3 + 1] = ka1;
+      sKaE[tid * 3 + 2] = ka2;
+    }
     c00 = block_sum(c00, red);
     c01 = block_sum(c01, red);
     c02 = block_sum(c02, red);
@@ -506,10 +596,10 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
         sx += k0 * sAev[b];
         if (b <= a) ka[b] += k0;
       }
-      sV[a] = rr + sx + (ke[0] * E0 + ke[1] * E1 + ke[2] * E2) - D.bp[p * NP + a];
-      sKaE[a * 3 + 0] = ka0 + ke[0];
-      sKaE[a * 3 + 1] = ka1 + ke[1];
-      sKaE[a * 3 + 2] = ka2 + ke[2];
+      sV[a] = sRp[a] + sx + (ke[0] * E0 + ke[1] * E1 + ke[2] * E2) - D.bp[p * NP + a];
+      sKaE[a * 3 + 0] += ke[0];
+      sKaE[a * 3 + 1] += ke[1];
+      sKaE[a * 3 + 2] += ke[2];
       sa0 = ke[0] * sAev[a];
       sa1 = ke[1] * sAev[a];
       sa2 = ke[2] * sAev[a];
