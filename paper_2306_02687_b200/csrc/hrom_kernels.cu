@@ -125,33 +125,42 @@ __device__ __forceinline__ int tri_(int i) { return i * (i + 1) / 2; }
 
 // Left-looking Cholesky of the packed lower triangle sK (row i at i(i+1)/2)
 // in place; lane i owns row i (n <= 32). sInv[j] = 1 / L_jj. False if not SPD.
+// Look-ahead by one column: while column j's pivot goes through shuffle ->
+// rsqrt -> scale, each lane already forms the dot product of column j+1 over
+// the final entries k < j; only the k = j term waits for the new column.
 __device__ bool warp_cholesky(double* sK, double* sInv, int n, int lane) {
+  const bool act = lane < n;
+  const double* ri = sK + tri_(act ? lane : 0);
+  double s = act ? ri[0] : 0.0;  // K_ij - sum_{k<j} L_ik L_jk for column j = 0
   for (int j = 0; j < n; ++j) {
-    double s = 0.0;
-    if (lane >= j && lane < n) {
-      const double* ri = sK + tri_(lane);
-      const double* rj = sK + tri_(j);
+    double part = 0.0;  // sum_{k<j} L_ik L_{j+1,k}
+    if (act && lane > j && j + 1 < n) {
+      const double* rn = sK + tri_(j + 1);
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int k = 0;
       for (; k + 3 < j; k += 4) {
-        a0 += ri[k] * rj[k];
-        a1 += ri[k + 1] * rj[k + 1];
-        a2 += ri[k + 2] * rj[k + 2];
-        a3 += ri[k + 3] * rj[k + 3];
+        a0 += ri[k] * rn[k];
+        a1 += ri[k + 1] * rn[k + 1];
+        a2 += ri[k + 2] * rn[k + 2];
+        a3 += ri[k + 3] * rn[k + 3];
       }
-      for (; k < j; ++k) a0 += ri[k] * rj[k];
-      s = ri[j] - ((a0 + a1) + (a2 + a3));
+      if (k < j) a0 += ri[k] * rn[k];
+      if (k + 1 < j) a1 += ri[k + 1] * rn[k + 1];
+      if (k + 2 < j) a2 += ri[k + 2] * rn[k + 2];
+      part = (a0 + a1) + (a2 + a3);
     }
     const double d = __shfl_sync(0xffffffffu, s, j);
     if (!(d > 0.0)) return false;
     const double inv = rsqrt_fast(d);
-    const double ljj = d * inv;
+    const double lij = s * inv;
     if (lane == j) {
-      sK[tri_(j) + j] = ljj;
+      sK[tri_(j) + j] = d * inv;
       sInv[j] = inv;
-    } else if (lane > j && lane < n) {
-      sK[tri_(lane) + j] = s * inv;
+    } else if (act && lane > j) {
+      sK[tri_(lane) + j] = lij;
     }
+    const double lnj = __shfl_sync(0xffffffffu, lij, (j + 1) & 31);  // L_{j+1,j}
+    if (act && lane > j && j + 1 < n) s = ri[j + 1] - (part + lij * lnj);
     __syncwarp();
   }
   return true;
