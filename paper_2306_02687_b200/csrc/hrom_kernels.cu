@@ -81,7 +81,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // D(8x8) += A(8x4) B(4x8), fp64 tensor core. Fragments: a = A[lane/4][lane%4],
 // b = B[lane%4][lane/4], d = D[lane/4][2*(lane%4) + {0,1}].
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -253,6 +253,10 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
 #ifndef FE2_KWRES
 #define FE2_KWRES 8
 #endif
+#ifndef FE2_GROUP_UNROLL
+#define FE2_GROUP_UNROLL 1
+#endif
+constexpr int kGroupUnroll = FE2_GROUP_UNROLL;  // plastic-group loop unroll (tuning)
 constexpr int kW = FE2_KW;            // warps per CTA (streamed-G ring)
 constexpr int kWRes = FE2_KWRES;      // warps per CTA when the whole G2 is resident in shared memory
 constexpr int kMaxStages = FE2_STAGES;  // G-chunk ring depth (shared by the CTA), at most
@@ -638,7 +642,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       __syncwarp();
       // plastic contraction on DMMA: k = 3 slot + i, four k per k-step
       const int ng = np4 >> 2;
-#pragma unroll 1
+#pragma unroll kGroupUnroll
       for (int g = 0; g < ng; ++g) {
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
