@@ -260,7 +260,6 @@ constexpr int kGroupUnroll = FE2_GROUP_UNROLL;  // plastic-group loop unroll (tu
 constexpr int kW = FE2_KW;            // warps per CTA (streamed-G ring)
 constexpr int kWRes = FE2_KWRES;      // warps per CTA when the whole G2 is resident in shared memory
 constexpr int kMaxStages = FE2_STAGES;  // G-chunk ring depth (shared by the CTA), at most
-constexpr int kHS = 2;      // per-warp history ring depth (TMA, 5 x 256 B per stage)
 
 template <int NP, int W>
 struct IncLayout {
@@ -269,16 +268,14 @@ struct IncLayout {
   static constexpr int kSlots = kQC * 6 + kQC * 3 + kQC;     // w ΔC (6 unique), w Δσ, point index
   static constexpr int kTri = NP * (NP + 1) / 2;              // packed lower K_aa
   static constexpr int kUnion = (kSlots > kTri) ? kSlots : kTri;
-  static constexpr int kHist = kHS * 5 * kQC;                 // per-warp history ring (TMA)
-  static constexpr int WS = 6 * NP + 3 * NP + kUnion + kHist;  // per-warp scratch (doubles)
+  static constexpr int WS = 6 * NP + 3 * NP + kUnion;  // per-warp scratch (doubles)
   // ring depth: as deep as the 227 KB shared-memory budget allows (<= kMaxStages)
   static constexpr long kBudget = 227L * 1024 - 512 - static_cast<long>(W) * WS * 8;
   static constexpr int kFit = static_cast<int>(kBudget / (static_cast<long>(chunk) * 8));
   static constexpr int ST = kFit < 2 ? 2 : (kFit > kMaxStages ? kMaxStages : kFit);
   static constexpr size_t ring_bytes = static_cast<size_t>(ST) * chunk * sizeof(double);
-  // control block: full[ST] (u64) | hbar[W][kHS] (u64) | cnt[ST] (int) | ctrl (u64)
-  static constexpr int kHbarOff = ST * 8;
-  static constexpr int kCntOff = kHbarOff + W * kHS * 8;
+  // control block: full[ST] (u64) | cnt[ST] (int) | ctrl (u64)
+  static constexpr int kCntOff = ST * 8;
   static constexpr int kCtrlOff = ((kCntOff + ST * 4 + 7) / 8) * 8;
   static constexpr size_t bytes = ring_bytes + static_cast<size_t>(W) * WS * sizeof(double) + kCtrlOff + 8;
   // resident variant: the whole G2 (nch chunks) in shared memory, no ring
@@ -397,7 +394,6 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   double* wbase = reinterpret_cast<double*>(smem_raw + ring_bytes) + static_cast<size_t>(warp) * L::WS;
   unsigned char* ctrl_base = smem_raw + ring_bytes + static_cast<size_t>(W) * L::WS * sizeof(double);
   uint64_t* full = reinterpret_cast<uint64_t*>(ctrl_base);
-  uint64_t* hbar = reinterpret_cast<uint64_t*>(ctrl_base + L::kHbarOff) + warp * kHS;
   int* cnt = reinterpret_cast<int*>(ctrl_base + L::kCntOff);
   unsigned long long* ctrl = reinterpret_cast<unsigned long long*>(ctrl_base + L::kCtrlOff);
 
@@ -413,7 +409,6 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   double* sDS = sU + kQC * 6;                       // [32][3] w Δσ (commit pass: w S(Δεp))
   int* sQ = reinterpret_cast<int*>(sU + kQC * 9);   // [32]    chunk-local cubature index
   double* sK = sU;                                  // K_aa packed lower (after an assembly pass)
-  double* hb = sU + L::kUnion;                      // [kHS][5][32] history stages
 
   const ModelDev& M = A.M;
   const PointsDev& D = A.D;
@@ -429,9 +424,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     }
     *ctrl = (static_cast<unsigned long long>(W) << 32) | static_cast<unsigned long long>(L::ST);
   }
-  if (lane == 0)
-    for (int s = 0; s < kHS; ++s) mbar_init(&hbar[s], 1);
-  if (lane == 0) fence_mbar_init();
+  if (threadIdx.x == 0) fence_mbar_init();
   __syncthreads();
   if (RES) {  // the whole operator, once: nch bulk copies on one barrier
     if (threadIdx.x == 0) {
@@ -469,66 +462,26 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   bool k_linear = false;  // the last assembly had no plastic point (K_aa == K_e)
   const int n = M.n;
 
-  // ------------------------------------------------ per-warp history stream
-  // (point, chunk) items of εp(4), eq arrive by TMA bulk copies into kHS
-  // shared stages. Within a pass the next chunks are in flight while the
-  // current one computes; the first chunks of the predicted next pass (same
-  // point after an assembly, next point after the final commit) are issued
-  // at the end of a pass, so they load during the Newton / Cholesky phase.
-  int h_iss = 0, h_con = 0;  // positions issued / consumed
-  int64_t pf_p = -1;         // point of the prefetched next-pass items
-  int pf_n = 0;              // how many of its first chunks are in flight
-  const int h_first = nch < kHS ? nch : kHS;
-  auto h_issue = [&](int64_t p, int c) {
-    const int s = h_iss % kHS;
-    if (lane == 0) {
-      const double* base = D.hist + (D.st[p].pad[0] ? D.hist_alt : 0);  // the committed buffer of p
-      fence_proxy_async();  // the stage's previous generic reads precede the async writes
-      mbar_expect_tx(&hbar[s], 5 * kQC * sizeof(double));
-      tma_load_1d(hb + s * 5 * kQC, base + (p * nch + c) * (5 * kQC), 5 * kQC * sizeof(double), &hbar[s]);
-    }
-    ++h_iss;
-  };
-  auto h_take = [&]() -> const double* {
-    const int s = h_con % kHS;
-    mbar_wait(&hbar[s], static_cast<uint32_t>((h_con / kHS) & 1));
-    ++h_con;
-    return hb + s * 5 * kQC;
-  };
-  auto h_begin = [&](int64_t p, bool after_write) {
-    if (pf_p != p) {  // discard prefetches made for another point
-      while (h_con < h_iss) h_take();
-      __syncwarp();
-      pf_n = 0;
-    }
-    if (after_write && pf_n == 0) {  // this warp's history stores -> async-proxy reads
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      __syncwarp();
-    }
-    for (int c = pf_n; c < h_first; ++c) h_issue(p, c);
-    pf_p = -1;
-    pf_n = 0;
-  };
-  auto h_prefetch = [&](int64_t p) {  // first chunks of point p's next pass, discarding stale ones
-    while (h_con < h_iss) h_take();
-    __syncwarp();
-    for (int c = 0; c < h_first; ++c) h_issue(p, c);
-    pf_p = p;
-    pf_n = h_first;
-  };
-  auto h_next = [&](int64_t p, int c, int64_t pred) {  // after consuming chunk c of point p
-    const int nc = c + kHS;
-    if (nc < nch) {
-      h_issue(p, nc);
-    } else if (pred >= 0 && nc - nch < h_first && pf_n == nc - nch && (pf_p == pred || pf_n == 0)) {
-      h_issue(pred, nc - nch);
-      pf_p = pred;
-      ++pf_n;
-    }
+  // ------------------------------------------------ per-lane history loads
+  // Lane = cubature point: its (εp, eq) come from the point's committed buffer
+  // by coalesced 8-B loads (256 B per warp and component), one chunk ahead; at
+  // the end of a pass the first chunk of the predicted next pass (same point,
+  // or the next point after the final acceptance) is loaded so it arrives
+  // during the Newton phase. The lane that reads a history entry is the lane
+  // that wrote its candidate, so program order covers read-after-write.
+  double nh0 = 0.0, nh1 = 0.0, nh2 = 0.0, nh3 = 0.0, nh4 = 0.0;  // chunk 0 of point pf_p
+  int64_t pf_p = -1;
+  auto hload = [&](int64_t p, int c, double& a0, double& a1, double& a2, double& a3, double& a4) {
+    const double* b = D.hist + (D.st[p].pad[0] ? D.hist_alt : 0) + (p * nch + c) * (5 * kQC) + lane;
+    a0 = b[0];
+    a1 = b[kQC];
+    a2 = b[2 * kQC];
+    a3 = b[3 * kQC];
+    a4 = b[4 * kQC];
   };
 
   // ---------------------------------------------------------------- passes
-  auto assembly_pass = [&](int64_t p, double E0, double E1, double E2, int64_t pred, bool after_write) {
+  auto assembly_pass = [&](int64_t p, double E0, double E1, double E2, int64_t pred) {
     double acc[NTP][2];
     double kae[NT][3];
     double rr[NT];
@@ -544,18 +497,24 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     const bool cur = D.st[p].pad[0] != 0;  // committed buffer; the candidate goes to the other one
     double* hcand = D.hist + (cur ? 0 : D.hist_alt) + p * nch * (5 * kQC) + lane;
     uint8_t* fcand = D.flags ? D.flags + (cur ? 0 : D.flags_alt) + p * M.K2p : nullptr;
-    h_begin(p, after_write);
+    double x0, x1, x2, x3, x4;  // history of the next chunk
+    if (pf_p == p) {
+      x0 = nh0;
+      x1 = nh1;
+      x2 = nh2;
+      x3 = nh3;
+      x4 = nh4;
+    } else {
+      hload(p, 0, x0, x1, x2, x3, x4);
+    }
+    pf_p = -1;
     for (int c = 0; c < nch; ++c) {
-      double h0, h1, h2, h3, h4;
-      {
-        const double* Hs = h_take();
-        h0 = Hs[lane];
-        h1 = Hs[kQC + lane];
-        h2 = Hs[2 * kQC + lane];
-        h3 = Hs[3 * kQC + lane];
-        h4 = Hs[4 * kQC + lane];
-        __syncwarp();
-        h_next(p, c, pred);
+      const double h0 = x0, h1 = x1, h2 = x2, h3 = x3, h4 = x4;
+      if (c + 1 < nch) {
+        hload(p, c + 1, x0, x1, x2, x3, x4);
+      } else if (pred >= 0) {
+        hload(pred, 0, nh0, nh1, nh2, nh3, nh4);
+        pf_p = pred;
       }
       const double* Gb = ring_wait(R, seq);
       const int q = c * kQC + lane;
@@ -883,7 +842,6 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       p_next = grab();
       continue;
     }
-    bool after_write = false;  // the previous pass (a sub-step commit) wrote this point's history
     // warm start α = α_committed, E = E_prev + (E_k - E_prev) * 1 (rve.hpp:465-472)
     for (int a = lane; a < NP; a += 32) {
       const double ac = dbg ? ((a < n) ? A.dbg_alpha[a] : 0.0) : D.alpha_c[p * NP + a];
@@ -896,8 +854,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     double a = 1.0, rn_it = 0.0, best_rn = 0.0, best_a = 1.0, ref = 0.0, done = 0.0, frac = 1.0;
     int err = 0;
     while (true) {
-      assembly_pass(p, E0, E1, E2, dbg ? -1 : p, after_write);
-      after_write = false;
+      assembly_pass(p, E0, E1, E2, dbg ? -1 : p);
       if (dbg) {
         dump();
         break;
@@ -1049,14 +1006,15 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       if (action == 1) {
         if (lane == 0 && A.O.pcount) A.O.pcount[p] = pc;
         p_next = grab();
-        if (p_next < D.P) h_prefetch(p_next);
+        if (p_next < D.P) {
+          hload(p_next, 0, nh0, nh1, nh2, nh3, nh4);
+          pf_p = p_next;
+        }
         break;
       }
       // converged sub-step: the next one starts from the new committed state
-      // (prefetched chunks came from the old buffer; the new one was written
-      // by generic stores -> fence before the async-proxy reads)
+      // (the chunk prefetched during the pass came from the old buffer)
       pf_p = -1;
-      after_write = true;
       const double nt = fmin(1.0, done + frac);
       E0 = lerp_rn(Ep0, Et0, nt);
       E1 = lerp_rn(Ep1, Et1, nt);
@@ -1075,7 +1033,6 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     }
     if (p_next < 0) p_next = grab();
   }
-  while (h_con < h_iss) h_take();  // no TMA may be in flight at exit
   ring_drain(R, seq, lane);
   if (A.cnt && lane == 0) {
     atomicAdd(&A.cnt->assemblies, n_asm);
