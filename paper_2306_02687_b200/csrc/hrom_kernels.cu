@@ -471,8 +471,11 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   // that wrote its candidate, so program order covers read-after-write.
   double nh0 = 0.0, nh1 = 0.0, nh2 = 0.0, nh3 = 0.0, nh4 = 0.0;  // chunk 0 of point pf_p
   int64_t pf_p = -1;
-  auto hload = [&](int64_t p, int c, double& a0, double& a1, double& a2, double& a3, double& a4) {
-    const double* b = D.hist + (D.st[p].pad[0] ? D.hist_alt : 0) + (p * nch + c) * (5 * kQC) + lane;
+  auto hbase = [&](int64_t p) -> const double* {  // committed buffer of point p, this lane
+    return D.hist + (D.st[p].pad[0] ? D.hist_alt : 0) + p * nch * (5 * kQC) + lane;
+  };
+  auto hload = [&](const double* base, int c, double& a0, double& a1, double& a2, double& a3, double& a4) {
+    const double* b = base + c * (5 * kQC);
     a0 = b[0];
     a1 = b[kQC];
     a2 = b[2 * kQC];
@@ -498,6 +501,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     double* hcand = D.hist + (cur ? 0 : D.hist_alt) + p * nch * (5 * kQC) + lane;
     uint8_t* fcand = D.flags ? D.flags + (cur ? 0 : D.flags_alt) + p * M.K2p : nullptr;
     double x0, x1, x2, x3, x4;  // history of the next chunk
+    const double* hcur = D.hist + (cur ? D.hist_alt : 0) + p * nch * (5 * kQC) + lane;
     if (pf_p == p) {
       x0 = nh0;
       x1 = nh1;
@@ -505,18 +509,18 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       x3 = nh3;
       x4 = nh4;
     } else {
-      hload(p, 0, x0, x1, x2, x3, x4);
+      hload(hcur, 0, x0, x1, x2, x3, x4);
     }
     pf_p = -1;
     for (int c = 0; c < nch; ++c) {
       const double h0 = x0, h1 = x1, h2 = x2, h3 = x3, h4 = x4;
       if (c + 1 < nch) {
-        hload(p, c + 1, x0, x1, x2, x3, x4);
+        hload(hcur, c + 1, x0, x1, x2, x3, x4);
       } else if (pred >= 0) {
-        hload(pred, 0, nh0, nh1, nh2, nh3, nh4);
+        hload(pred == p ? hcur : hbase(pred), 0, nh0, nh1, nh2, nh3, nh4);
         pf_p = pred;
       }
-      const double* Gb = ring_wait(R, seq);
+      const double* Gb = RES ? R.buf + static_cast<size_t>(c) * L::chunk : ring_wait(R, seq);
       const int q = c * kQC + lane;
       // lane = cubature point: strain, elastic trial, yield test
       const double* Gq = Gb + lane * S;
@@ -1007,7 +1011,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
         if (lane == 0 && A.O.pcount) A.O.pcount[p] = pc;
         p_next = grab();
         if (p_next < D.P) {
-          hload(p_next, 0, nh0, nh1, nh2, nh3, nh4);
+          hload(hbase(p_next), 0, nh0, nh1, nh2, nh3, nh4);
           pf_p = p_next;
         }
         break;
