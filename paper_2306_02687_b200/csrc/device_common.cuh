@@ -85,7 +85,7 @@ __device__ __forceinline__ int tri(int i) { return i * (i + 1) / 2; }  // packed
 struct Trial {
   double t0, t1, t2, t3;  // trial stress (packed 4)
   double d0, d1, d2, d3;  // trial deviator
-  double ss, q_tr, f;
+  double ss, inv_ns, q_tr, f;  // |s_tr|^2, 1/|s_tr|, sqrt(3/2)|s_tr|, yield function
 };
 
 // trial_state (materials.hpp:162-169) and f = q_tr - (sy0 + h eq) (:208)
@@ -99,13 +99,15 @@ __device__ __forceinline__ Trial trial_state(const MatDev& m, double ep0, double
   T.t1 = lt + two_mu * x1;
   T.t2 = lt + two_mu * x2;
   T.t3 = two_mu * x3;
-  const double p = (T.t0 + T.t1 + T.t2) / 3.0;
+  const double p = (T.t0 + T.t1 + T.t2) * (1.0 / 3.0);
   T.d0 = T.t0 - p;
   T.d1 = T.t1 - p;
   T.d2 = T.t2 - p;
   T.d3 = T.t3;
   T.ss = T.d0 * T.d0 + T.d1 * T.d1 + T.d2 * T.d2 + 2.0 * T.d3 * T.d3;
-  T.q_tr = sqrt(1.5) * sqrt(T.ss);
+  // |s_tr| and its reciprocal from one MUFU rsqrt seed (no IEEE sqrt sequence)
+  T.inv_ns = T.ss > 0.0 ? rsqrt_fast(T.ss) : 0.0;
+  T.q_tr = 1.2247448713915890491 * (T.ss * T.inv_ns);  // sqrt(3/2) |s_tr|
   T.f = T.q_tr - (m.sy0 + m.h * eq);
   return T;
 }
@@ -120,12 +122,12 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
   Corr c;
   const double mu = m.mu;
   const double dlam = T.f * m.inv_denom;
-  const double inv_q = rcp_fast(T.q_tr);
+  const double inv_q = 0.81649658092772603273 * T.inv_ns;  // 1/q_tr = sqrt(2/3) / |s_tr|
   const double cs = 3.0 * mu * dlam * inv_q;
   c.ds0 = -cs * T.d0;
   c.ds1 = -cs * T.d1;
   c.ds2 = -cs * T.d3;
-  const double inv_n = 1.2247448713915890491 * inv_q;  // 1/|s_tr| = sqrt(3/2) / q_tr
+  const double inv_n = T.inv_ns;
   const double n0 = T.d0 * inv_n, n1 = T.d1 * inv_n, n3 = T.d3 * inv_n;
   const double mu2 = 6.0 * mu * mu;
   const double c1 = mu2 * dlam * inv_q;

@@ -441,6 +441,7 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
           for (int a = 0; a < n; ++a)
             G2[static_cast<size_t>(q2) * S + i * NP + a] = G[(static_cast<size_t>(q) * 3 + i) * n + a];
         w2[q2] = w[q];
+        G2[static_cast<size_t>(q2) * S + 3 * NP] = w[q];  // the weight also rides in the row's pad
       }
       // elastic predictor over ALL cubature points (J2 points with the J2
       // material's C_e): K_e = Σ w G^T C_e G, K_aE,e = Σ w G^T C_e, C_EE,e = Σ w C_e.

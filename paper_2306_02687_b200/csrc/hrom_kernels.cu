@@ -189,7 +189,7 @@ __device__ double warp_chol_solve(const double* sK, const double* sInv, int n, i
 struct Trial {
   double t0, t1, t2, t3;  // trial stress (packed 4)
   double d0, d1, d2, d3;  // trial deviator
-  double ss, q_tr, f;
+  double ss, inv_ns, q_tr, f;  // |s_tr|^2, 1/|s_tr|, sqrt(3/2)|s_tr|, yield function
 };
 
 __device__ __forceinline__ Trial trial_state(const MatDev& m, double ep0, double ep1, double ep2, double ep3,
@@ -202,13 +202,15 @@ __device__ __forceinline__ Trial trial_state(const MatDev& m, double ep0, double
   T.t1 = lt + two_mu * x1;
   T.t2 = lt + two_mu * x2;
   T.t3 = two_mu * x3;
-  const double p = (T.t0 + T.t1 + T.t2) / 3.0;
+  const double p = (T.t0 + T.t1 + T.t2) * (1.0 / 3.0);
   T.d0 = T.t0 - p;
   T.d1 = T.t1 - p;
   T.d2 = T.t2 - p;
   T.d3 = T.t3;
   T.ss = T.d0 * T.d0 + T.d1 * T.d1 + T.d2 * T.d2 + 2.0 * T.d3 * T.d3;
-  T.q_tr = sqrt(1.5) * sqrt(T.ss);
+  // |s_tr| and its reciprocal from one MUFU rsqrt seed (no IEEE sqrt sequence)
+  T.inv_ns = T.ss > 0.0 ? rsqrt_fast(T.ss) : 0.0;
+  T.q_tr = 1.2247448713915890491 * (T.ss * T.inv_ns);  // sqrt(3/2) |s_tr|
   T.f = T.q_tr - (m.sy0 + m.h * eq);
   return T;
 }
@@ -222,12 +224,12 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
   Corr c;
   const double mu = m.mu;
   const double dlam = T.f * m.inv_denom;  // f / (3 mu + h)
-  const double inv_q = rcp_fast(T.q_tr);
+  const double inv_q = 0.81649658092772603273 * T.inv_ns;  // 1/q_tr = sqrt(2/3) / |s_tr|
   const double cs = 3.0 * mu * dlam * inv_q;
   c.ds0 = -cs * T.d0;
   c.ds1 = -cs * T.d1;
   c.ds2 = -cs * T.d3;
-  const double inv_n = 1.2247448713915890491 * inv_q;  // 1/|s_tr| = sqrt(3/2) / q_tr
+  const double inv_n = T.inv_ns;
   const double n0 = T.d0 * inv_n, n1 = T.d1 * inv_n, n3 = T.d3 * inv_n;
   const double mu2 = 6.0 * mu * mu;
   const double c1 = mu2 * dlam * inv_q;
@@ -552,7 +554,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
         double n0 = h0, n1 = h1, n2 = h2, n3 = h3, n4 = h4;
         if (plastic) {
           const double dlam = T.f * mt.inv_denom;
-          const double ce = 1.5 * dlam * rcp_fast(T.q_tr);
+          const double ce = 1.5 * dlam * (0.81649658092772603273 * T.inv_ns);
           n0 = h0 + ce * T.d0;
           n1 = h1 + ce * T.d1;
           n2 = h2 + ce * T.d2;
@@ -569,7 +571,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       }
       if (plastic) {
         const Corr cr = radial_return(mt, T);
-        const double wq = M.w2[q];
+        const double wq = Gq[3 * NP];  // cubature weight rides in the row's pad
         const int slot = __popc(bal & ((1u << lane) - 1u));
         const double w00 = wq * cr.dc00, w01 = wq * cr.dc01, w02 = wq * cr.dc02;
         const double w11 = wq * cr.dc11, w12 = wq * cr.dc12, w22 = wq * cr.dc22;

@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
           double n0 = h0, n1 = h1, n2 = h2, n3 = h3, n4 = h4;
           if (plastic) {
             const double dlam = T.f * mt.inv_denom;
-            const double ce = 1.5 * dlam * rcp_fast(T.q_tr);
+            const double ce = 1.5 * dlam * (0.81649658092772603273 * T.inv_ns);
             n0 = h0 + ce * T.d0;
             n1 = h1 + ce * T.d1;
             n2 = h2 + ce * T.d2;
