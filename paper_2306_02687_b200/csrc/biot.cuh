@@ -35,7 +35,7 @@ __device__ __forceinline__ void update_biot(const MatDev& m, double ep0, double 
   const double x0 = (U00 - 1.0) - ep0, x1 = (U11 - 1.0) - ep1, x2 = 0.0 - ep2, x3 = 0.5 * (U01 + U10) - ep3;
   const double lt = lam * (x0 + x1 + x2);
   const double t0 = lt + two_mu * x0, t1 = lt + two_mu * x1, t2 = lt + two_mu * x2, t3 = two_mu * x3;
-  const double p = (t0 + t1 + t2) / 3.0;
+  const double p = (t0 + t1 + t2) * (1.0 / 3.0);
   const double d0 = t0 - p, d1 = t1 - p, d2 = t2 - p, d3 = t3;
   const double ss = d0 * d0 + d1 * d1 + d2 * d2 + 2.0 * d3 * d3;
   const double inv_ns = ss > 0.0 ? dev::rsqrt_fast(ss) : 0.0;
