@@ -151,6 +151,13 @@ int fe2_hrom_read_state(fe2_hrom_t h, double* alpha, double* state, uint8_t* fla
 int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, const double* E,
                             double* r, double* Kaa, double* KaE, double* C_EE, double* S_raw);
 
+/* Save / return to the committed state of every point (history, α, loads,
+ * previous path point, failure codes): a macro Newton iteration that does not
+ * converge is undone by fe2_hrom_restore (the micro commit of the reference's
+ * nested scheme happens only when the macro step is accepted). */
+int fe2_hrom_snapshot(fe2_hrom_t h);
+int fe2_hrom_restore(fe2_hrom_t h);
+
 typedef struct {
   int64_t points;
   int n, K, K_j2;
@@ -171,6 +178,35 @@ int fe2_hrom_reset_stats(fe2_hrom_t h);
 int fe2_hrom_set_timing(fe2_hrom_t h, int on);
 /* order all later work of the handle on `stream` (cudaStream_t; NULL = own) */
 int fe2_hrom_set_stream(fe2_hrom_t h, void* stream);
+
+/* ---- macro FE driver of the two-scale beam (the caller
+ * of the hot path; SPEC.md:455-518 fe2.macro_step / solve_program, nested
+ * variant): plane-strain L x H strip of Tri6 pairs (build_beam_mesh,
+ * mesh.hpp:133-169), left edge clamped, vertical tip displacement U on the
+ * x = L edge, reaction R. Each macro Newton iteration runs converged micro
+ * solves for all macro Gauss points (one engine increment from the committed
+ * state, fe2_hrom_restore) and assembles the tangent from C_macro; accepted
+ * steps commit (fe2_hrom_snapshot). Program: n_load steps to u_max, then
+ * unloading in the same steps until R changes sign (U_residual = linear zero
+ * crossing; NaN if none within max_unload steps). Host code; the engine must
+ * be a small-strain handle with fe2_macro_points() points allocated. */
+typedef struct {
+  double length, height;      /* beam L x H (desk default 4 x 1) */
+  int nx, ny;                 /* cells along x / y, two Tri6 each (desk: 8 x 2 = 32 elements) */
+  double u_max;               /* peak tip displacement */
+  int n_load;                 /* load steps to u_max */
+  int max_unload;             /* unload steps at most */
+  double tol;                 /* macro residual tolerance relative to max(|f_int|, largest accepted |f_int|) (1e-6) */
+  int max_iter;               /* macro Newton iterations per step (20) */
+  int max_bisections;         /* macro step bisections (4) */
+  fe2_newton_opts_t micro;    /* micro Newton options */
+} fe2_macro_config_t;
+int fe2_macro_points(const fe2_macro_config_t* cfg, int64_t* n_points);
+/* per macro Gauss point: B[36] (3 x 12 strain operator), w, element (nullable) */
+int fe2_macro_gauss(const fe2_macro_config_t* cfg, double* B, double* w, int* elem);
+/* rows[k] = (U, R, macro iterations of the step, cumulative micro iterations, wall ms) */
+int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows, int max_rows, int* n_rows,
+                  double* u_residual);
 
 /* ---- offline stage (host only, no GPU): seeded hyper-ROM model and paths
  * matching BASELINE.json configs. */

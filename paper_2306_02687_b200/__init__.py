@@ -22,6 +22,7 @@ from .hrom import (  # noqa: F401
     update_material_batch,
     update_material_soa_device,
 )
+from .fe2 import MacroConfig, macro_gauss, macro_points, solve_program  # noqa: F401
 
 __all__ = [
     "ElasticParams",
@@ -35,4 +36,8 @@ __all__ = [
     "make_paths",
     "update_material_batch",
     "update_material_soa_device",
+    "MacroConfig",
+    "macro_gauss",
+    "macro_points",
+    "solve_program",
 ]

@@ -144,7 +144,26 @@ struct fe2_hrom_s {
     D.flags_alt = (nbuf() == 2 && flags) ? static_cast<int64_t>(P) * K2p : 0;
     return D;
   }
+  // snapshot of the committed point state (fe2_hrom_snapshot / _restore)
+  unsigned char* snap = nullptr;
+  size_t snap_bytes = 0;
+  struct Part {
+    void* p;
+    size_t bytes;
+  };
+  std::vector<Part> state_parts() const {
+    std::vector<Part> v = {{hist, static_cast<size_t>(nbuf()) * P * K2p * 5 * sizeof(double)},
+                           {alpha_c, static_cast<size_t>(P) * NP * sizeof(double)},
+                           {bp, static_cast<size_t>(P) * NP * sizeof(double)},
+                           {E_c, static_cast<size_t>(P) * ncomp() * sizeof(double)},
+                           {sp, static_cast<size_t>(P) * 4 * sizeof(double)},
+                           {st, static_cast<size_t>(P) * sizeof(PointState)}};
+    if (flags) v.push_back({flags, static_cast<size_t>(nbuf()) * P * K2p});
+    return v;
+  }
   void free_points() {
+    dfree(snap);
+    snap_bytes = 0;
     dfree(hist);
     dfree(alpha_c);
     dfree(E_c);
@@ -719,6 +738,41 @@ int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, co
     std::memcpy(KaE, o.data() + n + n * n, 3 * n * sizeof(double));
     std::memcpy(C_EE, o.data() + n + n * n + 3 * n, 9 * sizeof(double));
     std::memcpy(S_raw, o.data() + n + n * n + 3 * n + 9, 3 * sizeof(double));
+  });
+}
+
+int fe2_hrom_snapshot(fe2_hrom_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated");
+    CK(cudaSetDevice(h->device));
+    const auto parts = h->state_parts();
+    size_t total = 0;
+    for (const auto& pt : parts) total += (pt.bytes + 255) / 256 * 256;
+    if (h->snap_bytes != total) {
+      dfree(h->snap);
+      h->snap = dalloc<unsigned char>(total);
+      h->snap_bytes = total;
+    }
+    size_t off = 0;
+    for (const auto& pt : parts) {
+      CK(cudaMemcpyAsync(h->snap + off, pt.p, pt.bytes, cudaMemcpyDeviceToDevice, h->stream));
+      off += (pt.bytes + 255) / 256 * 256;
+    }
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int fe2_hrom_restore(fe2_hrom_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated");
+    check(h->snap != nullptr, Code::config, "no snapshot (fe2_hrom_snapshot)");
+    CK(cudaSetDevice(h->device));
+    size_t off = 0;
+    for (const auto& pt : h->state_parts()) {
+      CK(cudaMemcpyAsync(pt.p, h->snap + off, pt.bytes, cudaMemcpyDeviceToDevice, h->stream));
+      off += (pt.bytes + 255) / 256 * 256;
+    }
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 

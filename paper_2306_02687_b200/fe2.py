@@ -1,0 +1,79 @@
+"""Macro FE driver of the two-scale beam over the native C ABI
+(fe2_macro_*; SPEC.md:455-518 fe2.macro_step / solve_program, nested
+variant). The macro loop is host C++ in the library;
+every macro Newton iteration is one engine increment for all macro Gauss
+points on the device."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .hrom import HyperRomEngine, NewtonOptions, _check, _Opts, lib
+
+
+class _MacroCfg(C.Structure):
+    _fields_ = [("length", C.c_double), ("height", C.c_double), ("nx", C.c_int), ("ny", C.c_int),
+                ("u_max", C.c_double), ("n_load", C.c_int), ("max_unload", C.c_int), ("tol", C.c_double),
+                ("max_iter", C.c_int), ("max_bisections", C.c_int), ("micro", _Opts)]
+
+
+lib.fe2_macro_points.argtypes = [C.POINTER(_MacroCfg), C.POINTER(C.c_int64)]
+lib.fe2_macro_gauss.argtypes = [C.POINTER(_MacroCfg), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                C.POINTER(C.c_int)]
+lib.fe2_macro_run.argtypes = [C.POINTER(_MacroCfg), C.c_void_p, C.POINTER(C.c_double), C.c_int,
+                              C.POINTER(C.c_int), C.POINTER(C.c_double)]
+lib.fe2_hrom_snapshot.argtypes = [C.c_void_p]
+lib.fe2_hrom_restore.argtypes = [C.c_void_p]
+
+
+@dataclass
+class MacroConfig:
+    """Desk beam (SPEC fe2 DESIGN DECISIONS): L/H = 4, 32 Tri6 elements."""
+    length: float = 4.0
+    height: float = 1.0
+    nx: int = 8
+    ny: int = 2
+    u_max: float = 0.3
+    n_load: int = 10
+    max_unload: int = 30
+    tol: float = 1e-6
+    max_iter: int = 20
+    max_bisections: int = 4
+    micro: NewtonOptions = field(default_factory=NewtonOptions)
+
+    def _c(self):
+        return _MacroCfg(self.length, self.height, self.nx, self.ny, self.u_max, self.n_load, self.max_unload,
+                         self.tol, self.max_iter, self.max_bisections, self.micro._c())
+
+
+def macro_points(cfg: MacroConfig) -> int:
+    n = C.c_int64()
+    _check(lib.fe2_macro_points(C.byref(cfg._c()), C.byref(n)))
+    return n.value
+
+
+def macro_gauss(cfg: MacroConfig):
+    """Per macro Gauss point: B (3 x 12), weight, element."""
+    P = macro_points(cfg)
+    B, w, e = np.empty((P, 3, 12)), np.empty(P), np.empty(P, dtype=np.int32)
+    _check(lib.fe2_macro_gauss(C.byref(cfg._c()), B.ctypes.data_as(C.POINTER(C.c_double)),
+                               w.ctypes.data_as(C.POINTER(C.c_double)), e.ctypes.data_as(C.POINTER(C.c_int))))
+    return B, w, e
+
+
+def solve_program(cfg: MacroConfig, engine: HyperRomEngine, max_rows: int = 256):
+    """Load / unload program on the beam (solve_program). Returns the curve
+    rows (U, R, macro iterations, cumulative micro iterations, wall ms) and
+    the residual displacement U_res of the unloaded beam."""
+    P = macro_points(cfg)
+    if engine.P != P:
+        engine.alloc_points(P)
+    rows = np.empty((max_rows, 5))
+    n, ures = C.c_int(), C.c_double()
+    _check(lib.fe2_macro_run(C.byref(cfg._c()), engine._h, rows.ctypes.data_as(C.POINTER(C.c_double)), max_rows,
+                             C.byref(n), C.byref(ures)))
+    r = rows[:n.value]
+    return dict(U=r[:, 0].copy(), R=r[:, 1].copy(), macro_iters=r[:, 2].astype(int),
+                micro_iters=r[:, 3].astype(np.int64), wall_ms=r[:, 4].copy(), U_residual=ures.value)

@@ -1,0 +1,39 @@
+"""The device macro driver (fe2_macro_run: host C++ macro Newton + one engine
+increment per macro iteration, snapshot/restore for the nested micro
+commit) against the oracle driver (numpy macro Newton + replayed oracle
+hyper-ROM) on the desk beam: identical step sequence and macro iteration
+counts, reactions within 1e-8 relative, same residual displacement. The
+micro solves see macro strains that differ from the oracle's by rounding
+(1e-13 relative, accumulated through the macro Newton), so a micro point
+sitting on a convergence-test knife edge may take one more or fewer Newton
+iteration: cumulative micro counts agree to 1e-3 (the hot-path tests pin
+exact counts on identical inputs)."""
+import numpy as np
+import pytest
+
+import macro_oracle as MO
+import paper_2306_02687_b200 as F
+import pyoracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("u_max,n_load", [(0.02, 5), (0.3, 10)])
+def test_device_macro_driver_matches_oracle(u_max, n_load):
+    m = F.HyperRomModel(33, 12, 200, 0)
+    eng = F.HyperRomEngine.from_model(m)
+    cfg = F.MacroConfig(u_max=u_max, n_load=n_load)
+    g = F.solve_program(cfg, eng)
+    beam = MO.build_beam(cfg.length, cfg.height, cfg.nx, cfg.ny)
+    orc = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume)
+    rows, ures = MO.solve_program(beam, MO.ReplayEngine(orc, len(beam["w"]), threads=16), u_max=u_max,
+                                  n_load=n_load, max_unload=cfg.max_unload, tol=cfg.tol, max_iter=cfg.max_iter)
+    assert len(g["U"]) == len(rows)
+    np.testing.assert_allclose(g["U"], rows[:, 0], rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(g["macro_iters"], rows[:, 2].astype(int))
+    np.testing.assert_allclose(g["micro_iters"], rows[:, 3], rtol=1e-3, atol=0)
+    scale = np.abs(rows[:, 1]).max()
+    assert np.abs(g["R"] - rows[:, 1]).max() <= 1e-8 * scale
+    if u_max > 0.1:
+        assert g["U_residual"] > 0.0
+    assert abs(g["U_residual"] - ures) <= 1e-8 * u_max
