@@ -285,61 +285,91 @@ __device__ __forceinline__ void store_dispatch(int warp, double* sK, const doubl
   }
 }
 
-// CTA Cholesky of the packed lower sK (thread i = row i, n <= 256).
+// The factorization and substitutions run on the first NW = ceil(NP/32)
+// warps only (thread i = row i), synchronised by a named barrier over those
+// warps; the other warps wait once at the closing CTA barrier.
+template <int NW>
+__device__ __forceinline__ void rows_sync() {
+  if constexpr (NW >= kBW)
+    __syncthreads();
+  else
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+}
+
+// Left-looking Cholesky of the packed lower sK. False (CTA-uniform) if not SPD.
+template <int NW>
 __device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
   const int tid = threadIdx.x;
-  for (int j = 0; j < n; ++j) {
-    double s = 0.0;
-    if (tid >= j && tid < n) {
-      const double* ri = sK + tri(tid);
-      const double* rj = sK + tri(j);
-      double a0 = 0.0, a1 = 0.0;
-      int k = 0;
-      for (; k + 1 < j; k += 2) {
-        a0 += ri[k] * rj[k];
-        a1 += ri[k + 1] * rj[k + 1];
+  if (tid < NW * 32) {
+    bool ok = true;
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      if (tid >= j && tid < n) {
+        const double* ri = sK + tri(tid);
+        const double* rj = sK + tri(j);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int k = 0;
+        for (; k + 3 < j; k += 4) {
+          a0 += ri[k] * rj[k];
+          a1 += ri[k + 1] * rj[k + 1];
+          a2 += ri[k + 2] * rj[k + 2];
+          a3 += ri[k + 3] * rj[k + 3];
+        }
+        for (; k < j; ++k) a0 += ri[k] * rj[k];
+        s = ri[j] - ((a0 + a1) + (a2 + a3));
+        if (tid == j) red[0] = s;
       }
-      if (k < j) a0 += ri[k] * rj[k];
-      s = ri[j] - (a0 + a1);
-      if (tid == j) red[0] = s;
+      rows_sync<NW>();
+      const double d = red[0];
+      if (!(d > 0.0)) {  // uniform over the row warps
+        ok = false;
+        break;
+      }
+      const double inv = rsqrt_fast(d);
+      if (tid == j) {
+        sK[tri(j) + j] = d * inv;
+        sInv[j] = inv;
+      } else if (tid > j && tid < n) {
+        sK[tri(tid) + j] = s * inv;
+      }
+      rows_sync<NW>();
     }
-    __syncthreads();
-    const double d = red[0];
-    if (!(d > 0.0)) return false;  // uniform
-    const double inv = rsqrt_fast(d);
-    if (tid == j) {
-      sK[tri(j) + j] = d * inv;
-      sInv[j] = inv;
-    } else if (tid > j && tid < n) {
-      sK[tri(tid) + j] = s * inv;
-    }
-    __syncthreads();
+    if (tid == 0) red[1] = ok ? 1.0 : 0.0;
   }
-  return true;
+  __syncthreads();
+  return red[1] != 0.0;
 }
 
 // Forward substitution L y = b in place on sB[n] (cols RHS interleaved: sB[i*cols + c]).
+template <int NW>
 __device__ void cta_forward(const double* sK, const double* sInv, double* sB, int n, int cols) {
   const int tid = threadIdx.x;
-  for (int j = 0; j < n; ++j) {
-    if (tid < cols) sB[j * cols + tid] *= sInv[j];
-    __syncthreads();
-    if (tid > j && tid < n) {
-      const double l = sK[tri(tid) + j];
-      for (int c = 0; c < cols; ++c) sB[tid * cols + c] -= l * sB[j * cols + c];
+  if (tid < NW * 32) {
+    for (int j = 0; j < n; ++j) {
+      if (tid < cols) sB[j * cols + tid] *= sInv[j];
+      rows_sync<NW>();
+      if (tid > j && tid < n) {
+        const double l = sK[tri(tid) + j];
+        for (int c = 0; c < cols; ++c) sB[tid * cols + c] -= l * sB[j * cols + c];
+      }
+      rows_sync<NW>();
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 // Backward substitution L^T x = y in place (single RHS).
+template <int NW>
 __device__ void cta_backward(const double* sK, const double* sInv, double* sB, int n) {
   const int tid = threadIdx.x;
-  for (int j = n - 1; j >= 0; --j) {
-    if (tid == 0) sB[j] *= sInv[j];
-    __syncthreads();
-    if (tid < j) sB[tid] -= sK[tri(j) + tid] * sB[j];
-    __syncthreads();
+  if (tid < NW * 32) {
+    for (int j = n - 1; j >= 0; --j) {
+      if (tid == 0) sB[j] *= sInv[j];
+      rows_sync<NW>();
+      if (tid < j) sB[tid] -= sK[tri(j) + tid] * sB[j];
+      rows_sync<NW>();
+    }
   }
+  __syncthreads();
 }
 
 template <int NT>
@@ -634,7 +664,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
       __syncthreads();
       return true;
     }
-    return cta_cholesky(sK, sInv, red, n);
+    return cta_cholesky<(NP + 31) / 32>(sK, sInv, red, n);
   };
 
   // accept the last pass's state: flip to its candidate history, α_c, and move
@@ -753,7 +783,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
                   break;
                 }
                 // condensation X = L^-1 K_aE, C = (C_EE - X^T X)/V (homogenize, rve.hpp:372-390)
-                cta_forward(sK, sInv, sKaE, n, 3);
+                cta_forward<(NP + 31) / 32>(sK, sInv, sKaE, n, 3);
                 double x0 = 0, x1 = 0, x2 = 0;
                 if (tid < n) {
                   x0 = sKaE[tid * 3 + 0];
@@ -820,8 +850,8 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
             }
             if (tid < n) sDA[tid] = -sV[tid];
             __syncthreads();
-            cta_forward(sK, sInv, sDA, n, 1);
-            cta_backward(sK, sInv, sDA, n);
+            cta_forward<(NP + 31) / 32>(sK, sInv, sDA, n, 1);
+            cta_backward<(NP + 31) / 32>(sK, sInv, sDA, n);
             for (int b = tid; b < NP; b += kBT) sAev[b] = (b < n) ? axpy_rn(sAl[b], 1.0, sDA[b]) : 0.0;
             rn_it = rn;
             a = 1.0;
