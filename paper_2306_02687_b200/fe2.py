@@ -24,8 +24,6 @@ lib.fe2_macro_gauss.argtypes = [C.POINTER(_MacroCfg), C.POINTER(C.c_double), C.P
                                 C.POINTER(C.c_int)]
 lib.fe2_macro_run.argtypes = [C.POINTER(_MacroCfg), C.c_void_p, C.POINTER(C.c_double), C.c_int,
                               C.POINTER(C.c_int), C.POINTER(C.c_double)]
-lib.fe2_hrom_snapshot.argtypes = [C.c_void_p]
-lib.fe2_hrom_restore.argtypes = [C.c_void_p]
 
 
 @dataclass

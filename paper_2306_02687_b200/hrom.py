@@ -91,6 +91,8 @@ def _load():
     L.fe2_hrom_reset_stats.argtypes = [C.c_void_p]
     L.fe2_hrom_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     L.fe2_hrom_reset_points.argtypes = [C.c_void_p]
+    L.fe2_hrom_snapshot.argtypes = [C.c_void_p]
+    L.fe2_hrom_restore.argtypes = [C.c_void_p]
     L.fe2_hrom_output_ptrs.argtypes = [C.c_void_p] + [C.POINTER(C.c_void_p)] * 6
     L.fe2_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.fe2_model_free.argtypes = [C.c_void_p]
@@ -266,6 +268,14 @@ class HyperRomEngine:
 
     def reset_points(self):
         _check(lib.fe2_hrom_reset_points(self._h))
+
+    def snapshot(self):
+        """Save the committed state of every point (deferred-commit callers)."""
+        _check(lib.fe2_hrom_snapshot(self._h))
+
+    def restore(self):
+        """Return every point to the last snapshot."""
+        _check(lib.fe2_hrom_restore(self._h))
 
     def output_ptrs(self):
         """Device pointers (ints) of the handle's own output buffers:

@@ -270,3 +270,27 @@ def test_material_soa_device_matches_oracle(N):
     np.testing.assert_array_equal(sig.T, s2)
     np.testing.assert_array_equal(hout.T, so2)
     np.testing.assert_array_equal(pl.astype(bool), pl2)
+
+
+def test_snapshot_restore_replays_bitwise():
+    """fe2_hrom_snapshot / _restore (the macro driver's deferred commit):
+    after a restore the same increment gives bit-identical outputs and
+    state, for the warp-per-point and the CTA-per-point kernels."""
+    for n, K in ((12, 200), (40, 300)):
+        m = F.HyperRomModel(33, n, K, 0)
+        E = F.make_paths(1, 0, 64, 50)
+        eng = F.HyperRomEngine.from_model(m)
+        eng.alloc_points(64, keep_flags=True)
+        for k in range(20):
+            eng.solve_increment(E[:, k])
+        eng.snapshot()
+        a = eng.solve_increment(E[:, 20])
+        sa = eng.read_state(flags=True)
+        eng.solve_increment(E[:, 21])  # move on, then undo both
+        eng.restore()
+        b = eng.solve_increment(E[:, 20])
+        sb = eng.read_state(flags=True)
+        for key in a:
+            np.testing.assert_array_equal(a[key], b[key])
+        for x, y in zip(sa, sb):
+            np.testing.assert_array_equal(x, y)
