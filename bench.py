@@ -36,6 +36,9 @@ CONFIGS = {
     0: dict(name="config0_small_strain_j2", P=1024, n=12, K=200, incr=20, path=0, subdivisions=33),
     # configs[2]: finite-strain Biot J2 (parity unpinned: no reference code)
     2: dict(name="config2_finite_strain_biot_j2", P=262144, n=32, K=600, incr=30, path=2, subdivisions=33),
+    # configs[3]: the multi-GPU case — P is the TOTAL point count, split over the ranks
+    # (strong scaling); n = 64 runs the CTA-per-point kernel. ~2 min per step on one GPU.
+    3: dict(name="config3_multi_gpu", P=1048576, n=64, K=2000, incr=20, path=0, subdivisions=33, strong=True),
 }
 METRIC = "macro Gauss-point hyper-ROM evaluations/sec (fp64)"
 UNIT = "evals/s"
@@ -192,16 +195,28 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def rank_points(cfg, ws, rank):
+    """(points on this rank, first global point id): weak scaling gives every rank
+    cfg["P"] points; a strong-scaling config splits cfg["P"] in contiguous blocks."""
+    if cfg.get("strong"):
+        per = (cfg["P"] + ws - 1) // ws
+        lo = min(cfg["P"], rank * per)
+        return min(per, cfg["P"] - lo), lo
+    return cfg["P"], rank * cfg["P"]
+
+
 class DeviceRun:
     """One config on this rank: model, engine, device-resident path and outputs."""
 
-    def __init__(self, F, torch, cfg, rank, local, dev, stream):
+    def __init__(self, F, torch, cfg, rank, local, dev, stream, ws=1):
         self.cfg, self.dev, self.stream, self.torch = cfg, dev, stream, torch
         self.finite = cfg["path"] == 2
         self.nc, self.nt = (4, 16) if self.finite else (3, 9)
-        P, incr = cfg["P"], cfg["incr"]
+        P, p0 = rank_points(cfg, ws, rank)
+        incr = cfg["incr"]
+        self.P = P
         self.model = F.HyperRomModel(cfg["subdivisions"], cfg["n"], cfg["K"], seed=0)
-        E_host = F.make_paths(cfg["path"], 0, P, incr, p0=rank * P)  # (P, incr, nc), global-id streams
+        E_host = F.make_paths(cfg["path"], 0, P, incr, p0=p0)  # (P, incr, nc), global-id streams
         self.E_inc = np.ascontiguousarray(E_host.transpose(1, 0, 2))  # (incr, P, nc)
         self.eng = F.HyperRomEngine.from_model(self.model, device=local, finite_strain=self.finite)
         self.eng.alloc_points(P)
@@ -316,8 +331,8 @@ def main():
     except Exception:
         peak, peak_src = 37.0, "fallback: DMMA peak estimate"
 
-    run = DeviceRun(F, torch, cfg, rank, local, dev, stream)
-    eng, model, P, incr = run.eng, run.model, cfg["P"], cfg["incr"]
+    run = DeviceRun(F, torch, cfg, rank, local, dev, stream, ws)
+    eng, model, P, incr = run.eng, run.model, run.P, cfg["incr"]
     nc, nt = run.nc, run.nt
     for _ in range(args.warmup):
         run.device_step(dist, ws)
@@ -331,7 +346,8 @@ def main():
     stats = eng.stats()
     eng.set_timing(False)
     launches = stats["kernel_launches"] - launches0
-    evals = ws * P * incr * args.steps
+    P_total = cfg["P"] if cfg.get("strong") else ws * P
+    evals = P_total * incr * args.steps
     value = evals / (ms / 1e3)
 
     # ---- e2e through the host-buffer C-ABI (pinned host memory)
@@ -356,7 +372,7 @@ def main():
     e2e_step()
     e2e_steps = max(1, min(args.steps, 3))
     ms_e2e = timed(e2e_step, e2e_steps)
-    e2e_value = ws * P * incr * e2e_steps / (ms_e2e / 1e3)
+    e2e_value = P_total * incr * e2e_steps / (ms_e2e / 1e3)
     h2d = incr * P * nc * 8
     d2h = incr * P * (nc * 8 + nt * 8 + 8 + 3 * 4)
 
@@ -412,7 +428,7 @@ def main():
         if c == args.config or c not in CONFIGS:
             continue
         xcfg = dict(CONFIGS[c])
-        xrun = DeviceRun(F, torch, xcfg, rank, local, dev, stream)
+        xrun = DeviceRun(F, torch, xcfg, rank, local, dev, stream, ws)
         xrun.device_step(dist, ws)
         xrun.check_converged()
         xrun.eng.reset_stats()
@@ -476,7 +492,8 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded Φ, cubature and paths, BASELINE configs)",
         "config": {"workload": cfg["name"], "points_per_rank": P, "modes": cfg["n"], "cubature": cfg["K"],
                    "cubature_j2": model.K_j2, "increments": incr, "parallelism": f"dp{ws} (points sharded)",
@@ -490,8 +507,8 @@ def main():
         "roofline_constitutive": constitutive,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
-        "newton": {"assemblies_per_eval": stats["timed_assemblies"] / (evals / ws),
-                   "commits_per_eval": stats["timed_commits"] / (evals / ws),
+        "newton": {"assemblies_per_eval": stats["timed_assemblies"] / (P * incr * args.steps),
+                   "commits_per_eval": stats["timed_commits"] / (P * incr * args.steps),
                    "plastic_fraction": stats["timed_plastic_evals"] / max(1, stats["timed_assemblies"] * K_j2)},
         "extra_configs": extras,
     }
