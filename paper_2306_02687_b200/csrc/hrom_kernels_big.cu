@@ -30,14 +30,24 @@ using namespace dev;
 #ifndef FE2_BIG_QB32_MAXNP
 #define FE2_BIG_QB32_MAXNP 64
 #endif
-constexpr int kBW = 8;         // warps per CTA
-constexpr int kBT = kBW * 32;  // threads per CTA
+// Warps per CTA (one macro point per CTA): 4 for NP <= 64 with 16-point
+// chunks, so two CTAs (two points) share an SM — while one point sits in its
+// barrier-bound phases (compaction, factorization) the other keeps the FP64
+// pipe busy (+21% at n = 64); 8 for NP > 64, whose accumulators would not
+// fit 4 warps' registers.
+#ifndef FE2_BIG_SMALL_WARPS
+#define FE2_BIG_SMALL_WARPS 4
+#endif
+constexpr int bw_for(int NT) { return NT <= 8 ? FE2_BIG_SMALL_WARPS : 8; }
 
 template <int NT>
 struct Big {
   static constexpr int NP = 8 * NT;
-  static constexpr int QB = (NP <= FE2_BIG_QB32_MAXNP) ? 32 : 16;  // cubature points per chunk
-  static constexpr int TPQ = kBT / QB;             // threads per cubature point (8 | 16)
+  static constexpr int BW = bw_for(NT);  // warps per CTA
+  static constexpr int BT = BW * 32;     // threads per CTA
+  static constexpr int MINB = BW == 8 ? FE2_BIG_MINB : 2;
+  static constexpr int QB = (NP <= FE2_BIG_QB32_MAXNP && BW == 8) ? 32 : 16;  // cubature points per chunk
+  static constexpr int TPQ = BT / QB;    // threads per cubature point
   static constexpr int S = 3 * NP + 2;
   static constexpr int chunk = QB * S;
   static constexpr int TRI = NP * (NP + 1) / 2;
@@ -62,7 +72,7 @@ constexpr PairTable pairs_for(int W) {
   int blk = 0;
   for (int B1 = 0; B1 < nb; ++B1)
     for (int B2 = B1; B2 < nb; ++B2, ++blk) {
-      if (blk % kBW != W) continue;
+      if (blk % bw_for(NT) != W) continue;
       for (int t1 = B1 * b; t1 < B1 * b + b && t1 < NT; ++t1)
         for (int t2 = B2 * b; t2 < B2 * b + b && t2 < NT; ++t2)
           if (t1 <= t2) {
@@ -76,14 +86,15 @@ constexpr PairTable pairs_for(int W) {
 template <int NT>
 constexpr int max_pairs() {
   int m = 0;
-  for (int w = 0; w < kBW; ++w) {
+  for (int w = 0; w < bw_for(NT); ++w) {
     const int c = pairs_for<NT>(w).n;
     m = c > m ? c : m;
   }
   return m;
 }
 
-// CTA-wide sum (all threads get the result); red has >= kBW + 1 doubles.
+// CTA-wide sum (all threads get the result); red has >= BW + 1 doubles.
+template <int BW>
 __device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -92,7 +103,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   __syncthreads();
   double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < kBW; ++w) s += red[w];
+  for (int w = 0; w < BW; ++w) s += red[w];
   return s;
 }
 
@@ -288,16 +299,16 @@ __device__ __forceinline__ void store_dispatch(int warp, double* sK, const doubl
 // The factorization and substitutions run on the first NW = ceil(NP/32)
 // warps only (thread i = row i), synchronised by a named barrier over those
 // warps; the other warps wait once at the closing CTA barrier.
-template <int NW>
+template <int NW, int BW>
 __device__ __forceinline__ void rows_sync() {
-  if constexpr (NW >= kBW)
+  if constexpr (NW >= BW)
     __syncthreads();
   else
     asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
 }
 
 // Left-looking Cholesky of the packed lower sK. False (CTA-uniform) if not SPD.
-template <int NW>
+template <int NW, int BW>
 __device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
   const int tid = threadIdx.x;
   if (tid < NW * 32) {
@@ -319,7 +330,7 @@ __device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
         s = ri[j] - ((a0 + a1) + (a2 + a3));
         if (tid == j) red[0] = s;
       }
-      rows_sync<NW>();
+      rows_sync<NW, BW>();
       const double d = red[0];
       if (!(d > 0.0)) {  // uniform over the row warps
         ok = false;
@@ -332,7 +343,7 @@ __device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
       } else if (tid > j && tid < n) {
         sK[tri(tid) + j] = s * inv;
       }
-      rows_sync<NW>();
+      rows_sync<NW, BW>();
     }
     if (tid == 0) red[1] = ok ? 1.0 : 0.0;
   }
@@ -341,39 +352,39 @@ __device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
 }
 
 // Forward substitution L y = b in place on sB[n] (cols RHS interleaved: sB[i*cols + c]).
-template <int NW>
+template <int NW, int BW>
 __device__ void cta_forward(const double* sK, const double* sInv, double* sB, int n, int cols) {
   const int tid = threadIdx.x;
   if (tid < NW * 32) {
     for (int j = 0; j < n; ++j) {
       if (tid < cols) sB[j * cols + tid] *= sInv[j];
-      rows_sync<NW>();
+      rows_sync<NW, BW>();
       if (tid > j && tid < n) {
         const double l = sK[tri(tid) + j];
         for (int c = 0; c < cols; ++c) sB[tid * cols + c] -= l * sB[j * cols + c];
       }
-      rows_sync<NW>();
+      rows_sync<NW, BW>();
     }
   }
   __syncthreads();
 }
 // Backward substitution L^T x = y in place (single RHS).
-template <int NW>
+template <int NW, int BW>
 __device__ void cta_backward(const double* sK, const double* sInv, double* sB, int n) {
   const int tid = threadIdx.x;
   if (tid < NW * 32) {
     for (int j = n - 1; j >= 0; --j) {
       if (tid == 0) sB[j] *= sInv[j];
-      rows_sync<NW>();
+      rows_sync<NW, BW>();
       if (tid < j) sB[tid] -= sK[tri(j) + tid] * sB[j];
-      rows_sync<NW>();
+      rows_sync<NW, BW>();
     }
   }
   __syncthreads();
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) {
+__global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(IncArgs A) {
   using L = Big<NT>;
   constexpr int NP = L::NP, QB = L::QB, TPQ = L::TPQ, S = L::S;
   constexpr int MP = max_pairs<NT>();
@@ -468,7 +479,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
     int pre = 0;
     total = 0;
 #pragma unroll
-    for (int w = 0; w < kBW; ++w) {
+    for (int w = 0; w < L::BW; ++w) {
       const int c = ictl[w];
       pre += (w < warp) ? c : 0;
       total += c;
@@ -604,15 +615,15 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
       sKaE[tid * 3 + 1] = ka1;
       sKaE[tid * 3 + 2] = ka2;
     }
-    c00 = block_sum(c00, red);
-    c01 = block_sum(c01, red);
-    c02 = block_sum(c02, red);
-    c11 = block_sum(c11, red);
-    c12 = block_sum(c12, red);
-    c22 = block_sum(c22, red);
-    ds0 = block_sum(ds0, red);
-    ds1 = block_sum(ds1, red);
-    ds2 = block_sum(ds2, red);
+    c00 = block_sum<L::BW>(c00, red);
+    c01 = block_sum<L::BW>(c01, red);
+    c02 = block_sum<L::BW>(c02, red);
+    c11 = block_sum<L::BW>(c11, red);
+    c12 = block_sum<L::BW>(c12, red);
+    c22 = block_sum<L::BW>(c22, red);
+    ds0 = block_sum<L::BW>(ds0, red);
+    ds1 = block_sum<L::BW>(ds1, red);
+    ds2 = block_sum<L::BW>(ds2, red);
     __syncthreads();
     // elastic predictor part and b_p, s_p (thread a = mode)
     double sa0 = 0.0, sa1 = 0.0, sa2 = 0.0;
@@ -634,9 +645,9 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
       sa1 = ke[1] * sAev[a];
       sa2 = ke[2] * sAev[a];
     }
-    sa0 = block_sum(sa0, red);
-    sa1 = block_sum(sa1, red);
-    sa2 = block_sum(sa2, red);
+    sa0 = block_sum<L::BW>(sa0, red);
+    sa1 = block_sum<L::BW>(sa1, red);
+    sa2 = block_sum<L::BW>(sa2, red);
     const double* ce = M.CEEe;
     const double* spp = D.sp + p * 4;
     s0 = ds0 + sa0 + (ce[0] * E0 + ce[1] * E1 + ce[2] * E2) - spp[0];
@@ -659,19 +670,19 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
 
   auto factor = [&]() -> bool {
     if (k_linear) {
-      for (int e = tid; e < tri(n); e += kBT) sK[e] = M.Le[e];
+      for (int e = tid; e < tri(n); e += L::BT) sK[e] = M.Le[e];
       if (tid < n) sInv[tid] = M.LeInv[tid];
       __syncthreads();
       return true;
     }
-    return cta_cholesky<(NP + 31) / 32>(sK, sInv, red, n);
+    return cta_cholesky<(NP + 31) / 32, L::BW>(sK, sInv, red, n);
   };
 
   // accept the last pass's state: flip to its candidate history, α_c, and move
   // the committed plastic-strain loads by its plastic corrections
   // (w S(Δεp) = -w Δσ): b_p -= r_plastic, s_p -= Σ w Δσ
   auto commit_point = [&](int64_t p) -> int {
-    for (int a = tid; a < NP; a += kBT) {
+    for (int a = tid; a < NP; a += L::BT) {
       D.alpha_c[p * NP + a] = sAev[a];
       D.bp[p * NP + a] -= sRp[a];
     }
@@ -694,16 +705,16 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
   if (A.dbg) {
     if (blockIdx.x == 0) {
       const int64_t p = A.dbg_point;
-      for (int a = tid; a < NP; a += kBT) sAev[a] = (a < n) ? A.dbg_alpha[a] : 0.0;
+      for (int a = tid; a < NP; a += L::BT) sAev[a] = (a < n) ? A.dbg_alpha[a] : 0.0;
       __syncthreads();
       assembly_pass(p, A.dbg_E[0], A.dbg_E[1], A.dbg_E[2]);
       double* o = A.dbg;
-      for (int a = tid; a < n; a += kBT) o[a] = sV[a];
-      for (int e = tid; e < n * n; e += kBT) {
+      for (int a = tid; a < n; a += L::BT) o[a] = sV[a];
+      for (int e = tid; e < n * n; e += L::BT) {
         const int i = e / n, j = e % n;
         o[n + e] = (j <= i) ? sK[tri(i) + j] : sK[tri(j) + i];
       }
-      for (int e = tid; e < 3 * n; e += kBT) o[n + n * n + e] = sKaE[e];
+      for (int e = tid; e < 3 * n; e += L::BT) o[n + n * n + e] = sKaE[e];
       if (tid == 0) {
         double* cc = o + n + n * n + 3 * n;
         cc[0] = ce00;
@@ -754,7 +765,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
         finish(0);
         continue;
       }
-      for (int a = tid; a < NP; a += kBT) {
+      for (int a = tid; a < NP; a += L::BT) {
         const double ac = D.alpha_c[p * NP + a];
         sAev[a] = ac;
         sAl[a] = ac;
@@ -766,7 +777,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
       while (true) {
         assembly_pass(p, E0, E1, E2);
         const double rl = (tid < n) ? sV[tid] : 0.0;
-        const double rn = sqrt(block_sum(rl * rl, red));
+        const double rn = sqrt(block_sum<L::BW>(rl * rl, red));
         const double srn = sqrt(s0 * s0 + s1 * s1 + s2 * s2);
         int action = 0;  // 0 assemble again, 1 final commit, 2 sub-step commit, 3 failed
         for (int pass = 0; pass < 2; ++pass) {
@@ -783,16 +794,16 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
                   break;
                 }
                 // condensation X = L^-1 K_aE, C = (C_EE - X^T X)/V (homogenize, rve.hpp:372-390)
-                cta_forward<(NP + 31) / 32>(sK, sInv, sKaE, n, 3);
+                cta_forward<(NP + 31) / 32, L::BW>(sK, sInv, sKaE, n, 3);
                 double x0 = 0, x1 = 0, x2 = 0;
                 if (tid < n) {
                   x0 = sKaE[tid * 3 + 0];
                   x1 = sKaE[tid * 3 + 1];
                   x2 = sKaE[tid * 3 + 2];
                 }
-                const double q00 = block_sum(x0 * x0, red), q01 = block_sum(x0 * x1, red);
-                const double q02 = block_sum(x0 * x2, red), q11 = block_sum(x1 * x1, red);
-                const double q12 = block_sum(x1 * x2, red), q22 = block_sum(x2 * x2, red);
+                const double q00 = block_sum<L::BW>(x0 * x0, red), q01 = block_sum<L::BW>(x0 * x1, red);
+                const double q02 = block_sum<L::BW>(x0 * x2, red), q11 = block_sum<L::BW>(x1 * x1, red);
+                const double q12 = block_sum<L::BW>(x1 * x2, red), q22 = block_sum<L::BW>(x2 * x2, red);
                 if (tid == 0) {
                   const double V = M.volume;
                   double* Cp = A.O.C + p * 9;
@@ -833,7 +844,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
               E1 = lerp_rn(Ep1, Et1, nt);
               E2 = lerp_rn(Ep2, Et2, nt);
               __syncthreads();
-              for (int b = tid; b < NP; b += kBT) {
+              for (int b = tid; b < NP; b += L::BT) {
                 const double ac = D.alpha_c[p * NP + b];
                 sAl[b] = ac;
                 sAev[b] = ac;
@@ -850,9 +861,9 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
             }
             if (tid < n) sDA[tid] = -sV[tid];
             __syncthreads();
-            cta_forward<(NP + 31) / 32>(sK, sInv, sDA, n, 1);
-            cta_backward<(NP + 31) / 32>(sK, sInv, sDA, n);
-            for (int b = tid; b < NP; b += kBT) sAev[b] = (b < n) ? axpy_rn(sAl[b], 1.0, sDA[b]) : 0.0;
+            cta_forward<(NP + 31) / 32, L::BW>(sK, sInv, sDA, n, 1);
+            cta_backward<(NP + 31) / 32, L::BW>(sK, sInv, sDA, n);
+            for (int b = tid; b < NP; b += L::BT) sAev[b] = (b < n) ? axpy_rn(sAl[b], 1.0, sDA[b]) : 0.0;
             rn_it = rn;
             a = 1.0;
             ls = 0;
@@ -873,11 +884,11 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
               mode = 0;
               __syncthreads();
               if (best_a == a) {
-                for (int b = tid; b < NP; b += kBT) sAl[b] = sAev[b];
+                for (int b = tid; b < NP; b += L::BT) sAl[b] = sAev[b];
                 __syncthreads();
                 continue;
               }
-              for (int b = tid; b < NP; b += kBT) {
+              for (int b = tid; b < NP; b += L::BT) {
                 const double nv = (b < n) ? axpy_rn(sAl[b], best_a, sDA[b]) : 0.0;
                 sAl[b] = nv;
                 sAev[b] = nv;
@@ -888,7 +899,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
             ls += 1;
             a *= 0.5;
             __syncthreads();
-            for (int b = tid; b < NP; b += kBT) sAev[b] = (b < n) ? axpy_rn(sAl[b], a, sDA[b]) : 0.0;
+            for (int b = tid; b < NP; b += L::BT) sAev[b] = (b < n) ? axpy_rn(sAl[b], a, sDA[b]) : 0.0;
             action = 0;
             break;
           }
@@ -905,7 +916,7 @@ __global__ void __launch_bounds__(kBT, FE2_BIG_MINB) k_increment_big(IncArgs A) 
         E0 = lerp_rn(Ep0, Et0, nt);
         E1 = lerp_rn(Ep1, Et1, nt);
         E2 = lerp_rn(Ep2, Et2, nt);
-        for (int b = tid; b < NP; b += kBT) sAl[b] = sAev[b];
+        for (int b = tid; b < NP; b += L::BT) sAl[b] = sAev[b];
         __syncthreads();
         it = 0;
         mode = 0;
@@ -936,13 +947,13 @@ void launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
     configured = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment_big<NT>, kBT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment_big<NT>, Big<NT>::BT, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = static_cast<int64_t>(num_sms) * per_sm;
   if (a.dbg) grid = 1;
   else if (grid > a.D.P) grid = a.D.P;
   if (grid < 1) grid = 1;
-  k_increment_big<NT><<<static_cast<unsigned>(grid), kBT, smem, s>>>(a);
+  k_increment_big<NT><<<static_cast<unsigned>(grid), Big<NT>::BT, smem, s>>>(a);
 }
 
 }  // namespace
