@@ -208,11 +208,23 @@ int fe2_macro_gauss(const fe2_macro_config_t* cfg, double* B, double* w, int* el
 int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows, int max_rows, int* n_rows,
                   double* u_residual);
 
+/* ---- Empirical Cubature Method (SPEC.md:333-369
+ * hyper.ecm_select), host only: U[m][k] = orthonormal integrand modes at the m
+ * integration points (e.g. left singular vectors of the force snapshots),
+ * w_full[m] = the full-rule weights. A constant column is appended (volume
+ * exactness). Greedy max-correlation selection with least-squares re-fit and
+ * removal of non-positive weights; stops at rel_residual <= tol or m_target
+ * points (at most k + 1). ids/weights need min(m_target, k + 1) entries;
+ * returned ids ascending, weights > 0. */
+int fe2_ecm_select(const double* U, const double* w_full, int m, int k, int m_target, double tol, int* ids,
+                   double* weights, int* m_out, double* rel_residual);
+
 /* ---- offline stage (host only, no GPU): seeded hyper-ROM model and paths
  * matching BASELINE.json configs. */
 typedef struct fe2_model_s* fe2_model_t;
 /* default_cell(subdivisions) RVE (mesh.hpp:185-191, :218-352), linear BC,
- * n random orthonormal modes, K random cubature points. */
+ * n random orthonormal modes, K random cubature points (K = 0: the full rule,
+ * every integration point with its own quadrature weight — ECM training). */
 int fe2_model_build(int subdivisions, int n, int K, uint64_t seed, fe2_model_t* out);
 void fe2_model_free(fe2_model_t m);
 int fe2_model_sizes(fe2_model_t m, int* n, int* K, int* n_free, double* volume);

@@ -287,6 +287,8 @@ Model build_model(int sub, int n, int K, std::uint64_t seed) {
   for (int d = 0; d < 2 * n_nodes; ++d)
     if (!cell.on_boundary[d / 2]) dof_free[d] = nf++;
   if (n < 1 || n > nf) throw Failure(Code::config, "mode count out of range");
+  const bool full_rule = K == 0;  // all integration points with their own weights (training / ECM)
+  if (full_rule) K = n_ip;
   if (K < 1 || K > n_ip) throw Failure(Code::config, "cubature size out of range");
 
   std::vector<double> phi((size_t)nf * n);
@@ -301,7 +303,15 @@ Model build_model(int sub, int n, int K, std::uint64_t seed) {
   md.K = K;
   md.n_free = nf;
   md.volume = cell.area;
-  {
+  if (full_rule) {
+    for (int i = 0; i < n_ip; ++i) {
+      const auto& t = cell.tri[i / 3];
+      double Bq[3][12];
+      const double det = strain_operator(cell, t, kGauss[i % 3][0], kGauss[i % 3][1], Bq);
+      md.ip.push_back(i);
+      md.w.push_back(kGaussW * det);
+    }
+  } else {
     SeededStream s(seed ^ kRuleStream);
     std::vector<int> perm(n_ip);
     for (int i = 0; i < n_ip; ++i) perm[i] = i;
