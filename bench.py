@@ -365,10 +365,14 @@ def main():
 
     def e2e_step():
         eng.reset_points()
+        if ws == 1:  # asynchronous host-buffer API: output copies overlap the next increment
+            for k in range(incr):
+                eng.solve_increment_async_into(E_pin[k], o_sig, o_C, o_it, o_pc, o_res, o_st)
+            eng.wait()
+            return
         for k in range(incr):
             eng.solve_increment_into(E_pin[k], o_sig, o_C, o_it, o_pc, o_res, o_st)
-            if ws > 1:
-                run.gather(dist, ws, e_sig, e_C, e_res, e_st)
+            run.gather(dist, ws, e_sig, e_C, e_res, e_st)
 
     e2e_step()
     e2e_steps = max(1, min(args.steps, 3))
@@ -501,7 +505,9 @@ def main():
                    "l2": "inputs larger than L2 (history %.2f GB per rank > 126 MB L2)" % (P * model.K_j2 * 48 / 1e9),
                    "step": "one full trajectory of all points (reset to virgin state)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "steps": e2e_steps, "api": "fe2_hrom_solve_increment (host buffers, pinned)"},
+                "steps": e2e_steps,
+                "api": "fe2_hrom_solve_increment_async + fe2_hrom_wait (host buffers, pinned)" if ws == 1 else
+                       "fe2_hrom_solve_increment (host buffers, pinned) + NCCL all-gather"},
         "gpu_launches": launches,
         "roofline": roofline,
         "roofline_hbm": roofline_hbm,

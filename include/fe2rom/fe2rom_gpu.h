@@ -134,6 +134,19 @@ int fe2_hrom_solve_increment(fe2_hrom_t h, const double* E, const fe2_newton_opt
                              double* sigma, double* C, int* iters, int* plastic_count,
                              double* res_norm, int* status);
 
+/* Asynchronous form of fe2_hrom_solve_increment (same arguments, host
+ * buffers — pin them, cudaHostAlloc, for the copies to overlap): returns once
+ * the increment is queued. Inputs are staged and outputs produced in two
+ * alternating device buffers, and each increment's outputs are copied to the
+ * host on a second stream while the next increment computes. E must stay
+ * unchanged and the outputs are only valid until / after fe2_hrom_wait
+ * (the copies run asynchronously). Increments are applied in call order. */
+int fe2_hrom_solve_increment_async(fe2_hrom_t h, const double* E, const fe2_newton_opts_t* opts,
+                                   double* sigma, double* C, int* iters, int* plastic_count,
+                                   double* res_norm, int* status);
+/* Wait for every queued asynchronous increment and output copy. */
+int fe2_hrom_wait(fe2_hrom_t h);
+
 /* Same, on DEVICE buffers already resident in HBM (E, outputs), ordered on
  * `stream` (cudaStream_t, NULL = the handle's stream). The call returns
  * after the increment is complete on `stream`. */

@@ -95,6 +95,18 @@ struct fe2_hrom_s {
   int* work = nullptr;              // work-queue counter
   IncCounters* cnt = nullptr;       // device counters of a launch
   IncCounters* h_cnt = nullptr;     // pinned copy
+  // asynchronous host-buffer increments (fe2_hrom_solve_increment_async):
+  // double-buffered device inputs/outputs, output copies on a second stream
+  struct AsyncBuf {
+    double *dE = nullptr, *sig = nullptr, *C = nullptr, *res = nullptr;
+    int *it = nullptr, *pc = nullptr, *st = nullptr;
+    cudaEvent_t done = nullptr, copied = nullptr;
+    bool used = false;
+  } abuf[2];
+  int acur = 0;
+  int64_t async_pending = 0;  // launches since the last fe2_hrom_wait
+  cudaStream_t copy_stream = nullptr;
+  IncCounters* cnt_async = nullptr;  // device accumulator of async launches
   // staging for the host-buffer API and default outputs
   double *dE = nullptr, *o_sigma = nullptr, *o_C = nullptr, *o_res = nullptr;
   int *o_iters = nullptr, *o_status = nullptr, *o_pc = nullptr;
@@ -161,7 +173,24 @@ struct fe2_hrom_s {
     if (flags) v.push_back({flags, static_cast<size_t>(nbuf()) * P * K2p});
     return v;
   }
+  void free_async() {
+    if (copy_stream) cudaStreamSynchronize(copy_stream);
+    for (auto& b : abuf) {
+      dfree(b.dE);
+      dfree(b.sig);
+      dfree(b.C);
+      dfree(b.res);
+      dfree(b.it);
+      dfree(b.pc);
+      dfree(b.st);
+      if (b.done) cudaEventDestroy(b.done);
+      if (b.copied) cudaEventDestroy(b.copied);
+      b = AsyncBuf{};
+    }
+    acur = 0;
+  }
   void free_points() {
+    free_async();
     dfree(snap);
     snap_bytes = 0;
     dfree(hist);
@@ -192,7 +221,10 @@ struct fe2_hrom_s {
   }
   ~fe2_hrom_s() {
     cudaSetDevice(device);
+    if (copy_stream) cudaStreamSynchronize(copy_stream);
     free_points();
+    dfree(cnt_async);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     dfree(G2);
     dfree(w2);
     dfree(Ke);
@@ -622,6 +654,83 @@ int fe2_hrom_solve_increment(fe2_hrom_t h, const double* E, const fe2_newton_opt
     if (res_norm) CK(cudaMemcpyAsync(res_norm, h->o_res, P * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (status) CK(cudaMemcpyAsync(status, h->o_status, P * sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+  });
+}
+
+int fe2_hrom_solve_increment_async(fe2_hrom_t h, const double* E, const fe2_newton_opts_t* opts, double* sigma,
+                                   double* C, int* iters, int* plastic_count, double* res_norm, int* status) {
+  return guard([&] {
+    check(h != nullptr && E != nullptr, Code::config, "bad arguments");
+    check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+    CK(cudaSetDevice(h->device));
+    const NewtonCfg cfg = make_cfg(opts);
+    const int64_t P = h->P;
+    const int nc = h->ncomp(), nt = h->ntan();
+    cudaStream_t s = h->stream;
+    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    if (!h->cnt_async) {
+      h->cnt_async = dalloc<IncCounters>(1);
+      CK(cudaMemset(h->cnt_async, 0, sizeof(IncCounters)));
+    }
+    auto& b = h->abuf[h->acur];
+    if (!b.dE) {
+      b.dE = dalloc<double>(P * nc);
+      b.sig = dalloc<double>(P * nc);
+      b.C = dalloc<double>(P * nt);
+      b.res = dalloc<double>(P);
+      b.it = dalloc<int>(P);
+      b.pc = dalloc<int>(P);
+      b.st = dalloc<int>(P);
+      CK(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&b.copied, cudaEventDisableTiming));
+    }
+    if (b.used) CK(cudaStreamWaitEvent(s, b.copied, 0));  // its previous outputs have left the device
+    CK(cudaMemcpyAsync(b.dE, E, P * nc * sizeof(double), cudaMemcpyHostToDevice, s));
+    IncArgs a{};
+    a.M = h->model();
+    a.D = h->points();
+    a.O = Outputs{b.sig, b.C, b.res, b.it, b.st, b.pc};
+    a.cfg = cfg;
+    a.dE = b.dE;
+    a.work = h->work;
+    a.cnt = h->cnt_async;  // accumulates until fe2_hrom_wait
+    CK(cudaMemsetAsync(h->work, 0, sizeof(int), s));
+    launch_any(h, a, h->num_sms, s);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(b.done, s));
+    // the outputs of this increment go to the host on the copy stream while the next one computes
+    cudaStream_t c = h->copy_stream;
+    CK(cudaStreamWaitEvent(c, b.done, 0));
+    if (sigma) CK(cudaMemcpyAsync(sigma, b.sig, P * nc * sizeof(double), cudaMemcpyDeviceToHost, c));
+    if (C) CK(cudaMemcpyAsync(C, b.C, P * nt * sizeof(double), cudaMemcpyDeviceToHost, c));
+    if (iters) CK(cudaMemcpyAsync(iters, b.it, P * sizeof(int), cudaMemcpyDeviceToHost, c));
+    if (plastic_count) CK(cudaMemcpyAsync(plastic_count, b.pc, P * sizeof(int), cudaMemcpyDeviceToHost, c));
+    if (res_norm) CK(cudaMemcpyAsync(res_norm, b.res, P * sizeof(double), cudaMemcpyDeviceToHost, c));
+    if (status) CK(cudaMemcpyAsync(status, b.st, P * sizeof(int), cudaMemcpyDeviceToHost, c));
+    CK(cudaEventRecord(b.copied, c));
+    b.used = true;
+    h->acur ^= 1;
+    h->async_pending += 1;
+    h->stats.kernel_launches += 1;
+    h->stats.increments += 1;
+  });
+}
+
+int fe2_hrom_wait(fe2_hrom_t h) {
+  return guard([&] {
+    check(h != nullptr, Code::config, "bad arguments");
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->copy_stream) CK(cudaStreamSynchronize(h->copy_stream));
+    if (h->async_pending > 0 && h->cnt_async) {
+      IncCounters c{};
+      CK(cudaMemcpy(&c, h->cnt_async, sizeof(IncCounters), cudaMemcpyDeviceToHost));
+      CK(cudaMemset(h->cnt_async, 0, sizeof(IncCounters)));
+      h->stats.assemblies += static_cast<int64_t>(c.assemblies);
+      h->stats.commits += static_cast<int64_t>(c.commits);
+      h->stats.plastic_evals += static_cast<int64_t>(c.plastic_evals);
+      h->async_pending = 0;
+    }
   });
 }
 

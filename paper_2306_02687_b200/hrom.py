@@ -82,6 +82,8 @@ def _load():
     L.fe2_hrom_destroy.restype = None
     L.fe2_hrom_alloc_points.argtypes = [C.c_void_p, C.c_int64, C.c_int]
     L.fe2_hrom_solve_increment.argtypes = [C.c_void_p, _dp, C.POINTER(_Opts), _dp, _dp, _ip, _ip, _dp, _ip]
+    L.fe2_hrom_solve_increment_async.argtypes = [C.c_void_p, _dp, C.POINTER(_Opts), _dp, _dp, _ip, _ip, _dp, _ip]
+    L.fe2_hrom_wait.argtypes = [C.c_void_p]
     L.fe2_hrom_solve_increment_device.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Opts), C.c_void_p, C.c_void_p,
                                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     L.fe2_hrom_read_state.argtypes = [C.c_void_p, _dp, _dp, _u8p]
@@ -290,6 +292,17 @@ class HyperRomEngine:
         o = (opts or NewtonOptions())._c()
         _check(lib.fe2_hrom_solve_increment(self._h, _d(E), C.byref(o), _d(sigma), _d(Cm), _i(iters), _i(pc),
                                             _d(res), _i(status)))
+
+    def solve_increment_async_into(self, E, sigma, Cm, iters, pc, res, status, opts: NewtonOptions | None = None):
+        """Queue one increment (host buffers, pinned for overlap); the outputs
+        are written asynchronously — valid after wait()."""
+        o = (opts or NewtonOptions())._c()
+        _check(lib.fe2_hrom_solve_increment_async(self._h, _d(E), C.byref(o), _d(sigma), _d(Cm), _i(iters), _i(pc),
+                                                  _d(res), _i(status)))
+
+    def wait(self):
+        """Wait for all queued asynchronous increments and their output copies."""
+        _check(lib.fe2_hrom_wait(self._h))
 
     def solve_increment(self, E, opts: NewtonOptions | None = None):
         """E (P,3) host → dict of sigma (P,3), C (P,3,3), iters, plastic_count, res_norm, status.

@@ -294,3 +294,29 @@ def test_snapshot_restore_replays_bitwise():
             np.testing.assert_array_equal(a[key], b[key])
         for x, y in zip(sa, sb):
             np.testing.assert_array_equal(x, y)
+
+
+def test_async_host_api_matches_sync():
+    """fe2_hrom_solve_increment_async + fe2_hrom_wait gives the same outputs
+    and state as the synchronous call (double-buffered outputs, copy stream)."""
+    m = F.HyperRomModel(33, 24, 400, 0)
+    E = F.make_paths(1, 0, 256, 12)
+    a_eng = F.HyperRomEngine.from_model(m)
+    a_eng.alloc_points(256)
+    b_eng = F.HyperRomEngine.from_model(m)
+    b_eng.alloc_points(256)
+    outs = []
+    for k in range(12):
+        bufs = (np.empty((256, 3)), np.empty((256, 9)), np.empty(256, np.int32), np.empty(256, np.int32),
+                np.empty(256), np.empty(256, np.int32))
+        a_eng.solve_increment_async_into(np.ascontiguousarray(E[:, k]), *bufs)
+        outs.append(bufs)
+    a_eng.wait()
+    for k in range(12):
+        ref = b_eng.solve_increment(E[:, k])
+        np.testing.assert_array_equal(outs[k][0], ref["sigma"])
+        np.testing.assert_array_equal(outs[k][1].reshape(256, 3, 3), ref["C"])
+        np.testing.assert_array_equal(outs[k][2], ref["iters"])
+        np.testing.assert_array_equal(outs[k][5], ref["status"])
+    np.testing.assert_array_equal(a_eng.read_state()[1], b_eng.read_state()[1])
+    assert a_eng.stats()["assemblies"] == b_eng.stats()["assemblies"]
