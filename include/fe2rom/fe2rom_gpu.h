@@ -239,6 +239,13 @@ typedef struct fe2_model_s* fe2_model_t;
  * n random orthonormal modes, K random cubature points (K = 0: the full rule,
  * every integration point with its own quadrature weight — ECM training). */
 int fe2_model_build(int subdivisions, int n, int K, uint64_t seed, fe2_model_t* out);
+/* The same on an RVE read from a plain-text mesh in the reference's format
+ * (write_mesh / read_mesh, mesh.hpp:413-489: "fe2rom-mesh 1", nodes, Tri6
+ * elements with material ids 0 = matrix / 1 = inclusion, node sets); the
+ * linear BC acts on the nodes of the mesh's bounding box. */
+int fe2_model_build_from_mesh(const char* path, int n, int K, uint64_t seed, fe2_model_t* out);
+/* Write the default_cell(subdivisions) RVE in that format (bit-exact %.17g). */
+int fe2_mesh_write(int subdivisions, const char* path);
 void fe2_model_free(fe2_model_t m);
 int fe2_model_sizes(fe2_model_t m, int* n, int* K, int* n_free, double* volume);
 int fe2_model_arrays(fe2_model_t m, double* G, double* w, int* ip_id, int* mat_id);

@@ -20,6 +20,7 @@ from .hrom import (  # noqa: F401
     lib,
     make_paths,
     update_material_batch,
+    write_mesh,
     update_material_soa_device,
 )
 from .fe2 import MacroConfig, macro_gauss, macro_points, solve_program  # noqa: F401
@@ -34,6 +35,7 @@ __all__ = [
     "device_count",
     "lib",
     "make_paths",
+    "write_mesh",
     "update_material_batch",
     "update_material_soa_device",
     "MacroConfig",

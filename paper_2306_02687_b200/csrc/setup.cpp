@@ -21,7 +21,10 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <map>
 #include <numbers>
 #include <random>
 #include <string>
@@ -278,8 +281,96 @@ struct Model {
   std::vector<int> ip, mat;
 };
 
-Model build_model(int sub, int n, int K, std::uint64_t seed) {
-  const Cell cell = mesh_default_cell(sub);
+// Plain-text mesh in the reference's format (write_mesh / read_mesh,
+// mesh.hpp:413-489): "fe2rom-mesh 1", nodes "id x y" (%.17g, bit-exact
+// round trip), elements "e material n0..n5", node sets. The linear-BC
+// boundary of a read mesh is the nodes on its bounding box.
+void finish_cell(Cell& cell) {
+  double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+  for (size_t k = 0; k < cell.x.size(); ++k) {
+    x0 = std::min(x0, cell.x[k]);
+    x1 = std::max(x1, cell.x[k]);
+    y0 = std::min(y0, cell.y[k]);
+    y1 = std::max(y1, cell.y[k]);
+  }
+  const double tol = 1e-12 * std::max(1.0, std::max(x1 - x0, y1 - y0));
+  cell.on_boundary.assign(cell.x.size(), 0);
+  for (size_t k = 0; k < cell.x.size(); ++k)
+    cell.on_boundary[k] = std::abs(cell.x[k] - x0) < tol || std::abs(cell.x[k] - x1) < tol ||
+                          std::abs(cell.y[k] - y0) < tol || std::abs(cell.y[k] - y1) < tol;
+  double area = 0.0, Bop[3][12];
+  for (const auto& t : cell.tri) {  // per-element sums first, as mesh_default_cell (compute_area)
+    double ae = 0.0;
+    for (int q = 0; q < 3; ++q) ae += kGaussW * strain_operator(cell, t, kGauss[q][0], kGauss[q][1], Bop);
+    area += ae;
+  }
+  cell.area = area;
+}
+
+void mesh_write(const Cell& cell, std::FILE* f) {
+  std::fprintf(f, "fe2rom-mesh 1\nnodes %zu\n", cell.x.size());
+  for (size_t k = 0; k < cell.x.size(); ++k) std::fprintf(f, "%zu %.17g %.17g\n", k, cell.x[k], cell.y[k]);
+  std::fprintf(f, "elements %zu\n", cell.tri.size());
+  for (size_t e = 0; e < cell.tri.size(); ++e) {
+    std::fprintf(f, "%zu %d", e, cell.phase[e]);
+    for (int a = 0; a < 6; ++a) std::fprintf(f, " %d", cell.tri[e][a]);
+    std::fprintf(f, "\n");
+  }
+  // node sets of the unit cell (build_rve_mesh, mesh.hpp:344-347), in std::map order
+  std::map<std::string, std::vector<int>> sets;
+  for (size_t k = 0; k < cell.x.size(); ++k) {
+    if (std::abs(cell.x[k]) < 1e-12) sets["left"].push_back(static_cast<int>(k));
+    if (std::abs(cell.x[k] - 1.0) < 1e-12) sets["right"].push_back(static_cast<int>(k));
+    if (std::abs(cell.y[k]) < 1e-12) sets["bottom"].push_back(static_cast<int>(k));
+    if (std::abs(cell.y[k] - 1.0) < 1e-12) sets["top"].push_back(static_cast<int>(k));
+  }
+  for (const auto& [name, ids] : sets) {
+    std::fprintf(f, "set %s %zu\n", name.c_str(), ids.size());
+    for (size_t i = 0; i < ids.size(); ++i) std::fprintf(f, "%d%c", ids[i], i + 1 < ids.size() ? ' ' : '\n');
+  }
+}
+
+Cell mesh_read(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  check(is.good(), Code::io, "cannot open mesh file: " + path);
+  std::string magic, key;
+  int version = 0, count = 0;
+  is >> magic >> version;
+  check(magic == "fe2rom-mesh" && version == 1, Code::io, "not a fe2rom mesh file");
+  is >> key >> count;
+  check(key == "nodes" && count >= 0, Code::io, "malformed mesh file (nodes)");
+  Cell cell;
+  cell.x.resize(count);
+  cell.y.resize(count);
+  for (int i = 0; i < count; ++i) {
+    int id = -1;
+    is >> id >> cell.x[i] >> cell.y[i];
+    check(is.good() && id == i, Code::io, "node ids must be dense");
+  }
+  is >> key >> count;
+  check(key == "elements" && count >= 0, Code::io, "malformed mesh file (elements)");
+  cell.tri.resize(count);
+  cell.phase.resize(count);
+  for (int e = 0; e < count; ++e) {
+    int id = -1;
+    is >> id >> cell.phase[e];
+    for (int a = 0; a < 6; ++a) {
+      is >> cell.tri[e][a];
+      check(cell.tri[e][a] >= 0 && cell.tri[e][a] < static_cast<int>(cell.x.size()), Code::io,
+            "element references missing node");
+    }
+    check(is.good(), Code::io, "malformed mesh file (element)");
+  }
+  check(!cell.tri.empty(), Code::mesh, "mesh has no elements");
+  finish_cell(cell);  // node sets are not needed: the linear BC acts on the bounding box
+  return cell;
+}
+
+Model build_model_on(const Cell& cell, int n, int K, std::uint64_t seed);
+
+Model build_model(int sub, int n, int K, std::uint64_t seed) { return build_model_on(mesh_default_cell(sub), n, K, seed); }
+
+Model build_model_on(const Cell& cell, int n, int K, std::uint64_t seed) {
   const int n_nodes = (int)cell.x.size();
   const int n_ip = 3 * (int)cell.tri.size();
   std::vector<int> dof_free(2 * n_nodes, -1);
@@ -414,6 +505,21 @@ extern "C" {
 
 int fe2_model_build(int subdivisions, int n, int K, uint64_t seed, fe2_model_t* out) {
   return fe2::guard([&] { *out = new fe2_model_s{fe2::build_model(subdivisions, n, K, seed)}; });
+}
+int fe2_model_build_from_mesh(const char* path, int n, int K, uint64_t seed, fe2_model_t* out) {
+  return fe2::guard([&] {
+    fe2::check(path && out, fe2::Code::config, "bad arguments");
+    *out = new fe2_model_s{fe2::build_model_on(fe2::mesh_read(path), n, K, seed)};
+  });
+}
+int fe2_mesh_write(int subdivisions, const char* path) {
+  return fe2::guard([&] {
+    fe2::check(path != nullptr, fe2::Code::config, "bad arguments");
+    std::FILE* f = std::fopen(path, "wb");
+    fe2::check(f != nullptr, fe2::Code::io, std::string("cannot open for write: ") + path);
+    fe2::mesh_write(fe2::mesh_default_cell(subdivisions), f);
+    std::fclose(f);
+  });
 }
 void fe2_model_free(fe2_model_t m) { delete m; }
 int fe2_model_sizes(fe2_model_t m, int* n, int* K, int* n_free, double* volume) {

@@ -97,6 +97,8 @@ def _load():
     L.fe2_hrom_restore.argtypes = [C.c_void_p]
     L.fe2_hrom_output_ptrs.argtypes = [C.c_void_p] + [C.POINTER(C.c_void_p)] * 6
     L.fe2_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
+    L.fe2_model_build_from_mesh.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
+    L.fe2_mesh_write.argtypes = [C.c_int, C.c_char_p]
     L.fe2_model_free.argtypes = [C.c_void_p]
     L.fe2_model_free.restype = None
     L.fe2_model_sizes.argtypes = [C.c_void_p, _ip, _ip, _ip, _dp]
@@ -191,9 +193,14 @@ class HyperRomModel:
     (mesh.hpp:185-191) — G[K,3,n], w[K], ip ids, material ids (0 matrix J2,
     1 inclusion), volume. Host only."""
 
-    def __init__(self, subdivisions=33, n=12, K=200, seed=0):
+    def __init__(self, subdivisions=33, n=12, K=200, seed=0, mesh_file: str | None = None):
+        """subdivisions: default_cell RVE; or mesh_file: an RVE in the
+        reference's plain-text mesh format (write_mesh, mesh.hpp:413-489)."""
         h = C.c_void_p()
-        _check(lib.fe2_model_build(subdivisions, n, K, seed, C.byref(h)))
+        if mesh_file is not None:
+            _check(lib.fe2_model_build_from_mesh(str(mesh_file).encode(), n, K, seed, C.byref(h)))
+        else:
+            _check(lib.fe2_model_build(subdivisions, n, K, seed, C.byref(h)))
         try:
             n_, K_, nf, vol = C.c_int(), C.c_int(), C.c_int(), C.c_double()
             _check(lib.fe2_model_sizes(h, C.byref(n_), C.byref(K_), C.byref(nf), C.byref(vol)))
@@ -213,6 +220,11 @@ class HyperRomModel:
     @property
     def K_j2(self):
         return int(np.sum(self.mat == 0))
+
+
+def write_mesh(subdivisions, path):
+    """Write the default_cell(subdivisions) RVE in the reference's mesh format."""
+    _check(lib.fe2_mesh_write(subdivisions, str(path).encode()))
 
 
 def make_paths(kind, seed, P, n_incr, p0=0):
