@@ -74,3 +74,26 @@ def build_rule(model_full: HyperRomModel, paths, m_target, tol=1e-6, svd_tol=1e-
     k = int(np.sum(S > svd_tol * S[0]))
     ids, w, res = ecm_select(Uf[:, :k], model_full.w, m_target, tol)
     return ids, w, res, k
+
+
+def save_rule(path, ids, weights):
+    """CubatureRule as text (SPEC.md hyper External Interfaces): one
+    "point_id weight" line per point, weights in %.17g (bit-exact)."""
+    with open(path, "w") as f:
+        f.write(f"fe2rom-rule 1\n{len(ids)}\n")
+        for q, w in zip(ids, weights):
+            f.write(f"{int(q)} {float(w):.17g}\n")
+
+
+def load_rule(path):
+    with open(path) as f:
+        head = f.readline().split()
+        if head != ["fe2rom-rule", "1"]:
+            raise ValueError("not a fe2rom rule file")
+        m = int(f.readline())
+        rows = [f.readline().split() for _ in range(m)]
+    ids = np.array([int(r[0]) for r in rows], dtype=np.int32)
+    w = np.array([float(r[1]) for r in rows])
+    if (w <= 0).any() or len(set(ids.tolist())) != m:
+        raise ValueError("rule weights must be positive and point ids unique")
+    return ids, w

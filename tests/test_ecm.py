@@ -53,3 +53,13 @@ def test_residual_monotone_in_target():
     res = [E.ecm_select(U, w, t, 0.0)[2] for t in (5, 10, 20, 30, 41)]
     assert all(b <= a * (1 + 1e-12) for a, b in zip(res, res[1:]))
     assert res[-1] < 1e-10
+
+
+def test_rule_text_round_trip(tmp_path):
+    rng = np.random.default_rng(4)
+    ids = np.sort(rng.choice(6075, 87, replace=False)).astype(np.int32)
+    w = rng.uniform(1e-5, 1e-3, 87)
+    E.save_rule(tmp_path / "rule.txt", ids, w)
+    i2, w2 = E.load_rule(tmp_path / "rule.txt")
+    np.testing.assert_array_equal(i2, ids)
+    np.testing.assert_array_equal(w2, w)
