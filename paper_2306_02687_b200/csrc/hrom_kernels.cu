@@ -10,27 +10,27 @@
 //   Σraw = K_aE,e^T α + C_EE,e E − s_p + Σ_plastic w Δσ_q
 // with K_e, K_aE,e, C_EE,e constant over the model (host, once) and
 // b_p = Σ w G^T S(εp), s_p = Σ w S(εp) constant over an increment (kept
-// per point, updated by the commit pass from the plastic increments only).
+// per point; accepting a state moves them by that pass's plastic parts).
 //
 // k_increment — ONE persistent launch per load increment. Each warp owns a
 // macro point at a time (work queue) and drives it through the whole
 // increment of run_trajectory (rve.hpp:459-491): assembly passes and the
 // reduced Newton / line-search state machine of micro_newton
 // (rve.hpp:285-346), bisected sub-steps (:473-478), the static condensation
-// C = (C_EE − K_Ea K_aa^-1 K_aE)/V of homogenize (:350-392), and the commit
-// pass that writes the history (commit-after-acceptance, :283-284, :480).
-//  - A pass streams the J2 cubature rows G_q in 32-point chunks from a
-//    kStages-deep shared-memory ring filled by TMA bulk copies
-//    (cp.async.bulk + mbarrier). Every warp consumes the same cyclic chunk
-//    sequence; the last warp to release a stage refills it. No CTA barrier:
-//    warps drift freely, so compute-bound assembly passes of some warps
-//    overlap the HBM-bound commit passes and Cholesky phases of others.
+// C = (C_EE − K_Ea K_aa^-1 K_aE)/V of homogenize (:350-392), and the
+// commit-after-acceptance of the history (:283-284, :480).
+//  - G rows: the whole J2 operator resident in shared memory when it fits
+//    (RES, 8 warps), else a ring of 32-point chunks filled by TMA bulk copies
+//    (cp.async.bulk + mbarrier) that all warps consume in the same cyclic
+//    order (the last warp to release a stage refills it; no CTA barrier).
 //  - Assembly pass: lane = cubature point (ε_q, elastic trial, yield test on
-//    the history stream, prefetched a chunk ahead); plastic points are
-//    compacted (ballot/popc) and only they are contracted on the FP64 tensor
-//    cores (mma.sync m8n8k4 f64 = DMMA). K_aa stays in shared memory.
-//  - Commit pass: recompute at the converged (E, α), write εp, eq of the
-//    plastic points (80 B/point stream), fold Δεp into b_p, s_p.
+//    the history loaded one chunk ahead); plastic points are compacted
+//    (ballot/popc) and only they are contracted on the FP64 tensor cores
+//    (mma.sync m8n8k4 f64 = DMMA). K_aa stays in shared memory. The pass also
+//    writes the candidate history of its state into the point's non-committed
+//    buffer (double-buffered history).
+//  - Accepting a converged state flips the point's buffer bit, stores α_c and
+//    moves b_p, s_p by the pass's plastic corrections — no commit pass.
 #include <cstdio>
 #include <cstdlib>
 
