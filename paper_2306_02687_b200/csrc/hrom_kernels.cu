@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   double* sKaE = sRp + NP;       // K_aE [NP][3]
   double* sU = sKaE + 3 * NP;
   double* sDC = sU;                                 // [32][6] w ΔC (00 01 02 11 12 22) of the plastic slots
-  double* sDS = sU + kQC * 6;                       // [32][3] w Δσ (commit pass: w S(Δεp))
+  double* sDS = sU + kQC * 6;                       // [32][3] w Δσ of the plastic slots
   int* sQ = reinterpret_cast<int*>(sU + kQC * 9);   // [32]    chunk-local cubature index
   double* sK = sU;                                  // K_aa packed lower (after an assembly pass)
 
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   const NewtonCfg& cfg = A.cfg;
   constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
 
-  // Every large piece (assembly pass, factorization, commit pass) has exactly
+  // Every large piece (assembly pass, factorization, acceptance) has exactly
   // one call site below, so each is inlined once: the kernel's instruction
   // footprint stays small enough that warps in different phases do not
   // thrash the instruction cache.

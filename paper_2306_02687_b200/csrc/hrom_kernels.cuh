@@ -84,7 +84,7 @@ struct IncCounters {
   unsigned long long assemblies;
   unsigned long long commits;
   unsigned long long plastic_evals;
-  unsigned long long commit_plastic;  // J2 points whose history was written by commit passes
+  unsigned long long commit_plastic;  // plastic J2 points of the accepted states
 };
 
 struct IncArgs {

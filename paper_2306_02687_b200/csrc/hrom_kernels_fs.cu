@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
   const NewtonCfg& cfg = A.cfg;
   constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
 
-  // One call site each for the assembly pass, the LU and the commit pass
+  // One call site each for the assembly pass, the LU and the acceptance
   // (small instruction footprint); the debug dump runs through the same loop.
   const bool dbg = A.dbg != nullptr;  // assembly dump: r, K_aa, K_aF, K_Fa, C_FF, P_raw
   auto dump = [&]() {
