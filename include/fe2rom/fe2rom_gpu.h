@@ -201,8 +201,10 @@ int fe2_hrom_set_stream(fe2_hrom_t h, void* stream);
  * state, fe2_hrom_restore) and assembles the tangent from C_macro; accepted
  * steps commit (fe2_hrom_snapshot). Program: n_load steps to u_max, then
  * unloading in the same steps until R changes sign (U_residual = linear zero
- * crossing; NaN if none within max_unload steps). Host code; the engine must
- * be a small-strain handle with fe2_macro_points() points allocated. */
+ * crossing; NaN if none within max_unload steps). Host code; the engine
+ * holds fe2_macro_points() points. A finite-strain engine (fe2_hrom_create_fs)
+ * makes it a total-Lagrangian FE² run: H = F - I from the 4-row gradient
+ * operator, f_int = sum w Bg^T P, K = sum w Bg^T A Bg (LU). */
 typedef struct {
   double length, height;      /* beam L x H (desk default 4 x 1) */
   int nx, ny;                 /* cells along x / y, two Tri6 each (desk: 8 x 2 = 32 elements) */

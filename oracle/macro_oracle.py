@@ -67,9 +67,11 @@ class ReplayEngine:
         self.path = []  # committed increments, each (P, 3)
 
     def solve(self, E):
-        path = np.stack(self.path + [E], axis=1)  # (P, k, 3)
+        path = np.stack(self.path + [E], axis=1)  # (P, k, 3 | 4)
         r = self.h.run(path, **self.opts)
-        return dict(sigma=r["sigma"][:, -1], C=r["C"][:, -1], iters=r["iters"][:, -1], status=r["status"][:, -1])
+        fs = isinstance(self.h, O.HromFs)  # finite strain: P_M, A_M
+        return dict(sigma=r["P" if fs else "sigma"][:, -1], C=r["A" if fs else "C"][:, -1], iters=r["iters"][:, -1],
+                    status=r["status"][:, -1])
 
     def commit(self, E):
         self.path.append(np.array(E))
@@ -81,6 +83,13 @@ def solve_program(m, engine: ReplayEngine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, 
     cumulative micro iters) and U_residual."""
     beam = build_beam(L, H, nx, ny) if m is None else m
     B, w, elem, tri = beam["B"], beam["w"], beam["elem"], beam["tri"]
+    if isinstance(engine.h, O.HromFs):  # total Lagrangian: H = F - I from the gradient operator
+        Bg = np.zeros((len(w), 4, 12))
+        Bg[:, 0, 0::2] = B[:, 0, 0::2]
+        Bg[:, 1, 0::2] = B[:, 2, 0::2]
+        Bg[:, 2, 1::2] = B[:, 2, 1::2]
+        Bg[:, 3, 1::2] = B[:, 1, 1::2]
+        B = Bg
     P = len(w)
     nd = 2 * len(beam["xy"])
     role = np.zeros(nd, dtype=int)

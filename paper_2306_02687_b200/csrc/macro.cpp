@@ -133,6 +133,38 @@ bool chol_solve(std::vector<double>& A, int n, std::vector<double>& b) {
   return true;
 }
 
+// dense LU solve with partial pivoting (finite-strain macro tangent: A = dP/dF is
+// not symmetric); false if singular
+bool lu_solve(std::vector<double>& A, int n, std::vector<double>& b) {
+  for (int j = 0; j < n; ++j) {
+    int p = j;
+    double best = std::abs(A[static_cast<size_t>(j) * n + j]);
+    for (int i = j + 1; i < n; ++i)
+      if (std::abs(A[static_cast<size_t>(i) * n + j]) > best) {
+        best = std::abs(A[static_cast<size_t>(i) * n + j]);
+        p = i;
+      }
+    if (!(best > 0.0)) return false;
+    if (p != j) {
+      for (int k = 0; k < n; ++k) std::swap(A[static_cast<size_t>(j) * n + k], A[static_cast<size_t>(p) * n + k]);
+      std::swap(b[j], b[p]);
+    }
+    const double inv = 1.0 / A[static_cast<size_t>(j) * n + j];
+    for (int i = j + 1; i < n; ++i) {
+      const double l = A[static_cast<size_t>(i) * n + j] * inv;
+      if (l == 0.0) continue;
+      for (int k = j + 1; k < n; ++k) A[static_cast<size_t>(i) * n + k] -= l * A[static_cast<size_t>(j) * n + k];
+      b[i] -= l * b[j];
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int k = i + 1; k < n; ++k) s -= A[static_cast<size_t>(i) * n + k] * b[k];
+    b[i] = s / A[static_cast<size_t>(i) * n + i];
+  }
+  return true;
+}
+
 void engine_check(int rc) {
   if (rc != 0) throw Failure(static_cast<Code>(rc - 1), std::string("engine: ") + fe2_last_error());
 }
@@ -172,9 +204,26 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
     check(cfg->n_load >= 1 && cfg->max_iter >= 1 && cfg->tol > 0.0, Code::config, "invalid macro options");
     int kin = 0;
     engine_check(fe2_hrom_kinematics(engine, &kin));
-    check(kin == 0, Code::config, "the macro beam driver uses the small-strain engine");
     const Beam m = build_beam(cfg->length, cfg->height, cfg->nx, cfg->ny);
     const int P = static_cast<int>(m.w.size());
+    // per-Gauss-point operator: small strain (E11, E22, g12) = B u; finite strain
+    // (total Lagrangian) H = F - I = (dux/dX, dux/dY, duy/dX, duy/dY) = Bg u
+    const int nr = kin ? 4 : 3;
+    std::vector<double> Op(static_cast<size_t>(P) * nr * 12, 0.0);
+    for (int g = 0; g < P; ++g) {
+      double* o = Op.data() + static_cast<size_t>(g) * nr * 12;
+      const double* B = m.B[g].data();
+      if (!kin) {
+        std::memcpy(o, B, 36 * sizeof(double));
+      } else {
+        for (int a = 0; a < 6; ++a) {
+          o[0 * 12 + 2 * a] = B[0 * 12 + 2 * a];          // dN/dx
+          o[1 * 12 + 2 * a] = B[2 * 12 + 2 * a];          // dN/dy
+          o[2 * 12 + 2 * a + 1] = B[2 * 12 + 2 * a + 1];  // dN/dx
+          o[3 * 12 + 2 * a + 1] = B[1 * 12 + 2 * a + 1];  // dN/dy
+        }
+      }
+    }
     fe2_hrom_stats_t est{};
     engine_check(fe2_hrom_stats(engine, &est));
     check(est.points == P, Code::config, "engine must hold one point per macro Gauss point (fe2_macro_points)");
@@ -188,7 +237,7 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
     for (int d = 0; d < nd; ++d)
       if (role[d] == 0) fidx[d] = nf++;
 
-    std::vector<double> u(nd, 0.0), E(3 * P), sig(3 * P), C(9 * P), res(P), fint(nd), Kff, rhs;
+    std::vector<double> u(nd, 0.0), E(nr * P), sig(nr * P), C(nr * nr * P), res(P), fint(nd), Kff, rhs;
     std::vector<int> it(P), pc(P), st(P);
     const fe2_newton_opts_t mopt = cfg->micro;
     auto dofs = [&](int e, int d) { return 2 * m.tri[e][d / 2] + d % 2; };
@@ -199,10 +248,11 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
     auto micro_solve = [&]() -> bool {
       for (int g = 0; g < P; ++g) {
         const int e = m.elem[g];
-        for (int i = 0; i < 3; ++i) {
+        const double* o = Op.data() + static_cast<size_t>(g) * nr * 12;
+        for (int i = 0; i < nr; ++i) {
           double s = 0.0;
-          for (int d = 0; d < 12; ++d) s += m.B[g][i * 12 + d] * u[dofs(e, d)];
-          E[3 * g + i] = s;
+          for (int d = 0; d < 12; ++d) s += o[i * 12 + d] * u[dofs(e, d)];
+          E[nr * g + i] = s;
         }
       }
       engine_check(fe2_hrom_restore(engine));
@@ -215,9 +265,10 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
       std::fill(fint.begin(), fint.end(), 0.0);
       for (int g = 0; g < P; ++g) {
         const int e = m.elem[g];
+        const double* o = Op.data() + static_cast<size_t>(g) * nr * 12;
         for (int d = 0; d < 12; ++d) {
           double s = 0.0;
-          for (int i = 0; i < 3; ++i) s += m.B[g][i * 12 + d] * sig[3 * g + i];
+          for (int i = 0; i < nr; ++i) s += o[i * 12 + d] * sig[nr * g + i];
           fint[dofs(e, d)] += m.w[g] * s;
         }
       }
@@ -240,26 +291,34 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
         Kff.assign(static_cast<size_t>(nf) * nf, 0.0);
         for (int g = 0; g < P; ++g) {
           const int e = m.elem[g];
-          double CB[3][12];
-          for (int i = 0; i < 3; ++i)
-            for (int d = 0; d < 12; ++d)
-              CB[i][d] = C[9 * g + 3 * i] * m.B[g][d] + C[9 * g + 3 * i + 1] * m.B[g][12 + d] +
-                         C[9 * g + 3 * i + 2] * m.B[g][24 + d];
+          const double* o = Op.data() + static_cast<size_t>(g) * nr * 12;
+          const double* Cg = C.data() + static_cast<size_t>(g) * nr * nr;
+          double CB[4][12];
+          for (int i = 0; i < nr; ++i)
+            for (int d = 0; d < 12; ++d) {
+              double s = 0.0;
+              for (int j = 0; j < nr; ++j) s += Cg[i * nr + j] * o[j * 12 + d];
+              CB[i][d] = s;
+            }
           for (int a = 0; a < 12; ++a) {
             const int fa = fidx[dofs(e, a)];
             if (fa < 0) continue;
             for (int b = 0; b < 12; ++b) {
               const int fb = fidx[dofs(e, b)];
               if (fb < 0) continue;
-              Kff[static_cast<size_t>(fa) * nf + fb] +=
-                  m.w[g] * (m.B[g][a] * CB[0][b] + m.B[g][12 + a] * CB[1][b] + m.B[g][24 + a] * CB[2][b]);
+              double s = 0.0;
+              for (int i = 0; i < nr; ++i) s += o[i * 12 + a] * CB[i][b];
+              Kff[static_cast<size_t>(fa) * nf + fb] += m.w[g] * s;
             }
           }
         }
         rhs.assign(nf, 0.0);
         for (int d = 0; d < nd; ++d)
           if (fidx[d] >= 0) rhs[fidx[d]] = -fint[d];
-        check(chol_solve(Kff, nf, rhs), Code::solver, "macro tangent is not positive definite");
+        if (kin)
+          check(lu_solve(Kff, nf, rhs), Code::solver, "finite-strain macro tangent is singular");
+        else
+          check(chol_solve(Kff, nf, rhs), Code::solver, "macro tangent is not positive definite");
         for (int d = 0; d < nd; ++d)
           if (fidx[d] >= 0) u[d] += rhs[fidx[d]];
       }

@@ -37,3 +37,21 @@ def test_device_macro_driver_matches_oracle(u_max, n_load):
     if u_max > 0.1:
         assert g["U_residual"] > 0.0
     assert abs(g["U_residual"] - ures) <= 1e-8 * u_max
+
+
+def test_device_finite_strain_macro_driver_matches_oracle():
+    """Total-Lagrangian FE² beam on the finite-strain engine (config-2
+    kinematics) against the oracle driver on the finite-strain oracle."""
+    m = F.HyperRomModel(33, 12, 200, 0)
+    eng = F.HyperRomEngine.from_model(m, finite_strain=True)
+    cfg = F.MacroConfig(u_max=0.3, n_load=10)
+    g = F.solve_program(cfg, eng)
+    beam = MO.build_beam(cfg.length, cfg.height, cfg.nx, cfg.ny)
+    orc = O.HromFs(m.G4, m.w, m.mat, m.materials, m.volume)
+    rows, ures = MO.solve_program(beam, MO.ReplayEngine(orc, len(beam["w"]), threads=16), u_max=cfg.u_max,
+                                  n_load=cfg.n_load, max_unload=cfg.max_unload, tol=cfg.tol, max_iter=cfg.max_iter)
+    assert len(g["U"]) == len(rows)
+    np.testing.assert_array_equal(g["macro_iters"], rows[:, 2].astype(int))
+    np.testing.assert_allclose(g["micro_iters"], rows[:, 3], rtol=1e-3, atol=0)
+    assert np.abs(g["R"] - rows[:, 1]).max() <= 1e-8 * np.abs(rows[:, 1]).max()
+    assert g["U_residual"] > 0.0 and abs(g["U_residual"] - ures) <= 1e-8 * cfg.u_max

@@ -62,3 +62,17 @@ def test_oracle_driver_plastic_residual_displacement(desk_hrom):
     assert secant[-1] < 0.98 * secant[0]  # yielding softens the response
     assert 0.0 < ures < 0.3
     assert (rows[:, 2] >= 1).all()
+
+
+def test_oracle_finite_strain_driver_small_load_limit():
+    """Total-Lagrangian FE² with the finite-strain oracle: for a small tip
+    displacement the reaction equals the small-strain driver's to O(U)."""
+    md = O.Model(subdivisions=33, n=12, K=200, seed=0)
+    desk = [("j2", 1.0, 0.3, 0.01, 0.016), ("elastic", 10.0, 0.3)]
+    G4 = O.model_g4(33, 12, 200, 0)
+    beam = MO.build_beam(4.0, 1.0, 8, 2)
+    ss = O.Hrom(md.G, md.w, md.mat, desk, md.volume)
+    fs = O.HromFs(G4, md.w, md.mat, desk, md.volume)
+    r_ss, _ = MO.solve_program(beam, MO.ReplayEngine(ss, len(beam["w"])), u_max=1e-3, n_load=2, max_unload=0)
+    r_fs, _ = MO.solve_program(beam, MO.ReplayEngine(fs, len(beam["w"])), u_max=1e-3, n_load=2, max_unload=0)
+    np.testing.assert_allclose(r_fs[:, 1], r_ss[:, 1], rtol=5e-3)
