@@ -253,6 +253,50 @@ int fe2_model_sizes(fe2_model_t m, int* n, int* K, int* n_free, double* volume);
 int fe2_model_arrays(fe2_model_t m, double* G, double* w, int* ip_id, int* mat_id);
 /* G4[K][4][n]: the displacement-gradient operator of the same Φ and cubature */
 int fe2_model_g4(fe2_model_t m, double* G4);
+/* The same with a given basis (e.g. fe2_pod_basis) instead of the seeded Φ:
+ * basis[n][n_dofs] column-major over ALL DOFs (mode j at basis + j * n_dofs,
+ * the reference ReducedBasis::V); boundary rows are ignored.
+ * mesh_path NULL selects default_cell(subdivisions). */
+int fe2_model_build_basis(int subdivisions, const char* mesh_path, const double* basis, int n, int K, uint64_t seed,
+                          fe2_model_t* out);
+
+/* ---- high-fidelity RVE solve and POD basis ----------
+ * fe2_hf_* is the full-field micro problem on the device: per-element
+ * material update + element stiffness kernel, deterministic gather of the
+ * dense free stiffness, cuSOLVER Cholesky (loaded at first use). Replaces
+ * micro_newton + homogenize + run_trajectory with SnapshotRecorder
+ * (rve.hpp:285-392, :397-494; linear BC). */
+typedef struct fe2_hf_s* fe2_hf_t;
+/* RVE = default_cell(subdivisions) or mesh_path; materials indexed by the
+ * element material id. */
+int fe2_hf_create(int device, int subdivisions, const char* mesh_path, const fe2_material_t* materials, int n_materials,
+                  fe2_hf_t* out);
+void fe2_hf_destroy(fe2_hf_t h);
+int fe2_hf_sizes(fe2_hf_t h, int* n_dofs, int* n_free, int* n_ips, double* volume);
+/* run_trajectory from the virgin state along E[n_steps][3] (bisection,
+ * warm start = committed solution + affine increment, rve.hpp:459-471).
+ * Per step: sigma[3], C[9] (homogenize), Newton iterations (all attempts),
+ * max |u - E.x|, last residual norm; snapshots (nullable) [n_steps][n_dofs]
+ * = the converged fluctuation field u - E.x (the x_u column, rve.hpp:486-490).
+ * Non-convergence after max_bisections -> solver error. */
+int fe2_hf_trajectory(fe2_hf_t h, int n_steps, const double* E, const fe2_newton_opts_t* opts, double* sigma,
+                      double* C, int* iterations, double* u_fluct_inf, double* res_last, double* snapshots);
+/* build_elastic_modes: fluctuation responses of the
+ * elastic RVE (every material's elastic part) to unit macro strains
+ * (1,0,0),(0,1,0),(0,0,1), orthonormalised (Gram-Schmidt, twice); modes whose
+ * remaining norm is <= 1e-10 |E.x| are dropped (homogeneous RVE -> 0 modes).
+ * modes[3][n_dofs] column-major; *count = modes kept. */
+int fe2_hf_elastic_modes(fe2_hf_t h, double* modes, int* count);
+/* pod: V = [elastic | leading left singular vectors of X
+ * deflated against the elastic modes], re-orthonormalised. X[n_cols][n_rows]
+ * and elastic[n_elastic][n_rows] column-major; V[n_target][n_rows]. Deflated
+ * singular values (descending, n_cols of them) go to singular_values; a POD
+ * mode's largest-magnitude entry is positive. Deflated rank counts singular
+ * values > 1e-10 |X|_F; n_target > n_elastic + rank -> rank error with
+ * *max_modes = n_elastic + rank. SVD on the device (cuSOLVER gesvd). */
+int fe2_pod_basis(int device, const double* X, int64_t n_rows, int n_cols, const double* elastic, int n_elastic,
+                  int n_target, double* V, double* singular_values, int* max_modes);
+
 /* path kind 0 = config-0 uniaxial rotated, 1 = config-1 reversal:
  * E[P][n_incr][3]; kind 2 = config-2 finite strain: H[P][n_incr][4]
  * (F = I + (k/n_incr) H_end, H_end ~ U[-0.08, 0.08]^4 with det F > 0.8),

@@ -1689,7 +1689,7 @@ int orc_mesh_ip(orc_mesh_t m, int ip, double* B36, double* w, int* element) {
 
 int orc_hf_trajectory(orc_mesh_t m, const orc_material_t* mats, int n_mats, int n_steps, const double* E,
                       const orc_newton_opts_t* opts, double* sigma, double* C, int* iterations,
-                      double* u_fluct_inf, double* res_last) {
+                      double* u_fluct_inf, double* res_last, double* snapshots) {
   return guarded([&] {
     std::vector<Mat> ms;
     for (int i = 0; i < n_mats; ++i) ms.push_back(to_mat(mats[i]));
@@ -1731,6 +1731,12 @@ int orc_hf_trajectory(orc_mesh_t m, const orc_material_t* mats, int n_mats, int 
             double mx = 0.0;
             for (int i = 0; i < p.mesh.n_dofs(); ++i) mx = std::max(mx, std::abs(r.u_full[i] - aff2[i]));
             u_fluct_inf[k] = mx;
+          }
+          if (snapshots) {  // SnapshotRecorder x_u column, rve.hpp:486-490
+            std::vector<double> aff3;
+            affine_field(p.mesh, Ev, aff3);
+            for (int i = 0; i < p.mesh.n_dofs(); ++i)
+              snapshots[(size_t)k * p.mesh.n_dofs() + i] = r.u_full[i] - aff3[i];
           }
           if (res_last) res_last[k] = r.res_hist.back();
         }

@@ -78,10 +78,12 @@ typedef struct {
 
 /* Run a strain path E[n_steps][3] on the HF RVE (materials by element id).
  * Per step outputs: sigma[3], C[9], iterations, converged flag.
- * u_fluct_inf (optional, per step): max |u - E.x| over all DOFs. */
+ * u_fluct_inf (optional, per step): max |u - E.x| over all DOFs.
+ * snapshots (optional) [n_steps][n_dofs]: the converged fluctuation u - E.x
+ * of each step (SnapshotRecorder x_u, rve.hpp:486-490). */
 int orc_hf_trajectory(orc_mesh_t m, const orc_material_t* mats, int n_mats, int n_steps,
                       const double* E, const orc_newton_opts_t* opts, double* sigma, double* C,
-                      int* iterations, double* u_fluct_inf, double* res_hist_last);
+                      int* iterations, double* u_fluct_inf, double* res_hist_last, double* snapshots);
 
 /* ---- hyper-ROM model (offline stage): Φ, cubature rule, G_q ------------
  * Φ: Gaussian (Rng) on free DOFs, Householder thin QR, zero rows on the

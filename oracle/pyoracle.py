@@ -65,7 +65,7 @@ def _load():
     L.orc_mesh_arrays.argtypes = [C.c_void_p, _dp, _ip, _ip]
     L.orc_mesh_ip.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _ip]
     L.orc_hf_trajectory.argtypes = [C.c_void_p, C.POINTER(_Mat), C.c_int, C.c_int, _dp, C.POINTER(_Opts), _dp, _dp,
-                                    _ip, _dp, _dp]
+                                    _ip, _dp, _dp, _dp]
     L.orc_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.orc_model_build_on_mesh.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.orc_model_free.argtypes = [C.c_void_p]
@@ -172,16 +172,20 @@ class Mesh:
         _check(lib.orc_mesh_ip(self._h, i, _d(B), C.byref(w), C.byref(e)))
         return B, w.value, e.value
 
-    def hf_trajectory(self, materials, E_path, tol=1e-8, max_iter=30, max_bisections=4):
+    def hf_trajectory(self, materials, E_path, tol=1e-8, max_iter=30, max_bisections=4, snapshots=False):
         E_path = np.ascontiguousarray(E_path, dtype=np.float64).reshape(-1, 3)
         k = E_path.shape[0]
         mats = (_Mat * len(materials))(*[mat_struct(m) for m in materials])
         o = _Opts(tol, max_iter, max_bisections)
         sig, Cm, it = np.empty((k, 3)), np.empty((k, 3, 3)), np.empty(k, dtype=np.int32)
         uf, rl = np.empty(k), np.empty(k)
+        X = np.empty((k, 2 * self.n_nodes)) if snapshots else None
         _check(lib.orc_hf_trajectory(self._h, mats, len(materials), k, _d(E_path), C.byref(o), _d(sig), _d(Cm),
-                                     _i(it), _d(uf), _d(rl)))
-        return dict(sigma=sig, C=Cm, iterations=it, u_fluct_inf=uf, res_last=rl)
+                                     _i(it), _d(uf), _d(rl), _d(X) if snapshots else None))
+        out = dict(sigma=sig, C=Cm, iterations=it, u_fluct_inf=uf, res_last=rl)
+        if snapshots:
+            out["snapshots"] = X
+        return out
 
 
 class Model:

@@ -24,6 +24,7 @@ from .hrom import (  # noqa: F401
     update_material_soa_device,
 )
 from .fe2 import MacroConfig, macro_gauss, macro_points, solve_program  # noqa: F401
+from .pod import HfRve, pod_basis  # noqa: F401
 
 __all__ = [
     "ElasticParams",
@@ -42,4 +43,6 @@ __all__ = [
     "macro_gauss",
     "macro_points",
     "solve_program",
+    "HfRve",
+    "pod_basis",
 ]

@@ -12,8 +12,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libfe2rom_gpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["hrom_host.cu", "hrom_kernels.cu", "hrom_kernels_big.cu", "hrom_kernels_fs.cu", "material_soa.cu", "setup.cpp", "macro.cpp", "ecm.cpp"]
-HEADERS = ["common.hpp", "material.cuh", "hrom_kernels.cuh", "device_common.cuh", "biot.cuh"]
+SOURCES = ["hrom_host.cu", "hrom_kernels.cu", "hrom_kernels_big.cu", "hrom_kernels_fs.cu", "material_soa.cu", "setup.cpp", "macro.cpp", "ecm.cpp", "hf.cu"]
+HEADERS = ["common.hpp", "material.cuh", "hrom_kernels.cuh", "device_common.cuh", "biot.cuh", "host_util.cuh", "rve.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -35,7 +35,7 @@ def build_native(force=False, verbose=False, out=None, defines=()):
         return target
     os.makedirs(os.path.dirname(target), exist_ok=True)
     cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-I", os.path.join(ROOT, "include"),
-           "-I", CSRC, "-o", target + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+           "-I", CSRC, "-o", target + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

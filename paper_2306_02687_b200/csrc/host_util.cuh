@@ -1,0 +1,52 @@
+// Host-side helpers shared by the C-ABI translation units (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "common.hpp"
+#include "fe2rom/fe2rom_gpu.h"
+#include "material.cuh"
+
+namespace fe2 {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Failure(Code::numeric, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class T>
+inline T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+template <class T>
+inline void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+inline void require_device(int device) {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw Failure(Code::numeric, "no CUDA device available: the B200 engine has no CPU fallback");
+  check(device >= 0 && device < count, Code::config, "device index out of range");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  check(prop.major == 10, Code::numeric, std::string("the engine is built for sm_100a (B200); found ") + prop.name);
+  CK(cudaSetDevice(device));
+}
+
+inline MatDev to_dev(const fe2_material_t& m) {
+  check(m.kind == 0 || m.kind == 1, Code::config, "unsupported material kind");
+  const double E = m.p[0], nu = m.p[1];
+  check(E > 0.0 && nu >= 0.0 && nu < 0.5, Code::config, "invalid elastic parameters");            // materials.hpp:80-82
+  if (m.kind == 1) check(m.p[2] > 0.0 && m.p[3] >= 0.0, Code::config, "invalid J2 parameters");  // :83-87
+  return make_mat(m.kind, E, nu, m.kind == 1 ? m.p[2] : 0.0, m.kind == 1 ? m.p[3] : 0.0);
+}
+
+}  // namespace fe2

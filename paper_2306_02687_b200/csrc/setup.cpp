@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "rve.hpp"
 
 namespace fe2 {
 
@@ -366,11 +367,14 @@ Cell mesh_read(const std::string& path) {
   return cell;
 }
 
-Model build_model_on(const Cell& cell, int n, int K, std::uint64_t seed);
+Model build_model_on(const Cell& cell, int n, int K, std::uint64_t seed, const double* basis = nullptr);
 
 Model build_model(int sub, int n, int K, std::uint64_t seed) { return build_model_on(mesh_default_cell(sub), n, K, seed); }
 
-Model build_model_on(const Cell& cell, int n, int K, std::uint64_t seed) {
+// basis: optional Φ over all DOFs, column-major (mode j at basis + j * 2 n_nodes),
+// e.g. a POD basis (fe2_pod_basis); its boundary rows are ignored (linear BC).
+// Without it Φ is the seeded orthonormal basis.
+Model build_model_on(const Cell& cell, int n, int K, std::uint64_t seed, const double* basis) {
   const int n_nodes = (int)cell.x.size();
   const int n_ip = 3 * (int)cell.tri.size();
   std::vector<int> dof_free(2 * n_nodes, -1);
@@ -383,7 +387,11 @@ Model build_model_on(const Cell& cell, int n, int K, std::uint64_t seed) {
   if (K < 1 || K > n_ip) throw Failure(Code::config, "cubature size out of range");
 
   std::vector<double> phi((size_t)nf * n);
-  {
+  if (basis) {
+    for (int d = 0; d < 2 * n_nodes; ++d)
+      if (dof_free[d] >= 0)
+        for (int j = 0; j < n; ++j) phi[(size_t)dof_free[d] * n + j] = basis[(size_t)j * 2 * n_nodes + d];
+  } else {
     SeededStream s(seed ^ kPhiStream);
     for (int j = 0; j < n; ++j)
       for (int i = 0; i < nf; ++i) phi[(size_t)i * n + j] = s.gauss();
@@ -495,6 +503,61 @@ void make_paths(int kind, std::uint64_t seed, std::int64_t p0, std::int64_t P, i
   }
 }
 
+
+Cell load_cell(int subdivisions, const char* mesh_path) {
+  return mesh_path ? mesh_read(mesh_path) : mesh_default_cell(subdivisions);
+}
+
+RveData rve_data(int subdivisions, const char* mesh_path) {
+  const Cell cell = load_cell(subdivisions, mesh_path);
+  RveData r;
+  r.n_nodes = (int)cell.x.size();
+  r.n_el = (int)cell.tri.size();
+  r.x = cell.x;
+  r.y = cell.y;
+  r.volume = cell.area;
+  r.phase = cell.phase;
+  r.free_index.assign(2 * r.n_nodes, -1);
+  for (int d = 0; d < 2 * r.n_nodes; ++d)
+    if (!cell.on_boundary[d / 2]) r.free_index[d] = r.n_free++;
+  r.conn.resize((size_t)6 * r.n_el);
+  r.B.resize((size_t)36 * 3 * r.n_el);
+  r.w.resize((size_t)3 * r.n_el);
+  for (int e = 0; e < r.n_el; ++e) {
+    for (int a = 0; a < 6; ++a) r.conn[(size_t)6 * e + a] = cell.tri[e][a];
+    for (int g = 0; g < 3; ++g) {
+      double Bq[3][12];
+      const double det = strain_operator(cell, cell.tri[e], kGauss[g][0], kGauss[g][1], Bq);
+      std::memcpy(r.B.data() + (size_t)36 * (3 * e + g), Bq, sizeof(Bq));
+      r.w[3 * e + g] = kGaussW * det;
+    }
+  }
+  return r;
+}
+
+int orthonormalize_columns(std::vector<double>& A, std::int64_t rows, int cols, const std::vector<double>& drop_tol) {
+  int kept = 0;
+  for (int j = 0; j < cols; ++j) {
+    double* v = A.data() + (size_t)j * rows;
+    double nrm = 0.0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int c = 0; c < kept; ++c) {
+        const double* q = A.data() + (size_t)c * rows;
+        double dot = 0.0;
+        for (std::int64_t i = 0; i < rows; ++i) dot += q[i] * v[i];
+        for (std::int64_t i = 0; i < rows; ++i) v[i] -= dot * q[i];
+      }
+    for (std::int64_t i = 0; i < rows; ++i) nrm += v[i] * v[i];
+    nrm = std::sqrt(nrm);
+    if (!(nrm > drop_tol[j])) continue;
+    double* dst = A.data() + (size_t)kept * rows;
+    for (std::int64_t i = 0; i < rows; ++i) dst[i] = v[i] / nrm;
+    ++kept;
+  }
+  A.resize((size_t)kept * rows);
+  return kept;
+}
+
 }  // namespace fe2
 
 struct fe2_model_s {
@@ -510,6 +573,13 @@ int fe2_model_build_from_mesh(const char* path, int n, int K, uint64_t seed, fe2
   return fe2::guard([&] {
     fe2::check(path && out, fe2::Code::config, "bad arguments");
     *out = new fe2_model_s{fe2::build_model_on(fe2::mesh_read(path), n, K, seed)};
+  });
+}
+int fe2_model_build_basis(int subdivisions, const char* mesh_path, const double* basis, int n, int K, uint64_t seed,
+                          fe2_model_t* out) {
+  return fe2::guard([&] {
+    fe2::check(basis && out && n >= 1, fe2::Code::config, "bad arguments");
+    *out = new fe2_model_s{fe2::build_model_on(fe2::load_cell(subdivisions, mesh_path), n, K, seed, basis)};
   });
 }
 int fe2_mesh_write(int subdivisions, const char* path) {

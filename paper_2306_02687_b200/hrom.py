@@ -99,6 +99,14 @@ def _load():
     L.fe2_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.fe2_model_build_from_mesh.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.fe2_mesh_write.argtypes = [C.c_int, C.c_char_p]
+    L.fe2_model_build_basis.argtypes = [C.c_int, C.c_char_p, _dp, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
+    L.fe2_hf_create.argtypes = [C.c_int, C.c_int, C.c_char_p, C.POINTER(_Material), C.c_int, C.POINTER(C.c_void_p)]
+    L.fe2_hf_destroy.argtypes = [C.c_void_p]
+    L.fe2_hf_destroy.restype = None
+    L.fe2_hf_sizes.argtypes = [C.c_void_p, _ip, _ip, _ip, _dp]
+    L.fe2_hf_trajectory.argtypes = [C.c_void_p, C.c_int, _dp, C.POINTER(_Opts), _dp, _dp, _ip, _dp, _dp, _dp]
+    L.fe2_hf_elastic_modes.argtypes = [C.c_void_p, _dp, _ip]
+    L.fe2_pod_basis.argtypes = [C.c_int, _dp, C.c_int64, C.c_int, _dp, C.c_int, C.c_int, _dp, _dp, _ip]
     L.fe2_model_free.argtypes = [C.c_void_p]
     L.fe2_model_free.restype = None
     L.fe2_model_sizes.argtypes = [C.c_void_p, _ip, _ip, _ip, _dp]
@@ -193,11 +201,18 @@ class HyperRomModel:
     (mesh.hpp:185-191) — G[K,3,n], w[K], ip ids, material ids (0 matrix J2,
     1 inclusion), volume. Host only."""
 
-    def __init__(self, subdivisions=33, n=12, K=200, seed=0, mesh_file: str | None = None):
+    def __init__(self, subdivisions=33, n=12, K=200, seed=0, mesh_file: str | None = None, basis=None):
         """subdivisions: default_cell RVE; or mesh_file: an RVE in the
-        reference's plain-text mesh format (write_mesh, mesh.hpp:413-489)."""
+        reference's plain-text mesh format (write_mesh, mesh.hpp:413-489).
+        basis: optional Φ (n, n_dofs) over all DOFs (e.g. pod.pod_basis)
+        instead of the seeded orthonormal modes; n is then basis.shape[0]."""
         h = C.c_void_p()
-        if mesh_file is not None:
+        if basis is not None:
+            basis = np.ascontiguousarray(basis, dtype=np.float64)
+            n = basis.shape[0]
+            path = None if mesh_file is None else str(mesh_file).encode()
+            _check(lib.fe2_model_build_basis(subdivisions, path, _d(basis), n, K, seed, C.byref(h)))
+        elif mesh_file is not None:
             _check(lib.fe2_model_build_from_mesh(str(mesh_file).encode(), n, K, seed, C.byref(h)))
         else:
             _check(lib.fe2_model_build(subdivisions, n, K, seed, C.byref(h)))
