@@ -7,7 +7,7 @@
  * interface (paths relative to /root/reference/proj/include/fe2rom/):
  *
  *   fe2_material_update_batch  <- update_material        materials.hpp:317-325
- *                                 (batched; update4 J2/elastic :199-214)
+ *                                 (batched; update4 elastic / J2 / power law / creep :199-292)
  *   fe2_hrom_create            <- build_rve_problem      rve.hpp:167-185, in the
  *                                 reduced form of SPEC.md:351-359 (G_q = B_q Φ,
  *                                 cubature weights), materials by id (:158-162)
@@ -56,12 +56,17 @@
 extern "C" {
 #endif
 
-/* Material parameters (materials.hpp:37-49, validate :80-87).
+/* Material parameters (materials.hpp:37-76, validate :80-98).
  * kind 0: ElasticParams  p = {E, nu}
- * kind 1: J2LinearParams p = {E, nu, sigma_y0, hardening} */
+ * kind 1: J2LinearParams p = {E, nu, sigma_y0, hardening}
+ * kind 2: PowerLawParams p = {E, nu, sigma_y0, N}          sy(e) = sy0 (1 + E e / sy0)^N
+ * kind 3: CreepParams    p = {E, nu, A, n, m, dt}          deq/dt = (q/A)^(n/(m+1)) ((m+1) eq)^(m/(m+1));
+ *                        dt = time of one load increment (PathStep::dt; bisected sub-steps use their share)
+ * The hyper-ROM engines (fe2_hrom_create*) and the SoA update carry kinds 0/1;
+ * fe2_material_update_batch and the HF solver (fe2_hf_*) carry all four. */
 typedef struct {
   int kind;
-  double p[4];
+  double p[6];
 } fe2_material_t;
 
 /* MicroOptions (rve.hpp:195-200) + TrajectoryOptions::max_bisections (:439-443) */

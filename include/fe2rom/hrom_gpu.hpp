@@ -4,7 +4,8 @@
 // solve to the GPU batch without other dependencies.
 //
 // Reference names kept (paths relative to /root/reference/proj/include/fe2rom/):
-//   ElasticParams, J2LinearParams, Material       materials.hpp:37-49, :78
+//   ElasticParams, J2LinearParams, PowerLawParams,
+//   CreepParams, Material                          materials.hpp:37-78
 //   MaterialState (eps_p[4], eq, sigma33)          materials.hpp:102-106
 //   MicroOptions {tol, max_iter}                   rve.hpp:195-200
 //   TrajectoryOptions {micro, max_bisections}      rve.hpp:439-443
@@ -54,7 +55,21 @@ struct J2LinearParams {
   double sigma_y0 = 0.01;
   double hardening = 0.016;
 };
-using Material = std::variant<ElasticParams, J2LinearParams>;
+struct PowerLawParams {  // materials.hpp:51-65
+  double E = 1.0;
+  double nu = 0.3;
+  double sigma_y0 = 0.01;
+  double N = 0.1;
+};
+struct CreepParams {  // materials.hpp:67-76; dt = time of one load increment
+  double E = 1.0;
+  double nu = 0.14;
+  double A = 22.09;
+  double n = 1.06;
+  double m = -0.56;
+  double dt = 1.0;
+};
+using Material = std::variant<ElasticParams, J2LinearParams, PowerLawParams, CreepParams>;
 
 struct MaterialState {
   std::array<double, 4> eps_p{0, 0, 0, 0};
@@ -86,13 +101,27 @@ inline fe2_material_t to_c(const Material& m) {
     c.kind = 0;
     c.p[0] = e->E;
     c.p[1] = e->nu;
-  } else {
-    const auto& j = std::get<J2LinearParams>(m);
+  } else if (auto* j = std::get_if<J2LinearParams>(&m)) {
     c.kind = 1;
-    c.p[0] = j.elastic.E;
-    c.p[1] = j.elastic.nu;
-    c.p[2] = j.sigma_y0;
-    c.p[3] = j.hardening;
+    c.p[0] = j->elastic.E;
+    c.p[1] = j->elastic.nu;
+    c.p[2] = j->sigma_y0;
+    c.p[3] = j->hardening;
+  } else if (auto* pl = std::get_if<PowerLawParams>(&m)) {
+    c.kind = 2;
+    c.p[0] = pl->E;
+    c.p[1] = pl->nu;
+    c.p[2] = pl->sigma_y0;
+    c.p[3] = pl->N;
+  } else {
+    const auto& cr = std::get<CreepParams>(m);
+    c.kind = 3;
+    c.p[0] = cr.E;
+    c.p[1] = cr.nu;
+    c.p[2] = cr.A;
+    c.p[3] = cr.n;
+    c.p[4] = cr.m;
+    c.p[5] = cr.dt;
   }
   return c;
 }

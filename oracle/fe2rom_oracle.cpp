@@ -94,10 +94,14 @@ struct State {
 };
 
 struct Mat {
-  int kind = 0;  // 0 elastic, 1 J2 linear
+  int kind = 0;  // 0 elastic, 1 J2 linear, 2 power law, 3 strain-hardening creep
   double E = 1.0, nu = 0.3, sy0 = 0.01, h = 0.016;
+  double N = 0.1;                               // power law (materials.hpp:51-65)
+  double A = 22.09, n = 1.06, m = -0.56, dt = 1.0;  // creep (:67-76); dt = PathStep::dt
   double lambda() const { return E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)); }  // :49
   double mu() const { return 0.5 * E / (1.0 + nu); }                          // :50
+  double yield_stress(double eq) const { return sy0 * std::pow(1.0 + E * eq / sy0, N); }      // :59-61
+  double yield_slope(double eq) const { return E * N * std::pow(1.0 + E * eq / sy0, N - 1.0); }  // :62-64
 };
 
 inline Mat to_mat(const orc_material_t& m) {
@@ -108,12 +112,24 @@ inline Mat to_mat(const orc_material_t& m) {
   if (m.kind == 1) {
     r.sy0 = m.p[2];
     r.h = m.p[3];
+  } else if (m.kind == 2) {
+    r.sy0 = m.p[2];
+    r.N = m.p[3];
+  } else if (m.kind == 3) {
+    r.A = m.p[2];
+    r.n = m.p[3];
+    r.m = m.p[4];
+    r.dt = m.p[5];
   }
-  // validate (materials.hpp:80-87)
-  require(m.kind == 0 || m.kind == 1, ErrorCode::config, "unsupported material kind");
+  // validate (materials.hpp:80-98)
+  require(m.kind >= 0 && m.kind <= 3, ErrorCode::config, "unsupported material kind");
   require(r.E > 0.0 && r.nu >= 0.0 && r.nu < 0.5, ErrorCode::config, "invalid elastic parameters");
   if (m.kind == 1)
     require(r.sy0 > 0.0 && r.h >= 0.0, ErrorCode::config, "invalid J2 parameters");
+  if (m.kind == 2)
+    require(r.sy0 > 0.0 && r.N > 0.0 && r.N < 1.0, ErrorCode::config, "invalid power-law parameters");
+  if (m.kind == 3)
+    require(r.A > 0.0 && r.n > 0.0 && r.m > -1.0, ErrorCode::config, "invalid creep parameters");
   return r;
 }
 
@@ -153,7 +169,8 @@ inline void elastic_stress4(double l, double mu, const double* e, double* s) {  
   s[3] = 2.0 * mu * e[3];
 }
 
-// update4 for ElasticParams (:199-203) and J2LinearParams (:205-214), with
+// update4 for ElasticParams (:199-203), J2LinearParams (:205-214),
+// PowerLawParams (:216-244) and CreepParams (:246-292), with
 // trial_state (:162-169), elastic_result (:187-195), finish_return (:173-185)
 // and radial_return_tangent4 (:138-154).
 inline Result4 update4(const Mat& m, const State& s0, const double* eps) {
@@ -165,10 +182,78 @@ inline Result4 update4(const Mat& m, const State& s0, const double* eps) {
   dev4(sig_tr, s_tr);
   const double q_tr = std::sqrt(1.5) * norm4(s_tr);
   bool plastic = false;
-  double f = 0.0;
-  if (m.kind == 1) {
-    f = q_tr - (m.sy0 + m.h * s0.eq);
+  double dlam = 0.0, dlam_dqtr = 0.0;
+  if (m.kind == 1) {  // closed form (:205-214)
+    const double f = q_tr - (m.sy0 + m.h * s0.eq);
     plastic = !(f <= 0.0);
+    const double denom = 3.0 * mu + m.h;
+    dlam = f / denom;
+    dlam_dqtr = 1.0 / denom;
+  } else if (m.kind == 2) {  // power law: safeguarded Newton on g (:216-244)
+    const double f_tr = q_tr - m.yield_stress(s0.eq);
+    if (!(f_tr <= 0.0)) {
+      auto g = [&](double x) { return q_tr - 3.0 * mu * x - m.yield_stress(s0.eq + x); };
+      double lo = 0.0, hi = f_tr / (3.0 * mu), x = hi * 0.5;
+      const double tol = 1e-12 * std::max(m.sy0, q_tr);
+      bool converged = false;
+      for (int it = 0; it < 50; ++it) {
+        const double gx = g(x);
+        if (std::abs(gx) <= tol) {
+          converged = true;
+          break;
+        }
+        if (gx > 0.0) lo = x;
+        else hi = x;
+        const double slope = 3.0 * mu + m.yield_slope(s0.eq + x);
+        double next = x + gx / slope;
+        if (!(next > lo && next < hi)) next = 0.5 * (lo + hi);
+        x = next;
+      }
+      require(converged, ErrorCode::material, "power-law return map did not converge");
+      plastic = true;
+      dlam = x;
+      dlam_dqtr = 1.0 / (3.0 * mu + m.yield_slope(s0.eq + x));
+    }
+  } else if (m.kind == 3) {  // strain-hardening creep: safeguarded Newton on R (:246-292)
+    require(m.dt > 0.0, ErrorCode::material, "creep update needs dt > 0");
+    if (q_tr > 1e-14 * m.E) {
+      const double p1 = m.n / (m.m + 1.0), p2 = m.m / (m.m + 1.0), eq_floor = 1e-12;
+      auto hard = [&](double e) { return std::pow((m.m + 1.0) * std::max(e, eq_floor), p2); };
+      auto hard_slope = [&](double e) {
+        if (e <= eq_floor) return 0.0;
+        return p2 * (m.m + 1.0) * std::pow((m.m + 1.0) * e, p2 - 1.0);
+      };
+      auto rate_q = [&](double q) { return std::pow(q / m.A, p1); };
+      auto rate_q_slope = [&](double q) { return p1 / m.A * std::pow(q / m.A, p1 - 1.0); };
+      auto R = [&](double x) { return x - m.dt * rate_q(q_tr - 3.0 * mu * x) * hard(s0.eq + x); };
+      double lo = 0.0, hi = q_tr / (3.0 * mu);
+      require(!(R(hi) < 0.0), ErrorCode::material, "creep return bracket failure");
+      double x = 0.5 * hi;
+      const double tol = 1e-14 * std::max(1.0, hi);
+      bool converged = false;
+      double Rp = 1.0;
+      for (int it = 0; it < 200; ++it) {
+        const double q = q_tr - 3.0 * mu * x;
+        const double e = s0.eq + x;
+        const double Rx = x - m.dt * rate_q(q) * hard(e);
+        Rp = 1.0 + 3.0 * mu * m.dt * rate_q_slope(q) * hard(e) - m.dt * rate_q(q) * hard_slope(e);
+        if (std::abs(Rx) <= tol) {
+          converged = true;
+          break;
+        }
+        if (Rx < 0.0) lo = x;
+        else hi = x;
+        double next = (Rp > 0.0) ? x - Rx / Rp : 0.5 * (lo + hi);
+        if (!(next > lo && next < hi)) next = 0.5 * (lo + hi);
+        x = next;
+      }
+      require(converged, ErrorCode::material, "creep return map did not converge");
+      if (x > 0.0) {
+        plastic = true;
+        dlam = x;
+        dlam_dqtr = m.dt * rate_q_slope(q_tr - 3.0 * mu * x) * hard(s0.eq + x) / Rp;
+      }
+    }
   }
   if (!plastic) {
     for (int i = 0; i < 4; ++i) out.sigma[i] = sig_tr[i];
@@ -178,9 +263,6 @@ inline Result4 update4(const Mat& m, const State& s0, const double* eps) {
     out.plastic = false;
     return out;
   }
-  const double denom = 3.0 * mu + m.h;
-  const double dlam = f / denom;
-  const double dlam_dqtr = 1.0 / denom;
   double dir[4];
   for (int i = 0; i < 4; ++i) dir[i] = s_tr[i] / q_tr;
   const double c_sig = 3.0 * mu * dlam;
@@ -534,6 +616,7 @@ struct HfProblem {
   std::vector<std::array<double, 36>> B;  // per ip
   std::vector<double> w;                   // per ip
   double volume = 0.0;
+  double dt_scale = 1.0;  // fraction of the increment's dt (bisected sub-steps, rve.hpp:466)
 };
 
 inline HfProblem build_hf(const Mesh& mesh, const std::vector<Mat>& mats) {  // rve.hpp:167-185
@@ -602,7 +685,9 @@ inline void hf_assemble(const HfProblem& p, const std::vector<double>& u_full,
         for (int c = 0; c < 12; ++c) s += B[r * 12 + c] * u_el[c];
         eps[r] = s;
       }
-      const Result3 res = update_material(p.mats[el.mat], s0[ip], eps);
+      Mat mat = p.mats[el.mat];
+      mat.dt *= p.dt_scale;
+      const Result3 res = update_material(mat, s0[ip], eps);
       scratch.states[ip] = res.state;
       for (int i = 0; i < 3; ++i) scratch.sigma[ip][i] = res.sigma[i];
       for (int i = 0; i < 3; ++i)
@@ -1693,7 +1778,7 @@ int orc_hf_trajectory(orc_mesh_t m, const orc_material_t* mats, int n_mats, int 
   return guarded([&] {
     std::vector<Mat> ms;
     for (int i = 0; i < n_mats; ++i) ms.push_back(to_mat(mats[i]));
-    const HfProblem p = build_hf(m->mesh, ms);
+    HfProblem p = build_hf(m->mesh, ms);
     const int nf = p.dm.n_free;
     std::vector<State> states(p.mesh.n_ips());
     std::vector<double> u_free(nf, 0.0);
@@ -1711,6 +1796,7 @@ int orc_hf_trajectory(orc_mesh_t m, const orc_material_t* mats, int n_mats, int 
         std::vector<double> u0(nf);
         for (int i = 0; i < p.mesh.n_dofs(); ++i)
           if (p.dm.free_index[i] >= 0) u0[p.dm.free_index[i]] = u_free[p.dm.free_index[i]] + aff[i];
+        p.dt_scale = target - done;
         HfSolve r = hf_newton(p, Ev, states, u0, opts->tol, opts->max_iter);
         its += r.iterations;
         if (!r.converged) {

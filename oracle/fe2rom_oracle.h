@@ -31,11 +31,13 @@
 extern "C" {
 #endif
 
-/* material kinds: 0 = ElasticParams {E, nu}, 1 = J2LinearParams {E, nu, sy0, h}
- * (materials.hpp:37-49). */
+/* material kinds (materials.hpp:37-76): 0 = ElasticParams {E, nu},
+ * 1 = J2LinearParams {E, nu, sy0, h}, 2 = PowerLawParams {E, nu, sy0, N},
+ * 3 = CreepParams {E, nu, A, n, m, dt} (dt: time of one load increment,
+ * PathStep::dt; bisected sub-steps use their fraction of it). */
 typedef struct {
   int kind;
-  double p[4];
+  double p[6];
 } orc_material_t;
 
 const char* orc_last_error(void);

@@ -26,7 +26,7 @@ class OracleError(RuntimeError):
 
 
 class _Mat(C.Structure):
-    _fields_ = [("kind", C.c_int), ("p", C.c_double * 4)]
+    _fields_ = [("kind", C.c_int), ("p", C.c_double * 6)]
 
 
 class _Opts(C.Structure):
@@ -98,14 +98,20 @@ def _i(a):
 
 
 def mat_struct(m):
-    """m: ('elastic', E, nu) | ('j2', E, nu, sy0, h) or an object with kind fields."""
-    if hasattr(m, "sigma_y0"):
-        return _Mat(1, (C.c_double * 4)(m.E, m.nu, m.sigma_y0, m.hardening))
+    """m: ('elastic', E, nu) | ('j2', E, nu, sy0, h) | ('powerlaw', E, nu, sy0, N)
+    | ('creep', E, nu, A, n, m, dt), or an object with the product's fields."""
+    def mk(kind, *p):
+        return _Mat(kind, (C.c_double * 6)(*(list(p) + [0.0] * (6 - len(p)))))
+    if hasattr(m, "hardening"):
+        return mk(1, m.E, m.nu, m.sigma_y0, m.hardening)
+    if hasattr(m, "N"):
+        return mk(2, m.E, m.nu, m.sigma_y0, m.N)
+    if hasattr(m, "A"):
+        return mk(3, m.E, m.nu, m.A, m.n, m.m, m.dt)
     if hasattr(m, "E"):
-        return _Mat(0, (C.c_double * 4)(m.E, m.nu, 0.0, 0.0))
-    if m[0] == "j2":
-        return _Mat(1, (C.c_double * 4)(*m[1:5]))
-    return _Mat(0, (C.c_double * 4)(m[1], m[2], 0.0, 0.0))
+        return mk(0, m.E, m.nu)
+    kinds = {"elastic": 0, "j2": 1, "powerlaw": 2, "creep": 3}
+    return mk(kinds[m[0]], *m[1:])
 
 
 class Rng:

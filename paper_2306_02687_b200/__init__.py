@@ -10,12 +10,14 @@ Python mirror of the reference's material-point and solver interface
 no CPU fallback: without the library or a B200, calls raise.
 """
 from .hrom import (  # noqa: F401
+    CreepParams,
     ElasticParams,
     Fe2Error,
     HyperRomEngine,
     HyperRomModel,
     J2LinearParams,
     NewtonOptions,
+    PowerLawParams,
     device_count,
     lib,
     make_paths,
@@ -27,6 +29,8 @@ from .fe2 import MacroConfig, macro_gauss, macro_points, solve_program  # noqa: 
 from .pod import HfRve, pod_basis  # noqa: F401
 
 __all__ = [
+    "CreepParams",
+    "PowerLawParams",
     "ElasticParams",
     "Fe2Error",
     "HyperRomEngine",

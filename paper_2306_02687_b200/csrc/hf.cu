@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(144) k_hf_element(int n_el, const int* __restr
                                                     const double* __restrict__ u, const double* __restrict__ st0,
                                                     int with_K, double* __restrict__ f_el, double* __restrict__ k_el,
                                                     double* __restrict__ st_out, double* __restrict__ sig_out,
-                                                    double* __restrict__ C_out) {
+                                                    double* __restrict__ C_out, int* __restrict__ err) {
   const int e = blockIdx.x, t = threadIdx.x;
   if (e >= n_el) return;
   __shared__ double sB[3][36], sS[3][3], sC[3][9], sW[3];
@@ -132,7 +132,10 @@ __global__ void __launch_bounds__(144) k_hf_element(int n_el, const int* __restr
       eps[r] = s;
     }
     const double* s0 = st0 + (size_t)6 * ip;
-    const MatOut o = update_material(mats.m[phase[e]], s0[0], s0[1], s0[2], s0[3], s0[4], eps[0], eps[1], eps[2]);
+    bool ok = true;
+    const MatOut o =
+        update_material_any(mats.m[phase[e]], s0[0], s0[1], s0[2], s0[3], s0[4], eps[0], eps[1], eps[2], ok);
+    if (!ok) atomicExch(err, 1);
     sS[t][0] = o.s0;
     sS[t][1] = o.s1;
     sS[t][2] = o.s2;
@@ -224,6 +227,7 @@ struct fe2_hf_s {
   cusolverDnHandle_t sol = nullptr;
   int *d_conn = nullptr, *d_phase = nullptr, *d_free = nullptr, *d_inc_ptr = nullptr, *d_inc = nullptr;
   int* d_info = nullptr;
+  int* d_err = nullptr;  // set by k_hf_element when a return map fails
   double *d_B = nullptr, *d_w = nullptr, *d_u = nullptr, *d_st0 = nullptr, *d_st1 = nullptr;
   double *d_fel = nullptr, *d_kel = nullptr, *d_f = nullptr, *d_K = nullptr, *d_sig = nullptr, *d_C = nullptr;
   double *d_rhs = nullptr, *d_work = nullptr;
@@ -236,7 +240,7 @@ struct fe2_hf_s {
   ~fe2_hf_s() {
     if (sol) Cusolver::get().destroy(sol);
     if (stream) cudaStreamDestroy(stream);
-    for (int* p : {d_conn, d_phase, d_free, d_inc_ptr, d_inc, d_info})
+    for (int* p : {d_conn, d_phase, d_free, d_inc_ptr, d_inc, d_info, d_err})
       if (p) cudaFree(p);
     for (double* p : {d_B, d_w, d_u, d_st0, d_st1, d_fel, d_kel, d_f, d_K, d_sig, d_C, d_rhs, d_work})
       if (p) cudaFree(p);
@@ -257,14 +261,17 @@ struct fe2_hf_s {
     CK(cudaMemcpyAsync(d_u, u_full.data(), sizeof(double) * nd(), cudaMemcpyHostToDevice, stream));
     if (with_K) CK(cudaMemsetAsync(d_K, 0, sizeof(double) * nf() * nf(), stream));
     k_hf_element<<<r.n_el, 144, 0, stream>>>(r.n_el, d_conn, d_phase, mt, d_B, d_w, d_u, d_st0, with_K ? 1 : 0,
-                                             d_fel, d_kel, d_st1, d_sig, d_C);
+                                             d_fel, d_kel, d_st1, d_sig, d_C, d_err);
     CK(cudaGetLastError());
     k_hf_gather<<<(nd() + 127) / 128, 128, 0, stream>>>(nd(), d_inc_ptr, d_inc, d_conn, d_free, nf(), d_fel, d_kel,
                                                         with_K ? 1 : 0, d_f, d_K);
     CK(cudaGetLastError());
     f_full.resize(nd());
     CK(cudaMemcpyAsync(f_full.data(), d_f, sizeof(double) * nd(), cudaMemcpyDeviceToHost, stream));
+    int err = 0;
+    CK(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    check(err == 0, Code::material, "material return map did not converge");
     if (with_K) factored = false;
   }
 
@@ -426,6 +433,7 @@ struct fe2_hf_s {
                   double* sigma, double* C, int* iterations, double* u_fluct_inf, double* res_last, double* snaps) {
     const int n = nf(), N = nd();
     CK(cudaMemsetAsync(d_st0, 0, sizeof(double) * 6 * r.n_ips(), stream));
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
     std::vector<double> u_free(n, 0.0), aff, u0(n);
     double E_prev[3] = {0, 0, 0}, E_comm[3] = {0, 0, 0};
     for (int k = 0; k < n_steps; ++k) {
@@ -439,7 +447,9 @@ struct fe2_hf_s {
         affine(dE, aff);
         for (int i = 0; i < N; ++i)
           if (r.free_index[i] >= 0) u0[r.free_index[i]] = u_free[r.free_index[i]] + aff[i];
-        Newton res = newton(Ev, u0, tol, max_iter, mt);
+        MatTable ms = mt;  // creep: the sub-step's fraction of the increment's dt (rve.hpp:466)
+        for (MatDev& md : ms.m) md.dt *= target - done;
+        Newton res = newton(Ev, u0, tol, max_iter, ms);
         its += res.iterations;
         if (!res.converged) {
           check(++bis <= max_bisections, Code::solver, "micro trajectory failed after max bisections");
@@ -527,6 +537,8 @@ int fe2_hf_create(int device, int subdivisions, const char* mesh_path, const fe2
     up_d(h->d_B, r.B);
     up_d(h->d_w, r.w);
     h->d_info = dalloc<int>(1);
+    h->d_err = dalloc<int>(1);
+    CK(cudaMemset(h->d_err, 0, sizeof(int)));
     h->d_u = dalloc<double>(N);
     h->d_f = dalloc<double>(N);
     h->d_st0 = dalloc<double>((size_t)6 * r.n_ips());

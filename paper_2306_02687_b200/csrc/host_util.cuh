@@ -41,12 +41,23 @@ inline void require_device(int device) {
   CK(cudaSetDevice(device));
 }
 
-inline MatDev to_dev(const fe2_material_t& m) {
-  check(m.kind == 0 || m.kind == 1, Code::config, "unsupported material kind");
+inline MatDev to_dev(const fe2_material_t& m) {  // validate, materials.hpp:80-98
+  check(m.kind >= 0 && m.kind <= 3, Code::config, "unsupported material kind");
   const double E = m.p[0], nu = m.p[1];
-  check(E > 0.0 && nu >= 0.0 && nu < 0.5, Code::config, "invalid elastic parameters");            // materials.hpp:80-82
-  if (m.kind == 1) check(m.p[2] > 0.0 && m.p[3] >= 0.0, Code::config, "invalid J2 parameters");  // :83-87
+  check(E > 0.0 && nu >= 0.0 && nu < 0.5, Code::config, "invalid elastic parameters");
+  if (m.kind == 1) check(m.p[2] > 0.0 && m.p[3] >= 0.0, Code::config, "invalid J2 parameters");
+  if (m.kind == 2)
+    check(m.p[2] > 0.0 && m.p[3] > 0.0 && m.p[3] < 1.0, Code::config, "invalid power-law parameters");
+  if (m.kind == 3) check(m.p[2] > 0.0 && m.p[3] > 0.0 && m.p[4] > -1.0, Code::config, "invalid creep parameters");
+  if (m.kind >= 2) return make_mat_general(m.kind, E, nu, m.p + 2);
   return make_mat(m.kind, E, nu, m.kind == 1 ? m.p[2] : 0.0, m.kind == 1 ? m.p[3] : 0.0);
+}
+
+// The hyper-ROM engines carry the closed-form J2 / elastic points only.
+inline void require_engine_material(const MatDev& m) {
+  check(m.kind <= 1, Code::config,
+        "the hyper-ROM engine supports elastic and J2 materials; power-law / creep run through "
+        "fe2_material_update_batch and the HF solver");
 }
 
 }  // namespace fe2

@@ -370,10 +370,15 @@ int fe2_material_update_batch(int device, const fe2_material_t* mat, int64_t N, 
     double *d_sig = dalloc<double>(N * 3), *d_C = dalloc<double>(N * 9);
     double* d_out = state_out ? dalloc<double>(N * 6) : nullptr;
     uint8_t* d_pl = plastic ? dalloc<uint8_t>(N) : nullptr;
+    int* d_err = dalloc<int>(1);
+    CK(cudaMemset(d_err, 0, sizeof(int)));
     CK(cudaMemcpy(d_eps, eps, N * 3 * sizeof(double), cudaMemcpyHostToDevice));
     if (state_in) CK(cudaMemcpy(d_in, state_in, N * 6 * sizeof(double), cudaMemcpyHostToDevice));
-    launch_material_batch(m, N, d_eps, d_in, d_sig, d_C, d_out, d_pl, nullptr);
+    launch_material_batch(m, N, d_eps, d_in, d_sig, d_C, d_out, d_pl, d_err, nullptr);
     CK(cudaGetLastError());
+    int err = 0;
+    CK(cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    dfree(d_err);
     CK(cudaMemcpy(sigma, d_sig, N * 3 * sizeof(double), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(C, d_C, N * 9 * sizeof(double), cudaMemcpyDeviceToHost));
     if (state_out) CK(cudaMemcpy(state_out, d_out, N * 6 * sizeof(double), cudaMemcpyDeviceToHost));
@@ -384,6 +389,8 @@ int fe2_material_update_batch(int device, const fe2_material_t* mat, int64_t N, 
     dfree(d_C);
     dfree(d_out);
     dfree(d_pl);
+    check(err == 0, Code::material, m.kind == 2 ? "power-law return map did not converge"
+                                                : "creep return map did not converge (or dt <= 0)");
   });
 }
 
@@ -393,6 +400,7 @@ int fe2_material_update_soa_device(int device, const fe2_material_t* mat, int64_
   return guard([&] {
     check(mat && d_eps && d_sigma && d_C6 && N >= 0, Code::config, "bad arguments");
     const MatDev m = to_dev(*mat);
+    check(m.kind <= 1, Code::config, "the SoA device update supports elastic and J2 materials");
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
       throw Failure(Code::numeric, "no CUDA device available: the B200 engine has no CPU fallback");
@@ -415,7 +423,10 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
     check(n <= 128, Code::config, "this build supports n <= 128 modes");
     check(volume > 0.0, Code::config, "RVE volume must be positive");
     std::vector<MatDev> md;
-    for (int i = 0; i < n_mats; ++i) md.push_back(to_dev(mats[i]));
+    for (int i = 0; i < n_mats; ++i) {
+      md.push_back(to_dev(mats[i]));
+      require_engine_material(md.back());
+    }
     require_device(device);
     auto h = new fe2_hrom_s;
     try {
@@ -892,7 +903,10 @@ int fe2_hrom_create_fs(int device, int n, int K, const double* G4, const double*
     check(n <= 32, Code::config, "the finite-strain path supports n <= 32 modes");
     check(volume > 0.0, Code::config, "RVE volume must be positive");
     std::vector<MatDev> md;
-    for (int i = 0; i < n_mats; ++i) md.push_back(to_dev(mats[i]));
+    for (int i = 0; i < n_mats; ++i) {
+      md.push_back(to_dev(mats[i]));
+      require_engine_material(md.back());
+    }
     require_device(device);
     auto h = new fe2_hrom_s;
     try {

@@ -1049,13 +1049,16 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
 }
 
 __global__ void k_material_batch(MatDev m, int64_t N, const double* eps, const double* st_in, double* sigma,
-                                 double* C, double* st_out, uint8_t* plastic) {
+                                 double* C, double* st_out, uint8_t* plastic, int* err) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= N) return;
   double s[5] = {0, 0, 0, 0, 0};
   if (st_in)
     for (int c = 0; c < 5; ++c) s[c] = st_in[i * 6 + c];
-  const MatOut o = update_material(m, s[0], s[1], s[2], s[3], s[4], eps[i * 3], eps[i * 3 + 1], eps[i * 3 + 2]);
+  bool ok = true;
+  const MatOut o =
+      update_material_any(m, s[0], s[1], s[2], s[3], s[4], eps[i * 3], eps[i * 3 + 1], eps[i * 3 + 2], ok);
+  if (!ok && err) atomicExch(err, 1);
   sigma[i * 3 + 0] = o.s0;
   sigma[i * 3 + 1] = o.s1;
   sigma[i * 3 + 2] = o.s2;
@@ -1139,10 +1142,10 @@ void launch_increment(const IncArgs& a, int num_sms, cudaStream_t s) {
 }
 
 void launch_material_batch(const MatDev& m, int64_t N, const double* eps, const double* st_in, double* sigma,
-                           double* C, double* st_out, uint8_t* plastic, cudaStream_t s) {
+                           double* C, double* st_out, uint8_t* plastic, int* err, cudaStream_t s) {
   const int threads = 256;
   const unsigned grid = static_cast<unsigned>((N + threads - 1) / threads);
-  k_material_batch<<<grid, threads, 0, s>>>(m, N, eps, st_in, sigma, C, st_out, plastic);
+  k_material_batch<<<grid, threads, 0, s>>>(m, N, eps, st_in, sigma, C, st_out, plastic, err);
 }
 
 }  // namespace fe2

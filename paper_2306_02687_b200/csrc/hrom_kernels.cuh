@@ -111,7 +111,7 @@ void launch_increment(const IncArgs& a, int num_sms, cudaStream_t s);
 bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s);
 size_t increment_big_smem(int NP);
 void launch_material_batch(const MatDev& m, int64_t N, const double* eps, const double* st_in, double* sigma,
-                           double* C, double* st_out, uint8_t* plastic, cudaStream_t s);
+                           double* C, double* st_out, uint8_t* plastic, int* err, cudaStream_t s);
 size_t increment_smem(int NP);
 // batched constitutive update on SoA device buffers (material_soa.cu)
 void launch_material_soa(const MatDev& m, int64_t N, const double* eps, const double* hin, double* sig, double* C6,

@@ -33,7 +33,7 @@ class Fe2Error(RuntimeError):
 
 
 class _Material(C.Structure):
-    _fields_ = [("kind", C.c_int), ("p", C.c_double * 4)]
+    _fields_ = [("kind", C.c_int), ("p", C.c_double * 6)]
 
 
 class _Opts(C.Structure):
@@ -145,7 +145,7 @@ class ElasticParams:  # materials.hpp:37-43
     nu: float = 0.3
 
     def _c(self):
-        return _Material(0, (C.c_double * 4)(self.E, self.nu, 0.0, 0.0))
+        return _Material(0, (C.c_double * 6)(self.E, self.nu, 0.0, 0.0, 0.0, 0.0))
 
 
 @dataclass
@@ -156,7 +156,31 @@ class J2LinearParams:  # materials.hpp:45-49
     hardening: float = 0.016
 
     def _c(self):
-        return _Material(1, (C.c_double * 4)(self.E, self.nu, self.sigma_y0, self.hardening))
+        return _Material(1, (C.c_double * 6)(self.E, self.nu, self.sigma_y0, self.hardening, 0.0, 0.0))
+
+
+@dataclass
+class PowerLawParams:  # materials.hpp:51-65: sy(e) = sy0 (1 + E e / sy0)^N
+    E: float = 1.0
+    nu: float = 0.3
+    sigma_y0: float = 0.01
+    N: float = 0.1
+
+    def _c(self):
+        return _Material(2, (C.c_double * 6)(self.E, self.nu, self.sigma_y0, self.N, 0.0, 0.0))
+
+
+@dataclass
+class CreepParams:  # materials.hpp:67-76; dt = time of one load increment (PathStep::dt)
+    E: float = 1.0
+    nu: float = 0.14
+    A: float = 22.09
+    n: float = 1.06
+    m: float = -0.56
+    dt: float = 1.0
+
+    def _c(self):
+        return _Material(3, (C.c_double * 6)(self.E, self.nu, self.A, self.n, self.m, self.dt))
 
 
 @dataclass
