@@ -219,7 +219,8 @@ typedef struct {
   double tol;                 /* macro residual tolerance relative to max(|f_int|, largest accepted |f_int|) (1e-6) */
   int max_iter;               /* macro Newton iterations per step (20) */
   int max_bisections;         /* macro step bisections (4) */
-  fe2_newton_opts_t micro;    /* micro Newton options */
+  fe2_newton_opts_t micro;    /* micro Newton options (monolithic: micro.tol = the joint micro tolerance) */
+  int scheme;                 /* 0 = nested (converged micro solves per macro iteration), 1 = monolithic */
 } fe2_macro_config_t;
 int fe2_macro_points(const fe2_macro_config_t* cfg, int64_t* n_points);
 /* per macro Gauss point: B[36] (3 x 12 strain operator), w, element (nullable) */
@@ -227,6 +228,27 @@ int fe2_macro_gauss(const fe2_macro_config_t* cfg, double* B, double* w, int* el
 /* rows[k] = (U, R, macro iterations of the step, cumulative micro iterations, wall ms) */
 int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows, int max_rows, int* n_rows,
                   double* u_residual);
+
+/* ---- monolithic scheme (SPEC.md:474-481 HF_monolithic / hyper-ROM): the
+ * micro problems advance ONE reduced Newton iteration per macro iteration,
+ * sharing the macro linearisation. Small-strain handles, n <= 32.
+ *   fe2_hrom_mono_begin     start a macro step from the committed state
+ *                           (α = α_committed; history candidates discarded)
+ *   fe2_hrom_mono_iterate   for every point at this macro iterate's E[P*3]:
+ *                           α -= K^-1 (r + K_aE ΔE) with the previous iteration's
+ *                           factors (ΔE = change of E since then), assemble at
+ *                           (E, α), factor, and return the condensed stress
+ *                           Σ~ = (Σ_raw - K_Eα K^-1 r)/V, C = (C_EE - K_Eα K^-1 K_aE)/V,
+ *                           rel_res = |r| / max(|r| at the step's first
+ *                           iteration, |Σ_raw| now, 1e-30), plastic counts and
+ *                           status (5 = solver: singular K_αα)
+ *   fe2_hrom_mono_commit    adopt the last iterate (α, history) as committed
+ * The caller accepts a step when its macro residual and every rel_res are
+ * below tolerance (fe2_macro_run with scheme = 1). */
+int fe2_hrom_mono_begin(fe2_hrom_t h);
+int fe2_hrom_mono_iterate(fe2_hrom_t h, const double* E, double* sigma, double* C, double* rel_res,
+                          int* plastic_count, int* status);
+int fe2_hrom_mono_commit(fe2_hrom_t h);
 
 /* ---- Empirical Cubature Method (SPEC.md:333-369
  * hyper.ecm_select), host only: U[m][k] = orthonormal integrand modes at the m

@@ -1902,7 +1902,7 @@ int orc_hrom_run(orc_hrom_t h, int64_t P, int n_incr, const double* E, const orc
 }
 
 int orc_hrom_assemble(orc_hrom_t h, const double* alpha, const double* E, const double* state, double* r,
-                      double* Kaa, double* KaE, double* C_EE, double* S_raw, int* plastic_count) {
+                      double* Kaa, double* KaE, double* C_EE, double* S_raw, int* plastic_count, double* state_out) {
   return guarded([&] {
     std::vector<State> s0(h->h.K);
     if (state)
@@ -1915,6 +1915,8 @@ int orc_hrom_assemble(orc_hrom_t h, const double* alpha, const double* E, const 
     std::memcpy(C_EE, A.C_EE, sizeof A.C_EE);
     std::memcpy(S_raw, A.S_raw, sizeof A.S_raw);
     if (plastic_count) *plastic_count = A.plastic_count;
+    if (state_out)
+      for (int q = 0; q < h->h.K; ++q) pack_state(A.states[q], state_out + (size_t)q * 6);
   });
 }
 

@@ -135,10 +135,11 @@ int orc_hrom_run(orc_hrom_t h, int64_t P, int n_incr, const double* E,
                  const orc_newton_opts_t* opts, int n_threads, orc_hrom_out_t* out);
 
 /* One assembly (hyper_assemble) at (α, E) from a given per-point history
- * state[K][6]: r[n], K[n][n], KaE[n][3], C_EE[9], S_raw[3]. */
+ * state[K][6]: r[n], K[n][n], KaE[n][3], C_EE[9], S_raw[3]; state_out[K][6]
+ * (nullable) = the updated history of that assembly. */
 int orc_hrom_assemble(orc_hrom_t h, const double* alpha, const double* E, const double* state,
                       double* r, double* Kaa, double* KaE, double* C_EE, double* S_raw,
-                      int* plastic_count);
+                      int* plastic_count, double* state_out);
 
 /* ---- finite strain, Biot stress (BASELINE config 2) — PARITY UNPINNED:
  * the reference has no finite-strain code. Components ordered (F00, F01,

@@ -77,8 +77,66 @@ class ReplayEngine:
         self.path.append(np.array(E))
 
 
-def solve_program(m, engine: ReplayEngine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, n_load=10, max_unload=30,
-                  tol=1e-6, max_iter=20, max_bisections=4):
+class MonoEngine:
+    """Monolithic scheme: one reduced Newton iteration of
+    every point per macro iteration, micro condensed (same algebra as
+    fe2_hrom_mono_*): α -= K⁻¹(r + K_aE ΔE) with the previous iteration's
+    factors, assemble at (E, α) from the committed history, return
+    Σ~ = (Σ_raw − K_Eα K⁻¹ r)/V, C = (C_EE − K_Eα K⁻¹ K_aE)/V and |r|/ref with
+    ref = max(|r| at the step's first iteration, |Σ_raw| now, 1e-30) — the
+    current stress scale, since E itself moves during a monolithic step."""
+
+    def __init__(self, hrom: O.Hrom, P, volume):
+        self.h, self.P, self.V = hrom, P, volume
+        n, K = hrom.n, hrom.K
+        self.alpha_c = np.zeros((P, n))
+        self.state_c = np.zeros((P, K, 6))
+        self.first = True
+
+    def begin(self):
+        self.first = True
+
+    def iterate(self, E):
+        P, n, V = self.P, self.h.n, self.V
+        if self.first:
+            self.alpha_w = self.alpha_c.copy()
+            self.ref = np.zeros(P)
+        else:
+            dE = E - self.E_w
+            self.alpha_w = self.alpha_w - (self.zr + np.einsum("pai,pi->pa", self.Z, dE))
+        self.zr, self.Z, self.E_w = np.zeros((P, n)), np.zeros((P, n, 3)), np.array(E, dtype=float)
+        self.state_w = np.zeros_like(self.state_c)
+        sig, Cm, rel, st = np.zeros((P, 3)), np.zeros((P, 3, 3)), np.zeros(P), np.zeros(P, dtype=int)
+        for p in range(P):
+            a = self.h.assemble(self.alpha_w[p], E[p], self.state_c[p])
+            rn = np.linalg.norm(a["r"])
+            if self.first:
+                self.ref[p] = rn  # the step's initial micro residual
+            ref = max(self.ref[p], np.linalg.norm(a["S_raw"]), 1e-30)
+            try:
+                L = np.linalg.cholesky(a["Kaa"])
+            except np.linalg.LinAlgError:
+                st[p] = 5
+                continue
+            solve = lambda b: np.linalg.solve(L.T, np.linalg.solve(L, b))  # noqa: E731
+            self.zr[p] = solve(a["r"])
+            self.Z[p] = solve(a["KaE"])
+            q = a["KaE"].T @ self.Z[p]
+            Cm[p] = (a["C_EE"] - 0.5 * (q + q.T)) / V
+            sig[p] = (a["S_raw"] - a["KaE"].T @ self.zr[p]) / V
+            rel[p] = rn / ref
+            self.state_w[p] = a["state"]
+        self.first = False
+        return dict(sigma=sig, C=Cm, rel_res=rel, status=st)
+
+    def commit(self):
+        self.alpha_c = self.alpha_w.copy()
+        self.state_c = self.state_w.copy()
+        self.first = True
+
+
+def solve_program(m, engine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, n_load=10, max_unload=30,
+                  tol=1e-6, max_iter=20, max_bisections=4, micro_tol=1e-8):
     """Same algorithm as fe2_macro_run. Returns rows (U, R, macro iters,
     cumulative micro iters) and U_residual."""
     beam = build_beam(L, H, nx, ny) if m is None else m
@@ -101,14 +159,23 @@ def solve_program(m, engine: ReplayEngine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, 
     edofs = np.array([[2 * t[d // 2] + d % 2 for d in range(12)] for t in tri])
     gdofs = edofs[elem]  # (P, 12)
     u = np.zeros(nd)
-    state = dict(micro=0, fint=np.zeros(nd), E=None, fscale=0.0)
+    state = dict(micro=0, fint=np.zeros(nd), E=None, fscale=0.0, micro_ok=True)
+
+    mono = isinstance(engine, MonoEngine)
 
     def micro_solve():
         E = np.einsum("gid,gd->gi", B, u[gdofs])
-        out = engine.solve(E)
-        if (out["status"] != 0).any():
-            return None
-        state["micro"] += int(out["iters"].sum())
+        if mono:
+            out = engine.iterate(E)
+            if (out["status"] != 0).any():
+                return None
+            state["micro"] += P
+            state["micro_ok"] = bool((out["rel_res"] <= micro_tol).all())
+        else:
+            out = engine.solve(E)
+            if (out["status"] != 0).any():
+                return None
+            state["micro"] += int(out["iters"].sum())
         fint = np.zeros(nd)
         np.add.at(fint, gdofs, w[:, None] * np.einsum("gid,gi->gd", B, out["sigma"]))
         state["fint"], state["E"] = fint, E
@@ -117,13 +184,15 @@ def solve_program(m, engine: ReplayEngine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, 
     def macro_step(U):
         for n_ in beam["tip"]:
             u[2 * n_ + 1] = U
+        if mono:
+            engine.begin()
         for k in range(max_iter + 1):
             out = micro_solve()
             if out is None:
                 return -1
             fint = state["fint"]
             rn, fn = np.linalg.norm(fint[free]), np.linalg.norm(fint)
-            if rn <= tol * max(fn, state["fscale"], 1e-30):
+            if rn <= tol * max(fn, state["fscale"], 1e-30) and (not mono or state["micro_ok"]):
                 return k
             if k == max_iter:
                 return -1
@@ -153,7 +222,10 @@ def solve_program(m, engine: ReplayEngine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, 
                 frac *= 0.5
                 continue
             iters += k
-            engine.commit(state["E"])
+            if mono:
+                engine.commit()
+            else:
+                engine.commit(state["E"])
             state["fscale"] = max(state["fscale"], np.linalg.norm(state["fint"]))
             done_state["U"], done_state["u"] = U, u.copy()
             done = target

@@ -77,7 +77,7 @@ def _load():
                                   C.POINTER(C.c_void_p)]
     L.orc_hrom_free.argtypes = [C.c_void_p]
     L.orc_hrom_run.argtypes = [C.c_void_p, C.c_int64, C.c_int, _dp, C.POINTER(_Opts), C.c_int, C.POINTER(_Out)]
-    L.orc_hrom_assemble.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _ip]
+    L.orc_hrom_assemble.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _ip, _dp]
     return L
 
 
@@ -265,9 +265,10 @@ class Hrom:
         E = np.ascontiguousarray(E, dtype=np.float64)
         st = None if state is None else np.ascontiguousarray(state, dtype=np.float64)
         r, Kaa, KaE, CEE, S, pc = np.empty(n), np.empty((n, n)), np.empty((n, 3)), np.empty((3, 3)), np.empty(3), C.c_int()
+        so = np.empty((self.K, 6))
         _check(lib.orc_hrom_assemble(self._h, _d(alpha), _d(E), _d(st), _d(r), _d(Kaa), _d(KaE), _d(CEE), _d(S),
-                                     C.byref(pc)))
-        return dict(r=r, Kaa=Kaa, KaE=KaE, C_EE=CEE, S_raw=S, plastic_count=pc.value)
+                                     C.byref(pc), _d(so)))
+        return dict(r=r, Kaa=Kaa, KaE=KaE, C_EE=CEE, S_raw=S, plastic_count=pc.value, state=so)
 
 
 # ---- finite strain, Biot stress (config 2; parity unpinned) ----------------

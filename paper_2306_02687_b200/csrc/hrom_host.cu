@@ -56,6 +56,8 @@ struct fe2_hrom_s {
   PointState* st = nullptr;
   uint8_t* flags = nullptr;
   int* work = nullptr;              // work-queue counter
+  double* mono = nullptr;           // monolithic scheme: per-point working records (mono_stride)
+  bool mono_first = true;           // the next fe2_hrom_mono_iterate starts a step
   IncCounters* cnt = nullptr;       // device counters of a launch
   IncCounters* h_cnt = nullptr;     // pinned copy
   // asynchronous host-buffer increments (fe2_hrom_solve_increment_async):
@@ -154,6 +156,8 @@ struct fe2_hrom_s {
   }
   void free_points() {
     free_async();
+    dfree(mono);
+    mono_first = true;
     dfree(snap);
     snap_bytes = 0;
     dfree(hist);
@@ -606,6 +610,65 @@ int fe2_hrom_solve_increment_device(fe2_hrom_t h, const double* d_E, const fe2_n
     Outputs O{d_sigma ? d_sigma : h->o_sigma, d_C ? d_C : h->o_C, d_res ? d_res : h->o_res,
               d_iters ? d_iters : h->o_iters, d_status ? d_status : h->o_status, d_pc ? d_pc : h->o_pc};
     run_increment(h, d_E, make_cfg(opts), O, stream ? static_cast<cudaStream_t>(stream) : h->stream);
+  });
+}
+
+int fe2_hrom_mono_begin(fe2_hrom_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+    check(h->kin == 0 && h->NP <= 32, Code::config, "the monolithic iteration needs a small-strain handle with n <= 32");
+    h->mono_first = true;
+  });
+}
+
+int fe2_hrom_mono_iterate(fe2_hrom_t h, const double* E, double* sigma, double* C, double* rel_res,
+                          int* plastic_count, int* status) {
+  return guard([&] {
+    check(h != nullptr && E != nullptr, Code::config, "bad arguments");
+    check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+    check(h->kin == 0 && h->NP <= 32, Code::config, "the monolithic iteration needs a small-strain handle with n <= 32");
+    CK(cudaSetDevice(h->device));
+    const int64_t P = h->P;
+    cudaStream_t s = h->stream;
+    if (!h->mono) {
+      h->mono = dalloc<double>(static_cast<size_t>(P) * mono_stride(h->NP));
+      CK(cudaMemsetAsync(h->mono, 0, static_cast<size_t>(P) * mono_stride(h->NP) * sizeof(double), s));
+    }
+    CK(cudaMemcpyAsync(h->dE, E, P * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    IncArgs a{};
+    a.M = h->model();
+    a.D = h->points();
+    a.O = Outputs{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc};
+    a.cfg = NewtonCfg{1e-8, 1, 0};
+    a.dE = h->dE;
+    a.work = h->work;
+    a.cnt = h->cnt;
+    a.mono = h->mono;
+    a.mono_first = h->mono_first ? 1 : 0;
+    CK(cudaMemsetAsync(h->work, 0, sizeof(int), s));
+    CK(cudaMemsetAsync(h->cnt, 0, sizeof(IncCounters), s));
+    launch_increment_mono(a, h->num_sms, s);
+    CK(cudaGetLastError());
+    h->stats.kernel_launches += 1;
+    h->mono_first = false;
+    if (sigma) CK(cudaMemcpyAsync(sigma, h->o_sigma, P * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (C) CK(cudaMemcpyAsync(C, h->o_C, P * 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (rel_res) CK(cudaMemcpyAsync(rel_res, h->o_res, P * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (plastic_count) CK(cudaMemcpyAsync(plastic_count, h->o_pc, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (status) CK(cudaMemcpyAsync(status, h->o_status, P * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+int fe2_hrom_mono_commit(fe2_hrom_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+    check(h->mono != nullptr && !h->mono_first, Code::config, "fe2_hrom_mono_commit needs a monolithic iterate");
+    CK(cudaSetDevice(h->device));
+    launch_mono_commit(h->points(), h->NP, h->mono, h->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    h->mono_first = true;
   });
 }
 

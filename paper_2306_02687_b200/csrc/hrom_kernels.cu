@@ -383,7 +383,7 @@ __device__ void ring_drain(const Ring& R, int seq, int lane) {
 // RES: the whole projected operator G2 sits in shared memory for the kernel's
 // lifetime (loaded once by TMA): warps never wait on each other for G chunks.
 // Otherwise G2 streams through the CTA-shared ring (W warps, ST stages).
-template <int NT, int W, bool RES>
+template <int NT, int W, bool RES, bool MONO = false>
 __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArgs A) {
   constexpr int NP = 8 * NT;
   constexpr int NTP = NT * (NT + 1) / 2;
@@ -812,6 +812,91 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     }
   };
 
+  // Monolithic scheme ("micro problems advance one Newton
+  // iteration per macro iteration sharing the same consistent linearization"):
+  // one reduced iteration of point p at the macro strain E of this macro
+  // iterate. The linearised micro equation K Δα = -(r + K_aE ΔE) is
+  // condensed: the macro code receives Σ~ = (Σ_raw - K_Eα K^-1 r) / V and
+  // C = (C_EE - K_Eα K^-1 K_aE) / V, and the next call moves α by
+  // -(K^-1 r + K^-1 K_aE ΔE) once ΔE is known. No commit (launch_mono_commit).
+  auto mono_point = [&](int64_t p, double E0, double E1, double E2) {
+    double* rec = A.mono + p * mono_stride(NP);
+    const double* z = rec;
+    double* tail = rec + 6 * NP;
+    if (A.mono_first) {
+      for (int b = lane; b < NP; b += 32) sAev[b] = D.alpha_c[p * NP + b];
+    } else {
+      const double d0 = E0 - tail[0], d1 = E1 - tail[1], d2 = E2 - tail[2];
+      for (int b = lane; b < NP; b += 32)
+        sAev[b] = (b < n) ? rec[5 * NP + b] - (z[b] + z[NP + b] * d0 + z[2 * NP + b] * d1 + z[3 * NP + b] * d2)
+                          : 0.0;
+    }
+    __syncwarp();
+    assembly_pass(p, E0, E1, E2, -1);
+    const double rl = (lane < n) ? sV[lane] : 0.0;
+    const double rn = sqrt(warp_sum(rl * rl));
+    // micro scale: max(|r| at the step's first iteration, |Σ_raw| now) — E moves during a monolithic step
+    const double r_first = A.mono_first ? rn : tail[6];
+    const double ref = fmax(fmax(r_first, sqrt(s0 * s0 + s1 * s1 + s2 * s2)), 1e-30);
+    if (!factor()) {
+      if (lane == 0) {
+        A.O.status[p] = kSolver;
+        A.O.iters[p] = 1;
+        A.O.res[p] = rn / ref;
+      }
+      __syncwarp();
+      return;
+    }
+    const double k0 = (lane < n) ? sKaE[lane * 3 + 0] : 0.0;
+    const double k1 = (lane < n) ? sKaE[lane * 3 + 1] : 0.0;
+    const double k2 = (lane < n) ? sKaE[lane * 3 + 2] : 0.0;
+    const double zr = warp_chol_solve(sK, sInv, n, lane, rl);
+    const double z0 = warp_chol_solve(sK, sInv, n, lane, k0);
+    const double z1 = warp_chol_solve(sK, sInv, n, lane, k1);
+    const double z2 = warp_chol_solve(sK, sInv, n, lane, k2);
+    const double t0 = warp_sum(k0 * zr), t1 = warp_sum(k1 * zr), t2 = warp_sum(k2 * zr);
+    const double q00 = warp_sum(k0 * z0), q11 = warp_sum(k1 * z1), q22 = warp_sum(k2 * z2);
+    const double q01 = 0.5 * (warp_sum(k0 * z1) + warp_sum(k1 * z0));
+    const double q02 = 0.5 * (warp_sum(k0 * z2) + warp_sum(k2 * z0));
+    const double q12 = 0.5 * (warp_sum(k1 * z2) + warp_sum(k2 * z1));
+    if (lane < NP) {
+      rec[lane] = zr;
+      rec[NP + lane] = z0;
+      rec[2 * NP + lane] = z1;
+      rec[3 * NP + lane] = z2;
+      rec[4 * NP + lane] = sRp[lane];
+      rec[5 * NP + lane] = sAev[lane];
+    }
+    if (lane == 0) {
+      const double V = M.volume;
+      double* Cp = A.O.C + p * 9;
+      Cp[0] = (ce00 - q00) / V;
+      Cp[1] = (ce01 - q01) / V;
+      Cp[2] = (ce02 - q02) / V;
+      Cp[3] = Cp[1];
+      Cp[4] = (ce11 - q11) / V;
+      Cp[5] = (ce12 - q12) / V;
+      Cp[6] = Cp[2];
+      Cp[7] = Cp[5];
+      Cp[8] = (ce22 - q22) / V;
+      A.O.sigma[p * 3 + 0] = (s0 - t0) / V;
+      A.O.sigma[p * 3 + 1] = (s1 - t1) / V;
+      A.O.sigma[p * 3 + 2] = (s2 - t2) / V;
+      A.O.res[p] = rn / ref;
+      A.O.iters[p] = 1;
+      A.O.status[p] = 0;
+      if (A.O.pcount) A.O.pcount[p] = np_last;
+      tail[0] = E0;
+      tail[1] = E1;
+      tail[2] = E2;
+      tail[3] = dsp0;
+      tail[4] = dsp1;
+      tail[5] = dsp2;
+      tail[6] = r_first;
+    }
+    __syncwarp();
+  };
+
   // ------------------------------------------------------------ point loop
   auto grab = [&]() -> int64_t {
     if (dbg) return (blockIdx.x == 0 && warp == 0 && seq == 0) ? A.dbg_point : D.P;
@@ -845,6 +930,11 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
         D.E_c[p * 3 + 1] = Et1;
         D.E_c[p * 3 + 2] = Et2;
       }
+      p_next = grab();
+      continue;
+    }
+    if constexpr (MONO) {
+      mono_point(p, Et0, Et1, Et2);
       p_next = grab();
       continue;
     }
@@ -1086,9 +1176,9 @@ __global__ void k_material_batch(MatDev m, int64_t N, const double* eps, const d
 
 constexpr size_t kMaxDynSmem = 227 * 1024;
 
-template <int NT, int W, bool RES>
+template <int NT, int W, bool RES, bool MONO = false>
 void launch_inc_variant(const IncArgs& a, int num_sms, cudaStream_t s, size_t smem) {
-  auto kern = k_increment<NT, W, RES>;
+  auto kern = k_increment<NT, W, RES, MONO>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaxDynSmem));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
@@ -1128,6 +1218,36 @@ size_t increment_smem(int NP) {
     case 24: return IncLayout<24, kW>::bytes;
     case 32: return IncLayout<32, kW>::bytes;
     default: return 0;
+  }
+}
+
+__global__ void k_mono_commit(PointsDev D, int NP, const double* __restrict__ mono) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= D.P || D.st[p].err) return;
+  const double* rec = mono + p * mono_stride(NP);
+  for (int a = 0; a < NP; ++a) {
+    D.alpha_c[p * NP + a] = rec[5 * NP + a];
+    D.bp[p * NP + a] -= rec[4 * NP + a];
+  }
+  for (int i = 0; i < 3; ++i) {
+    D.E_c[p * 3 + i] = rec[6 * NP + i];
+    D.sp[p * 4 + i] -= rec[6 * NP + 3 + i];
+  }
+  D.st[p].pad[0] ^= 1;
+}
+
+void launch_mono_commit(const PointsDev& D, int NP, const double* mono, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>((D.P + 127) / 128);
+  k_mono_commit<<<grid, 128, 0, s>>>(D, NP, mono);
+}
+
+void launch_increment_mono(const IncArgs& a, int num_sms, cudaStream_t s) {
+  switch (a.M.NP) {
+    case 8: launch_inc_variant<1, kW, false, true>(a, num_sms, s, IncLayout<8, kW>::bytes); break;
+    case 16: launch_inc_variant<2, kW, false, true>(a, num_sms, s, IncLayout<16, kW>::bytes); break;
+    case 24: launch_inc_variant<3, kW, false, true>(a, num_sms, s, IncLayout<24, kW>::bytes); break;
+    case 32: launch_inc_variant<4, kW, false, true>(a, num_sms, s, IncLayout<32, kW>::bytes); break;
+    default: break;
   }
 }
 

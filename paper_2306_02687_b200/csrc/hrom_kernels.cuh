@@ -103,11 +103,23 @@ struct IncArgs {
   // watchdog trace (mapped pinned host memory, FE2_TRACE=1): per warp
   // {ring position, state code, point, stage-counter snapshot}
   volatile int* trace;
+  // monolithic iteration (k_increment<..., MONO>): per-point working record
+  // [P][mono_stride(NP)], see mono_stride; mono_first = first iteration of a step
+  double* mono;
+  int mono_first;
 };
+
+// Per-point record of the monolithic scheme: z[4][NP] (K^-1 r, K^-1 K_aE),
+// r_plastic[NP], α_w[NP] (the evaluation point), E[3], Σ_plastic[3], ref, pad.
+constexpr int mono_stride(int NP) { return 6 * NP + 8; }
 
 // host launchers (hrom_kernels.cu: NP <= 32, one warp per point;
 // hrom_kernels_big.cu: NP in {40,48,56,64,80,96,112,128}, one CTA per point)
 void launch_increment(const IncArgs& a, int num_sms, cudaStream_t s);
+// one monolithic Newton iteration for every point (no commit), NP <= 32
+void launch_increment_mono(const IncArgs& a, int num_sms, cudaStream_t s);
+// adopt the last monolithic iterate of every live point as its committed state
+void launch_mono_commit(const PointsDev& D, int NP, const double* mono, cudaStream_t s);
 bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s);
 size_t increment_big_smem(int NP);
 void launch_material_batch(const MatDev& m, int64_t N, const double* eps, const double* st_in, double* sigma,

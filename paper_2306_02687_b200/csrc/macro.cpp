@@ -3,7 +3,13 @@
 // variant — every macro Newton iteration runs fully converged micro solves
 // (one engine increment for all macro Gauss points) and assembles the macro
 // tangent from their condensed C_macro; the micro history is committed only
-// when the macro step converges (engine snapshot / restore).
+// when the macro step converges (engine snapshot / restore). scheme = 1 runs
+// the monolithic variant instead (SPEC.md:474-481 and its DESIGN DECISION:
+// single-iteration-coupled Newton, micro condensed every iteration): each
+// macro iteration advances every micro problem by ONE reduced Newton iteration
+// (fe2_hrom_mono_iterate) and assembles the macro residual / tangent from the
+// condensed stress and tangent; a step is accepted when the macro residual AND
+// every micro residual are below tolerance (fe2_hrom_mono_commit).
 //
 // Macro problem (SPEC "desk" defaults): plane strain L x H strip of
 // structured Tri6 pairs (build_beam_mesh, mesh.hpp:133-169), left edge
@@ -245,6 +251,10 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
     // one trial micro solve at displacement u from the committed state; false if any point failed
     long long micro_total = 0;
     double fscale = 0.0;  // largest |f_int| of an accepted step: the residual's absolute floor near R = 0
+    const bool mono = cfg->scheme == 1;
+    check(cfg->scheme == 0 || cfg->scheme == 1, Code::config, "scheme must be 0 (nested) or 1 (monolithic)");
+    check(!mono || kin == 0, Code::config, "the monolithic scheme runs on small-strain handles");
+    bool micro_ok = true;  // monolithic: every point's micro residual below micro.tol
     auto micro_solve = [&]() -> bool {
       for (int g = 0; g < P; ++g) {
         const int e = m.elem[g];
@@ -255,12 +265,22 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
           E[nr * g + i] = s;
         }
       }
-      engine_check(fe2_hrom_restore(engine));
-      engine_check(fe2_hrom_solve_increment(engine, E.data(), &mopt, sig.data(), C.data(), it.data(), pc.data(),
-                                            res.data(), st.data()));
-      for (int g = 0; g < P; ++g) {
-        if (st[g] != 0) return false;
-        micro_total += it[g];
+      if (mono) {  // one micro iteration per point, condensed stress and tangent
+        engine_check(fe2_hrom_mono_iterate(engine, E.data(), sig.data(), C.data(), res.data(), pc.data(), st.data()));
+        micro_ok = true;
+        for (int g = 0; g < P; ++g) {
+          if (st[g] != 0) return false;
+          micro_total += 1;
+          micro_ok = micro_ok && res[g] <= mopt.tol;
+        }
+      } else {
+        engine_check(fe2_hrom_restore(engine));
+        engine_check(fe2_hrom_solve_increment(engine, E.data(), &mopt, sig.data(), C.data(), it.data(), pc.data(),
+                                              res.data(), st.data()));
+        for (int g = 0; g < P; ++g) {
+          if (st[g] != 0) return false;
+          micro_total += it[g];
+        }
       }
       std::fill(fint.begin(), fint.end(), 0.0);
       for (int g = 0; g < P; ++g) {
@@ -277,6 +297,7 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
     // macro Newton for a prescribed tip displacement; returns iterations or -1
     auto macro_step = [&](double U) -> int {
       for (int nd_ : m.tip) u[2 * nd_ + 1] = U;
+      if (mono) engine_check(fe2_hrom_mono_begin(engine));
       for (int k = 0; k <= cfg->max_iter; ++k) {
         if (!micro_solve()) return -1;
         double rn = 0.0, fn = 0.0;
@@ -286,7 +307,7 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
         }
         rn = std::sqrt(rn);
         fn = std::sqrt(fn);
-        if (rn <= cfg->tol * std::max(std::max(fn, fscale), 1e-30)) return k;
+        if (rn <= cfg->tol * std::max(std::max(fn, fscale), 1e-30) && micro_ok) return k;
         if (k == cfg->max_iter) return -1;
         Kff.assign(static_cast<size_t>(nf) * nf, 0.0);
         for (int g = 0; g < P; ++g) {
@@ -354,7 +375,8 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
           continue;
         }
         iters_sum += k;
-        engine_check(fe2_hrom_snapshot(engine));  // accept: the micro states are committed
+        // accept: the micro states are committed
+        engine_check(mono ? fe2_hrom_mono_commit(engine) : fe2_hrom_snapshot(engine));
         {
           double fn = 0.0;
           for (int d = 0; d < nd; ++d) fn += fint[d] * fint[d];

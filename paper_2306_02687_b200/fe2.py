@@ -2,7 +2,8 @@
 (fe2_macro_*; SPEC.md:455-518 fe2.macro_step / solve_program, nested
 variant; SURVEY §8(f) rank 1). The macro loop is host C++ in the library;
 every macro Newton iteration is one engine increment for all macro Gauss
-points on the device."""
+points on the device (nested), or one monolithic micro iteration of all of
+them (scheme="monolithic": fe2_hrom_mono_*)."""
 from __future__ import annotations
 
 import ctypes as C
@@ -16,7 +17,7 @@ from .hrom import HyperRomEngine, NewtonOptions, _check, _Opts, lib
 class _MacroCfg(C.Structure):
     _fields_ = [("length", C.c_double), ("height", C.c_double), ("nx", C.c_int), ("ny", C.c_int),
                 ("u_max", C.c_double), ("n_load", C.c_int), ("max_unload", C.c_int), ("tol", C.c_double),
-                ("max_iter", C.c_int), ("max_bisections", C.c_int), ("micro", _Opts)]
+                ("max_iter", C.c_int), ("max_bisections", C.c_int), ("micro", _Opts), ("scheme", C.c_int)]
 
 
 lib.fe2_macro_points.argtypes = [C.POINTER(_MacroCfg), C.POINTER(C.c_int64)]
@@ -40,10 +41,13 @@ class MacroConfig:
     max_iter: int = 20
     max_bisections: int = 4
     micro: NewtonOptions = field(default_factory=NewtonOptions)
+    scheme: str = "nested"  # or "monolithic"
 
     def _c(self):
+        assert self.scheme in ("nested", "monolithic")
         return _MacroCfg(self.length, self.height, self.nx, self.ny, self.u_max, self.n_load, self.max_unload,
-                         self.tol, self.max_iter, self.max_bisections, self.micro._c())
+                         self.tol, self.max_iter, self.max_bisections, self.micro._c(),
+                         1 if self.scheme == "monolithic" else 0)
 
 
 def macro_points(cfg: MacroConfig) -> int:

@@ -94,6 +94,9 @@ def _load():
     L.fe2_hrom_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     L.fe2_hrom_reset_points.argtypes = [C.c_void_p]
     L.fe2_hrom_snapshot.argtypes = [C.c_void_p]
+    L.fe2_hrom_mono_begin.argtypes = [C.c_void_p]
+    L.fe2_hrom_mono_iterate.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _ip, _ip]
+    L.fe2_hrom_mono_commit.argtypes = [C.c_void_p]
     L.fe2_hrom_restore.argtypes = [C.c_void_p]
     L.fe2_hrom_output_ptrs.argtypes = [C.c_void_p] + [C.POINTER(C.c_void_p)] * 6
     L.fe2_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
@@ -329,6 +332,23 @@ class HyperRomEngine:
     def restore(self):
         """Return every point to the last snapshot."""
         _check(lib.fe2_hrom_restore(self._h))
+
+    def mono_begin(self):
+        """Monolithic scheme: start a step from the committed state."""
+        _check(lib.fe2_hrom_mono_begin(self._h))
+
+    def mono_iterate(self, E):
+        """One monolithic micro iteration of every point at macro strains E
+        (P,3): condensed sigma (P,3), C (P,3,3), rel_res, plastic_count, status."""
+        E = np.ascontiguousarray(E, dtype=np.float64).reshape(self.P, 3)
+        sig, Cm, rr = np.empty((self.P, 3)), np.empty((self.P, 3, 3)), np.empty(self.P)
+        pc, st = np.empty(self.P, dtype=np.int32), np.empty(self.P, dtype=np.int32)
+        _check(lib.fe2_hrom_mono_iterate(self._h, _d(E), _d(sig), _d(Cm), _d(rr), _i(pc), _i(st)))
+        return dict(sigma=sig, C=Cm, rel_res=rr, plastic_count=pc, status=st)
+
+    def mono_commit(self):
+        """Adopt the last monolithic iterate of every point as committed."""
+        _check(lib.fe2_hrom_mono_commit(self._h))
 
     def output_ptrs(self):
         """Device pointers (ints) of the handle's own output buffers:

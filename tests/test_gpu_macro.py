@@ -55,3 +55,36 @@ def test_device_finite_strain_macro_driver_matches_oracle():
     np.testing.assert_allclose(g["micro_iters"], rows[:, 3], rtol=1e-3, atol=0)
     assert np.abs(g["R"] - rows[:, 1]).max() <= 1e-8 * np.abs(rows[:, 1]).max()
     assert g["U_residual"] > 0.0 and abs(g["U_residual"] - ures) <= 1e-8 * cfg.u_max
+
+
+@pytest.mark.parametrize("u_max,n_load", [(0.02, 3), (0.3, 10)])
+def test_device_monolithic_driver_matches_oracle(u_max, n_load):
+    """Monolithic scheme (fe2_hrom_mono_*): the device macro driver against
+    the oracle's monolithic driver — identical steps and macro iteration
+    counts, micro iterations = P per macro iteration, R within 1e-8."""
+    m = F.HyperRomModel(33, 12, 200, 0)
+    eng = F.HyperRomEngine.from_model(m)
+    cfg = F.MacroConfig(u_max=u_max, n_load=n_load, scheme="monolithic")
+    g = F.solve_program(cfg, eng)
+    beam = MO.build_beam(cfg.length, cfg.height, cfg.nx, cfg.ny)
+    orc = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume)
+    rows, ures = MO.solve_program(beam, MO.MonoEngine(orc, len(beam["w"]), m.volume), u_max=u_max, n_load=n_load,
+                                  max_unload=cfg.max_unload, tol=cfg.tol, max_iter=cfg.max_iter,
+                                  micro_tol=cfg.micro.tol)
+    assert len(g["U"]) == len(rows)
+    np.testing.assert_allclose(g["U"], rows[:, 0], rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(g["macro_iters"], rows[:, 2].astype(int))
+    np.testing.assert_array_equal(g["micro_iters"], rows[:, 3])
+    assert np.abs(g["R"] - rows[:, 1]).max() <= 1e-8 * np.abs(rows[:, 1]).max()
+    assert abs(g["U_residual"] - ures) <= 1e-8 * u_max
+
+
+def test_device_monolithic_reaches_the_nested_fixed_point():
+    """same R(U) curve and residual displacement as the nested
+    scheme (within the tolerances), with far fewer micro iterations."""
+    m = F.HyperRomModel(33, 12, 200, 0)
+    nested = F.solve_program(F.MacroConfig(u_max=0.3, n_load=10), F.HyperRomEngine.from_model(m))
+    mono = F.solve_program(F.MacroConfig(u_max=0.3, n_load=10, scheme="monolithic"), F.HyperRomEngine.from_model(m))
+    assert len(mono["U"]) == len(nested["U"])
+    assert np.abs(mono["R"] - nested["R"]).max() < 1e-5 * np.abs(nested["R"]).max()
+    assert abs(mono["U_residual"] - nested["U_residual"]) < 1e-4 * 0.3

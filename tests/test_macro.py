@@ -76,3 +76,32 @@ def test_oracle_finite_strain_driver_small_load_limit():
     r_ss, _ = MO.solve_program(beam, MO.ReplayEngine(ss, len(beam["w"])), u_max=1e-3, n_load=2, max_unload=0)
     r_fs, _ = MO.solve_program(beam, MO.ReplayEngine(fs, len(beam["w"])), u_max=1e-3, n_load=2, max_unload=0)
     np.testing.assert_allclose(r_fs[:, 1], r_ss[:, 1], rtol=5e-3)
+
+
+def test_oracle_monolithic_reaches_the_nested_fixed_point(desk_hrom):
+    """the monolithic scheme converges to the nested scheme's
+    fixed point (same R(U) curve and U_res within the tolerances); every
+    accepted step has all micro residuals below micro tol."""
+    beam = MO.build_beam(4.0, 1.0, 8, 2)
+    P = len(beam["w"])
+    kw = dict(u_max=0.3, n_load=5, max_unload=30)
+    rn, un = MO.solve_program(beam, MO.ReplayEngine(desk_hrom, P), **kw)
+    rm, um = MO.solve_program(beam, MO.MonoEngine(desk_hrom, P, desk_hrom_volume()), **kw)
+    assert len(rn) == len(rm)
+    np.testing.assert_allclose(rm[:, 0], rn[:, 0], rtol=0, atol=1e-12)
+    assert np.abs(rm[:, 1] - rn[:, 1]).max() < 1e-5 * np.abs(rn[:, 1]).max()
+    assert abs(um - un) < 1e-4 * 0.3
+    assert um > 0
+
+
+def test_oracle_monolithic_elastic_equals_nested(desk_hrom):
+    beam = MO.build_beam(4.0, 1.0, 8, 2)
+    P = len(beam["w"])
+    rn, _ = MO.solve_program(beam, MO.ReplayEngine(desk_hrom, P), u_max=0.02, n_load=3, max_unload=0)
+    rm, _ = MO.solve_program(beam, MO.MonoEngine(desk_hrom, P, desk_hrom_volume()), u_max=0.02, n_load=3,
+                             max_unload=0)
+    np.testing.assert_allclose(rm[:, 1], rn[:, 1], rtol=1e-8)
+
+
+def desk_hrom_volume():
+    return O.Model(subdivisions=33, n=12, K=200, seed=0).volume
