@@ -228,6 +228,12 @@ int fe2_macro_gauss(const fe2_macro_config_t* cfg, double* B, double* w, int* el
 /* rows[k] = (U, R, macro iterations of the step, cumulative micro iterations, wall ms) */
 int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows, int max_rows, int* n_rows,
                   double* u_residual);
+/* The same program with full-field RVEs at the macro points (HF FE², nested;
+ * the reference the hyper-ROM curves are compared with):
+ * hf holds fe2_macro_points() points (fe2_hf_alloc_points). */
+typedef struct fe2_hf_s* fe2_hf_t;
+int fe2_macro_run_hf(const fe2_macro_config_t* cfg, fe2_hf_t hf, double* rows, int max_rows, int* n_rows,
+                     double* u_residual);
 
 /* ---- monolithic scheme (SPEC.md:474-481 HF_monolithic / hyper-ROM): the
  * micro problems advance ONE reduced Newton iteration per macro iteration,
@@ -293,7 +299,6 @@ int fe2_model_build_basis(int subdivisions, const char* mesh_path, const double*
  * dense free stiffness, cuSOLVER Cholesky (loaded at first use). Replaces
  * micro_newton + homogenize + run_trajectory with SnapshotRecorder
  * (rve.hpp:285-392, :397-494; linear BC). */
-typedef struct fe2_hf_s* fe2_hf_t;
 /* RVE = default_cell(subdivisions) or mesh_path; materials indexed by the
  * element material id. */
 int fe2_hf_create(int device, int subdivisions, const char* mesh_path, const fe2_material_t* materials, int n_materials,
@@ -308,6 +313,19 @@ int fe2_hf_sizes(fe2_hf_t h, int* n_dofs, int* n_free, int* n_ips, double* volum
  * Non-convergence after max_bisections -> solver error. */
 int fe2_hf_trajectory(fe2_hf_t h, int n_steps, const double* E, const fe2_newton_opts_t* opts, double* sigma,
                       double* C, int* iterations, double* u_fluct_inf, double* res_last, double* snapshots);
+/* HF engine of an FE² run (SPEC.md:474-477 HF_nested): P macro points, each
+ * an RVE with its own committed state (virgin at allocation). One call = one
+ * path step of run_trajectory for every point from its committed state
+ * (bisection, warm start); Σ[P*3], C[P*9] (homogenize), iterations, status
+ * (0, or 1 + ErrorCode when the point's step failed — it keeps its state).
+ * snapshot / restore save and return to the committed states (deferred
+ * commits, fe2_macro_run_hf). Points are solved one after another. */
+int fe2_hf_alloc_points(fe2_hf_t h, int64_t P);
+int fe2_hf_points(fe2_hf_t h, int64_t* P);
+int fe2_hf_solve_increment(fe2_hf_t h, const double* E, const fe2_newton_opts_t* opts, double* sigma, double* C,
+                           int* iters, int* status);
+int fe2_hf_snapshot(fe2_hf_t h);
+int fe2_hf_restore(fe2_hf_t h);
 /* build_elastic_modes: fluctuation responses of the
  * elastic RVE (every material's elastic part) to unit macro strains
  * (1,0,0),(0,1,0),(0,0,1), orthonormalised (Gram-Schmidt, twice); modes whose

@@ -233,6 +233,12 @@ struct fe2_hf_s {
   double *d_rhs = nullptr, *d_work = nullptr;
   int lwork = 0;
   bool factored = false;  // d_K holds the Cholesky factor of the last assembled stiffness
+  double* st_comm = nullptr;  // committed states the assembly reads (d_st0, or a point's block)
+  // macro-point batch (fe2_hf_alloc_points): per point committed states on the
+  // device, committed free displacements / strains on the host; snapshot copies
+  int64_t P = 0;
+  double *d_pst = nullptr, *d_pst_snap = nullptr;
+  std::vector<double> pu, pu_snap, pE, pE_snap;  // [P][nf], [P][6] = (E_prev, E_comm)
 
   int nd() const { return r.n_dofs(); }
   int nf() const { return r.n_free; }
@@ -242,7 +248,7 @@ struct fe2_hf_s {
     if (stream) cudaStreamDestroy(stream);
     for (int* p : {d_conn, d_phase, d_free, d_inc_ptr, d_inc, d_info, d_err})
       if (p) cudaFree(p);
-    for (double* p : {d_B, d_w, d_u, d_st0, d_st1, d_fel, d_kel, d_f, d_K, d_sig, d_C, d_rhs, d_work})
+    for (double* p : {d_B, d_w, d_u, d_st0, d_st1, d_fel, d_kel, d_f, d_K, d_sig, d_C, d_rhs, d_work, d_pst, d_pst_snap})
       if (p) cudaFree(p);
   }
 
@@ -260,7 +266,7 @@ struct fe2_hf_s {
   void assemble(const std::vector<double>& u_full, bool with_K, const MatTable& mt, std::vector<double>& f_full) {
     CK(cudaMemcpyAsync(d_u, u_full.data(), sizeof(double) * nd(), cudaMemcpyHostToDevice, stream));
     if (with_K) CK(cudaMemsetAsync(d_K, 0, sizeof(double) * nf() * nf(), stream));
-    k_hf_element<<<r.n_el, 144, 0, stream>>>(r.n_el, d_conn, d_phase, mt, d_B, d_w, d_u, d_st0, with_K ? 1 : 0,
+    k_hf_element<<<r.n_el, 144, 0, stream>>>(r.n_el, d_conn, d_phase, mt, d_B, d_w, d_u, st_comm, with_K ? 1 : 0,
                                              d_fel, d_kel, d_st1, d_sig, d_C, d_err);
     CK(cudaGetLastError());
     k_hf_gather<<<(nd() + 127) / 128, 128, 0, stream>>>(nd(), d_inc_ptr, d_inc, d_conn, d_free, nf(), d_fel, d_kel,
@@ -428,60 +434,132 @@ struct fe2_hf_s {
     for (int k = 0; k < 9; ++k) C[k] = c_hom[k] / r.volume;
   }
 
+  // One path step of run_trajectory (rve.hpp:459-491) from the committed
+  // state (st_comm on the device, u_free, E_comm) towards E_target, E_prev
+  // being the previous path point: warm start = committed solution + affine
+  // increment, bisection on non-convergence (throws ErrorCode::solver after
+  // max_bisections). On success the committed state has advanced; the last
+  // converged Newton result is returned (its d_sig / d_C / d_K are current).
+  Newton increment(const double* E_prev, const double* E_target, std::vector<double>& u_free, double* E_comm,
+                   double tol, int max_iter, int max_bisections, const MatTable& mt, int& its) {
+    const int N = nd();
+    std::vector<double> aff, u0(nf());
+    double done = 0.0, frac = 1.0;
+    int bis = 0;
+    its = 0;
+    Newton res;
+    while (done < 1.0 - 1e-12) {
+      const double target = std::min(1.0, done + frac);
+      double Ev[3], dE[3];
+      for (int i = 0; i < 3; ++i) Ev[i] = E_prev[i] + (E_target[i] - E_prev[i]) * target;
+      for (int i = 0; i < 3; ++i) dE[i] = Ev[i] - E_comm[i];
+      affine(dE, aff);
+      for (int i = 0; i < N; ++i)
+        if (r.free_index[i] >= 0) u0[r.free_index[i]] = u_free[r.free_index[i]] + aff[i];
+      MatTable ms = mt;  // creep: the sub-step's fraction of the increment's dt (rve.hpp:466)
+      for (MatDev& md : ms.m) md.dt *= target - done;
+      res = newton(Ev, u0, tol, max_iter, ms);
+      its += res.iterations;
+      if (!res.converged) {
+        check(++bis <= max_bisections, Code::solver, "micro trajectory failed after max bisections");
+        frac *= 0.5;
+        continue;
+      }
+      CK(cudaMemcpyAsync(st_comm, d_st1, sizeof(double) * 6 * r.n_ips(), cudaMemcpyDeviceToDevice, stream));
+      for (int i = 0; i < N; ++i)
+        if (r.free_index[i] >= 0) u_free[r.free_index[i]] = res.u_full[i];
+      for (int i = 0; i < 3; ++i) E_comm[i] = Ev[i];
+      done = target;
+    }
+    return res;
+  }
+
   // run_trajectory (rve.hpp:448-494) from the virgin state.
   void trajectory(int n_steps, const double* E, double tol, int max_iter, int max_bisections, const MatTable& mt,
                   double* sigma, double* C, int* iterations, double* u_fluct_inf, double* res_last, double* snaps) {
     const int n = nf(), N = nd();
+    st_comm = d_st0;
     CK(cudaMemsetAsync(d_st0, 0, sizeof(double) * 6 * r.n_ips(), stream));
     CK(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
-    std::vector<double> u_free(n, 0.0), aff, u0(n);
+    std::vector<double> u_free(n, 0.0), aff;
     double E_prev[3] = {0, 0, 0}, E_comm[3] = {0, 0, 0};
     for (int k = 0; k < n_steps; ++k) {
-      double done = 0.0, frac = 1.0;
-      int bis = 0, its = 0;
-      while (done < 1.0 - 1e-12) {
-        const double target = std::min(1.0, done + frac);
-        double Ev[3], dE[3];
-        for (int i = 0; i < 3; ++i) Ev[i] = E_prev[i] + (E[3 * k + i] - E_prev[i]) * target;
-        for (int i = 0; i < 3; ++i) dE[i] = Ev[i] - E_comm[i];
-        affine(dE, aff);
-        for (int i = 0; i < N; ++i)
-          if (r.free_index[i] >= 0) u0[r.free_index[i]] = u_free[r.free_index[i]] + aff[i];
-        MatTable ms = mt;  // creep: the sub-step's fraction of the increment's dt (rve.hpp:466)
-        for (MatDev& md : ms.m) md.dt *= target - done;
-        Newton res = newton(Ev, u0, tol, max_iter, ms);
-        its += res.iterations;
-        if (!res.converged) {
-          check(++bis <= max_bisections, Code::solver, "micro trajectory failed after max bisections");
-          frac *= 0.5;
-          continue;
-        }
-        CK(cudaMemcpyAsync(d_st0, d_st1, sizeof(double) * 6 * r.n_ips(), cudaMemcpyDeviceToDevice, stream));
-        for (int i = 0; i < N; ++i)
-          if (r.free_index[i] >= 0) u_free[r.free_index[i]] = res.u_full[i];
-        for (int i = 0; i < 3; ++i) E_comm[i] = Ev[i];
-        done = target;
-        if (done >= 1.0 - 1e-12) {
-          if (sigma || C) {
-            double s3[3], c9[9];
-            homogenize(s3, c9);
-            if (sigma) std::memcpy(sigma + 3 * k, s3, sizeof(s3));
-            if (C) std::memcpy(C + 9 * k, c9, sizeof(c9));
-          }
-          affine(Ev, aff);
-          double mx = 0.0;
-          for (int i = 0; i < N; ++i) {
-            const double wv = res.u_full[i] - aff[i];
-            mx = std::max(mx, std::abs(wv));
-            if (snaps) snaps[(size_t)k * N + i] = wv;
-          }
-          if (u_fluct_inf) u_fluct_inf[k] = mx;
-          if (res_last) res_last[k] = res.res_last;
-        }
+      int its = 0;
+      const Newton res = increment(E_prev, E + 3 * k, u_free, E_comm, tol, max_iter, max_bisections, mt, its);
+      if (sigma || C) {
+        double s3[3], c9[9];
+        homogenize(s3, c9);
+        if (sigma) std::memcpy(sigma + 3 * k, s3, sizeof(s3));
+        if (C) std::memcpy(C + 9 * k, c9, sizeof(c9));
       }
+      affine(E_comm, aff);
+      double mx = 0.0;
+      for (int i = 0; i < N; ++i) {
+        const double wv = res.u_full[i] - aff[i];
+        mx = std::max(mx, std::abs(wv));
+        if (snaps) snaps[(size_t)k * N + i] = wv;
+      }
+      if (u_fluct_inf) u_fluct_inf[k] = mx;
+      if (res_last) res_last[k] = res.res_last;
       if (iterations) iterations[k] = its;
       for (int i = 0; i < 3; ++i) E_prev[i] = E[3 * k + i];
     }
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  // A batch of P macro points, each an RVE with its own committed state
+  // (the HF engine of an FE² run, SPEC.md:474-477 HF_nested). One increment
+  // per call for every point; a point whose step fails keeps its committed
+  // state and reports status 1 + ErrorCode.
+  void alloc_points(int64_t n_points) {
+    dfree(d_pst);
+    dfree(d_pst_snap);
+    P = n_points;
+    d_pst = dalloc<double>(static_cast<size_t>(P) * 6 * r.n_ips());
+    d_pst_snap = dalloc<double>(static_cast<size_t>(P) * 6 * r.n_ips());
+    CK(cudaMemsetAsync(d_pst, 0, sizeof(double) * P * 6 * r.n_ips(), stream));
+    CK(cudaMemsetAsync(d_pst_snap, 0, sizeof(double) * P * 6 * r.n_ips(), stream));
+    pu.assign(static_cast<size_t>(P) * nf(), 0.0);
+    pE.assign(static_cast<size_t>(P) * 6, 0.0);
+    pu_snap = pu;
+    pE_snap = pE;
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  void solve_points(const double* E, double tol, int max_iter, int max_bisections, double* sigma, double* C,
+                    int* iters, int* status) {
+    const int n = nf();
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
+    std::vector<double> u_free(n);
+    for (int64_t p = 0; p < P; ++p) {
+      st_comm = d_pst + static_cast<size_t>(p) * 6 * r.n_ips();
+      double* Ep = pE.data() + 6 * p;  // (E_prev, E_comm)
+      std::copy(pu.begin() + p * n, pu.begin() + (p + 1) * n, u_free.begin());
+      double E_comm[3] = {Ep[3], Ep[4], Ep[5]};
+      int its = 0, code = 0;
+      const size_t sb = sizeof(double) * 6 * r.n_ips();
+      CK(cudaMemcpyAsync(d_st0, st_comm, sb, cudaMemcpyDeviceToDevice, stream));  // backup for a failed step
+      try {
+        increment(Ep, E + 3 * p, u_free, E_comm, tol, max_iter, max_bisections, mats, its);
+        double s3[3], c9[9];
+        homogenize(s3, c9);
+        if (sigma) std::memcpy(sigma + 3 * p, s3, sizeof(s3));
+        if (C) std::memcpy(C + 9 * p, c9, sizeof(c9));
+        std::copy(u_free.begin(), u_free.end(), pu.begin() + p * n);
+        for (int i = 0; i < 3; ++i) {
+          Ep[i] = E[3 * p + i];
+          Ep[3 + i] = E_comm[i];
+        }
+      } catch (const Failure& f) {
+        code = 1 + static_cast<int>(f.code);
+        CK(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
+        // a failed bisection may have committed sub-steps: return to the call's start
+        CK(cudaMemcpyAsync(st_comm, d_st0, sb, cudaMemcpyDeviceToDevice, stream));
+      }
+      if (iters) iters[p] = its;
+      if (status) status[p] = code;
+    }
+    st_comm = d_st0;
     CK(cudaStreamSynchronize(stream));
   }
 };
@@ -579,6 +657,56 @@ int fe2_hf_trajectory(fe2_hf_t h, int n_steps, const double* E, const fe2_newton
     CK(cudaSetDevice(h->device));
     h->trajectory(n_steps, E, opts->tol, opts->max_iter, opts->max_bisections, h->mats, sigma, C, iterations,
                   u_fluct_inf, res_last, snapshots);
+  });
+}
+
+int fe2_hf_alloc_points(fe2_hf_t h, int64_t P) {
+  return guard([&] {
+    check(h != nullptr && P >= 1, Code::config, "bad arguments");
+    CK(cudaSetDevice(h->device));
+    h->alloc_points(P);
+  });
+}
+
+int fe2_hf_solve_increment(fe2_hf_t h, const double* E, const fe2_newton_opts_t* opts, double* sigma, double* C,
+                           int* iters, int* status) {
+  return guard([&] {
+    check(h && E && opts, Code::config, "bad arguments");
+    check(h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
+    check(opts->tol > 0.0 && opts->max_iter >= 1 && opts->max_bisections >= 0, Code::config, "bad Newton options");
+    CK(cudaSetDevice(h->device));
+    h->solve_points(E, opts->tol, opts->max_iter, opts->max_bisections, sigma, C, iters, status);
+  });
+}
+
+int fe2_hf_snapshot(fe2_hf_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpyAsync(h->d_pst_snap, h->d_pst, sizeof(double) * h->P * 6 * h->r.n_ips(), cudaMemcpyDeviceToDevice,
+                       h->stream));
+    h->pu_snap = h->pu;
+    h->pE_snap = h->pE;
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int fe2_hf_restore(fe2_hf_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpyAsync(h->d_pst, h->d_pst_snap, sizeof(double) * h->P * 6 * h->r.n_ips(), cudaMemcpyDeviceToDevice,
+                       h->stream));
+    h->pu = h->pu_snap;
+    h->pE = h->pE_snap;
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int fe2_hf_points(fe2_hf_t h, int64_t* P) {
+  return guard([&] {
+    check(h != nullptr && P != nullptr, Code::config, "bad arguments");
+    *P = h->P;
   });
 }
 

@@ -203,13 +203,19 @@ int fe2_macro_gauss(const fe2_macro_config_t* cfg, double* B, double* w, int* el
   });
 }
 
-int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows, int max_rows, int* n_rows,
-                  double* u_residual) {
-  return guard([&] {
-    check(cfg && engine && rows && n_rows && max_rows > 0, Code::config, "bad arguments");
+}  // extern "C"
+
+namespace {
+
+// The load program on either micro backend: a hyper-ROM engine (engine) or
+// full-field HF RVEs (hf, nested scheme only).
+void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf, double* rows, int max_rows,
+                   int* n_rows, double* u_residual) {
+  {
+    check(cfg && (engine || hf) && rows && n_rows && max_rows > 0, Code::config, "bad arguments");
     check(cfg->n_load >= 1 && cfg->max_iter >= 1 && cfg->tol > 0.0, Code::config, "invalid macro options");
     int kin = 0;
-    engine_check(fe2_hrom_kinematics(engine, &kin));
+    if (engine) engine_check(fe2_hrom_kinematics(engine, &kin));
     const Beam m = build_beam(cfg->length, cfg->height, cfg->nx, cfg->ny);
     const int P = static_cast<int>(m.w.size());
     // per-Gauss-point operator: small strain (E11, E22, g12) = B u; finite strain
@@ -230,9 +236,15 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
         }
       }
     }
-    fe2_hrom_stats_t est{};
-    engine_check(fe2_hrom_stats(engine, &est));
-    check(est.points == P, Code::config, "engine must hold one point per macro Gauss point (fe2_macro_points)");
+    int64_t held = 0;
+    if (engine) {
+      fe2_hrom_stats_t est{};
+      engine_check(fe2_hrom_stats(engine, &est));
+      held = est.points;
+    } else {
+      engine_check(fe2_hf_points(hf, &held));
+    }
+    check(held == P, Code::config, "engine must hold one point per macro Gauss point (fe2_macro_points)");
     const int nd = 2 * static_cast<int>(m.x.size());
     // DOF roles: fixed (left: x, y), prescribed (tip: y), free (others)
     std::vector<int> role(nd, 0);  // 0 free, 1 fixed at 0, 2 prescribed U
@@ -254,6 +266,7 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
     const bool mono = cfg->scheme == 1;
     check(cfg->scheme == 0 || cfg->scheme == 1, Code::config, "scheme must be 0 (nested) or 1 (monolithic)");
     check(!mono || kin == 0, Code::config, "the monolithic scheme runs on small-strain handles");
+    check(!mono || engine, Code::config, "the monolithic scheme runs on a hyper-ROM engine");
     bool micro_ok = true;  // monolithic: every point's micro residual below micro.tol
     auto micro_solve = [&]() -> bool {
       for (int g = 0; g < P; ++g) {
@@ -272,6 +285,13 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
           if (st[g] != 0) return false;
           micro_total += 1;
           micro_ok = micro_ok && res[g] <= mopt.tol;
+        }
+      } else if (hf) {
+        engine_check(fe2_hf_restore(hf));
+        engine_check(fe2_hf_solve_increment(hf, E.data(), &mopt, sig.data(), C.data(), it.data(), st.data()));
+        for (int g = 0; g < P; ++g) {
+          if (st[g] != 0) return false;
+          micro_total += it[g];
         }
       } else {
         engine_check(fe2_hrom_restore(engine));
@@ -347,8 +367,13 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
     };
 
     const auto t0 = std::chrono::steady_clock::now();
-    engine_check(fe2_hrom_reset_points(engine));
-    engine_check(fe2_hrom_snapshot(engine));  // committed: virgin state
+    if (engine) {
+      engine_check(fe2_hrom_reset_points(engine));
+      engine_check(fe2_hrom_snapshot(engine));  // committed: virgin state
+    } else {
+      engine_check(fe2_hf_alloc_points(hf, P));
+      engine_check(fe2_hf_snapshot(hf));
+    }
     int nrow = 0;
     double U_done = 0.0;
     std::vector<double> u_done = u;
@@ -376,7 +401,7 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
         }
         iters_sum += k;
         // accept: the micro states are committed
-        engine_check(mono ? fe2_hrom_mono_commit(engine) : fe2_hrom_snapshot(engine));
+        engine_check(mono ? fe2_hrom_mono_commit(engine) : (hf ? fe2_hf_snapshot(hf) : fe2_hrom_snapshot(engine)));
         {
           double fn = 0.0;
           for (int d = 0; d < nd; ++d) fn += fint[d] * fint[d];
@@ -409,6 +434,26 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
     }
     *n_rows = nrow;
     if (u_residual) *u_residual = ures;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows, int max_rows, int* n_rows,
+                  double* u_residual) {
+  return guard([&] {
+    check(engine != nullptr, Code::config, "null engine");
+    macro_program(cfg, engine, nullptr, rows, max_rows, n_rows, u_residual);
+  });
+}
+
+int fe2_macro_run_hf(const fe2_macro_config_t* cfg, fe2_hf_t hf, double* rows, int max_rows, int* n_rows,
+                     double* u_residual) {
+  return guard([&] {
+    check(hf != nullptr, Code::config, "null HF handle");
+    macro_program(cfg, nullptr, hf, rows, max_rows, n_rows, u_residual);
   });
 }
 

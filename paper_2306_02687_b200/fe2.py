@@ -25,6 +25,7 @@ lib.fe2_macro_gauss.argtypes = [C.POINTER(_MacroCfg), C.POINTER(C.c_double), C.P
                                 C.POINTER(C.c_int)]
 lib.fe2_macro_run.argtypes = [C.POINTER(_MacroCfg), C.c_void_p, C.POINTER(C.c_double), C.c_int,
                               C.POINTER(C.c_int), C.POINTER(C.c_double)]
+lib.fe2_macro_run_hf.argtypes = lib.fe2_macro_run.argtypes
 
 
 @dataclass
@@ -65,17 +66,35 @@ def macro_gauss(cfg: MacroConfig):
     return B, w, e
 
 
-def solve_program(cfg: MacroConfig, engine: HyperRomEngine, max_rows: int = 256):
-    """Load / unload program on the beam (solve_program). Returns the curve
-    rows (U, R, macro iterations, cumulative micro iterations, wall ms) and
-    the residual displacement U_res of the unloaded beam."""
+def solve_program(cfg: MacroConfig, engine, max_rows: int = 256):
+    """Load / unload program on the beam (solve_program). engine: a
+    HyperRomEngine (hyper-ROM FE²) or a pod.HfRve (full-field HF FE²,
+    nested). Returns the curve rows (U, R, macro iterations, cumulative micro
+    iterations, wall ms) and the residual displacement U_res of the unloaded beam."""
     P = macro_points(cfg)
-    if engine.P != P:
+    if getattr(engine, "P", 0) != P:
         engine.alloc_points(P)
     rows = np.empty((max_rows, 5))
     n, ures = C.c_int(), C.c_double()
-    _check(lib.fe2_macro_run(C.byref(cfg._c()), engine._h, rows.ctypes.data_as(C.POINTER(C.c_double)), max_rows,
-                             C.byref(n), C.byref(ures)))
+    run = lib.fe2_macro_run if isinstance(engine, HyperRomEngine) else lib.fe2_macro_run_hf
+    _check(run(C.byref(cfg._c()), engine._h, rows.ctypes.data_as(C.POINTER(C.c_double)), max_rows, C.byref(n),
+               C.byref(ures)))
     r = rows[:n.value]
     return dict(U=r[:, 0].copy(), R=r[:, 1].copy(), macro_iters=r[:, 2].astype(int),
                 micro_iters=r[:, 3].astype(np.int64), wall_ms=r[:, 4].copy(), U_residual=ures.value)
+
+
+def curve_error(test, ref):
+    """curve_error: max over the common U grid of
+    |R_test - R_ref| / max |R_ref|, both curves interpolated linearly on the
+    load branch (rows up to the peak U)."""
+    def branch(c):
+        k = int(np.argmax(c["U"])) + 1
+        return c["U"][:k], c["R"][:k]
+    Ut, Rt = branch(test)
+    Ur, Rr = branch(ref)
+    lo, hi = max(Ut[0], Ur[0]), min(Ut[-1], Ur[-1])
+    if not hi > lo:
+        raise ValueError("curves do not overlap")
+    grid = np.union1d(Ut[(Ut >= lo) & (Ut <= hi)], Ur[(Ur >= lo) & (Ur <= hi)])
+    return float(np.abs(np.interp(grid, Ut, Rt) - np.interp(grid, Ur, Rr)).max() / np.abs(Rr).max())

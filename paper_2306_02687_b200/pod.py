@@ -58,6 +58,28 @@ class HfRve:
             out["snapshots"] = X
         return out
 
+    # ---- HF engine of an FE² run: P macro points with their own states
+    def alloc_points(self, P):
+        """P macro points in the virgin state (fe2_hf_alloc_points)."""
+        _check(lib.fe2_hf_alloc_points(self._h, P))
+        self.P = P
+
+    def solve_increment(self, E, opts: NewtonOptions | None = None):
+        """One path step for every point from its committed state: E (P,3) ->
+        sigma (P,3), C (P,3,3), iters, status (0 or 1 + ErrorCode)."""
+        E = np.ascontiguousarray(E, dtype=np.float64).reshape(self.P, 3)
+        o = (opts or NewtonOptions())._c()
+        sig, Cm = np.empty((self.P, 3)), np.empty((self.P, 3, 3))
+        it, st = np.empty(self.P, dtype=np.int32), np.empty(self.P, dtype=np.int32)
+        _check(lib.fe2_hf_solve_increment(self._h, _d(E), C.byref(o), _d(sig), _d(Cm), _i(it), _i(st)))
+        return dict(sigma=sig, C=Cm, iters=it, status=st)
+
+    def snapshot(self):
+        _check(lib.fe2_hf_snapshot(self._h))
+
+    def restore(self):
+        _check(lib.fe2_hf_restore(self._h))
+
     def elastic_modes(self):
         """build_elastic_modes (SPEC.md:270-277): (count, n_dofs) orthonormal
         fluctuation responses to unit macro strains; 0 rows for a homogeneous RVE."""
