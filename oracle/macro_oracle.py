@@ -181,7 +181,26 @@ def solve_program(m, engine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, n_load=10, max
         state["fint"], state["E"] = fint, E
         return out
 
+    def Kff_of(C):
+        CB = np.einsum("gij,gjd->gid", C, B)
+        Ke = w[:, None, None] * np.einsum("gia,gib->gab", B, CB)
+        K = np.zeros((nd, nd))
+        np.add.at(K, (gdofs[:, :, None], gdofs[:, None, :]), Ke)
+        return K
+
+    def predict(U):
+        """Δu_f = -K_ff⁻¹ K_fp ΔU with the last accepted state's tangent."""
+        dU = U - u[2 * beam["tip"][0] + 1]
+        if dU == 0.0:
+            return
+        du = np.zeros(nd)
+        for n_ in beam["tip"]:
+            du[2 * n_ + 1] = dU
+        K = Kff_of(state["C_acc"])
+        u[free] += np.linalg.solve(K[np.ix_(free, free)], -(K @ du)[free])
+
     def macro_step(U):
+        predict(U)
         for n_ in beam["tip"]:
             u[2 * n_ + 1] = U
         if mono:
@@ -192,18 +211,21 @@ def solve_program(m, engine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, n_load=10, max
                 return -1
             fint = state["fint"]
             rn, fn = np.linalg.norm(fint[free]), np.linalg.norm(fint)
+            state["C"] = out["C"]
             if rn <= tol * max(fn, state["fscale"], 1e-30) and (not mono or state["micro_ok"]):
                 return k
             if k == max_iter:
                 return -1
-            CB = np.einsum("gij,gjd->gid", out["C"], B)
-            Ke = w[:, None, None] * np.einsum("gia,gib->gab", B, CB)
-            K = np.zeros((nd, nd))
-            np.add.at(K, (gdofs[:, :, None], gdofs[:, None, :]), Ke)
-            Kff = K[np.ix_(free, free)]
+            state["C"] = out["C"]
+            Kff = Kff_of(out["C"])[np.ix_(free, free)]
             u[free] += np.linalg.solve(Kff, -fint[free])
         return -1
 
+    # tangent of the virgin state for the first step's predictor
+    if mono:
+        engine.begin()
+    state["C_acc"] = micro_solve()["C"]
+    state["micro"] = 0
     rows = []
     done_state = dict(U=0.0, u=u.copy())
 
@@ -228,6 +250,7 @@ def solve_program(m, engine, L=4.0, H=1.0, nx=8, ny=2, u_max=0.3, n_load=10, max
                 engine.commit(state["E"])
             state["fscale"] = max(state["fscale"], np.linalg.norm(state["fint"]))
             done_state["U"], done_state["u"] = U, u.copy()
+            state["C_acc"] = state["C"]
             done = target
         R = sum(state["fint"][2 * n_ + 1] for n_ in beam["tip"])
         rows.append((done_state["U"], R, iters, state["micro"]))

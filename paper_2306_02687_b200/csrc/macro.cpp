@@ -314,26 +314,13 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
       }
       return true;
     };
-    // macro Newton for a prescribed tip displacement; returns iterations or -1
-    auto macro_step = [&](double U) -> int {
-      for (int nd_ : m.tip) u[2 * nd_ + 1] = U;
-      if (mono) engine_check(fe2_hrom_mono_begin(engine));
-      for (int k = 0; k <= cfg->max_iter; ++k) {
-        if (!micro_solve()) return -1;
-        double rn = 0.0, fn = 0.0;
-        for (int d = 0; d < nd; ++d) {
-          fn += fint[d] * fint[d];
-          if (role[d] == 0) rn += fint[d] * fint[d];
-        }
-        rn = std::sqrt(rn);
-        fn = std::sqrt(fn);
-        if (rn <= cfg->tol * std::max(std::max(fn, fscale), 1e-30) && micro_ok) return k;
-        if (k == cfg->max_iter) return -1;
+    // K_ff = Σ_g w B_gᵀ C_g B_g over the free DOFs
+    auto assemble_K = [&](const std::vector<double>& Cc) {
         Kff.assign(static_cast<size_t>(nf) * nf, 0.0);
         for (int g = 0; g < P; ++g) {
           const int e = m.elem[g];
           const double* o = Op.data() + static_cast<size_t>(g) * nr * 12;
-          const double* Cg = C.data() + static_cast<size_t>(g) * nr * nr;
+          const double* Cg = Cc.data() + static_cast<size_t>(g) * nr * nr;
           double CB[4][12];
           for (int i = 0; i < nr; ++i)
             for (int d = 0; d < 12; ++d) {
@@ -353,13 +340,66 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
             }
           }
         }
+    };
+    auto solve_K = [&]() {
+      if (kin)
+        check(lu_solve(Kff, nf, rhs), Code::solver, "finite-strain macro tangent is singular");
+      else
+        check(chol_solve(Kff, nf, rhs), Code::solver, "macro tangent is not positive definite");
+    };
+    // Step predictor: the prescribed tip increment ΔU spread over the free DOFs
+    // with the tangent of the last accepted state, Δu_f = -K_ff⁻¹ K_fp ΔU
+    // (keeps the first iterate of a plastic step near the solution).
+    std::vector<double> C_acc;
+    auto predict = [&](double U) {
+      const double dU = U - u[2 * m.tip[0] + 1];
+      if (dU == 0.0 || C_acc.empty()) return;
+      std::vector<double> du(nd, 0.0), fp(nd, 0.0);
+      for (int nd_ : m.tip) du[2 * nd_ + 1] = dU;
+      for (int g = 0; g < P; ++g) {
+        const int e = m.elem[g];
+        const double* o = Op.data() + static_cast<size_t>(g) * nr * 12;
+        const double* Cg = C_acc.data() + static_cast<size_t>(g) * nr * nr;
+        double eg[4] = {0, 0, 0, 0}, sg[4] = {0, 0, 0, 0};
+        for (int i = 0; i < nr; ++i)
+          for (int d = 0; d < 12; ++d) eg[i] += o[i * 12 + d] * du[dofs(e, d)];
+        for (int i = 0; i < nr; ++i)
+          for (int j = 0; j < nr; ++j) sg[i] += Cg[i * nr + j] * eg[j];
+        for (int d = 0; d < 12; ++d) {
+          double t = 0.0;
+          for (int i = 0; i < nr; ++i) t += o[i * 12 + d] * sg[i];
+          fp[dofs(e, d)] += m.w[g] * t;
+        }
+      }
+      assemble_K(C_acc);
+      rhs.assign(nf, 0.0);
+      for (int d = 0; d < nd; ++d)
+        if (fidx[d] >= 0) rhs[fidx[d]] = -fp[d];
+      solve_K();
+      for (int d = 0; d < nd; ++d)
+        if (fidx[d] >= 0) u[d] += rhs[fidx[d]];
+    };
+    // macro Newton for a prescribed tip displacement; returns iterations or -1
+    auto macro_step = [&](double U) -> int {
+      predict(U);
+      for (int nd_ : m.tip) u[2 * nd_ + 1] = U;
+      if (mono) engine_check(fe2_hrom_mono_begin(engine));
+      for (int k = 0; k <= cfg->max_iter; ++k) {
+        if (!micro_solve()) return -1;
+        double rn = 0.0, fn = 0.0;
+        for (int d = 0; d < nd; ++d) {
+          fn += fint[d] * fint[d];
+          if (role[d] == 0) rn += fint[d] * fint[d];
+        }
+        rn = std::sqrt(rn);
+        fn = std::sqrt(fn);
+        if (rn <= cfg->tol * std::max(std::max(fn, fscale), 1e-30) && micro_ok) return k;
+        if (k == cfg->max_iter) return -1;
+        assemble_K(C);
         rhs.assign(nf, 0.0);
         for (int d = 0; d < nd; ++d)
           if (fidx[d] >= 0) rhs[fidx[d]] = -fint[d];
-        if (kin)
-          check(lu_solve(Kff, nf, rhs), Code::solver, "finite-strain macro tangent is singular");
-        else
-          check(chol_solve(Kff, nf, rhs), Code::solver, "macro tangent is not positive definite");
+        solve_K();
         for (int d = 0; d < nd; ++d)
           if (fidx[d] >= 0) u[d] += rhs[fidx[d]];
       }
@@ -374,6 +414,11 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
       engine_check(fe2_hf_alloc_points(hf, P));
       engine_check(fe2_hf_snapshot(hf));
     }
+    // tangent of the virgin state (u = 0) for the first step's predictor
+    if (mono) engine_check(fe2_hrom_mono_begin(engine));
+    check(micro_solve(), Code::solver, "micro solve at the virgin state failed");
+    C_acc = C;
+    micro_total = 0;
     int nrow = 0;
     double U_done = 0.0;
     std::vector<double> u_done = u;
@@ -409,6 +454,7 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
         }
         u_done = u;
         U_done = U;
+        C_acc = C;
         done = target;
       }
       check(nrow < max_rows, Code::config, "curve buffer too small");

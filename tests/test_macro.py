@@ -61,7 +61,9 @@ def test_oracle_driver_plastic_residual_displacement(desk_hrom):
     secant = load[:, 1] / load[:, 0]
     assert secant[-1] < 0.98 * secant[0]  # yielding softens the response
     assert 0.0 < ures < 0.3
-    assert (rows[:, 2] >= 1).all()
+    # the step predictor (last accepted tangent) is exact for elastic steps;
+    # plastic loading steps still iterate
+    assert (rows[:, 2] >= 0).all() and load[:, 2].max() >= 1
 
 
 def test_oracle_finite_strain_driver_small_load_limit():
