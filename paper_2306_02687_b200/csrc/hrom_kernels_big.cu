@@ -9,10 +9,16 @@
 //    of ε_q = E + G_q α and reduce with shuffles; one lane runs the elastic
 //    trial / yield test / radial return.
 //  - Plastic points of a chunk are compacted CTA-wide (ballot + warp prefix,
-//    deterministic order) and contracted on the FP64 tensor cores (DMMA):
-//    the NT(NT+1)/2 upper tile pairs of K_aa are split over the 8 warps in
-//    2x2 / 4x4 tile blocks so each warp loads few distinct fragments; the
-//    K_aE and r corrections are scalar (O(n) per point).
+//    deterministic order); each plastic slot's operand rows are then staged
+//    once in shared memory — A rows G_q (3 x NP) and B rows (w ΔC_q) G_q —
+//    with a row stride of NP + 4 doubles (≡ 4 or 12 mod 16), so every DMMA
+//    fragment is ONE conflict-free 64-bit shared load (the staging area
+//    aliases K_aa, which is dead during an assembly pass).
+//  - The NT(NT+1)/2 upper tile pairs of K_aa are contracted on the FP64
+//    tensor cores (DMMA) in register blocks balanced over the warps at
+//    compile time (largest-first), fragments prefetched one k-step ahead;
+//    the K_aE and r corrections ride on the diagonal-tile owners' fragments
+//    (NT <= 8) or are summed from the staged rows.
 //  - Newton / line search / bisection / condensation run CTA-wide:
 //    left-looking Cholesky of the packed K_aa with one row per thread.
 #include "device_common.cuh"
@@ -51,14 +57,20 @@ struct Big {
   static constexpr int S = 3 * NP + 2;
   static constexpr int chunk = QB * S;
   static constexpr int TRI = NP * (NP + 1) / 2;
+  static constexpr int RS = NP + 4;           // staged row stride (≡ 4 or 12 mod 16 doubles)
+  static constexpr int STG = 2 * 3 * QB * RS;  // staged A rows | B rows
+  static constexpr int KREG = TRI > STG ? TRI : STG;
   static constexpr int RED = 64;
-  // doubles: ring[2][chunk] | sK[TRI] | vectors 9 NP | slots QB*(6+3) + QB ints | red
-  static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + TRI + 9 * NP + QB * 10 + RED;
+  // doubles: ring[2][chunk] | sK[TRI] ∪ stage[STG] | vectors 9 NP | slots QB*(6+3) + QB ints | red
+  static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + KREG + 9 * NP + QB * 10 + RED;
   static constexpr size_t bytes = dbl * sizeof(double) + 2 * sizeof(uint64_t) + 16 * sizeof(int);
 };
 
-// Tile pairs (t1 <= t2) of one warp: upper-triangle tile blocks of size b,
-// dealt round-robin to the 8 warps (compile time).
+// Tile pairs (t1 <= t2) of one warp. The upper triangle is cut into tile
+// blocks (b x b; for NT = 8 the off-diagonal block is split into two 2 x 4
+// halves) and the blocks are dealt largest-first to the least-loaded warp, so
+// the DMMA count per warp is balanced and each warp reuses its fragments
+// across a block (NT = 8, 4 warps: 10/10/8/8 pairs from 8/8/6/6 loads).
 struct PairTable {
   int n;
   int t1[160];
@@ -66,21 +78,55 @@ struct PairTable {
 };
 template <int NT>
 constexpr PairTable pairs_for(int W) {
-  PairTable P{};
-  const int b = NT >= 12 ? 4 : 2;
+  constexpr int BW = bw_for(NT);
+  const int b = (NT == 8 || NT == 16) ? 4 : 2;
+  const bool split = NT == 8;
   const int nb = (NT + b - 1) / b;
-  int blk = 0;
+  // blocks as (row tiles [r0, r1), col tiles [c0, c1)), pair count
+  int r0[64] = {}, r1[64] = {}, c0[64] = {}, c1[64] = {}, cnt[64] = {}, nbk = 0;
   for (int B1 = 0; B1 < nb; ++B1)
-    for (int B2 = B1; B2 < nb; ++B2, ++blk) {
-      if (blk % bw_for(NT) != W) continue;
-      for (int t1 = B1 * b; t1 < B1 * b + b && t1 < NT; ++t1)
-        for (int t2 = B2 * b; t2 < B2 * b + b && t2 < NT; ++t2)
-          if (t1 <= t2) {
-            P.t1[P.n] = t1;
-            P.t2[P.n] = t2;
-            ++P.n;
-          }
+    for (int B2 = B1; B2 < nb; ++B2) {
+      const int ra = B1 * b, rb = (B1 * b + b < NT) ? B1 * b + b : NT;
+      const int ca = B2 * b, cb = (B2 * b + b < NT) ? B2 * b + b : NT;
+      const int parts = (split && B1 != B2) ? 2 : 1;
+      const int h = (rb - ra + parts - 1) / parts;
+      for (int s = 0; s < parts; ++s) {
+        r0[nbk] = ra + s * h;
+        r1[nbk] = (ra + s * h + h < rb) ? ra + s * h + h : rb;
+        c0[nbk] = ca;
+        c1[nbk] = cb;
+        int c = 0;
+        for (int t1 = r0[nbk]; t1 < r1[nbk]; ++t1)
+          for (int t2 = c0[nbk]; t2 < c1[nbk]; ++t2) c += t1 <= t2 ? 1 : 0;
+        cnt[nbk] = c;
+        ++nbk;
+      }
     }
+  // largest-first to the least-loaded warp (ties: lowest index)
+  int load[8] = {}, owner[64] = {};
+  bool done[64] = {};
+  for (int k = 0; k < nbk; ++k) {
+    int best = -1;
+    for (int j = 0; j < nbk; ++j)
+      if (!done[j] && (best < 0 || cnt[j] > cnt[best])) best = j;
+    done[best] = true;
+    int w = 0;
+    for (int v = 1; v < BW; ++v)
+      if (load[v] < load[w]) w = v;
+    owner[best] = w;
+    load[w] += cnt[best];
+  }
+  PairTable P{};
+  for (int j = 0; j < nbk; ++j) {
+    if (owner[j] != W) continue;
+    for (int t1 = r0[j]; t1 < r1[j]; ++t1)
+      for (int t2 = c0[j]; t2 < c1[j]; ++t2)
+        if (t1 <= t2) {
+          P.t1[P.n] = t1;
+          P.t2[P.n] = t2;
+          ++P.n;
+        }
+  }
   return P;
 }
 template <int NT>
@@ -91,6 +137,24 @@ constexpr int max_pairs() {
     m = c > m ? c : m;
   }
   return m;
+}
+template <int NT>
+constexpr int total_pairs() {
+  int m = 0;
+  for (int w = 0; w < bw_for(NT); ++w) m += pairs_for<NT>(w).n;
+  return m;
+}
+static_assert(total_pairs<5>() == 15 && total_pairs<8>() == 36 && total_pairs<12>() == 78 &&
+                  total_pairs<16>() == 136,
+              "tile-pair partition must cover the upper triangle");
+static_assert(max_pairs<8>() == 10 && max_pairs<16>() == 20, "unexpected partition balance");
+
+// non-volatile DMMA (pure in its operands: the scheduler may interleave the
+// fragment loads of the next k-step)
+__device__ __forceinline__ void dmma_nv(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
 // CTA-wide sum (all threads get the result); red has >= BW + 1 doubles.
@@ -114,7 +178,7 @@ __device__ __forceinline__ void dmma_pairs(double (&acc)[MP][2], const double (&
   if constexpr (J < pairs_for<NT>(W).n) {
     constexpr int t1 = pairs_for<NT>(W).t1[J];
     constexpr int t2 = pairs_for<NT>(W).t2[J];
-    dmma(acc[J][0], acc[J][1], A[t1], B[t2]);
+    dmma_nv(acc[J][0], acc[J][1], A[t1], B[t2]);
     dmma_pairs<NT, W, J + 1, MP>(acc, A, B);
   }
 }
@@ -149,14 +213,14 @@ constexpr bool uses_col(int W, int t) {
     if (P.t2[j] == t) return true;
   return false;
 }
+// fragments of one k-step from the staged rows: A[T] = A row (lane's k) at
+// mode 8T + col, B[T] likewise (only the tiles warp W uses are loaded)
 template <int NT, int W, int T>
-__device__ __forceinline__ void load_frags(const double* gp, int i, double k0, double k1, double k2, double (&A)[NT],
-                                           double (&B)[NT]) {
+__device__ __forceinline__ void load_frags(const double* pa, const double* pb, double (&A)[NT], double (&B)[NT]) {
   if constexpr (T < NT) {
-    constexpr int NP = 8 * NT;
-    if constexpr (uses_row<NT>(W, T)) A[T] = gp[i * NP + T * 8];
-    if constexpr (uses_col<NT>(W, T)) B[T] = k0 * gp[T * 8] + k1 * gp[NP + T * 8] + k2 * gp[2 * NP + T * 8];
-    load_frags<NT, W, T + 1>(gp, i, k0, k1, k2, A, B);
+    if constexpr (uses_row<NT>(W, T)) A[T] = pa[T * 8];
+    if constexpr (uses_col<NT>(W, T)) B[T] = pb[T * 8];
+    load_frags<NT, W, T + 1>(pa, pb, A, B);
   }
 }
 
@@ -189,30 +253,47 @@ __device__ __forceinline__ void diag_acc(const double (&A)[NT], const double (&B
   }
 }
 
-// DMMA over the chunk's plastic slots for warp W's tile pairs.
+// DMMA over the chunk's staged plastic rows for warp W's tile pairs: k-step
+// ks covers staged rows 4ks..4ks+3 (row f = 3 slot + strain row i); lane
+// (m, col) reads row 4ks + m. The three k-steps of a group of four slots are
+// unrolled (the K_aE row of lane m is (s + m) mod 3 at k-step s of the group)
+// and the next k-step's fragments are loaded before the current DMMAs.
 template <int NT, int W, int MP>
-__device__ __forceinline__ void contract(const double* Gb, const double* sDC, const double* sDS, const int* sQ,
-                                         int np4, double (&acc)[MP][2], double (&kae)[NT][3], double (&rr)[NT],
-                                         int lane) {
-  constexpr int S = Big<NT>::S;
+__device__ __forceinline__ void contract(const double* stA, const double* stB, const double* sDS, int np4,
+                                         double (&acc)[MP][2], double (&kae)[NT][3], double (&rr)[NT], int lane) {
+  constexpr int RS = Big<NT>::RS;
   const int m = lane & 3, col = lane >> 2;
   const int ng = np4 >> 2;
+  const double* pa = stA + m * RS + col;
+  const double* pb = stB + m * RS + col;
+  const double* pw = sDS + m;
+  if constexpr (NT > 8 || NT == 6) {  // no room for a prefetch set in the registers (ptxas -v)
+#pragma unroll 1
+    for (int g = 0; g < ng; ++g) {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int f = 12 * g + 4 * s;
+        double A[NT], B[NT];
+        load_frags<NT, W, 0>(pa + f * RS, pb + f * RS, A, B);
+        dmma_pairs<NT, W, 0, MP>(acc, A, B);
+      }
+    }
+    return;
+  }
+  double A0[NT], B0[NT], A1[NT], B1[NT], A2[NT], B2[NT];
+  if (ng > 0) load_frags<NT, W, 0>(pa, pb, A0, B0);
 #pragma unroll 1
   for (int g = 0; g < ng; ++g) {
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      const int slot = 4 * g + (4 * s + m) / 3;
-      const int i = (4 * s + m) % 3;
-      const int bb = i > 0 ? 1 : 0;
-      const double* wc = sDC + slot * 6;
-      const double k0 = wc[i], k1 = wc[i + 1 + bb], k2 = wc[i + 2 + bb];
-      const double ws = sDS[slot * 3 + i];
-      const double* gp = Gb + sQ[slot] * S + col;
-      double A[NT], B[NT];
-      load_frags<NT, W, 0>(gp, i, k0, k1, k2, A, B);
-      dmma_pairs<NT, W, 0, MP>(acc, A, B);
-      diag_acc<NT, W, 0>(A, B, ws, s, kae, rr);
-    }
+    const int f = 12 * g;  // first staged row of the group
+    load_frags<NT, W, 0>(pa + (f + 4) * RS, pb + (f + 4) * RS, A1, B1);
+    dmma_pairs<NT, W, 0, MP>(acc, A0, B0);
+    diag_acc<NT, W, 0>(A0, B0, pw[f], 0, kae, rr);
+    load_frags<NT, W, 0>(pa + (f + 8) * RS, pb + (f + 8) * RS, A2, B2);
+    dmma_pairs<NT, W, 0, MP>(acc, A1, B1);
+    diag_acc<NT, W, 0>(A1, B1, pw[f + 4], 1, kae, rr);
+    if (g + 1 < ng) load_frags<NT, W, 0>(pa + (f + 12) * RS, pb + (f + 12) * RS, A0, B0);
+    dmma_pairs<NT, W, 0, MP>(acc, A2, B2);
+    diag_acc<NT, W, 0>(A2, B2, pw[f + 8], 2, kae, rr);
   }
 }
 
@@ -254,18 +335,18 @@ __device__ __forceinline__ void store_tiles(double* sK, const double (&acc)[MP][
 }
 
 template <int NT, int MP>
-__device__ __forceinline__ void contract_dispatch(int warp, const double* Gb, const double* sDC, const double* sDS,
-                                                  const int* sQ, int np4, double (&acc)[MP][2],
-                                                  double (&kae)[NT][3], double (&rr)[NT], int lane) {
+__device__ __forceinline__ void contract_dispatch(int warp, const double* stA, const double* stB, const double* sDS,
+                                                  int np4, double (&acc)[MP][2], double (&kae)[NT][3],
+                                                  double (&rr)[NT], int lane) {
   switch (warp) {
-    case 0: contract<NT, 0, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
-    case 1: contract<NT, 1, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
-    case 2: contract<NT, 2, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
-    case 3: contract<NT, 3, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
-    case 4: contract<NT, 4, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
-    case 5: contract<NT, 5, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
-    case 6: contract<NT, 6, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
-    default: contract<NT, 7, MP>(Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane); break;
+    case 0: contract<NT, 0, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 1: contract<NT, 1, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 2: contract<NT, 2, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 3: contract<NT, 3, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 4: contract<NT, 4, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 5: contract<NT, 5, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 6: contract<NT, 6, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
+    default: contract<NT, 7, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
   }
 }
 template <int NT>
@@ -391,7 +472,9 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
   double* sK = ring + 2 * static_cast<size_t>(L::chunk);
-  double* sAev = sK + L::TRI;
+  double* stA = sK;                      // staged rows alias sK (dead during an assembly pass)
+  double* stB = sK + 3 * QB * L::RS;
+  double* sAev = sK + L::KREG;
   double* sAl = sAev + NP;
   double* sDA = sAl + NP;
   double* sV = sDA + NP;
@@ -588,18 +671,37 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       n_pl += static_cast<unsigned long long>(tid == 0 ? np : 0);
       np_tot += np;
       __syncthreads();
-      contract_dispatch<NT, MP>(warp, Gb, sDC, sDS, sQ, np4, acc, kae, rr, lane);
+      // stage the slots' operand rows: A = G_q (3 rows), B = (w ΔC_q) G_q;
+      // warp w stages slots w, w + BW, ... (lanes over the modes)
+      for (int sl = warp; sl < np4; sl += L::BW) {
+        const double* dc = sDC + sl * 6;
+        const double d00 = dc[0], d01 = dc[1], d02 = dc[2], d11 = dc[3], d12 = dc[4], d22 = dc[5];
+        const double* Gq = Gb + sQ[sl] * S;
+        double* ar = stA + 3 * sl * L::RS;
+        double* br = stB + 3 * sl * L::RS;
+#pragma unroll
+        for (int a = lane; a < NP; a += 32) {
+          const double g0 = Gq[a], g1 = Gq[NP + a], g2 = Gq[2 * NP + a];
+          ar[a] = g0;
+          ar[L::RS + a] = g1;
+          ar[2 * L::RS + a] = g2;
+          br[a] = d00 * g0 + d01 * g1 + d02 * g2;
+          br[L::RS + a] = d01 * g0 + d11 * g1 + d12 * g2;
+          br[2 * L::RS + a] = d02 * g0 + d12 * g1 + d22 * g2;
+        }
+      }
+      __syncthreads();
+      contract_dispatch<NT, MP>(warp, stA, stB, sDS, np4, acc, kae, rr, lane);
       if constexpr (!kFragCorr<NT>) {
-        if (tid < NP) {  // r and K_aE corrections of mode a = tid
+        if (tid < NP) {  // r and K_aE corrections of mode a = tid, from the staged rows
           for (int sl = 0; sl < np; ++sl) {
-            const double* Gq = Gb + sQ[sl] * S + tid;
-            const double g0 = Gq[0], g1 = Gq[NP], g2 = Gq[2 * NP];
-            const double* dc = sDC + sl * 6;
+            const double* ar = stA + 3 * sl * L::RS + tid;
+            const double* br = stB + 3 * sl * L::RS + tid;
             const double* ds = sDS + sl * 3;
-            rm += g0 * ds[0] + g1 * ds[1] + g2 * ds[2];
-            ka0 += g0 * dc[0] + g1 * dc[1] + g2 * dc[2];
-            ka1 += g0 * dc[1] + g1 * dc[3] + g2 * dc[4];
-            ka2 += g0 * dc[2] + g1 * dc[4] + g2 * dc[5];
+            rm += ar[0] * ds[0] + ar[L::RS] * ds[1] + ar[2 * L::RS] * ds[2];
+            ka0 += br[0];
+            ka1 += br[L::RS];
+            ka2 += br[2 * L::RS];
           }
         }
       }
