@@ -60,7 +60,7 @@ struct Big {
   static constexpr int RS = NP + 4;           // staged row stride (≡ 4 or 12 mod 16 doubles)
   static constexpr int STG = 2 * 3 * QB * RS;  // staged A rows | B rows
   static constexpr int KREG = TRI > STG ? TRI : STG;
-  static constexpr int RED = 64;
+  static constexpr int RED = 128;  // >= BW * 12 (block_sum_n)
   // doubles: ring[2][chunk] | sK[TRI] ∪ stage[STG] | vectors 9 NP | slots QB*(6+3) + QB ints | red
   static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + KREG + 9 * NP + QB * 10 + RED;
   static constexpr size_t bytes = dbl * sizeof(double) + 2 * sizeof(uint64_t) + 16 * sizeof(int);
@@ -388,6 +388,28 @@ __device__ __forceinline__ void rows_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
 }
 
+// CTA-wide sums of N values at once (two barriers in all; the same summation
+// order as block_sum for each value). red has >= BW * N doubles.
+template <int BW, int N>
+__device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = warp_sum(v[k]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) red[warp * N + k] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < BW; ++w) s += red[w * N + k];
+    v[k] = s;
+  }
+}
+
 // Left-looking Cholesky of the packed lower sK. False (CTA-uniform) if not SPD.
 template <int NW, int BW>
 __device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
@@ -534,14 +556,17 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   };
   // strain of this thread's cubature point (threads of a point split the modes)
   auto strain = [&](const double* Gb, double E0, double E1, double E2, double& e0, double& e1, double& e2) {
-    const double* Gq = Gb + qi * S;
+    // 128-bit loads of mode pairs (2j, 2j+1); rows are 16-B aligned (S, NP even)
+    const double2* Gq = reinterpret_cast<const double2*>(Gb + qi * S);
+    const double2* al2 = reinterpret_cast<const double2*>(sAev);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll 4
-    for (int a = sub; a < NP; a += TPQ) {
-      const double al = sAev[a];
-      a0 += Gq[a] * al;
-      a1 += Gq[NP + a] * al;
-      a2 += Gq[2 * NP + a] * al;
+#pragma unroll
+    for (int j = sub; j < NP / 2; j += TPQ) {
+      const double2 al = al2[j];
+      const double2 g0 = Gq[j], g1 = Gq[NP / 2 + j], g2 = Gq[NP + j];
+      a0 += g0.x * al.x + g0.y * al.y;
+      a1 += g1.x * al.x + g1.y * al.y;
+      a2 += g2.x * al.x + g2.y * al.y;
     }
 #pragma unroll
     for (int o = TPQ / 2; o > 0; o >>= 1) {
@@ -575,6 +600,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   double dsp0 = 0, dsp1 = 0, dsp2 = 0;  // plastic parts of Σraw
   int np_last = 0;
   bool k_linear = false;
+  double rn_pass = 0.0;  // |r| of the last pass
 
   auto assembly_pass = [&](int64_t p, double E0, double E1, double E2) {
     double acc[MP][2];
@@ -672,7 +698,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       np_tot += np;
       __syncthreads();
       // stage the slots' operand rows: A = G_q (3 rows), B = (w ΔC_q) G_q;
-      // warp w stages slots w, w + BW, ... (lanes over the modes)
+      // warp w stages slots w, w + BW, ... (lanes over the modes). (Giving
+      // the warps without diagonal corrections more slots was slower.)
       for (int sl = warp; sl < np4; sl += L::BW) {
         const double* dc = sDC + sl * 6;
         const double d00 = dc[0], d01 = dc[1], d02 = dc[2], d11 = dc[3], d12 = dc[4], d22 = dc[5];
@@ -717,18 +744,22 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       sKaE[tid * 3 + 1] = ka1;
       sKaE[tid * 3 + 2] = ka2;
     }
-    c00 = block_sum<L::BW>(c00, red);
-    c01 = block_sum<L::BW>(c01, red);
-    c02 = block_sum<L::BW>(c02, red);
-    c11 = block_sum<L::BW>(c11, red);
-    c12 = block_sum<L::BW>(c12, red);
-    c22 = block_sum<L::BW>(c22, red);
-    ds0 = block_sum<L::BW>(ds0, red);
-    ds1 = block_sum<L::BW>(ds1, red);
-    ds2 = block_sum<L::BW>(ds2, red);
-    __syncthreads();
+    // one CTA reduction for the nine plastic sums and the elastic Σ part
+    // (its barriers also publish sK / sRp / sKaE)
+    double rs[12] = {c00, c01, c02, c11, c12, c22, ds0, ds1, ds2, 0.0, 0.0, 0.0};
+    if (tid < n) {
+      const double* ke = M.KaEe + tid * 3;
+      const double al = sAev[tid];
+      rs[9] = ke[0] * al;
+      rs[10] = ke[1] * al;
+      rs[11] = ke[2] * al;
+    }
+    block_sum_n<L::BW, 12>(rs, red);
+    c00 = rs[0], c01 = rs[1], c02 = rs[2], c11 = rs[3], c12 = rs[4], c22 = rs[5];
+    ds0 = rs[6], ds1 = rs[7], ds2 = rs[8];
+    const double sa0 = rs[9], sa1 = rs[10], sa2 = rs[11];
     // elastic predictor part and b_p, s_p (thread a = mode)
-    double sa0 = 0.0, sa1 = 0.0, sa2 = 0.0;
+    double rl = 0.0;
     if (tid < n) {
       const int a = tid;
       const double* ke = M.KaEe + a * 3;
@@ -739,17 +770,13 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
         sx += k0 * sAev[b];
         if (b <= a) ka[b] += k0;
       }
-      sV[a] = sRp[a] + sx + (ke[0] * E0 + ke[1] * E1 + ke[2] * E2) - D.bp[p * NP + a];
+      rl = sRp[a] + sx + (ke[0] * E0 + ke[1] * E1 + ke[2] * E2) - D.bp[p * NP + a];
+      sV[a] = rl;
       sKaE[a * 3 + 0] += ke[0];
       sKaE[a * 3 + 1] += ke[1];
       sKaE[a * 3 + 2] += ke[2];
-      sa0 = ke[0] * sAev[a];
-      sa1 = ke[1] * sAev[a];
-      sa2 = ke[2] * sAev[a];
     }
-    sa0 = block_sum<L::BW>(sa0, red);
-    sa1 = block_sum<L::BW>(sa1, red);
-    sa2 = block_sum<L::BW>(sa2, red);
+    rn_pass = sqrt(block_sum<L::BW>(rl * rl, red));  // also publishes sK, sV, sKaE
     const double* ce = M.CEEe;
     const double* spp = D.sp + p * 4;
     s0 = ds0 + sa0 + (ce[0] * E0 + ce[1] * E1 + ce[2] * E2) - spp[0];
@@ -767,7 +794,6 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
     np_last = np_tot;
     k_linear = (np_tot == 0);
     ++n_asm;
-    __syncthreads();
   };
 
   auto factor = [&]() -> bool {
@@ -777,7 +803,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       __syncthreads();
       return true;
     }
-    return cta_cholesky<(NP + 31) / 32, L::BW>(sK, sInv, red, n);
+    return cta_cholesky<(NP + 31) / 32, L::BW>(sK, sInv, red + L::RED - 2, n);  // clear of block sums
   };
 
   // accept the last pass's state: flip to its candidate history, α_c, and move
@@ -878,8 +904,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       double a = 1.0, rn_it = 0.0, best_rn = 0.0, best_a = 1.0, ref = 0.0, done = 0.0, frac = 1.0;
       while (true) {
         assembly_pass(p, E0, E1, E2);
-        const double rl = (tid < n) ? sV[tid] : 0.0;
-        const double rn = sqrt(block_sum<L::BW>(rl * rl, red));
+        const double rn = rn_pass;
         const double srn = sqrt(s0 * s0 + s1 * s1 + s2 * s2);
         int action = 0;  // 0 assemble again, 1 final commit, 2 sub-step commit, 3 failed
         for (int pass = 0; pass < 2; ++pass) {
@@ -903,9 +928,9 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
                   x1 = sKaE[tid * 3 + 1];
                   x2 = sKaE[tid * 3 + 2];
                 }
-                const double q00 = block_sum<L::BW>(x0 * x0, red), q01 = block_sum<L::BW>(x0 * x1, red);
-                const double q02 = block_sum<L::BW>(x0 * x2, red), q11 = block_sum<L::BW>(x1 * x1, red);
-                const double q12 = block_sum<L::BW>(x1 * x2, red), q22 = block_sum<L::BW>(x2 * x2, red);
+                double qs[6] = {x0 * x0, x0 * x1, x0 * x2, x1 * x1, x1 * x2, x2 * x2};
+                block_sum_n<L::BW, 6>(qs, red);
+                const double q00 = qs[0], q01 = qs[1], q02 = qs[2], q11 = qs[3], q12 = qs[4], q22 = qs[5];
                 if (tid == 0) {
                   const double V = M.volume;
                   double* Cp = A.O.C + p * 9;
