@@ -206,6 +206,9 @@ def rank_points(cfg, ws, rank):
     return cfg["P"], rank * cfg["P"]
 
 
+COMM = [None]  # this rank's NCCL communicator (fe2_nccl_comm_init), N > 1
+
+
 class DeviceRun:
     """One config on this rank: model, engine, device-resident path and outputs."""
 
@@ -235,18 +238,17 @@ class DeviceRun:
         self.gathered = None
 
     def gather(self, dist, ws, sig, C, res, st):
-        """All-gather (Σ | P, C | A, residual norm, status) of every point."""
+        """The monolithic scheme's exchange: all-gather (Σ | P, C | A, residual
+        norm, status) of every point over NCCL through the engine's C ABI
+        (fe2_hrom_gather: device-side packing into this rank's block,
+        in-place ncclAllGather, max all-reduce of the failure flag)."""
         if ws == 1:
             return
         if self.gathered is None:
             self.gathered = self.torch.empty((ws,) + tuple(self.pack.shape), dtype=self.pack.dtype,
                                              device=self.dev)
-        nc, nt = self.nc, self.nt
-        self.pack[:, 0:nc] = sig
-        self.pack[:, nc:nc + nt] = C
-        self.pack[:, nc + nt] = res
-        self.pack[:, nc + nt + 1] = st.to(self.torch.float64)
-        dist.all_gather_into_tensor(self.gathered, self.pack)
+        self.any_failed = self.eng.gather(COMM[0], self.gathered.data_ptr(), sig.data_ptr(), C.data_ptr(),
+                                          res.data_ptr(), st.data_ptr())
 
     def device_step(self, dist, ws):
         self.eng.reset_points()
@@ -303,6 +305,10 @@ def main():
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
+        # the engine's own NCCL communicator for the per-increment exchange
+        uid = [F.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        COMM[0] = F.NcclComm(local, ws, rank, uid[0])
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -452,6 +458,7 @@ def main():
 
     if rank != 0:
         if ws > 1:
+            COMM[0].close()
             dist.destroy_process_group()
         return
 
@@ -521,6 +528,7 @@ def main():
     }
     print(json.dumps(line), flush=True)
     if ws > 1:
+        COMM[0].close()
         dist.destroy_process_group()
 
 

@@ -159,6 +159,34 @@ int fe2_hrom_solve_increment_device(fe2_hrom_t h, const double* d_E, const fe2_n
                                     double* d_sigma, double* d_C, int* d_iters, int* d_plastic_count,
                                     double* d_res_norm, int* d_status, void* stream);
 
+/* ---- multi-GPU exchange of the monolithic scheme ----
+ * Points are sharded in contiguous equal blocks over the ranks of one box,
+ * one handle per device; the engines never communicate during assembly,
+ * factorisation or condensation. After an increment (or monolithic macro
+ * iteration) every rank needs every point's condensed response, so the only
+ * collective is an NCCL all-gather of per-point records over NVLink, plus a
+ * max all-reduce of "some point failed" for lockstep termination.
+ * libnccl.so.2 is dlopen'ed at first use (no link-time dependency).
+ *   fe2_nccl_get_unique_id: rank 0 creates the 128-byte id, the caller
+ *     broadcasts it (MPI, torch.distributed, a file ...);
+ *   fe2_nccl_comm_init / _destroy: one communicator per rank and device.
+ * fe2_hrom_gather packs this rank's P_local records
+ *   {Σ (nc) | C_macro (nt) | ‖r‖ | status} — nc, nt = 3, 9 small strain
+ *   (14 doubles per point), 4, 16 finite strain (P_M, A_M) —
+ * from the given device outputs of the last increment (NULL = the handle's
+ * own buffers, fe2_hrom_output_ptrs) into d_all[rank], all-gathers in place
+ * into d_all [world][P_local][nc + nt + 2] (device, doubles; P_local must be
+ * equal on every rank) and writes the all-reduced failure flag to
+ * *any_failed (host). Ordered on the handle's stream, which it synchronises.
+ * Replaces nothing in the reference (its RVE solves run in one process,
+ * SPEC.md:247, :511); the records are what fe2.macro_step consumes
+ * (SPEC.md:474-481). Errors: ErrorCode::rank for NCCL failures. */
+int fe2_nccl_get_unique_id(void* id128);
+int fe2_nccl_comm_init(int device, int nranks, int rank, const void* id128, void** comm);
+int fe2_nccl_comm_destroy(void* comm);
+int fe2_hrom_gather(fe2_hrom_t h, void* comm, const double* d_sigma, const double* d_C, const double* d_res_norm,
+                    const int* d_status, double* d_all, int* any_failed);
+
 /* Committed state readback (host): alpha[P*n], state[P*K*6] in the caller's
  * cubature order (elastic-material points report eps_p = 0, eq = 0 and the
  * sigma33 of their last commit), flags[P*K] (needs keep_flags). Nullable. */

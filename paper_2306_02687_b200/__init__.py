@@ -19,7 +19,9 @@ from .hrom import (  # noqa: F401
     NewtonOptions,
     PowerLawParams,
     device_count,
+    NcclComm,
     lib,
+    nccl_unique_id,
     make_paths,
     update_material_batch,
     write_mesh,

@@ -60,4 +60,9 @@ inline void require_engine_material(const MatDev& m) {
         "fe2_material_update_batch and the HF solver");
 }
 
+// exchange.cu: pack the per-point records {Σ | C | ‖r‖ | status} into this
+// rank's block of d_all, NCCL all-gather in place, max-reduce the failure flag.
+void exchange_records(int device, cudaStream_t stream, void* comm, int64_t P, int nc, int nt, const double* d_sigma,
+                      const double* d_C, const double* d_res, const int* d_status, double* d_all, int* any_failed);
+
 }  // namespace fe2

@@ -941,6 +941,16 @@ int fe2_hrom_reset_stats(fe2_hrom_t h) {
   });
 }
 
+int fe2_hrom_gather(fe2_hrom_t h, void* comm, const double* d_sigma, const double* d_C, const double* d_res_norm,
+                    const int* d_status, double* d_all, int* any_failed) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated");
+    exchange_records(h->device, h->stream, comm, h->P, h->ncomp(), h->ntan(), d_sigma ? d_sigma : h->o_sigma,
+                     d_C ? d_C : h->o_C, d_res_norm ? d_res_norm : h->o_res, d_status ? d_status : h->o_status, d_all,
+                     any_failed);
+  });
+}
+
 int fe2_hrom_set_stream(fe2_hrom_t h, void* stream) {
   return guard([&] {
     check(h != nullptr, Code::config, "bad arguments");

@@ -99,6 +99,10 @@ def _load():
     L.fe2_hrom_mono_commit.argtypes = [C.c_void_p]
     L.fe2_hrom_restore.argtypes = [C.c_void_p]
     L.fe2_hrom_output_ptrs.argtypes = [C.c_void_p] + [C.POINTER(C.c_void_p)] * 6
+    L.fe2_nccl_get_unique_id.argtypes = [C.c_void_p]
+    L.fe2_nccl_comm_init.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+    L.fe2_nccl_comm_destroy.argtypes = [C.c_void_p]
+    L.fe2_hrom_gather.argtypes = [C.c_void_p] * 7 + [_ip]
     L.fe2_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.fe2_model_build_from_mesh.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.fe2_mesh_write.argtypes = [C.c_int, C.c_char_p]
@@ -283,6 +287,38 @@ def make_paths(kind, seed, P, n_incr, p0=0):
     return E
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id (rank 0 makes it; broadcast it to the other ranks)."""
+    buf = C.create_string_buffer(128)
+    _check(lib.fe2_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+class NcclComm:
+    """One NCCL communicator per rank and device (fe2_nccl_comm_init)."""
+
+    def __init__(self, device: int, nranks: int, rank: int, uid: bytes):
+        assert len(uid) == 128
+        self.nranks, self.rank = nranks, rank
+        self._c = C.c_void_p()
+        _check(lib.fe2_nccl_comm_init(device, nranks, rank, C.create_string_buffer(uid, 128), C.byref(self._c)))
+
+    @property
+    def ptr(self):
+        return self._c.value
+
+    def close(self):
+        if self._c.value:
+            _check(lib.fe2_nccl_comm_destroy(self._c))
+            self._c = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class HyperRomEngine:
     """One device's batch of macro Gauss points evaluated with a hyper-ROM
     RVE model: the reduced form of run_trajectory (rve.hpp:448-494) per
@@ -361,6 +397,17 @@ class HyperRomEngine:
         ps = [C.c_void_p() for _ in range(6)]
         _check(lib.fe2_hrom_output_ptrs(self._h, *[C.byref(p) for p in ps]))
         return [p.value for p in ps]
+
+    def gather(self, comm: "NcclComm", d_all: int, sigma=0, Cm=0, res=0, status=0) -> bool:
+        """fe2_hrom_gather: all-gather every rank's records {Σ | C | ‖r‖ |
+        status} of the last increment into the device buffer d_all
+        ([world][P_local][nc + nt + 2] doubles) over NCCL; the device
+        outputs default to the handle's own buffers. Returns the all-reduced
+        "some point failed" flag."""
+        flag = np.zeros(1, dtype=np.int32)
+        _check(lib.fe2_hrom_gather(self._h, comm.ptr, sigma or None, Cm or None, res or None, status or None, d_all,
+                                   _i(flag)))
+        return bool(flag[0])
 
     def solve_increment_into(self, E, sigma, Cm, iters, pc, res, status, opts: NewtonOptions | None = None):
         """Host-buffer C-ABI call writing into caller-provided (e.g. pinned)

@@ -64,3 +64,18 @@ def test_oracle_header_is_test_infrastructure_only():
             if f.endswith((".py", ".cu", ".cpp", ".hpp", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f), encoding="utf-8").read()
                 assert "pyoracle" not in txt and "fe2rom_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_exchange_entry_points_validate_and_need_a_device():
+    """fe2_hrom_gather / fe2_nccl_comm_init: argument checks
+    with the reference taxonomy; no communicator without a CUDA device."""
+    flag = np.zeros(1, dtype=np.int32)
+    rc = F.lib.fe2_hrom_gather(None, None, None, None, None, None, None, flag.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+    assert rc == 1  # ErrorCode::config ("no points allocated")
+    out = ctypes.c_void_p()
+    rc = F.lib.fe2_nccl_comm_init(0, 2, 5, ctypes.create_string_buffer(128), ctypes.byref(out))
+    assert rc == 1  # rank out of range -> config
+    if F.device_count() == 0:
+        with pytest.raises(F.Fe2Error) as e:
+            F.NcclComm(0, 1, 0, bytes(128))
+        assert e.value.kind == "numeric" and "no CPU fallback" in str(e.value)
