@@ -23,7 +23,8 @@ struct PointState {
 struct ModelDev {
   int n;        // modes
   int NP;       // modes padded to a multiple of 8 (DMMA tile)
-  int S;        // doubles per cubature point in G2 (3*NP + 2: 16-B rows, conflict-free 128-bit lane loads)
+  int S;        // doubles per cubature point in G2: 3*NP + 2 (NP <= 32: 16-B rows, conflict-free 128-bit
+                // lane loads) or 3*(NP + 4) (NP > 32: strain rows padded to NP + 4, k_increment_big)
   int K2;       // J2 cubature points
   int K2p;      // padded to a multiple of kQC
   int nchunks;  // K2p / kQC

@@ -54,15 +54,16 @@ struct Big {
   static constexpr int MINB = BW == 8 ? FE2_BIG_MINB : 2;
   static constexpr int QB = (NP <= FE2_BIG_QB32_MAXNP && BW == 8) ? 32 : 16;  // cubature points per chunk
   static constexpr int TPQ = BT / QB;    // threads per cubature point
-  static constexpr int S = 3 * NP + 2;
+  static constexpr int RS = NP + 4;  // strain-row stride in G chunks and staged rows (≡ 4 or 12 mod 16)
+  static constexpr int S = 3 * RS;    // doubles per cubature point in G2 (ModelDev::S for NP > 32)
   static constexpr int chunk = QB * S;
   static constexpr int TRI = NP * (NP + 1) / 2;
-  static constexpr int RS = NP + 4;           // staged row stride (≡ 4 or 12 mod 16 doubles)
-  static constexpr int STG = 2 * 3 * QB * RS;  // staged A rows | B rows
+  static constexpr int STG = 3 * QB * RS;  // staged B rows
   static constexpr int KREG = TRI > STG ? TRI : STG;
   static constexpr int RED = 128;  // >= BW * 12 (block_sum_n)
-  // doubles: ring[2][chunk] | sK[TRI] ∪ stage[STG] | vectors 9 NP | slots QB*(6+3) + QB ints | red
-  static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + KREG + 9 * NP + QB * 10 + RED;
+  // doubles: ring[2][chunk] | sK[TRI] ∪ stage[STG] | vectors 9 NP | slots QB*(6+3) | ints sQ[QB],
+  // row offsets[3 QB] | red
+  static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + KREG + 9 * NP + QB * 11 + RED;
   static constexpr size_t bytes = dbl * sizeof(double) + 2 * sizeof(uint64_t) + 16 * sizeof(int);
 };
 
@@ -253,18 +254,22 @@ __device__ __forceinline__ void diag_acc(const double (&A)[NT], const double (&B
   }
 }
 
-// DMMA over the chunk's staged plastic rows for warp W's tile pairs: k-step
-// ks covers staged rows 4ks..4ks+3 (row f = 3 slot + strain row i); lane
-// (m, col) reads row 4ks + m. The three k-steps of a group of four slots are
-// unrolled (the K_aE row of lane m is (s + m) mod 3 at k-step s of the group)
-// and the next k-step's fragments are loaded before the current DMMAs.
+// DMMA over the chunk's plastic rows for warp W's tile pairs: k-step ks
+// covers rows 4ks..4ks+3 (row f = 3 slot + strain row i); lane (m, col) reads
+// row 4ks + m — its A fragment straight from the G chunk at the staged row
+// offset sRO[f], its B fragment from the staged (w ΔC_q) G_q rows. The three
+// k-steps of a group of four slots are unrolled (the K_aE row of lane m is
+// (s + m) mod 3 at k-step s of the group) and the next k-step's fragments are
+// loaded before the current DMMAs.
 template <int NT, int W, int MP>
-__device__ __forceinline__ void contract(const double* stA, const double* stB, const double* sDS, int np4,
-                                         double (&acc)[MP][2], double (&kae)[NT][3], double (&rr)[NT], int lane) {
+__device__ __forceinline__ void contract(const double* Gb, const int* sRO, const double* stB, const double* sDS,
+                                         int np4, double (&acc)[MP][2], double (&kae)[NT][3], double (&rr)[NT],
+                                         int lane) {
   constexpr int RS = Big<NT>::RS;
   const int m = lane & 3, col = lane >> 2;
   const int ng = np4 >> 2;
-  const double* pa = stA + m * RS + col;
+  const double* ga = Gb + col;
+  const int* ro = sRO + m;
   const double* pb = stB + m * RS + col;
   const double* pw = sDS + m;
   if constexpr (NT > 8 || NT == 6) {  // no room for a prefetch set in the registers (ptxas -v)
@@ -274,24 +279,24 @@ __device__ __forceinline__ void contract(const double* stA, const double* stB, c
       for (int s = 0; s < 3; ++s) {
         const int f = 12 * g + 4 * s;
         double A[NT], B[NT];
-        load_frags<NT, W, 0>(pa + f * RS, pb + f * RS, A, B);
+        load_frags<NT, W, 0>(ga + ro[f], pb + f * RS, A, B);
         dmma_pairs<NT, W, 0, MP>(acc, A, B);
       }
     }
     return;
   }
   double A0[NT], B0[NT], A1[NT], B1[NT], A2[NT], B2[NT];
-  if (ng > 0) load_frags<NT, W, 0>(pa, pb, A0, B0);
+  if (ng > 0) load_frags<NT, W, 0>(ga + ro[0], pb, A0, B0);
 #pragma unroll 1
   for (int g = 0; g < ng; ++g) {
     const int f = 12 * g;  // first staged row of the group
-    load_frags<NT, W, 0>(pa + (f + 4) * RS, pb + (f + 4) * RS, A1, B1);
+    load_frags<NT, W, 0>(ga + ro[f + 4], pb + (f + 4) * RS, A1, B1);
     dmma_pairs<NT, W, 0, MP>(acc, A0, B0);
     diag_acc<NT, W, 0>(A0, B0, pw[f], 0, kae, rr);
-    load_frags<NT, W, 0>(pa + (f + 8) * RS, pb + (f + 8) * RS, A2, B2);
+    load_frags<NT, W, 0>(ga + ro[f + 8], pb + (f + 8) * RS, A2, B2);
     dmma_pairs<NT, W, 0, MP>(acc, A1, B1);
     diag_acc<NT, W, 0>(A1, B1, pw[f + 4], 1, kae, rr);
-    if (g + 1 < ng) load_frags<NT, W, 0>(pa + (f + 12) * RS, pb + (f + 12) * RS, A0, B0);
+    if (g + 1 < ng) load_frags<NT, W, 0>(ga + ro[f + 12], pb + (f + 12) * RS, A0, B0);
     dmma_pairs<NT, W, 0, MP>(acc, A2, B2);
     diag_acc<NT, W, 0>(A2, B2, pw[f + 8], 2, kae, rr);
   }
@@ -335,18 +340,18 @@ __device__ __forceinline__ void store_tiles(double* sK, const double (&acc)[MP][
 }
 
 template <int NT, int MP>
-__device__ __forceinline__ void contract_dispatch(int warp, const double* stA, const double* stB, const double* sDS,
-                                                  int np4, double (&acc)[MP][2], double (&kae)[NT][3],
-                                                  double (&rr)[NT], int lane) {
+__device__ __forceinline__ void contract_dispatch(int warp, const double* Gb, const int* sRO, const double* stB,
+                                                  const double* sDS, int np4, double (&acc)[MP][2],
+                                                  double (&kae)[NT][3], double (&rr)[NT], int lane) {
   switch (warp) {
-    case 0: contract<NT, 0, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
-    case 1: contract<NT, 1, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
-    case 2: contract<NT, 2, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
-    case 3: contract<NT, 3, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
-    case 4: contract<NT, 4, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
-    case 5: contract<NT, 5, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
-    case 6: contract<NT, 6, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
-    default: contract<NT, 7, MP>(stA, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 0: contract<NT, 0, MP>(Gb, sRO, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 1: contract<NT, 1, MP>(Gb, sRO, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 2: contract<NT, 2, MP>(Gb, sRO, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 3: contract<NT, 3, MP>(Gb, sRO, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 4: contract<NT, 4, MP>(Gb, sRO, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 5: contract<NT, 5, MP>(Gb, sRO, stB, sDS, np4, acc, kae, rr, lane); break;
+    case 6: contract<NT, 6, MP>(Gb, sRO, stB, sDS, np4, acc, kae, rr, lane); break;
+    default: contract<NT, 7, MP>(Gb, sRO, stB, sDS, np4, acc, kae, rr, lane); break;
   }
 }
 template <int NT>
@@ -410,48 +415,55 @@ __device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
   }
 }
 
-// Left-looking Cholesky of the packed lower sK. False (CTA-uniform) if not SPD.
-template <int NW, int BW>
+// Left-looking Cholesky of the packed lower sK on the whole CTA: TPR
+// adjacent threads per row split each dot product (stride TPR) and combine it
+// with shuffles. False (CTA-uniform) if not SPD.
+template <int BT, int NP>
 __device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
+  constexpr int TPR = (2 * NP <= BT) ? 2 : 1;
   const int tid = threadIdx.x;
-  if (tid < NW * 32) {
-    bool ok = true;
-    for (int j = 0; j < n; ++j) {
-      double s = 0.0;
-      if (tid >= j && tid < n) {
-        const double* ri = sK + tri(tid);
-        const double* rj = sK + tri(j);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int k = 0;
-        for (; k + 3 < j; k += 4) {
-          a0 += ri[k] * rj[k];
-          a1 += ri[k + 1] * rj[k + 1];
-          a2 += ri[k + 2] * rj[k + 2];
-          a3 += ri[k + 3] * rj[k + 3];
-        }
-        for (; k < j; ++k) a0 += ri[k] * rj[k];
-        s = ri[j] - ((a0 + a1) + (a2 + a3));
-        if (tid == j) red[0] = s;
+  const int row = tid / TPR, h = tid % TPR;
+  const bool live = row < n;
+  bool ok = true;
+  for (int j = 0; j < n; ++j) {
+    double s = 0.0;
+    const double* ri = sK + tri(row);
+    const double* rj = sK + tri(j);
+    if (live && row >= j) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int k = h;
+      for (; k + 3 * TPR < j; k += 4 * TPR) {
+        a0 += ri[k] * rj[k];
+        a1 += ri[k + TPR] * rj[k + TPR];
+        a2 += ri[k + 2 * TPR] * rj[k + 2 * TPR];
+        a3 += ri[k + 3 * TPR] * rj[k + 3 * TPR];
       }
-      rows_sync<NW, BW>();
-      const double d = red[0];
-      if (!(d > 0.0)) {  // uniform over the row warps
-        ok = false;
-        break;
-      }
-      const double inv = rsqrt_fast(d);
-      if (tid == j) {
+      for (; k < j; k += TPR) a0 += ri[k] * rj[k];
+      s = (a0 + a1) + (a2 + a3);
+    }
+    if constexpr (TPR == 2) s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (live && row >= j) {
+      s = ri[j] - s;
+      if (row == j && h == 0) red[0] = s;
+    }
+    __syncthreads();
+    const double d = red[0];
+    if (!(d > 0.0)) {  // uniform over the CTA
+      ok = false;
+      break;
+    }
+    const double inv = rsqrt_fast(d);
+    if (h == 0 && live) {
+      if (row == j) {
         sK[tri(j) + j] = d * inv;
         sInv[j] = inv;
-      } else if (tid > j && tid < n) {
-        sK[tri(tid) + j] = s * inv;
+      } else if (row > j) {
+        sK[tri(row) + j] = s * inv;
       }
-      rows_sync<NW, BW>();
     }
-    if (tid == 0) red[1] = ok ? 1.0 : 0.0;
+    __syncthreads();
   }
-  __syncthreads();
-  return red[1] != 0.0;
+  return ok;
 }
 
 // Forward substitution L y = b in place on sB[n] (cols RHS interleaved: sB[i*cols + c]).
@@ -494,8 +506,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
   double* sK = ring + 2 * static_cast<size_t>(L::chunk);
-  double* stA = sK;                      // staged rows alias sK (dead during an assembly pass)
-  double* stB = sK + 3 * QB * L::RS;
+  double* stB = sK;  // staged B rows alias sK (dead during an assembly pass)
   double* sAev = sK + L::KREG;
   double* sAl = sAev + NP;
   double* sDA = sAl + NP;
@@ -506,7 +517,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   double* sDC = sKaE + 3 * NP;
   double* sDS = sDC + QB * 6;
   int* sQ = reinterpret_cast<int*>(sDS + QB * 3);
-  double* red = sDS + QB * 4;
+  int* sRO = sQ + QB;  // [3 QB] G-chunk offset of plastic row f = 3 slot + i
+  double* red = sDS + QB * 5;
   uint64_t* full = reinterpret_cast<uint64_t*>(red + L::RED);
   int* ictl = reinterpret_cast<int*>(full + 2);  // [0..7] warp counts, [8] point
 
@@ -529,7 +541,9 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       mbar_expect_tx(&full[s], kChunkBytes);
       tma_load_1d(ring + s * L::chunk, M.G2 + static_cast<size_t>(s % nch) * L::chunk, kChunkBytes, &full[s]);
     }
-  int pos = 0;  // ring position (chunk pos % nch, stage pos % 2)
+  // ring positions (global chunk sequence: chunk pos % nch, stage pos % 2):
+  // tpos = next to take, rpos = next to refill (after the chunk's last barrier)
+  int tpos = 0, rpos = 0;
   unsigned long long n_asm = 0, n_com = 0, n_pl = 0, n_cpl = 0;
 
   const int qi = tid / TPQ, sub = tid % TPQ;  // cubature point of this thread within a chunk, mode slice
@@ -540,30 +554,31 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
     return D.hist + (buf ? D.hist_alt : 0) + (p * (M.K2p / kQC) + q / kQC) * (5 * kQC) + (q % kQC);
   };
   auto ring_take = [&]() -> const double* {
-    const int s = pos & 1;
-    mbar_wait(&full[s], static_cast<uint32_t>((pos >> 1) & 1));
+    const int s = tpos & 1;
+    mbar_wait(&full[s], static_cast<uint32_t>((tpos >> 1) & 1));
+    ++tpos;
     return ring + s * L::chunk;
   };
   auto ring_release = [&]() {  // after the CTA barrier that ends the chunk
     if (tid == 0) {
-      const int s = pos & 1;
+      const int s = rpos & 1;
       fence_proxy_async();
       mbar_expect_tx(&full[s], kChunkBytes);
-      tma_load_1d(ring + s * L::chunk, M.G2 + static_cast<size_t>((pos + 2) % nch) * L::chunk, kChunkBytes,
+      tma_load_1d(ring + s * L::chunk, M.G2 + static_cast<size_t>((rpos + 2) % nch) * L::chunk, kChunkBytes,
                   &full[s]);
     }
-    ++pos;
+    ++rpos;
   };
   // strain of this thread's cubature point (threads of a point split the modes)
   auto strain = [&](const double* Gb, double E0, double E1, double E2, double& e0, double& e1, double& e2) {
-    // 128-bit loads of mode pairs (2j, 2j+1); rows are 16-B aligned (S, NP even)
+    // 128-bit loads of mode pairs (2j, 2j+1); rows are 16-B aligned (S, RS even)
     const double2* Gq = reinterpret_cast<const double2*>(Gb + qi * S);
     const double2* al2 = reinterpret_cast<const double2*>(sAev);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
     for (int j = sub; j < NP / 2; j += TPQ) {
       const double2 al = al2[j];
-      const double2 g0 = Gq[j], g1 = Gq[NP / 2 + j], g2 = Gq[NP + j];
+      const double2 g0 = Gq[j], g1 = Gq[L::RS / 2 + j], g2 = Gq[L::RS + j];
       a0 += g0.x * al.x + g0.y * al.y;
       a1 += g1.x * al.x + g1.y * al.y;
       a2 += g2.x * al.x + g2.y * al.y;
@@ -697,32 +712,31 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       n_pl += static_cast<unsigned long long>(tid == 0 ? np : 0);
       np_tot += np;
       __syncthreads();
-      // stage the slots' operand rows: A = G_q (3 rows), B = (w ΔC_q) G_q;
-      // warp w stages slots w, w + BW, ... (lanes over the modes). (Giving
-      // the warps without diagonal corrections more slots was slower.)
+      // stage the slots' B rows (w ΔC_q) G_q and the G-chunk offsets of their A
+      // rows; warp w stages slots w, w + BW, ... (lanes over the modes). (Each
+      // warp staging its own slots, one CTA barrier less per chunk, spilled at
+      // NT = 8 and gained 3% at NT = 16 only.)
       for (int sl = warp; sl < np4; sl += L::BW) {
         const double* dc = sDC + sl * 6;
         const double d00 = dc[0], d01 = dc[1], d02 = dc[2], d11 = dc[3], d12 = dc[4], d22 = dc[5];
-        const double* Gq = Gb + sQ[sl] * S;
-        double* ar = stA + 3 * sl * L::RS;
+        const int qo = sQ[sl] * S;
+        const double* Gq = Gb + qo;
         double* br = stB + 3 * sl * L::RS;
+        if (lane < 3) sRO[3 * sl + lane] = qo + lane * L::RS;
 #pragma unroll
         for (int a = lane; a < NP; a += 32) {
-          const double g0 = Gq[a], g1 = Gq[NP + a], g2 = Gq[2 * NP + a];
-          ar[a] = g0;
-          ar[L::RS + a] = g1;
-          ar[2 * L::RS + a] = g2;
+          const double g0 = Gq[a], g1 = Gq[L::RS + a], g2 = Gq[2 * L::RS + a];
           br[a] = d00 * g0 + d01 * g1 + d02 * g2;
           br[L::RS + a] = d01 * g0 + d11 * g1 + d12 * g2;
           br[2 * L::RS + a] = d02 * g0 + d12 * g1 + d22 * g2;
         }
       }
       __syncthreads();
-      contract_dispatch<NT, MP>(warp, stA, stB, sDS, np4, acc, kae, rr, lane);
+      contract_dispatch<NT, MP>(warp, Gb, sRO, stB, sDS, np4, acc, kae, rr, lane);
       if constexpr (!kFragCorr<NT>) {
         if (tid < NP) {  // r and K_aE corrections of mode a = tid, from the staged rows
           for (int sl = 0; sl < np; ++sl) {
-            const double* ar = stA + 3 * sl * L::RS + tid;
+            const double* ar = Gb + sQ[sl] * S + tid;
             const double* br = stB + 3 * sl * L::RS + tid;
             const double* ds = sDS + sl * 3;
             rm += ar[0] * ds[0] + ar[L::RS] * ds[1] + ar[2 * L::RS] * ds[2];
@@ -803,7 +817,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       __syncthreads();
       return true;
     }
-    return cta_cholesky<(NP + 31) / 32, L::BW>(sK, sInv, red + L::RED - 2, n);  // clear of block sums
+    return cta_cholesky<L::BT, NP>(sK, sInv, red + L::RED - 2, n);  // clear of block sums
   };
 
   // accept the last pass's state: flip to its candidate history, α_c, and move
@@ -1054,8 +1068,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   // no TMA may be in flight at exit: the two positions issued ahead
   __syncthreads();
   for (int k = 0; k < 2; ++k) {
-    mbar_wait(&full[pos & 1], static_cast<uint32_t>((pos >> 1) & 1));
-    ++pos;
+    mbar_wait(&full[rpos & 1], static_cast<uint32_t>((rpos >> 1) & 1));
+    ++rpos;
   }
   if (A.cnt && tid == 0) {
     atomicAdd(&A.cnt->assemblies, n_asm);
@@ -1066,7 +1080,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
 }
 
 template <int NT>
-void launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
+bool launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
+  if (a.M.S != Big<NT>::S) return false;  // G2 rows must carry the padded strain-row stride
   const size_t smem = Big<NT>::bytes;
   static bool configured = false;
   if (!configured) {
@@ -1081,6 +1096,7 @@ void launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
   else if (grid > a.D.P) grid = a.D.P;
   if (grid < 1) grid = 1;
   k_increment_big<NT><<<static_cast<unsigned>(grid), Big<NT>::BT, smem, s>>>(a);
+  return true;
 }
 
 }  // namespace
@@ -1088,14 +1104,14 @@ void launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
 // NP = 40, 48, 56, 64 (32-point chunks) and 80, 96, 112, 128 (16-point chunks)
 bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s) {
   switch (a.M.NP) {
-    case 40: launch_big_nt<5>(a, num_sms, s); return true;
-    case 48: launch_big_nt<6>(a, num_sms, s); return true;
-    case 56: launch_big_nt<7>(a, num_sms, s); return true;
-    case 64: launch_big_nt<8>(a, num_sms, s); return true;
-    case 80: launch_big_nt<10>(a, num_sms, s); return true;
-    case 96: launch_big_nt<12>(a, num_sms, s); return true;
-    case 112: launch_big_nt<14>(a, num_sms, s); return true;
-    case 128: launch_big_nt<16>(a, num_sms, s); return true;
+    case 40: return launch_big_nt<5>(a, num_sms, s);
+    case 48: return launch_big_nt<6>(a, num_sms, s);
+    case 56: return launch_big_nt<7>(a, num_sms, s);
+    case 64: return launch_big_nt<8>(a, num_sms, s);
+    case 80: return launch_big_nt<10>(a, num_sms, s);
+    case 96: return launch_big_nt<12>(a, num_sms, s);
+    case 112: return launch_big_nt<14>(a, num_sms, s);
+    case 128: return launch_big_nt<16>(a, num_sms, s);
     default: return false;
   }
 }
