@@ -220,10 +220,40 @@ class HyperRomBatch {
 
   fe2_hrom_t handle() const { return h_; }
 
+  // Multi-GPU exchange (one batch per rank and device, equal P per rank):
+  // all-gather every rank's {Σ (3) | C_macro (9) | ‖r‖ | status} records of
+  // the last increment into the device buffer d_all [world][P][14]; returns
+  // true if a point failed on any rank. See fe2_hrom_gather.
+  bool gather(void* nccl_comm, double* d_all) {
+    int failed = 0;
+    check(fe2_hrom_gather(h_, nccl_comm, nullptr, nullptr, nullptr, nullptr, d_all, &failed));
+    return failed != 0;
+  }
+
  private:
   fe2_hrom_t h_ = nullptr;
   int n_ = 0, K_ = 0;
   int64_t P_ = 0;
+};
+
+// One NCCL communicator per rank and device (fe2_nccl_comm_init); rank 0
+// creates the id with unique_id() and the caller broadcasts its 128 bytes.
+class NcclComm {
+ public:
+  using Id = std::array<unsigned char, 128>;
+  static Id unique_id() {
+    Id id{};
+    check(fe2_nccl_get_unique_id(id.data()));
+    return id;
+  }
+  NcclComm(int device, int nranks, int rank, const Id& id) { check(fe2_nccl_comm_init(device, nranks, rank, id.data(), &c_)); }
+  ~NcclComm() { fe2_nccl_comm_destroy(c_); }
+  NcclComm(const NcclComm&) = delete;
+  NcclComm& operator=(const NcclComm&) = delete;
+  void* get() const { return c_; }
+
+ private:
+  void* c_ = nullptr;
 };
 
 // Finite-strain (Biot stress) response of one macro point: first
