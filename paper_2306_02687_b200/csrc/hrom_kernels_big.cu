@@ -67,11 +67,12 @@ struct Big {
   static constexpr size_t bytes = dbl * sizeof(double) + 2 * sizeof(uint64_t) + 16 * sizeof(int);
 };
 
-// Tile pairs (t1 <= t2) of one warp. The upper triangle is cut into tile
-// blocks (b x b; for NT = 8 the off-diagonal block is split into two 2 x 4
-// halves) and the blocks are dealt largest-first to the least-loaded warp, so
-// the DMMA count per warp is balanced and each warp reuses its fragments
-// across a block (NT = 8, 4 warps: 10/10/8/8 pairs from 8/8/6/6 loads).
+// Tile pairs (t1 <= t2) of one warp. NT = 2 x warps (n = 64 on 4 warps,
+// n = 128 on 8): folded tile rows, NT + 1 pairs per warp. Otherwise the upper
+// triangle is cut into tile blocks (b x b; the off-diagonal blocks of NT = 8
+// split into 2 x 4 halves) dealt largest-first to the least-loaded warp. The
+// contraction is DMMA-issue bound per warp once the fragments are single
+// conflict-free loads, so balance beats fragment reuse.
 struct PairTable {
   int n;
   int t1[160];
@@ -80,6 +81,18 @@ struct PairTable {
 template <int NT>
 constexpr PairTable pairs_for(int W) {
   constexpr int BW = bw_for(NT);
+  if constexpr (2 * BW == NT) {
+    // folded rows: warp W owns tile rows W and NT-1-W, (NT - W) + (W + 1) =
+    // NT + 1 pairs each — exactly balanced, two diagonal tiles per warp
+    PairTable P{};
+    for (int r : {W, NT - 1 - W})
+      for (int t2 = r; t2 < NT; ++t2) {
+        P.t1[P.n] = r;
+        P.t2[P.n] = t2;
+        ++P.n;
+      }
+    return P;
+  }
   const int b = (NT == 8 || NT == 16) ? 4 : 2;
   const bool split = NT == 8;
   const int nb = (NT + b - 1) / b;
@@ -148,7 +161,7 @@ constexpr int total_pairs() {
 static_assert(total_pairs<5>() == 15 && total_pairs<8>() == 36 && total_pairs<12>() == 78 &&
                   total_pairs<16>() == 136,
               "tile-pair partition must cover the upper triangle");
-static_assert(max_pairs<8>() == 10 && max_pairs<16>() == 20, "unexpected partition balance");
+static_assert(max_pairs<8>() == 9 && max_pairs<16>() == 17, "unexpected partition balance");
 
 // non-volatile DMMA (pure in its operands: the scheduler may interleave the
 // fragment loads of the next k-step)
