@@ -511,8 +511,32 @@ __device__ void cta_backward(const double* sK, const double* sInv, double* sB, i
   __syncthreads();
 }
 
+// Phase timeline of thread 0 of every CTA (tuning builds only: -DFE2_BIG_PROF;
+// the last CTA prints the sums): 0 ring wait, 1 strain + material,
+// 2 compaction + slots, 3 staging, 4 contraction, 5 chunk tail, 6 pass tail,
+// 7 Newton / factorisation / condensation.
+#ifdef FE2_BIG_PROF
+__device__ unsigned long long g_big_prof[9];
+#define BIG_T(k)                                              \
+  do {                                                        \
+    if (threadIdx.x == 0) {                                   \
+      const long long t_ = clock64();                         \
+      prof[k] += static_cast<unsigned long long>(t_ - t_prof); \
+      t_prof = t_;                                            \
+    }                                                         \
+  } while (0)
+#else
+#define BIG_T(k) \
+  do {           \
+  } while (0)
+#endif
+
 template <int NT>
 __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(IncArgs A) {
+#ifdef FE2_BIG_PROF
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_prof = clock64();
+#endif
   using L = Big<NT>;
   constexpr int NP = L::NP, QB = L::QB, TPQ = L::TPQ, S = L::S;
   constexpr int MP = max_pairs<NT>();
@@ -650,8 +674,10 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       h3 = H[3 * kQC];
       h4 = H[4 * kQC];
     }
+    BIG_T(7);
     for (int c = 0; c < nch; ++c) {
       const double* Gb = ring_take();
+      BIG_T(0);
       const int q = c * QB + qi;
       double e0, e1, e2;
       strain(Gb, E0, E1, E2, e0, e1, e2);
@@ -690,6 +716,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
         }
       }
       int slot, np;
+      BIG_T(1);
       compact(plastic, slot, np);
       if (plastic) {
         const double wq = M.w2[q];
@@ -725,27 +752,55 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       n_pl += static_cast<unsigned long long>(tid == 0 ? np : 0);
       np_tot += np;
       __syncthreads();
+      BIG_T(2);
       // stage the slots' B rows (w ΔC_q) G_q and the G-chunk offsets of their A
-      // rows; warp w stages slots w, w + BW, ... (lanes over the modes). (Each
-      // warp staging its own slots, one CTA barrier less per chunk, spilled at
-      // NT = 8 and gained 3% at NT = 16 only.)
-      for (int sl = warp; sl < np4; sl += L::BW) {
-        const double* dc = sDC + sl * 6;
-        const double d00 = dc[0], d01 = dc[1], d02 = dc[2], d11 = dc[3], d12 = dc[4], d22 = dc[5];
-        const int qo = sQ[sl] * S;
-        const double* Gq = Gb + qo;
-        double* br = stB + 3 * sl * L::RS;
-        if (lane < 3) sRO[3 * sl + lane] = qo + lane * L::RS;
+      // rows; warp w stages slots w, w + BW, ... (lanes over the modes), two
+      // slots at a time with every load issued before the first store (the
+      // compiler cannot move loads above possibly aliasing shared stores)
+      {
+        constexpr int NA = NP / 32 > 0 ? (NP + 31) / 32 : 1;  // modes per lane
+        for (int s0 = warp; s0 < np4; s0 += 2 * L::BW) {
+          const int s1 = s0 + L::BW;
+          const bool two = s1 < np4;
+          double d[2][6], g[2][NA][3];
+          int qo[2];
 #pragma unroll
-        for (int a = lane; a < NP; a += 32) {
-          const double g0 = Gq[a], g1 = Gq[L::RS + a], g2 = Gq[2 * L::RS + a];
-          br[a] = d00 * g0 + d01 * g1 + d02 * g2;
-          br[L::RS + a] = d01 * g0 + d11 * g1 + d12 * g2;
-          br[2 * L::RS + a] = d02 * g0 + d12 * g1 + d22 * g2;
+          for (int u = 0; u < 2; ++u) {
+            const int sl = u ? (two ? s1 : s0) : s0;
+            qo[u] = sQ[sl] * S;
+#pragma unroll
+            for (int e = 0; e < 6; ++e) d[u][e] = sDC[sl * 6 + e];
+#pragma unroll
+            for (int k = 0; k < NA; ++k) {
+              const int a = lane + 32 * k;
+              const double* Gq = Gb + qo[u] + (a < NP ? a : 0);
+              g[u][k][0] = Gq[0];
+              g[u][k][1] = Gq[L::RS];
+              g[u][k][2] = Gq[2 * L::RS];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) break;
+            const int sl = u ? s1 : s0;
+            double* br = stB + 3 * sl * L::RS;
+            if (lane < 3) sRO[3 * sl + lane] = qo[u] + lane * L::RS;
+#pragma unroll
+            for (int k = 0; k < NA; ++k) {
+              const int a = lane + 32 * k;
+              if (a >= NP) break;
+              const double g0 = g[u][k][0], g1 = g[u][k][1], g2 = g[u][k][2];
+              br[a] = d[u][0] * g0 + d[u][1] * g1 + d[u][2] * g2;
+              br[L::RS + a] = d[u][1] * g0 + d[u][3] * g1 + d[u][4] * g2;
+              br[2 * L::RS + a] = d[u][2] * g0 + d[u][4] * g1 + d[u][5] * g2;
+            }
+          }
         }
       }
       __syncthreads();
+      BIG_T(3);
       contract_dispatch<NT, MP>(warp, Gb, sRO, stB, sDS, np4, acc, kae, rr, lane);
+      BIG_T(4);
       if constexpr (!kFragCorr<NT>) {
         if (tid < NP) {  // r and K_aE corrections of mode a = tid, from the staged rows
           for (int sl = 0; sl < np; ++sl) {
@@ -761,6 +816,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       }
       __syncthreads();
       ring_release();
+      BIG_T(5);
     }
     store_dispatch<NT, MP>(warp, sK, acc, lane);
     if constexpr (kFragCorr<NT>) {
@@ -821,6 +877,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
     np_last = np_tot;
     k_linear = (np_tot == 0);
     ++n_asm;
+    BIG_T(6);
   };
 
   auto factor = [&]() -> bool {
@@ -1084,6 +1141,23 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
     mbar_wait(&full[rpos & 1], static_cast<uint32_t>((rpos >> 1) & 1));
     ++rpos;
   }
+#ifdef FE2_BIG_PROF
+  BIG_T(7);
+  if (tid == 0) {
+    for (int k = 0; k < 8; ++k) atomicAdd(&g_big_prof[k], prof[k]);
+    __threadfence();
+    if (atomicAdd(&g_big_prof[8], 1ull) == gridDim.x - 1) {
+      unsigned long long s = 0;
+      for (int k = 0; k < 8; ++k) s += g_big_prof[k];
+      printf("FE2_BIG_PROF NT=%d cycles%%: wait %.1f material %.1f compact %.1f stage %.1f contract %.1f tail %.1f "
+             "pass-tail %.1f newton %.1f\n",
+             NT, 100.0 * g_big_prof[0] / s, 100.0 * g_big_prof[1] / s, 100.0 * g_big_prof[2] / s,
+             100.0 * g_big_prof[3] / s, 100.0 * g_big_prof[4] / s, 100.0 * g_big_prof[5] / s,
+             100.0 * g_big_prof[6] / s, 100.0 * g_big_prof[7] / s);
+      for (int k = 0; k < 9; ++k) g_big_prof[k] = 0;
+    }
+  }
+#endif
   if (A.cnt && tid == 0) {
     atomicAdd(&A.cnt->assemblies, n_asm);
     atomicAdd(&A.cnt->commits, n_com);
