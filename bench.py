@@ -276,7 +276,10 @@ class DeviceRun:
             definition = "SURVEY §8(d) config 2: F_asm = 8 K n (n+5) per point-assembly (all cubature points; full K_aa, K_aF, r)"
         else:  # every plastic point = 3 k-entries = 0.75 k-steps of NTP DMMA.8x8x4
             executed = stats["timed_plastic_evals"] * 0.75 * (nt * (nt + 1) // 2) * 512
-            kernel = "k_increment (persistent: DMMA hyper-assembly + warp Cholesky/Newton/condensation + commit)"
+            kernel = ("k_increment (persistent: DMMA hyper-assembly + warp Cholesky/Newton/condensation + commit)"
+                      if n <= 32 else
+                      "k_increment_big (persistent, CTA per point: staged-B DMMA hyper-assembly + CTA Cholesky/"
+                      "Newton/condensation)")
             definition = "SURVEY §8(d) F_asm = 3 K_J2 n (n+9) per point-assembly (elastic block precomputed)"
         launches_t = max(1, stats["timed_launches"])
         return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

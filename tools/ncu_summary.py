@@ -65,6 +65,26 @@ def full(report, out, label):
     print(json.dumps(res, indent=1))
 
 
+def _short_name(full):
+    """'void ns::<unnamed>::k_increment<3, 8, 1, 0>(ns::IncArgs)' -> 'k_increment'."""
+    s = full.strip()
+    if s.endswith(")"):  # drop the (balanced) argument list
+        depth = 0
+        for i in range(len(s) - 1, -1, -1):
+            depth += {")": 1, "(": -1}.get(s[i], 0)
+            if depth == 0:
+                s = s[:i]
+                break
+    if s.endswith(">"):  # drop the (balanced) template arguments
+        depth = 0
+        for i in range(len(s) - 1, -1, -1):
+            depth += {">": 1, "<": -1}.get(s[i], 0)
+            if depth == 0:
+                s = s[:i]
+                break
+    return s.replace("::", " ").split()[-1] if s.strip() else full
+
+
 def launches(path, out):
     text = open(path).read()
     lines = [ln for ln in text.splitlines() if ln.startswith('"')]
@@ -75,7 +95,7 @@ def launches(path, out):
     for r in rows[1:]:
         if r[im] != "gpu__time_duration.sum":
             continue
-        name = r[ik].split("(")[0].split("<")[0].split("::")[-1].strip()
+        name = _short_name(r[ik])
         agg[name][0] += 1
         agg[name][1] += _num(r[iv])
     tot = sum(t for _, t in agg.values()) or 1.0
