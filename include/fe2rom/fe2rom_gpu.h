@@ -265,7 +265,8 @@ int fe2_macro_run_hf(const fe2_macro_config_t* cfg, fe2_hf_t hf, double* rows, i
 
 /* ---- monolithic scheme (SPEC.md:474-481 HF_monolithic / hyper-ROM): the
  * micro problems advance ONE reduced Newton iteration per macro iteration,
- * sharing the macro linearisation. Small-strain handles, n <= 32.
+ * sharing the macro linearisation. Small-strain handles, any supported n
+ * (warp-per-point kernel for n <= 32, CTA-per-point kernel above).
  *   fe2_hrom_mono_begin     start a macro step from the committed state
  *                           (α = α_committed; history candidates discarded)
  *   fe2_hrom_mono_iterate   for every point at this macro iterate's E[P*3]:

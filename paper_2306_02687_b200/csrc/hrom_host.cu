@@ -622,7 +622,7 @@ int fe2_hrom_solve_increment_device(fe2_hrom_t h, const double* d_E, const fe2_n
 int fe2_hrom_mono_begin(fe2_hrom_t h) {
   return guard([&] {
     check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
-    check(h->kin == 0 && h->NP <= 32, Code::config, "the monolithic iteration needs a small-strain handle with n <= 32");
+    check(h->kin == 0, Code::config, "the monolithic iteration needs a small-strain handle");
     h->mono_first = true;
   });
 }
@@ -632,7 +632,7 @@ int fe2_hrom_mono_iterate(fe2_hrom_t h, const double* E, double* sigma, double* 
   return guard([&] {
     check(h != nullptr && E != nullptr, Code::config, "bad arguments");
     check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
-    check(h->kin == 0 && h->NP <= 32, Code::config, "the monolithic iteration needs a small-strain handle with n <= 32");
+    check(h->kin == 0, Code::config, "the monolithic iteration needs a small-strain handle");
     CK(cudaSetDevice(h->device));
     const int64_t P = h->P;
     cudaStream_t s = h->stream;
@@ -653,7 +653,10 @@ int fe2_hrom_mono_iterate(fe2_hrom_t h, const double* E, double* sigma, double* 
     a.mono_first = h->mono_first ? 1 : 0;
     CK(cudaMemsetAsync(h->work, 0, sizeof(int), s));
     CK(cudaMemsetAsync(h->cnt, 0, sizeof(IncCounters), s));
-    launch_increment_mono(a, h->num_sms, s);
+    if (h->NP <= 32)
+      launch_increment_mono(a, h->num_sms, s);
+    else
+      check(launch_increment_big_mono(a, h->num_sms, s), Code::config, "unsupported mode count");
     CK(cudaGetLastError());
     h->stats.kernel_launches += 1;
     h->mono_first = false;

@@ -122,6 +122,8 @@ void launch_increment_mono(const IncArgs& a, int num_sms, cudaStream_t s);
 // adopt the last monolithic iterate of every live point as its committed state
 void launch_mono_commit(const PointsDev& D, int NP, const double* mono, cudaStream_t s);
 bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s);
+// one monolithic Newton iteration for every point, NP in the launch_increment_big set
+bool launch_increment_big_mono(const IncArgs& a, int num_sms, cudaStream_t s);
 size_t increment_big_smem(int NP);
 void launch_material_batch(const MatDev& m, int64_t N, const double* eps, const double* st_in, double* sigma,
                            double* C, double* st_out, uint8_t* plastic, int* err, cudaStream_t s);

@@ -64,7 +64,9 @@ struct Big {
   // doubles: ring[2][chunk] | sK[TRI] ∪ stage[STG] | vectors 9 NP | slots QB*(6+3) | ints sQ[QB],
   // row offsets[3 QB] | red
   static constexpr size_t dbl = 2 * static_cast<size_t>(chunk) + KREG + 9 * NP + QB * 11 + RED;
-  static constexpr size_t bytes = dbl * sizeof(double) + 2 * sizeof(uint64_t) + 16 * sizeof(int);
+  // + control words, then sZ[NP][4] (monolithic iteration only) at the end
+  static constexpr size_t zoff = dbl * sizeof(double) + 2 * sizeof(uint64_t) + 16 * sizeof(int);
+  static constexpr size_t bytes = zoff + 4 * NP * sizeof(double);
 };
 
 // Tile pairs (t1 <= t2) of one warp. NT = 2 x warps (n = 64 on 4 warps,
@@ -510,6 +512,24 @@ __device__ void cta_backward(const double* sK, const double* sInv, double* sB, i
   }
   __syncthreads();
 }
+// The same for four interleaved RHS (monolithic iteration: K^-1 [r | K_aE]).
+template <int NW, int BW>
+__device__ void cta_backward4(const double* sK, const double* sInv, double* sB, int n) {
+  const int tid = threadIdx.x;
+  if (tid < NW * 32) {
+    for (int j = n - 1; j >= 0; --j) {
+      if (tid < 4) sB[j * 4 + tid] *= sInv[j];
+      rows_sync<NW, BW>();
+      if (tid < j) {
+        const double l = sK[tri(j) + tid];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sB[tid * 4 + c] -= l * sB[j * 4 + c];
+      }
+      rows_sync<NW, BW>();
+    }
+  }
+  __syncthreads();
+}
 
 // Phase timeline of thread 0 of every CTA (tuning builds only: -DFE2_BIG_PROF;
 // the last CTA prints the sums): 0 ring wait, 1 strain + material,
@@ -531,7 +551,7 @@ __device__ unsigned long long g_big_prof[9];
   } while (0)
 #endif
 
-template <int NT>
+template <int NT, bool MONO = false>
 __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(IncArgs A) {
 #ifdef FE2_BIG_PROF
   unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -558,6 +578,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   double* red = sDS + QB * 5;
   uint64_t* full = reinterpret_cast<uint64_t*>(red + L::RED);
   int* ictl = reinterpret_cast<int*>(full + 2);  // [0..7] warp counts, [8] point
+  double* sZ = reinterpret_cast<double*>(smem_raw + L::zoff);  // [NP][4] monolithic K^-1 [r | K_aE]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const ModelDev& M = A.M;
@@ -914,6 +935,94 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   const NewtonCfg& cfg = A.cfg;
   constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
 
+  // One monolithic Newton iteration of point p (the paper's scheme; same
+  // algebra as k_increment<..., MONO>): α ← α_w − K⁻¹(r + K_aE ΔE)
+  // with the previous iteration's solves, assemble at (E, α) from the committed
+  // history, factor, and return the condensed Σ̃ = (Σ_raw − K_Eα K⁻¹ r)/V and
+  // C = (C_EE − K_Eα K⁻¹ K_aE)/V; record z = K⁻¹[r | K_aE], the plastic loads
+  // and α for the next iteration / fe2_hrom_mono_commit. No commit here.
+  auto mono_point = [&](int64_t p, double E0, double E1, double E2) {
+    double* rec = A.mono + p * mono_stride(NP);
+    double* tail = rec + 6 * NP;
+    if (A.mono_first) {
+      for (int a = tid; a < NP; a += L::BT) sAev[a] = D.alpha_c[p * NP + a];
+    } else {
+      const double d0 = E0 - tail[0], d1 = E1 - tail[1], d2 = E2 - tail[2];
+      for (int a = tid; a < NP; a += L::BT)
+        sAev[a] = (a < n) ? rec[5 * NP + a] - (rec[a] + rec[NP + a] * d0 + rec[2 * NP + a] * d1 + rec[3 * NP + a] * d2)
+                          : 0.0;
+    }
+    __syncthreads();
+    assembly_pass(p, E0, E1, E2);
+    const double rn = rn_pass;
+    // micro scale: max(|r| at the step's first iteration, |Σ_raw| now) — E moves during a monolithic step
+    const double r_first = A.mono_first ? rn : tail[6];
+    const double ref = fmax(fmax(r_first, sqrt(s0 * s0 + s1 * s1 + s2 * s2)), 1e-30);
+    if (!factor()) {
+      if (tid == 0) {
+        A.O.status[p] = kSolver;
+        A.O.iters[p] = 1;
+        A.O.res[p] = rn / ref;
+      }
+      __syncthreads();
+      return;
+    }
+    for (int a = tid; a < NP; a += L::BT) {
+      const bool in = a < n;
+      sZ[a * 4 + 0] = in ? sV[a] : 0.0;
+      sZ[a * 4 + 1] = in ? sKaE[a * 3 + 0] : 0.0;
+      sZ[a * 4 + 2] = in ? sKaE[a * 3 + 1] : 0.0;
+      sZ[a * 4 + 3] = in ? sKaE[a * 3 + 2] : 0.0;
+    }
+    __syncthreads();
+    cta_forward<(NP + 31) / 32, L::BW>(sK, sInv, sZ, n, 4);
+    cta_backward4<(NP + 31) / 32, L::BW>(sK, sInv, sZ, n);
+    double v[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (tid < n) {
+      const double k0 = sKaE[tid * 3 + 0], k1 = sKaE[tid * 3 + 1], k2 = sKaE[tid * 3 + 2];
+      const double zr = sZ[tid * 4 + 0], z0 = sZ[tid * 4 + 1], z1 = sZ[tid * 4 + 2], z2 = sZ[tid * 4 + 3];
+      v[0] = k0 * zr, v[1] = k1 * zr, v[2] = k2 * zr;
+      v[3] = k0 * z0, v[4] = k1 * z1, v[5] = k2 * z2;
+      v[6] = k0 * z1, v[7] = k1 * z0, v[8] = k0 * z2, v[9] = k2 * z0, v[10] = k1 * z2, v[11] = k2 * z1;
+    }
+    block_sum_n<L::BW, 12>(v, red);
+    const double q01 = 0.5 * (v[6] + v[7]), q02 = 0.5 * (v[8] + v[9]), q12 = 0.5 * (v[10] + v[11]);
+    for (int a = tid; a < NP; a += L::BT) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) rec[c * NP + a] = sZ[a * 4 + c];
+      rec[4 * NP + a] = sRp[a];
+      rec[5 * NP + a] = sAev[a];
+    }
+    if (tid == 0) {
+      const double V = M.volume;
+      double* Cp = A.O.C + p * 9;
+      Cp[0] = (ce00 - v[3]) / V;
+      Cp[1] = (ce01 - q01) / V;
+      Cp[2] = (ce02 - q02) / V;
+      Cp[3] = Cp[1];
+      Cp[4] = (ce11 - v[4]) / V;
+      Cp[5] = (ce12 - q12) / V;
+      Cp[6] = Cp[2];
+      Cp[7] = Cp[5];
+      Cp[8] = (ce22 - v[5]) / V;
+      A.O.sigma[p * 3 + 0] = (s0 - v[0]) / V;
+      A.O.sigma[p * 3 + 1] = (s1 - v[1]) / V;
+      A.O.sigma[p * 3 + 2] = (s2 - v[2]) / V;
+      A.O.res[p] = rn / ref;
+      A.O.iters[p] = 1;
+      A.O.status[p] = 0;
+      if (A.O.pcount) A.O.pcount[p] = np_last;
+      tail[0] = E0;
+      tail[1] = E1;
+      tail[2] = E2;
+      tail[3] = dsp0;
+      tail[4] = dsp1;
+      tail[5] = dsp2;
+      tail[6] = r_first;
+    }
+    __syncthreads();
+  };
+
   if (A.dbg) {
     if (blockIdx.x == 0) {
       const int64_t p = A.dbg_point;
@@ -975,6 +1084,10 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       if (dead) {
         write_fail(dead, 0, qnan());
         finish(0);
+        continue;
+      }
+      if constexpr (MONO) {  // E_c moves at fe2_hrom_mono_commit (k_mono_commit)
+        mono_point(p, Et0, Et1, Et2);
         continue;
       }
       for (int a = tid; a < NP; a += L::BT) {
@@ -1166,28 +1279,30 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   }
 }
 
-template <int NT>
+template <int NT, bool MONO = false>
 bool launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
   if (a.M.S != Big<NT>::S) return false;  // G2 rows must carry the padded strain-row stride
   const size_t smem = Big<NT>::bytes;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_increment_big<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_increment_big<NT, MONO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
     configured = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment_big<NT>, Big<NT>::BT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment_big<NT, MONO>, Big<NT>::BT, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = static_cast<int64_t>(num_sms) * per_sm;
   if (a.dbg) grid = 1;
   else if (grid > a.D.P) grid = a.D.P;
   if (grid < 1) grid = 1;
-  k_increment_big<NT><<<static_cast<unsigned>(grid), Big<NT>::BT, smem, s>>>(a);
+  k_increment_big<NT, MONO><<<static_cast<unsigned>(grid), Big<NT>::BT, smem, s>>>(a);
   return true;
 }
 
 }  // namespace
 
+#ifndef FE2_BIG_MONO_TU
 // NP = 40, 48, 56, 64 (32-point chunks) and 80, 96, 112, 128 (16-point chunks)
 bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s) {
   switch (a.M.NP) {
@@ -1216,5 +1331,22 @@ size_t increment_big_smem(int NP) {
     default: return 0;
   }
 }
+
+#else
+bool launch_increment_big_mono(const IncArgs& a, int num_sms, cudaStream_t s) {
+  switch (a.M.NP) {
+    case 40: return launch_big_nt<5, true>(a, num_sms, s);
+    case 48: return launch_big_nt<6, true>(a, num_sms, s);
+    case 56: return launch_big_nt<7, true>(a, num_sms, s);
+    case 64: return launch_big_nt<8, true>(a, num_sms, s);
+    case 80: return launch_big_nt<10, true>(a, num_sms, s);
+    case 96: return launch_big_nt<12, true>(a, num_sms, s);
+    case 112: return launch_big_nt<14, true>(a, num_sms, s);
+    case 128: return launch_big_nt<16, true>(a, num_sms, s);
+    default: return false;
+  }
+}
+
+#endif  // FE2_BIG_MONO_TU
 
 }  // namespace fe2
