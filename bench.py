@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--mono-iters", type=int, default=3,
+                    help="monolithic-scheme iterations per increment timed after e2e (0 = skip)")
     ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
     ap.add_argument("--points", type=int, default=0, help="override points per rank (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -365,12 +367,14 @@ def main():
     E_pin = pin(run.E_inc)
     o_sig, o_C, o_res = pin(np.empty((P, nc))), pin(np.empty((P, nt))), pin(np.empty(P))
     o_it, o_pc, o_st = (pin(np.empty(P, dtype=np.int32)) for _ in range(3))
+    e2e_bufs = []
     if ws > 1:  # the engine's own device output buffers, gathered after each host-API call
         p_sig, p_C, p_it, p_pc, p_res, p_st = eng.output_ptrs()
         e_sig = wrap_dev(p_sig, (P, nc), "<f8", dev)
         e_C = wrap_dev(p_C, (P, nt), "<f8", dev)
         e_res = wrap_dev(p_res, (P,), "<f8", dev)
         e_st = wrap_dev(p_st, (P,), "<i4", dev)
+        e2e_bufs.extend([e_sig, e_C, e_res, e_st])
 
     def e2e_step():
         eng.reset_points()
@@ -389,6 +393,37 @@ def main():
     e2e_value = P_total * incr * e2e_steps / (ms_e2e / 1e3)
     h2d = incr * P * nc * 8
     d2h = incr * P * (nc * 8 + nt * 8 + 8 + 3 * 4)
+
+    # ---- the monolithic scheme (the paper's method): every macro iteration advances
+    # each micro problem by ONE reduced Newton iteration, returns the condensed Σ
+    # and C_macro, and (N > 1) all-gathers them — SURVEY §8(e) config 3's "gathered
+    # each Newton iteration". Host-buffer C-ABI calls (fe2_hrom_mono_iterate), a
+    # fixed number of iterations per load increment, then fe2_hrom_mono_commit.
+    mono = None
+    if args.mono_iters > 0 and not run.finite:
+        if ws > 1 and not e2e_bufs:
+            p_sig, p_C, p_it, p_pc, p_res, p_st = eng.output_ptrs()
+            e2e_bufs.extend([wrap_dev(p_sig, (P, nc), "<f8", dev), wrap_dev(p_C, (P, nt), "<f8", dev),
+                             wrap_dev(p_res, (P,), "<f8", dev), wrap_dev(p_st, (P,), "<i4", dev)])
+
+        def mono_step():
+            eng.reset_points()
+            for k in range(incr):
+                eng.mono_begin()
+                for _ in range(args.mono_iters):
+                    eng.mono_iterate(run.E_inc[k])
+                    if ws > 1:
+                        run.gather(dist, ws, *e2e_bufs)
+                eng.mono_commit()
+
+        mono_step()
+        ms_mono = timed(mono_step, 1)
+        mono = {"value": P_total * incr * args.mono_iters / (ms_mono / 1e3), "unit": "point-iterations/s",
+                "iterations_per_increment": args.mono_iters, "ms_per_step": ms_mono,
+                "api": "fe2_hrom_mono_iterate (host buffers) per macro iteration"
+                       + (" + fe2_hrom_gather (NCCL)" if ws > 1 else "") + ", fe2_hrom_mono_commit per increment",
+                "note": "one condensed micro Newton iteration per point per macro iteration (the monolithic scheme); "
+                        "not the converged-increment unit of `value`"}
 
     # ---- the batched constitutive update on SoA HBM buffers (north_star item 1):
     # the HBM-bound kernel, timed alone on device-resident inputs: strains U[±0.03]
@@ -528,6 +563,7 @@ def main():
                    "commits_per_eval": stats["timed_commits"] / (P * incr * args.steps),
                    "plastic_fraction": stats["timed_plastic_evals"] / max(1, stats["timed_assemblies"] * K_j2)},
         "extra_configs": extras,
+        "monolithic": mono,
     }
     print(json.dumps(line), flush=True)
     if ws > 1:
