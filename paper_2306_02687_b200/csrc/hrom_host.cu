@@ -997,7 +997,7 @@ int fe2_hrom_create_fs(int device, int n, int K, const double* G4, const double*
       CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
       h->n = n;
       h->NP = (n + 7) / 8 * 8;
-      h->S = 4 * h->NP + 2;
+      h->S = 4 * (h->NP + 4) + 2;  // rows padded to NP + 4 (FsLayout: conflict-free A fragments)
       h->K = K;
       h->volume = volume;
       h->G.assign(G4, G4 + static_cast<size_t>(K) * 4 * n);
@@ -1025,13 +1025,14 @@ int fe2_hrom_create_fs(int device, int n, int K, const double* G4, const double*
       h->Kel = static_cast<int>(h->el_idx.size());
       h->Kelp = (h->Kel + kQC - 1) / kQC * kQC;
       const int NP = h->NP, S = h->S;
-      // rows [G4 row 0..3 (NP each) | w | 0]: J2 points (padded to K2p), then elastic points
+      // rows [G4 row 0..3 (NP + 4 each) | w | 0]: J2 points (padded to K2p), then elastic points
+      const int RG = NP + 4;
       std::vector<double> G2(static_cast<size_t>(h->K2p + h->Kelp) * S, 0.0);
       auto put = [&](int slot, int q) {
         for (int i = 0; i < 4; ++i)
           for (int a = 0; a < n; ++a)
-            G2[static_cast<size_t>(slot) * S + i * NP + a] = G4[(static_cast<size_t>(q) * 4 + i) * n + a];
-        G2[static_cast<size_t>(slot) * S + 4 * NP] = w[q];
+            G2[static_cast<size_t>(slot) * S + i * RG + a] = G4[(static_cast<size_t>(q) * 4 + i) * n + a];
+        G2[static_cast<size_t>(slot) * S + 4 * RG] = w[q];
       };
       for (int q2 = 0; q2 < h->K2; ++q2) put(q2, h->j2_idx[q2]);
       for (int e = 0; e < h->Kel; ++e) put(h->K2p + e, h->el_idx[e]);

@@ -39,7 +39,7 @@ struct ModelDev {
   double volume;
   MatDev mat2;            // the (single) J2 material of the history-carrying points
   // finite strain (kinematics 1): G2 is the 4-row gradient operator with rows
-  // [4 NP | w | 0] (S = 4 NP + 2), J2 chunks [0, nch_hist) then elastic chunks
+  // [4 x (NP + 4) | w | 0] (S = 4 (NP + 4) + 2), J2 chunks [0, nch_hist) then elastic chunks
   int nch_hist;           // chunks carrying history (J2 points, = K2p / kQC)
   int K_el;               // elastic cubature points (chunks nch_hist .. nchunks-1)
   MatDev matE;            // the (single) elastic material of the finite-strain model

@@ -47,7 +47,11 @@ constexpr int kSl = 21;         // slot stride: w A (16) | w P (4) | pad — con
 
 template <int NP>
 struct FsLayout {
-  static constexpr int S = 4 * NP + 2;  // [G row 0..3 (NP each) | w | 0]
+  // [G row 0..3 (RS each: NP + 4 pad) | w | 0]: RS ≡ 4 or 12 mod 16 doubles puts the
+  // four k-lanes' A-fragment rows of a point on distinct banks, S ≡ 2 mod 16 keeps
+  // the lanes' 128-bit row loads of the deformation step conflict-free
+  static constexpr int RS = NP + 4;
+  static constexpr int S = 4 * RS + 2;
   static constexpr int chunk = kQC * S;
   static constexpr int kSlots = kQC * kSl;
   static constexpr int LDK = NP + 1;                    // K_aa / LU row stride
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       const double2 al = av[k];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const double2 x = reinterpret_cast<const double2*>(Gq + r * NP)[k];
+        const double2 x = reinterpret_cast<const double2*>(Gq + r * L::RS)[k];
         a[r] += x.x * al.x;
         b[r] += x.y * al.y;
       }
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
       const int nv = valid(c);
       double F[4];
       deformation(Gb, H0, H1, H2, H3, F);
-      const double wq = Gb[lane * S + 4 * NP];
+      const double wq = Gb[lane * S + 4 * L::RS];
       BiotOut o;
       update_biot<true>(c < nchh ? M.mat2 : M.matE, h[0], h[1], h[2], h[3], h[4], F[0], F[1], F[2], F[3], o);
       const int npc = __popc(__ballot_sync(0xffffffffu, o.plastic && lane < nv));
@@ -451,8 +455,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) k_increment_fs(IncArgs A) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
 #pragma unroll
-          for (int r = 0; r < 4; ++r) pg[t][r] = g[r * NP + t * 8];
-          pa[t] = g[m * NP + t * 8];
+          for (int r = 0; r < 4; ++r) pg[t][r] = g[r * L::RS + t * 8];
+          pa[t] = g[m * L::RS + t * 8];
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) pw[r] = sq[m * 4 + r];
