@@ -120,7 +120,9 @@ int fe2_hrom_kinematics(fe2_hrom_t h, int* kinematics);
 int fe2_hrom_fs_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, const double* H, double* r,
                                double* Kaa, double* KaF, double* KFa, double* C_FF, double* P_raw);
 
-/* Allocate P macro points in the virgin state (α = 0, MaterialState{}).
+/* Allocate P >= 1 macro points in the virgin state (α = 0, MaterialState{}).
+ * P = 0 is ErrorCode::config; a batch that does not fit in HBM is
+ * ErrorCode::numeric and leaves the handle usable for a smaller P.
  * keep_flags != 0 also keeps per-(point, cubature point) plastic flags of
  * the last commit (P*K bytes) for parity checks. */
 int fe2_hrom_alloc_points(fe2_hrom_t h, int64_t P, int keep_flags);

@@ -20,7 +20,12 @@ template <class T>
 inline T* dalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
-  CK(cudaMalloc(&p, count * sizeof(T)));
+  const cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // not sticky: clear it so later launch checks do not report it
+    throw Failure(Code::numeric, std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
+                                     " bytes failed: " + cudaGetErrorString(e));
+  }
   return static_cast<T*>(p);
 }
 template <class T>

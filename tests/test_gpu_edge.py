@@ -66,3 +66,21 @@ def test_finite_strain_without_j2_points():
     H = F.make_paths(2, 0, 32, 6)
     g, o = run_both(m.G4, m.w, mat, m.materials, m.volume, H, finite=True)
     check(g, o, finite=True)
+
+
+def test_empty_and_oversized_batches_fail_cleanly():
+    """P = 0 is a config error; a batch beyond HBM fails with ErrorCode::numeric
+    (device allocation) and the handle then serves a normal batch."""
+    m = F.HyperRomModel(33, 12, 200, 0)
+    eng = F.HyperRomEngine.from_model(m)
+    with pytest.raises(F.Fe2Error) as e:
+        eng.alloc_points(0)
+    assert e.value.kind == "config"
+    with pytest.raises(F.Fe2Error) as e:
+        eng.alloc_points((1 << 31) - 1)  # ~0.5 PB of history
+    assert e.value.kind == "numeric" and "allocation" in str(e.value)
+    E = F.make_paths(0, 0, 16, 4)
+    eng.alloc_points(16)
+    outs = [eng.solve_increment(E[:, k]) for k in range(4)]
+    o = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume).run(E, threads=4)
+    np.testing.assert_array_equal(np.stack([x["iters"] for x in outs], 1), o["iters"])
