@@ -571,8 +571,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   double* sInv = sV + NP;
   double* sRp = sInv + NP;   // plastic part of r of the last pass (for the commit)
   double* sKaE = sRp + NP;   // [NP][3]
-  double* sDC = sKaE + 3 * NP;
-  double* sDS = sDC + QB * 6;
+  double* sDS = sKaE + 3 * NP + QB * 6;  // (QB * 6 doubles before it are spare)
   int* sQ = reinterpret_cast<int*>(sDS + QB * 3);
   int* sRO = sQ + QB;  // [3 QB] G-chunk offset of plastic row f = 3 slot + i
   double* red = sDS + QB * 5;
@@ -739,85 +738,68 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       int slot, np;
       BIG_T(1);
       compact(plastic, slot, np);
-      if (plastic) {
-        const double wq = M.w2[q];
-        double* dc = sDC + slot * 6;
-        dc[0] = wq * cr.dc00;
-        dc[1] = wq * cr.dc01;
-        dc[2] = wq * cr.dc02;
-        dc[3] = wq * cr.dc11;
-        dc[4] = wq * cr.dc12;
-        dc[5] = wq * cr.dc22;
-        sDS[slot * 3 + 0] = wq * cr.ds0;
-        sDS[slot * 3 + 1] = wq * cr.ds1;
-        sDS[slot * 3 + 2] = wq * cr.ds2;
-        sQ[slot] = qi;
-        c00 += dc[0];
-        c01 += dc[1];
-        c02 += dc[2];
-        c11 += dc[3];
-        c12 += dc[4];
-        c22 += dc[5];
-        ds0 += sDS[slot * 3 + 0];
-        ds1 += sDS[slot * 3 + 1];
-        ds2 += sDS[slot * 3 + 2];
-      }
-      const int np4 = (np + 3) & ~3;
-      if (tid < np4 - np) {
-        const int z = np + tid;
-#pragma unroll
-        for (int e = 0; e < 6; ++e) sDC[z * 6 + e] = 0.0;
-        sDS[z * 3 + 0] = sDS[z * 3 + 1] = sDS[z * 3 + 2] = 0.0;
-        sQ[z] = 0;
-      }
-      n_pl += static_cast<unsigned long long>(tid == 0 ? np : 0);
-      np_tot += np;
-      __syncthreads();
-      BIG_T(2);
-      // stage the slots' B rows (w ΔC_q) G_q and the G-chunk offsets of their A
-      // rows; warp w stages slots w, w + BW, ... (lanes over the modes), two
-      // slots at a time with every load issued before the first store (the
-      // compiler cannot move loads above possibly aliasing shared stores)
+      // The point's TPQ threads stage its operand rows right away (no staging
+      // pass, no CTA barrier before it): the return-map lane's w ΔC_q, slot and
+      // flag go to its siblings by shuffles, each thread writes the B rows
+      // (w ΔC_q) G_q of its modes (128-bit) and lanes sub < 3 the A-row offsets.
       {
-        constexpr int NA = NP / 32 > 0 ? (NP + 31) / 32 : 1;  // modes per lane
-        for (int s0 = warp; s0 < np4; s0 += 2 * L::BW) {
-          const int s1 = s0 + L::BW;
-          const bool two = s1 < np4;
-          double d[2][6], g[2][NA][3];
-          int qo[2];
+        const int src = lane & ~(TPQ - 1);
+        const double wq = (sub == 0 && plastic) ? M.w2[q] : 0.0;
+        double d00 = wq * cr.dc00, d01 = wq * cr.dc01, d02 = wq * cr.dc02;
+        double d11 = wq * cr.dc11, d12 = wq * cr.dc12, d22 = wq * cr.dc22;
+        if (plastic) {  // the return-map lane (sub == 0)
+          sDS[slot * 3 + 0] = wq * cr.ds0;
+          sDS[slot * 3 + 1] = wq * cr.ds1;
+          sDS[slot * 3 + 2] = wq * cr.ds2;
+          sQ[slot] = qi;
+          c00 += d00;
+          c01 += d01;
+          c02 += d02;
+          c11 += d11;
+          c12 += d12;
+          c22 += d22;
+          ds0 += sDS[slot * 3 + 0];
+          ds1 += sDS[slot * 3 + 1];
+          ds2 += sDS[slot * 3 + 2];
+        }
+        const bool pl = __shfl_sync(0xffffffffu, plastic ? 1 : 0, src) != 0;
+        const int ps = __shfl_sync(0xffffffffu, slot, src);
+        d00 = __shfl_sync(0xffffffffu, d00, src);
+        d01 = __shfl_sync(0xffffffffu, d01, src);
+        d02 = __shfl_sync(0xffffffffu, d02, src);
+        d11 = __shfl_sync(0xffffffffu, d11, src);
+        d12 = __shfl_sync(0xffffffffu, d12, src);
+        d22 = __shfl_sync(0xffffffffu, d22, src);
+        if (pl) {
+          const double2* Gq = reinterpret_cast<const double2*>(Gb + qi * S);
+          double2* br = reinterpret_cast<double2*>(stB + 3 * ps * L::RS);
+          if (sub < 3) sRO[3 * ps + sub] = qi * S + sub * L::RS;
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int sl = u ? (two ? s1 : s0) : s0;
-            qo[u] = sQ[sl] * S;
-#pragma unroll
-            for (int e = 0; e < 6; ++e) d[u][e] = sDC[sl * 6 + e];
-#pragma unroll
-            for (int k = 0; k < NA; ++k) {
-              const int a = lane + 32 * k;
-              const double* Gq = Gb + qo[u] + (a < NP ? a : 0);
-              g[u][k][0] = Gq[0];
-              g[u][k][1] = Gq[L::RS];
-              g[u][k][2] = Gq[2 * L::RS];
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (u == 1 && !two) break;
-            const int sl = u ? s1 : s0;
-            double* br = stB + 3 * sl * L::RS;
-            if (lane < 3) sRO[3 * sl + lane] = qo[u] + lane * L::RS;
-#pragma unroll
-            for (int k = 0; k < NA; ++k) {
-              const int a = lane + 32 * k;
-              if (a >= NP) break;
-              const double g0 = g[u][k][0], g1 = g[u][k][1], g2 = g[u][k][2];
-              br[a] = d[u][0] * g0 + d[u][1] * g1 + d[u][2] * g2;
-              br[L::RS + a] = d[u][1] * g0 + d[u][3] * g1 + d[u][4] * g2;
-              br[2 * L::RS + a] = d[u][2] * g0 + d[u][4] * g1 + d[u][5] * g2;
-            }
+          for (int j = sub; j < NP / 2; j += TPQ) {
+            const double2 g0 = Gq[j], g1 = Gq[L::RS / 2 + j], g2 = Gq[L::RS + j];
+            br[j] = make_double2(d00 * g0.x + d01 * g1.x + d02 * g2.x, d00 * g0.y + d01 * g1.y + d02 * g2.y);
+            br[L::RS / 2 + j] =
+                make_double2(d01 * g0.x + d11 * g1.x + d12 * g2.x, d01 * g0.y + d11 * g1.y + d12 * g2.y);
+            br[L::RS + j] = make_double2(d02 * g0.x + d12 * g1.x + d22 * g2.x, d02 * g0.y + d12 * g1.y + d22 * g2.y);
           }
         }
       }
+      const int np4 = (np + 3) & ~3;
+      {  // pad slots [np, np4): zero B rows, Δσ and valid A-row offsets
+        const int per = 3 * (NP / 2);
+        for (int e = tid; e < (np4 - np) * per; e += L::BT) {
+          const int z = np + e / per, r = e % per;
+          reinterpret_cast<double2*>(stB + (3 * z + r / (NP / 2)) * L::RS)[r % (NP / 2)] = make_double2(0.0, 0.0);
+        }
+        if (tid < 3 * (np4 - np)) {
+          const int z = np + tid / 3, i = tid % 3;
+          sRO[3 * z + i] = i * L::RS;
+          sDS[3 * z + i] = 0.0;
+        }
+      }
+      n_pl += static_cast<unsigned long long>(tid == 0 ? np : 0);
+      np_tot += np;
+      BIG_T(2);
       __syncthreads();
       BIG_T(3);
       contract_dispatch<NT, MP>(warp, Gb, sRO, stB, sDS, np4, acc, kae, rr, lane);
