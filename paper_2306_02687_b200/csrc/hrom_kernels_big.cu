@@ -481,6 +481,98 @@ __device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
   return ok;
 }
 
+// Left-looking blocked Cholesky (panels of kPB columns) of the packed lower
+// sK on the whole CTA: per panel, (1) every row thread subtracts the products
+// with the previous columns (TPR threads per row split the k range), (2) lanes
+// of warp 0 factor the kPB x kPB diagonal block with shuffles, (3) the rows
+// below solve against it — 3 barriers per panel instead of 2 per column.
+// False (CTA-uniform) if not SPD.
+constexpr int kPB = 4;
+template <int BT, int NP>
+__device__ bool cta_cholesky_blk(double* sK, double* sInv, double* flag, int n) {
+  constexpr int TPR = (2 * NP <= BT) ? 2 : 1;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int row = tid / TPR, h = tid % TPR;
+  const bool live = row < n;
+  double* ri = sK + tri(live ? row : 0);
+  for (int j0 = 0; j0 < n; j0 += kPB) {
+    const int nb = min(kPB, n - j0);
+    double s[kPB];
+#pragma unroll
+    for (int c = 0; c < kPB; ++c) s[c] = 0.0;
+    if (live && row >= j0 && j0 > 0) {
+      for (int k = h; k < j0; k += TPR) {
+        const double lr = ri[k];
+#pragma unroll
+        for (int c = 0; c < kPB; ++c)
+          if (c < nb && j0 + c <= row) s[c] += lr * sK[tri(j0 + c) + k];
+      }
+    }
+    if constexpr (TPR == 2) {
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) s[c] += __shfl_xor_sync(0xffffffffu, s[c], 1);
+    }
+    if (live && row >= j0 && h == 0 && j0 > 0) {
+#pragma unroll
+      for (int c = 0; c < kPB; ++c)
+        if (c < nb && j0 + c <= row) ri[j0 + c] -= s[c];
+    }
+    __syncthreads();
+    if (tid < 32) {  // diagonal block: lane r < nb holds block row r
+      double a[kPB];
+      const int r = lane < nb ? lane : 0;
+      const double* br = sK + tri(j0 + r) + j0;
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) a[c] = (c <= r && c < nb) ? br[c] : 0.0;
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < kPB; ++k) {
+        if (k < nb) {
+          const double d = __shfl_sync(0xffffffffu, a[k], k);
+          if (!(d > 0.0)) ok = false;
+          const double inv = rsqrt_fast(d);
+          if (lane == k) {
+            a[k] = d * inv;
+            sInv[j0 + k] = inv;
+          } else if (lane > k) {
+            a[k] *= inv;
+          }
+#pragma unroll
+          for (int c = k + 1; c < kPB; ++c) {
+            const double lck = __shfl_sync(0xffffffffu, a[k], c);
+            if (lane >= c && lane < nb) a[c] -= a[k] * lck;
+          }
+        }
+      }
+      if (lane < nb) {
+        double* bw = sK + tri(j0 + lane) + j0;
+#pragma unroll
+        for (int c = 0; c < kPB; ++c)
+          if (c <= lane) bw[c] = a[c];
+      }
+      if (lane == 0) flag[0] = ok ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (flag[0] == 0.0) return false;
+    if (live && h == 0 && row >= j0 + nb) {
+      double l[kPB];
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) {
+        if (c < nb) {
+          double t = ri[j0 + c];
+          const double* lc = sK + tri(j0 + c) + j0;
+#pragma unroll
+          for (int k = 0; k < c; ++k) t -= l[k] * lc[k];
+          l[c] = t * sInv[j0 + c];
+          ri[j0 + c] = l[c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
 // Forward substitution L y = b in place on sB[n] (cols RHS interleaved: sB[i*cols + c]).
 template <int NW, int BW>
 __device__ void cta_forward(const double* sK, const double* sInv, double* sB, int n, int cols) {
@@ -890,7 +982,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       __syncthreads();
       return true;
     }
-    return cta_cholesky<L::BT, NP>(sK, sInv, red + L::RED - 2, n);  // clear of block sums
+    return cta_cholesky_blk<L::BT, NP>(sK, sInv, red + L::RED - 2, n);  // clear of block sums
   };
 
   // accept the last pass's state: flip to its candidate history, α_c, and move
