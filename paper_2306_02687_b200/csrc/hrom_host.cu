@@ -441,13 +441,14 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
       // 64 modes, whose mode split needs NP a multiple of 16
       h->NP = (n + 7) / 8 * 8;
       if (h->NP > 64) h->NP = (n + 15) / 16 * 16;
-      // G2 row of a cubature point: [G0 | G1 | G2 | w, 0] (S = 3 NP + 2) for
-      // the warp-per-point kernel; for the CTA-per-point kernel (NP > 32) each
+      // G2 record of a cubature point: rows G0 | G1 | G2 at g2_row_offset(NP, i)
+      // then [w, 0] for the warp-per-point kernel (the three rows on distinct
+      // bank groups); for the CTA-per-point kernel (NP > 32) each
       // strain row is padded to RG = NP + 4 doubles (≡ 4 or 12 mod 16), S =
       // 3 RG, so its DMMA A fragments read the rows of consecutive cubature
       // points conflict-free straight from the G chunk (weight in row 0's pad).
-      const int RG = h->NP > 32 ? h->NP + 4 : h->NP;
-      h->S = h->NP > 32 ? 3 * RG : 3 * h->NP + 2;
+      const int RG = h->NP + 4;  // NP > 32
+      h->S = h->NP > 32 ? 3 * RG : g2_row_offset(h->NP, 2) + h->NP + 2;
       h->K = K;
       h->volume = volume;
       h->G.assign(G, G + static_cast<size_t>(K) * 3 * n);
@@ -474,9 +475,11 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
         const int q = h->j2_idx[q2];
         for (int i = 0; i < 3; ++i)
           for (int a = 0; a < n; ++a)
-            G2[static_cast<size_t>(q2) * S + i * RG + a] = G[(static_cast<size_t>(q) * 3 + i) * n + a];
+            G2[static_cast<size_t>(q2) * S + (NP > 32 ? i * RG : g2_row_offset(NP, i)) + a] =
+                G[(static_cast<size_t>(q) * 3 + i) * n + a];
         w2[q2] = w[q];
-        G2[static_cast<size_t>(q2) * S + (NP > 32 ? NP : 3 * NP)] = w[q];  // the weight also rides in a pad
+        // the weight also rides in a pad (row 0's for NP > 32, the record's last two doubles otherwise)
+        G2[static_cast<size_t>(q2) * S + (NP > 32 ? NP : S - 2)] = w[q];
       }
       // elastic predictor over ALL cubature points (J2 points with the J2
       // material's C_e): K_e = Σ w G^T C_e G, K_aE,e = Σ w G^T C_e, C_EE,e = Σ w C_e.

@@ -265,7 +265,10 @@ constexpr int kMaxStages = FE2_STAGES;  // G-chunk ring depth (shared by the CTA
 
 template <int NP, int W>
 struct IncLayout {
-  static constexpr int S = 3 * NP + 2;
+  // G2 record of a cubature point: rows at R1 / R2 (see g2_row_offset) then
+  // [w | 0]; S/2 odd keeps the lane-per-point 128-bit row loads conflict-free
+  static constexpr int R1 = g2_row_offset(NP, 1), R2 = g2_row_offset(NP, 2);
+  static constexpr int S = R2 + NP + 2;
   static constexpr int chunk = kQC * S;                      // doubles per ring stage
   static constexpr int kSlots = kQC * 6 + kQC * 3 + kQC;     // w ΔC (6 unique), w Δσ, point index
   static constexpr int kTri = NP * (NP + 1) / 2;              // packed lower K_aa
@@ -529,8 +532,8 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       double e0 = 0.0, e1 = 0.0, e2 = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
       {  // ε = G_q α with 128-bit shared loads (rows are 16-B aligned, S even)
         const double2* g0v = reinterpret_cast<const double2*>(Gq);
-        const double2* g1v = reinterpret_cast<const double2*>(Gq + NP);
-        const double2* g2v = reinterpret_cast<const double2*>(Gq + 2 * NP);
+        const double2* g1v = reinterpret_cast<const double2*>(Gq + L::R1);
+        const double2* g2v = reinterpret_cast<const double2*>(Gq + L::R2);
         const double2* av = reinterpret_cast<const double2*>(sAev);
 #pragma unroll 4
         for (int a = 0; a < NP / 2; ++a) {
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       }
       if (plastic) {
         const Corr cr = radial_return(mt, T);
-        const double wq = Gq[3 * NP];  // cubature weight rides in the row's pad
+        const double wq = Gq[L::R2 + NP];  // cubature weight rides in the record's pad
         const int slot = __popc(bal & ((1u << lane) - 1u));
         const double w00 = wq * cr.dc00, w01 = wq * cr.dc01, w02 = wq * cr.dc02;
         const double w11 = wq * cr.dc11, w12 = wq * cr.dc12, w22 = wq * cr.dc22;
@@ -613,6 +616,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
         for (int s = 0; s < 3; ++s) {
           const int slot = 4 * g + qo[s];
           const int i = io[s];
+          const int ro_i = i * L::R1;  // row i of the slot's point (rows R1 apart)
           // row i of the symmetric w ΔC from its 6 unique entries (00 01 02 11 12 22)
           const int b = i > 0 ? 1 : 0;
           const double* wc = sDC + slot * 6;
@@ -622,8 +626,8 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
           double Af[NT], Bf[NT];
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
-            const double g0 = gp[t * 8], g1 = gp[NP + t * 8], g2 = gp[2 * NP + t * 8];
-            Af[t] = gp[i * NP + t * 8];
+            const double g0 = gp[t * 8], g1 = gp[L::R1 + t * 8], g2 = gp[L::R2 + t * 8];
+            Af[t] = gp[ro_i + t * 8];
             Bf[t] = k0 * g0 + k1 * g1 + k2 * g2;
             kae[t][s] += Bf[t];
             rr[t] += ws * Af[t];

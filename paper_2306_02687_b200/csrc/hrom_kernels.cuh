@@ -20,11 +20,20 @@ struct PointState {
   int pad[3];
 };
 
+// Offset of strain row i (0..2) in a cubature point's G2 record for the
+// warp-per-point kernel (NP <= 32). For NP ≡ 0 mod 16 the rows are padded to
+// NP + 4 doubles so the three rows of a point start on distinct bank groups
+// (rows NP apart would all collide: a 4-way conflict on the DMMA A-fragment
+// loads; +26% at n = 16, +9-12% at n = 32); NP ≡ 8 mod 16 keeps rows NP
+// apart (a padded variant measured slower at n = 8 and 24).
+constexpr int g2_row_stride(int NP) { return NP % 16 == 0 ? NP + 4 : NP; }
+constexpr int g2_row_offset(int NP, int i) { return i * g2_row_stride(NP); }
+
 struct ModelDev {
   int n;        // modes
   int NP;       // modes padded to a multiple of 8 (DMMA tile)
-  int S;        // doubles per cubature point in G2: 3*NP + 2 (NP <= 32: 16-B rows, conflict-free 128-bit
-                // lane loads) or 3*(NP + 4) (NP > 32: strain rows padded to NP + 4, k_increment_big)
+  int S;        // doubles per cubature point in G2: g2_row_offset(NP, 2) + NP + 2 (NP <= 32: rows at
+                // g2_row_offset, [w | 0] last) or 3*(NP + 4) (NP > 32: rows padded to NP + 4, k_increment_big)
   int K2;       // J2 cubature points
   int K2p;      // padded to a multiple of kQC
   int nchunks;  // K2p / kQC
