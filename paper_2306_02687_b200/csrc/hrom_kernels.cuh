@@ -25,7 +25,7 @@ struct PointState {
 // NP + 4 doubles so the three rows of a point start on distinct bank groups
 // (rows NP apart would all collide: a 4-way conflict on the DMMA A-fragment
 // loads; +26% at n = 16, +9-12% at n = 32); NP ≡ 8 mod 16 keeps rows NP
-// apart (a padded variant measured slower at n = 8 and 24).
+// apart (padding them to NP + 4 measured 5-10% slower at n = 8 and 24).
 constexpr int g2_row_stride(int NP) { return NP % 16 == 0 ? NP + 4 : NP; }
 constexpr int g2_row_offset(int NP, int i) { return i * g2_row_stride(NP); }
 
