@@ -1,26 +1,30 @@
 // B200 (sm_100a) persistent increment kernel for LARGE reduced bases
-// (n = 33…128, BASELINE configs 3 and 4): one CTA of 8 warps per macro point.
+// (n = 33…128, BASELINE configs 3 and 4): one CTA per macro point (4 warps and
+// two CTAs per SM for n <= 64, 8 warps above).
 //
 // Same algebra and same increment/Newton semantics as k_increment
 // (hrom_kernels.cu), re-tiled for n > 32:
-//  - G chunks (QB = 32 or 16 cubature points) stream through a 2-stage
-//    shared ring by TMA bulk copies; the CTA walks them in lockstep.
-//  - Material phase: TPQ = 256/QB threads per cubature point split the modes
-//    of ε_q = E + G_q α and reduce with shuffles; one lane runs the elastic
-//    trial / yield test / radial return.
+//  - G chunks (QB = 16 cubature points; strain rows padded to RS = NP + 4
+//    doubles) stream through a 2-stage shared ring by TMA bulk copies; the
+//    CTA walks them in lockstep.
+//  - Material phase: TPQ = BT/QB threads per cubature point split the modes of
+//    ε_q = E + G_q α (128-bit loads) and reduce with shuffles; one lane runs
+//    the elastic trial / yield test / radial return and writes the candidate
+//    history (double-buffered, no commit pass).
 //  - Plastic points of a chunk are compacted CTA-wide (ballot + warp prefix,
-//    deterministic order); each plastic slot's operand rows are then staged
-//    once in shared memory — A rows G_q (3 x NP) and B rows (w ΔC_q) G_q —
-//    with a row stride of NP + 4 doubles (≡ 4 or 12 mod 16), so every DMMA
-//    fragment is ONE conflict-free 64-bit shared load (the staging area
-//    aliases K_aa, which is dead during an assembly pass).
+//    deterministic order); each plastic point's threads then stage its B rows
+//    (w ΔC_q) G_q (stride RS, aliasing K_aa, dead during a pass) and the
+//    G-chunk offsets of its A rows, so every DMMA fragment is ONE conflict-free
+//    64-bit shared load.
 //  - The NT(NT+1)/2 upper tile pairs of K_aa are contracted on the FP64
-//    tensor cores (DMMA) in register blocks balanced over the warps at
-//    compile time (largest-first), fragments prefetched one k-step ahead;
-//    the K_aE and r corrections ride on the diagonal-tile owners' fragments
-//    (NT <= 8) or are summed from the staged rows.
-//  - Newton / line search / bisection / condensation run CTA-wide:
-//    left-looking Cholesky of the packed K_aa with one row per thread.
+//    tensor cores (DMMA) in compile-time register blocks (folded tile rows for
+//    n = 64 / 128: NT + 1 pairs per warp), fragments prefetched one k-step
+//    ahead; the K_aE and r corrections ride on the diagonal-tile owners'
+//    fragments (n <= 64) or are summed from the staged rows.
+//  - Newton / line search / bisection / condensation run CTA-wide: blocked
+//    left-looking Cholesky of the packed K_aa (4-column panels), substitutions
+//    on the row warps. MONO = the monolithic scheme's single iteration
+//    (fe2_hrom_mono_iterate; instantiated in hrom_kernels_big_mono.cu).
 #include "device_common.cuh"
 #include "hrom_kernels.cuh"
 
@@ -71,8 +75,8 @@ struct Big {
 
 // Tile pairs (t1 <= t2) of one warp. NT = 2 x warps (n = 64 on 4 warps,
 // n = 128 on 8): folded tile rows, NT + 1 pairs per warp. Otherwise the upper
-// triangle is cut into tile blocks (b x b; the off-diagonal blocks of NT = 8
-// split into 2 x 4 halves) dealt largest-first to the least-loaded warp. The
+// triangle is cut into b x b tile blocks dealt largest-first to the
+// least-loaded warp. The
 // contraction is DMMA-issue bound per warp once the fragments are single
 // conflict-free loads, so balance beats fragment reuse.
 struct PairTable {
@@ -95,8 +99,7 @@ constexpr PairTable pairs_for(int W) {
       }
     return P;
   }
-  const int b = (NT == 8 || NT == 16) ? 4 : 2;
-  const bool split = NT == 8;
+  const int b = 2;
   const int nb = (NT + b - 1) / b;
   // blocks as (row tiles [r0, r1), col tiles [c0, c1)), pair count
   int r0[64] = {}, r1[64] = {}, c0[64] = {}, c1[64] = {}, cnt[64] = {}, nbk = 0;
@@ -104,7 +107,7 @@ constexpr PairTable pairs_for(int W) {
     for (int B2 = B1; B2 < nb; ++B2) {
       const int ra = B1 * b, rb = (B1 * b + b < NT) ? B1 * b + b : NT;
       const int ca = B2 * b, cb = (B2 * b + b < NT) ? B2 * b + b : NT;
-      const int parts = (split && B1 != B2) ? 2 : 1;
+      const int parts = 1;
       const int h = (rb - ra + parts - 1) / parts;
       for (int s = 0; s < parts; ++s) {
         r0[nbk] = ra + s * h;
@@ -428,57 +431,6 @@ __device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
     for (int w = 0; w < BW; ++w) s += red[w * N + k];
     v[k] = s;
   }
-}
-
-// Left-looking Cholesky of the packed lower sK on the whole CTA: TPR
-// adjacent threads per row split each dot product (stride TPR) and combine it
-// with shuffles. False (CTA-uniform) if not SPD.
-template <int BT, int NP>
-__device__ bool cta_cholesky(double* sK, double* sInv, double* red, int n) {
-  constexpr int TPR = (2 * NP <= BT) ? 2 : 1;
-  const int tid = threadIdx.x;
-  const int row = tid / TPR, h = tid % TPR;
-  const bool live = row < n;
-  bool ok = true;
-  for (int j = 0; j < n; ++j) {
-    double s = 0.0;
-    const double* ri = sK + tri(row);
-    const double* rj = sK + tri(j);
-    if (live && row >= j) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int k = h;
-      for (; k + 3 * TPR < j; k += 4 * TPR) {
-        a0 += ri[k] * rj[k];
-        a1 += ri[k + TPR] * rj[k + TPR];
-        a2 += ri[k + 2 * TPR] * rj[k + 2 * TPR];
-        a3 += ri[k + 3 * TPR] * rj[k + 3 * TPR];
-      }
-      for (; k < j; k += TPR) a0 += ri[k] * rj[k];
-      s = (a0 + a1) + (a2 + a3);
-    }
-    if constexpr (TPR == 2) s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (live && row >= j) {
-      s = ri[j] - s;
-      if (row == j && h == 0) red[0] = s;
-    }
-    __syncthreads();
-    const double d = red[0];
-    if (!(d > 0.0)) {  // uniform over the CTA
-      ok = false;
-      break;
-    }
-    const double inv = rsqrt_fast(d);
-    if (h == 0 && live) {
-      if (row == j) {
-        sK[tri(j) + j] = d * inv;
-        sInv[j] = inv;
-      } else if (row > j) {
-        sK[tri(row) + j] = s * inv;
-      }
-    }
-    __syncthreads();
-  }
-  return ok;
 }
 
 // Left-looking blocked Cholesky (panels of kPB columns) of the packed lower
