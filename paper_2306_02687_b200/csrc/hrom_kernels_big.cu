@@ -166,7 +166,7 @@ constexpr int total_pairs() {
 static_assert(total_pairs<5>() == 15 && total_pairs<8>() == 36 && total_pairs<12>() == 78 &&
                   total_pairs<16>() == 136,
               "tile-pair partition must cover the upper triangle");
-static_assert(max_pairs<8>() == 9 && max_pairs<16>() == 17, "unexpected partition balance");
+static_assert((bw_for(8) != 4 || max_pairs<8>() == 9) && max_pairs<16>() == 17, "unexpected partition balance");
 
 // non-volatile DMMA (pure in its operands: the scheduler may interleave the
 // fragment loads of the next k-step)
