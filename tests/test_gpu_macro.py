@@ -58,12 +58,13 @@ def test_device_finite_strain_macro_driver_matches_oracle():
 
 
 @pytest.mark.parametrize("u_max,n_load,n,K", [(0.02, 3, 12, 200), (0.3, 10, 12, 200), (0.3, 6, 40, 300),
-                                             (0.3, 4, 64, 500)])
+                                             (0.3, 4, 64, 500), (0.3, 3, 128, 600)])
 def test_device_monolithic_driver_matches_oracle(u_max, n_load, n, K):
     """Monolithic scheme (fe2_hrom_mono_*): the device macro driver against
     the oracle's monolithic driver — identical steps and macro iteration
     counts, micro iterations = P per macro iteration, R within 1e-8. n = 12
-    runs the warp-per-point kernel, n = 40 / 64 the CTA-per-point one."""
+    runs the warp-per-point kernel, n = 40 / 64 / 128 the CTA-per-point one
+    (4- and 8-warp CTAs)."""
     m = F.HyperRomModel(33, n, K, 0)
     eng = F.HyperRomEngine.from_model(m)
     cfg = F.MacroConfig(u_max=u_max, n_load=n_load, scheme="monolithic")
