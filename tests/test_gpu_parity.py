@@ -208,13 +208,18 @@ def test_large_basis_assembly_matches_oracle(n, K):
 
 @pytest.mark.parametrize("n,K,P,incr", [(64, 600, 48, 6), (128, 1000, 16, 4)])
 def test_large_basis_trajectory_parity(n, K, P, incr):
+    """CTA-per-point kernel end to end: iteration counts, per-(point,
+    cubature point) plastic flags of every commit, Σ / C, committed state."""
     m = F.HyperRomModel(33, n, K, 2)
     E = F.make_paths(0, 2, P, incr)
-    eng, g = run_gpu(m, E, keep_flags=True)
-    o = O.Hrom(m.G, m.w, m.mat, m.materials, m.volume).run(E, threads=16, flags=True)
+    eng, g, o = run_both(m, E, P)
     assert (o["status"] == 0).all() and (g["status"] == 0).all()
     np.testing.assert_array_equal(g["iters"], o["iters"])
     np.testing.assert_array_equal(g["plastic_count"], o["plastic_count"])
+    np.testing.assert_array_equal(g["flags"], o["plastic_flags"])
+    alpha, state, _ = eng.read_state()
+    np.testing.assert_allclose(alpha, o["alpha"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(state, o["state"], rtol=1e-9, atol=1e-12)
     assert path_rel_err(g["sigma"], o["sigma"]).max() < REL
     assert rel_err(g["C"].reshape(-1, 9), o["C"].reshape(-1, 9)).max() < REL
 
