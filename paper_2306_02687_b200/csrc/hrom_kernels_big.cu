@@ -45,6 +45,15 @@ using namespace dev;
 // barrier-bound phases (compaction, factorization) the other keeps the FP64
 // pipe busy (+21% at n = 64); 8 for NP > 64, whose accumulators would not
 // fit 4 warps' registers.
+// The assembly pass is a lambda with two call sites (Newton loop, debug
+// probe); NVVM inlines it for n = 64 / 128 but not for the other widths, whose
+// kernels are compiled in hrom_kernels_big_other.cu with it forced inline
+// (forcing it here cost n = 64 3%).
+#ifdef FE2_BIG_INLINE_PASS
+#define FE2_BIG_PASS_ATTR __attribute__((always_inline))
+#else
+#define FE2_BIG_PASS_ATTR
+#endif
 #ifndef FE2_BIG_SMALL_WARPS
 #define FE2_BIG_SMALL_WARPS 4
 #endif
@@ -718,7 +727,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   bool k_linear = false;
   double rn_pass = 0.0;  // |r| of the last pass
 
-  auto assembly_pass = [&](int64_t p, double E0, double E1, double E2) {
+  auto assembly_pass = [&](int64_t p, double E0, double E1, double E2) FE2_BIG_PASS_ATTR {
     double acc[MP][2];
 #pragma unroll
     for (int j = 0; j < MP; ++j) acc[j][0] = acc[j][1] = 0.0;
@@ -1328,19 +1337,14 @@ bool launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
 
 }  // namespace
 
-#ifndef FE2_BIG_MONO_TU
-// NP = 40, 48, 56, 64 (32-point chunks) and 80, 96, 112, 128 (16-point chunks)
+#if !defined(FE2_BIG_MONO_TU) && !defined(FE2_BIG_OTHER_TU)
+// NP = 64 and 128 (BASELINE configs 3/4) here; 40, 48, 56, 80, 96, 112 in
+// hrom_kernels_big_other.cu
 bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s) {
   switch (a.M.NP) {
-    case 40: return launch_big_nt<5>(a, num_sms, s);
-    case 48: return launch_big_nt<6>(a, num_sms, s);
-    case 56: return launch_big_nt<7>(a, num_sms, s);
     case 64: return launch_big_nt<8>(a, num_sms, s);
-    case 80: return launch_big_nt<10>(a, num_sms, s);
-    case 96: return launch_big_nt<12>(a, num_sms, s);
-    case 112: return launch_big_nt<14>(a, num_sms, s);
     case 128: return launch_big_nt<16>(a, num_sms, s);
-    default: return false;
+    default: return launch_increment_big_other(a, num_sms, s);
   }
 }
 
@@ -1355,6 +1359,19 @@ size_t increment_big_smem(int NP) {
     case 112: return Big<14>::bytes;
     case 128: return Big<16>::bytes;
     default: return 0;
+  }
+}
+
+#elif defined(FE2_BIG_OTHER_TU)
+bool launch_increment_big_other(const IncArgs& a, int num_sms, cudaStream_t s) {
+  switch (a.M.NP) {
+    case 40: return launch_big_nt<5>(a, num_sms, s);
+    case 48: return launch_big_nt<6>(a, num_sms, s);
+    case 56: return launch_big_nt<7>(a, num_sms, s);
+    case 80: return launch_big_nt<10>(a, num_sms, s);
+    case 96: return launch_big_nt<12>(a, num_sms, s);
+    case 112: return launch_big_nt<14>(a, num_sms, s);
+    default: return false;
   }
 }
 
