@@ -246,6 +246,9 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
 #ifndef FE2_KW
 #define FE2_KW 16
 #endif
+#ifndef FE2_MONO_KW
+#define FE2_MONO_KW 16
+#endif
 #ifndef FE2_STAGES
 #define FE2_STAGES 6
 #endif
@@ -1251,10 +1254,10 @@ void launch_mono_commit(const PointsDev& D, int NP, const double* mono, cudaStre
 void launch_increment_mono(const IncArgs& a, int num_sms, cudaStream_t s) {
   switch (a.M.NP) {
     // the monolithic iteration keeps 16 warps (measured 14% faster than 8 at n = 24)
-    case 8: launch_inc_variant<1, FE2_KW, false, true>(a, num_sms, s, IncLayout<8, FE2_KW>::bytes); break;
-    case 16: launch_inc_variant<2, FE2_KW, false, true>(a, num_sms, s, IncLayout<16, FE2_KW>::bytes); break;
-    case 24: launch_inc_variant<3, FE2_KW, false, true>(a, num_sms, s, IncLayout<24, FE2_KW>::bytes); break;
-    case 32: launch_inc_variant<4, FE2_KW, false, true>(a, num_sms, s, IncLayout<32, FE2_KW>::bytes); break;
+    case 8: launch_inc_variant<1, FE2_MONO_KW, false, true>(a, num_sms, s, IncLayout<8, FE2_MONO_KW>::bytes); break;
+    case 16: launch_inc_variant<2, FE2_MONO_KW, false, true>(a, num_sms, s, IncLayout<16, FE2_MONO_KW>::bytes); break;
+    case 24: launch_inc_variant<3, FE2_MONO_KW, false, true>(a, num_sms, s, IncLayout<24, FE2_MONO_KW>::bytes); break;
+    case 32: launch_inc_variant<4, FE2_MONO_KW, false, true>(a, num_sms, s, IncLayout<32, FE2_MONO_KW>::bytes); break;
     default: break;
   }
 }
