@@ -69,9 +69,12 @@ def test_oracle_header_is_test_infrastructure_only():
 def test_exchange_entry_points_validate_and_need_a_device():
     """fe2_hrom_gather / fe2_nccl_comm_init: argument checks
     with the reference taxonomy; no communicator without a CUDA device."""
-    flag = np.zeros(1, dtype=np.int32)
-    rc = F.lib.fe2_hrom_gather(None, None, None, None, None, None, None, flag.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+    flag = np.zeros(2, dtype=np.int32)
+    rc = F.lib.fe2_hrom_gather(None, None, None, None, None, None, 0.0, None,
+                               flag.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
     assert rc == 1  # ErrorCode::config ("no points allocated")
+    rc = F.lib.fe2_hrom_gather_layout(None, None, None, None)
+    assert rc == 1
     out = ctypes.c_void_p()
     rc = F.lib.fe2_nccl_comm_init(0, 2, 5, ctypes.create_string_buffer(128), ctypes.byref(out))
     assert rc == 1  # rank out of range -> config
