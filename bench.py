@@ -10,6 +10,15 @@ over ranks: every rank owns P points (global ids rank*P..), and after every
 increment the macro stress, condensed tangent, residual norms and status are
 all-gathered over NCCL (the monolithic scheme's exchange).
 
+  monolithic : the paper's scheme on the same workload — one condensed reduced
+           Newton iteration of every point per macro iteration, the NCCL
+           exchange after EVERY iteration, lockstep termination (also at N = 1,
+           one-rank communicator).
+  extra_configs : config 2 (finite strain) and config 3 (1,048,576 points,
+           n = 64, K = 2,000, split over the ranks: strong scaling) with their
+           own rooflines; config 3 also runs the monolithic scheme with the
+           per-iteration exchange (the north_star scaling run).
+
   value  : device-resident inputs (all increments' E already in HBM),
            CUDA events on the engine's stream, max over ranks.
   e2e    : the host-buffer C-ABI call fe2_hrom_solve_increment per increment
@@ -51,17 +60,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--mono-iters", type=int, default=3,
-                    help="monolithic-scheme iterations per increment timed after e2e (0 = skip)")
+    ap.add_argument("--no-mono", dest="mono", action="store_false",
+                    help="skip the monolithic-scheme runs (per-iteration exchange, lockstep termination)")
     ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
     ap.add_argument("--points", type=int, default=0, help="override points per rank (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-points", type=int, default=0)
     ap.add_argument("--constitutive-points", type=int, default=1 << 25,
                     help="material points of the SoA constitutive-update roofline run (0 = skip)")
-    ap.add_argument("--extra-configs", default="2",
-                    help="comma-separated configs also timed device-resident (1 warm-up + 1 step) into "
-                         "extra_configs of the line; '' to skip")
+    ap.add_argument("--extra-configs", default="2,3",
+                    help="comma-separated configs also timed device-resident (2-increment warm-up + 1 step) "
+                         "into extra_configs of the line; config 3 adds its monolithic run; '' to skip")
     return ap.parse_args()
 
 
@@ -236,6 +245,7 @@ class DeviceRun:
         self.d_pc = torch.empty(P, dtype=i32, device=dev)
         self.d_st = torch.empty(P, dtype=i32, device=dev)
         self.width = self.nc + self.nt + 2
+        self.steps_timed = 1
         self.pack = torch.empty((P, self.width), dtype=f64, device=dev)
         self.gathered = None
 
@@ -246,15 +256,51 @@ class DeviceRun:
         in-place ncclAllGather, max all-reduce of the failure flag)."""
         if ws == 1:
             return
-        if self.gathered is None:
-            self.gathered = self.torch.empty((ws,) + tuple(self.pack.shape), dtype=self.pack.dtype,
-                                             device=self.dev)
+        self.ensure_gather_buffer()
         self.any_failed = self.eng.gather(COMM[0], self.gathered.data_ptr(), sig.data_ptr(), C.data_ptr(),
                                           res.data_ptr(), st.data_ptr())
 
-    def device_step(self, dist, ws):
+    def ensure_gather_buffer(self):
+        """[world][P_max][width] device buffer of the exchange (fe2_hrom_gather_layout:
+        ranks may hold different point counts; their blocks are padded to P_max)."""
+        if self.gathered is None:
+            p_max, self.counts = self.eng.gather_layout(COMM[0])
+            self.gathered = self.torch.empty((COMM[0].nranks, p_max, self.width), dtype=self.pack.dtype,
+                                             device=self.dev)
+
+    def mono_step(self, tol=1e-8, max_iter=30):
+        """The monolithic scheme with the exchange after EVERY Newton iteration (SURVEY
+        §8(e), BASELINE config 3): per load increment, fe2_hrom_mono_begin, then
+        fe2_hrom_mono_iterate_device (one condensed reduced-Newton iteration of every point,
+        device-resident E) followed by fe2_hrom_gather of {Σ, C_macro, ‖r‖, status} of all
+        points over NCCL with the max all-reduce of "some point failed" / "some point above
+        tol" — lockstep termination when no point on any rank is above tol — then
+        fe2_hrom_mono_commit. Returns the number of iterations of each increment."""
         self.eng.reset_points()
+        self.ensure_gather_buffer()
+        its = []
         for k in range(self.cfg["incr"]):
+            self.eng.mono_begin()
+            for it in range(1, max_iter + 1):
+                self.eng.mono_iterate_device(self.dE[k].data_ptr(), self.d_sig.data_ptr(), self.d_C.data_ptr(),
+                                             self.d_res.data_ptr(), self.d_pc.data_ptr(), self.d_st.data_ptr(),
+                                             self.stream.cuda_stream)
+                failed, above = self.eng.gather(COMM[0], self.gathered.data_ptr(), self.d_sig.data_ptr(),
+                                                self.d_C.data_ptr(), self.d_res.data_ptr(), self.d_st.data_ptr(),
+                                                res_tol=tol, flags=True)
+                if failed:
+                    raise SystemExit(f"bench: monolithic iteration failed ({self.cfg['name']}, increment {k})")
+                if not above:
+                    break
+            else:
+                raise SystemExit(f"bench: monolithic iteration not converged in {max_iter} ({self.cfg['name']})")
+            its.append(it)
+            self.eng.mono_commit()
+        return its
+
+    def device_step(self, dist, ws, n_incr=None):
+        self.eng.reset_points()
+        for k in range(self.cfg["incr"] if n_incr is None else n_incr):
             self.eng.solve_increment_device(self.dE[k].data_ptr(), self.d_sig.data_ptr(), self.d_C.data_ptr(),
                                             self.d_it.data_ptr(), self.d_pc.data_ptr(), self.d_res.data_ptr(),
                                             self.d_st.data_ptr(), self.stream.cuda_stream)
@@ -266,33 +312,87 @@ class DeviceRun:
             raise SystemExit(f"bench: {int((st != 0).sum())} points of {self.cfg['name']} failed to converge")
 
     def roofline(self, stats, ms, peak, peak_src):
+        """F_asm = 3 K n (n+9) per point-assembly with K = the cubature points
+        the kernel actually contracts. The increment kernels contract only the plastic J2
+        points (elastic-predictor split), so `achieved` counts
+        timed_plastic_evals x 3 n (n+9); the count as if every J2 point were contracted is
+        kept under `algorithmic_equiv` (not a roofline claim). Config 2 contracts every
+        cubature point: 8 K n (n+5)."""
         cfg, model = self.cfg, self.model
         n, K_j2 = cfg["n"], model.K_j2
         kms = stats["kernel_ms"]
-        F_asm = flops_per_assembly(n, K_j2, cfg["K"], self.finite)
-        achieved = stats["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12 if kms else None
         nt = (n + 7) // 8
+        equiv = None
         if self.finite:  # every cubature point: NT^2 + NT DMMA.8x8x4 (512 flop) per point-assembly
+            F_asm = flops_per_assembly(n, K_j2, cfg["K"], True)
+            flops = stats["timed_assemblies"] * F_asm
             executed = stats["timed_assemblies"] * cfg["K"] * (nt * nt + nt) * 512
             kernel = "k_increment_fs (persistent: Biot update + DMMA k-step per cubature point + warp LU/Newton/condensation + commit)"
-            definition = "SURVEY §8(d) config 2: F_asm = 8 K n (n+5) per point-assembly (all cubature points; full K_aa, K_aF, r)"
-        else:  # every plastic point = 3 k-entries = 0.75 k-steps of NTP DMMA.8x8x4
+            definition = "SURVEY §8(d) config 2: F_asm = 8 K n (n+5) per point-assembly (all cubature points contracted)"
+        else:  # every plastic point = 3 k-entries = 0.75 k-steps of NT(NT+1)/2 DMMA.8x8x4
+            flops = stats["timed_plastic_evals"] * 3.0 * n * (n + 9)
             executed = stats["timed_plastic_evals"] * 0.75 * (nt * (nt + 1) // 2) * 512
             kernel = ("k_increment (persistent: DMMA hyper-assembly + warp Cholesky/Newton/condensation + commit)"
                       if n <= 32 else
                       "k_increment_big (persistent, CTA per point: staged-B DMMA hyper-assembly + CTA Cholesky/"
                       "Newton/condensation)")
-            definition = "SURVEY §8(d) F_asm = 3 K_J2 n (n+9) per point-assembly (elastic block precomputed)"
+            definition = ("SURVEY §8(d) F_asm = 3 K n (n+9) per point-assembly, K = the plastic J2 points the "
+                          "kernel contracts (elastic points enter through the precomputed elastic block)")
+            F_asm = 3.0 * K_j2 * n * (n + 9)
+            if kms:
+                eq = stats["timed_assemblies"] * F_asm / (kms / 1e3) / 1e12
+                equiv = {"achieved": eq, "frac": eq / peak, "flops_per_point_assembly": F_asm,
+                         "note": "3 K_J2 n (n+9): as if every J2 point were contracted; the elastic-predictor "
+                                 "split does that work once per model, so this is throughput-equivalent only"}
+        achieved = flops / (kms / 1e3) / 1e12 if kms else None
         launches_t = max(1, stats["timed_launches"])
         return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "kernel": kernel, "peak_source": peak_src,
-                "flops_per_point_assembly": F_asm, "flops_definition": definition,
+                "flops_definition": definition, "flops_per_step": flops / max(1, self.steps_timed),
+                "contracted_points_per_assembly": (stats["timed_plastic_evals"] / max(1, stats["timed_assemblies"])
+                                                   if not self.finite else cfg["K"]),
                 "executed_dmma_tflops": executed / (kms / 1e3) / 1e12 if kms else None,
+                "algorithmic_equiv": equiv,
                 "avg_launch_ms": kms / launches_t, "share_of_step": kms / ms if ms else None}
+
+    def roofline_hbm(self, stats, hbm, hbm_src):
+        """DRAM traffic of the increment kernel: per launch every point reads its committed
+        history (eps_p[4], eq: 40 B per J2 point) and writes its candidate (40 B) once; the
+        repeated assembly passes of the Newton loop hit L2 (ncu: DRAM bytes per launch =
+        1.02 x this, profiles/). achieved = that / the average launch time."""
+        kms = stats["kernel_ms"]
+        per_launch = self.P * self.model.K_j2 * 80.0
+        gbs = per_launch * stats["timed_launches"] / (kms / 1e3) / 1e9 if kms else None
+        return {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                "frac": gbs / hbm if gbs else None, "peak_source": hbm_src,
+                "kernel": "history stream of the increment kernel (eps_p[4], eq SoA, double-buffered)",
+                "bytes_definition": "80 B per J2 cubature point per point per increment launch "
+                                    "(40 B committed read + 40 B candidate write)",
+                "bytes_per_launch": per_launch}
+
+
+def mono_record(run, ms, its, st, P_total, peak, peak_src):
+    """JSON record of a monolithic-scheme run (DeviceRun.mono_step)."""
+    n_inc = len(its)
+    pit = P_total * sum(its)
+    rf = run.roofline(st, ms, peak, peak_src)
+    rf["kernel"] = ("k_increment<..., MONO>" if run.cfg["n"] <= 32 else "k_increment_big<NT, MONO>") + \
+        " (one condensed reduced-Newton iteration per launch)"
+    return {"value": P_total * n_inc / (ms / 1e3), "unit": UNIT,
+            "point_iterations_per_s": pit / (ms / 1e3), "iterations_per_increment": its,
+            "ms_per_step": ms, "tol": 1e-8,
+            "api": "per iteration: fe2_hrom_mono_iterate_device + fe2_hrom_gather (NCCL all-gather of "
+                   "{Σ, C_macro, ‖r‖, status} + max all-reduce of failed / above-tol; lockstep termination); "
+                   "fe2_hrom_mono_begin / _commit per increment",
+            "exchanges": sum(its), "roofline": rf,
+            "note": "evals/s = converged increments (all points below tol) per second, the unit of `value`"}
 
 
 def main():
     args = parse()
+    # the JSON line must be the only stdout line: keep NCCL's version banner off stdout
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     cfg = dict(CONFIGS[args.config])
     if args.points:
         cfg["P"] = args.points
@@ -343,6 +443,14 @@ def main():
     except Exception:
         peak, peak_src = 37.0, "fallback: DMMA peak estimate"
 
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        hbm_src = "MEASURED_PEAKS.json"
+    except Exception:
+        hbm, hbm_src = 6650.0, "fallback 6.65 TB/s"
+    if COMM[0] is None and args.mono:  # one-rank communicator: the N = 1 exchange runs the same path
+        COMM[0] = F.NcclComm(local, 1, 0, F.nccl_unique_id())
+
     run = DeviceRun(F, torch, cfg, rank, local, dev, stream, ws)
     eng, model, P, incr = run.eng, run.model, run.P, cfg["incr"]
     nc, nt = run.nc, run.nt
@@ -357,6 +465,7 @@ def main():
         ms = timed(lambda: run.device_step(dist, ws), args.steps)
     stats = eng.stats()
     eng.set_timing(False)
+    run.steps_timed = args.steps
     launches = stats["kernel_launches"] - launches0
     P_total = cfg["P"] if cfg.get("strong") else ws * P
     evals = P_total * incr * args.steps
@@ -394,36 +503,22 @@ def main():
     h2d = incr * P * nc * 8
     d2h = incr * P * (nc * 8 + nt * 8 + 8 + 3 * 4)
 
-    # ---- the monolithic scheme (the paper's method): every macro iteration advances
-    # each micro problem by ONE reduced Newton iteration, returns the condensed Σ
-    # and C_macro, and (N > 1) all-gathers them — SURVEY §8(e) config 3's "gathered
-    # each Newton iteration". Host-buffer C-ABI calls (fe2_hrom_mono_iterate), a
-    # fixed number of iterations per load increment, then fe2_hrom_mono_commit.
+    # ---- the monolithic scheme (the paper's method) on the same workload: every macro
+    # iteration advances each micro problem by ONE reduced Newton iteration and returns the
+    # condensed Σ and C_macro; after EVERY iteration the records of all points are
+    # all-gathered over NCCL (fe2_hrom_gather, also at N = 1 with a one-rank communicator)
+    # and the ranks stop together when no point is above the tolerance.
     mono = None
-    if args.mono_iters > 0 and not run.finite:
-        if ws > 1 and not e2e_bufs:
-            p_sig, p_C, p_it, p_pc, p_res, p_st = eng.output_ptrs()
-            e2e_bufs.extend([wrap_dev(p_sig, (P, nc), "<f8", dev), wrap_dev(p_C, (P, nt), "<f8", dev),
-                             wrap_dev(p_res, (P,), "<f8", dev), wrap_dev(p_st, (P,), "<i4", dev)])
-
-        def mono_step():
-            eng.reset_points()
-            for k in range(incr):
-                eng.mono_begin()
-                for _ in range(args.mono_iters):
-                    eng.mono_iterate(run.E_inc[k])
-                    if ws > 1:
-                        run.gather(dist, ws, *e2e_bufs)
-                eng.mono_commit()
-
-        mono_step()
-        ms_mono = timed(mono_step, 1)
-        mono = {"value": P_total * incr * args.mono_iters / (ms_mono / 1e3), "unit": "point-iterations/s",
-                "iterations_per_increment": args.mono_iters, "ms_per_step": ms_mono,
-                "api": "fe2_hrom_mono_iterate (host buffers) per macro iteration"
-                       + (" + fe2_hrom_gather (NCCL)" if ws > 1 else "") + ", fe2_hrom_mono_commit per increment",
-                "note": "one condensed micro Newton iteration per point per macro iteration (the monolithic scheme); "
-                        "not the converged-increment unit of `value`"}
+    if args.mono and not run.finite:
+        run.mono_step()
+        run.eng.reset_stats()
+        run.eng.set_timing(True)
+        its_box = [None]
+        ms_mono = timed(lambda: its_box.__setitem__(0, run.mono_step()), 1)
+        mst = run.eng.stats()
+        run.eng.set_timing(False)
+        its = its_box[0]
+        mono = mono_record(run, ms_mono, its, mst, P_total, peak, peak_src)
 
     # ---- the batched constitutive update on SoA HBM buffers (north_star item 1):
     # the HBM-bound kernel, timed alone on device-resident inputs: strains U[±0.03]
@@ -471,33 +566,48 @@ def main():
                         "plastic_fraction": float(c_pl.float().mean().item())}
         del c_eps, c_h, c_sig, c_C6, c_pl
 
-    # ---- other BASELINE configs, device-resident (weak scaling, same rank layout)
+    # ---- other BASELINE configs, device-resident (same rank layout: weak for configs 1/2,
+    # strong for config 3, whose points are split over the ranks)
     extras = {}
     for c in [int(x) for x in args.extra_configs.split(",") if x.strip()]:
         if c == args.config or c not in CONFIGS:
             continue
         xcfg = dict(CONFIGS[c])
         xrun = DeviceRun(F, torch, xcfg, rank, local, dev, stream, ws)
-        xrun.device_step(dist, ws)
-        xrun.check_converged()
+        xrun.device_step(dist, ws, n_incr=2)  # warm-up: the first increments (kernels, allocations)
         xrun.eng.reset_stats()
         xrun.eng.set_timing(True)
         xms = timed(lambda: xrun.device_step(dist, ws), 1)
+        xrun.check_converged()
         xst = xrun.eng.stats()
-        xev = ws * xcfg["P"] * xcfg["incr"]
-        extras[xcfg["name"]] = {
-            "value": xev / (xms / 1e3), "unit": UNIT, "steps": 1, "warmup": 1, "ms_per_step": xms,
-            "points_per_rank": xcfg["P"], "modes": xcfg["n"], "cubature": xcfg["K"], "increments": xcfg["incr"],
+        xrun.eng.set_timing(False)
+        xP_total = xcfg["P"] if xcfg.get("strong") else ws * xcfg["P"]
+        xev = xP_total * xcfg["incr"]
+        rec = {
+            "value": xev / (xms / 1e3), "unit": UNIT, "steps": 1, "warmup": "2 increments", "ms_per_step": xms,
+            "points_total": xP_total, "points_per_rank": xrun.P, "modes": xcfg["n"], "cubature": xcfg["K"],
+            "cubature_j2": xrun.model.K_j2, "increments": xcfg["incr"],
+            "scaling": "strong" if xcfg.get("strong") else "weak",
             "roofline": xrun.roofline(xst, xms, peak, peak_src),
-            "newton": {"assemblies_per_eval": xst["timed_assemblies"] / (xev / ws)},
+            "newton": {"assemblies_per_eval": xst["timed_assemblies"] / (xrun.P * xcfg["incr"])},
             "parity": "unpinned (no reference finite-strain code; oracle fs_* checked by tests/test_gpu_fs.py)"
-            if xrun.finite else "pinned"}
+            if xrun.finite else "oracle parity tests/test_gpu_full_configs.py"}
+        if not xrun.finite:
+            rec["roofline_hbm"] = xrun.roofline_hbm(xst, hbm, hbm_src)
+        if c == 3 and args.mono:  # the north_star multi-GPU scheme: exchange every Newton iteration
+            xrun.eng.reset_stats()
+            xrun.eng.set_timing(True)
+            its_box = [None]
+            mms = timed(lambda: its_box.__setitem__(0, xrun.mono_step()), 1)
+            mst = xrun.eng.stats()
+            xrun.eng.set_timing(False)
+            rec["monolithic"] = mono_record(xrun, mms, its_box[0], mst, xP_total, peak, peak_src)
+        extras[xcfg["name"]] = rec
         del xrun
 
     if rank != 0:
-        if ws > 1:
-            COMM[0].close()
-            dist.destroy_process_group()
+        COMM[0].close()
+        dist.destroy_process_group()
         return
 
     # ---- roofline of the dominant kernel (one persistent launch per increment)
@@ -515,22 +625,13 @@ def main():
             constitutive["traffic"] = json.load(open(prof)).get("constitutive_soa", {}).get("dram_bytes_per_launch")
         except Exception:
             pass
-    kms = stats["kernel_ms"]
     K_j2 = model.K_j2
-    try:
-        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-        hbm_src = "MEASURED_PEAKS.json"
-    except Exception:
-        hbm, hbm_src = 6650.0, "fallback 6.65 TB/s"
-    # history stream of the same kernel (double-buffered history, no commit pass):
-    # every assembly pass reads 40 B and writes its 40-B candidate per J2 point
-    hbm_bytes = stats["timed_assemblies"] * K_j2 * 80
-    bytes_def = "40 B read + 40 B candidate written per J2 point per assembly pass (no commit pass)"
-    gbs = hbm_bytes / (kms / 1e3) / 1e9 if kms else None
-    roofline_hbm = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
-                    "frac": gbs / hbm if gbs else None, "peak_source": hbm_src,
-                    "kernel": "history stream of the increment kernel (eps_p[4], eq SoA)",
-                    "bytes_definition": bytes_def, "bytes_per_step": hbm_bytes / args.steps}
+    roofline_hbm = run.roofline_hbm(stats, hbm, hbm_src)
+    if os.path.exists(prof):
+        try:
+            roofline_hbm["traffic"] = json.load(open(prof)).get(cfg["name"], {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
@@ -566,8 +667,9 @@ def main():
         "monolithic": mono,
     }
     print(json.dumps(line), flush=True)
-    if ws > 1:
+    if COMM[0] is not None:
         COMM[0].close()
+    if ws > 1:
         dist.destroy_process_group()
 
 

@@ -162,32 +162,42 @@ int fe2_hrom_solve_increment_device(fe2_hrom_t h, const double* d_E, const fe2_n
                                     double* d_res_norm, int* d_status, void* stream);
 
 /* ---- multi-GPU exchange of the monolithic scheme ----
- * Points are sharded in contiguous equal blocks over the ranks of one box,
- * one handle per device; the engines never communicate during assembly,
+ * Points are sharded in contiguous blocks over the ranks of one box, one
+ * handle per device; the engines never communicate during assembly,
  * factorisation or condensation. After an increment (or monolithic macro
  * iteration) every rank needs every point's condensed response, so the only
  * collective is an NCCL all-gather of per-point records over NVLink, plus a
- * max all-reduce of "some point failed" for lockstep termination.
+ * max all-reduce of two flags for lockstep termination.
  * libnccl.so.2 is dlopen'ed at first use (no link-time dependency).
  *   fe2_nccl_get_unique_id: rank 0 creates the 128-byte id, the caller
  *     broadcasts it (MPI, torch.distributed, a file ...);
  *   fe2_nccl_comm_init / _destroy: one communicator per rank and device.
- * fe2_hrom_gather packs this rank's P_local records
+ *   fe2_hrom_gather_layout: every rank's point count P_r over comm (one
+ *     all-gather of an int64, host-synchronising; the handle caches it, and
+ *     fe2_hrom_gather computes it on first use). The gathered buffer holds
+ *     world blocks of P_max = max_r P_r rows; rank r's points are rows
+ *     [r*P_max, r*P_max + P_r) and the rest of its block is padding
+ *     (status -1, NaN values). counts[world] is nullable.
+ * fe2_hrom_gather packs this rank's records
  *   {Σ (nc) | C_macro (nt) | ‖r‖ | status} — nc, nt = 3, 9 small strain
  *   (14 doubles per point), 4, 16 finite strain (P_M, A_M) —
- * from the given device outputs of the last increment (NULL = the handle's
- * own buffers, fe2_hrom_output_ptrs) into d_all[rank], all-gathers in place
- * into d_all [world][P_local][nc + nt + 2] (device, doubles; P_local must be
- * equal on every rank) and writes the all-reduced failure flag to
- * *any_failed (host). Ordered on the handle's stream, which it synchronises.
+ * from the given device outputs of the last increment / monolithic iterate
+ * (NULL = the handle's own buffers, fe2_hrom_output_ptrs) into its block of
+ * d_all, all-gathers in place into d_all [world][P_max][nc + nt + 2]
+ * (device, doubles) and max-reduces flags[0] = "some point failed"
+ * (status > 0) and flags[1] = "some point has ‖r‖ > res_tol" (the
+ * monolithic iteration's termination test; pass +inf to ignore). With
+ * flags != NULL (host int[2]) the call synchronises the handle's stream and
+ * returns the flags; with NULL it stays asynchronous on the stream.
  * Replaces nothing in the reference (its RVE solves run in one process,
  * SPEC.md:247, :511); the records are what fe2.macro_step consumes
  * (SPEC.md:474-481). Errors: ErrorCode::rank for NCCL failures. */
 int fe2_nccl_get_unique_id(void* id128);
 int fe2_nccl_comm_init(int device, int nranks, int rank, const void* id128, void** comm);
 int fe2_nccl_comm_destroy(void* comm);
+int fe2_hrom_gather_layout(fe2_hrom_t h, void* comm, int64_t* P_max, int64_t* counts);
 int fe2_hrom_gather(fe2_hrom_t h, void* comm, const double* d_sigma, const double* d_C, const double* d_res_norm,
-                    const int* d_status, double* d_all, int* any_failed);
+                    const int* d_status, double res_tol, double* d_all, int* flags);
 
 /* Committed state readback (host): alpha[P*n], state[P*K*6] in the caller's
  * cubature order (elastic-material points report eps_p = 0, eq = 0 and the
@@ -285,6 +295,10 @@ int fe2_macro_run_hf(const fe2_macro_config_t* cfg, fe2_hf_t hf, double* rows, i
 int fe2_hrom_mono_begin(fe2_hrom_t h);
 int fe2_hrom_mono_iterate(fe2_hrom_t h, const double* E, double* sigma, double* C, double* rel_res,
                           int* plastic_count, int* status);
+/* The same on device buffers (E[P*3] in HBM; NULL outputs = the handle's own,
+ * fe2_hrom_output_ptrs), asynchronous on `stream` (NULL = the handle's). */
+int fe2_hrom_mono_iterate_device(fe2_hrom_t h, const double* d_E, double* d_sigma, double* d_C, double* d_rel_res,
+                                 int* d_plastic_count, int* d_status, void* stream);
 int fe2_hrom_mono_commit(fe2_hrom_t h);
 
 /* ---- Empirical Cubature Method (SPEC.md:333-369

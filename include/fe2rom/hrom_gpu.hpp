@@ -22,6 +22,7 @@
 #include <stdexcept>
 #include <string>
 #include <variant>
+#include <cmath>
 #include <vector>
 
 #include "fe2rom/fe2rom_gpu.h"
@@ -220,14 +221,23 @@ class HyperRomBatch {
 
   fe2_hrom_t handle() const { return h_; }
 
-  // Multi-GPU exchange (one batch per rank and device, equal P per rank):
+  // Multi-GPU exchange (one batch per rank and device, any P per rank):
   // all-gather every rank's {Σ (3) | C_macro (9) | ‖r‖ | status} records of
-  // the last increment into the device buffer d_all [world][P][14]; returns
-  // true if a point failed on any rank. See fe2_hrom_gather.
+  // the last increment into the device buffer d_all [world][P_max][14]
+  // (P_max from gather_layout; padding rows have status -1); returns true if
+  // a point failed on any rank. See fe2_hrom_gather.
   bool gather(void* nccl_comm, double* d_all) {
-    int failed = 0;
-    check(fe2_hrom_gather(h_, nccl_comm, nullptr, nullptr, nullptr, nullptr, d_all, &failed));
-    return failed != 0;
+    int flags[2] = {0, 0};
+    check(fe2_hrom_gather(h_, nccl_comm, nullptr, nullptr, nullptr, nullptr, HUGE_VAL, d_all, flags));
+    return flags[0] != 0;
+  }
+  // Rows per rank block of the gathered buffer (max point count over the ranks).
+  int64_t gather_layout(void* nccl_comm, std::vector<int64_t>* counts = nullptr) {
+    int64_t p_max = 0;
+    std::vector<int64_t> c(64);
+    check(fe2_hrom_gather_layout(h_, nccl_comm, &p_max, c.data()));
+    if (counts) *counts = c;
+    return p_max;
   }
 
  private:

@@ -26,6 +26,13 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(src, obj, defines):
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", "-I", os.path.join(ROOT, "include"),
+           "-I", CSRC, "-o", obj, os.path.join(CSRC, src)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return src, r.returncode, r.stdout + r.stderr
+
+
 def build_native(force=False, verbose=False, out=None, defines=()):
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "fe2rom", "fe2rom_gpu.h"))
@@ -34,16 +41,26 @@ def build_native(force=False, verbose=False, out=None, defines=()):
     if not force and not _stale(target, deps):
         return target
     os.makedirs(os.path.dirname(target), exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-I", os.path.join(ROOT, "include"),
-           "-I", CSRC, "-o", target + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit, in parallel, then one link
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = target + ".obj"
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, s + ".o") for s in SOURCES]
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(lambda so: _compile(so[0], so[1], defines), zip(SOURCES, objs)))
+    log = "".join(f"==== {src}\n{txt}" for src, _, txt in results)
+    failed = [src for src, rc, _ in results if rc != 0]
+    if failed:
+        sys.stderr.write(log)
+        raise RuntimeError(f"nvcc build of libfe2rom_gpu.so failed ({', '.join(failed)})")
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", target + ".tmp", *objs, "-ldl"], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc build of libfe2rom_gpu.so failed")
+        raise RuntimeError("link of libfe2rom_gpu.so failed")
     with open(target + ".ptxas.log", "w") as f:
-        f.write(r.stdout + r.stderr)
+        f.write(log)
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write(log)
     os.replace(target + ".tmp", target)
     return target
 

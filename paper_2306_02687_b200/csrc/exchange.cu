@@ -1,11 +1,12 @@
 // Multi-GPU exchange of the monolithic scheme: macro points
-// are sharded in contiguous equal blocks over the ranks of one box, one engine
+// are sharded in contiguous blocks over the ranks of one box (any sizes: blocks are
+// padded to the largest rank's count in the gathered buffer), one engine
 // handle per device, and after every increment / macro iteration each rank
 // needs every point's condensed response. The per-point records
 // {Σ (nc) | C (nt) | ‖r‖ | status} are packed on the device straight into
 // this rank's block of the receive buffer and all-gathered in place over NCCL
-// (NVLink / NVSwitch); a max all-reduce of the local "some point failed" flag
-// gives the lockstep termination test. This is the only collective on the
+// (NVLink / NVSwitch); a max all-reduce of the local "some point failed" and "some
+// point above the residual tolerance" flags gives the lockstep termination test. This is the only collective on the
 // path: assembly, factorisation and condensation never communicate.
 //
 // libnccl.so.2 is dlopen'ed at first use (the process's NCCL — torch's bundled
@@ -17,8 +18,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
+#include <vector>
 #include <type_traits>
 
 #include "common.hpp"
@@ -76,28 +79,34 @@ void nccl_check(ncclResult_t r, const char* what) {
     throw Failure(Code::rank, std::string("NCCL ") + what + " failed: " + Nccl::get().error_string(r));
 }
 
-// One thread per (point, record field): record p = [sigma(nc) | C(nt) | res | status]
-// at out[p * R]; flag |= (status != 0).
-__global__ void k_pack_records(int64_t P, int nc, int nt, const double* __restrict__ sigma,
+// One thread per (row, record field) of this rank's padded block of P_max rows:
+// record p = [sigma(nc) | C(nt) | res | status] at out[p * R]; rows p >= P are padding
+// (NaN, status -1). flags[0] |= (status > 0): a failed point; flags[1] |= (res > res_tol):
+// a point not yet converged (the monolithic iteration's lockstep termination test).
+__global__ void k_pack_records(int64_t P, int64_t P_max, int nc, int nt, const double* __restrict__ sigma,
                                const double* __restrict__ C, const double* __restrict__ res,
-                               const int* __restrict__ status, double* __restrict__ out, int* __restrict__ flag) {
+                               const int* __restrict__ status, double res_tol, double* __restrict__ out,
+                               int* __restrict__ flags) {
   const int R = nc + nt + 2;
-  const int64_t total = P * R;
+  const int64_t total = P_max * R;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t p = e / R;
     const int f = static_cast<int>(e - p * R);
     double v;
-    if (f < nc) {
+    if (p >= P) {
+      v = f == nc + nt + 1 ? -1.0 : __longlong_as_double(0x7ff8000000000000LL);
+    } else if (f < nc) {
       v = sigma[p * nc + f];
     } else if (f < nc + nt) {
       v = C[p * nt + (f - nc)];
     } else if (f == nc + nt) {
       v = res[p];
+      if (!(v <= res_tol)) atomicOr(flags + 1, 1);
     } else {
       const int s = status[p];
       v = static_cast<double>(s);
-      if (s != 0) atomicOr(flag, 1);
+      if (s > 0) atomicOr(flags, 1);
     }
     out[e] = v;
   }
@@ -105,38 +114,67 @@ __global__ void k_pack_records(int64_t P, int nc, int nt, const double* __restri
 
 }  // namespace
 
-// Pack this rank's records into d_all[rank block], all-gather in place, and
-// max-reduce the failure flag (host result; synchronises `stream`).
-void exchange_records(int device, cudaStream_t stream, void* comm_v, int64_t P, int nc, int nt, const double* d_sigma,
-                      const double* d_C, const double* d_res, const int* d_status, double* d_all, int* any_failed) {
+// Block layout of the exchange: every rank's P_local (one in-place ncclAllGather of an
+// int64 per rank; host-synchronising, done once per communicator by the caller).
+void exchange_layout(int device, cudaStream_t stream, void* comm_v, int64_t P, int64_t* scratch,
+                     ExchangeLayout* out) {
   const Nccl& N = Nccl::get();
   auto comm = static_cast<ncclComm_t>(comm_v);
   check(comm != nullptr, Code::config, "null NCCL communicator");
-  check(d_sigma && d_C && d_res && d_status && d_all, Code::config, "null device buffer");
   int world = 0, rank = 0;
   nccl_check(N.comm_count(comm, &world), "ncclCommCount");
   nccl_check(N.comm_user_rank(comm, &rank), "ncclCommUserRank");
+  check(world <= kMaxRanks, Code::rank, "too many ranks for the exchange layout");
+  CK(cudaSetDevice(device));
+  int64_t* d = scratch;  // kMaxRanks int64 of device scratch owned by the handle
+  CK(cudaMemcpyAsync(d + rank, &P, sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+  nccl_check(N.all_gather(d + rank, d, 1, ncclInt64, comm, stream), "ncclAllGather(P_local)");
+  std::vector<int64_t> counts(world);
+  CK(cudaMemcpyAsync(counts.data(), d, world * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  out->comm = comm_v;
+  out->world = world;
+  out->rank = rank;
+  out->P_local = P;
+  out->P_max = 0;
+  out->P_total = 0;
+  for (int r = 0; r < world; ++r) {
+    check(counts[r] >= 0, Code::rank, "bad point count from a rank");
+    out->P_max = std::max(out->P_max, counts[r]);
+    out->P_total += counts[r];
+    out->counts[r] = counts[r];
+  }
+}
+
+// Pack this rank's records into d_all[rank * P_max * R ...] (padding rows beyond P_local),
+// all-gather in place, max-reduce the two flags; with flags_host the flags are copied
+// (pinned h_flags) and the stream synchronised, otherwise everything stays asynchronous.
+void exchange_records(int device, cudaStream_t stream, const ExchangeLayout& L, int nc, int nt,
+                      const double* d_sigma, const double* d_C, const double* d_res, const int* d_status,
+                      double res_tol, double* d_all, int* d_flags, int* h_flags, int* flags_host) {
+  const Nccl& N = Nccl::get();
+  auto comm = static_cast<ncclComm_t>(L.comm);
+  check(d_sigma && d_C && d_res && d_status && d_all, Code::config, "null device buffer");
   CK(cudaSetDevice(device));
   const int R = nc + nt + 2;
-  const size_t count = static_cast<size_t>(P) * R;
-  double* mine = d_all + static_cast<size_t>(rank) * count;
-  int* flag = nullptr;
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), stream));
-  CK(cudaMemsetAsync(flag, 0, sizeof(int), stream));
-  if (P > 0) {
+  const size_t count = static_cast<size_t>(L.P_max) * R;
+  double* mine = d_all + static_cast<size_t>(L.rank) * count;
+  CK(cudaMemsetAsync(d_flags, 0, 2 * sizeof(int), stream));
+  if (count > 0) {
     const int64_t blocks = (static_cast<int64_t>(count) + 255) / 256;
     k_pack_records<<<static_cast<unsigned>(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, stream>>>(
-        P, nc, nt, d_sigma, d_C, d_res, d_status, mine, flag);
+        L.P_local, L.P_max, nc, nt, d_sigma, d_C, d_res, d_status, res_tol, mine, d_flags);
     CK(cudaGetLastError());
   }
   // in place: sendbuff = recvbuff + rank * sendcount
   nccl_check(N.all_gather(mine, d_all, count, ncclFloat64, comm, stream), "ncclAllGather");
-  nccl_check(N.all_reduce(flag, flag, 1, ncclInt32, ncclMax, comm, stream), "ncclAllReduce");
-  int h = 0;
-  CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
-  CK(cudaFreeAsync(flag, stream));
-  CK(cudaStreamSynchronize(stream));
-  if (any_failed) *any_failed = h;
+  nccl_check(N.all_reduce(d_flags, d_flags, 2, ncclInt32, ncclMax, comm, stream), "ncclAllReduce");
+  if (flags_host) {
+    CK(cudaMemcpyAsync(h_flags, d_flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    flags_host[0] = h_flags[0];
+    flags_host[1] = h_flags[1];
+  }
 }
 
 }  // namespace fe2

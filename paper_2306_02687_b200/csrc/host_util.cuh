@@ -65,9 +65,20 @@ inline void require_engine_material(const MatDev& m) {
         "fe2_material_update_batch and the HF solver");
 }
 
-// exchange.cu: pack the per-point records {Σ | C | ‖r‖ | status} into this
-// rank's block of d_all, NCCL all-gather in place, max-reduce the failure flag.
-void exchange_records(int device, cudaStream_t stream, void* comm, int64_t P, int nc, int nt, const double* d_sigma,
-                      const double* d_C, const double* d_res, const int* d_status, double* d_all, int* any_failed);
+// exchange.cu: the block layout over a communicator (every rank's point count; the
+// gathered buffer holds world blocks of P_max rows), then per exchange: pack the per-point
+// records {Σ | C | ‖r‖ | status} into this rank's block of d_all (padding rows status -1),
+// NCCL all-gather in place, max-reduce {some point failed, some point above res_tol}.
+constexpr int kMaxRanks = 64;
+struct ExchangeLayout {
+  void* comm = nullptr;
+  int world = 0, rank = 0;
+  int64_t P_local = 0, P_max = 0, P_total = 0;
+  int64_t counts[kMaxRanks] = {};
+};
+void exchange_layout(int device, cudaStream_t stream, void* comm, int64_t P, int64_t* d_scratch, ExchangeLayout* out);
+void exchange_records(int device, cudaStream_t stream, const ExchangeLayout& L, int nc, int nt,
+                      const double* d_sigma, const double* d_C, const double* d_res, const int* d_status,
+                      double res_tol, double* d_all, int* d_flags, int* h_flags, int* flags_host);
 
 }  // namespace fe2

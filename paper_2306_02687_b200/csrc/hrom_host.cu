@@ -75,6 +75,12 @@ struct fe2_hrom_s {
   // staging for the host-buffer API and default outputs
   double *dE = nullptr, *o_sigma = nullptr, *o_C = nullptr, *o_res = nullptr;
   int *o_iters = nullptr, *o_status = nullptr, *o_pc = nullptr;
+  // multi-GPU exchange (fe2_hrom_gather): layout over the last communicator, device
+  // scratch for the point counts and the two reduced flags, pinned flag readback
+  ExchangeLayout xlayout{};
+  int64_t* x_scratch = nullptr;
+  int* x_flags = nullptr;
+  int* h_xflags = nullptr;
   // stats
   bool timing = false;
   fe2_hrom_stats_t stats{};
@@ -200,6 +206,9 @@ struct fe2_hrom_s {
     dfree(LeInv);
     dfree(work);
     dfree(cnt);
+    dfree(x_scratch);
+    dfree(x_flags);
+    if (h_xflags) cudaFreeHost(h_xflags);
     if (h_cnt) cudaFreeHost(h_cnt);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -594,6 +603,7 @@ int fe2_hrom_reset_points(fe2_hrom_t h) {
     check(h != nullptr && h->P > 0, Code::config, "no points allocated");
     CK(cudaSetDevice(h->device));
     h->zero_points(h->stream);
+    h->mono_first = true;  // a pending monolithic iterate belongs to the discarded state
   });
 }
 
@@ -630,45 +640,80 @@ int fe2_hrom_mono_begin(fe2_hrom_t h) {
   });
 }
 
+namespace {
+// One monolithic iteration of every point at the macro iterate d_E (device), outputs into O.
+void mono_launch(fe2_hrom_t h, const double* d_E, const Outputs& O, cudaStream_t s) {
+  check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+  check(h->kin == 0, Code::config, "the monolithic iteration needs a small-strain handle");
+  const int64_t P = h->P;
+  if (!h->mono) {
+    h->mono = dalloc<double>(static_cast<size_t>(P) * mono_stride(h->NP));
+    CK(cudaMemsetAsync(h->mono, 0, static_cast<size_t>(P) * mono_stride(h->NP) * sizeof(double), s));
+  }
+  IncArgs a{};
+  a.M = h->model();
+  a.D = h->points();
+  a.O = O;
+  a.cfg = NewtonCfg{1e-8, 1, 0};
+  a.dE = d_E;
+  a.work = h->work;
+  a.cnt = h->cnt;
+  a.mono = h->mono;
+  a.mono_first = h->mono_first ? 1 : 0;
+  CK(cudaMemsetAsync(h->work, 0, sizeof(int), s));
+  CK(cudaMemsetAsync(h->cnt, 0, sizeof(IncCounters), s));
+  if (h->timing) CK(cudaEventRecord(h->ev[0], s));
+  if (h->NP <= 32)
+    launch_increment_mono(a, h->num_sms, s);
+  else
+    check(launch_increment_big_mono(a, h->num_sms, s), Code::config, "unsupported mode count");
+  CK(cudaGetLastError());
+  if (h->timing) {  // timing builds the stats synchronously (counters + events)
+    CK(cudaEventRecord(h->ev[1], s));
+    CK(cudaMemcpyAsync(h->h_cnt, h->cnt, sizeof(IncCounters), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+    const IncCounters c = *h->h_cnt;
+    h->stats.kernel_ms += ms;
+    h->stats.timed_launches += 1;
+    h->stats.timed_assemblies += static_cast<int64_t>(c.assemblies);
+    h->stats.timed_plastic_evals += static_cast<int64_t>(c.plastic_evals);
+  }
+  h->stats.kernel_launches += 1;
+  h->mono_first = false;
+}
+}  // namespace
+
 int fe2_hrom_mono_iterate(fe2_hrom_t h, const double* E, double* sigma, double* C, double* rel_res,
                           int* plastic_count, int* status) {
   return guard([&] {
     check(h != nullptr && E != nullptr, Code::config, "bad arguments");
     check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
-    check(h->kin == 0, Code::config, "the monolithic iteration needs a small-strain handle");
     CK(cudaSetDevice(h->device));
     const int64_t P = h->P;
     cudaStream_t s = h->stream;
-    if (!h->mono) {
-      h->mono = dalloc<double>(static_cast<size_t>(P) * mono_stride(h->NP));
-      CK(cudaMemsetAsync(h->mono, 0, static_cast<size_t>(P) * mono_stride(h->NP) * sizeof(double), s));
-    }
     CK(cudaMemcpyAsync(h->dE, E, P * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
-    IncArgs a{};
-    a.M = h->model();
-    a.D = h->points();
-    a.O = Outputs{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc};
-    a.cfg = NewtonCfg{1e-8, 1, 0};
-    a.dE = h->dE;
-    a.work = h->work;
-    a.cnt = h->cnt;
-    a.mono = h->mono;
-    a.mono_first = h->mono_first ? 1 : 0;
-    CK(cudaMemsetAsync(h->work, 0, sizeof(int), s));
-    CK(cudaMemsetAsync(h->cnt, 0, sizeof(IncCounters), s));
-    if (h->NP <= 32)
-      launch_increment_mono(a, h->num_sms, s);
-    else
-      check(launch_increment_big_mono(a, h->num_sms, s), Code::config, "unsupported mode count");
-    CK(cudaGetLastError());
-    h->stats.kernel_launches += 1;
-    h->mono_first = false;
+    mono_launch(h, h->dE, Outputs{h->o_sigma, h->o_C, h->o_res, h->o_iters, h->o_status, h->o_pc}, s);
     if (sigma) CK(cudaMemcpyAsync(sigma, h->o_sigma, P * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (C) CK(cudaMemcpyAsync(C, h->o_C, P * 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (rel_res) CK(cudaMemcpyAsync(rel_res, h->o_res, P * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (plastic_count) CK(cudaMemcpyAsync(plastic_count, h->o_pc, P * sizeof(int), cudaMemcpyDeviceToHost, s));
     if (status) CK(cudaMemcpyAsync(status, h->o_status, P * sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+  });
+}
+
+int fe2_hrom_mono_iterate_device(fe2_hrom_t h, const double* d_E, double* d_sigma, double* d_C, double* d_rel_res,
+                                 int* d_plastic_count, int* d_status, void* stream) {
+  return guard([&] {
+    check(h != nullptr && d_E != nullptr, Code::config, "bad arguments");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+    mono_launch(h, d_E,
+                Outputs{d_sigma ? d_sigma : h->o_sigma, d_C ? d_C : h->o_C, d_rel_res ? d_rel_res : h->o_res,
+                        h->o_iters, d_status ? d_status : h->o_status, d_plastic_count ? d_plastic_count : h->o_pc},
+                s);
   });
 }
 
@@ -931,6 +976,7 @@ int fe2_hrom_restore(fe2_hrom_t h) {
       off += (pt.bytes + 255) / 256 * 256;
     }
     CK(cudaStreamSynchronize(h->stream));
+    h->mono_first = true;  // a pending monolithic iterate belongs to the replaced state
   });
 }
 
@@ -953,13 +999,41 @@ int fe2_hrom_reset_stats(fe2_hrom_t h) {
   });
 }
 
-int fe2_hrom_gather(fe2_hrom_t h, void* comm, const double* d_sigma, const double* d_C, const double* d_res_norm,
-                    const int* d_status, double* d_all, int* any_failed) {
+namespace {
+void ensure_layout(fe2_hrom_t h, void* comm) {
+  if (!h->x_scratch) {
+    h->x_scratch = dalloc<int64_t>(kMaxRanks);
+    h->x_flags = dalloc<int>(2);
+    CK(cudaMallocHost(&h->h_xflags, 2 * sizeof(int)));
+  }
+  if (h->xlayout.comm != comm || h->xlayout.P_local != h->P)
+    exchange_layout(h->device, h->stream, comm, h->P, h->x_scratch, &h->xlayout);
+}
+}  // namespace
+
+int fe2_hrom_gather_layout(fe2_hrom_t h, void* comm, int64_t* P_max, int64_t* counts) {
   return guard([&] {
     check(h != nullptr && h->P > 0, Code::config, "no points allocated");
-    exchange_records(h->device, h->stream, comm, h->P, h->ncomp(), h->ntan(), d_sigma ? d_sigma : h->o_sigma,
-                     d_C ? d_C : h->o_C, d_res_norm ? d_res_norm : h->o_res, d_status ? d_status : h->o_status, d_all,
-                     any_failed);
+    check(comm != nullptr, Code::config, "null NCCL communicator");
+    CK(cudaSetDevice(h->device));
+    h->xlayout.comm = nullptr;  // always re-exchange the counts here
+    ensure_layout(h, comm);
+    if (P_max) *P_max = h->xlayout.P_max;
+    if (counts)
+      for (int r = 0; r < h->xlayout.world; ++r) counts[r] = h->xlayout.counts[r];
+  });
+}
+
+int fe2_hrom_gather(fe2_hrom_t h, void* comm, const double* d_sigma, const double* d_C, const double* d_res_norm,
+                    const int* d_status, double res_tol, double* d_all, int* flags) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated");
+    check(comm != nullptr, Code::config, "null NCCL communicator");
+    CK(cudaSetDevice(h->device));
+    ensure_layout(h, comm);
+    exchange_records(h->device, h->stream, h->xlayout, h->ncomp(), h->ntan(), d_sigma ? d_sigma : h->o_sigma,
+                     d_C ? d_C : h->o_C, d_res_norm ? d_res_norm : h->o_res, d_status ? d_status : h->o_status,
+                     res_tol, d_all, h->x_flags, h->h_xflags, flags);
   });
 }
 

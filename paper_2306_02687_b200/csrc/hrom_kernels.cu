@@ -389,6 +389,27 @@ __device__ void ring_drain(const Ring& R, int seq, int lane) {
   trace(R, seq, 5);
 }
 
+// Phase timeline of lane 0 of every warp (tuning builds only: -DFE2_INC_PROF; the
+// last warp to finish prints the sums): 0 strain GEMV (incl. ring wait), 1 trial /
+// yield / candidate history / slots, 2 DMMA contraction, 3 pass tail (reductions,
+// K_aa scatter, elastic predictor), 4 factorisation, 5 rest of the Newton state
+// machine (solves, condensation, commit, work queue).
+#ifdef FE2_INC_PROF
+__device__ unsigned long long g_inc_prof[7];
+#define INC_T(k)                                              \
+  do {                                                        \
+    if (lane == 0) {                                          \
+      const long long t_ = clock64();                         \
+      prof[k] += static_cast<unsigned long long>(t_ - t_prof); \
+      t_prof = t_;                                            \
+    }                                                         \
+  } while (0)
+#else
+#define INC_T(k) \
+  do {           \
+  } while (0)
+#endif
+
 // RES: the whole projected operator G2 sits in shared memory for the kernel's
 // lifetime (loaded once by TMA): warps never wait on each other for G chunks.
 // Otherwise G2 streams through the CTA-shared ring (W warps, ST stages).
@@ -400,6 +421,10 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   constexpr int S = L::S;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef FE2_INC_PROF
+  unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
+  long long t_prof = clock64();
+#endif
   const size_t ring_bytes = RES ? static_cast<size_t>(A.M.nchunks) * L::chunk * sizeof(double) : L::ring_bytes;
   double* ring_buf = reinterpret_cast<double*>(smem_raw);
   double* wbase = reinterpret_cast<double*>(smem_raw + ring_bytes) + static_cast<size_t>(warp) * L::WS;
@@ -523,6 +548,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       hload(hcur, 0, x0, x1, x2, x3, x4);
     }
     pf_p = -1;
+    INC_T(5);
     for (int c = 0; c < nch; ++c) {
       const double h0 = x0, h1 = x1, h2 = x2, h3 = x3, h4 = x4;
       if (c + 1 < nch) {
@@ -552,6 +578,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
           f2 += x2.y * al.y;
         }
       }
+      INC_T(0);
       const Trial T = trial_state(mt, h0, h1, h2, h3, h4, E0 + (e0 + f0), E1 + (e1 + f1), E2 + (e2 + f2));
       const bool plastic = (T.f > 0.0) && (q < M.K2);
       const unsigned bal = __ballot_sync(0xffffffffu, plastic);
@@ -614,6 +641,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
         sQ[lane] = 0;
       }
       __syncwarp();
+      INC_T(1);
       // plastic contraction on DMMA: k = 3 slot + i, four k per k-step
       const int ng = np4 >> 2;
 #pragma unroll kGroupUnroll
@@ -648,6 +676,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
             }
         }
       }
+      INC_T(2);
       ring_release(R, seq, lane);
       ++seq;
     }
@@ -754,18 +783,23 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     k_linear = (np_tot == 0);
     ++n_asm;
     __syncwarp();
+    INC_T(3);
   };
 
   // Factor K_aa. With no plastic point in the assembly K_aa == K_e exactly,
   // whose factor was computed once on the host.
   auto factor = [&]() -> bool {
+    INC_T(5);
     if (k_linear) {
       for (int e = lane; e < tri_(n); e += 32) sK[e] = M.Le[e];  // packed lower, coalesced
       if (lane < n) sInv[lane] = M.LeInv[lane];
       __syncwarp();
+      INC_T(4);
       return true;
     }
-    return warp_cholesky(sK, sInv, n, lane);
+    const bool ok = warp_cholesky(sK, sInv, n, lane);
+    INC_T(4);
+    return ok;
   };
 
   // Accept the state of the last assembly pass: its candidate history (already
@@ -1140,6 +1174,22 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     if (p_next < 0) p_next = grab();
   }
   ring_drain(R, seq, lane);
+#ifdef FE2_INC_PROF
+  INC_T(5);
+  if (lane == 0) {
+    for (int k = 0; k < 6; ++k) atomicAdd(&g_inc_prof[k], prof[k]);
+    __threadfence();
+    if (atomicAdd(&g_inc_prof[6], 1ull) == static_cast<unsigned long long>(gridDim.x) * W - 1) {
+      unsigned long long s_ = 0;
+      for (int k = 0; k < 6; ++k) s_ += g_inc_prof[k];
+      printf("FE2_INC_PROF NT=%d W=%d cycles%%: gemv %.1f material %.1f dmma %.1f pass-tail %.1f factor %.1f "
+             "newton %.1f (total %llu warp-cycles)\n",
+             NT, W, 100.0 * g_inc_prof[0] / s_, 100.0 * g_inc_prof[1] / s_, 100.0 * g_inc_prof[2] / s_,
+             100.0 * g_inc_prof[3] / s_, 100.0 * g_inc_prof[4] / s_, 100.0 * g_inc_prof[5] / s_, s_);
+      for (int k = 0; k < 7; ++k) g_inc_prof[k] = 0;
+    }
+  }
+#endif
   if (A.cnt && lane == 0) {
     atomicAdd(&A.cnt->assemblies, n_asm);
     atomicAdd(&A.cnt->commits, n_com);

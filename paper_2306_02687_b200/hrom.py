@@ -102,7 +102,9 @@ def _load():
     L.fe2_nccl_get_unique_id.argtypes = [C.c_void_p]
     L.fe2_nccl_comm_init.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
     L.fe2_nccl_comm_destroy.argtypes = [C.c_void_p]
-    L.fe2_hrom_gather.argtypes = [C.c_void_p] * 7 + [_ip]
+    L.fe2_hrom_gather.argtypes = [C.c_void_p] * 6 + [C.c_double, C.c_void_p, _ip]
+    L.fe2_hrom_gather_layout.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.fe2_hrom_mono_iterate_device.argtypes = [C.c_void_p] * 8
     L.fe2_model_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.fe2_model_build_from_mesh.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]
     L.fe2_mesh_write.argtypes = [C.c_int, C.c_char_p]
@@ -398,16 +400,35 @@ class HyperRomEngine:
         _check(lib.fe2_hrom_output_ptrs(self._h, *[C.byref(p) for p in ps]))
         return [p.value for p in ps]
 
-    def gather(self, comm: "NcclComm", d_all: int, sigma=0, Cm=0, res=0, status=0) -> bool:
+    def gather_layout(self, comm: "NcclComm"):
+        """fe2_hrom_gather_layout: (P_max, per-rank point counts) over comm; the
+        gathered buffer holds world blocks of P_max rows (padding: status -1)."""
+        pmax = C.c_int64()
+        counts = (C.c_int64 * comm.nranks)()
+        _check(lib.fe2_hrom_gather_layout(self._h, comm.ptr, C.byref(pmax), counts))
+        return pmax.value, list(counts)
+
+    def gather(self, comm: "NcclComm", d_all: int, sigma=0, Cm=0, res=0, status=0, res_tol=float("inf"),
+               flags=False, wait=True):
         """fe2_hrom_gather: all-gather every rank's records {Σ | C | ‖r‖ |
-        status} of the last increment into the device buffer d_all
-        ([world][P_local][nc + nt + 2] doubles) over NCCL; the device
-        outputs default to the handle's own buffers. Returns the all-reduced
-        "some point failed" flag."""
-        flag = np.zeros(1, dtype=np.int32)
-        _check(lib.fe2_hrom_gather(self._h, comm.ptr, sigma or None, Cm or None, res or None, status or None, d_all,
-                                   _i(flag)))
-        return bool(flag[0])
+        status} of the last increment / monolithic iterate into the device
+        buffer d_all ([world][P_max][nc + nt + 2] doubles) over NCCL; the
+        device outputs default to the handle's own buffers. Returns the
+        all-reduced "some point failed" flag, or with flags=True the pair
+        (some point failed, some point has ‖r‖ > res_tol); wait=False keeps
+        the call asynchronous (returns None)."""
+        fl = np.zeros(2, dtype=np.int32)
+        _check(lib.fe2_hrom_gather(self._h, comm.ptr, sigma or None, Cm or None, res or None, status or None,
+                                   float(res_tol), d_all, _i(fl) if wait else None))
+        if not wait:
+            return None
+        return (bool(fl[0]), bool(fl[1])) if flags else bool(fl[0])
+
+    def mono_iterate_device(self, E_ptr, sigma=0, Cm=0, rel_res=0, pc=0, status=0, stream=0):
+        """fe2_hrom_mono_iterate_device: one monolithic iteration at the macro
+        strains E_ptr (device, P x 3), asynchronous; NULL outputs = the handle's."""
+        _check(lib.fe2_hrom_mono_iterate_device(self._h, E_ptr, sigma or None, Cm or None, rel_res or None,
+                                                pc or None, status or None, stream or None))
 
     def solve_increment_into(self, E, sigma, Cm, iters, pc, res, status, opts: NewtonOptions | None = None):
         """Host-buffer C-ABI call writing into caller-provided (e.g. pinned)

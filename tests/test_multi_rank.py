@@ -14,10 +14,11 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2306_02687_b200 import make_paths
-from paper_2306_02687_b200.shard import all_gather_outputs, pack_outputs, shard_range, unpack_outputs
+from paper_2306_02687_b200.shard import (all_gather_counts, all_gather_outputs, gather_rows, pack_outputs, pad_block,
+                                         shard_range, unpack_outputs)
 
 DESK = [("j2", 1.0, 0.3, 0.01, 0.016), ("elastic", 10.0, 0.3)]
-P_TOTAL, N_INCR = 10, 6
+P_TOTAL, N_INCR = 11, 6  # 11 points on 2 ranks: unequal blocks (6, 5), padded like the device
 
 
 def _free_port():
@@ -41,18 +42,19 @@ def _worker(rank, world, port, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     md = O.Model(8, 6, 40, 5)
     h = O.Hrom(md.G, md.w, md.mat, DESK, md.volume)
-    per = (P_TOTAL + world - 1) // world  # equal blocks for all_gather_into_tensor (pad the last)
     p0, p1 = shard_range(P_TOTAL, rank, world)
+    counts = all_gather_counts(p1 - p0)  # fe2_hrom_gather_layout
+    per = max(counts)
     E = make_paths(0, 11, p1 - p0, N_INCR, p0=p0)
     r = h.run(E)
     gathered = []
     for k in range(N_INCR):
-        blk = np.zeros((per, 14))
-        blk[: p1 - p0] = pack_outputs(r["sigma"][:, k], r["C"][:, k], r["res_norm"][:, k], r["status"][:, k])
+        blk = pad_block(pack_outputs(r["sigma"][:, k], r["C"][:, k], r["res_norm"][:, k], r["status"][:, k]), per)
         g = all_gather_outputs(torch.from_numpy(blk))
         gathered.append(g.numpy())
     if rank == 0:
         np.save(out_path, np.stack(gathered))
+        np.save(out_path + ".counts.npy", np.array(counts))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -67,9 +69,11 @@ def test_sharded_gather_equals_single_process(tmp_path):
     out = str(tmp_path / "g.npy")
     mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True, start_method="spawn")
     g = np.load(out)  # (N_INCR, world*per, 14)
-    per = (P_TOTAL + world - 1) // world
-    rows = np.concatenate([np.arange(r * per, r * per + (shard_range(P_TOTAL, r, world)[1] - shard_range(P_TOTAL, r, world)[0]))
-                           for r in range(world)])
+    counts = np.load(out + ".counts.npy").tolist()
+    assert counts == [6, 5]
+    rows = gather_rows(counts)
+    pad = np.setdiff1d(np.arange(g.shape[1]), rows)
+    assert len(pad) == 1 and (g[:, pad, 13] == -1).all() and np.isnan(g[:, pad, :13]).all()
     md = O.Model(8, 6, 40, 5)
     ref = O.Hrom(md.G, md.w, md.mat, DESK, md.volume).run(make_paths(0, 11, P_TOTAL, N_INCR))
     for k in range(N_INCR):
