@@ -34,91 +34,21 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "device_common.cuh"
 #include "hrom_kernels.cuh"
 
 namespace fe2 {
 
 namespace {
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
+using namespace dev;  // TMA / mbarrier, DMMA, warp reductions, fast reciprocals (device_common.cuh)
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
-}
-
-// D(8x8) += A(8x4) B(4x8), fp64 tensor core. Fragments: a = A[lane/4][lane%4],
-// b = B[lane%4][lane/4], d = D[lane/4][2*(lane%4) + {0,1}].
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+// D(8x8) += A(8x4) B(4x8) without `volatile`: the compiler may hoist the next
+// k-step's fragment loads above it (measured faster in this kernel's loops).
+__device__ __forceinline__ void dmma_nv(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// x + a*y rounded as the reference's `u_free + alpha * du` (no contraction).
-__device__ __forceinline__ double axpy_rn(double x, double a, double y) { return __dadd_rn(x, __dmul_rn(a, y)); }
-
-// E_prev + (E_tgt - E_prev) * target, as run_trajectory (rve.hpp:465).
-__device__ __forceinline__ double lerp_rn(double e0, double e1, double t) {
-  return __dadd_rn(e0, __dmul_rn(__dsub_rn(e1, e0), t));
-}
-
-__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
-
-// 1/x and 1/sqrt(x) from the MUFU seeds (~2^-22 relative) plus two Newton
-// steps (quadratic: ~2^-88 before rounding, i.e. within an ulp of the fp64
-// result); no IEEE division/sqrt sequences on the critical path.
-__device__ __forceinline__ double rcp_fast(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-__device__ __forceinline__ double rsqrt_fast(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  return y * fma(-hx * y, y, 1.5);
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ int tri_(int i) { return i * (i + 1) / 2; }
@@ -183,66 +113,6 @@ __device__ double warp_chol_solve(const double* sK, const double* sInv, int n, i
   return x;
 }
 
-// Elastic trial state of update4 (materials.hpp:162-169) and the yield test
-// (:208-210); the plastic branch returns the radial-return corrections
-// Δσ = σ − σ_tr (condensed) and ΔC = C − C_e (6 unique).
-struct Trial {
-  double t0, t1, t2, t3;  // trial stress (packed 4)
-  double d0, d1, d2, d3;  // trial deviator
-  double ss, inv_ns, q_tr, f;  // |s_tr|^2, 1/|s_tr|, sqrt(3/2)|s_tr|, yield function
-};
-
-__device__ __forceinline__ Trial trial_state(const MatDev& m, double ep0, double ep1, double ep2, double ep3,
-                                             double eq, double e11, double e22, double g12) {
-  Trial T;
-  const double two_mu = 2.0 * m.mu;
-  const double x0 = e11 - ep0, x1 = e22 - ep1, x2 = 0.0 - ep2, x3 = 0.5 * g12 - ep3;
-  const double lt = m.lam * (x0 + x1 + x2);
-  T.t0 = lt + two_mu * x0;
-  T.t1 = lt + two_mu * x1;
-  T.t2 = lt + two_mu * x2;
-  T.t3 = two_mu * x3;
-  const double p = (T.t0 + T.t1 + T.t2) * (1.0 / 3.0);
-  T.d0 = T.t0 - p;
-  T.d1 = T.t1 - p;
-  T.d2 = T.t2 - p;
-  T.d3 = T.t3;
-  T.ss = T.d0 * T.d0 + T.d1 * T.d1 + T.d2 * T.d2 + 2.0 * T.d3 * T.d3;
-  // |s_tr| and its reciprocal from one MUFU rsqrt seed (no IEEE sqrt sequence)
-  T.inv_ns = T.ss > 0.0 ? rsqrt_fast(T.ss) : 0.0;
-  T.q_tr = 1.2247448713915890491 * (T.ss * T.inv_ns);  // sqrt(3/2) |s_tr|
-  T.f = T.q_tr - (m.sy0 + m.h * eq);
-  return T;
-}
-
-struct Corr {
-  double dc00, dc01, dc02, dc11, dc12, dc22;  // ΔC
-  double ds0, ds1, ds2;                       // Δσ (11, 22, 12)
-};
-
-__device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
-  Corr c;
-  const double mu = m.mu;
-  const double dlam = T.f * m.inv_denom;  // f / (3 mu + h)
-  const double inv_q = 0.81649658092772603273 * T.inv_ns;  // 1/q_tr = sqrt(2/3) / |s_tr|
-  const double cs = 3.0 * mu * dlam * inv_q;
-  c.ds0 = -cs * T.d0;
-  c.ds1 = -cs * T.d1;
-  c.ds2 = -cs * T.d3;
-  const double inv_n = T.inv_ns;
-  const double n0 = T.d0 * inv_n, n1 = T.d1 * inv_n, n3 = T.d3 * inv_n;
-  const double mu2 = 6.0 * mu * mu;
-  const double c1 = mu2 * dlam * inv_q;
-  const double c2 = mu2 * (m.inv_denom - dlam * inv_q);
-  c.dc00 = -c1 * (2.0 / 3.0) - c2 * (n0 * n0);
-  c.dc01 = c1 * (1.0 / 3.0) - c2 * (n0 * n1);
-  c.dc02 = -c2 * (n0 * n3);
-  c.dc11 = -c1 * (2.0 / 3.0) - c2 * (n1 * n1);
-  c.dc12 = -c2 * (n1 * n3);
-  c.dc22 = -0.5 * c1 - c2 * (n3 * n3);
-  return c;
-}
-
 #ifndef FE2_KW
 #define FE2_KW 16
 #endif
@@ -256,7 +126,7 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
 #define FE2_MINB 1
 #endif
 #ifndef FE2_KWRES
-#define FE2_KWRES 8
+#define FE2_KWRES 12
 #endif
 #ifndef FE2_GROUP_UNROLL
 #define FE2_GROUP_UNROLL 1
@@ -266,7 +136,10 @@ constexpr int kGroupUnroll = FE2_GROUP_UNROLL;  // plastic-group loop unroll (tu
 // from NP = 16 on the 16-warp build spilled 0.5-1.1 KB per thread and 8 warps
 // with 255 registers measured faster (n = 32, K = 1,000 / 4,000: +9% / +15%)
 constexpr int kw_for(int NT) { return NT == 1 ? FE2_KW : 8; }
-constexpr int kWRes = FE2_KWRES;      // warps per CTA when the whole G2 is resident in shared memory
+// warps per CTA when the whole G2 is resident in shared memory: 12 (168 registers, the
+// warp-uniform Newton state in shared memory, WarpSt) — measured +12% over 8 warps with
+// 255 registers at n = 24; NP = 32 spills at 168 registers and keeps 8
+constexpr int kwres_for(int NT) { return NT == 4 ? 8 : FE2_KWRES; }
 constexpr int kMaxStages = FE2_STAGES;  // G-chunk ring depth (shared by the CTA), at most
 
 template <int NP, int W>
@@ -279,7 +152,8 @@ struct IncLayout {
   static constexpr int kSlots = kQC * 6 + kQC * 3 + kQC;     // w ΔC (6 unique), w Δσ, point index
   static constexpr int kTri = NP * (NP + 1) / 2;              // packed lower K_aa
   static constexpr int kUnion = (kSlots > kTri) ? kSlots : kTri;
-  static constexpr int WS = 6 * NP + 3 * NP + kUnion;  // per-warp scratch (doubles)
+  static constexpr int kState = 40;                     // WarpSt (warp-uniform Newton / pass state)
+  static constexpr int WS = 6 * NP + 3 * NP + kUnion + kState;  // per-warp scratch (doubles)
   // ring depth: as deep as the 227 KB shared-memory budget allows (<= kMaxStages)
   static constexpr long kBudget = 227L * 1024 - 512 - static_cast<long>(W) * WS * 8;
   static constexpr int kFit = static_cast<int>(kBudget / (static_cast<long>(chunk) * 8));
@@ -389,6 +263,22 @@ __device__ void ring_drain(const Ring& R, int seq, int lane) {
   trace(R, seq, 5);
 }
 
+// Warp-uniform state of the point a warp is driving, kept in the warp's shared
+// scratch instead of registers: the outputs of the last assembly pass (written
+// once per pass), the point's macro strains (written once per point) and the
+// micro_newton / run_trajectory state machine, parked here across each assembly
+// pass. Every lane stores its own identical copy and nothing is read-modify-
+// written in shared memory, so lanes need not run converged. Keeping this out
+// of the register file lets the chunk loop run at <= 168 registers (12 warps).
+struct WarpSt {
+  double s0, s1, s2, ce00, ce01, ce02, ce11, ce12, ce22, dsp0, dsp1, dsp2;  // pass outputs
+  double a, rn_it, best_rn, best_a, ref, done, frac;                        // Newton / line search
+  double E0, E1, E2, Ep0, Ep1, Ep2, Et0, Et1, Et2;                          // macro strain
+  int mode, it, ls, iters, bis, err, np_last, k_linear;
+  unsigned cnt[4];  // assemblies, commits, plastic evaluations, plastic points of accepted states (lane 0)
+};
+static_assert(sizeof(WarpSt) <= 40 * sizeof(double), "WarpSt exceeds IncLayout::kState");
+
 // Phase timeline of lane 0 of every warp (tuning builds only: -DFE2_INC_PROF; the
 // last warp to finish prints the sums): 0 strain GEMV (incl. ring wait), 1 trial /
 // yield / candidate history / slots, 2 DMMA contraction, 3 pass tail (reductions,
@@ -488,14 +378,20 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     io[s] = (4 * s + m) % 3;
   }
   int seq = 0;
-  unsigned long long n_asm = 0, n_com = 0, n_pl = 0, n_cpl = 0;
+  WarpSt* const W_ = reinterpret_cast<WarpSt*>(wbase + L::WS - L::kState);
+  // counters: lane 0's private copies in the warp state (only lane 0 updates / reads them)
+  unsigned* const cnt_ = W_->cnt;
+  if (lane == 0) cnt_[0] = cnt_[1] = cnt_[2] = cnt_[3] = 0;
 
   // outputs of an assembly pass (warp-uniform after the reductions)
-  double s0 = 0, s1 = 0, s2 = 0, ce00 = 0, ce01 = 0, ce02 = 0, ce11 = 0, ce12 = 0, ce22 = 0;
-  double dsp0 = 0, dsp1 = 0, dsp2 = 0;  // plastic parts of Σraw (for the commit)
-  int np_last = 0;                      // plastic points of the last pass
+  double &s0 = W_->s0, &s1 = W_->s1, &s2 = W_->s2, &ce00 = W_->ce00, &ce01 = W_->ce01, &ce02 = W_->ce02;
+  double &ce11 = W_->ce11, &ce12 = W_->ce12, &ce22 = W_->ce22;
+  double &dsp0 = W_->dsp0, &dsp1 = W_->dsp1, &dsp2 = W_->dsp2;  // plastic parts of Σraw (for the commit)
+  int& np_last = W_->np_last;   // plastic points of the last pass
+  int& k_linear = W_->k_linear;  // the last assembly had no plastic point (K_aa == K_e)
+  s0 = s1 = s2 = ce00 = ce01 = ce02 = ce11 = ce12 = ce22 = dsp0 = dsp1 = dsp2 = 0.0;
+  np_last = k_linear = 0;
   const bool dbg = A.dbg != nullptr;
-  bool k_linear = false;  // the last assembly had no plastic point (K_aa == K_e)
   const int n = M.n;
 
   // ------------------------------------------------ per-lane history loads
@@ -583,7 +479,6 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       const bool plastic = (T.f > 0.0) && (q < M.K2);
       const unsigned bal = __ballot_sync(0xffffffffu, plastic);
       const int np = __popc(bal);
-      n_pl += static_cast<unsigned long long>(np);
       np_tot += np;
       {  // candidate history of this state (finish_return, materials.hpp:173-185): written every
          // pass into the non-committed buffer, adopted by a flip if the state is accepted
@@ -671,7 +566,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
           for (int t1 = 0; t1 < NT; ++t1)
 #pragma unroll
             for (int t2 = t1; t2 < NT; ++t2) {
-              dmma(acc[ti][0], acc[ti][1], Af[t1], Bf[t2]);
+              dmma_nv(acc[ti][0], acc[ti][1], Af[t1], Bf[t2]);
               ++ti;
             }
         }
@@ -780,8 +675,11 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     dsp1 = ds1;
     dsp2 = ds2;
     np_last = np_tot;
-    k_linear = (np_tot == 0);
-    ++n_asm;
+    k_linear = (np_tot == 0) ? 1 : 0;
+    if (lane == 0) {
+      cnt_[2] += static_cast<unsigned>(np_tot);
+      cnt_[0] += 1;
+    }
     __syncwarp();
     INC_T(3);
   };
@@ -817,8 +715,10 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       D.sp[p * 4 + 2] -= dsp2;
       D.st[p].pad[0] ^= 1;
     }
-    ++n_com;
-    n_cpl += static_cast<unsigned long long>(np_last);
+    if (lane == 0) {
+      cnt_[1] += 1;
+      cnt_[3] += static_cast<unsigned>(np_last);
+    }
     __syncwarp();
     return np_last;
   };
@@ -952,10 +852,13 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   while (p_next < D.P) {
     const int64_t p = p_next;
     p_next = -1;
-    const double Ep0 = dbg ? 0.0 : D.E_c[p * 3 + 0], Ep1 = dbg ? 0.0 : D.E_c[p * 3 + 1],
-                 Ep2 = dbg ? 0.0 : D.E_c[p * 3 + 2];
-    const double Et0 = dbg ? A.dbg_E[0] : A.dE[p * 3 + 0], Et1 = dbg ? A.dbg_E[1] : A.dE[p * 3 + 1],
-                 Et2 = dbg ? A.dbg_E[2] : A.dE[p * 3 + 2];
+    double &Ep0 = W_->Ep0, &Ep1 = W_->Ep1, &Ep2 = W_->Ep2, &Et0 = W_->Et0, &Et1 = W_->Et1, &Et2 = W_->Et2;
+    Ep0 = dbg ? 0.0 : D.E_c[p * 3 + 0];
+    Ep1 = dbg ? 0.0 : D.E_c[p * 3 + 1];
+    Ep2 = dbg ? 0.0 : D.E_c[p * 3 + 2];
+    Et0 = dbg ? A.dbg_E[0] : A.dE[p * 3 + 0];
+    Et1 = dbg ? A.dbg_E[1] : A.dE[p * 3 + 1];
+    Et2 = dbg ? A.dbg_E[2] : A.dE[p * 3 + 2];
     const int dead = dbg ? 0 : D.st[p].err;
     auto write_fail = [&](int code, int iters, double rn) {
       if (lane == 0) {
@@ -994,7 +897,21 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     double a = 1.0, rn_it = 0.0, best_rn = 0.0, best_a = 1.0, ref = 0.0, done = 0.0, frac = 1.0;
     int err = 0;
     while (true) {
+      // park the Newton state in shared memory across the pass: the registers are
+      // free for the chunk loop (each lane stores its own, warp-uniform copy; no
+      // read-modify-write of shared state, so convergence does not matter)
+      W_->E0 = E0, W_->E1 = E1, W_->E2 = E2;
+      W_->mode = mode, W_->it = it, W_->ls = ls, W_->iters = iters, W_->bis = bis, W_->err = err;
+      W_->a = a, W_->rn_it = rn_it, W_->best_rn = best_rn, W_->best_a = best_a, W_->ref = ref;
+      W_->done = done, W_->frac = frac;
       assembly_pass(p, E0, E1, E2, dbg ? -1 : p);
+      {  // volatile reloads: the compiler may not forward the parked values in registers
+        const volatile WarpSt* V = W_;
+        E0 = V->E0, E1 = V->E1, E2 = V->E2;
+        mode = V->mode, it = V->it, ls = V->ls, iters = V->iters, bis = V->bis, err = V->err;
+        a = V->a, rn_it = V->rn_it, best_rn = V->best_rn, best_a = V->best_a, ref = V->ref;
+        done = V->done, frac = V->frac;
+      }
       if (dbg) {
         dump();
         break;
@@ -1191,10 +1108,10 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   }
 #endif
   if (A.cnt && lane == 0) {
-    atomicAdd(&A.cnt->assemblies, n_asm);
-    atomicAdd(&A.cnt->commits, n_com);
-    atomicAdd(&A.cnt->plastic_evals, n_pl);
-    atomicAdd(&A.cnt->commit_plastic, n_cpl);
+    atomicAdd(&A.cnt->assemblies, static_cast<unsigned long long>(cnt_[0]));
+    atomicAdd(&A.cnt->commits, static_cast<unsigned long long>(cnt_[1]));
+    atomicAdd(&A.cnt->plastic_evals, static_cast<unsigned long long>(cnt_[2]));
+    atomicAdd(&A.cnt->commit_plastic, static_cast<unsigned long long>(cnt_[3]));
   }
 }
 
@@ -1262,9 +1179,10 @@ bool resident_disabled() {
 template <int NT>
 void launch_inc_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
   constexpr int NP = 8 * NT;
-  const size_t res = IncLayout<NP, kWRes>::res_bytes(a.M.nchunks);
+  constexpr int WR = kwres_for(NT);
+  const size_t res = IncLayout<NP, WR>::res_bytes(a.M.nchunks);
   if (res <= kMaxDynSmem && !resident_disabled())
-    launch_inc_variant<NT, kWRes, true>(a, num_sms, s, res);
+    launch_inc_variant<NT, WR, true>(a, num_sms, s, res);
   else
     launch_inc_variant<NT, kw_for(NT), false>(a, num_sms, s, IncLayout<NP, kw_for(NT)>::bytes);
 }
