@@ -371,12 +371,6 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   }
 
   const int m = lane & 3, col = lane >> 2;
-  int qo[3], io[3];
-#pragma unroll
-  for (int s = 0; s < 3; ++s) {
-    qo[s] = (4 * s + m) / 3;
-    io[s] = (4 * s + m) % 3;
-  }
   int seq = 0;
   WarpSt* const W_ = reinterpret_cast<WarpSt*>(wbase + L::WS - L::kState);
   // counters: lane 0's private copies in the warp state (only lane 0 updates / reads them)
@@ -537,36 +531,42 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       }
       __syncwarp();
       INC_T(1);
-      // plastic contraction on DMMA: k = 3 slot + i, four k per k-step
+      // plastic contraction on DMMA. A group = 4 plastic slots; k-lane m owns slot 4g + m
+      // and the k-step i (0..2) contracts strain row i of the four slots: the lane loads
+      // its slot's three G rows ONCE per group (each element once, no re-loads per
+      // row), forms the three rows of B = (w ΔC) G in registers and feeds A = G row i.
       const int ng = np4 >> 2;
 #pragma unroll kGroupUnroll
       for (int g = 0; g < ng; ++g) {
+        const int slot = 4 * g + m;
+        const double* wc = sDC + slot * 6;  // w ΔC: 00 01 02 11 12 22
+        const double w00 = wc[0], w01 = wc[1], w02 = wc[2], w11 = wc[3], w12 = wc[4], w22 = wc[5];
+        const double ws0 = sDS[slot * 3 + 0], ws1 = sDS[slot * 3 + 1], ws2 = sDS[slot * 3 + 2];
+        const double* gp = Gb + sQ[slot] * S + col;
+        double G0[NT], G1[NT], G2[NT], B0[NT], B1[NT], B2[NT];
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
-          const int slot = 4 * g + qo[s];
-          const int i = io[s];
-          const int ro_i = i * L::R1;  // row i of the slot's point (rows R1 apart)
-          // row i of the symmetric w ΔC from its 6 unique entries (00 01 02 11 12 22)
-          const int b = i > 0 ? 1 : 0;
-          const double* wc = sDC + slot * 6;
-          const double k0 = wc[i], k1 = wc[i + 1 + b], k2 = wc[i + 2 + b];
-          const double ws = sDS[slot * 3 + i];
-          const double* gp = Gb + sQ[slot] * S + col;
-          double Af[NT], Bf[NT];
+        for (int t = 0; t < NT; ++t) {
+          G0[t] = gp[t * 8];
+          G1[t] = gp[L::R1 + t * 8];
+          G2[t] = gp[L::R2 + t * 8];
+          B0[t] = w00 * G0[t] + w01 * G1[t] + w02 * G2[t];
+          B1[t] = w01 * G0[t] + w11 * G1[t] + w12 * G2[t];
+          B2[t] = w02 * G0[t] + w12 * G1[t] + w22 * G2[t];
+          kae[t][0] += B0[t];
+          kae[t][1] += B1[t];
+          kae[t][2] += B2[t];
+          rr[t] += ws0 * G0[t] + ws1 * G1[t] + ws2 * G2[t];
+        }
 #pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            const double g0 = gp[t * 8], g1 = gp[L::R1 + t * 8], g2 = gp[L::R2 + t * 8];
-            Af[t] = gp[ro_i + t * 8];
-            Bf[t] = k0 * g0 + k1 * g1 + k2 * g2;
-            kae[t][s] += Bf[t];
-            rr[t] += ws * Af[t];
-          }
+        for (int i = 0; i < 3; ++i) {  // k-step i: row i of the four slots
           int ti = 0;
 #pragma unroll
           for (int t1 = 0; t1 < NT; ++t1)
 #pragma unroll
             for (int t2 = t1; t2 < NT; ++t2) {
-              dmma_nv(acc[ti][0], acc[ti][1], Af[t1], Bf[t2]);
+              const double a_ = i == 0 ? G0[t1] : (i == 1 ? G1[t1] : G2[t1]);
+              const double b_ = i == 0 ? B0[t2] : (i == 1 ? B1[t2] : B2[t2]);
+              dmma_nv(acc[ti][0], acc[ti][1], a_, b_);
               ++ti;
             }
         }
@@ -583,9 +583,8 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       double ki[3];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int s = (i - (m % 3) + 3) % 3;  // slot s holds strain row (s + m) mod 3
-        double x = (s == 0) ? kae[t][0] : ((s == 1) ? kae[t][1] : kae[t][2]);
+      for (int i = 0; i < 3; ++i) {  // kae[t][i]: strain row i of this lane's slots
+        double x = kae[t][i];
         x += __shfl_xor_sync(0xffffffffu, x, 1);
         x += __shfl_xor_sync(0xffffffffu, x, 2);
         ki[i] = x;
