@@ -153,7 +153,8 @@ struct IncLayout {
   static constexpr int kTri = NP * (NP + 1) / 2;              // packed lower K_aa
   static constexpr int kUnion = (kSlots > kTri) ? kSlots : kTri;
   static constexpr int kState = 40;                     // WarpSt (warp-uniform Newton / pass state)
-  static constexpr int WS = 6 * NP + 3 * NP + kUnion + kState;  // per-warp scratch (doubles)
+  // per-warp scratch (doubles), even so that every warp's α vector stays 16-B aligned
+  static constexpr int WS = (6 * NP + 3 * NP + kUnion + kState + 1) & ~1;
   // ring depth: as deep as the 227 KB shared-memory budget allows (<= kMaxStages)
   static constexpr long kBudget = 227L * 1024 - 512 - static_cast<long>(W) * WS * 8;
   static constexpr int kFit = static_cast<int>(kBudget / (static_cast<long>(chunk) * 8));
