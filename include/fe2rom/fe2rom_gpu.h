@@ -62,8 +62,9 @@ extern "C" {
  * kind 2: PowerLawParams p = {E, nu, sigma_y0, N}          sy(e) = sy0 (1 + E e / sy0)^N
  * kind 3: CreepParams    p = {E, nu, A, n, m, dt}          deq/dt = (q/A)^(n/(m+1)) ((m+1) eq)^(m/(m+1));
  *                        dt = time of one load increment (PathStep::dt; bisected sub-steps use their share)
- * The hyper-ROM engines (fe2_hrom_create*) and the SoA update carry kinds 0/1;
- * fe2_material_update_batch and the HF solver (fe2_hf_*) carry all four. */
+ * The small-strain hyper-ROM engine (fe2_hrom_create; one inelastic material per
+ * model), fe2_material_update_batch and the HF solver (fe2_hf_*) carry all four;
+ * the finite-strain engine, the monolithic iteration and the SoA update carry 0/1. */
 typedef struct {
   int kind;
   double p[6];

@@ -1039,8 +1039,10 @@ struct Assembly {
 };
 
 // ε_q = E + G_q α (decision 6) ; update_material ; weighted sums.
+// dt_scale: the fraction of the increment a (bisected) sub-step covers; a creep
+// material integrates over PathStep::dt x dt_scale (rve.hpp:466, MicroOptions::dt)
 inline void hrom_assemble(const Hrom& h, const double* alpha, const double* E,
-                          const std::vector<State>& s0, bool with_K, Assembly& A) {
+                          const std::vector<State>& s0, bool with_K, Assembly& A, double dt_scale = 1.0) {
   const int n = h.n;
   A.r.assign(n, 0.0);
   if (with_K) {
@@ -1061,7 +1063,9 @@ inline void hrom_assemble(const Hrom& h, const double* alpha, const double* E,
       for (int a = 0; a < n; ++a) s += Gq[i * n + a] * alpha[a];
       eps[i] = E[i] + s;
     }
-    const Result3 res = update_material(h.mats[h.mat[q]], s0[q], eps);
+    Mat mq = h.mats[h.mat[q]];
+    mq.dt *= dt_scale;
+    const Result3 res = update_material(mq, s0[q], eps);
     A.states[q] = res.state;
     A.plastic[q] = res.plastic ? 1 : 0;
     A.plastic_count += res.plastic ? 1 : 0;
@@ -1101,7 +1105,7 @@ struct PointResult {
 };
 
 inline PointResult hrom_newton(const Hrom& h, const std::vector<double>& alpha0, const double* E,
-                               const std::vector<State>& s0, double tol, int max_iter) {
+                               const std::vector<State>& s0, double tol, int max_iter, double dt_scale = 1.0) {
   const int n = h.n;
   PointResult pr;
   std::vector<double> alpha = alpha0, du(n), mres(n), trial_alpha(n);
@@ -1109,7 +1113,7 @@ inline PointResult hrom_newton(const Hrom& h, const std::vector<double>& alpha0,
   Assembly T;
   double ref = 0.0;
   for (int it = 0; it <= max_iter; ++it) {
-    hrom_assemble(h, alpha.data(), E, s0, true, A);
+    hrom_assemble(h, alpha.data(), E, s0, true, A, dt_scale);
     const double rn = A.rn;
     if (it == 0) ref = std::max({rn, norm2(A.S_raw, 3), 1e-30});
     if (rn <= tol * ref) {
@@ -1130,7 +1134,7 @@ inline PointResult hrom_newton(const Hrom& h, const std::vector<double>& alpha0,
     double a = 1.0, best_a = 1.0, best_rn = std::numeric_limits<double>::infinity();
     for (int ls = 0; ls < 8; ++ls) {
       for (int i = 0; i < n; ++i) trial_alpha[i] = alpha[i] + a * du[i];
-      hrom_assemble(h, trial_alpha.data(), E, s0, false, T);
+      hrom_assemble(h, trial_alpha.data(), E, s0, false, T, dt_scale);
       const double trial = T.rn;
       if (trial < best_rn) {
         best_rn = trial;
@@ -1199,6 +1203,7 @@ inline void hrom_point_trajectory(const Hrom& h, std::int64_t pi, int n_incr, co
   std::vector<State> states(K);
   double E_prev[3] = {0, 0, 0};
   bool dead = false;
+  int dead_code = 0;  // the error that ended the trajectory, reported for every later increment
   for (int k = 0; k < n_incr; ++k) {
     const std::int64_t o = pi * n_incr + k;
     const double* Ek = Ep + 3 * k;
@@ -1215,7 +1220,7 @@ inline void hrom_point_trajectory(const Hrom& h, std::int64_t pi, int n_incr, co
         for (int i = 0; i < 3; ++i) E[i] = E_prev[i] + (Ek[i] - E_prev[i]) * target;
         PointResult pr;
         try {
-          pr = hrom_newton(h, alpha_c, E, states, tol, max_iter);
+          pr = hrom_newton(h, alpha_c, E, states, tol, max_iter, target - done);
         } catch (const Error& e) {
           status = 1 + (int)e.code;
           dead = true;
@@ -1247,8 +1252,9 @@ inline void hrom_point_trajectory(const Hrom& h, std::int64_t pi, int n_incr, co
           std::memcpy(out->plastic_flags + (size_t)o * K, pr.A.plastic.data(), (size_t)K);
       }
     } else {
-      status = 1 + (int)ErrorCode::solver;
+      status = dead_code;
     }
+    if (dead && !dead_code) dead_code = status;
     if (status != 0) {  // run_trajectory throws: no response for this increment
       for (double& s : sig) s = NAN;
       for (double& c : C) c = NAN;
@@ -1591,6 +1597,7 @@ inline void fs_point_trajectory(const HromFs& h, std::int64_t pi, int n_incr, co
   std::vector<State> states(K);
   double H_prev[4] = {0, 0, 0, 0};
   bool dead = false;
+  int dead_code = 0;  // the error that ended the trajectory, reported for every later increment
   for (int k = 0; k < n_incr; ++k) {
     const std::int64_t o = pi * n_incr + k;
     const double* Hk = Hp + 4 * k;
@@ -1638,8 +1645,9 @@ inline void fs_point_trajectory(const HromFs& h, std::int64_t pi, int n_incr, co
         done = target;
       }
     } else {
-      status = 1 + (int)ErrorCode::solver;
+      status = dead_code;
     }
+    if (dead && !dead_code) dead_code = status;
     if (status != 0) {
       for (double& v : P) v = NAN;
       for (double& v : AM) v = NAN;

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libfe2rom_gpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["hrom_host.cu", "hrom_kernels.cu", "hrom_kernels_big.cu", "hrom_kernels_big_mono.cu", "hrom_kernels_big_other.cu", "hrom_kernels_fs.cu", "material_soa.cu", "setup.cpp", "macro.cpp", "ecm.cpp", "hf.cu", "exchange.cu"]
+SOURCES = ["hrom_host.cu", "hrom_kernels.cu", "hrom_kernels_big.cu", "hrom_kernels_big_mono.cu", "hrom_kernels_big_other.cu", "hrom_kernels_big_gen.cu", "hrom_kernels_fs.cu", "material_soa.cu", "setup.cpp", "macro.cpp", "ecm.cpp", "hf.cu", "exchange.cu"]
 HEADERS = ["common.hpp", "material.cuh", "hrom_kernels.cuh", "device_common.cuh", "biot.cuh", "host_util.cuh", "rve.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",

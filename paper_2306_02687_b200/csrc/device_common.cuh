@@ -141,5 +141,113 @@ __device__ __forceinline__ Corr radial_return(const MatDev& m, const Trial& T) {
   return c;
 }
 
+// The scalar return of an iterative material (the history-carrying points of
+// a power-law or creep model) on the trial state T: the reference's
+// safeguarded Newton iterations, power law materials.hpp:216-244 (plastic iff
+// f_tr > 0), strain-hardening creep :246-292 (inelastic iff the solve gives
+// dlam > 0; dt = the sub-step's time, PathStep::dt x its fraction,
+// rve.hpp:466). q_tr is formed as the reference does, sqrt(3/2) sqrt(|s_tr|²).
+// Out: dlam, kq = d(dlam)/d(q_tr); ok = false when the iteration does not
+// converge, the creep bracket fails or dt <= 0 (ErrorCode::material).
+struct GenRet {
+  double dlam, kq;
+  bool plastic, ok;
+};
+static __device__ __noinline__ GenRet general_return(const MatDev& m, double ss, double eq, double dt) {
+  GenRet g{0.0, 0.0, false, true};
+  const double mu = m.mu;
+  const double q_tr = 1.2247448713915890491 * sqrt(ss);
+  if (m.kind == 2) {
+    auto sy = [&](double e) { return m.sy0 * pow(1.0 + m.E * e / m.sy0, m.N); };
+    auto sy_slope = [&](double e) { return m.E * m.N * pow(1.0 + m.E * e / m.sy0, m.N - 1.0); };
+    const double f_tr = q_tr - sy(eq);
+    if (f_tr <= 0.0) return g;
+    double lo = 0.0, hi = f_tr / (3.0 * mu), x = hi * 0.5;
+    const double tol = 1e-12 * fmax(m.sy0, q_tr);
+    bool conv = false;
+    for (int it = 0; it < 50; ++it) {
+      const double gx = q_tr - 3.0 * mu * x - sy(eq + x);
+      if (fabs(gx) <= tol) {
+        conv = true;
+        break;
+      }
+      if (gx > 0.0) lo = x;
+      else hi = x;
+      double next = x + gx / (3.0 * mu + sy_slope(eq + x));
+      if (!(next > lo && next < hi)) next = 0.5 * (lo + hi);
+      x = next;
+    }
+    g.ok = conv;
+    g.plastic = true;
+    g.dlam = x;
+    g.kq = 1.0 / (3.0 * mu + sy_slope(eq + x));
+    return g;
+  }
+  // creep (kind 3)
+  if (!(dt > 0.0)) {
+    g.ok = false;
+    return g;
+  }
+  if (!(q_tr > 1e-14 * m.E)) return g;
+  const double p1 = m.cn / (m.cm + 1.0), p2 = m.cm / (m.cm + 1.0), eq_floor = 1e-12;
+  auto hard = [&](double e) { return pow((m.cm + 1.0) * fmax(e, eq_floor), p2); };
+  auto hard_slope = [&](double e) { return e <= eq_floor ? 0.0 : p2 * (m.cm + 1.0) * pow((m.cm + 1.0) * e, p2 - 1.0); };
+  auto rate_q = [&](double q) { return pow(q / m.A, p1); };
+  auto rate_q_slope = [&](double q) { return p1 / m.A * pow(q / m.A, p1 - 1.0); };
+  double lo = 0.0, hi = q_tr / (3.0 * mu);
+  if (hi - dt * rate_q(q_tr - 3.0 * mu * hi) * hard(eq + hi) < 0.0) {  // bracket failure
+    g.ok = false;
+    return g;
+  }
+  double x = 0.5 * hi, Rp = 1.0;
+  const double tol = 1e-14 * fmax(1.0, hi);
+  bool conv = false;
+  for (int it = 0; it < 200; ++it) {
+    const double q = q_tr - 3.0 * mu * x;
+    const double e = eq + x;
+    const double Rx = x - dt * rate_q(q) * hard(e);
+    Rp = 1.0 + 3.0 * mu * dt * rate_q_slope(q) * hard(e) - dt * rate_q(q) * hard_slope(e);
+    if (fabs(Rx) <= tol) {
+      conv = true;
+      break;
+    }
+    if (Rx < 0.0) lo = x;
+    else hi = x;
+    double next = (Rp > 0.0) ? x - Rx / Rp : 0.5 * (lo + hi);
+    if (!(next > lo && next < hi)) next = 0.5 * (lo + hi);
+    x = next;
+  }
+  g.ok = conv;
+  if (conv && x > 0.0) {
+    g.plastic = true;
+    g.dlam = x;
+    g.kq = dt * rate_q_slope(q_tr - 3.0 * mu * x) * hard(eq + x) / Rp;
+  }
+  return g;
+}
+
+// radial_return with a given multiplier and sensitivity (iterative materials)
+__device__ __forceinline__ Corr radial_return_gen(const MatDev& m, const Trial& T, double dlam, double kq) {
+  Corr c;
+  const double mu = m.mu;
+  const double inv_q = 0.81649658092772603273 * T.inv_ns;
+  const double cs = 3.0 * mu * dlam * inv_q;
+  c.ds0 = -cs * T.d0;
+  c.ds1 = -cs * T.d1;
+  c.ds2 = -cs * T.d3;
+  const double inv_n = T.inv_ns;
+  const double n0 = T.d0 * inv_n, n1 = T.d1 * inv_n, n3 = T.d3 * inv_n;
+  const double mu2 = 6.0 * mu * mu;
+  const double c1 = mu2 * dlam * inv_q;
+  const double c2 = mu2 * (kq - dlam * inv_q);
+  c.dc00 = -c1 * (2.0 / 3.0) - c2 * (n0 * n0);
+  c.dc01 = c1 * (1.0 / 3.0) - c2 * (n0 * n1);
+  c.dc02 = -c2 * (n0 * n3);
+  c.dc11 = -c1 * (2.0 / 3.0) - c2 * (n1 * n1);
+  c.dc12 = -c2 * (n1 * n3);
+  c.dc22 = -0.5 * c1 - c2 * (n3 * n3);
+  return c;
+}
+
 }  // namespace dev
 }  // namespace fe2

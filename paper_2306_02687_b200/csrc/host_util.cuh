@@ -58,11 +58,11 @@ inline MatDev to_dev(const fe2_material_t& m) {  // validate, materials.hpp:80-9
   return make_mat(m.kind, E, nu, m.kind == 1 ? m.p[2] : 0.0, m.kind == 1 ? m.p[3] : 0.0);
 }
 
-// The hyper-ROM engines carry the closed-form J2 / elastic points only.
+// The finite-strain (Biot) engine carries closed-form J2 / elastic points only.
 inline void require_engine_material(const MatDev& m) {
   check(m.kind <= 1, Code::config,
-        "the hyper-ROM engine supports elastic and J2 materials; power-law / creep run through "
-        "fe2_material_update_batch and the HF solver");
+        "the finite-strain hyper-ROM engine supports elastic and J2 materials; power-law / creep run "
+        "through the small-strain engine, fe2_material_update_batch and the HF solver");
 }
 
 // exchange.cu: the block layout over a communicator (every rank's point count; the

@@ -435,11 +435,8 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
     check(n >= 1 && K >= 1 && G && w && mat_id && mats && n_mats >= 1, Code::config, "bad model arguments");
     check(n <= 128, Code::config, "this build supports n <= 128 modes");
     check(volume > 0.0, Code::config, "RVE volume must be positive");
-    std::vector<MatDev> md;
-    for (int i = 0; i < n_mats; ++i) {
-      md.push_back(to_dev(mats[i]));
-      require_engine_material(md.back());
-    }
+    std::vector<MatDev> md;  // any kind: J2 closed form, power law / creep by their return maps
+    for (int i = 0; i < n_mats; ++i) md.push_back(to_dev(mats[i]));
     require_device(device);
     auto h = new fe2_hrom_s;
     try {
@@ -467,8 +464,9 @@ int fe2_hrom_create(int device, int n, int K, const double* G, const double* w, 
         check(mat_id[q] >= 0 && mat_id[q] < n_mats, Code::config, "cubature material id out of range");
         check(w[q] > 0.0, Code::config, "cubature weights must be positive");
         h->qmat.push_back(md[mat_id[q]]);
-        if (md[mat_id[q]].kind == 1) {
-          check(j2_mat < 0 || j2_mat == mat_id[q], Code::config, "this build supports one J2 material per model");
+        if (md[mat_id[q]].kind >= 1) {  // history-carrying (J2, power law or creep)
+          check(j2_mat < 0 || j2_mat == mat_id[q], Code::config,
+                "this build supports one inelastic (J2 / power-law / creep) material per model");
           j2_mat = mat_id[q];
           h->j2_idx.push_back(q);
         } else {
@@ -636,6 +634,8 @@ int fe2_hrom_mono_begin(fe2_hrom_t h) {
   return guard([&] {
     check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
     check(h->kin == 0, Code::config, "the monolithic iteration needs a small-strain handle");
+    check(h->mat2.kind <= 1, Code::config,
+          "the monolithic iteration supports J2 / elastic models (power law / creep: fe2_hrom_solve_increment)");
     h->mono_first = true;
   });
 }
@@ -645,6 +645,8 @@ namespace {
 void mono_launch(fe2_hrom_t h, const double* d_E, const Outputs& O, cudaStream_t s) {
   check(h->P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
   check(h->kin == 0, Code::config, "the monolithic iteration needs a small-strain handle");
+  check(h->mat2.kind <= 1, Code::config,
+        "the monolithic iteration supports J2 / elastic models (power law / creep: fe2_hrom_solve_increment)");
   const int64_t P = h->P;
   if (!h->mono) {
     h->mono = dalloc<double>(static_cast<size_t>(P) * mono_stride(h->NP));

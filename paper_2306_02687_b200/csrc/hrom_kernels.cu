@@ -276,6 +276,7 @@ struct WarpSt {
   double a, rn_it, best_rn, best_a, ref, done, frac;                        // Newton / line search
   double E0, E1, E2, Ep0, Ep1, Ep2, Et0, Et1, Et2;                          // macro strain
   int mode, it, ls, iters, bis, err, np_last, k_linear;
+  int merr, pad_;  // iterative materials: some return map of the last pass failed (ErrorCode::material)
   unsigned cnt[4];  // assemblies, commits, plastic evaluations, plastic points of accepted states (lane 0)
 };
 static_assert(sizeof(WarpSt) <= 40 * sizeof(double), "WarpSt exceeds IncLayout::kState");
@@ -304,7 +305,9 @@ __device__ unsigned long long g_inc_prof[7];
 // RES: the whole projected operator G2 sits in shared memory for the kernel's
 // lifetime (loaded once by TMA): warps never wait on each other for G chunks.
 // Otherwise G2 streams through the CTA-shared ring (W warps, ST stages).
-template <int NT, int W, bool RES, bool MONO = false>
+// GEN: the history-carrying points follow an iterative material (power law /
+// creep, general_return) instead of the closed-form J2 return.
+template <int NT, int W, bool RES, bool MONO = false, bool GEN = false>
 __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArgs A) {
   constexpr int NP = 8 * NT;
   constexpr int NTP = NT * (NT + 1) / 2;
@@ -424,6 +427,9 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     }
     double c00 = 0.0, c01 = 0.0, c02 = 0.0, c11 = 0.0, c12 = 0.0, c22 = 0.0, ds0 = 0.0, ds1 = 0.0, ds2 = 0.0;
     int np_tot = 0;
+    bool merr = false;  // GEN: a return map of this pass failed
+    // GEN creep: the time of this sub-step, PathStep::dt x (target - done) (rve.hpp:466)
+    const double dt_sub = GEN ? mt.dt * (fmin(1.0, W_->done + W_->frac) - W_->done) : 0.0;
     const bool cur = D.st[p].pad[0] != 0;  // committed buffer; the candidate goes to the other one
     double* hcand = D.hist + (cur ? 0 : D.hist_alt) + p * nch * (5 * kQC) + lane;
     uint8_t* fcand = D.flags ? D.flags + (cur ? 0 : D.flags_alt) + p * M.K2p : nullptr;
@@ -471,7 +477,20 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       }
       INC_T(0);
       const Trial T = trial_state(mt, h0, h1, h2, h3, h4, E0 + (e0 + f0), E1 + (e1 + f1), E2 + (e2 + f2));
-      const bool plastic = (T.f > 0.0) && (q < M.K2);
+      bool plastic;
+      double dlam_g = 0.0, kq_g = 0.0;
+      if constexpr (GEN) {
+        plastic = false;
+        if (q < M.K2) {
+          const GenRet g = general_return(mt, T.ss, h4, dt_sub);
+          plastic = g.plastic;
+          dlam_g = g.dlam;
+          kq_g = g.kq;
+          merr = merr || !g.ok;
+        }
+      } else {
+        plastic = (T.f > 0.0) && (q < M.K2);
+      }
       const unsigned bal = __ballot_sync(0xffffffffu, plastic);
       const int np = __popc(bal);
       np_tot += np;
@@ -479,7 +498,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
          // pass into the non-committed buffer, adopted by a flip if the state is accepted
         double n0 = h0, n1 = h1, n2 = h2, n3 = h3, n4 = h4;
         if (plastic) {
-          const double dlam = T.f * mt.inv_denom;
+          const double dlam = GEN ? dlam_g : T.f * mt.inv_denom;
           const double ce = 1.5 * dlam * (0.81649658092772603273 * T.inv_ns);
           n0 = h0 + ce * T.d0;
           n1 = h1 + ce * T.d1;
@@ -496,7 +515,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
         if (fcand && q < M.K2) fcand[q] = plastic ? 1 : 0;
       }
       if (plastic) {
-        const Corr cr = radial_return(mt, T);
+        const Corr cr = GEN ? radial_return_gen(mt, T, dlam_g, kq_g) : radial_return(mt, T);
         const double wq = Gq[L::R2 + NP];  // cubature weight rides in the record's pad
         const int slot = __popc(bal & ((1u << lane) - 1u));
         const double w00 = wq * cr.dc00, w01 = wq * cr.dc01, w02 = wq * cr.dc02;
@@ -676,6 +695,7 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     dsp2 = ds2;
     np_last = np_tot;
     k_linear = (np_tot == 0) ? 1 : 0;
+    if constexpr (GEN) W_->merr = __any_sync(0xffffffffu, merr) ? 1 : 0;
     if (lane == 0) {
       cnt_[2] += static_cast<unsigned>(np_tot);
       cnt_[0] += 1;
@@ -724,7 +744,8 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
   };
 
   const NewtonCfg& cfg = A.cfg;
-  constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
+  constexpr int kSolver = 1 + 4;    // 1 + ErrorCode::solver
+  constexpr int kMaterial = 1 + 3;  // 1 + ErrorCode::material
 
   // Every large piece (assembly pass, factorization, acceptance) has exactly
   // one call site below, so each is inlined once: the kernel's instruction
@@ -915,6 +936,15 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       if (dbg) {
         dump();
         break;
+      }
+      if constexpr (GEN) {
+        // a failed return map throws out of micro_newton and run_trajectory
+        // (materials.hpp:244, :287): the point's trajectory ends here
+        if (W_->merr) {
+          err = kMaterial;
+          write_fail(err, iters, qnan());
+          break;
+        }
       }
       const double rl = (lane < n) ? sV[lane] : 0.0;
       const double rn = sqrt(warp_sum(rl * rl));
@@ -1153,9 +1183,9 @@ __global__ void k_material_batch(MatDev m, int64_t N, const double* eps, const d
 
 constexpr size_t kMaxDynSmem = 227 * 1024;
 
-template <int NT, int W, bool RES, bool MONO = false>
+template <int NT, int W, bool RES, bool MONO = false, bool GEN = false>
 void launch_inc_variant(const IncArgs& a, int num_sms, cudaStream_t s, size_t smem) {
-  auto kern = k_increment<NT, W, RES, MONO>;
+  auto kern = k_increment<NT, W, RES, MONO, GEN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaxDynSmem));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
@@ -1176,15 +1206,15 @@ bool resident_disabled() {
   return off;
 }
 
-template <int NT>
+template <int NT, bool GEN>
 void launch_inc_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
   constexpr int NP = 8 * NT;
   constexpr int WR = kwres_for(NT);
   const size_t res = IncLayout<NP, WR>::res_bytes(a.M.nchunks);
   if (res <= kMaxDynSmem && !resident_disabled())
-    launch_inc_variant<NT, WR, true>(a, num_sms, s, res);
+    launch_inc_variant<NT, WR, true, false, GEN>(a, num_sms, s, res);
   else
-    launch_inc_variant<NT, kw_for(NT), false>(a, num_sms, s, IncLayout<NP, kw_for(NT)>::bytes);
+    launch_inc_variant<NT, kw_for(NT), false, false, GEN>(a, num_sms, s, IncLayout<NP, kw_for(NT)>::bytes);
 }
 
 }  // namespace
@@ -1231,11 +1261,12 @@ void launch_increment_mono(const IncArgs& a, int num_sms, cudaStream_t s) {
 }
 
 void launch_increment(const IncArgs& a, int num_sms, cudaStream_t s) {
+  const bool gen = a.M.mat2.kind >= 2;  // power-law / creep history points
   switch (a.M.NP) {
-    case 8: launch_inc_nt<1>(a, num_sms, s); break;
-    case 16: launch_inc_nt<2>(a, num_sms, s); break;
-    case 24: launch_inc_nt<3>(a, num_sms, s); break;
-    case 32: launch_inc_nt<4>(a, num_sms, s); break;
+    case 8: gen ? launch_inc_nt<1, true>(a, num_sms, s) : launch_inc_nt<1, false>(a, num_sms, s); break;
+    case 16: gen ? launch_inc_nt<2, true>(a, num_sms, s) : launch_inc_nt<2, false>(a, num_sms, s); break;
+    case 24: gen ? launch_inc_nt<3, true>(a, num_sms, s) : launch_inc_nt<3, false>(a, num_sms, s); break;
+    case 32: gen ? launch_inc_nt<4, true>(a, num_sms, s) : launch_inc_nt<4, false>(a, num_sms, s); break;
     default: break;
   }
 }

@@ -132,6 +132,7 @@ void launch_increment_mono(const IncArgs& a, int num_sms, cudaStream_t s);
 void launch_mono_commit(const PointsDev& D, int NP, const double* mono, cudaStream_t s);
 bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s);
 bool launch_increment_big_other(const IncArgs& a, int num_sms, cudaStream_t s);  // NP not 64 / 128
+bool launch_increment_big_gen(const IncArgs& a, int num_sms, cudaStream_t s);    // power-law / creep models
 // one monolithic Newton iteration for every point, NP in the launch_increment_big set
 bool launch_increment_big_mono(const IncArgs& a, int num_sms, cudaStream_t s);
 size_t increment_big_smem(int NP);

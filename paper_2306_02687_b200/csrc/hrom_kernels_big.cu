@@ -604,7 +604,8 @@ __device__ unsigned long long g_big_prof[9];
   } while (0)
 #endif
 
-template <int NT, bool MONO = false>
+// GEN: iterative history material (power law / creep, general_return)
+template <int NT, bool MONO = false, bool GEN = false>
 __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(IncArgs A) {
 #ifdef FE2_BIG_PROF
   unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -726,6 +727,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   int np_last = 0;
   bool k_linear = false;
   double rn_pass = 0.0;  // |r| of the last pass
+  double dt_pass = A.M.mat2.dt;  // GEN creep: time of the sub-step being assembled (rve.hpp:466)
+  bool merr_pass = false;        // GEN: a return map of the last pass failed (ErrorCode::material)
 
   auto assembly_pass = [&](int64_t p, double E0, double E1, double E2) FE2_BIG_PASS_ATTR {
     double acc[MP][2];
@@ -737,6 +740,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
     for (int t = 0; t < NT; ++t) rr[t] = kae[t][0] = kae[t][1] = kae[t][2] = 0.0;
     double rm = 0.0, ka0 = 0.0, ka1 = 0.0, ka2 = 0.0;  // NT > 8: thread a < NP, mode a
     int np_tot = 0;
+    double merr = 0.0;  // GEN: return-map failures of this thread's points
     const bool cur = D.st[p].pad[0] != 0;
     double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
     if (sub == 0) {
@@ -758,12 +762,23 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       Corr cr{};
       if (sub == 0) {
         const Trial T = trial_state(mt, h0, h1, h2, h3, h4, e0, e1, e2);
-        plastic = (T.f > 0.0) && (q < M.K2);
-        if (plastic) cr = radial_return(mt, T);
+        double dlam_g = 0.0;
+        if constexpr (GEN) {
+          if (q < M.K2) {
+            const GenRet g = general_return(mt, T.ss, h4, dt_pass);
+            plastic = g.plastic;
+            dlam_g = g.dlam;
+            if (!g.ok) merr = 1.0;
+            if (plastic) cr = radial_return_gen(mt, T, g.dlam, g.kq);
+          }
+        } else {
+          plastic = (T.f > 0.0) && (q < M.K2);
+          if (plastic) cr = radial_return(mt, T);
+        }
         {  // candidate history (finish_return) into the non-committed buffer
           double n0 = h0, n1 = h1, n2 = h2, n3 = h3, n4 = h4;
           if (plastic) {
-            const double dlam = T.f * mt.inv_denom;
+            const double dlam = GEN ? dlam_g : T.f * mt.inv_denom;
             const double ce = 1.5 * dlam * (0.81649658092772603273 * T.inv_ns);
             n0 = h0 + ce * T.d0;
             n1 = h1 + ce * T.d1;
@@ -885,7 +900,9 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
     }
     // one CTA reduction for the nine plastic sums and the elastic Σ part
     // (its barriers also publish sK / sRp / sKaE)
-    double rs[12] = {c00, c01, c02, c11, c12, c22, ds0, ds1, ds2, 0.0, 0.0, 0.0};
+    constexpr int kRs = GEN ? 13 : 12;  // GEN: + the return-map failure count
+    double rs[kRs] = {c00, c01, c02, c11, c12, c22, ds0, ds1, ds2, 0.0, 0.0, 0.0};
+    if constexpr (GEN) rs[kRs - 1] = merr;
     if (tid < n) {
       const double* ke = M.KaEe + tid * 3;
       const double al = sAev[tid];
@@ -893,7 +910,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       rs[10] = ke[1] * al;
       rs[11] = ke[2] * al;
     }
-    block_sum_n<L::BW, 12>(rs, red);
+    block_sum_n<L::BW, kRs>(rs, red);
+    if constexpr (GEN) merr_pass = rs[kRs - 1] != 0.0;
     c00 = rs[0], c01 = rs[1], c02 = rs[2], c11 = rs[3], c12 = rs[4], c22 = rs[5];
     ds0 = rs[6], ds1 = rs[7], ds2 = rs[8];
     const double sa0 = rs[9], sa1 = rs[10], sa2 = rs[11];
@@ -968,7 +986,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   };
 
   const NewtonCfg& cfg = A.cfg;
-  constexpr int kSolver = 1 + 4;  // 1 + ErrorCode::solver
+  constexpr int kSolver = 1 + 4;    // 1 + ErrorCode::solver
+  constexpr int kMaterial = 1 + 3;  // 1 + ErrorCode::material
 
   // One monolithic Newton iteration of point p (the paper's scheme; same
   // algebra as k_increment<..., MONO>): α ← α_w − K⁻¹(r + K_aE ΔE)
@@ -1135,7 +1154,17 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       int mode = 0, it = 0, ls = 0, iters = 0, bis = 0, err = 0;
       double a = 1.0, rn_it = 0.0, best_rn = 0.0, best_a = 1.0, ref = 0.0, done = 0.0, frac = 1.0;
       while (true) {
+        if constexpr (GEN) dt_pass = mt.dt * (fmin(1.0, done + frac) - done);
         assembly_pass(p, E0, E1, E2);
+        if constexpr (GEN) {
+          // a failed return map throws out of micro_newton and run_trajectory
+          // (materials.hpp:244, :287): the point's trajectory ends here
+          if (merr_pass) {
+            err = kMaterial;
+            write_fail(err, iters, qnan());
+            break;
+          }
+        }
         const double rn = rn_pass;
         const double srn = sqrt(s0 * s0 + s1 * s1 + s2 * s2);
         int action = 0;  // 0 assemble again, 1 final commit, 2 sub-step commit, 3 failed
@@ -1314,33 +1343,36 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
   }
 }
 
-template <int NT, bool MONO = false>
-bool launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
+template <int NT, bool MONO = false, bool GEN = false>
+bool launch_big_nt_(const IncArgs& a, int num_sms, cudaStream_t s) {
   if (a.M.S != Big<NT>::S) return false;  // G2 rows must carry the padded strain-row stride
   const size_t smem = Big<NT>::bytes;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_increment_big<NT, MONO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    configured = true;
-  }
+  // per launch: the opt-in is per device context (a handle may live on any device) and cheap
+  cudaFuncSetAttribute(k_increment_big<NT, MONO, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment_big<NT, MONO>, Big<NT>::BT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment_big<NT, MONO, GEN>, Big<NT>::BT, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = static_cast<int64_t>(num_sms) * per_sm;
   if (a.dbg) grid = 1;
   else if (grid > a.D.P) grid = a.D.P;
   if (grid < 1) grid = 1;
-  k_increment_big<NT, MONO><<<static_cast<unsigned>(grid), Big<NT>::BT, smem, s>>>(a);
+  k_increment_big<NT, MONO, GEN><<<static_cast<unsigned>(grid), Big<NT>::BT, smem, s>>>(a);
   return true;
+}
+
+template <int NT, bool MONO = false>
+bool launch_big_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
+  return launch_big_nt_<NT, MONO, false>(a, num_sms, s);
 }
 
 }  // namespace
 
-#if !defined(FE2_BIG_MONO_TU) && !defined(FE2_BIG_OTHER_TU)
+#if !defined(FE2_BIG_MONO_TU) && !defined(FE2_BIG_OTHER_TU) && !defined(FE2_BIG_GEN_TU)
 // NP = 64 and 128 (BASELINE configs 3/4) here; 40, 48, 56, 80, 96, 112 in
-// hrom_kernels_big_other.cu
+// hrom_kernels_big_other.cu; power-law / creep models in hrom_kernels_big_gen.cu
 bool launch_increment_big(const IncArgs& a, int num_sms, cudaStream_t s) {
+  if (a.M.mat2.kind >= 2) return launch_increment_big_gen(a, num_sms, s);
   switch (a.M.NP) {
     case 64: return launch_big_nt<8>(a, num_sms, s);
     case 128: return launch_big_nt<16>(a, num_sms, s);
@@ -1371,6 +1403,21 @@ bool launch_increment_big_other(const IncArgs& a, int num_sms, cudaStream_t s) {
     case 80: return launch_big_nt<10>(a, num_sms, s);
     case 96: return launch_big_nt<12>(a, num_sms, s);
     case 112: return launch_big_nt<14>(a, num_sms, s);
+    default: return false;
+  }
+}
+
+#elif defined(FE2_BIG_GEN_TU)
+bool launch_increment_big_gen(const IncArgs& a, int num_sms, cudaStream_t s) {
+  switch (a.M.NP) {
+    case 40: return launch_big_nt_<5, false, true>(a, num_sms, s);
+    case 48: return launch_big_nt_<6, false, true>(a, num_sms, s);
+    case 56: return launch_big_nt_<7, false, true>(a, num_sms, s);
+    case 64: return launch_big_nt_<8, false, true>(a, num_sms, s);
+    case 80: return launch_big_nt_<10, false, true>(a, num_sms, s);
+    case 96: return launch_big_nt_<12, false, true>(a, num_sms, s);
+    case 112: return launch_big_nt_<14, false, true>(a, num_sms, s);
+    case 128: return launch_big_nt_<16, false, true>(a, num_sms, s);
     default: return false;
   }
 }

@@ -753,11 +753,8 @@ template <int NT>
 void launch_fs_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
   constexpr int NP = 8 * NT;
   const size_t smem = FsLayout<NP>::bytes;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_increment_fs<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    configured = true;
-  }
+  // per launch: the opt-in is per device context (a handle may live on any device) and cheap
+  cudaFuncSetAttribute(k_increment_fs<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_increment_fs<NT>, kFW * 32, smem);
   if (per_sm < 1) per_sm = 1;

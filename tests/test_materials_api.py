@@ -25,8 +25,10 @@ def test_invalid_parameters_rejected_before_device(bad):
     assert e.value.code == 1  # config
 
 
-def test_engine_rejects_iterative_materials_before_device():
+def test_finite_strain_engine_rejects_iterative_materials_before_device():
+    """The small-strain engine carries power law / creep (general_return); the
+    finite-strain (Biot) engine is J2-only and says so before touching a device."""
     m = F.HyperRomModel(8, 4, 20, 0)
     with pytest.raises(F.Fe2Error) as e:
-        F.HyperRomEngine(m.G, m.w, m.mat, [F.CreepParams(), F.ElasticParams(10.0, 0.3)], m.volume)
+        F.HyperRomEngine(m.G4, m.w, m.mat, [F.CreepParams(), F.ElasticParams(10.0, 0.3)], m.volume)
     assert e.value.code == 1
