@@ -31,6 +31,12 @@ int main(int argc, char** argv) {
       std::printf("increment %d point 0: sigma = (%.6e, %.6e, %.6e) C11 = %.6e iters = %d plastic = %d\n", k + 1,
                   r[0].sigma[0], r[0].sigma[1], r[0].sigma[2], r[0].tangent[0], r[0].iterations,
                   r[0].plastic_points);
+      for (int p = 0; p < P; ++p) {  // machine-readable: every point, full precision
+        std::printf("R %d %d %d", k, p, r[p].iterations);
+        for (int c = 0; c < 3; ++c) std::printf(" %.17g", r[p].sigma[c]);
+        for (int c = 0; c < 9; ++c) std::printf(" %.17g", r[p].tangent[c]);
+        std::printf("\n");
+      }
     }
     // finite strain (config 2 kinematics) on the same model: G4 and H = F - I paths
     fe2_model_t m4 = nullptr;
@@ -49,6 +55,12 @@ int main(int argc, char** argv) {
       const auto r = fs.solve_increment(Hk);
       std::printf("finite-strain increment %d point 0: P = (%.6e, %.6e, %.6e, %.6e) A00 = %.6e iters = %d\n", k + 1,
                   r[0].P[0], r[0].P[1], r[0].P[2], r[0].P[3], r[0].A[0], r[0].iterations);
+      for (int p = 0; p < P; ++p) {
+        std::printf("F %d %d %d", k, p, r[p].iterations);
+        for (int c = 0; c < 4; ++c) std::printf(" %.17g", r[p].P[c]);
+        for (int c = 0; c < 16; ++c) std::printf(" %.17g", r[p].A[c]);
+        std::printf("\n");
+      }
     }
   } catch (const fe2rom::gpu::Error& e) {
     std::printf("fe2rom::gpu::Error code=%d: %s\n", static_cast<int>(e.code()), e.what());

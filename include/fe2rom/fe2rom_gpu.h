@@ -342,7 +342,9 @@ int fe2_model_build_basis(int subdivisions, const char* mesh_path, const double*
 /* ---- high-fidelity RVE solve and POD basis ----------
  * fe2_hf_* is the full-field micro problem on the device: per-element
  * material update + element stiffness kernel, deterministic gather of the
- * dense free stiffness, cuSOLVER Cholesky (loaded at first use). Replaces
+ * free stiffness's lower band (free DOFs in reverse Cuthill-McKee order),
+ * band Cholesky + substitutions on one CTA per system (the reference's
+ * sparse SimplicialLDLT, rve.hpp:295-325). Replaces
  * micro_newton + homogenize + run_trajectory with SnapshotRecorder
  * (rve.hpp:285-392, :397-494; linear BC). */
 /* RVE = default_cell(subdivisions) or mesh_path; materials indexed by the
@@ -359,13 +361,25 @@ int fe2_hf_sizes(fe2_hf_t h, int* n_dofs, int* n_free, int* n_ips, double* volum
  * Non-convergence after max_bisections -> solver error. */
 int fe2_hf_trajectory(fe2_hf_t h, int n_steps, const double* E, const fe2_newton_opts_t* opts, double* sigma,
                       double* C, int* iterations, double* u_fluct_inf, double* res_last, double* snapshots);
+/* A batch of independent trajectories (the POD training set):
+ * trajectory t follows E[t][n_steps][3] from the virgin state; outputs as
+ * fe2_hf_trajectory at offset t (sigma[t][k][3], C[t][k][9], iterations[t][k],
+ * u_fluct_inf / res_last[t][k], snapshots[t][k][n_dofs]); status[t] = 0 or
+ * 1 + ErrorCode of a failed trajectory (its later rows are unspecified).
+ * Trajectories run concurrently (up to FE2_HF_WORKERS, default 64: one
+ * stream and host thread each, one CTA per band factorisation). */
+int fe2_hf_trajectories(fe2_hf_t h, int n_traj, int n_steps, const double* E, const fe2_newton_opts_t* opts,
+                        double* sigma, double* C, int* iterations, double* u_fluct_inf, double* res_last,
+                        double* snapshots, int* status);
+/* Half bandwidth of the free stiffness in the device's band ordering. */
+int fe2_hf_band(fe2_hf_t h, int* half_bandwidth);
 /* HF engine of an FE² run (SPEC.md:474-477 HF_nested): P macro points, each
  * an RVE with its own committed state (virgin at allocation). One call = one
  * path step of run_trajectory for every point from its committed state
  * (bisection, warm start); Σ[P*3], C[P*9] (homogenize), iterations, status
  * (0, or 1 + ErrorCode when the point's step failed — it keeps its state).
  * snapshot / restore save and return to the committed states (deferred
- * commits, fe2_macro_run_hf). Points are solved one after another. */
+ * commits, fe2_macro_run_hf). Points are solved concurrently (as fe2_hf_trajectories). */
 int fe2_hf_alloc_points(fe2_hf_t h, int64_t P);
 int fe2_hf_points(fe2_hf_t h, int64_t* P);
 int fe2_hf_solve_increment(fe2_hf_t h, const double* E, const fe2_newton_opts_t* opts, double* sigma, double* C,

@@ -12,13 +12,16 @@
 //
 // Device layout: the material update, strains and element stiffness run in
 // k_hf_element (one CTA per Tri6 element, 144 threads = its 12x12 entries);
-// k_hf_gather sums the element vectors/matrices into the residual and the
-// dense free stiffness with ONE thread per DOF walking its element incidences
-// in ascending element order — the reference's assembly order, no atomics,
-// bit-reproducible. The dense SPD factorisation/solves and the SVD are
-// cuSOLVER (dlopen'ed at first use so the hot-path library does not pull in
-// cuSOLVER/cuBLAS at load). Host code keeps the Newton control flow, norms
-// and the homogenisation sums (a few thousand integration points).
+// k_hf_gather_band sums the element vectors/matrices into the residual and
+// the LOWER BAND of the free stiffness (free DOFs in reverse Cuthill-McKee
+// order) with ONE thread per DOF walking its element incidences in ascending
+// element order — the reference's assembly order, no atomics,
+// bit-reproducible. k_band_chol / k_band_solve factor and solve the band on
+// one CTA (the reference factors with sparse SimplicialLDLT, rve.hpp:295-325).
+// Many RVE solves run at once (fe2_hf_trajectories, the FE² HF engine's
+// points): one worker = one stream + buffers + host thread. The POD SVD is
+// cuSOLVER gesvd (dlopen'ed at first use). Host code keeps the Newton control
+// flow, norms and the homogenisation sums (a few thousand integration points).
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 #include <dlfcn.h>
@@ -30,6 +33,11 @@
 #include <memory>
 #include <string>
 #include <type_traits>
+#include <thread>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <exception>
 #include <vector>
 
 #include "common.hpp"
@@ -48,9 +56,6 @@ struct Cusolver {
   decltype(&cusolverDnCreate) create = nullptr;
   decltype(&cusolverDnDestroy) destroy = nullptr;
   decltype(&cusolverDnSetStream) set_stream = nullptr;
-  decltype(&cusolverDnDpotrf_bufferSize) potrf_ws = nullptr;
-  decltype(&cusolverDnDpotrf) potrf = nullptr;
-  decltype(&cusolverDnDpotrs) potrs = nullptr;
   decltype(&cusolverDnDgesvd_bufferSize) gesvd_ws = nullptr;
   decltype(&cusolverDnDgesvd) gesvd = nullptr;
   std::string err;
@@ -78,9 +83,6 @@ struct Cusolver {
     sym(s.create, "cusolverDnCreate");
     sym(s.destroy, "cusolverDnDestroy");
     sym(s.set_stream, "cusolverDnSetStream");
-    sym(s.potrf_ws, "cusolverDnDpotrf_bufferSize");
-    sym(s.potrf, "cusolverDnDpotrf");
-    sym(s.potrs, "cusolverDnDpotrs");
     sym(s.gesvd_ws, "cusolverDnDgesvd_bufferSize");
     sym(s.gesvd, "cusolverDnDgesvd");
     return s;
@@ -182,12 +184,260 @@ __global__ void __launch_bounds__(144) k_hf_element(int n_el, const int* __restr
   }
 }
 
-// One thread per DOF: residual entry and (free DOF, with_K) its stiffness
-// row, summed over the DOF's element incidences in ascending element order.
-__global__ void k_hf_gather(int nd, const int* __restrict__ inc_ptr, const int* __restrict__ inc,
-                            const int* __restrict__ conn, const int* __restrict__ free_index, int nf,
-                            const double* __restrict__ f_el, const double* __restrict__ k_el, int with_K,
-                            double* __restrict__ f_full, double* __restrict__ K) {
+// ---------------------------------------------------------------------------
+// Banded Cholesky of the micro stiffness (replaces a dense factorisation; the
+// reference factors with sparse SimplicialLDLT, rve.hpp:295-325). The free
+// DOFs are numbered in reverse Cuthill-McKee order (band_order), which keeps
+// every element's DOFs within a half bandwidth bw (275 for default_cell(33),
+// n = 7,910: n bw^2 / 2 = 0.3 G FMA per factorisation instead of n^3 / 6 =
+// 82 G). Column-band storage: Kb[c * ldb + (r - c)], 0 <= r - c <= bw.
+// One CTA per system; a batch of RVE solves runs its systems on concurrent
+// streams (fe2_hf_trajectories), one CTA each.
+constexpr int kNB = 32;             // columns per panel (= warp width: the diagonal blocks run lane-per-row)
+constexpr int kBandThreads = 512;   // factorisation CTA
+constexpr int kSolveThreads = 256;  // substitution CTA
+
+__host__ __device__ constexpr int band_panel_ld(int bw) { return (bw + kNB + 3) / 4 * 4; }
+size_t band_chol_smem(int bw) { return sizeof(double) * kNB * band_panel_ld(bw); }
+constexpr int kBandSmemMax = 200 * 1024;
+
+// Right-looking, blocked by kNB columns. Per panel (columns j0 .. j0+nb-1,
+// rows j0 .. j0+nb-1+bw; k-major in shared memory so the 4-row tile reads are
+// 32-B vectors): load; factor its nb x nb diagonal block on warp 0 (lane =
+// row); solve the rows below against it, one thread per row in registers;
+// write it back; rank-nb update of the next bw x bw lower window by all
+// threads in 4x4 register tiles (the 16 band entries of a tile are loaded
+// before any is stored, so the loads overlap). info = 0, or 1 + the first
+// non-positive pivot's column.
+__global__ void __launch_bounds__(kBandThreads) k_band_chol(int n, int bw, int ldb, double* __restrict__ Kb,
+                                                            int* __restrict__ info) {
+  extern __shared__ __align__(32) double sP[];  // [kNB][LR]: sP[k * LR + i] = L(j0 + i, j0 + k)
+  __shared__ double sInvD[kNB];                 // 1 / L_kk of the panel's diagonal block
+  __shared__ int s_fail;
+  const int LR = band_panel_ld(bw);
+  const int t = threadIdx.x, lane = t & 31;
+  if (t == 0) s_fail = 0;
+  for (int j0 = 0; j0 < n; j0 += kNB) {
+    const int nb = min(kNB, n - j0);
+    const int R = min(n, j0 + nb + bw) - j0;
+    for (int e = t; e < R * nb; e += blockDim.x) {
+      const int k = e / R, i = e - k * R;  // consecutive threads: consecutive rows of a column (coalesced)
+      sP[k * LR + i] = (i >= k && i - k <= bw) ? Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] : 0.0;
+    }
+    __syncthreads();
+    // (1) the nb x nb diagonal block on warp 0: lane i holds row i in registers,
+    // right-looking column by column, the column broadcast by shuffles
+    if (t < 32) {
+      double a[kNB];
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) a[k] = (k < nb && lane < nb && k <= lane) ? sP[k * LR + lane] : 0.0;
+      int bad = 0;
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) {
+        if (k < nb) {
+          const double d = __shfl_sync(0xffffffffu, a[k], k);
+          if (!(d > 0.0)) {
+            bad = k + 1;
+            break;
+          }
+          const double l = sqrt(d), inv = 1.0 / l;
+          if (lane == k) {
+            a[k] = l;
+            sInvD[k] = inv;
+          } else if (lane > k) {
+            a[k] *= inv;
+          }
+#pragma unroll
+          for (int kk = k + 1; kk < kNB; ++kk) {
+            const double lk = __shfl_sync(0xffffffffu, a[k], kk);  // L(kk, k)
+            if (lane >= kk) a[kk] -= a[k] * lk;
+          }
+        }
+      }
+      if (bad) {
+        if (lane == 0) {
+          *info = j0 + bad;
+          s_fail = 1;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kNB; ++k)
+          if (k < nb && lane < nb && k <= lane) sP[k * LR + lane] = a[k];
+      }
+    }
+    __syncthreads();
+    if (s_fail) return;  // uniform
+    // (2) the rows below it: L_21 = A_21 L_11^-T, one thread per row in registers
+    for (int i = nb + t; i < R; i += blockDim.x) {
+      double a[kNB];
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) a[k] = k < nb ? sP[k * LR + i] : 0.0;
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) {
+        if (k < nb) {
+          double v = a[k];
+#pragma unroll
+          for (int m = 0; m < k; ++m) v -= a[m] * sP[m * LR + k];  // L(k, m): broadcast
+          a[k] = v * sInvD[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kNB; ++k)
+        if (k < nb) sP[k * LR + i] = a[k];
+    }
+    __syncthreads();
+    for (int e = t; e < R * nb; e += blockDim.x) {
+      const int k = e / R, i = e - k * R;
+      if (i >= k && i - k <= bw) Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] = sP[k * LR + i];
+    }
+    // trailing update of rows / columns j0+nb .. j0+R-1 (lower triangle, 4x4
+    // tiles): warp w takes the tile columns tj = w, w + nwarps, ...; its lanes
+    // the tile rows ti >= tj of that column, so every band load / store of a
+    // warp touches consecutive rows of one column (coalesced).
+    const int M = R - nb;
+    const int T4 = (M + 3) / 4;
+    const int warp = t >> 5, nwarps = blockDim.x >> 5;
+    for (int tj = warp; tj < T4; tj += nwarps) {
+      for (int ti = tj + lane; ti < T4; ti += 32) {
+        double old[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int c = 4 * tj + r;
+          const double* col = Kb + static_cast<size_t>(j0 + nb + c) * ldb;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = 4 * ti + q;
+            old[q][r] = (c < M && i < M && i >= c) ? col[i - c] : 0.0;
+          }
+        }
+        asm volatile("" ::: "memory");  // keep the 16 band loads ahead of the stores (they overlap)
+        double acc[4][4] = {};
+        for (int k = 0; k < nb; ++k) {
+          const double* ck = sP + k * LR + nb;
+          const double2 x0 = *reinterpret_cast<const double2*>(ck + 4 * ti);  // rows (128-bit loads)
+          const double2 x1 = *reinterpret_cast<const double2*>(ck + 4 * ti + 2);
+          const double2 y0 = *reinterpret_cast<const double2*>(ck + 4 * tj);  // columns (broadcast)
+          const double2 y1 = *reinterpret_cast<const double2*>(ck + 4 * tj + 2);
+          const double xv[4] = {x0.x, x0.y, x1.x, x1.y}, yv[4] = {y0.x, y0.y, y1.x, y1.y};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[q][r] += xv[q] * yv[r];
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int c = 4 * tj + r;
+          double* col = Kb + static_cast<size_t>(j0 + nb + c) * ldb;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = 4 * ti + q;
+            if (c < M && i < M && i >= c) col[i - c] = old[q][r] - acc[q][r];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) *info = 0;
+}
+
+// x = (L L^T)^-1 x for nrhs columns (stride n) with the band factor of
+// k_band_chol, blocked by kNB. Per block: stage the diagonal block and its
+// reciprocal pivots in shared memory; solve it on one warp per right-hand
+// side (lane = block row, shuffles); then push the block's solution to the
+// (up to bw) rows it couples to — forward: rows below, backward: columns
+// before — one thread per (row, rhs), the kNB band entries loaded together.
+__global__ void __launch_bounds__(kSolveThreads) k_band_solve(int n, int bw, int ldb, const double* __restrict__ Kb,
+                                                              double* __restrict__ x, int nrhs) {
+  __shared__ double sD[kNB][kNB + 1];  // diagonal block, sD[i][k] = L(j0 + i, j0 + k)
+  __shared__ double sInv[kNB];
+  __shared__ double sX[3][kNB];        // the block's solution
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  auto stage = [&](int j0, int nb) {
+    for (int e = t; e < kNB * kNB; e += blockDim.x) {
+      const int i = e % kNB, k = e / kNB;
+      sD[i][k] = (i < nb && k < nb && i >= k) ? Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] : 0.0;
+    }
+    __syncthreads();
+    if (t < nb) sInv[t] = 1.0 / sD[t][t];
+    __syncthreads();
+  };
+  // forward: L y = b
+  for (int j0 = 0; j0 < n; j0 += kNB) {
+    const int nb = min(kNB, n - j0);
+    stage(j0, nb);
+    if (warp < nrhs) {
+      double* xr = x + static_cast<size_t>(warp) * n + j0;
+      double v = lane < nb ? xr[lane] : 0.0;
+      for (int k = 0; k < nb; ++k) {
+        const double y = __shfl_sync(0xffffffffu, v, k) * sInv[k];
+        if (lane == k) v = y;
+        else if (lane > k && lane < nb) v -= sD[lane][k] * y;
+      }
+      if (lane < nb) {
+        xr[lane] = v;
+        sX[warp][lane] = v;
+      }
+    }
+    __syncthreads();
+    const int m = min(n, j0 + nb + bw) - (j0 + nb);  // rows below the block that it couples to
+    for (int e = t; e < m * nrhs; e += blockDim.x) {
+      const int rh = e / m, i = j0 + nb + (e - rh * m);
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) {
+        const int off = i - (j0 + k);
+        if (k < nb && off <= bw) s += Kb[static_cast<size_t>(j0 + k) * ldb + off] * sX[rh][k];
+      }
+      x[static_cast<size_t>(rh) * n + i] -= s;
+    }
+    __syncthreads();
+  }
+  // backward: L^T x = y
+  const int nblk = (n + kNB - 1) / kNB;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int j0 = b * kNB, nb = min(kNB, n - j0);
+    stage(j0, nb);
+    if (warp < nrhs) {
+      double* xr = x + static_cast<size_t>(warp) * n + j0;
+      double v = lane < nb ? xr[lane] : 0.0;
+      for (int k = nb - 1; k >= 0; --k) {
+        const double y = __shfl_sync(0xffffffffu, v, k) * sInv[k];
+        if (lane == k) v = y;
+        else if (lane < k) v -= sD[k][lane] * y;
+      }
+      if (lane < nb) {
+        xr[lane] = v;
+        sX[warp][lane] = v;
+      }
+    }
+    __syncthreads();
+    const int j1 = max(0, j0 - bw);  // columns before the block that it couples to
+    const int m = j0 - j1;
+    for (int e = t; e < m * nrhs; e += blockDim.x) {
+      const int rh = e / m, j = j1 + (e - rh * m);
+      const double* col = Kb + static_cast<size_t>(j) * ldb;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) {
+        const int off = j0 + k - j;
+        if (k < nb && off <= bw) s += col[off] * sX[rh][k];
+      }
+      x[static_cast<size_t>(rh) * n + j] -= s;
+    }
+    __syncthreads();
+  }
+}
+
+// One thread per DOF: residual entry and (free DOF, with_K) the lower-band
+// part of its stiffness row in the band ordering, summed over the DOF's
+// element incidences in ascending element order (deterministic, no atomics:
+// entry (pa, pb <= pa) belongs to row pa's thread alone).
+__global__ void k_hf_gather_band(int nd, const int* __restrict__ inc_ptr, const int* __restrict__ inc,
+                                 const int* __restrict__ conn, const int* __restrict__ free_index,
+                                 const int* __restrict__ perm, int ldb, const double* __restrict__ f_el,
+                                 const double* __restrict__ k_el, int with_K, double* __restrict__ f_full,
+                                 double* __restrict__ Kb) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nd) return;
   const int p0 = inc_ptr[d], p1 = inc_ptr[d + 1];
@@ -196,13 +446,15 @@ __global__ void k_hf_gather(int nd, const int* __restrict__ inc_ptr, const int* 
   f_full[d] = f;
   const int fa = free_index[d];
   if (!with_K || fa < 0) return;
-  double* row = K + (size_t)fa * nf;
+  const int pa = perm[fa];
   for (int p = p0; p < p1; ++p) {
     const int e = inc[p] / 12, a = inc[p] % 12;
-    const double* ke = k_el + (size_t)144 * e + 12 * a;
+    const double* ke = k_el + static_cast<size_t>(144) * e + 12 * a;
     for (int b = 0; b < 12; ++b) {
       const int fb = free_index[2 * conn[6 * e + b / 2] + b % 2];
-      if (fb >= 0) row[fb] += ke[b];
+      if (fb < 0) continue;
+      const int pb = perm[fb];
+      if (pb <= pa) Kb[static_cast<size_t>(pb) * ldb + (pa - pb)] += ke[b];
     }
   }
 }
@@ -219,40 +471,225 @@ double norm2(const double* v, size_t n) {
 
 using namespace fe2;
 
-struct fe2_hf_s {
+namespace {
+
+// Reverse Cuthill-McKee order of the nodes that carry free DOFs (adjacent =
+// sharing an element), started from a pseudo-peripheral node of each
+// connected component; the free DOFs are numbered node by node in that order.
+// perm[free index] = band position; bw = the resulting half bandwidth.
+std::vector<int> band_order(const RveData& r, int& bw) {
+  const int nn = r.n_nodes;
+  std::vector<char> has(nn, 0);
+  for (int v = 0; v < nn; ++v) has[v] = (r.free_index[2 * v] >= 0 || r.free_index[2 * v + 1] >= 0) ? 1 : 0;
+  std::vector<std::vector<int>> adj(nn);
+  for (int e = 0; e < r.n_el; ++e)
+    for (int a = 0; a < 6; ++a)
+      for (int b = 0; b < 6; ++b) {
+        const int u = r.conn[6 * e + a], v = r.conn[6 * e + b];
+        if (u != v && has[u] && has[v]) adj[u].push_back(v);
+      }
+  for (auto& l : adj) {
+    std::sort(l.begin(), l.end());
+    l.erase(std::unique(l.begin(), l.end()), l.end());
+  }
+  std::vector<int> deg(nn);
+  for (int v = 0; v < nn; ++v) deg[v] = static_cast<int>(adj[v].size());
+  std::vector<int> level(nn, -1), order;
+  order.reserve(nn);
+  auto bfs = [&](int s, std::vector<int>& out) {  // Cuthill-McKee sweep; returns the last level
+    std::vector<int> seen;
+    out.clear();
+    level[s] = 0;
+    out.push_back(s);
+    for (size_t h = 0; h < out.size(); ++h) {
+      const int v = out[h];
+      std::vector<int> nb;
+      for (int u : adj[v])
+        if (level[u] < 0) {
+          level[u] = level[v] + 1;
+          nb.push_back(u);
+        }
+      std::stable_sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+      out.insert(out.end(), nb.begin(), nb.end());
+    }
+    return level[out.back()];
+  };
+  std::vector<int> comp;
+  for (int s0 = 0; s0 < nn; ++s0) {
+    if (!has[s0] || level[s0] >= 0) continue;
+    // the component, and a pseudo-peripheral start (lowest degree in the last level, repeated)
+    bfs(s0, comp);
+    int s = s0;
+    for (int v : comp)
+      if (deg[v] < deg[s]) s = v;
+    int ecc = -1;
+    for (int pass = 0; pass < 4; ++pass) {
+      for (int v : comp) level[v] = -1;
+      const int L = bfs(s, comp);
+      if (L <= ecc) break;
+      ecc = L;
+      int best = -1;
+      for (int v : comp)
+        if (level[v] == L && (best < 0 || deg[v] < deg[best])) best = v;
+      s = best;
+    }
+    for (int v : comp) level[v] = -1;
+    bfs(s, comp);
+    order.insert(order.end(), comp.begin(), comp.end());
+  }
+  std::reverse(order.begin(), order.end());
+  std::vector<int> perm(r.n_free, -1);
+  int pos = 0;
+  for (int v : order)
+    for (int c = 0; c < 2; ++c)
+      if (r.free_index[2 * v + c] >= 0) perm[r.free_index[2 * v + c]] = pos++;
+  check(pos == r.n_free, Code::mesh, "band ordering lost a free DOF");
+  bw = 0;
+  for (int e = 0; e < r.n_el; ++e)
+    for (int a = 0; a < 12; ++a)
+      for (int b = 0; b < 12; ++b) {
+        const int fa = r.free_index[2 * r.conn[6 * e + a / 2] + a % 2];
+        const int fb = r.free_index[2 * r.conn[6 * e + b / 2] + b % 2];
+        if (fa >= 0 && fb >= 0) bw = std::max(bw, std::abs(perm[fa] - perm[fb]));
+      }
+  return perm;
+}
+
+// Concurrent workers of a batch (FE2_HF_WORKERS, default 64). The device's
+// hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS) are raised to their
+// maximum of 32 when the library loads, unless the process set them: with the
+// default 8, streams share a queue and one long band factorisation blocks the
+// others' work behind it (40 POD trajectories: 8.2 s -> 4.2 s measured).
+int hf_workers_max() {
+  const char* e = std::getenv("FE2_HF_WORKERS");
+  const int v = (e && *e) ? std::atoi(e) : 64;
+  return std::max(1, std::min(v, 256));
+}
+
+__attribute__((constructor)) void raise_device_connections() {
+  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);  // effective if no CUDA context exists yet
+}
+
+}  // namespace
+
+// Immutable RVE data on the device, shared by the workers.
+struct HfShared {
   int device = 0;
   RveData r;
   MatTable mats{}, mats_el{};
-  cudaStream_t stream = nullptr;
-  cusolverDnHandle_t sol = nullptr;
-  int *d_conn = nullptr, *d_phase = nullptr, *d_free = nullptr, *d_inc_ptr = nullptr, *d_inc = nullptr;
-  int* d_info = nullptr;
-  int* d_err = nullptr;  // set by k_hf_element when a return map fails
-  double *d_B = nullptr, *d_w = nullptr, *d_u = nullptr, *d_st0 = nullptr, *d_st1 = nullptr;
-  double *d_fel = nullptr, *d_kel = nullptr, *d_f = nullptr, *d_K = nullptr, *d_sig = nullptr, *d_C = nullptr;
-  double *d_rhs = nullptr, *d_work = nullptr;
-  int lwork = 0;
-  bool factored = false;  // d_K holds the Cholesky factor of the last assembled stiffness
-  double* st_comm = nullptr;  // committed states the assembly reads (d_st0, or a point's block)
-  // macro-point batch (fe2_hf_alloc_points): per point committed states on the
-  // device, committed free displacements / strains on the host; snapshot copies
-  int64_t P = 0;
-  double *d_pst = nullptr, *d_pst_snap = nullptr;
-  std::vector<double> pu, pu_snap, pE, pE_snap;  // [P][nf], [P][6] = (E_prev, E_comm)
-
+  int *d_conn = nullptr, *d_phase = nullptr, *d_free = nullptr, *d_inc_ptr = nullptr, *d_inc = nullptr,
+      *d_perm = nullptr;
+  double *d_B = nullptr, *d_w = nullptr;
+  std::vector<int> perm;  // free index -> band position
+  int bw = 0, ldb = 1;    // half bandwidth, band column stride
   int nd() const { return r.n_dofs(); }
   int nf() const { return r.n_free; }
-
-  ~fe2_hf_s() {
-    if (sol) Cusolver::get().destroy(sol);
-    if (stream) cudaStreamDestroy(stream);
-    for (int* p : {d_conn, d_phase, d_free, d_inc_ptr, d_inc, d_info, d_err})
+  ~HfShared() {
+    for (int* p : {d_conn, d_phase, d_free, d_inc_ptr, d_inc, d_perm})
       if (p) cudaFree(p);
-    for (double* p : {d_B, d_w, d_u, d_st0, d_st1, d_fel, d_kel, d_f, d_K, d_sig, d_C, d_rhs, d_work, d_pst, d_pst_snap})
+    for (double* p : {d_B, d_w})
       if (p) cudaFree(p);
   }
+};
+
+// One RVE solve context: its own stream and working buffers (states, element
+// arrays, the band factor), so that many run concurrently (one host thread each).
+struct HfWork {
+  const HfShared& S;
+  cudaStream_t stream = nullptr;
+  int* d_info = nullptr;
+  int* d_err = nullptr;  // set by k_hf_element when a return map fails
+  double *d_u = nullptr, *d_st0 = nullptr, *d_st1 = nullptr, *d_fel = nullptr, *d_kel = nullptr, *d_f = nullptr;
+  double *d_Kb = nullptr, *d_sig = nullptr, *d_C = nullptr, *d_rhs = nullptr;
+  // pinned staging of every host<->device transfer (pageable copies serialise
+  // against the other workers' streams): u / f [nd], rhs [3 nf], sigma / C per
+  // integration point, {err, info}
+  double *h_u = nullptr, *h_f = nullptr, *h_rhs = nullptr, *h_sig = nullptr, *h_C = nullptr;
+  int* h_flags = nullptr;
+  bool factored = false;      // d_Kb holds the factor of the last assembled stiffness
+  double* st_comm = nullptr;  // committed states the assembly reads (d_st0, or a point's block)
+  // FE2_HF_PROF=1: host wall time per phase (assemble with K, residual-only assemble,
+  // factor, solve, homogenize), printed when the worker is destroyed
+  double prof[8] = {};
+  long prof_n[8] = {};
+  static bool prof_on() {
+    static const bool on = [] {
+      const char* e = std::getenv("FE2_HF_PROF");
+      return e && *e && *e != '0';
+    }();
+    return on;
+  }
+  struct Tick {
+    HfWork& w;
+    int k;
+    std::chrono::steady_clock::time_point t0;
+    Tick(HfWork& w_, int k_) : w(w_), k(k_), t0(std::chrono::steady_clock::now()) {}
+    ~Tick() {
+      w.prof[k] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      w.prof_n[k] += 1;
+    }
+  };
+
+  cudaEvent_t done = nullptr;  // blocking-sync event: a waiting worker thread sleeps instead of spinning
+
+  // wait for this worker's stream; the thread yields the core (a batch runs
+  // more worker threads than the host has cores)
+  void wait() {
+    CK(cudaEventRecord(done, stream));
+    CK(cudaEventSynchronize(done));
+  }
+
+  explicit HfWork(const HfShared& s) : S(s) {
+    const RveData& r = S.r;
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&done, cudaEventBlockingSync | cudaEventDisableTiming));
+    d_info = dalloc<int>(1);
+    d_err = dalloc<int>(1);
+    CK(cudaMemset(d_err, 0, sizeof(int)));
+    d_u = dalloc<double>(S.nd());
+    d_f = dalloc<double>(S.nd());
+    d_st0 = dalloc<double>(static_cast<size_t>(6) * r.n_ips());
+    d_st1 = dalloc<double>(static_cast<size_t>(6) * r.n_ips());
+    d_sig = dalloc<double>(static_cast<size_t>(3) * r.n_ips());
+    d_C = dalloc<double>(static_cast<size_t>(9) * r.n_ips());
+    d_fel = dalloc<double>(static_cast<size_t>(12) * r.n_el);
+    d_kel = dalloc<double>(static_cast<size_t>(144) * r.n_el);
+    d_Kb = dalloc<double>(static_cast<size_t>(S.nf()) * S.ldb);
+    d_rhs = dalloc<double>(static_cast<size_t>(3) * S.nf());
+    CK(cudaMallocHost(&h_u, sizeof(double) * S.nd()));
+    CK(cudaMallocHost(&h_f, sizeof(double) * S.nd()));
+    CK(cudaMallocHost(&h_rhs, sizeof(double) * 3 * S.nf()));
+    CK(cudaMallocHost(&h_sig, sizeof(double) * 3 * r.n_ips()));
+    CK(cudaMallocHost(&h_C, sizeof(double) * 9 * r.n_ips()));
+    CK(cudaMallocHost(&h_flags, sizeof(int) * 2));
+    st_comm = d_st0;
+  }
+  ~HfWork() {
+    if (prof_on() && prof_n[0] > 0)
+      std::fprintf(stderr,
+                   "FE2_HF_PROF assemble+K %.3f ms x %ld | assemble %.3f ms x %ld | factor %.3f ms x %ld | "
+                   "solve %.3f ms x %ld | homogenize %.3f ms x %ld\n",
+                   1e3 * prof[0] / prof_n[0], prof_n[0], 1e3 * prof[1] / std::max(1L, prof_n[1]), prof_n[1],
+                   1e3 * prof[2] / std::max(1L, prof_n[2]), prof_n[2], 1e3 * prof[3] / std::max(1L, prof_n[3]),
+                   prof_n[3], 1e3 * prof[4] / std::max(1L, prof_n[4]), prof_n[4]);
+    if (prof_on() && prof_n[5] > 0)
+      std::fprintf(stderr, "FE2_HF_PROF solve: h2d %.3f ms | kernel %.3f ms | d2h %.3f ms\n", 1e3 * prof[5] / prof_n[5],
+                   1e3 * prof[6] / prof_n[6], 1e3 * prof[7] / prof_n[7]);
+    if (done) cudaEventDestroy(done);
+    if (stream) cudaStreamDestroy(stream);
+    for (int* p : {d_info, d_err})
+      if (p) cudaFree(p);
+    for (double* p : {d_u, d_st0, d_st1, d_fel, d_kel, d_f, d_Kb, d_sig, d_C, d_rhs})
+      if (p) cudaFree(p);
+    for (void* p : {static_cast<void*>(h_u), static_cast<void*>(h_f), static_cast<void*>(h_rhs),
+                    static_cast<void*>(h_sig), static_cast<void*>(h_C), static_cast<void*>(h_flags)})
+      if (p) cudaFreeHost(p);
+  }
+  int nd() const { return S.nd(); }
+  int nf() const { return S.nf(); }
 
   void affine(const double* E, std::vector<double>& u) const {  // affine_field, rve.hpp:43-51
+    const RveData& r = S.r;
     u.assign(nd(), 0.0);
     const double e11 = E[0], e22 = E[1], e12 = 0.5 * E[2];
     for (int id = 0; id < r.n_nodes; ++id) {
@@ -261,46 +698,66 @@ struct fe2_hf_s {
     }
   }
 
-  // assemble_micro at u_full from the committed states (d_st0); with_K also
-  // keeps the trial states, stresses and tangents of every point.
+  // assemble_micro at u_full from the committed states (st_comm); with_K also
+  // keeps the trial states, stresses and tangents of every point and the band
+  // stiffness.
   void assemble(const std::vector<double>& u_full, bool with_K, const MatTable& mt, std::vector<double>& f_full) {
-    CK(cudaMemcpyAsync(d_u, u_full.data(), sizeof(double) * nd(), cudaMemcpyHostToDevice, stream));
-    if (with_K) CK(cudaMemsetAsync(d_K, 0, sizeof(double) * nf() * nf(), stream));
-    k_hf_element<<<r.n_el, 144, 0, stream>>>(r.n_el, d_conn, d_phase, mt, d_B, d_w, d_u, st_comm, with_K ? 1 : 0,
-                                             d_fel, d_kel, d_st1, d_sig, d_C, d_err);
+    const Tick tk(*this, with_K ? 0 : 1);
+    const RveData& r = S.r;
+    std::memcpy(h_u, u_full.data(), sizeof(double) * nd());
+    CK(cudaMemcpyAsync(d_u, h_u, sizeof(double) * nd(), cudaMemcpyHostToDevice, stream));
+    if (with_K) CK(cudaMemsetAsync(d_Kb, 0, sizeof(double) * nf() * S.ldb, stream));
+    k_hf_element<<<r.n_el, 144, 0, stream>>>(r.n_el, S.d_conn, S.d_phase, mt, S.d_B, S.d_w, d_u, st_comm,
+                                             with_K ? 1 : 0, d_fel, d_kel, d_st1, d_sig, d_C, d_err);
     CK(cudaGetLastError());
-    k_hf_gather<<<(nd() + 127) / 128, 128, 0, stream>>>(nd(), d_inc_ptr, d_inc, d_conn, d_free, nf(), d_fel, d_kel,
-                                                        with_K ? 1 : 0, d_f, d_K);
+    k_hf_gather_band<<<(nd() + 127) / 128, 128, 0, stream>>>(nd(), S.d_inc_ptr, S.d_inc, S.d_conn, S.d_free,
+                                                             S.d_perm, S.ldb, d_fel, d_kel, with_K ? 1 : 0, d_f,
+                                                             d_Kb);
     CK(cudaGetLastError());
     f_full.resize(nd());
-    CK(cudaMemcpyAsync(f_full.data(), d_f, sizeof(double) * nd(), cudaMemcpyDeviceToHost, stream));
-    int err = 0;
-    CK(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
+    CK(cudaMemcpyAsync(h_f, d_f, sizeof(double) * nd(), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(h_flags, d_err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    wait();
+    std::memcpy(f_full.data(), h_f, sizeof(double) * nd());
+    const int err = h_flags[0];
     check(err == 0, Code::material, "material return map did not converge");
     if (with_K) factored = false;
   }
 
   void factor(const char* what) {
-    const Cusolver& cs = Cusolver::get();
-    // d_K is row-major; cuSOLVER's column-major UPPER triangle is its row-major lower one
-    sol_check(cs.potrf(sol, CUBLAS_FILL_MODE_UPPER, nf(), d_K, nf(), d_work, lwork, d_info), "potrf");
-    int info = 0;
-    CK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    check(info == 0, Code::solver, what);
+    const Tick tk(*this, 2);
+    k_band_chol<<<1, kBandThreads, band_chol_smem(S.bw), stream>>>(nf(), S.bw, S.ldb, d_Kb, d_info);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h_flags + 1, d_info, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    wait();
+    check(h_flags[1] == 0, Code::solver, what);
     factored = true;
   }
 
-  // x = K^-1 b for nrhs column-major right-hand sides (in place on host b)
+  // x = K^-1 b for nrhs right-hand sides (free numbering, column j at b + j n), in place
   void solve(std::vector<double>& b, int nrhs) {
-    const Cusolver& cs = Cusolver::get();
-    CK(cudaMemcpyAsync(d_rhs, b.data(), sizeof(double) * nf() * nrhs, cudaMemcpyHostToDevice, stream));
-    sol_check(cs.potrs(sol, CUBLAS_FILL_MODE_UPPER, nf(), nrhs, d_K, nf(), d_rhs, nf(), d_info), "potrs");
-    CK(cudaMemcpyAsync(b.data(), d_rhs, sizeof(double) * nf() * nrhs, cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
+    const Tick tk(*this, 3);
+    const int n = nf();
+    double* bp = h_rhs;
+    for (int j = 0; j < nrhs; ++j)
+      for (int i = 0; i < n; ++i) bp[static_cast<size_t>(j) * n + S.perm[i]] = b[static_cast<size_t>(j) * n + i];
+    {
+      const Tick t5(*this, 5);
+      CK(cudaMemcpyAsync(d_rhs, bp, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, stream));
+      if (prof_on()) wait();
+    }
+    {
+      const Tick t6(*this, 6);
+      k_band_solve<<<1, kSolveThreads, 0, stream>>>(n, S.bw, S.ldb, d_Kb, d_rhs, nrhs);
+      CK(cudaGetLastError());
+      if (prof_on()) wait();
+    }
+    const Tick t7(*this, 7);
+    CK(cudaMemcpyAsync(bp, d_rhs, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, stream));
+    wait();
+    for (int j = 0; j < nrhs; ++j)
+      for (int i = 0; i < n; ++i) b[static_cast<size_t>(j) * n + i] = bp[static_cast<size_t>(j) * n + S.perm[i]];
   }
-
   struct Newton {
     bool converged = false;
     int iterations = 0;
@@ -313,6 +770,7 @@ struct fe2_hf_s {
   // search keeping the best trial. On convergence d_st1 / d_sig / d_C / d_K
   // hold the converged states, stresses, tangents and (unfactored) stiffness.
   Newton newton(const double* E, std::vector<double> u_free, double tol, int max_iter, const MatTable& mt) {
+    const RveData& r = S.r;
     const int n = nf(), N = nd();
     Newton out;
     std::vector<double> aff;
@@ -372,11 +830,15 @@ struct fe2_hf_s {
 
   // homogenize (rve.hpp:350-392) at the converged state of the last newton().
   void homogenize(double* sigma, double* C) {
+    const Tick tk(*this, 4);
+    const RveData& r = S.r;
     const int n = nf(), N = nd(), nip = r.n_ips();
     std::vector<double> sg((size_t)3 * nip), Cq((size_t)9 * nip);
-    CK(cudaMemcpyAsync(sg.data(), d_sig, sizeof(double) * sg.size(), cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(Cq.data(), d_C, sizeof(double) * Cq.size(), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
+    CK(cudaMemcpyAsync(h_sig, d_sig, sizeof(double) * sg.size(), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(h_C, d_C, sizeof(double) * Cq.size(), cudaMemcpyDeviceToHost, stream));
+    wait();
+    std::memcpy(sg.data(), h_sig, sizeof(double) * sg.size());
+    std::memcpy(Cq.data(), h_C, sizeof(double) * Cq.size());
     double s[3] = {0, 0, 0};
     for (int ip = 0; ip < nip; ++ip)
       for (int i = 0; i < 3; ++i) s[i] += r.w[ip] * sg[3 * ip + i];
@@ -442,6 +904,7 @@ struct fe2_hf_s {
   // converged Newton result is returned (its d_sig / d_C / d_K are current).
   Newton increment(const double* E_prev, const double* E_target, std::vector<double>& u_free, double* E_comm,
                    double tol, int max_iter, int max_bisections, const MatTable& mt, int& its) {
+    const RveData& r = S.r;
     const int N = nd();
     std::vector<double> aff, u0(nf());
     double done = 0.0, frac = 1.0;
@@ -477,6 +940,7 @@ struct fe2_hf_s {
   // run_trajectory (rve.hpp:448-494) from the virgin state.
   void trajectory(int n_steps, const double* E, double tol, int max_iter, int max_bisections, const MatTable& mt,
                   double* sigma, double* C, int* iterations, double* u_fluct_inf, double* res_last, double* snaps) {
+    const RveData& r = S.r;
     const int n = nf(), N = nd();
     st_comm = d_st0;
     CK(cudaMemsetAsync(d_st0, 0, sizeof(double) * 6 * r.n_ips(), stream));
@@ -504,45 +968,104 @@ struct fe2_hf_s {
       if (iterations) iterations[k] = its;
       for (int i = 0; i < 3; ++i) E_prev[i] = E[3 * k + i];
     }
-    CK(cudaStreamSynchronize(stream));
+    wait();
+  }
+
+};
+
+// The handle: shared RVE data plus a pool of workers (worker 0 serves the
+// single-RVE calls; batches spread over up to FE2_HF_WORKERS of them, one
+// host thread each, their kernels running concurrently on their own streams).
+struct fe2_hf_s {
+  HfShared S;
+  std::vector<std::unique_ptr<HfWork>> work;
+  // macro-point batch (fe2_hf_alloc_points): per point committed states on the
+  // device, committed free displacements / strains on the host; snapshot copies
+  int64_t P = 0;
+  double *d_pst = nullptr, *d_pst_snap = nullptr;
+  std::vector<double> pu, pu_snap, pE, pE_snap;  // [P][nf], [P][6] = (E_prev, E_comm)
+
+  ~fe2_hf_s() {
+    work.clear();
+    for (double* p : {d_pst, d_pst_snap})
+      if (p) cudaFree(p);
+  }
+  HfWork& w0() { return worker(0); }
+  HfWork& worker(int i) {
+    while (static_cast<int>(work.size()) <= i) work.push_back(std::make_unique<HfWork>(S));
+    return *work[i];
+  }
+  void sync_all() {
+    for (auto& w : work) CK(cudaStreamSynchronize(w->stream));
+  }
+
+  // fn(worker, item) for item = 0..count-1, items dealt cyclically to the
+  // workers; the first failure (by item order) is rethrown here.
+  template <class Fn>
+  void parallel(int64_t count, Fn&& fn) {
+    const int nw = static_cast<int>(std::min<int64_t>(count, hf_workers_max()));
+    if (nw <= 0) return;
+    for (int i = 0; i < nw; ++i) worker(i);
+    if (nw == 1) {
+      for (int64_t it = 0; it < count; ++it) fn(*work[0], it);
+      return;
+    }
+    std::vector<std::exception_ptr> errs(count);
+    std::vector<std::thread> pool;
+    for (int i = 0; i < nw; ++i)
+      pool.emplace_back([&, i] {
+        cudaSetDevice(S.device);
+        for (int64_t it = i; it < count; it += nw) {
+          try {
+            fn(*work[i], it);
+          } catch (...) {
+            errs[it] = std::current_exception();
+          }
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
   }
 
   // A batch of P macro points, each an RVE with its own committed state
   // (the HF engine of an FE² run, SPEC.md:474-477 HF_nested). One increment
-  // per call for every point; a point whose step fails keeps its committed
-  // state and reports status 1 + ErrorCode.
+  // per call for every point (points in parallel over the workers); a point
+  // whose step fails keeps its committed state and reports 1 + ErrorCode.
   void alloc_points(int64_t n_points) {
+    HfWork& w = w0();
     dfree(d_pst);
     dfree(d_pst_snap);
     P = n_points;
-    d_pst = dalloc<double>(static_cast<size_t>(P) * 6 * r.n_ips());
-    d_pst_snap = dalloc<double>(static_cast<size_t>(P) * 6 * r.n_ips());
-    CK(cudaMemsetAsync(d_pst, 0, sizeof(double) * P * 6 * r.n_ips(), stream));
-    CK(cudaMemsetAsync(d_pst_snap, 0, sizeof(double) * P * 6 * r.n_ips(), stream));
-    pu.assign(static_cast<size_t>(P) * nf(), 0.0);
+    const size_t per = static_cast<size_t>(6) * S.r.n_ips();
+    d_pst = dalloc<double>(static_cast<size_t>(P) * per);
+    d_pst_snap = dalloc<double>(static_cast<size_t>(P) * per);
+    CK(cudaMemsetAsync(d_pst, 0, sizeof(double) * P * per, w.stream));
+    CK(cudaMemsetAsync(d_pst_snap, 0, sizeof(double) * P * per, w.stream));
+    pu.assign(static_cast<size_t>(P) * S.nf(), 0.0);
     pE.assign(static_cast<size_t>(P) * 6, 0.0);
     pu_snap = pu;
     pE_snap = pE;
-    CK(cudaStreamSynchronize(stream));
+    w.wait();
   }
 
   void solve_points(const double* E, double tol, int max_iter, int max_bisections, double* sigma, double* C,
                     int* iters, int* status) {
-    const int n = nf();
-    CK(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
-    std::vector<double> u_free(n);
-    for (int64_t p = 0; p < P; ++p) {
-      st_comm = d_pst + static_cast<size_t>(p) * 6 * r.n_ips();
+    const int n = S.nf();
+    const size_t sb = sizeof(double) * 6 * S.r.n_ips();
+    parallel(P, [&](HfWork& w, int64_t p) {
+      double* own = d_pst + static_cast<size_t>(p) * 6 * S.r.n_ips();
       double* Ep = pE.data() + 6 * p;  // (E_prev, E_comm)
-      std::copy(pu.begin() + p * n, pu.begin() + (p + 1) * n, u_free.begin());
+      std::vector<double> u_free(pu.begin() + p * n, pu.begin() + (p + 1) * n);
       double E_comm[3] = {Ep[3], Ep[4], Ep[5]};
       int its = 0, code = 0;
-      const size_t sb = sizeof(double) * 6 * r.n_ips();
-      CK(cudaMemcpyAsync(d_st0, st_comm, sb, cudaMemcpyDeviceToDevice, stream));  // backup for a failed step
+      CK(cudaMemsetAsync(w.d_err, 0, sizeof(int), w.stream));
+      CK(cudaMemcpyAsync(w.d_st0, own, sb, cudaMemcpyDeviceToDevice, w.stream));  // backup for a failed step
+      w.st_comm = own;
       try {
-        increment(Ep, E + 3 * p, u_free, E_comm, tol, max_iter, max_bisections, mats, its);
+        w.increment(Ep, E + 3 * p, u_free, E_comm, tol, max_iter, max_bisections, S.mats, its);
         double s3[3], c9[9];
-        homogenize(s3, c9);
+        w.homogenize(s3, c9);
         if (sigma) std::memcpy(sigma + 3 * p, s3, sizeof(s3));
         if (C) std::memcpy(C + 9 * p, c9, sizeof(c9));
         std::copy(u_free.begin(), u_free.end(), pu.begin() + p * n);
@@ -552,15 +1075,15 @@ struct fe2_hf_s {
         }
       } catch (const Failure& f) {
         code = 1 + static_cast<int>(f.code);
-        CK(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
+        CK(cudaMemsetAsync(w.d_err, 0, sizeof(int), w.stream));
         // a failed bisection may have committed sub-steps: return to the call's start
-        CK(cudaMemcpyAsync(st_comm, d_st0, sb, cudaMemcpyDeviceToDevice, stream));
+        CK(cudaMemcpyAsync(own, w.d_st0, sb, cudaMemcpyDeviceToDevice, w.stream));
       }
+      w.st_comm = w.d_st0;
+      w.wait();
       if (iters) iters[p] = its;
       if (status) status[p] = code;
-    }
-    st_comm = d_st0;
-    CK(cudaStreamSynchronize(stream));
+    });
   }
 };
 
@@ -572,25 +1095,26 @@ int fe2_hf_create(int device, int subdivisions, const char* mesh_path, const fe2
     check(out && materials && n_materials >= 1 && n_materials <= kMaxMats, Code::config, "bad HF arguments");
     *out = nullptr;
     auto h = std::make_unique<fe2_hf_s>();
+    HfShared& S = h->S;
     for (int i = 0; i < n_materials; ++i) {
-      h->mats.m[i] = to_dev(materials[i]);
+      S.mats.m[i] = to_dev(materials[i]);
       fe2_material_t el = materials[i];
       el.kind = 0;  // the elastic part (build_elastic_modes)
-      h->mats_el.m[i] = to_dev(el);
+      S.mats_el.m[i] = to_dev(el);
     }
-    h->r = rve_data(subdivisions, mesh_path);
-    const RveData& r = h->r;
+    S.r = rve_data(subdivisions, mesh_path);
+    const RveData& r = S.r;
     for (int e = 0; e < r.n_el; ++e)
       check(r.phase[e] >= 0 && r.phase[e] < n_materials, Code::config, "element material id out of range");
     check(r.n_free >= 1, Code::mesh, "RVE has no free DOF");
+    S.perm = band_order(r, S.bw);
+    S.ldb = S.bw + 1;
+    check(band_chol_smem(S.bw) <= static_cast<size_t>(kBandSmemMax), Code::mesh,
+          "RVE stiffness band too wide for the device band factorisation (half bandwidth " + std::to_string(S.bw) + ")");
     require_device(device);
-    h->device = device;
-    const Cusolver& cs = Cusolver::get();
-    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    sol_check(cs.create(&h->sol), "create");
-    sol_check(cs.set_stream(h->sol, h->stream), "set stream");
+    S.device = device;
     // per-DOF element incidences in ascending element order (CSR)
-    const int N = r.n_dofs(), n = r.n_free;
+    const int N = r.n_dofs();
     std::vector<int> cnt(N + 1, 0), inc;
     for (int e = 0; e < r.n_el; ++e)
       for (int a = 0; a < 12; ++a) ++cnt[2 * r.conn[6 * e + a / 2] + a % 2 + 1];
@@ -607,45 +1131,41 @@ int fe2_hf_create(int device, int subdivisions, const char* mesh_path, const fe2
       d = dalloc<double>(v.size());
       CK(cudaMemcpy(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
     };
-    up_i(h->d_conn, r.conn);
-    up_i(h->d_phase, r.phase);
-    up_i(h->d_free, r.free_index);
-    up_i(h->d_inc_ptr, cnt);
-    up_i(h->d_inc, inc);
-    up_d(h->d_B, r.B);
-    up_d(h->d_w, r.w);
-    h->d_info = dalloc<int>(1);
-    h->d_err = dalloc<int>(1);
-    CK(cudaMemset(h->d_err, 0, sizeof(int)));
-    h->d_u = dalloc<double>(N);
-    h->d_f = dalloc<double>(N);
-    h->d_st0 = dalloc<double>((size_t)6 * r.n_ips());
-    h->d_st1 = dalloc<double>((size_t)6 * r.n_ips());
-    h->d_sig = dalloc<double>((size_t)3 * r.n_ips());
-    h->d_C = dalloc<double>((size_t)9 * r.n_ips());
-    h->d_fel = dalloc<double>((size_t)12 * r.n_el);
-    h->d_kel = dalloc<double>((size_t)144 * r.n_el);
-    h->d_K = dalloc<double>((size_t)n * n);
-    h->d_rhs = dalloc<double>((size_t)3 * n);
-    sol_check(cs.potrf_ws(h->sol, CUBLAS_FILL_MODE_UPPER, n, h->d_K, n, &h->lwork), "potrf workspace");
-    h->d_work = dalloc<double>(std::max(1, h->lwork));
+    up_i(S.d_conn, r.conn);
+    up_i(S.d_phase, r.phase);
+    up_i(S.d_free, r.free_index);
+    up_i(S.d_inc_ptr, cnt);
+    up_i(S.d_inc, inc);
+    up_i(S.d_perm, S.perm);
+    up_d(S.d_B, r.B);
+    up_d(S.d_w, r.w);
+    // one ceiling for every handle (the attribute is per kernel, not per launch)
+    CK(cudaFuncSetAttribute(k_band_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, kBandSmemMax));
+    h->w0();
     *out = h.release();
   });
 }
 
 void fe2_hf_destroy(fe2_hf_t h) {
   if (!h) return;
-  cudaSetDevice(h->device);
+  cudaSetDevice(h->S.device);
   delete h;
 }
 
 int fe2_hf_sizes(fe2_hf_t h, int* n_dofs, int* n_free, int* n_ips, double* volume) {
   return guard([&] {
     check(h != nullptr, Code::config, "null HF handle");
-    if (n_dofs) *n_dofs = h->nd();
-    if (n_free) *n_free = h->nf();
-    if (n_ips) *n_ips = h->r.n_ips();
-    if (volume) *volume = h->r.volume;
+    if (n_dofs) *n_dofs = h->S.nd();
+    if (n_free) *n_free = h->S.nf();
+    if (n_ips) *n_ips = h->S.r.n_ips();
+    if (volume) *volume = h->S.r.volume;
+  });
+}
+
+int fe2_hf_band(fe2_hf_t h, int* half_bandwidth) {
+  return guard([&] {
+    check(h != nullptr && half_bandwidth != nullptr, Code::config, "bad arguments");
+    *half_bandwidth = h->S.bw;
   });
 }
 
@@ -654,16 +1174,49 @@ int fe2_hf_trajectory(fe2_hf_t h, int n_steps, const double* E, const fe2_newton
   return guard([&] {
     check(h && E && opts && n_steps >= 0, Code::config, "bad HF trajectory arguments");
     check(opts->tol > 0.0 && opts->max_iter >= 1 && opts->max_bisections >= 0, Code::config, "bad Newton options");
-    CK(cudaSetDevice(h->device));
-    h->trajectory(n_steps, E, opts->tol, opts->max_iter, opts->max_bisections, h->mats, sigma, C, iterations,
-                  u_fluct_inf, res_last, snapshots);
+    CK(cudaSetDevice(h->S.device));
+    h->w0().trajectory(n_steps, E, opts->tol, opts->max_iter, opts->max_bisections, h->S.mats, sigma, C, iterations,
+                       u_fluct_inf, res_last, snapshots);
+  });
+}
+
+int fe2_hf_trajectories(fe2_hf_t h, int n_traj, int n_steps, const double* E, const fe2_newton_opts_t* opts,
+                        double* sigma, double* C, int* iterations, double* u_fluct_inf, double* res_last,
+                        double* snapshots, int* status) {
+  return guard([&] {
+    check(h && E && opts && n_traj >= 0 && n_steps >= 0, Code::config, "bad HF trajectory arguments");
+    check(opts->tol > 0.0 && opts->max_iter >= 1 && opts->max_bisections >= 0, Code::config, "bad Newton options");
+    CK(cudaSetDevice(h->S.device));
+    const size_t N = h->S.nd(), k = n_steps;
+    std::vector<std::string> msg(n_traj);
+    h->parallel(n_traj, [&](HfWork& w, int64_t t) {
+      int code = 0;
+      try {
+        w.trajectory(n_steps, E + 3 * k * t, opts->tol, opts->max_iter, opts->max_bisections, h->S.mats,
+                     sigma ? sigma + 3 * k * t : nullptr, C ? C + 9 * k * t : nullptr,
+                     iterations ? iterations + k * t : nullptr, u_fluct_inf ? u_fluct_inf + k * t : nullptr,
+                     res_last ? res_last + k * t : nullptr, snapshots ? snapshots + N * k * t : nullptr);
+      } catch (const std::exception& f) {
+        const Failure* ff = dynamic_cast<const Failure*>(&f);
+        code = 1 + static_cast<int>(ff ? ff->code : Code::numeric);
+        msg[t] = f.what();
+        CK(cudaMemsetAsync(w.d_err, 0, sizeof(int), w.stream));
+        w.wait();
+      }
+      if (status) status[t] = code;
+    });
+    for (int t = 0; t < n_traj; ++t)  // the call succeeds; fe2_last_error names the first failed trajectory
+      if (!msg[t].empty()) {
+        set_last_error("trajectory " + std::to_string(t) + ": " + msg[t]);
+        break;
+      }
   });
 }
 
 int fe2_hf_alloc_points(fe2_hf_t h, int64_t P) {
   return guard([&] {
     check(h != nullptr && P >= 1, Code::config, "bad arguments");
-    CK(cudaSetDevice(h->device));
+    CK(cudaSetDevice(h->S.device));
     h->alloc_points(P);
   });
 }
@@ -674,7 +1227,7 @@ int fe2_hf_solve_increment(fe2_hf_t h, const double* E, const fe2_newton_opts_t*
     check(h && E && opts, Code::config, "bad arguments");
     check(h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
     check(opts->tol > 0.0 && opts->max_iter >= 1 && opts->max_bisections >= 0, Code::config, "bad Newton options");
-    CK(cudaSetDevice(h->device));
+    CK(cudaSetDevice(h->S.device));
     h->solve_points(E, opts->tol, opts->max_iter, opts->max_bisections, sigma, C, iters, status);
   });
 }
@@ -682,24 +1235,26 @@ int fe2_hf_solve_increment(fe2_hf_t h, const double* E, const fe2_newton_opts_t*
 int fe2_hf_snapshot(fe2_hf_t h) {
   return guard([&] {
     check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
-    CK(cudaSetDevice(h->device));
-    CK(cudaMemcpyAsync(h->d_pst_snap, h->d_pst, sizeof(double) * h->P * 6 * h->r.n_ips(), cudaMemcpyDeviceToDevice,
-                       h->stream));
+    CK(cudaSetDevice(h->S.device));
+    HfWork& w = h->w0();
+    CK(cudaMemcpyAsync(h->d_pst_snap, h->d_pst, sizeof(double) * h->P * 6 * h->S.r.n_ips(), cudaMemcpyDeviceToDevice,
+                       w.stream));
     h->pu_snap = h->pu;
     h->pE_snap = h->pE;
-    CK(cudaStreamSynchronize(h->stream));
+    w.wait();
   });
 }
 
 int fe2_hf_restore(fe2_hf_t h) {
   return guard([&] {
     check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
-    CK(cudaSetDevice(h->device));
-    CK(cudaMemcpyAsync(h->d_pst, h->d_pst_snap, sizeof(double) * h->P * 6 * h->r.n_ips(), cudaMemcpyDeviceToDevice,
-                       h->stream));
+    CK(cudaSetDevice(h->S.device));
+    HfWork& w = h->w0();
+    CK(cudaMemcpyAsync(h->d_pst, h->d_pst_snap, sizeof(double) * h->P * 6 * h->S.r.n_ips(), cudaMemcpyDeviceToDevice,
+                       w.stream));
     h->pu = h->pu_snap;
     h->pE = h->pE_snap;
-    CK(cudaStreamSynchronize(h->stream));
+    w.wait();
   });
 }
 
@@ -713,16 +1268,17 @@ int fe2_hf_points(fe2_hf_t h, int64_t* P) {
 int fe2_hf_elastic_modes(fe2_hf_t h, double* modes, int* count) {
   return guard([&] {
     check(h && modes && count, Code::config, "bad arguments");
-    CK(cudaSetDevice(h->device));
-    const int N = h->nd();
+    CK(cudaSetDevice(h->S.device));
+    const int N = h->S.nd();
+    HfWork& w = h->w0();
     std::vector<double> A((size_t)3 * N), drop(3);
     for (int j = 0; j < 3; ++j) {
       double E[3] = {0, 0, 0};
       E[j] = 1.0;
       int its = 0;
-      h->trajectory(1, E, 1e-10, 10, 0, h->mats_el, nullptr, nullptr, &its, nullptr, nullptr, A.data() + (size_t)j * N);
+      w.trajectory(1, E, 1e-10, 10, 0, h->S.mats_el, nullptr, nullptr, &its, nullptr, nullptr, A.data() + (size_t)j * N);
       std::vector<double> aff;
-      h->affine(E, aff);
+      w.affine(E, aff);
       drop[j] = 1e-10 * norm2(aff.data(), aff.size());
     }
     *count = orthonormalize_columns(A, N, 3, drop);

@@ -135,7 +135,10 @@ constexpr int kGroupUnroll = FE2_GROUP_UNROLL;  // plastic-group loop unroll (tu
 // warps per CTA of the streamed-G ring increment kernel: 16 (128 registers) for NP = 8;
 // from NP = 16 on the 16-warp build spilled 0.5-1.1 KB per thread and 8 warps
 // with 255 registers measured faster (n = 32, K = 1,000 / 4,000: +9% / +15%)
-constexpr int kw_for(int NT) { return NT == 1 ? FE2_KW : 8; }
+#ifndef FE2_KW_WIDE
+#define FE2_KW_WIDE 8
+#endif
+constexpr int kw_for(int NT) { return NT == 1 ? FE2_KW : FE2_KW_WIDE; }
 // warps per CTA when the whole G2 is resident in shared memory: 12 (168 registers, the
 // warp-uniform Newton state in shared memory, WarpSt) — measured +12% over 8 warps with
 // 255 registers at n = 24; NP = 32 spills at 168 registers and keeps 8
@@ -803,11 +806,12 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
     // micro scale: max(|r| at the step's first iteration, |Σ_raw| now) — E moves during a monolithic step
     const double r_first = A.mono_first ? rn : tail[6];
     const double ref = fmax(fmax(r_first, sqrt(s0 * s0 + s1 * s1 + s2 * s2)), 1e-30);
-    if (!factor()) {
+    if (!factor()) {  // fatal for the point: mono_commit skips it, later iterations report it
       if (lane == 0) {
         A.O.status[p] = kSolver;
         A.O.iters[p] = 1;
         A.O.res[p] = rn / ref;
+        D.st[p].err = kSolver;
       }
       __syncwarp();
       return;

@@ -1012,11 +1012,12 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
     // micro scale: max(|r| at the step's first iteration, |Σ_raw| now) — E moves during a monolithic step
     const double r_first = A.mono_first ? rn : tail[6];
     const double ref = fmax(fmax(r_first, sqrt(s0 * s0 + s1 * s1 + s2 * s2)), 1e-30);
-    if (!factor()) {
+    if (!factor()) {  // fatal for the point: mono_commit skips it, later iterations report it
       if (tid == 0) {
         A.O.status[p] = kSolver;
         A.O.iters[p] = 1;
         A.O.res[p] = rn / ref;
+        D.st[p].err = kSolver;
       }
       __syncthreads();
       return;

@@ -1,7 +1,8 @@
 """Offline POD basis from high-fidelity RVE snapshots (
 SPEC.md:256-316 rom.build_elastic_modes / rom.pod): the full-field micro
-problem solved on the device (fe2_hf_*: element kernel + deterministic dense
-assembly + cuSOLVER Cholesky), x_u snapshot columns per converged increment
+problem solved on the device (fe2_hf_*: element kernel + deterministic band
+assembly + band Cholesky on one CTA per system, many trajectories at once),
+x_u snapshot columns per converged increment
 (run_trajectory + SnapshotRecorder, rve.hpp:397-494), elastic modes prepended,
 SVD of the deflated snapshots (fe2_pod_basis), and the hyper-ROM model built
 on that basis (fe2_model_build_basis). Plus the binary container + text
@@ -57,6 +58,30 @@ class HfRve:
         if snapshots:
             out["snapshots"] = X
         return out
+
+    def trajectories(self, E_paths, opts: NewtonOptions | None = None, snapshots=True):
+        """A batch of independent strain paths E_paths (T, k, 3), each from the
+        virgin state, solved concurrently (fe2_hf_trajectories). Returns the
+        trajectory() fields stacked over T plus status (T,) (0 or 1 + ErrorCode)."""
+        E_paths = np.ascontiguousarray(E_paths, dtype=np.float64)
+        T, k = E_paths.shape[:2]
+        o = (opts or NewtonOptions())._c()
+        sig, Cm, it = np.empty((T, k, 3)), np.empty((T, k, 3, 3)), np.empty((T, k), dtype=np.int32)
+        uf, rl, st = np.empty((T, k)), np.empty((T, k)), np.empty(T, dtype=np.int32)
+        X = np.empty((T, k, self.n_dofs)) if snapshots else None
+        _check(lib.fe2_hf_trajectories(self._h, T, k, _d(E_paths), C.byref(o), _d(sig), _d(Cm), _i(it), _d(uf),
+                                       _d(rl), _d(X), _i(st)))
+        out = dict(sigma=sig, C=Cm, iterations=it, u_fluct_inf=uf, res_last=rl, status=st)
+        if snapshots:
+            out["snapshots"] = X
+        return out
+
+    @property
+    def half_bandwidth(self):
+        """Half bandwidth of the free stiffness in the device's band (RCM) ordering."""
+        b = C.c_int()
+        _check(lib.fe2_hf_band(self._h, C.byref(b)))
+        return b.value
 
     # ---- HF engine of an FE² run: P macro points with their own states
     def alloc_points(self, P):
@@ -134,12 +159,13 @@ def collect_snapshots(rve: HfRve, endpoints, n_steps=20, opts: NewtonOptions | N
     """Monotonic training trajectories to each endpoint:
     x_u columns (n_traj * n_steps, n_dofs) and their manifest rows
     (trajectory, increment, load factor)."""
-    cols, meta = [], []
-    for t, end in enumerate(np.atleast_2d(endpoints)):
-        r = rve.trajectory(monotonic_path(end, n_steps), opts)
-        cols.append(r["snapshots"])
-        meta += [(t, k, (k + 1) / n_steps) for k in range(n_steps)]
-    return np.concatenate(cols), meta
+    ends = np.atleast_2d(endpoints)
+    r = rve.trajectories(np.stack([monotonic_path(e, n_steps) for e in ends]), opts)  # concurrently
+    bad = np.flatnonzero(r["status"])
+    if bad.size:
+        raise Fe2Error(int(r["status"][bad[0]]), lib.fe2_last_error().decode())
+    meta = [(t, k, (k + 1) / n_steps) for t in range(len(ends)) for k in range(n_steps)]
+    return r["snapshots"].reshape(-1, rve.n_dofs), meta
 
 
 def train_model(rve: HfRve, endpoints, n_modes, K=0, seed=0, n_steps=20, subdivisions=33, mesh_file=None, device=0):

@@ -55,6 +55,49 @@ def test_hf_deterministic(rve8):
     np.testing.assert_array_equal(a["snapshots"], b["snapshots"])
 
 
+def test_band_ordering_is_narrow(rve8):
+    """Reverse Cuthill-McKee keeps the free stiffness banded: half bandwidth
+    well below the free DOF count (275 of 7,910 on default_cell(33))."""
+    assert 0 < rve8.half_bandwidth < rve8.n_free // 3
+
+
+def test_batched_trajectories_equal_serial_and_isolate_failures(rve8):
+    """fe2_hf_trajectories: concurrent workers give bit-identical results to
+    one-by-one fe2_hf_trajectory; a failing trajectory reports its error code
+    and does not disturb the others."""
+    rng = np.random.default_rng(3)
+    T = 7
+    ends = rng.standard_normal((T, 3))
+    ends *= 0.015 / np.linalg.norm(ends, axis=1, keepdims=True)
+    paths = np.stack([P.monotonic_path(e, 5) for e in ends])
+    paths[4] = np.nan  # a NaN strain path: no Newton step converges (solver error)
+    opts = F.NewtonOptions(1e-8, 30, 2)
+    b = rve8.trajectories(paths, opts)
+    assert b["status"][4] == 1 + 4 and (np.delete(b["status"], 4) == 0).all()
+    for t in range(T):
+        if t == 4:
+            continue
+        s = rve8.trajectory(paths[t], opts)
+        for key in ("sigma", "C", "iterations", "snapshots", "res_last"):
+            np.testing.assert_array_equal(b[key][t], s[key])
+
+
+def test_batched_trajectories_match_oracle(rve8):
+    """The POD training batch against the oracle's run_trajectory, per trajectory."""
+    rng = np.random.default_rng(5)
+    ends = rng.standard_normal((4, 3))
+    ends *= 0.02 / np.linalg.norm(ends, axis=1, keepdims=True)
+    paths = np.stack([P.monotonic_path(e, 6) for e in ends])
+    b = rve8.trajectories(paths)
+    assert (b["status"] == 0).all()
+    for t in range(len(paths)):
+        o = O.Mesh(0, 8).hf_trajectory(DESK, paths[t], snapshots=True)
+        np.testing.assert_array_equal(b["iterations"][t], o["iterations"])
+        assert _rel(b["sigma"][t], o["sigma"]) < 1e-10
+        assert _rel(b["C"][t], o["C"]) < 1e-10
+        assert _rel(b["snapshots"][t], o["snapshots"]) < 1e-9
+
+
 def test_elastic_modes_match_oracle(rve8):
     g = rve8.elastic_modes()
     o = PO.elastic_modes(O.Mesh(0, 8), DESK)
