@@ -414,7 +414,10 @@ def main():
         uid = [F.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         COMM[0] = F.NcclComm(local, ws, rank, uid[0])
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream (not the legacy default stream, whose handle 0 the C ABI reads as "the
+    # engine's own stream"): torch's events, copies and the engine's kernels all run on it
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
 
     def barrier():
         if ws > 1:

@@ -117,7 +117,7 @@ __device__ double warp_chol_solve(const double* sK, const double* sInv, int n, i
 #define FE2_KW 16
 #endif
 #ifndef FE2_MONO_KW
-#define FE2_MONO_KW 16
+#define FE2_MONO_KW 12
 #endif
 #ifndef FE2_STAGES
 #define FE2_STAGES 6
@@ -143,6 +143,10 @@ constexpr int kw_for(int NT) { return NT == 1 ? FE2_KW : FE2_KW_WIDE; }
 // warp-uniform Newton state in shared memory, WarpSt) — measured +12% over 8 warps with
 // 255 registers at n = 24; NP = 32 spills at 168 registers and keeps 8
 constexpr int kwres_for(int NT) { return NT == 4 ? 8 : FE2_KWRES; }
+// warps per CTA of the monolithic iteration (ring-streamed G): 16 at NP = 8 (128 registers), 12
+// above (168 registers: the 16-warp builds spilled 64-320 B; measured +10% at n = 24, +2% at
+// n = 32, and 16 warps 7% faster at n = 12)
+constexpr int mono_kw(int NT) { return NT == 1 ? 16 : FE2_MONO_KW; }
 constexpr int kMaxStages = FE2_STAGES;  // G-chunk ring depth (shared by the CTA), at most
 
 template <int NP, int W>
@@ -1255,11 +1259,10 @@ void launch_mono_commit(const PointsDev& D, int NP, const double* mono, cudaStre
 
 void launch_increment_mono(const IncArgs& a, int num_sms, cudaStream_t s) {
   switch (a.M.NP) {
-    // the monolithic iteration keeps 16 warps (measured 14% faster than 8 at n = 24)
-    case 8: launch_inc_variant<1, FE2_MONO_KW, false, true>(a, num_sms, s, IncLayout<8, FE2_MONO_KW>::bytes); break;
-    case 16: launch_inc_variant<2, FE2_MONO_KW, false, true>(a, num_sms, s, IncLayout<16, FE2_MONO_KW>::bytes); break;
-    case 24: launch_inc_variant<3, FE2_MONO_KW, false, true>(a, num_sms, s, IncLayout<24, FE2_MONO_KW>::bytes); break;
-    case 32: launch_inc_variant<4, FE2_MONO_KW, false, true>(a, num_sms, s, IncLayout<32, FE2_MONO_KW>::bytes); break;
+    case 8: launch_inc_variant<1, mono_kw(1), false, true>(a, num_sms, s, IncLayout<8, mono_kw(1)>::bytes); break;
+    case 16: launch_inc_variant<2, mono_kw(2), false, true>(a, num_sms, s, IncLayout<16, mono_kw(2)>::bytes); break;
+    case 24: launch_inc_variant<3, mono_kw(3), false, true>(a, num_sms, s, IncLayout<24, mono_kw(3)>::bytes); break;
+    case 32: launch_inc_variant<4, mono_kw(4), false, true>(a, num_sms, s, IncLayout<32, mono_kw(4)>::bytes); break;
     default: break;
   }
 }

@@ -17,7 +17,8 @@ rep = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 m = F.HyperRomModel(33, n, K, 0)
 eng = F.HyperRomEngine.from_model(m)
 dev = torch.device("cuda", 0)
-stream = torch.cuda.current_stream(dev)
+stream = torch.cuda.Stream(device=dev)  # not the legacy default stream (handle 0 = the engine's own)
+torch.cuda.set_stream(stream)
 eng.set_stream(stream.cuda_stream)
 E = F.make_paths(path, 0, P, incr)
 dE = torch.from_numpy(np.ascontiguousarray(E.transpose(1, 0, 2))).to(dev)

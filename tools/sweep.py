@@ -36,7 +36,8 @@ def run_cell(name, n, K, P_max, incr, path, seconds, seed=0, points=0):
     m = F.HyperRomModel(33, n, K, seed)
     eng = F.HyperRomEngine.from_model(m, finite_strain=fs)
     dev = torch.device("cuda", 0)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(device=dev)  # not the legacy default stream (handle 0 = the engine's own)
+    torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
 
     def trajectory(P):
