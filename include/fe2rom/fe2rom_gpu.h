@@ -235,7 +235,10 @@ int fe2_hrom_stats(fe2_hrom_t h, fe2_hrom_stats_t* out);
 int fe2_hrom_reset_stats(fe2_hrom_t h);
 /* enable per-launch CUDA-event timing inside solve_increment */
 int fe2_hrom_set_timing(fe2_hrom_t h, int on);
-/* order all later work of the handle on `stream` (cudaStream_t; NULL = own) */
+/* order all later work of the handle on `stream` (cudaStream_t; NULL = own). NULL is also the
+ * legacy default stream's handle: a caller working on the default stream (e.g. torch's
+ * current_stream() without a stream context) gets the handle's non-blocking stream and must
+ * synchronise with it (fe2_hrom_wait), or pass a stream of its own. */
 int fe2_hrom_set_stream(fe2_hrom_t h, void* stream);
 
 /* ---- macro FE driver of the two-scale beam (the caller
