@@ -44,10 +44,21 @@ def test_creep_without_dt_is_material_error():
     assert e.value.code == 4  # 1 + ErrorCode::material
 
 
-def test_engine_rejects_iterative_materials():
+def test_engine_material_rules():
+    """The small-strain engine takes one inelastic (J2 / power law / creep) material per
+    model (the iterative ones through general_return, tests/test_gpu_general_materials.py);
+    two distinct inelastic materials, or an iterative one on the finite-strain handle,
+    are configuration errors."""
     m = F.HyperRomModel(8, 4, 20, 0)
-    with pytest.raises(F.Fe2Error):
-        F.HyperRomEngine(m.G, m.w, m.mat, [F.PowerLawParams(), F.ElasticParams(10.0, 0.3)], m.volume)
+    F.HyperRomEngine(m.G, m.w, m.mat, [F.PowerLawParams(), F.ElasticParams(10.0, 0.3)], m.volume).close()
+    mid = m.mat.copy()
+    mid[mid == 1] = 2  # the inclusions get a second inelastic material
+    with pytest.raises(F.Fe2Error) as e:
+        F.HyperRomEngine(m.G, m.w, mid, [F.PowerLawParams(), F.ElasticParams(10.0, 0.3), F.CreepParams()], m.volume)
+    assert e.value.code == 1
+    with pytest.raises(F.Fe2Error) as e:
+        F.HyperRomEngine(m.G4, m.w, m.mat, [F.PowerLawParams(), F.ElasticParams(10.0, 0.3)], m.volume)
+    assert e.value.code == 1
 
 
 @pytest.mark.parametrize("matrix,tol", [(F.PowerLawParams(1.0, 0.3, 0.01, 0.1), 1e-8), (F.CreepParams(1.0, 0.3, 5.0, 1.2, -0.3, 0.5), 1e-8)])
