@@ -388,6 +388,17 @@ int fe2_hf_points(fe2_hf_t h, int64_t* P);
 int fe2_hf_solve_increment(fe2_hf_t h, const double* E, const fe2_newton_opts_t* opts, double* sigma, double* C,
                            int* iters, int* status);
 int fe2_hf_snapshot(fe2_hf_t h);
+/* HF_monolithic: one condensed full-field Newton iteration of
+ * every point per call — the fluctuation moves by the previous iteration's
+ * linearisation, w <- w - K^-1 (r + K_fE dE), the point is assembled at (E, w)
+ * from its committed states, and Σ~ = (Σ_raw - K_Ef K^-1 r)/V,
+ * C = (C_EE - K_Ef K^-1 K_fE)/V and the relative micro residual
+ * |r| / max(|r_first|, |reactions|) are returned (status 0 or 1 + ErrorCode).
+ * begin starts a step from the committed state; commit adopts the last iterate.
+ * The same algebra as fe2_hrom_mono_* on the full field (Φ = identity). */
+int fe2_hf_mono_begin(fe2_hf_t h);
+int fe2_hf_mono_iterate(fe2_hf_t h, const double* E, double* sigma, double* C, double* rel_res, int* status);
+int fe2_hf_mono_commit(fe2_hf_t h);
 int fe2_hf_restore(fe2_hf_t h);
 /* build_elastic_modes: fluctuation responses of the
  * elastic RVE (every material's elastic part) to unit macro strains

@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(144) k_hf_element(int n_el, const int* __restr
 constexpr int kNB = 32;             // columns per panel (= warp width: the diagonal blocks run lane-per-row)
 constexpr int kBandThreads = 512;   // factorisation CTA
 constexpr int kSolveThreads = 256;  // substitution CTA
+constexpr int kMaxRhs = 4;          // right-hand sides per substitution (monolithic: K^-1 [r | K_fE])
 
 __host__ __device__ constexpr int band_panel_ld(int bw) { return (bw + kNB + 3) / 4 * 4; }
 size_t band_chol_smem(int bw) { return sizeof(double) * kNB * band_panel_ld(bw); }
@@ -351,12 +352,12 @@ __global__ void __launch_bounds__(kSolveThreads) k_band_solve(int n, int bw, int
                                                               double* __restrict__ x, int nrhs) {
   __shared__ double sD[kNB][kNB + 1];  // diagonal block, sD[i][k] = L(j0 + i, j0 + k)
   __shared__ double sInv[kNB];
-  __shared__ double sX[3][kNB];        // the block's solution
+  __shared__ double sX[kMaxRhs][kNB];  // the block's solution
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   auto stage = [&](int j0, int nb) {
     for (int e = t; e < kNB * kNB; e += blockDim.x) {
       const int i = e % kNB, k = e / kNB;
-      sD[i][k] = (i < nb && k < nb && i >= k) ? Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] : 0.0;
+      sD[i][k] = (i < nb && k < nb && i >= k && i - k <= bw) ? Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] : 0.0;
     }
     __syncthreads();
     if (t < nb) sInv[t] = 1.0 / sD[t][t];
@@ -655,10 +656,10 @@ struct HfWork {
     d_fel = dalloc<double>(static_cast<size_t>(12) * r.n_el);
     d_kel = dalloc<double>(static_cast<size_t>(144) * r.n_el);
     d_Kb = dalloc<double>(static_cast<size_t>(S.nf()) * S.ldb);
-    d_rhs = dalloc<double>(static_cast<size_t>(3) * S.nf());
+    d_rhs = dalloc<double>(static_cast<size_t>(kMaxRhs) * S.nf());
     CK(cudaMallocHost(&h_u, sizeof(double) * S.nd()));
     CK(cudaMallocHost(&h_f, sizeof(double) * S.nd()));
-    CK(cudaMallocHost(&h_rhs, sizeof(double) * 3 * S.nf()));
+    CK(cudaMallocHost(&h_rhs, sizeof(double) * kMaxRhs * S.nf()));
     CK(cudaMallocHost(&h_sig, sizeof(double) * 3 * r.n_ips()));
     CK(cudaMallocHost(&h_C, sizeof(double) * 9 * r.n_ips()));
     CK(cudaMallocHost(&h_flags, sizeof(int) * 2));
@@ -828,72 +829,147 @@ struct HfWork {
     return out;
   }
 
-  // homogenize (rve.hpp:350-392) at the converged state of the last newton().
-  void homogenize(double* sigma, double* C) {
-    const Tick tk(*this, 4);
+  // The integration-point stresses / tangents of the last assembly to the host,
+  // s = Σ w σ, c_avg = Σ w C and the macro-strain coupling of the free DOFs,
+  // kfe[j][n] = K_fE e_j = Σ w B_fᵀ C e_j (homogenize's right-hand sides, rve.hpp:372-380).
+  void point_sums(std::vector<double>& Cq, double* s, double* c_avg, std::vector<double>& kfe) {
     const RveData& r = S.r;
     const int n = nf(), N = nd(), nip = r.n_ips();
-    std::vector<double> sg((size_t)3 * nip), Cq((size_t)9 * nip);
+    std::vector<double> sg(static_cast<size_t>(3) * nip);
+    Cq.resize(static_cast<size_t>(9) * nip);
     CK(cudaMemcpyAsync(h_sig, d_sig, sizeof(double) * sg.size(), cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(h_C, d_C, sizeof(double) * Cq.size(), cudaMemcpyDeviceToHost, stream));
     wait();
     std::memcpy(sg.data(), h_sig, sizeof(double) * sg.size());
     std::memcpy(Cq.data(), h_C, sizeof(double) * Cq.size());
-    double s[3] = {0, 0, 0};
+    for (int i = 0; i < 3; ++i) s[i] = 0.0;
     for (int ip = 0; ip < nip; ++ip)
       for (int i = 0; i < 3; ++i) s[i] += r.w[ip] * sg[3 * ip + i];
-    for (int i = 0; i < 3; ++i) sigma[i] = s[i] / r.volume;
-    std::vector<double> rhs_full((size_t)N * 3, 0.0);
-    double c_avg[9] = {0};
+    std::vector<double> rhs_full(static_cast<size_t>(N) * 3, 0.0);
+    for (int k = 0; k < 9; ++k) c_avg[k] = 0.0;
     for (int ip = 0; ip < nip; ++ip) {
       const int* el = r.conn.data() + 6 * (ip / 3);
-      const double* B = r.B.data() + (size_t)36 * ip;
-      const double* Cp = Cq.data() + (size_t)9 * ip;
+      const double* B = r.B.data() + static_cast<size_t>(36) * ip;
+      const double* Cp = Cq.data() + static_cast<size_t>(9) * ip;
       for (int a = 0; a < 12; ++a) {
         const int ga = 2 * el[a / 2] + a % 2;
         for (int j = 0; j < 3; ++j) {
           double t = 0.0;
           for (int i = 0; i < 3; ++i) t += B[i * 12 + a] * Cp[3 * i + j];
-          rhs_full[(size_t)ga * 3 + j] += t * r.w[ip];
+          rhs_full[static_cast<size_t>(ga) * 3 + j] += t * r.w[ip];
         }
       }
       for (int k = 0; k < 9; ++k) c_avg[k] += r.w[ip] * Cp[k];
     }
-    if (!factored) factor("homogenize: singular converged stiffness");
-    std::vector<double> h((size_t)n * 3, 0.0);
+    kfe.assign(static_cast<size_t>(n) * 3, 0.0);
     for (int j = 0; j < 3; ++j)
       for (int i = 0; i < N; ++i)
-        if (r.free_index[i] >= 0) h[(size_t)j * n + r.free_index[i]] += rhs_full[(size_t)i * 3 + j];
+        if (r.free_index[i] >= 0) kfe[static_cast<size_t>(j) * n + r.free_index[i]] += rhs_full[static_cast<size_t>(i) * 3 + j];
+  }
+
+  // out = Σ_ip w C_ip B_ip v for a free-DOF vector v (boundary entries 0)
+  void cb_integral(const std::vector<double>& Cq, const double* v, double* out) const {
+    const RveData& r = S.r;
+    const int N = nd(), nip = r.n_ips();
+    std::vector<double> vf(N);
+    for (int i = 0; i < N; ++i) vf[i] = r.free_index[i] >= 0 ? v[r.free_index[i]] : 0.0;
+    out[0] = out[1] = out[2] = 0.0;
+    for (int ip = 0; ip < nip; ++ip) {
+      const int* el = r.conn.data() + 6 * (ip / 3);
+      const double* B = r.B.data() + static_cast<size_t>(36) * ip;
+      const double* Cp = Cq.data() + static_cast<size_t>(9) * ip;
+      double he[12];
+      for (int a = 0; a < 6; ++a) {
+        he[2 * a] = vf[2 * el[a]];
+        he[2 * a + 1] = vf[2 * el[a] + 1];
+      }
+      double bh[3];
+      for (int q = 0; q < 3; ++q) {
+        double t = 0.0;
+        for (int c = 0; c < 12; ++c) t += B[q * 12 + c] * he[c];
+        bh[q] = t;
+      }
+      for (int i = 0; i < 3; ++i) {
+        double t = 0.0;
+        for (int k = 0; k < 3; ++k) t += Cp[3 * i + k] * bh[k];
+        out[i] += r.w[ip] * t;
+      }
+    }
+  }
+
+  // homogenize (rve.hpp:350-392) at the converged state of the last newton():
+  // Σ = s / V, C = (c_avg + Σ_j C B h_j) / V with h_j = K^-1 (-K_fE e_j).
+  void homogenize(double* sigma, double* C) {
+    const Tick tk(*this, 4);
+    const int n = nf();
+    std::vector<double> Cq, h;
+    double s[3], c_avg[9];
+    point_sums(Cq, s, c_avg, h);
+    for (int i = 0; i < 3; ++i) sigma[i] = s[i] / S.r.volume;
+    if (!factored) factor("homogenize: singular converged stiffness");
     for (double& v : h) v = -v;
     solve(h, 3);
     double c_hom[9];
     for (int k = 0; k < 9; ++k) c_hom[k] = c_avg[k];
-    std::vector<double> h_full(N);
     for (int j = 0; j < 3; ++j) {
-      for (int i = 0; i < N; ++i) h_full[i] = r.free_index[i] >= 0 ? h[(size_t)j * n + r.free_index[i]] : 0.0;
-      for (int ip = 0; ip < nip; ++ip) {
-        const int* el = r.conn.data() + 6 * (ip / 3);
-        const double* B = r.B.data() + (size_t)36 * ip;
-        const double* Cp = Cq.data() + (size_t)9 * ip;
-        double he[12];
-        for (int a = 0; a < 6; ++a) {
-          he[2 * a] = h_full[2 * el[a]];
-          he[2 * a + 1] = h_full[2 * el[a] + 1];
-        }
-        double bh[3];
-        for (int q = 0; q < 3; ++q) {
-          double t = 0.0;
-          for (int c = 0; c < 12; ++c) t += B[q * 12 + c] * he[c];
-          bh[q] = t;
-        }
-        for (int i = 0; i < 3; ++i) {
-          double t = 0.0;
-          for (int k = 0; k < 3; ++k) t += Cp[3 * i + k] * bh[k];
-          c_hom[3 * i + j] += r.w[ip] * t;
-        }
-      }
+      double ch[3];
+      cb_integral(Cq, h.data() + static_cast<size_t>(j) * n, ch);
+      for (int i = 0; i < 3; ++i) c_hom[3 * i + j] += ch[i];
     }
-    for (int k = 0; k < 9; ++k) C[k] = c_hom[k] / r.volume;
+    for (int k = 0; k < 9; ++k) C[k] = c_hom[k] / S.r.volume;
+  }
+
+  // One monolithic micro iteration of a point (SPEC.md:474-481 HF_monolithic, the
+  // full-field counterpart of k_increment<..., MONO>): the fluctuation w (free DOFs,
+  // u = E.x + w) moves by the previous iteration's linearisation,
+  // w <- w - K^-1 (r + K_fE (E - E_prev)) (the first iteration of a step starts from the
+  // committed w); assemble at (E, w) from the committed states (trial states -> d_st1),
+  // factor, z = K^-1 [r | K_fE]; condensed Σ~ = (s - K_fEᵀ K^-1 r) / V and
+  // C = (c_avg - K_fEᵀ K^-1 K_fE) / V; rel_res = |r| / max(|r| at the step's first
+  // iteration, |boundary reactions|, 1e-30).
+  struct Mono {
+    std::vector<double> w, z;  // [nf], [4][nf]
+    double E[3] = {0, 0, 0};
+    double r_first = 0.0;
+  };
+  void mono_iteration(const double* E, bool first, Mono& ms, double* sigma, double* C, double& rel_res) {
+    const RveData& r = S.r;
+    const int n = nf(), N = nd();
+    if (!first) {
+      const double d0 = E[0] - ms.E[0], d1 = E[1] - ms.E[1], d2 = E[2] - ms.E[2];
+      for (int i = 0; i < n; ++i)
+        ms.w[i] -= ms.z[i] + ms.z[static_cast<size_t>(n) + i] * d0 + ms.z[static_cast<size_t>(2) * n + i] * d1 +
+                   ms.z[static_cast<size_t>(3) * n + i] * d2;
+    }
+    std::vector<double> aff, u_full(N), f_full;
+    affine(E, aff);
+    for (int i = 0; i < N; ++i) u_full[i] = aff[i] + (r.free_index[i] >= 0 ? ms.w[r.free_index[i]] : 0.0);
+    assemble(u_full, true, S.mats, f_full);
+    std::vector<double> res(n, 0.0);
+    double reac = 0.0;
+    for (int i = 0; i < N; ++i) {
+      if (r.free_index[i] >= 0) res[r.free_index[i]] += f_full[i];
+      else reac += f_full[i] * f_full[i];
+    }
+    const double rn = norm2(res.data(), n);
+    if (first) ms.r_first = rn;
+    rel_res = rn / std::max({ms.r_first, std::sqrt(reac), 1e-30});
+    std::vector<double> Cq, kfe;
+    double s[3], c_avg[9];
+    point_sums(Cq, s, c_avg, kfe);
+    factor("monolithic: singular micro stiffness");
+    ms.z.assign(static_cast<size_t>(4) * n, 0.0);
+    std::copy(res.begin(), res.end(), ms.z.begin());
+    std::copy(kfe.begin(), kfe.end(), ms.z.begin() + n);
+    solve(ms.z, 4);
+    double t[3];
+    cb_integral(Cq, ms.z.data(), t);  // K_fEᵀ K^-1 r
+    for (int i = 0; i < 3; ++i) sigma[i] = (s[i] - t[i]) / r.volume;
+    for (int j = 0; j < 3; ++j) {
+      cb_integral(Cq, ms.z.data() + static_cast<size_t>(1 + j) * n, t);  // K_fEᵀ K^-1 K_fE e_j
+      for (int i = 0; i < 3; ++i) C[3 * i + j] = (c_avg[3 * i + j] - t[i]) / r.volume;
+    }
+    for (int i = 0; i < 3; ++i) ms.E[i] = E[i];
   }
 
   // One path step of run_trajectory (rve.hpp:459-491) from the committed
@@ -984,10 +1060,15 @@ struct fe2_hf_s {
   int64_t P = 0;
   double *d_pst = nullptr, *d_pst_snap = nullptr;
   std::vector<double> pu, pu_snap, pE, pE_snap;  // [P][nf], [P][6] = (E_prev, E_comm)
+  // monolithic scheme: per point the iterate (fluctuation, K^-1 [r | K_fE], E) and the
+  // candidate states of its last assembly (adopted by fe2_hf_mono_commit)
+  std::vector<HfWork::Mono> pmono;
+  double* d_pcand = nullptr;
+  bool mono_first = true, mono_any = false;
 
   ~fe2_hf_s() {
     work.clear();
-    for (double* p : {d_pst, d_pst_snap})
+    for (double* p : {d_pst, d_pst_snap, d_pcand})
       if (p) cudaFree(p);
   }
   HfWork& w0() { return worker(0); }
@@ -1046,7 +1127,69 @@ struct fe2_hf_s {
     pE.assign(static_cast<size_t>(P) * 6, 0.0);
     pu_snap = pu;
     pE_snap = pE;
+    dfree(d_pcand);
+    pmono.clear();
+    mono_first = true;
+    mono_any = false;
     w.wait();
+  }
+
+  // One monolithic iteration of every point at the macro strains E (points in parallel
+  // over the workers); status 0 or 1 + ErrorCode per point.
+  void mono_points(const double* E, double* sigma, double* C, double* rel_res, int* status) {
+    const int n = S.nf();
+    const size_t sb = sizeof(double) * 6 * S.r.n_ips();
+    if (!d_pcand) d_pcand = dalloc<double>(static_cast<size_t>(P) * 6 * S.r.n_ips());
+    if (pmono.size() != static_cast<size_t>(P)) pmono.assign(P, HfWork::Mono{});
+    const bool first = mono_first;
+    parallel(P, [&](HfWork& w, int64_t p) {
+      HfWork::Mono& ms = pmono[p];
+      if (first) {  // the committed fluctuation: u_free - (E_comm . x) on the free DOFs
+        const double* Ec = pE.data() + 6 * p + 3;
+        std::vector<double> aff;
+        w.affine(Ec, aff);
+        ms.w.assign(n, 0.0);
+        for (int i = 0; i < S.nd(); ++i)
+          if (S.r.free_index[i] >= 0) ms.w[S.r.free_index[i]] = pu[p * n + S.r.free_index[i]] - aff[i];
+      }
+      int code = 0;
+      double s3[3] = {0, 0, 0}, c9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, rr = 0.0;
+      CK(cudaMemsetAsync(w.d_err, 0, sizeof(int), w.stream));
+      w.st_comm = d_pst + static_cast<size_t>(p) * 6 * S.r.n_ips();
+      try {
+        w.mono_iteration(E + 3 * p, first, ms, s3, c9, rr);
+        CK(cudaMemcpyAsync(d_pcand + static_cast<size_t>(p) * 6 * S.r.n_ips(), w.d_st1, sb,
+                           cudaMemcpyDeviceToDevice, w.stream));
+      } catch (const Failure& f) {
+        code = 1 + static_cast<int>(f.code);
+        CK(cudaMemsetAsync(w.d_err, 0, sizeof(int), w.stream));
+      }
+      w.st_comm = w.d_st0;
+      w.wait();
+      if (sigma) std::memcpy(sigma + 3 * p, s3, sizeof(s3));
+      if (C) std::memcpy(C + 9 * p, c9, sizeof(c9));
+      if (rel_res) rel_res[p] = rr;
+      if (status) status[p] = code;
+    });
+    mono_first = false;
+    mono_any = true;
+  }
+
+  // adopt every point's last monolithic iterate: its trial states, u = E.x + w, E
+  void mono_commit() {
+    HfWork& w = w0();
+    const int n = S.nf();
+    CK(cudaMemcpyAsync(d_pst, d_pcand, sizeof(double) * P * 6 * S.r.n_ips(), cudaMemcpyDeviceToDevice, w.stream));
+    for (int64_t p = 0; p < P; ++p) {
+      const HfWork::Mono& ms = pmono[p];
+      std::vector<double> aff;
+      w.affine(ms.E, aff);
+      for (int i = 0; i < S.nd(); ++i)
+        if (S.r.free_index[i] >= 0) pu[p * n + S.r.free_index[i]] = aff[i] + ms.w[S.r.free_index[i]];
+      for (int i = 0; i < 3; ++i) pE[6 * p + i] = pE[6 * p + 3 + i] = ms.E[i];
+    }
+    w.wait();
+    mono_first = true;
   }
 
   void solve_points(const double* E, double tol, int max_iter, int max_bisections, double* sigma, double* C,
@@ -1229,6 +1372,31 @@ int fe2_hf_solve_increment(fe2_hf_t h, const double* E, const fe2_newton_opts_t*
     check(opts->tol > 0.0 && opts->max_iter >= 1 && opts->max_bisections >= 0, Code::config, "bad Newton options");
     CK(cudaSetDevice(h->S.device));
     h->solve_points(E, opts->tol, opts->max_iter, opts->max_bisections, sigma, C, iters, status);
+  });
+}
+
+int fe2_hf_mono_begin(fe2_hf_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
+    h->mono_first = true;
+  });
+}
+
+int fe2_hf_mono_iterate(fe2_hf_t h, const double* E, double* sigma, double* C, double* rel_res, int* status) {
+  return guard([&] {
+    check(h != nullptr && E != nullptr, Code::config, "bad arguments");
+    check(h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
+    CK(cudaSetDevice(h->S.device));
+    h->mono_points(E, sigma, C, rel_res, status);
+  });
+}
+
+int fe2_hf_mono_commit(fe2_hf_t h) {
+  return guard([&] {
+    check(h != nullptr && h->P > 0, Code::config, "no points allocated (fe2_hf_alloc_points)");
+    check(h->mono_any && !h->mono_first, Code::config, "fe2_hf_mono_commit needs a monolithic iterate");
+    CK(cudaSetDevice(h->S.device));
+    h->mono_commit();
   });
 }
 

@@ -208,7 +208,7 @@ int fe2_macro_gauss(const fe2_macro_config_t* cfg, double* B, double* w, int* el
 namespace {
 
 // The load program on either micro backend: a hyper-ROM engine (engine) or
-// full-field HF RVEs (hf, nested scheme only).
+// full-field HF RVEs (hf), nested or monolithic (cfg->scheme).
 void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf, double* rows, int max_rows,
                    int* n_rows, double* u_residual) {
   {
@@ -266,7 +266,6 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
     const bool mono = cfg->scheme == 1;
     check(cfg->scheme == 0 || cfg->scheme == 1, Code::config, "scheme must be 0 (nested) or 1 (monolithic)");
     check(!mono || kin == 0, Code::config, "the monolithic scheme runs on small-strain handles");
-    check(!mono || engine, Code::config, "the monolithic scheme runs on a hyper-ROM engine");
     bool micro_ok = true;  // monolithic: every point's micro residual below micro.tol
     auto micro_solve = [&]() -> bool {
       for (int g = 0; g < P; ++g) {
@@ -279,7 +278,9 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
         }
       }
       if (mono) {  // one micro iteration per point, condensed stress and tangent
-        engine_check(fe2_hrom_mono_iterate(engine, E.data(), sig.data(), C.data(), res.data(), pc.data(), st.data()));
+        engine_check(engine ? fe2_hrom_mono_iterate(engine, E.data(), sig.data(), C.data(), res.data(), pc.data(),
+                                                    st.data())
+                            : fe2_hf_mono_iterate(hf, E.data(), sig.data(), C.data(), res.data(), st.data()));
         micro_ok = true;
         for (int g = 0; g < P; ++g) {
           if (st[g] != 0) return false;
@@ -383,7 +384,7 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
     auto macro_step = [&](double U) -> int {
       predict(U);
       for (int nd_ : m.tip) u[2 * nd_ + 1] = U;
-      if (mono) engine_check(fe2_hrom_mono_begin(engine));
+      if (mono) engine_check(engine ? fe2_hrom_mono_begin(engine) : fe2_hf_mono_begin(hf));
       for (int k = 0; k <= cfg->max_iter; ++k) {
         if (!micro_solve()) return -1;
         double rn = 0.0, fn = 0.0;
@@ -415,7 +416,7 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
       engine_check(fe2_hf_snapshot(hf));
     }
     // tangent of the virgin state (u = 0) for the first step's predictor
-    if (mono) engine_check(fe2_hrom_mono_begin(engine));
+    if (mono) engine_check(engine ? fe2_hrom_mono_begin(engine) : fe2_hf_mono_begin(hf));
     check(micro_solve(), Code::solver, "micro solve at the virgin state failed");
     C_acc = C;
     micro_total = 0;
@@ -446,7 +447,8 @@ void macro_program(const fe2_macro_config_t* cfg, fe2_hrom_t engine, fe2_hf_t hf
         }
         iters_sum += k;
         // accept: the micro states are committed
-        engine_check(mono ? fe2_hrom_mono_commit(engine) : (hf ? fe2_hf_snapshot(hf) : fe2_hrom_snapshot(engine)));
+        engine_check(mono ? (engine ? fe2_hrom_mono_commit(engine) : fe2_hf_mono_commit(hf))
+                          : (hf ? fe2_hf_snapshot(hf) : fe2_hrom_snapshot(engine)));
         {
           double fn = 0.0;
           for (int d = 0; d < nd; ++d) fn += fint[d] * fint[d];

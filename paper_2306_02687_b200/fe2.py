@@ -68,8 +68,9 @@ def macro_gauss(cfg: MacroConfig):
 
 def solve_program(cfg: MacroConfig, engine, max_rows: int = 256):
     """Load / unload program on the beam (solve_program). engine: a
-    HyperRomEngine (hyper-ROM FE²) or a pod.HfRve (full-field HF FE²,
-    nested). Returns the curve rows (U, R, macro iterations, cumulative micro
+    HyperRomEngine (hyper-ROM FE²; the plain ROM is a full-rule model, K = 0)
+    or a pod.HfRve (full-field HF FE²) — the four methods of SPEC.md:461 with
+    cfg.scheme nested or monolithic on either. Returns the curve rows (U, R, macro iterations, cumulative micro
     iterations, wall ms) and the residual displacement U_res of the unloaded beam."""
     P = macro_points(cfg)
     if getattr(engine, "P", 0) != P:

@@ -118,6 +118,9 @@ def _load():
     L.fe2_hf_trajectories.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.POINTER(_Opts), _dp, _dp, _ip, _dp, _dp,
                                       _dp, _ip]
     L.fe2_hf_band.argtypes = [C.c_void_p, _ip]
+    L.fe2_hf_mono_begin.argtypes = [C.c_void_p]
+    L.fe2_hf_mono_iterate.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _ip]
+    L.fe2_hf_mono_commit.argtypes = [C.c_void_p]
     L.fe2_hf_alloc_points.argtypes = [C.c_void_p, C.c_int64]
     L.fe2_hf_points.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     L.fe2_hf_solve_increment.argtypes = [C.c_void_p, _dp, C.POINTER(_Opts), _dp, _dp, _ip, _ip]

@@ -99,6 +99,22 @@ class HfRve:
         _check(lib.fe2_hf_solve_increment(self._h, _d(E), C.byref(o), _d(sig), _d(Cm), _i(it), _i(st)))
         return dict(sigma=sig, C=Cm, iters=it, status=st)
 
+    def mono_begin(self):
+        """HF_monolithic: start a step from the committed state."""
+        _check(lib.fe2_hf_mono_begin(self._h))
+
+    def mono_iterate(self, E):
+        """One condensed full-field Newton iteration of every point at macro strains
+        E (P,3): sigma (P,3), C (P,3,3), rel_res, status (fe2_hf_mono_iterate)."""
+        E = np.ascontiguousarray(E, dtype=np.float64).reshape(self.P, 3)
+        sig, Cm, rr = np.empty((self.P, 3)), np.empty((self.P, 3, 3)), np.empty(self.P)
+        st = np.empty(self.P, dtype=np.int32)
+        _check(lib.fe2_hf_mono_iterate(self._h, _d(E), _d(sig), _d(Cm), _d(rr), _i(st)))
+        return dict(sigma=sig, C=Cm, rel_res=rr, status=st)
+
+    def mono_commit(self):
+        _check(lib.fe2_hf_mono_commit(self._h))
+
     def snapshot(self):
         _check(lib.fe2_hf_snapshot(self._h))
 
