@@ -14,7 +14,8 @@ all-gathered over NCCL (the monolithic scheme's exchange).
            Newton iteration of every point per macro iteration, the NCCL
            exchange after EVERY iteration, lockstep termination (also at N = 1,
            one-rank communicator).
-  extra_configs : config 2 (finite strain) and config 3 (1,048,576 points,
+  extra_configs : config 2 (finite strain), config 4's full-size roofline sweep
+           (20 cells of 131,072 points, one GPU) and config 3 (1,048,576 points,
            n = 64, K = 2,000, split over the ranks: strong scaling) with their
            own rooflines; config 3 also runs the monolithic scheme with the
            per-iteration exchange (the north_star scaling run).
@@ -68,7 +69,7 @@ def parse():
     ap.add_argument("--cpu-sample-points", type=int, default=0)
     ap.add_argument("--constitutive-points", type=int, default=1 << 25,
                     help="material points of the SoA constitutive-update roofline run (0 = skip)")
-    ap.add_argument("--extra-configs", default="2,3",
+    ap.add_argument("--extra-configs", default="2,3,4",
                     help="comma-separated configs also timed device-resident (2-increment warm-up + 1 step) "
                          "into extra_configs of the line; config 3 adds its monolithic run; '' to skip")
     return ap.parse_args()
@@ -205,6 +206,27 @@ def run_reference(args, cfg):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def config4_sweep():
+    """BASELINE configs[4]: n in {8,16,32,64,128} x K in {100,400,1000,4000}, 131,072 points
+    x 5 increments each at full size (tools/sweep.py run_cell: one untimed P = 1,024
+    trajectory, then the timed one; CUDA events on the engine's stream). Per cell:
+    evals/s, the fraction of the DMMA peak on the contracted (plastic) points, the
+    DRAM history rate against HBM — the crossover the config asks for."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import sweep
+    cells = {}
+    for n in (8, 16, 32, 64, 128):
+        for K in (100, 400, 1000, 4000):
+            r = sweep.run_cell(f"n{n}_K{K}", n, K, 131072, 5, 0, seconds=1.0, points=131072)
+            if r["failed"]:
+                raise SystemExit(f"bench: config 4 cell n={n} K={K}: {r['failed']} points failed")
+            cells[f"n{n}_K{K}"] = {k: r[k] for k in ("evals_per_s", "ms", "assemblies_per_eval", "plastic_fraction",
+                                                     "frac_of_dmma_peak", "algorithmic_equiv_frac", "frac_of_hbm",
+                                                     "history_gbs")}
+    return {"workload": "config4: 131,072 points x 5 increments per cell, config-0 path generator",
+            "unit": UNIT, "cells": cells}
 
 
 def rank_points(cfg, ws, rank):
@@ -573,6 +595,10 @@ def main():
     # strong for config 3, whose points are split over the ranks)
     extras = {}
     for c in [int(x) for x in args.extra_configs.split(",") if x.strip()]:
+        if c == 4 and ws == 1:  # the roofline sweep: a single-GPU experiment (BASELINE configs[4])
+            extras["config4_roofline_sweep"] = config4_sweep()
+            torch.cuda.set_stream(stream)  # run_cell works on a stream of its own
+            continue
         if c == args.config or c not in CONFIGS:
             continue
         xcfg = dict(CONFIGS[c])
