@@ -158,29 +158,32 @@ static __device__ __noinline__ GenRet general_return(const MatDev& m, double ss,
   const double mu = m.mu;
   const double q_tr = 1.2247448713915890491 * sqrt(ss);
   if (m.kind == 2) {
+    // sy(e) = sy0 b^N with b = 1 + E e / sy0, and sy'(e) = E N b^(N-1) = sy(e) N E / (sy0 b):
+    // one pow per iteration for both (the reference evaluates two)
     auto sy = [&](double e) { return m.sy0 * pow(1.0 + m.E * e / m.sy0, m.N); };
-    auto sy_slope = [&](double e) { return m.E * m.N * pow(1.0 + m.E * e / m.sy0, m.N - 1.0); };
+    auto slope_of = [&](double e, double s) { return s * (m.N * m.E) / (m.sy0 + m.E * e); };
     const double f_tr = q_tr - sy(eq);
     if (f_tr <= 0.0) return g;
     double lo = 0.0, hi = f_tr / (3.0 * mu), x = hi * 0.5;
     const double tol = 1e-12 * fmax(m.sy0, q_tr);
     bool conv = false;
     for (int it = 0; it < 50; ++it) {
-      const double gx = q_tr - 3.0 * mu * x - sy(eq + x);
+      const double s = sy(eq + x);
+      const double gx = q_tr - 3.0 * mu * x - s;
       if (fabs(gx) <= tol) {
         conv = true;
         break;
       }
       if (gx > 0.0) lo = x;
       else hi = x;
-      double next = x + gx / (3.0 * mu + sy_slope(eq + x));
+      double next = x + gx / (3.0 * mu + slope_of(eq + x, s));
       if (!(next > lo && next < hi)) next = 0.5 * (lo + hi);
       x = next;
     }
     g.ok = conv;
     g.plastic = true;
     g.dlam = x;
-    g.kq = 1.0 / (3.0 * mu + sy_slope(eq + x));
+    g.kq = 1.0 / (3.0 * mu + slope_of(eq + x, sy(eq + x)));
     return g;
   }
   // creep (kind 3)
@@ -191,9 +194,7 @@ static __device__ __noinline__ GenRet general_return(const MatDev& m, double ss,
   if (!(q_tr > 1e-14 * m.E)) return g;
   const double p1 = m.cn / (m.cm + 1.0), p2 = m.cm / (m.cm + 1.0), eq_floor = 1e-12;
   auto hard = [&](double e) { return pow((m.cm + 1.0) * fmax(e, eq_floor), p2); };
-  auto hard_slope = [&](double e) { return e <= eq_floor ? 0.0 : p2 * (m.cm + 1.0) * pow((m.cm + 1.0) * e, p2 - 1.0); };
   auto rate_q = [&](double q) { return pow(q / m.A, p1); };
-  auto rate_q_slope = [&](double q) { return p1 / m.A * pow(q / m.A, p1 - 1.0); };
   double lo = 0.0, hi = q_tr / (3.0 * mu);
   if (hi - dt * rate_q(q_tr - 3.0 * mu * hi) * hard(eq + hi) < 0.0) {  // bracket failure
     g.ok = false;
@@ -205,8 +206,11 @@ static __device__ __noinline__ GenRet general_return(const MatDev& m, double ss,
   for (int it = 0; it < 200; ++it) {
     const double q = q_tr - 3.0 * mu * x;
     const double e = eq + x;
-    const double Rx = x - dt * rate_q(q) * hard(e);
-    Rp = 1.0 + 3.0 * mu * dt * rate_q_slope(q) * hard(e) - dt * rate_q(q) * hard_slope(e);
+    // F = (q/A)^p1 ((m+1) e)^p2 once per iteration: the slopes are F p1 / q and F p2 / e
+    // ((q/A)^(p1-1) p1 / A and p2 (m+1) ((m+1) e)^(p2-1) of the reference, :262-265)
+    const double rq = rate_q(q), hd = hard(e), F = rq * hd;
+    const double Rx = x - dt * F;
+    Rp = 1.0 + 3.0 * mu * dt * (F * p1 / q) - (e <= eq_floor ? 0.0 : dt * (F * p2 / e));
     if (fabs(Rx) <= tol) {
       conv = true;
       break;
@@ -221,7 +225,8 @@ static __device__ __noinline__ GenRet general_return(const MatDev& m, double ss,
   if (conv && x > 0.0) {
     g.plastic = true;
     g.dlam = x;
-    g.kq = dt * rate_q_slope(q_tr - 3.0 * mu * x) * hard(eq + x) / Rp;
+    const double q = q_tr - 3.0 * mu * x;
+    g.kq = dt * (p1 / m.A * pow(q / m.A, p1 - 1.0)) * hard(eq + x) / Rp;
   }
   return g;
 }
