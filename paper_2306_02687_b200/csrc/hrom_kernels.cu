@@ -96,6 +96,93 @@ __device__ bool warp_cholesky(double* sK, double* sInv, int n, int lane) {
   return true;
 }
 
+// Blocked right-looking Cholesky of the same packed lower sK (used at NT = 4):
+// per 8-column block b, (1) the 8 x 8 diagonal block on lanes 0-7 in registers
+// (lane r = block row, column broadcast by shuffles), (2) the rows below solved
+// against it, one lane per row in registers, (3) the lower block tiles of the
+// trailing matrix updated on the FP64 tensor cores, D = A - L_t1 L_t2ᵀ as two
+// DMMA m8n8k4 k-steps per tile. Pad rows (>= n) stay zero. sInv[j] = 1 / L_jj.
+template <int NT>
+__device__ bool warp_cholesky_blk(double* sK, double* sInv, int n, int lane) {
+#pragma unroll
+  for (int b = 0; b < NT; ++b) {
+    const int c0 = 8 * b;
+    if (c0 >= n) break;
+    {  // (1) diagonal block
+      const int r = lane & 7, row = c0 + r;
+      const bool vr = lane < 8 && row < n;
+      const double* rk = sK + tri_(vr ? row : 0) + c0;
+      double a[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = (vr && k <= r) ? rk[k] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (c0 + k < n) {
+          const double d = __shfl_sync(0xffffffffu, a[k], k);
+          if (!(d > 0.0)) return false;
+          const double inv = rsqrt_fast(d);
+          if (r == k) a[k] = d * inv;
+          else if (r > k) a[k] *= inv;
+          if (lane == k) sInv[c0 + k] = inv;
+#pragma unroll
+          for (int kk = k + 1; kk < 8; ++kk) {
+            const double lk = __shfl_sync(0xffffffffu, a[k], kk);  // L(c0 + kk, c0 + k)
+            if (r >= kk) a[kk] -= a[k] * lk;
+          }
+        }
+      }
+      if (vr) {
+        double* wk = sK + tri_(row) + c0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k <= r) wk[k] = a[k];
+      }
+    }
+    __syncwarp();
+    {  // (2) rows below the block (the block is full: c0 + 8 <= row < n)
+      const int row = c0 + 8 + lane;
+      if (row < n) {
+        double* xr = sK + tri_(row) + c0;
+        double x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = xr[k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double* lk = sK + tri_(c0 + k) + c0;  // row c0 + k of the diagonal block (broadcast)
+          double v = x[k];
+#pragma unroll
+          for (int m = 0; m < k; ++m) v -= x[m] * lk[m];
+          x[k] = v * sInv[c0 + k];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xr[k] = x[k];
+      }
+    }
+    __syncwarp();
+    // (3) trailing lower block tiles (t1 >= t2 > b)
+    const int fr = lane >> 2, fk = lane & 3;  // fragment row / k-lane
+#pragma unroll
+    for (int t1 = b + 1; t1 < NT; ++t1) {
+      if (8 * t1 >= n) break;
+#pragma unroll
+      for (int t2 = b + 1; t2 <= t1; ++t2) {
+        const int row = 8 * t1 + fr, col0 = 8 * t2 + 2 * fk;
+        double* drow = sK + tri_(row);
+        double d0 = (row >= col0) ? drow[col0] : 0.0;
+        double d1 = (row >= col0 + 1) ? drow[col0 + 1] : 0.0;
+        const double* la = sK + tri_(8 * t1 + fr) + c0 + fk;  // A = -L[8 t1 + r][c0 + k]
+        const double* lb = sK + tri_(8 * t2 + fr) + c0 + fk;  // B[k][c] = L[8 t2 + c][c0 + k]
+        dmma(d0, d1, -la[0], lb[0]);
+        dmma(d0, d1, -la[4], lb[4]);
+        if (row >= col0) drow[col0] = d0;
+        if (row >= col0 + 1) drow[col0 + 1] = d1;
+      }
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
 // Solve L L^T x = b (packed L); lane i holds b_i in, x_i out (n <= 32).
 __device__ double warp_chol_solve(const double* sK, const double* sInv, int n, int lane, double b) {
   double x = b;
@@ -722,7 +809,11 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       INC_T(4);
       return true;
     }
-    const bool ok = warp_cholesky(sK, sInv, n, lane);
+    // blocked (DMMA trailing updates) for four 8-column blocks: +5% at n = 32; at n <= 24 the
+    // left-looking form was measured faster (-1 to -2% blocked)
+    bool ok;
+    if constexpr (NT == 4) ok = warp_cholesky_blk<NT>(sK, sInv, n, lane);
+    else ok = warp_cholesky(sK, sInv, n, lane);
     INC_T(4);
     return ok;
   };
