@@ -809,10 +809,11 @@ __global__ void __launch_bounds__(W * 32, RES ? 1 : FE2_MINB) k_increment(IncArg
       INC_T(4);
       return true;
     }
-    // blocked (DMMA trailing updates) for four 8-column blocks: +5% at n = 32; at n <= 24 the
-    // left-looking form was measured faster (-1 to -2% blocked)
+    // blocked (DMMA trailing updates) for four 8-column blocks with G resident: +5% at n = 32,
+    // K = 600; the left-looking form was measured faster at n <= 24 (1-2%) and in the
+    // ring-streamed kernel (3% at n = 32, K = 4,000)
     bool ok;
-    if constexpr (NT == 4) ok = warp_cholesky_blk<NT>(sK, sInv, n, lane);
+    if constexpr (NT == 4 && RES) ok = warp_cholesky_blk<NT>(sK, sInv, n, lane);
     else ok = warp_cholesky(sK, sInv, n, lane);
     INC_T(4);
     return ok;
