@@ -931,6 +931,7 @@ struct HfWork {
     std::vector<double> w, z;  // [nf], [4][nf]
     double E[3] = {0, 0, 0};
     double r_first = 0.0;
+    bool failed = false;  // the last iterate failed: commit keeps the point's committed state
   };
   void mono_iteration(const double* E, bool first, Mono& ms, double* sigma, double* C, double& rel_res) {
     const RveData& r = S.r;
@@ -1160,8 +1161,10 @@ struct fe2_hf_s {
         w.mono_iteration(E + 3 * p, first, ms, s3, c9, rr);
         CK(cudaMemcpyAsync(d_pcand + static_cast<size_t>(p) * 6 * S.r.n_ips(), w.d_st1, sb,
                            cudaMemcpyDeviceToDevice, w.stream));
+        ms.failed = false;
       } catch (const Failure& f) {
         code = 1 + static_cast<int>(f.code);
+        ms.failed = true;
         CK(cudaMemsetAsync(w.d_err, 0, sizeof(int), w.stream));
       }
       w.st_comm = w.d_st0;
@@ -1179,9 +1182,12 @@ struct fe2_hf_s {
   void mono_commit() {
     HfWork& w = w0();
     const int n = S.nf();
-    CK(cudaMemcpyAsync(d_pst, d_pcand, sizeof(double) * P * 6 * S.r.n_ips(), cudaMemcpyDeviceToDevice, w.stream));
+    const size_t per = static_cast<size_t>(6) * S.r.n_ips();
     for (int64_t p = 0; p < P; ++p) {
       const HfWork::Mono& ms = pmono[p];
+      if (ms.failed) continue;  // as k_mono_commit skips failed points
+      CK(cudaMemcpyAsync(d_pst + p * per, d_pcand + p * per, sizeof(double) * per, cudaMemcpyDeviceToDevice,
+                         w.stream));
       std::vector<double> aff;
       w.affine(ms.E, aff);
       for (int i = 0; i < S.nd(); ++i)
