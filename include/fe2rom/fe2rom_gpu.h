@@ -217,6 +217,21 @@ int fe2_hrom_assemble_point(fe2_hrom_t h, int64_t point, const double* alpha, co
 int fe2_hrom_snapshot(fe2_hrom_t h);
 int fe2_hrom_restore(fe2_hrom_t h);
 
+/* Mixed control for every point (rve.hpp:496-571 mixed_control_step, the
+ * consumer pattern of the uniaxial-tension calibration): strain
+ * components with control[p*3+j] != 0 are prescribed (E_prescribed), the others
+ * are driven so the conjugate macro stresses reach sigma_target, by an outer
+ * Newton on the condensed tangent (complete pivoting) — every outer iteration
+ * re-solves the active points from their committed state. Converged when
+ * |Σ_u - target_u| <= tol (max(1e-12, |target|) + 1e-3) (reference defaults
+ * tol 1e-10, max_iter 25). E[P*3]: in the committed macro strains, out the
+ * converged ones; the engine is left at the accepted state (committed).
+ * status 0 or 1 + ErrorCode (solver: no convergence in max_iter or singular J;
+ * the micro solve's code if it failed). Small-strain handles. */
+int fe2_hrom_mixed_step(fe2_hrom_t h, const int* control, const double* E_prescribed, const double* sigma_target,
+                        double tol, int max_iter, const fe2_newton_opts_t* micro, double* E, double* sigma,
+                        double* C, int* outer_iters, int* status);
+
 typedef struct {
   int64_t points;
   int n, K, K_j2;

@@ -497,6 +497,125 @@ int fe2_macro_run(const fe2_macro_config_t* cfg, fe2_hrom_t engine, double* rows
   });
 }
 
+// Batched mixed control (rve.hpp:496-571 mixed_control_step, one step for every point of
+// the engine): prescribed strain components where control[p*3 + j] != 0, the others
+// driven so that the conjugate macro stresses hit sigma_target, by an outer Newton with
+// the condensed tangent — each outer iteration re-solves every still-active point from
+// its committed state (fe2_hrom_restore + one increment), J = C[u][u] with complete
+// pivoting (Eigen fullPivLu), converged when |Σ_u - target_u| <= tol (max(1e-12,
+// |target|) + 1e-3). E[P*3] in: the committed macro strains (start of the unknown
+// components), out: the converged ones; sigma / C / outer_iters / status per point.
+int fe2_hrom_mixed_step(fe2_hrom_t h, const int* control, const double* E_prescribed, const double* sigma_target,
+                        double tol, int max_iter, const fe2_newton_opts_t* micro, double* E, double* sigma,
+                        double* C, int* outer_iters, int* status) {
+  return guard([&] {
+    check(h && control && E_prescribed && sigma_target && micro && E, Code::config, "bad arguments");
+    check(tol > 0.0 && max_iter >= 0, Code::config, "invalid mixed-control options");
+    int kin = 0;
+    engine_check(fe2_hrom_kinematics(h, &kin));
+    check(kin == 0, Code::config, "mixed control runs on small-strain handles");
+    fe2_hrom_stats_t st{};
+    engine_check(fe2_hrom_stats(h, &st));
+    const int64_t P = st.points;
+    check(P > 0, Code::config, "no points allocated (fe2_hrom_alloc_points)");
+    std::vector<double> Ew(E, E + 3 * P), sg(3 * P), Cm(9 * P), res(P);
+    std::vector<int> it(P), pc(P), stt(P), active(P, 1), iters(P, 0), code(P, 0);
+    for (int64_t p = 0; p < P; ++p)
+      for (int j = 0; j < 3; ++j)
+        if (control[3 * p + j]) Ew[3 * p + j] = E_prescribed[3 * p + j];
+    engine_check(fe2_hrom_snapshot(h));  // the committed state every outer iteration starts from
+    for (int k = 0; k <= max_iter; ++k) {
+      engine_check(fe2_hrom_restore(h));
+      engine_check(fe2_hrom_solve_increment(h, Ew.data(), micro, sg.data(), Cm.data(), it.data(), pc.data(),
+                                            res.data(), stt.data()));
+      int n_active = 0;
+      for (int64_t p = 0; p < P; ++p) {
+        if (!active[p]) continue;
+        iters[p] = k;
+        if (stt[p] != 0) {  // the micro solve failed (mixed_control_step throws, rve.hpp:547)
+          code[p] = stt[p];
+          active[p] = 0;
+          continue;
+        }
+        int u[3], nu = 0;
+        for (int j = 0; j < 3; ++j)
+          if (!control[3 * p + j]) u[nu++] = j;
+        if (nu == 0) {
+          active[p] = 0;
+          continue;
+        }
+        const double* tg = sigma_target + 3 * p;
+        const double scale = std::max(1e-12, std::sqrt(tg[0] * tg[0] + tg[1] * tg[1] + tg[2] * tg[2])) + 1e-3;
+        double r[3], rn = 0.0;
+        for (int a = 0; a < nu; ++a) {
+          r[a] = sg[3 * p + u[a]] - tg[u[a]];
+          rn += r[a] * r[a];
+        }
+        if (std::sqrt(rn) <= tol * scale) {
+          active[p] = 0;
+          continue;
+        }
+        if (k == max_iter) {  // "mixed control did not converge" (rve.hpp:559)
+          code[p] = 1 + static_cast<int>(Code::solver);
+          active[p] = 0;
+          continue;
+        }
+        // J dE = -r with complete pivoting
+        double J[3][3], b[3];
+        int cp[3] = {0, 1, 2};
+        for (int a = 0; a < nu; ++a) {
+          b[a] = -r[a];
+          for (int c = 0; c < nu; ++c) J[a][c] = Cm[9 * p + 3 * u[a] + u[c]];
+        }
+        bool sing = false;
+        for (int c = 0; c < nu && !sing; ++c) {
+          int pr = c, pcn = c;
+          double best = -1.0;
+          for (int i = c; i < nu; ++i)
+            for (int jj = c; jj < nu; ++jj)
+              if (std::abs(J[i][jj]) > best) {
+                best = std::abs(J[i][jj]);
+                pr = i;
+                pcn = jj;
+              }
+          if (!(best > 0.0)) {
+            sing = true;
+            break;
+          }
+          for (int jj = 0; jj < nu; ++jj) std::swap(J[c][jj], J[pr][jj]);
+          std::swap(b[c], b[pr]);
+          for (int i = 0; i < nu; ++i) std::swap(J[i][c], J[i][pcn]);
+          std::swap(cp[c], cp[pcn]);
+          for (int i = c + 1; i < nu; ++i) {
+            const double l = J[i][c] / J[c][c];
+            for (int jj = c; jj < nu; ++jj) J[i][jj] -= l * J[c][jj];
+            b[i] -= l * b[c];
+          }
+        }
+        if (sing) {
+          code[p] = 1 + static_cast<int>(Code::solver);
+          active[p] = 0;
+          continue;
+        }
+        double x[3];
+        for (int i = nu - 1; i >= 0; --i) {
+          double s = b[i];
+          for (int jj = i + 1; jj < nu; ++jj) s -= J[i][jj] * x[jj];
+          x[i] = s / J[i][i];
+        }
+        for (int a = 0; a < nu; ++a) Ew[3 * p + u[cp[a]]] += x[a];
+        ++n_active;
+      }
+      if (n_active == 0) break;
+    }
+    std::memcpy(E, Ew.data(), sizeof(double) * 3 * P);
+    if (sigma) std::memcpy(sigma, sg.data(), sizeof(double) * 3 * P);
+    if (C) std::memcpy(C, Cm.data(), sizeof(double) * 9 * P);
+    if (outer_iters) std::memcpy(outer_iters, iters.data(), sizeof(int) * P);
+    if (status) std::memcpy(status, code.data(), sizeof(int) * P);
+  });
+}
+
 int fe2_macro_run_hf(const fe2_macro_config_t* cfg, fe2_hf_t hf, double* rows, int max_rows, int* n_rows,
                      double* u_residual) {
   return guard([&] {

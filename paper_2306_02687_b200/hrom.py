@@ -118,6 +118,8 @@ def _load():
     L.fe2_hf_trajectories.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.POINTER(_Opts), _dp, _dp, _ip, _dp, _dp,
                                       _dp, _ip]
     L.fe2_hf_band.argtypes = [C.c_void_p, _ip]
+    L.fe2_hrom_mixed_step.argtypes = [C.c_void_p, _ip, _dp, _dp, C.c_double, C.c_int, C.POINTER(_Opts), _dp, _dp,
+                                      _dp, _ip, _ip]
     L.fe2_hf_mono_begin.argtypes = [C.c_void_p]
     L.fe2_hf_mono_iterate.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _ip]
     L.fe2_hf_mono_commit.argtypes = [C.c_void_p]
@@ -514,6 +516,24 @@ class HyperRomEngine:
 
     def reset_stats(self):
         _check(lib.fe2_hrom_reset_stats(self._h))
+
+    def mixed_step(self, control, E_prescribed, sigma_target, E, tol=1e-10, max_iter=25,
+                   opts: NewtonOptions | None = None):
+        """Mixed control for every point (fe2_hrom_mixed_step; rve.hpp:496-571):
+        control (P,3) bool (True = strain prescribed), E_prescribed / sigma_target
+        (P,3); E (P,3) the committed macro strains. Returns E (converged), sigma,
+        C (P,3,3), outer_iters, status; the engine is left at the accepted state."""
+        P = self.P
+        ctl = np.ascontiguousarray(np.broadcast_to(np.asarray(control, dtype=np.int32), (P, 3)))
+        Ep = np.ascontiguousarray(np.broadcast_to(np.asarray(E_prescribed, dtype=np.float64), (P, 3)))
+        St = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma_target, dtype=np.float64), (P, 3)))
+        Eo = np.array(np.broadcast_to(np.asarray(E, dtype=np.float64), (P, 3)))
+        sig, Cm = np.empty((P, 3)), np.empty((P, 3, 3))
+        it, st = np.empty(P, dtype=np.int32), np.empty(P, dtype=np.int32)
+        o = (opts or NewtonOptions())._c()
+        _check(lib.fe2_hrom_mixed_step(self._h, _i(ctl), _d(Ep), _d(St), tol, max_iter, C.byref(o), _d(Eo), _d(sig),
+                                       _d(Cm), _i(it), _i(st)))
+        return dict(E=Eo, sigma=sig, C=Cm, outer_iters=it, status=st)
 
     def set_stream(self, stream_ptr):
         """Order the engine's work on a caller's cudaStream_t (int handle; 0 = own)."""
