@@ -194,7 +194,10 @@ __global__ void __launch_bounds__(144) k_hf_element(int n_el, const int* __restr
 // One CTA per system; a batch of RVE solves runs its systems on concurrent
 // streams (fe2_hf_trajectories), one CTA each.
 constexpr int kNB = 32;             // columns per panel (= warp width: the diagonal blocks run lane-per-row)
-constexpr int kBandThreads = 512;   // factorisation CTA
+#ifndef FE2_BAND_THREADS
+#define FE2_BAND_THREADS 512
+#endif
+constexpr int kBandThreads = FE2_BAND_THREADS;  // factorisation CTA
 constexpr int kSolveThreads = 256;  // substitution CTA
 constexpr int kMaxRhs = 4;          // right-hand sides per substitution (monolithic: K^-1 [r | K_fE])
 
@@ -202,142 +205,170 @@ __host__ __device__ constexpr int band_panel_ld(int bw) { return (bw + kNB + 3) 
 size_t band_chol_smem(int bw) { return sizeof(double) * kNB * band_panel_ld(bw); }
 constexpr int kBandSmemMax = 200 * 1024;
 
-// Right-looking, blocked by kNB columns. Per panel (columns j0 .. j0+nb-1,
-// rows j0 .. j0+nb-1+bw; k-major in shared memory so the 4-row tile reads are
-// 32-B vectors): load; factor its nb x nb diagonal block on warp 0 (lane =
-// row); solve the rows below against it, one thread per row in registers;
-// write it back; rank-nb update of the next bw x bw lower window by all
-// threads in 4x4 register tiles (the 16 band entries of a tile are loaded
-// before any is stored, so the loads overlap). info = 0, or 1 + the first
-// non-positive pivot's column.
+// Right-looking, blocked by kNB columns, with look-ahead. Per panel (columns
+// j0 .. j0+nb-1, rows j0 .. j0+nb-1+bw; k-major in shared memory so the 4-row
+// tile reads are 32-B vectors): its nb x nb diagonal block is already factored
+// (sDiag, by the previous panel's look-ahead); load the rows below; solve them
+// against the diagonal block, one thread per row in registers; write the panel
+// back; rank-nb update of the next bw x bw lower window in 4x4 register tiles
+// (warps on tile columns, lanes on tile rows: coalesced band loads / stores, the
+// 16 loads of a tile issued before any store) — first the tile columns of the
+// NEXT panel on all warps, then warp 0 factors the next diagonal block in
+// registers (lane = row, column broadcast by shuffles) while warps 1.. finish
+// the remaining tiles. info = 0, or 1 + the first non-positive pivot's column.
+__device__ __forceinline__ bool band_diag_factor(const double* __restrict__ Kb, int ldb, int bw, int c0, int nb,
+                                                 double (*sDiag)[kNB + 1], double* sInvD, int lane, int* bad_col) {
+  // stage the block (column k of it is contiguous in the band: lanes read rows k + lane)
+  for (int k = 0; k < nb; ++k) {
+    const int r = k + lane;
+    if (r < nb) sDiag[r][k] = (lane <= bw) ? Kb[static_cast<size_t>(c0 + k) * ldb + lane] : 0.0;
+  }
+  __syncwarp();
+  double a[kNB];
+#pragma unroll
+  for (int k = 0; k < kNB; ++k) a[k] = (k < nb && lane < nb && k <= lane) ? sDiag[lane][k] : 0.0;
+#pragma unroll
+  for (int k = 0; k < kNB; ++k) {
+    if (k < nb) {
+      const double d = __shfl_sync(0xffffffffu, a[k], k);
+      if (!(d > 0.0)) {
+        *bad_col = k;
+        return false;
+      }
+      const double l = sqrt(d), inv = 1.0 / l;
+      if (lane == k) {
+        a[k] = l;
+        sInvD[k] = inv;
+      } else if (lane > k) {
+        a[k] *= inv;
+      }
+#pragma unroll
+      for (int kk = k + 1; kk < kNB; ++kk) {
+        const double lk = __shfl_sync(0xffffffffu, a[k], kk);  // L(kk, k)
+        if (lane >= kk) a[kk] -= a[k] * lk;
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kNB; ++k) sDiag[lane][k] = (k <= lane) ? a[k] : 0.0;
+  return true;
+}
+
+// one 4x4 tile (rows 4 ti.., columns 4 tj.. of the window after column j0 + nb - 1)
+__device__ __forceinline__ void band_tile_update(double* __restrict__ Kb, int ldb, int j0, int nb, int M,
+                                                 const double* sP, int LR, int ti, int tj) {
+  double old[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int c = 4 * tj + r;
+    const double* col = Kb + static_cast<size_t>(j0 + nb + c) * ldb;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = 4 * ti + q;
+      old[q][r] = (c < M && i < M && i >= c) ? col[i - c] : 0.0;
+    }
+  }
+  asm volatile("" ::: "memory");  // keep the 16 band loads ahead of the stores (they overlap)
+  double acc[4][4] = {};
+  for (int k = 0; k < nb; ++k) {
+    const double* ck = sP + k * LR + nb;
+    const double2 x0 = *reinterpret_cast<const double2*>(ck + 4 * ti);  // rows (128-bit loads)
+    const double2 x1 = *reinterpret_cast<const double2*>(ck + 4 * ti + 2);
+    const double2 y0 = *reinterpret_cast<const double2*>(ck + 4 * tj);  // columns (broadcast)
+    const double2 y1 = *reinterpret_cast<const double2*>(ck + 4 * tj + 2);
+    const double xv[4] = {x0.x, x0.y, x1.x, x1.y}, yv[4] = {y0.x, y0.y, y1.x, y1.y};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[q][r] += xv[q] * yv[r];
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int c = 4 * tj + r;
+    double* col = Kb + static_cast<size_t>(j0 + nb + c) * ldb;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = 4 * ti + q;
+      if (c < M && i < M && i >= c) col[i - c] = old[q][r] - acc[q][r];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kBandThreads) k_band_chol(int n, int bw, int ldb, double* __restrict__ Kb,
                                                             int* __restrict__ info) {
-  extern __shared__ __align__(32) double sP[];  // [kNB][LR]: sP[k * LR + i] = L(j0 + i, j0 + k)
-  __shared__ double sInvD[kNB];                 // 1 / L_kk of the panel's diagonal block
+  extern __shared__ __align__(32) double sP[];  // [kNB][LR]: sP[k * LR + i] = L(j0 + i, j0 + k), i >= nb
+  __shared__ double sDiag[kNB][kNB + 1];        // the factored diagonal block of the current panel
+  __shared__ double sInvD[kNB];                 // 1 / L_kk of it
   __shared__ int s_fail;
   const int LR = band_panel_ld(bw);
-  const int t = threadIdx.x, lane = t & 31;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = blockDim.x >> 5;
   if (t == 0) s_fail = 0;
-  for (int j0 = 0; j0 < n; j0 += kNB) {
-    const int nb = min(kNB, n - j0);
-    const int R = min(n, j0 + nb + bw) - j0;
-    for (int e = t; e < R * nb; e += blockDim.x) {
-      const int k = e / R, i = e - k * R;  // consecutive threads: consecutive rows of a column (coalesced)
-      sP[k * LR + i] = (i >= k && i - k <= bw) ? Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] : 0.0;
-    }
-    __syncthreads();
-    // (1) the nb x nb diagonal block on warp 0: lane i holds row i in registers,
-    // right-looking column by column, the column broadcast by shuffles
-    if (t < 32) {
-      double a[kNB];
-#pragma unroll
-      for (int k = 0; k < kNB; ++k) a[k] = (k < nb && lane < nb && k <= lane) ? sP[k * LR + lane] : 0.0;
-      int bad = 0;
-#pragma unroll
-      for (int k = 0; k < kNB; ++k) {
-        if (k < nb) {
-          const double d = __shfl_sync(0xffffffffu, a[k], k);
-          if (!(d > 0.0)) {
-            bad = k + 1;
-            break;
-          }
-          const double l = sqrt(d), inv = 1.0 / l;
-          if (lane == k) {
-            a[k] = l;
-            sInvD[k] = inv;
-          } else if (lane > k) {
-            a[k] *= inv;
-          }
-#pragma unroll
-          for (int kk = k + 1; kk < kNB; ++kk) {
-            const double lk = __shfl_sync(0xffffffffu, a[k], kk);  // L(kk, k)
-            if (lane >= kk) a[kk] -= a[k] * lk;
-          }
-        }
+  __syncthreads();
+  // j0 = -kNB: only the look-ahead step (the first panel's diagonal block), so the
+  // diagonal factorisation has a single call site (register allocation)
+  for (int j0 = -kNB; j0 < n; j0 += kNB) {
+    const int nb = j0 < 0 ? 0 : min(kNB, n - j0);
+    const int R = j0 < 0 ? 0 : min(n, j0 + nb + bw) - j0;
+    const int M = R - nb;
+    const int T4 = (M + 3) / 4;
+    const int TA = min(T4, kNB / 4);  // tile columns of the next panel
+    if (j0 >= 0) {
+      for (int e = t; e < (R - nb) * nb; e += blockDim.x) {  // the rows below the diagonal block
+        const int k = e / (R - nb), i = nb + (e - k * (R - nb));
+        sP[k * LR + i] = (i - k <= bw) ? Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] : 0.0;
       }
-      if (bad) {
-        if (lane == 0) {
-          *info = j0 + bad;
-          s_fail = 1;
+      __syncthreads();
+      // L_21 = A_21 L_11^-T, one thread per row in registers
+      for (int i = nb + t; i < R; i += blockDim.x) {
+        asm volatile("" ::: "memory");  // keep the L(k, m) reads in the loop (hoisted, 528 values spill)
+        double a[kNB];
+#pragma unroll
+        for (int k = 0; k < kNB; ++k) a[k] = k < nb ? sP[k * LR + i] : 0.0;
+#pragma unroll
+        for (int k = 0; k < kNB; ++k) {
+          if (k < nb) {
+            double v = a[k];
+#pragma unroll
+            for (int m = 0; m < k; ++m) v -= a[m] * sDiag[k][m];  // L(k, m): broadcast
+            a[k] = v * sInvD[k];
+          }
         }
-      } else {
 #pragma unroll
         for (int k = 0; k < kNB; ++k)
-          if (k < nb && lane < nb && k <= lane) sP[k * LR + lane] = a[k];
+          if (k < nb) sP[k * LR + i] = a[k];
       }
+      __syncthreads();
+      for (int e = t; e < R * nb; e += blockDim.x) {  // the factored panel back to the band
+        const int k = e / R, i = e - k * R;
+        if (i >= k && i - k <= bw)
+          Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] = i < nb ? sDiag[i][k] : sP[k * LR + i];
+      }
+      // phase A: the next panel's columns, all warps (column w % TA, rows split over warp groups)
+      const int groups = TA > 0 && nwarps / TA > 0 ? nwarps / TA : 1;
+      if (TA > 0 && warp < TA * groups) {
+        const int tj = warp % TA, g = warp / TA;
+        for (int ti = tj + lane + 32 * g; ti < T4; ti += 32 * groups) band_tile_update(Kb, ldb, j0, nb, M, sP, LR, ti, tj);
+      }
+    }
+    __syncthreads();
+    // phase B: warp 0 factors the next diagonal block (its entries are final now) while
+    // the other warps update the remaining tile columns
+    const int c1 = j0 + kNB;  // the next panel (j0 + nb when j0 >= 0 and the panel is full)
+    if (warp == 0) {
+      if (c1 < n) {
+        int bc = 0;
+        if (!band_diag_factor(Kb, ldb, bw, c1, min(kNB, n - c1), sDiag, sInvD, lane, &bc) && lane == 0) {
+          *info = c1 + bc + 1;
+          s_fail = 1;
+        }
+      }
+    } else {
+      for (int tj = TA + warp - 1; tj < T4; tj += nwarps - 1)
+        for (int ti = tj + lane; ti < T4; ti += 32) band_tile_update(Kb, ldb, j0, nb, M, sP, LR, ti, tj);
     }
     __syncthreads();
     if (s_fail) return;  // uniform
-    // (2) the rows below it: L_21 = A_21 L_11^-T, one thread per row in registers
-    for (int i = nb + t; i < R; i += blockDim.x) {
-      double a[kNB];
-#pragma unroll
-      for (int k = 0; k < kNB; ++k) a[k] = k < nb ? sP[k * LR + i] : 0.0;
-#pragma unroll
-      for (int k = 0; k < kNB; ++k) {
-        if (k < nb) {
-          double v = a[k];
-#pragma unroll
-          for (int m = 0; m < k; ++m) v -= a[m] * sP[m * LR + k];  // L(k, m): broadcast
-          a[k] = v * sInvD[k];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kNB; ++k)
-        if (k < nb) sP[k * LR + i] = a[k];
-    }
-    __syncthreads();
-    for (int e = t; e < R * nb; e += blockDim.x) {
-      const int k = e / R, i = e - k * R;
-      if (i >= k && i - k <= bw) Kb[static_cast<size_t>(j0 + k) * ldb + (i - k)] = sP[k * LR + i];
-    }
-    // trailing update of rows / columns j0+nb .. j0+R-1 (lower triangle, 4x4
-    // tiles): warp w takes the tile columns tj = w, w + nwarps, ...; its lanes
-    // the tile rows ti >= tj of that column, so every band load / store of a
-    // warp touches consecutive rows of one column (coalesced).
-    const int M = R - nb;
-    const int T4 = (M + 3) / 4;
-    const int warp = t >> 5, nwarps = blockDim.x >> 5;
-    for (int tj = warp; tj < T4; tj += nwarps) {
-      for (int ti = tj + lane; ti < T4; ti += 32) {
-        double old[4][4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int c = 4 * tj + r;
-          const double* col = Kb + static_cast<size_t>(j0 + nb + c) * ldb;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int i = 4 * ti + q;
-            old[q][r] = (c < M && i < M && i >= c) ? col[i - c] : 0.0;
-          }
-        }
-        asm volatile("" ::: "memory");  // keep the 16 band loads ahead of the stores (they overlap)
-        double acc[4][4] = {};
-        for (int k = 0; k < nb; ++k) {
-          const double* ck = sP + k * LR + nb;
-          const double2 x0 = *reinterpret_cast<const double2*>(ck + 4 * ti);  // rows (128-bit loads)
-          const double2 x1 = *reinterpret_cast<const double2*>(ck + 4 * ti + 2);
-          const double2 y0 = *reinterpret_cast<const double2*>(ck + 4 * tj);  // columns (broadcast)
-          const double2 y1 = *reinterpret_cast<const double2*>(ck + 4 * tj + 2);
-          const double xv[4] = {x0.x, x0.y, x1.x, x1.y}, yv[4] = {y0.x, y0.y, y1.x, y1.y};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[q][r] += xv[q] * yv[r];
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int c = 4 * tj + r;
-          double* col = Kb + static_cast<size_t>(j0 + nb + c) * ldb;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int i = 4 * ti + q;
-            if (c < M && i < M && i >= c) col[i - c] = old[q][r] - acc[q][r];
-          }
-        }
-      }
-    }
-    __syncthreads();
   }
   if (t == 0) *info = 0;
 }
