@@ -623,6 +623,17 @@ def main():
             if xrun.finite else "oracle parity tests/test_gpu_full_configs.py"}
         if not xrun.finite:
             rec["roofline_hbm"] = xrun.roofline_hbm(xst, hbm, hbm_src)
+        nprof = os.path.join(ROOT, "profiles", "ncu_increment_summary.json")
+        if os.path.exists(nprof):  # the kernel's ncu capture: pipe utilisation, DRAM bytes (scaled to P)
+            try:
+                e = json.load(open(nprof)).get(xcfg["name"], {})
+                if e:
+                    rec["roofline"]["ncu"] = {k: e.get(k) for k in ("dmma_pipe_pct_active", "fp64_pipe_pct_active",
+                                                                    "issue_active_pct", "source")}
+                    if e.get("dram_bytes_per_launch") and e.get("points"):
+                        rec["roofline"]["traffic"] = e["dram_bytes_per_launch"] * xrun.P / e["points"]
+            except Exception:
+                pass
         if c == 3 and args.mono:  # the north_star multi-GPU scheme: exchange every Newton iteration
             xrun.eng.reset_stats()
             xrun.eng.set_timing(True)
@@ -649,6 +660,13 @@ def main():
         except Exception:
             traffic = None
     roofline["traffic"] = traffic
+    if os.path.exists(prof):  # the pipe utilisation of the same kernel from its ncu capture
+        try:
+            e = json.load(open(prof)).get(cfg["name"], {})
+            roofline["ncu"] = {k: e.get(k) for k in ("dmma_pipe_pct_active", "fp64_pipe_pct_active",
+                                                     "issue_active_pct", "warps_active_pct", "source")}
+        except Exception:
+            pass
     if constitutive is not None and os.path.exists(prof):
         try:
             constitutive["traffic"] = json.load(open(prof)).get("constitutive_soa", {}).get("dram_bytes_per_launch")
