@@ -98,11 +98,12 @@ def test_bisected_substeps(mat, path, tol, max_iter):
     assert (o["status"] == 0).mean() > 0.5
 
 
-@pytest.mark.parametrize("mat", [POWER, CREEP_FAST], ids=["power", "creep"])
-def test_cta_kernel(mat):
-    """n = 64 (the CTA-per-point kernel, k_increment_big<8, false, GEN>)."""
-    m = model(64, 1000, [mat, INCL])
-    E = F.make_paths(0, 0, 32, 8)
+@pytest.mark.parametrize("mat,n,K", [(POWER, 64, 1000), (CREEP_FAST, 64, 1000), (CREEP_FAST, 128, 1000),
+                                     (POWER, 40, 600)], ids=["power64", "creep64", "creep128", "power40"])
+def test_cta_kernel(mat, n, K):
+    """n > 32: the CTA-per-point kernel (k_increment_big<NT, false, GEN>, its own unit)."""
+    m = model(n, K, [mat, INCL])
+    E = F.make_paths(0, 0, 16 if n > 64 else 32, 8)
     g, o = compare(m, E)
     assert (o["status"] == 0).all()
 

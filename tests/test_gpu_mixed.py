@@ -68,3 +68,25 @@ def test_stress_target_and_mixed_masks():
         u = ~ctl[p]
         assert np.abs(o["sigma"][p][u] - tgt[p][u]).max() < 1e-10 * (np.linalg.norm(tgt[p]) + 1e-3)
         np.testing.assert_array_equal(o["E"][p][ctl[p]], Ep[p][ctl[p]])
+
+
+def test_mixed_control_on_the_cta_kernel_and_power_law():
+    """n = 64 (k_increment_big) with a power-law matrix: uniaxial stress, the replay property."""
+    P = 8
+    m = F.HyperRomModel(33, 64, 1000, 0)
+    m.materials = [F.PowerLawParams(1.0, 0.3, 0.01, 0.1), F.ElasticParams(10.0, 0.3)]
+    eng = F.HyperRomEngine.from_model(m)
+    eng.alloc_points(P)
+    E = np.zeros((P, 3))
+    steps = []
+    for k in range(1, 4):
+        Ep = np.zeros((P, 3))
+        Ep[:, 0] = 0.015 * k
+        o = eng.mixed_step([True, False, False], Ep, np.zeros((P, 3)), E)
+        assert (o["status"] == 0).all() and np.abs(o["sigma"][:, 1:]).max() < 1e-10
+        E = o["E"]
+        steps.append((E.copy(), o["sigma"].copy()))
+    ref = F.HyperRomEngine.from_model(m)
+    ref.alloc_points(P)
+    for Ek, sk in steps:
+        np.testing.assert_array_equal(ref.solve_increment(Ek)["sigma"], sk)
