@@ -82,3 +82,18 @@ def test_exchange_entry_points_validate_and_need_a_device():
         with pytest.raises(F.Fe2Error) as e:
             F.NcclComm(0, 1, 0, bytes(128))
         assert e.value.kind == "numeric" and "no CPU fallback" in str(e.value)
+
+
+def test_round2_entry_points_validate_arguments():
+    """fe2_hrom_mixed_step, fe2_hf_trajectories / _mono_* / _band: null handles and
+    bad options return ErrorCode::config (1) without touching a device."""
+    o = F.hrom.NewtonOptions()._c()
+    assert F.lib.fe2_hrom_mixed_step(None, None, None, None, 1e-10, 25, ctypes.byref(o), None, None, None, None,
+                                     None) == 1
+    assert F.lib.fe2_hf_trajectories(None, 1, 1, None, ctypes.byref(o), None, None, None, None, None, None,
+                                     None) == 1
+    assert F.lib.fe2_hf_mono_begin(None) == 1
+    assert F.lib.fe2_hf_mono_commit(None) == 1
+    assert F.lib.fe2_hf_mono_iterate(None, None, None, None, None, None) == 1
+    b = ctypes.c_int()
+    assert F.lib.fe2_hf_band(None, ctypes.byref(b)) == 1
