@@ -90,3 +90,15 @@ def test_mixed_control_on_the_cta_kernel_and_power_law():
     ref.alloc_points(P)
     for Ek, sk in steps:
         np.testing.assert_array_equal(ref.solve_increment(Ek)["sigma"], sk)
+
+
+def test_mixed_control_failure_status():
+    """max_iter = 0 cannot move the unknown components: status 1 + solver for the
+    points with an unmet target, 0 for the fully prescribed one."""
+    P = 3
+    eng = _engine(P)
+    ctl = np.array([[True, False, False], [True, True, True], [False, False, False]])
+    Ep = np.array([[0.01, 0.0, 0.0], [0.002, 0.001, 0.0], [0.0, 0.0, 0.0]])
+    tgt = np.array([[0.0, 0.0, 0.0], [0.0, 0.0, 0.0], [0.003, 0.0, 0.0]])
+    o = eng.mixed_step(ctl, Ep, tgt, np.zeros((P, 3)), max_iter=0)
+    assert o["status"][0] == 1 + 4 and o["status"][2] == 1 + 4 and o["status"][1] == 0
