@@ -15,7 +15,8 @@ import paper_2306_02687_b200 as F  # noqa: E402
 n, K, P, incr, path = (int(x) for x in sys.argv[1:6])
 rep = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 m = F.HyperRomModel(33, n, K, 0)
-eng = F.HyperRomEngine.from_model(m)
+fs = path == 2  # finite-strain Biot variant (config 2): H (4) in, P (4) and A (16) out
+eng = F.HyperRomEngine.from_model(m, finite_strain=fs)
 dev = torch.device("cuda", 0)
 stream = torch.cuda.Stream(device=dev)  # not the legacy default stream (handle 0 = the engine's own)
 torch.cuda.set_stream(stream)
@@ -23,7 +24,7 @@ eng.set_stream(stream.cuda_stream)
 E = F.make_paths(path, 0, P, incr)
 dE = torch.from_numpy(np.ascontiguousarray(E.transpose(1, 0, 2))).to(dev)
 outs = [torch.empty(s, dtype=t, device=dev) for s, t in
-        (((P, 3), torch.float64), ((P, 9), torch.float64), ((P,), torch.int32), ((P,), torch.int32),
+        (((P, 4 if fs else 3), torch.float64), ((P, 16 if fs else 9), torch.float64), ((P,), torch.int32), ((P,), torch.int32),
          ((P,), torch.float64), ((P,), torch.int32))]
 eng.alloc_points(P)
 for r in range(rep):
