@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
     double merr = 0.0;  // GEN: return-map failures of this thread's points
     const bool cur = D.st[p].pad[0] != 0;
     double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
-    if (sub == 0) {
+    {  // every thread of a cubature point holds its history (one broadcast load per point)
       const double* H = hist_ptr(p, qi, cur);
       h0 = H[0];
       h1 = H[kQC];
@@ -784,7 +784,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       strain(Gb, E0, E1, E2, e0, e1, e2);
       bool plastic = false;
       Corr cr{};
-      if (sub == 0) {
+      {  // the point's threads all run the return map on the reduced strain (same instruction
+         // count for the warp as one lane per point, no divergence, no broadcast afterwards)
         const Trial T = trial_state(mt, h0, h1, h2, h3, h4, e0, e1, e2);
         double dlam_g = 0.0;
         if constexpr (GEN) {
@@ -810,13 +811,15 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
             n3 = h3 + ce * T.d3;
             n4 = h4 + dlam;
           }
-          double* Hc = hist_ptr(p, q, !cur);
-          Hc[0] = n0;
-          Hc[kQC] = n1;
-          Hc[2 * kQC] = n2;
-          Hc[3 * kQC] = n3;
-          Hc[4 * kQC] = n4;
-          if (D.flags && q < M.K2) D.flags[(cur ? 0 : D.flags_alt) + p * M.K2p + q] = plastic ? 1 : 0;
+          if (sub == 0) {
+            double* Hc = hist_ptr(p, q, !cur);
+            Hc[0] = n0;
+            Hc[kQC] = n1;
+            Hc[2 * kQC] = n2;
+            Hc[3 * kQC] = n3;
+            Hc[4 * kQC] = n4;
+            if (D.flags && q < M.K2) D.flags[(cur ? 0 : D.flags_alt) + p * M.K2p + q] = plastic ? 1 : 0;
+          }
         }
         if (c + 1 < nch) {
           const double* H = hist_ptr(p, q + QB, cur);
@@ -836,10 +839,10 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       // (w ΔC_q) G_q of its modes (128-bit) and lanes sub < 3 the A-row offsets.
       {
         const int src = lane & ~(TPQ - 1);
-        const double wq = (sub == 0 && plastic) ? M.w2[q] : 0.0;
-        double d00 = wq * cr.dc00, d01 = wq * cr.dc01, d02 = wq * cr.dc02;
-        double d11 = wq * cr.dc11, d12 = wq * cr.dc12, d22 = wq * cr.dc22;
-        if (plastic) {  // the return-map lane (sub == 0)
+        const double wq = plastic ? M.w2[q] : 0.0;
+        const double d00 = wq * cr.dc00, d01 = wq * cr.dc01, d02 = wq * cr.dc02;
+        const double d11 = wq * cr.dc11, d12 = wq * cr.dc12, d22 = wq * cr.dc22;
+        if (plastic && sub == 0) {  // one lane per point accumulates the plastic sums
           sDS[slot * 3 + 0] = wq * cr.ds0;
           sDS[slot * 3 + 1] = wq * cr.ds1;
           sDS[slot * 3 + 2] = wq * cr.ds2;
@@ -854,14 +857,8 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
           ds1 += sDS[slot * 3 + 1];
           ds2 += sDS[slot * 3 + 2];
         }
-        const bool pl = __shfl_sync(0xffffffffu, plastic ? 1 : 0, src) != 0;
+        const bool pl = plastic;
         const int ps = __shfl_sync(0xffffffffu, slot, src);
-        d00 = __shfl_sync(0xffffffffu, d00, src);
-        d01 = __shfl_sync(0xffffffffu, d01, src);
-        d02 = __shfl_sync(0xffffffffu, d02, src);
-        d11 = __shfl_sync(0xffffffffu, d11, src);
-        d12 = __shfl_sync(0xffffffffu, d12, src);
-        d22 = __shfl_sync(0xffffffffu, d22, src);
         if (pl) {
           const double2* Gq = reinterpret_cast<const double2*>(Gb + qi * S);
           double2* br = reinterpret_cast<double2*>(stB + 3 * ps * L::RS);
