@@ -894,10 +894,14 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       contract_dispatch<NT, MP>(warp, Gb, sRO, stB, sDS, np4, acc, kae, rr, lane);
       BIG_T(4);
       if constexpr (!kFragCorr<NT>) {
-        if (tid < NP) {  // r and K_aE corrections of mode a = tid, from the staged rows
-          for (int sl = 0; sl < np; ++sl) {
-            const double* ar = Gb + sQ[sl] * S + tid;
-            const double* br = stB + 3 * sl * L::RS + tid;
+        // r and K_aE corrections from the staged rows: thread (h, a) sums mode a over the
+        // plastic slots h, h + HS, ... (HS = threads per mode; combined after the chunk loop)
+        constexpr int HS = L::BT / NP;
+        const int hh = tid / NP, am = tid - hh * NP;
+        if (hh < HS) {
+          for (int sl = hh; sl < np; sl += HS) {
+            const double* ar = Gb + sQ[sl] * S + am;
+            const double* br = stB + 3 * sl * L::RS + am;
             const double* ds = sDS + sl * 3;
             rm += ar[0] * ds[0] + ar[L::RS] * ds[1] + ar[2 * L::RS] * ds[2];
             ka0 += br[0];
@@ -909,6 +913,31 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       __syncthreads();
       ring_release();
       BIG_T(5);
+    }
+    if constexpr (!kFragCorr<NT>) {
+      constexpr int HS = L::BT / NP;
+      if constexpr (HS > 1) {  // partial sums of the slot classes h > 0, added in a fixed order
+        const int hh = tid / NP, am = tid - hh * NP;
+        if (hh > 0 && hh < HS) {
+          double* o = stB + ((hh - 1) * NP + am) * 4;  // the staging area is free after the last chunk
+          o[0] = rm;
+          o[1] = ka0;
+          o[2] = ka1;
+          o[3] = ka2;
+        }
+        __syncthreads();
+        if (hh == 0) {
+#pragma unroll
+          for (int h = 1; h < HS; ++h) {
+            const double* o = stB + ((h - 1) * NP + am) * 4;
+            rm += o[0];
+            ka0 += o[1];
+            ka1 += o[2];
+            ka2 += o[3];
+          }
+        }
+        __syncthreads();  // before the K_aa tiles overwrite the aliased area
+      }
     }
     store_dispatch<NT, MP>(warp, sK, acc, lane);
     if constexpr (kFragCorr<NT>) {
