@@ -64,7 +64,10 @@ struct Big {
   static constexpr int NP = 8 * NT;
   static constexpr int BW = bw_for(NT);  // warps per CTA
   static constexpr int BT = BW * 32;     // threads per CTA
-  static constexpr int MINB = BW == 8 ? FE2_BIG_MINB : 2;
+#ifndef FE2_BIG_SMALL_MINB
+#define FE2_BIG_SMALL_MINB 2
+#endif
+  static constexpr int MINB = BW == 8 ? FE2_BIG_MINB : FE2_BIG_SMALL_MINB;
   static constexpr int QB = (NP <= FE2_BIG_QB32_MAXNP && BW == 8) ? 32 : 16;  // cubature points per chunk
   static constexpr int TPQ = BT / QB;    // threads per cubature point
   static constexpr int RS = NP + 4;  // strain-row stride in G chunks and staged rows (≡ 4 or 12 mod 16)
@@ -335,6 +338,22 @@ __device__ __forceinline__ void contract(const double* Gb, const int* sRO, const
     }
     return;
   }
+#ifdef FE2_BIG_NOPREFETCH
+  {
+#pragma unroll 1
+    for (int g = 0; g < ng; ++g) {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int f = 12 * g + 4 * s;
+        double A[NT], B[NT];
+        load_frags<NT, W, 0>(ga + ro[f], pb + f * RS, A, B);
+        dmma_pairs<NT, W, 0, MP>(acc, A, B);
+        diag_acc<NT, W, 0>(A, B, pw[f], s, kae, rr);
+      }
+    }
+    return;
+  }
+#endif
   double A0[NT], B0[NT], A1[NT], B1[NT], A2[NT], B2[NT];
   if (ng > 0) load_frags<NT, W, 0>(ga + ro[0], pb, A0, B0);
 #pragma unroll 1
