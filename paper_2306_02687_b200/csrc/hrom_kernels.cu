@@ -1349,12 +1349,24 @@ void launch_mono_commit(const PointsDev& D, int NP, const double* mono, cudaStre
   k_mono_commit<<<grid, 128, 0, s>>>(D, NP, mono);
 }
 
+// the monolithic iteration: G resident in shared memory when it fits (as launch_inc_nt), else the ring
+template <int NT>
+void launch_mono_nt(const IncArgs& a, int num_sms, cudaStream_t s) {
+  constexpr int NP = 8 * NT;
+  constexpr int WR = kwres_for(NT);
+  const size_t res = IncLayout<NP, WR>::res_bytes(a.M.nchunks);
+  if (res <= kMaxDynSmem && !resident_disabled())
+    launch_inc_variant<NT, WR, true, true>(a, num_sms, s, res);
+  else
+    launch_inc_variant<NT, mono_kw(NT), false, true>(a, num_sms, s, IncLayout<NP, mono_kw(NT)>::bytes);
+}
+
 void launch_increment_mono(const IncArgs& a, int num_sms, cudaStream_t s) {
   switch (a.M.NP) {
-    case 8: launch_inc_variant<1, mono_kw(1), false, true>(a, num_sms, s, IncLayout<8, mono_kw(1)>::bytes); break;
-    case 16: launch_inc_variant<2, mono_kw(2), false, true>(a, num_sms, s, IncLayout<16, mono_kw(2)>::bytes); break;
-    case 24: launch_inc_variant<3, mono_kw(3), false, true>(a, num_sms, s, IncLayout<24, mono_kw(3)>::bytes); break;
-    case 32: launch_inc_variant<4, mono_kw(4), false, true>(a, num_sms, s, IncLayout<32, mono_kw(4)>::bytes); break;
+    case 8: launch_mono_nt<1>(a, num_sms, s); break;
+    case 16: launch_mono_nt<2>(a, num_sms, s); break;
+    case 24: launch_mono_nt<3>(a, num_sms, s); break;
+    case 32: launch_mono_nt<4>(a, num_sms, s); break;
     default: break;
   }
 }
