@@ -220,12 +220,16 @@ __device__ double warp_chol_solve(const double* sK, const double* sInv, int n, i
 #endif
 constexpr int kGroupUnroll = FE2_GROUP_UNROLL;  // plastic-group loop unroll (tuning)
 // warps per CTA of the streamed-G ring increment kernel: 16 (128 registers) for NP = 8;
-// from NP = 16 on the 16-warp build spilled 0.5-1.1 KB per thread and 8 warps
-// with 255 registers measured faster (n = 32, K = 1,000 / 4,000: +9% / +15%)
+// 12 (168 registers, no spills) for NP = 16 / 24 (n = 16: +19% at K = 1,000, +17% at K = 4,000
+// over 8 warps); NP = 32 spills 216 B at 168 registers and keeps 8 warps with 255 (the
+// 16-warp builds spilled 0.5-1.1 KB per thread from NP = 16 on)
 #ifndef FE2_KW_WIDE
 #define FE2_KW_WIDE 8
 #endif
-constexpr int kw_for(int NT) { return NT == 1 ? FE2_KW : FE2_KW_WIDE; }
+#ifndef FE2_KW_MID
+#define FE2_KW_MID 12
+#endif
+constexpr int kw_for(int NT) { return NT == 1 ? FE2_KW : (NT <= 3 ? FE2_KW_MID : FE2_KW_WIDE); }
 // warps per CTA when the whole G2 is resident in shared memory: 12 (168 registers, the
 // warp-uniform Newton state in shared memory, WarpSt) — measured +12% over 8 warps with
 // 255 registers at n = 24; NP = 32 spills at 168 registers and keeps 8
