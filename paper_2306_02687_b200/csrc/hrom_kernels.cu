@@ -233,7 +233,11 @@ constexpr int kw_for(int NT) { return NT == 1 ? FE2_KW : (NT <= 3 ? FE2_KW_MID :
 // warps per CTA when the whole G2 is resident in shared memory: 12 (168 registers, the
 // warp-uniform Newton state in shared memory, WarpSt) — measured +12% over 8 warps with
 // 255 registers at n = 24; NP = 32 spills at 168 registers and keeps 8
-constexpr int kwres_for(int NT) { return NT == 4 ? 8 : FE2_KWRES; }
+// ... and 16 warps (128 registers; 12 / 64 B of spills) for NP = 8 / 16: +6-11% at K = 100, +6% at K = 400
+#ifndef FE2_KWRES_SMALL
+#define FE2_KWRES_SMALL 16
+#endif
+constexpr int kwres_for(int NT) { return NT == 4 ? 8 : (NT <= 2 ? FE2_KWRES_SMALL : FE2_KWRES); }
 // warps per CTA of the monolithic iteration (ring-streamed G): 16 at NP = 8 (128 registers), 12
 // above (168 registers: the 16-warp builds spilled 64-320 B; measured +10% at n = 24, +2% at
 // n = 32, and 16 warps 7% faster at n = 12)
