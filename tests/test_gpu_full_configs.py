@@ -87,9 +87,10 @@ def test_config3_model_real_size():
     np.testing.assert_allclose(state, o["state"], rtol=1e-9, atol=1e-12)
 
 
-@pytest.mark.parametrize("n,K,P", [(128, 4000, 32), (64, 4000, 64), (8, 4000, 256)])
+@pytest.mark.parametrize("n,K,P", [(128, 4000, 32), (64, 4000, 64), (8, 4000, 256), (16, 4000, 128), (24, 1500, 128)])
 def test_config4_corners(n, K, P):
-    """Roofline-sweep corners: config-0 generator, 5 increments."""
+    """Roofline-sweep corners: config-0 generator, 5 increments. n = 16 / 24 with an operator too
+    large for shared memory run the 12-warp ring variant of k_increment."""
     m = F.HyperRomModel(33, n, K, 0)
     E = F.make_paths(0, 0, P, 5)
     _, g, fl = run_gpu_flags(m, E)
