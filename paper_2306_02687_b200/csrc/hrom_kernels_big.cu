@@ -68,7 +68,10 @@ struct Big {
 #define FE2_BIG_SMALL_MINB 2
 #endif
   static constexpr int MINB = BW == 8 ? FE2_BIG_MINB : FE2_BIG_SMALL_MINB;
-  static constexpr int QB = (NP <= FE2_BIG_QB32_MAXNP && BW == 8) ? 32 : 16;  // cubature points per chunk
+#ifndef FE2_BIG_QB_SMALL
+#define FE2_BIG_QB_SMALL 16
+#endif
+  static constexpr int QB = (NP <= FE2_BIG_QB32_MAXNP && BW == 8) ? 32 : (BW == 8 ? 16 : FE2_BIG_QB_SMALL);  // cubature points per chunk
   static constexpr int TPQ = BT / QB;    // threads per cubature point
   static constexpr int RS = NP + 4;  // strain-row stride in G chunks and staged rows (≡ 4 or 12 mod 16)
   static constexpr int S = 3 * RS;    // doubles per cubature point in G2 (ModelDev::S for NP > 32)
