@@ -856,9 +856,10 @@ __global__ void __launch_bounds__(Big<NT>::BT, Big<NT>::MINB) k_increment_big(In
       BIG_T(1);
       compact(plastic, slot, np);
       // The point's TPQ threads stage its operand rows right away (no staging
-      // pass, no CTA barrier before it): the return-map lane's w ΔC_q, slot and
-      // flag go to its siblings by shuffles, each thread writes the B rows
-      // (w ΔC_q) G_q of its modes (128-bit) and lanes sub < 3 the A-row offsets.
+      // pass, no CTA barrier before it): every thread already holds its point's
+      // w ΔC_q and flag (all of them ran the return map), the slot comes from the
+      // point's first lane; each thread writes the B rows (w ΔC_q) G_q of its
+      // modes (128-bit) and lanes sub < 3 the A-row offsets.
       {
         const int src = lane & ~(TPQ - 1);
         const double wq = plastic ? M.w2[q] : 0.0;
